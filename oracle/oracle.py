@@ -1,0 +1,356 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY — numpy/ctypes front end to the two CPU checkers.
+
+* ``Restatement``: the plain-C restatement (oracle/frs_oracle.c -> libfrs_oracle.so).
+* ``Reference``: the reference's own sources compiled by oracle/Makefile into
+  oracle/_ref/libfrspec_ref.so (patched for the drafting.cpp:200-219 use-after-free).
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline / reference arm may
+import this module. The product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+RESTATEMENT_SO = os.path.join(HERE, "libfrs_oracle.so")
+REFERENCE_SO = os.path.join(HERE, "_ref", "libfrspec_ref.so")
+
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_ip = C.POINTER(C.c_int)
+
+HIDDEN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int32),
+                        C.POINTER(C.c_int32), C.POINTER(C.c_float))
+
+
+def build(reference: bool = True) -> None:
+    """Compile the restatement (always) and the reference (.so in _ref/) when its sources exist."""
+    target = "all" if reference else "restatement"
+    subprocess.run(["make", "-s", "-C", HERE, target], check=True)
+
+
+def _c32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ci32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+class Restatement:
+    """Plain-C restatement (frs_oracle.h)."""
+
+    def __init__(self, path: str = RESTATEMENT_SO):
+        if not os.path.exists(path):
+            build(reference=False)
+        L = self.lib = C.CDLL(path)
+        L.frs_o_dot_f32.restype = C.c_float
+        L.frs_o_dot_f32.argtypes = [_f32p, _f32p, C.c_int]
+        L.frs_o_logits.argtypes = [_f32p, C.c_int, _f32p, C.c_int, C.c_int, _f32p]
+        L.frs_o_expf_glibc.restype = C.c_float
+        L.frs_o_expf_glibc.argtypes = [C.c_float]
+        L.frs_o_softmax.argtypes = [_f32p, C.c_int, C.c_float, _f32p, C.POINTER(C.c_float),
+                                    C.POINTER(C.c_double)]
+        L.frs_o_topk.argtypes = [_f32p, C.c_int, C.c_int, _i32p, _f32p]
+        L.frs_o_argmax.argtypes = [_f32p, C.c_int]
+        L.frs_o_draft_level.argtypes = [_f32p, C.c_int, _f32p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                        C.c_float, _i32p, _i32p, _f32p, _f32p, _f64p, C.c_void_p]
+        L.frs_o_verify_argmax.argtypes = [_f32p, C.c_int, _f32p, C.c_int, C.c_int, _i32p, _f32p]
+        L.frs_o_verify_greedy_ids.argtypes = [_i32p, _i32p, _i32p, C.c_int, _i32p, _ip, _i32p, _ip]
+        L.frs_o_tree_mask.argtypes = [_i32p, C.c_int, _u64p]
+        L.frs_o_count_frequencies.argtypes = [_i32p, C.c_int64, C.c_int, _u64p]
+        L.frs_o_build_subset.argtypes = [_u64p, C.c_int, C.c_int, _i32p, C.c_int, _i32p]
+        L.frs_o_subset_from_ranking.argtypes = [_i32p, C.c_int, C.c_int, C.c_int, _i32p, C.c_int, _i32p]
+        L.frs_o_restrict.argtypes = [_f32p, C.c_int, C.c_int, _i32p, C.c_int, _f32p]
+        L.frs_o_draft_tree.argtypes = [HIDDEN_FN, C.c_void_p, _f32p, C.c_int, C.c_int, C.c_void_p,
+                                       C.c_int, C.c_int, C.c_int, _i32p, _i32p, _i32p, _f64p, _ip]
+
+    def dot_f32(self, a, b) -> np.float32:
+        a, b = _c32(a), _c32(b)
+        return np.float32(self.lib.frs_o_dot_f32(a, b, a.size))
+
+    def logits(self, h, W):
+        h, W = _c32(h), _c32(W)
+        out = np.empty((h.shape[0], W.shape[0]), np.float32)
+        self.lib.frs_o_logits(h, h.shape[0], W, W.shape[0], W.shape[1], out)
+        return out
+
+    def expf(self, x: float) -> np.float32:
+        return np.float32(self.lib.frs_o_expf_glibc(float(x)))
+
+    def softmax(self, logits, temperature: float = 1.0):
+        x = _c32(logits)
+        p = np.empty_like(x)
+        mx, tot = C.c_float(), C.c_double()
+        if self.lib.frs_o_softmax(x, x.size, temperature, p, C.byref(mx), C.byref(tot)):
+            raise ValueError("softmax: rejected input")
+        return p, np.float32(mx.value), tot.value
+
+    def topk(self, values, k: int):
+        v = _c32(values)
+        idx, val = np.empty(k, np.int32), np.empty(k, np.float32)
+        if self.lib.frs_o_topk(v, v.size, k, idx, val):
+            raise ValueError("topk: k out of range")
+        return idx, val
+
+    def argmax(self, values) -> int:
+        v = _c32(values)
+        return int(self.lib.frs_o_argmax(v, v.size))
+
+    def draft_level(self, h, slab, ordered_ids, k: int, temperature: float = 1.0, want_logits=False):
+        h, slab = _c32(np.atleast_2d(h)), _c32(slab)
+        n, d = h.shape
+        v_sub = slab.shape[0]
+        ids = None if ordered_ids is None else _ci32(ordered_ids)
+        ridx, full = np.zeros((n, k), np.int32), np.zeros((n, k), np.int32)
+        prob, mx, tot = np.zeros((n, k), np.float32), np.zeros(n, np.float32), np.zeros(n, np.float64)
+        lg = np.empty((n, v_sub), np.float32) if want_logits else None
+        rc = self.lib.frs_o_draft_level(h, n, slab, v_sub, d, None if ids is None else ids.ctypes.data,
+                                        k, temperature, ridx, full, prob, mx, tot,
+                                        None if lg is None else lg.ctypes.data)
+        if rc:
+            raise ValueError("draft_level: rejected input")
+        out = dict(ridx=ridx, full=full, prob=prob, mx=mx, total=tot)
+        if want_logits:
+            out["logits"] = lg
+        return out
+
+    def verify_argmax(self, h, W):
+        h, W = _c32(np.atleast_2d(h)), _c32(W)
+        ids, vals = np.empty(h.shape[0], np.int32), np.empty(h.shape[0], np.float32)
+        self.lib.frs_o_verify_argmax(h, h.shape[0], W, W.shape[0], W.shape[1], ids, vals)
+        return ids, vals
+
+    def verify_greedy_ids(self, argmax_ids, tokens, parents):
+        a, t, p = _ci32(argmax_ids), _ci32(tokens), _ci32(parents)
+        k = t.size
+        em, path = np.empty(k + 1, np.int32), np.empty(k + 1, np.int32)
+        ne, npth = C.c_int(), C.c_int()
+        self.lib.frs_o_verify_greedy_ids(a, t, p, k, em, C.byref(ne), path, C.byref(npth))
+        return em[: ne.value].copy(), path[: npth.value].copy()
+
+    def tree_mask(self, parents):
+        p = _ci32(parents)
+        w = np.zeros(max(p.size, 1), np.uint64)
+        rc = self.lib.frs_o_tree_mask(p, p.size, w)
+        if rc == 2:
+            raise OverflowError("tree exceeds 64 nodes")
+        if rc:
+            raise ValueError("tree is not topological")
+        return w[: p.size]
+
+    def count_frequencies(self, stream, vocab_size: int):
+        s = _ci32(stream)
+        c = np.zeros(vocab_size, np.uint64)
+        if self.lib.frs_o_count_frequencies(s, s.size, vocab_size, c):
+            raise ValueError("count_frequencies: id out of range")
+        return c
+
+    def build_subset(self, counts, size: int, forced=()):
+        c = np.ascontiguousarray(counts, np.uint64)
+        f = _ci32(np.array(forced, np.int32))
+        out = np.empty(size, np.int32)
+        if self.lib.frs_o_build_subset(c, c.size, size, f, f.size, out):
+            raise ValueError("build_subset: rejected input")
+        return out
+
+    def subset_from_ranking(self, ranked, size: int, vocab_size: int, forced=()):
+        r = _ci32(ranked)
+        f = _ci32(np.array(forced, np.int32))
+        out = np.empty(size, np.int32)
+        if self.lib.frs_o_subset_from_ranking(r, r.size, size, vocab_size, f, f.size, out):
+            raise ValueError("subset_from_ranking: rejected input")
+        return out
+
+    def restrict(self, W, ordered):
+        W, o = _c32(W), _ci32(ordered)
+        out = np.empty((o.size, W.shape[1]), np.float32)
+        if self.lib.frs_o_restrict(W, W.shape[0], W.shape[1], o, o.size, out):
+            raise ValueError("restrict: id out of range")
+        return out
+
+    def draft_tree(self, provider, slab, ordered_ids, width: int, depth: int, total: int):
+        """provider(level, tokens[n], parent_cands[n]) -> hidden [n x d] float32."""
+        slab = _c32(slab)
+        d = slab.shape[1]
+        ids = None if ordered_ids is None else _ci32(ordered_ids)
+
+        def cb(_user, level, n, tok_p, par_p, out_p):
+            toks = np.ctypeslib.as_array(tok_p, (n,)).copy()
+            pars = np.ctypeslib.as_array(par_p, (n,)).copy()
+            try:
+                hid = _c32(provider(level, toks, pars)).reshape(n, d)
+            except Exception:  # pragma: no cover - surfaced as rc
+                return 9
+            C.memmove(out_p, hid.ctypes.data, hid.nbytes)
+            return 0
+
+        fn = HIDDEN_FN(cb)
+        tok, par, dep = (np.empty(64, np.int32) for _ in range(3))
+        lj, cnt = np.empty(64, np.float64), C.c_int()
+        rc = self.lib.frs_o_draft_tree(fn, None, slab, slab.shape[0], d,
+                                       None if ids is None else ids.ctypes.data, width, depth, total,
+                                       tok, par, dep, lj, C.byref(cnt))
+        if rc:
+            raise ValueError(f"draft_tree: rc={rc}")
+        n = cnt.value
+        return dict(tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(), log_joint=lj[:n].copy())
+
+
+class Reference:
+    """The compiled (patched) reference via oracle/ref_shim.cpp."""
+
+    def __init__(self, path: str = REFERENCE_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle` where /root/reference exists")
+        L = self.lib = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_dot_f32.restype = C.c_float
+        L.ref_dot_f32.argtypes = [_f32p, _f32p, C.c_int]
+        L.ref_matmul.argtypes = [_f32p, C.c_int, C.c_int, _f32p, C.c_int, _f32p]
+        L.ref_softmax.argtypes = [_f32p, C.c_int, C.c_float, _f32p]
+        L.ref_topk.argtypes = [_f32p, C.c_int, C.c_int, _i32p, _f32p]
+        L.ref_argmax.argtypes = [_f32p, C.c_int, C.POINTER(C.c_int32)]
+        L.ref_count_frequencies.argtypes = [_i32p, C.c_int64, C.c_int, _u64p, C.POINTER(C.c_uint64)]
+        L.ref_build_subset.argtypes = [_u64p, C.c_int, C.c_uint64, C.c_int, _i32p, C.c_int, _i32p]
+        L.ref_subset_from_ranking.argtypes = [_i32p, C.c_int, C.c_int, C.c_int, _i32p, C.c_int, _i32p]
+        L.ref_restrict_lm_head.argtypes = [_f32p, C.c_int, C.c_int, _i32p, C.c_int, _f32p]
+        L.ref_zipf_tokens.argtypes = [C.c_int, C.c_double, C.c_int64, C.c_uint64, _i32p]
+        L.ref_fill_gaussian.argtypes = [_f32p, C.c_int64, C.c_uint64, C.c_float]
+        L.ref_fill_gaussian.restype = None
+        L.ref_build_tree_mask.argtypes = [_i32p, C.c_int, _u64p]
+        L.ref_verify_greedy.argtypes = [_f32p, C.c_int, _f32p, C.c_int, _i32p, _i32p, _i32p, _ip, _i32p, _ip]
+        L.ref_model_lm_head.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _f32p]
+        L.ref_model_draft_tree.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_void_p, C.c_int, _i32p, C.c_int,
+                                                           C.c_int, C.c_int, C.c_int, _i32p, _i32p, _i32p, _f64p, _ip]
+        L.ref_model_draft_capture.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_void_p, C.c_int, _i32p, C.c_int,
+                                                              C.c_int, C.c_int, C.c_int, _f32p, _i32p, _i32p, _ip,
+                                                              _i32p, _i32p, _i32p, _f64p, _ip]
+
+    def _check(self, rc: int, what: str):
+        if rc:
+            msg = self.lib.ref_last_error().decode()
+            exc = {1: ValueError, 2: OverflowError, 3: IOError}.get(rc, RuntimeError)
+            raise exc(f"{what}: {msg}")
+
+    def dot_f32(self, a, b):
+        a, b = _c32(a), _c32(b)
+        return np.float32(self.lib.ref_dot_f32(a, b, a.size))
+
+    def matmul(self, a, bt):
+        a, bt = _c32(np.atleast_2d(a)), _c32(np.atleast_2d(bt))
+        out = np.empty((a.shape[0], bt.shape[0]), np.float32)
+        self._check(self.lib.ref_matmul(a, a.shape[0], a.shape[1], bt, bt.shape[0], out), "matmul")
+        return out
+
+    def softmax(self, logits, temperature: float = 1.0):
+        x = _c32(logits)
+        p = np.empty_like(x)
+        self._check(self.lib.ref_softmax(x, x.size, temperature, p), "softmax")
+        return p
+
+    def topk(self, values, k: int):
+        v = _c32(values)
+        idx, val = np.empty(k, np.int32), np.empty(k, np.float32)
+        self._check(self.lib.ref_topk(v, v.size, k, idx, val), "topk")
+        return idx, val
+
+    def argmax(self, values) -> int:
+        v = _c32(values)
+        o = C.c_int32()
+        self._check(self.lib.ref_argmax(v, v.size, C.byref(o)), "argmax")
+        return o.value
+
+    def count_frequencies(self, stream, vocab_size: int):
+        s = _ci32(stream)
+        c, tot = np.zeros(vocab_size, np.uint64), C.c_uint64()
+        self._check(self.lib.ref_count_frequencies(s, s.size, vocab_size, c, C.byref(tot)), "count_frequencies")
+        return c, tot.value
+
+    def build_subset(self, counts, size: int, forced=()):
+        c = np.ascontiguousarray(counts, np.uint64)
+        f = _ci32(np.array(forced, np.int32))
+        out = np.empty(size, np.int32)
+        self._check(self.lib.ref_build_subset(c, c.size, int(c.sum()), size, f, f.size, out), "build_subset")
+        return out
+
+    def subset_from_ranking(self, ranked, size: int, vocab_size: int, forced=()):
+        r = _ci32(ranked)
+        f = _ci32(np.array(forced, np.int32))
+        out = np.empty(size, np.int32)
+        self._check(self.lib.ref_subset_from_ranking(r, r.size, size, vocab_size, f, f.size, out),
+                    "subset_from_ranking")
+        return out
+
+    def restrict_lm_head(self, W, ordered):
+        W, o = _c32(W), _ci32(ordered)
+        out = np.empty((o.size, W.shape[1]), np.float32)
+        self._check(self.lib.ref_restrict_lm_head(W, W.shape[0], W.shape[1], o, o.size, out), "restrict_lm_head")
+        return out
+
+    def zipf_tokens(self, vocab_size: int, exponent: float, count: int, seed: int):
+        out = np.empty(count, np.int32)
+        self._check(self.lib.ref_zipf_tokens(vocab_size, exponent, count, seed, out), "zipf_tokens")
+        return out
+
+    def fill_gaussian(self, count: int, seed: int, std: float = 0.02):
+        out = np.empty(count, np.float32)
+        self.lib.ref_fill_gaussian(out, count, seed, std)
+        return out
+
+    def tree_mask(self, parents):
+        p = _ci32(parents)
+        w = np.zeros(max(p.size, 1), np.uint64)
+        self._check(self.lib.ref_build_tree_mask(p, p.size, w), "build_tree_mask")
+        return w[: p.size]
+
+    def verify_greedy(self, root_logits, node_logits, tokens, parents):
+        r, nl = _c32(root_logits), _c32(node_logits)
+        t, p = _ci32(tokens), _ci32(parents)
+        k = t.size
+        em, path = np.empty(k + 1, np.int32), np.empty(k + 1, np.int32)
+        ne, npth = C.c_int(), C.c_int()
+        self._check(self.lib.ref_verify_greedy(r, r.size, nl, k, t, p, em, C.byref(ne), path, C.byref(npth)),
+                    "verify_greedy")
+        return em[: ne.value].copy(), path[: npth.value].copy()
+
+    def model_lm_head(self, V, d, layers, heads, seed):
+        out = np.empty((V, d), np.float32)
+        self._check(self.lib.ref_model_lm_head(V, d, layers, heads, seed, out), "model_lm_head")
+        return out
+
+    def model_draft_tree(self, V, d, layers, heads, max_seq, seed, ordered, pending, width, depth, total):
+        o = None if ordered is None else _ci32(ordered)
+        pend = _ci32(pending)
+        tok, par, dep = (np.empty(64, np.int32) for _ in range(3))
+        lj, cnt = np.empty(64, np.float64), C.c_int()
+        self._check(self.lib.ref_model_draft_tree(V, d, layers, heads, max_seq, seed,
+                                                  None if o is None else o.ctypes.data,
+                                                  0 if o is None else o.size, pend, pend.size, width, depth,
+                                                  total, tok, par, dep, lj, C.byref(cnt)), "build_draft_tree")
+        n = cnt.value
+        return dict(tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(), log_joint=lj[:n].copy())
+
+    def model_draft_capture(self, V, d, layers, heads, max_seq, seed, ordered, pending, width, depth, total):
+        o = None if ordered is None else _ci32(ordered)
+        pend = _ci32(pending)
+        max_rows = 1 + (depth - 1) * width
+        hid = np.empty((max_rows, d), np.float32)
+        rtok, rlev, nrows = np.empty(max_rows, np.int32), np.empty(max_rows, np.int32), C.c_int()
+        tok, par, dep = (np.empty(64, np.int32) for _ in range(3))
+        lj, cnt = np.empty(64, np.float64), C.c_int()
+        self._check(self.lib.ref_model_draft_capture(V, d, layers, heads, max_seq, seed,
+                                                     None if o is None else o.ctypes.data,
+                                                     0 if o is None else o.size, pend, pend.size, width, depth,
+                                                     total, hid, rtok, rlev, C.byref(nrows), tok, par, dep, lj,
+                                                     C.byref(cnt)), "draft_capture")
+        n, r = cnt.value, nrows.value
+        return dict(hidden=hid[:r].copy(), row_token=rtok[:r].copy(), row_level=rlev[:r].copy(),
+                    tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(),
+                    log_joint=lj[:n].copy())

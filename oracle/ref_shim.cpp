@@ -1,0 +1,374 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY. Never linked into the product library.
+//
+// extern "C" shim over the *compiled reference* (the frspec sources under
+// /root/reference/proj, built from a patched build-dir copy by oracle/Makefile
+// into oracle/_ref/). Every entry point forwards to the reference's own public
+// API so tests can compare the CUDA path against the real reference behaviour:
+//
+//   ref_dot_f32 / ref_matmul   -> frspec::dot_f32 / matmul      kernels.cpp:13-60
+//   ref_softmax                -> frspec::softmax               kernels.cpp:62-91
+//   ref_topk / ref_argmax      -> frspec::topk / argmax         kernels.cpp:93-122
+//   ref_count_frequencies      -> frspec::count_frequencies     vocab.cpp:23-38
+//   ref_build_subset           -> frspec::build_subset          vocab.cpp:70-102
+//   ref_subset_from_ranking    -> frspec::subset_from_ranking   vocab.cpp:104-138
+//   ref_restrict_lm_head       -> frspec::restrict_lm_head      vocab.cpp:152-168
+//   ref_zipf_tokens            -> frspec::zipf_tokens           vocab.cpp:180-196
+//   ref_build_tree_mask        -> frspec::build_tree_mask       verification.cpp:13-27
+//   ref_verify_greedy          -> frspec::verify_greedy         verification.cpp:42-71
+//   ref_model_draft_tree       -> frspec::build_draft_tree      drafting.cpp:122-245
+//   ref_model_draft_capture    -> restated drafting loop calling frspec::forward_raw
+//                                 (model.cpp:208-284) to export per-level hidden states
+//
+// Errors: every function returns 0 on success, 1 for std::invalid_argument,
+// 2 CapacityError, 3 DataError, 4 logic/domain error, 5 anything else; the message
+// is available from ref_last_error().
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "frspec/drafting.h"
+#include "frspec/errors.h"
+#include "frspec/kernels.h"
+#include "frspec/matrix.h"
+#include "frspec/model.h"
+#include "frspec/verification.h"
+#include "frspec/vocab.h"
+
+using namespace frspec;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F && f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument & e) {
+        g_err = e.what();
+        return 1;
+    } catch (const CapacityError & e) {
+        g_err = e.what();
+        return 2;
+    } catch (const DataError & e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::logic_error & e) {
+        g_err = e.what();
+        return 4;
+    } catch (const std::exception & e) {
+        g_err = e.what();
+        return 5;
+    }
+}
+
+Matrix to_matrix(const float * p, int rows, int cols) {
+    Matrix m(rows, cols);
+    std::memcpy(m.data.data(), p, sizeof(float) * static_cast<size_t>(rows) * cols);
+    return m;
+}
+
+DraftTree tree_from(const int32_t * tokens, const int32_t * parents, const int32_t * depths, int k) {
+    DraftTree t;
+    for (int i = 0; i < k; ++i) t.nodes.push_back({tokens[i], parents[i], depths ? depths[i] : 0, 0.0});
+    return t;
+}
+
+void export_tree(const DraftTree & t, int32_t * tokens, int32_t * parents, int32_t * depths,
+                 double * log_joint, int * count) {
+    *count = static_cast<int>(t.nodes.size());
+    for (size_t i = 0; i < t.nodes.size(); ++i) {
+        tokens[i] = t.nodes[i].token_id;
+        parents[i] = t.nodes[i].parent;
+        depths[i] = t.nodes[i].depth;
+        log_joint[i] = t.nodes[i].log_joint;
+    }
+}
+
+struct ModelBundle {
+    TargetModel target;
+    DraftModel draft;
+    std::shared_ptr<const RankedSubset> subset;
+    RestrictedHead head;
+};
+
+ModelBundle make_bundle(int V, int d, int layers, int heads, int max_seq, uint64_t seed,
+                        const int32_t * ordered, int v_sub) {
+    ModelConfig cfg;
+    cfg.vocab_size = V;
+    cfg.hidden_dim = d;
+    cfg.num_layers = layers;
+    cfg.num_heads = heads;
+    cfg.max_seq_len = max_seq;
+    cfg.seed = seed;
+    ModelBundle b;
+    b.target = build_target(cfg);
+    b.draft = build_draft(b.target, DraftMode::truncated, 0.0f, 0);
+    if (ordered != nullptr) {
+        std::vector<Token> ids(ordered, ordered + v_sub);
+        b.subset = std::make_shared<const RankedSubset>(subset_from_ranking(ids, v_sub, V, {}));
+        b.head = restrict_lm_head(b.target.shared->lm_head, b.subset);
+    }
+    return b;
+}
+}  // namespace
+
+extern "C" {
+
+const char * ref_last_error(void) { return g_err.c_str(); }
+
+float ref_dot_f32(const float * a, const float * b, int n) { return dot_f32(a, b, n); }
+
+int ref_matmul(const float * a, int m, int k, const float * bt, int n, float * out) {
+    return guarded([&] {
+        Matrix r = matmul(to_matrix(a, m, k), to_matrix(bt, n, k));
+        std::memcpy(out, r.data.data(), sizeof(float) * static_cast<size_t>(m) * n);
+    });
+}
+
+int ref_softmax(const float * logits, int n, float temperature, float * probs) {
+    return guarded([&] {
+        ProbVector p = softmax(std::span<const float>(logits, n), temperature);
+        std::memcpy(probs, p.probs.data(), sizeof(float) * n);
+    });
+}
+
+int ref_topk(const float * values, int n, int k, int32_t * idx, float * val) {
+    return guarded([&] {
+        auto r = topk(std::span<const float>(values, n), k);
+        for (int i = 0; i < k; ++i) {
+            idx[i] = r[i].first;
+            val[i] = r[i].second;
+        }
+    });
+}
+
+int ref_argmax(const float * values, int n, int32_t * out) {
+    return guarded([&] { *out = argmax(std::span<const float>(values, n)); });
+}
+
+int ref_count_frequencies(const int32_t * stream, int64_t count, int vocab_size, uint64_t * counts,
+                          uint64_t * total) {
+    return guarded([&] {
+        FrequencyTable t = count_frequencies(std::span<const Token>(stream, count), vocab_size);
+        std::memcpy(counts, t.counts.data(), sizeof(uint64_t) * vocab_size);
+        *total = t.total;
+    });
+}
+
+int ref_build_subset(const uint64_t * counts, int vocab_size, uint64_t total, int size,
+                     const int32_t * forced, int n_forced, int32_t * ordered_out) {
+    return guarded([&] {
+        FrequencyTable t;
+        t.vocab_size = vocab_size;
+        t.counts.assign(counts, counts + vocab_size);
+        t.total = total;
+        RankedSubset s = build_subset(t, size, std::span<const Token>(forced, n_forced));
+        std::memcpy(ordered_out, s.ordered_ids.data(), sizeof(int32_t) * s.size());
+    });
+}
+
+int ref_subset_from_ranking(const int32_t * ranked, int n_ranked, int size, int vocab_size,
+                            const int32_t * forced, int n_forced, int32_t * ordered_out) {
+    return guarded([&] {
+        RankedSubset s = subset_from_ranking(std::span<const Token>(ranked, n_ranked), size, vocab_size,
+                                             std::span<const Token>(forced, n_forced));
+        std::memcpy(ordered_out, s.ordered_ids.data(), sizeof(int32_t) * s.size());
+    });
+}
+
+int ref_restrict_lm_head(const float * W, int V, int d, const int32_t * ordered, int v_sub,
+                         float * out) {
+    return guarded([&] {
+        std::vector<Token> ids(ordered, ordered + v_sub);
+        auto subset = std::make_shared<const RankedSubset>(subset_from_ranking(ids, v_sub, V, {}));
+        RestrictedHead h = restrict_lm_head(to_matrix(W, V, d), subset);
+        std::memcpy(out, h.matrix.data.data(), sizeof(float) * static_cast<size_t>(v_sub) * d);
+    });
+}
+
+int ref_zipf_tokens(int vocab_size, double exponent, int64_t count, uint64_t seed, int32_t * out) {
+    return guarded([&] {
+        TokenSequence t = zipf_tokens(vocab_size, exponent, static_cast<size_t>(count), seed);
+        std::memcpy(out, t.data(), sizeof(int32_t) * t.size());
+    });
+}
+
+// Seeded Gaussian fill with the reference's generator semantics (model.cpp:24-27):
+// std::mt19937_64(seed) + std::normal_distribution<float>(0, std_dev), compiled with
+// -ffp-contract=off so the stream is flag-independent.
+void ref_fill_gaussian(float * out, int64_t count, uint64_t seed, float std_dev) {
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<float> dist(0.0f, std_dev);
+    for (int64_t i = 0; i < count; ++i) out[i] = dist(rng);
+}
+
+int ref_build_tree_mask(const int32_t * parents, int k, uint64_t * words) {
+    return guarded([&] {
+        std::vector<int32_t> tok(k, 0);
+        TreeMask m = build_tree_mask(tree_from(tok.data(), parents, nullptr, k));
+        std::memcpy(words, m.words.data(), sizeof(uint64_t) * k);
+    });
+}
+
+int ref_verify_greedy(const float * root_logits, int V, const float * node_logits, int k,
+                      const int32_t * tokens, const int32_t * parents, int32_t * emitted,
+                      int * n_emitted, int32_t * path, int * n_path) {
+    return guarded([&] {
+        DraftTree t = tree_from(tokens, parents, nullptr, k);
+        VerifyOutcome o = verify_greedy(std::span<const float>(root_logits, V), to_matrix(node_logits, k, V), t);
+        *n_emitted = static_cast<int>(o.emitted.size());
+        *n_path = static_cast<int>(o.accepted_path.size());
+        std::copy(o.emitted.begin(), o.emitted.end(), emitted);
+        std::copy(o.accepted_path.begin(), o.accepted_path.end(), path);
+    });
+}
+
+// Exports the seeded toy model's LM head [V x d] (model.cpp:93-128).
+int ref_model_lm_head(int V, int d, int layers, int heads, uint64_t seed, float * out) {
+    return guarded([&] {
+        ModelBundle b = make_bundle(V, d, layers, heads, 8, seed, nullptr, 0);
+        std::memcpy(out, b.target.shared->lm_head.data.data(), sizeof(float) * static_cast<size_t>(V) * d);
+    });
+}
+
+// Runs the reference's build_draft_tree (greedy, restricted head when ordered != null) on
+// an empty cache with `pending` as the forwarded context.
+int ref_model_draft_tree(int V, int d, int layers, int heads, int max_seq, uint64_t seed,
+                         const int32_t * ordered, int v_sub, const int32_t * pending, int n_pending,
+                         int width, int depth, int total, int32_t * tokens, int32_t * parents,
+                         int32_t * depths, double * log_joint, int * count) {
+    return guarded([&] {
+        ModelBundle b = make_bundle(V, d, layers, heads, max_seq, seed, ordered, v_sub);
+        KVCache cache = make_cache(b.draft);
+        DraftParams p{width, depth, total};
+        DraftResult r = build_draft_tree(b.draft, cache, std::span<const Token>(pending, n_pending), p,
+                                         ordered ? &b.head : nullptr, nullptr, false);
+        export_tree(r.tree, tokens, parents, depths, log_joint, count);
+    });
+}
+
+// Same drafting run, restated around the reference's public forward_raw so that the
+// hidden state of every forwarded draft row can be exported (drafting.cpp:133-221 order).
+// hidden_out: [1 + (depth-1)*width] x d rows: row 0 is the root row (last pending row);
+// then, level by level, the forwarded beam rows in beam order. beam_tokens/beam_parents
+// record, per forwarded row, its token and parent candidate index (-1 for the root row).
+// n_rows receives the number of hidden rows written.
+int ref_model_draft_capture(int V, int d, int layers, int heads, int max_seq, uint64_t seed,
+                            const int32_t * ordered, int v_sub, const int32_t * pending,
+                            int n_pending, int width, int depth, int total, float * hidden_out,
+                            int32_t * row_token, int32_t * row_level, int * n_rows,
+                            int32_t * tokens, int32_t * parents, int32_t * depths,
+                            double * log_joint, int * count) {
+    return guarded([&] {
+        ModelBundle b = make_bundle(V, d, layers, heads, max_seq, seed, ordered, v_sub);
+        KVCache cache = make_cache(b.draft);
+        DraftParams params{width, depth, total};
+        validate_params(params);
+        const RankedSubset * subset = ordered ? b.subset.get() : nullptr;
+        const Matrix & head = ordered ? b.head.matrix : b.draft.shared->lm_head;
+        struct Cand {
+            Token token;
+            int parent, depth;
+            double log_joint;
+            int cache_row;
+        };
+        int rows = 0;
+        auto emit_row = [&](const Matrix & hid, int r, Token tok, int level) {
+            std::memcpy(hidden_out + static_cast<size_t>(rows) * d, hid.row(r), sizeof(float) * d);
+            row_token[rows] = tok;
+            row_level[rows] = level;
+            ++rows;
+        };
+        ForwardResult fwd = draft_forward(b.draft, std::span<const Token>(pending, n_pending), cache,
+                                          ordered ? &b.head : nullptr);
+        emit_row(fwd.hidden, fwd.hidden.rows - 1, pending[n_pending - 1], 0);
+        const int base_len = cache.len;
+        const int anchor_pos = cache.positions[base_len - 1];
+        std::vector<Cand> cands;
+        std::vector<int> beam;
+        {
+            ProbVector pr = softmax(fwd.logits.row_span(fwd.logits.rows - 1), 1.0f);
+            auto kids = topk(pr.probs, std::min(width, static_cast<int>(pr.probs.size())));
+            for (auto [idx, prob] : kids) {
+                beam.push_back(static_cast<int>(cands.size()));
+                cands.push_back({subset ? subset->full_id(idx) : idx, -1, 1, std::log((double)prob), -1});
+            }
+        }
+        for (int level = 1; level < depth && !beam.empty(); ++level) {
+            if (static_cast<int>(beam.size()) > width) {
+                std::sort(beam.begin(), beam.end(), [&](int a, int c) {
+                    if (cands[a].log_joint != cands[c].log_joint) return cands[a].log_joint > cands[c].log_joint;
+                    return a < c;
+                });
+                beam.resize(width);
+                std::sort(beam.begin(), beam.end());
+            }
+            const int batch = static_cast<int>(beam.size());
+            TokenSequence bt;
+            std::vector<int> bp;
+            BitMask visible(batch, cache.len + batch);
+            for (int i = 0; i < batch; ++i) {
+                Cand & c = cands[beam[i]];
+                c.cache_row = cache.len + i;
+                bt.push_back(c.token);
+                bp.push_back(anchor_pos + c.depth);
+                visible.set_range(i, 0, base_len);
+                for (int a = c.parent; a >= 0; a = cands[a].parent) visible.set(i, cands[a].cache_row);
+                visible.set(i, c.cache_row);
+            }
+            fwd = forward_raw(*b.draft.shared, {&b.draft.layer, 1}, bt, bp, visible, cache, head);
+            std::vector<int> next;
+            for (int i = 0; i < batch; ++i) {
+                emit_row(fwd.hidden, i, bt[i], level);
+                const int pidx = beam[i];
+                const int pdepth = cands[pidx].depth;
+                const double plj = cands[pidx].log_joint;
+                ProbVector pr = softmax(fwd.logits.row_span(i), 1.0f);
+                auto kids = topk(pr.probs, std::min(width, static_cast<int>(pr.probs.size())));
+                for (auto [idx, prob] : kids) {
+                    next.push_back(static_cast<int>(cands.size()));
+                    cands.push_back({subset ? subset->full_id(idx) : idx, pidx, pdepth + 1,
+                                     plj + std::log((double)prob), -1});
+                }
+            }
+            beam = std::move(next);
+        }
+        *n_rows = rows;
+        // select_top_k, greedy (drafting.cpp:79-118 with prefix_closed=false)
+        std::vector<int> order(cands.size());
+        for (size_t i = 0; i < cands.size(); ++i) order[i] = static_cast<int>(i);
+        std::sort(order.begin(), order.end(), [&](int a, int c) {
+            if (cands[a].log_joint != cands[c].log_joint) return cands[a].log_joint > cands[c].log_joint;
+            return a < c;
+        });
+        std::vector<char> sel(cands.size(), 0);
+        int cnt = 0;
+        for (int c : order) {
+            if (cands[c].parent >= 0 && !sel[cands[c].parent]) continue;
+            if (cnt + 1 > total) continue;
+            sel[c] = 1;
+            ++cnt;
+        }
+        std::vector<int> remap(cands.size(), -1);
+        int out = 0;
+        for (size_t i = 0; i < cands.size(); ++i) {
+            if (!sel[i]) continue;
+            remap[i] = out;
+            tokens[out] = cands[i].token;
+            parents[out] = cands[i].parent >= 0 ? remap[cands[i].parent] : -1;
+            depths[out] = cands[i].depth;
+            log_joint[out] = cands[i].log_joint;
+            ++out;
+        }
+        *count = out;
+    });
+}
+
+}  // extern "C"
