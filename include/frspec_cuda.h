@@ -1,0 +1,165 @@
+/* frspec_cuda.h — C ABI of the B200-native FR-Spec drafting hot path (libfrspec_cuda.so).
+ *
+ * Drop-in boundary for the reference's C++ hot-path API (/root/reference/proj). The
+ * reference has no FFI of its own; these entry points are what a binding of its
+ * library API would bind, one per hot-path function:
+ *
+ *   frs_slab_build          replaces restrict_lm_head            vocab.cpp:152-168, vocab.h:49-52
+ *   frs_draft_head_topk     replaces forward_raw's LM-head line + softmax + pick_children/topk
+ *                           + RankedSubset::full_id              model.cpp:276-279, kernels.cpp:62-111,
+ *                                                                drafting.cpp:37-43,138-156,199-215
+ *   frs_verify_head_argmax  replaces the target LM head + argmax model.cpp:324-338, kernels.cpp:113-122
+ *   frs_accept_greedy       replaces verify_greedy's walk        verification.cpp:31-71
+ *   frs_argmax_merge        (new) vocab-parallel merge of per-shard (value, id) argmax pairs
+ *   frs_count_frequencies / frs_build_subset / frs_subset_from_ranking / frs_tree_mask
+ *                           host-side restatements of vocab.cpp:23-138 / verification.cpp:13-27
+ *   frs_head_* / frs_draft_tree / frs_verify_greedy
+ *                           host-buffer conveniences mirroring RestrictedHead, build_draft_tree
+ *                           (drafting.cpp:122-245, head path) and verify_greedy.
+ *
+ * Conventions: plain pointers and sizes; `stream` is a cudaStream_t (NULL = legacy default
+ * stream). Device-pointer entry points are asynchronous on `stream` and never allocate
+ * after frs_ctx_reserve(); outputs go to caller-owned buffers. Every function returns an
+ * frs_status; frs_last_error() gives the thread-local message. Status codes map 1:1 onto
+ * the reference's exception types (errors.h:7-17).
+ */
+#ifndef FRSPEC_CUDA_H
+#define FRSPEC_CUDA_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FRS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FRS_API __attribute__((visibility("default")))
+#else
+#define FRS_API
+#endif
+
+typedef enum {
+    FRS_OK = 0,
+    FRS_EINVAL = 1,    /* std::invalid_argument (rejected arguments)          errors.h:7     */
+    FRS_ECAPACITY = 2, /* frspec::CapacityError (64-node trees, capacities)   errors.h:10-12 */
+    FRS_EDATA = 3,     /* frspec::DataError                                   errors.h:15-17 */
+    FRS_ELOGIC = 4,    /* std::logic_error / std::domain_error                               */
+    FRS_ECUDA = 5,     /* CUDA runtime failure                                               */
+    FRS_ENCCL = 6,     /* NCCL failure                                                       */
+    FRS_ENOTSUP = 7    /* shape/dtype/mode combination not built for this device            */
+} frs_status;
+
+typedef enum { FRS_DTYPE_F32 = 0, FRS_DTYPE_BF16 = 1 } frs_dtype;
+
+/* EXACT: CUDA-core kernels that reproduce the reference arithmetic bit for bit (dot_f32
+ *        lane order without FMA, glibc expf, index-order double Σ, (p desc, idx asc) top-k).
+ * FAST:  tcgen05 tensor-core head over a bf16 slab; ids/argmax certified against an
+ *        exact recompute of the candidates, probabilities within tolerance. */
+typedef enum { FRS_MODE_EXACT = 0, FRS_MODE_FAST = 1 } frs_mode;
+
+/* Per-row flag bits written to out_flags (when non-NULL). */
+#define FRS_FLAG_NONFINITE 0x1u  /* a logit was NaN/inf: the reference throws (kernels.cpp:72-74) */
+#define FRS_FLAG_SEQ_SUM 0x2u    /* Σ exp took the index-order sequential path                  */
+#define FRS_FLAG_UNCERTIFIED 0x4u /* FAST: candidate set could not be certified (ids may differ) */
+#define FRS_FLAG_RECOMPUTED 0x8u /* FAST: row fell back to the exact kernel                     */
+
+typedef struct frs_ctx frs_ctx;
+typedef struct frs_head frs_head;
+
+FRS_API int frs_abi_version(void);
+FRS_API const char *frs_last_error(void);
+
+FRS_API int frs_ctx_create(int device, frs_ctx **out);
+FRS_API int frs_ctx_destroy(frs_ctx *ctx);
+FRS_API int frs_ctx_sm_count(const frs_ctx *ctx);
+/* Pre-size workspaces for up to max_rows hidden rows against up to max_vocab head rows. */
+FRS_API int frs_ctx_reserve(frs_ctx *ctx, int max_rows, int64_t max_vocab, int d);
+
+/* K1 — restrict_lm_head (vocab.cpp:152-168): slab[i,:] = W[ordered_ids[i],:], bitwise for
+ * FRS_DTYPE_F32, round-to-nearest-even for FRS_DTYPE_BF16. W, ordered_ids, slab: device.
+ * Out-of-range ids -> FRS_EINVAL (this call synchronizes `stream` to report it). */
+FRS_API int frs_slab_build(frs_ctx *ctx, const float *W, int64_t V, int d, const int32_t *ordered_ids,
+                   int v_sub, int slab_dtype, void *slab, void *stream);
+FRS_API size_t frs_slab_bytes(int v_sub, int d, int slab_dtype);
+
+/* K2 — one draft level for n hidden rows h[n x d] (fp32, device) against the slab:
+ * logits = h . slab^T; per row softmax(logits / temperature); top-min(k, v_sub) by
+ * (prob desc, restricted index asc); full = ordered_ids[ridx] (identity when NULL).
+ * Outputs [n x k] (device): out_ridx, out_full, out_prob; optional [n]: out_rowmax (the
+ * softmax max), out_total (the double Σ), out_flags; optional [n x v_sub] out_logits. */
+FRS_API int frs_draft_head_topk(frs_ctx *ctx, const float *h, int n, int d, const void *slab, int v_sub,
+                        int slab_dtype, const int32_t *ordered_ids, int k, float temperature,
+                        int mode, int32_t *out_ridx, int32_t *out_full, float *out_prob,
+                        float *out_rowmax, double *out_total, float *out_logits,
+                        uint32_t *out_flags, void *stream);
+
+/* K3 — full-vocabulary verify head over rows [id_offset, id_offset + v_rows) of the LM head
+ * (W points at that shard): per row i of h[m x d], out_id[i] = id_offset + argmax_j
+ * dot_f32(h_i, W_j) with ties to the lowest id, out_val[i] = that logit. Device buffers. */
+FRS_API int frs_verify_head_argmax(frs_ctx *ctx, const float *h, int m, int d, const void *W, int v_rows,
+                           int w_dtype, int32_t id_offset, int mode, int32_t *out_id,
+                           float *out_val, uint32_t *out_flags, void *stream);
+
+/* K4 — greedy accept walk (verification.cpp:42-71). argmax_ids[0] belongs to the root
+ * position, argmax_ids[1+i] to draft node i. Writes out_emitted[<=k+1], out_path[<=k] and
+ * out_counts = {n_emitted, n_path}. Device buffers. */
+FRS_API int frs_accept_greedy(frs_ctx *ctx, const int32_t *argmax_ids, const int32_t *tokens,
+                      const int32_t *parents, int k, int32_t *out_emitted, int32_t *out_path,
+                      int32_t *out_counts, void *stream);
+
+/* K5 — merge per-shard argmax pairs vals/ids[shards x m] (shard-major) by (value desc,
+ * id asc): reproduces argmax's lowest-id rule over a contiguous vocab split. Device. */
+FRS_API int frs_argmax_merge(frs_ctx *ctx, const float *vals, const int32_t *ids, int shards, int m,
+                     float *out_val, int32_t *out_id, void *stream);
+
+/* Row gather out[i,:] = table[tokens[i],:] (the identity draft layer of the head-path decode
+ * loop). Device buffers. */
+FRS_API int frs_gather_rows(frs_ctx *ctx, const float *table, int64_t rows, int d, const int32_t *tokens,
+                    int n, float *out, void *stream);
+
+/* ---- host-side FR vocabulary (vocab.cpp:23-138) and tree mask (verification.cpp:13-27) ---- */
+FRS_API int frs_count_frequencies(const int32_t *stream, int64_t count, int vocab_size, uint64_t *counts);
+FRS_API int frs_build_subset(const uint64_t *counts, int vocab_size, int size, const int32_t *forced,
+                     int n_forced, int32_t *ordered_out);
+FRS_API int frs_subset_from_ranking(const int32_t *ranked, int n_ranked, int size, int vocab_size,
+                            const int32_t *forced, int n_forced, int32_t *ordered_out);
+FRS_API int frs_coverage(const uint64_t *counts, int vocab_size, const int32_t *ordered, int v_sub,
+                 double *out);
+FRS_API int frs_flops_ratio(int full_size, int restricted_size, double *out);
+FRS_API int frs_tree_mask(const int32_t *parents, int k, uint64_t *words);
+
+/* ---- device-resident RestrictedHead and host-buffer conveniences ---- */
+/* W is host memory unless w_on_device; ordered_ids is host memory (validated on the host). */
+FRS_API int frs_head_create(frs_ctx *ctx, const float *W, int64_t V, int d, int w_on_device,
+                    const int32_t *ordered_ids, int v_sub, int slab_dtype, frs_head **out);
+FRS_API int frs_head_destroy(frs_head *head);
+FRS_API int frs_head_info(const frs_head *head, const void **slab, const int32_t **ordered_dev,
+                  int *v_sub, int *d, int *slab_dtype);
+/* One level end to end with HOST buffers: H2D h, K2, D2H outputs, synchronize. */
+FRS_API int frs_head_draft_host(frs_head *head, const float *h_host, int n, int k, int mode,
+                        int32_t *ridx, int32_t *full, float *prob);
+
+/* Hidden-state provider for the head-path draft tree: fill hidden_dev[n x d] (device) for
+ * the n forwarded rows of `level` (level 0: the single root row, tokens[0] = root token;
+ * parent_cands[i] = parent candidate index, -1 at the root). Return 0 or an error code. */
+typedef int (*frs_hidden_fn)(void *user, int level, int n, const int32_t *tokens,
+                             const int32_t *parent_cands, float *hidden_dev, void *stream);
+/* build_draft_tree restricted to the head path (drafting.cpp:122-245, greedy): hidden rows
+ * come from fn, or from rows of hidden_table[V x d] (device) by token when fn is NULL.
+ * Tree outputs are host arrays of capacity `total`. */
+FRS_API int frs_draft_tree(frs_head *head, int32_t root_token, frs_hidden_fn fn, void *user,
+                   const float *hidden_table, int width, int depth, int total, int mode,
+                   int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint,
+                   int *count);
+/* verify_greedy (verification.cpp:42-71) with the target head on the device: h_dev holds
+ * 1 + k rows (root first), W the full LM head [V x d] (device). Host outputs. */
+FRS_API int frs_verify_greedy(frs_ctx *ctx, const float *h_dev, const void *W, int V, int d, int w_dtype,
+                      int mode, const int32_t *tokens, const int32_t *parents, int k,
+                      int32_t *emitted, int *n_emitted, int32_t *path, int *n_path);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRSPEC_CUDA_H */

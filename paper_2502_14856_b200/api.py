@@ -1,0 +1,438 @@
+"""Python mirror of the reference's hot-path API over libfrspec_cuda.so.
+
+Names, argument meaning and errors follow /root/reference/proj:
+  FrequencyTable / count_frequencies / build_subset / subset_from_ranking / coverage /
+  flops_ratio / RankedSubset / RestrictedHead / restrict_lm_head   (vocab.h:14-77)
+  DraftParams / DraftTree / build_draft_tree (head path)           (drafting.h:13-67)
+  TreeMask / build_tree_mask / VerifyOutcome / verify_greedy /
+  AcceptanceStats                                                  (verification.h:16-62)
+plus the device-level kernels draft_head_topk / verify_head_argmax / accept_greedy /
+argmax_merge (include/frspec_cuda.h). Device buffers are torch CUDA tensors (PyTorch is
+plumbing here: memory, streams); every computation runs in the CUDA library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (DTYPE_BF16, DTYPE_F32, MODE_EXACT, MODE_FAST, CapacityError, InvalidArgument, check,
+                   lib)
+
+_DTYPES = {"f32": DTYPE_F32, "fp32": DTYPE_F32, "float32": DTYPE_F32, "bf16": DTYPE_BF16, "bfloat16": DTYPE_BF16}
+_MODES = {"exact": MODE_EXACT, "fast": MODE_FAST}
+
+
+def _dtype(d) -> int:
+    if isinstance(d, int):
+        return d
+    return _DTYPES[str(d).replace("torch.", "")]
+
+
+def _mode(m) -> int:
+    return m if isinstance(m, int) else _MODES[m]
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _np_ptr(a: Optional[np.ndarray]):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _stream(stream) -> C.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+class Context:
+    """frs_ctx: one per device per host thread (SURVEY.md §8(b) threading)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        p = C.c_void_p()
+        check(lib().frs_ctx_create(device, C.byref(p)), "frs_ctx_create")
+        self.handle = p
+
+    @property
+    def sm_count(self) -> int:
+        return lib().frs_ctx_sm_count(self.handle)
+
+    def reserve(self, max_rows: int, max_vocab: int, d: int) -> None:
+        check(lib().frs_ctx_reserve(self.handle, max_rows, max_vocab, d), "frs_ctx_reserve")
+
+    def close(self) -> None:
+        if self.handle:
+            lib().frs_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- vocab (vocab.h:14-77)
+@dataclass
+class FrequencyTable:
+    vocab_size: int
+    counts: np.ndarray
+    total: int
+
+    def merge(self, other: "FrequencyTable") -> None:  # vocab.cpp:15-21
+        if other.vocab_size != self.vocab_size:
+            raise InvalidArgument("FrequencyTable::merge: vocab_size mismatch")
+        self.counts = self.counts + other.counts
+        self.total += other.total
+
+
+def count_frequencies(stream, vocab_size: int) -> FrequencyTable:
+    s = _i32(stream)
+    counts = np.zeros(max(vocab_size, 1), np.uint64)
+    check(lib().frs_count_frequencies(_np_ptr(s), s.size, vocab_size, _np_ptr(counts)), "count_frequencies")
+    return FrequencyTable(vocab_size, counts, int(s.size))
+
+
+@dataclass
+class RankedSubset:
+    vocab_size: int
+    ordered_ids: np.ndarray
+    full_to_restricted: np.ndarray = field(default=None)
+
+    def __post_init__(self):
+        self.ordered_ids = _i32(self.ordered_ids)
+        if self.full_to_restricted is None:
+            f2r = np.full(self.vocab_size, -1, np.int32)
+            f2r[self.ordered_ids] = np.arange(self.ordered_ids.size, dtype=np.int32)
+            self.full_to_restricted = f2r
+
+    def size(self) -> int:
+        return int(self.ordered_ids.size)
+
+    def full_id(self, restricted: int) -> int:
+        return int(self.ordered_ids[restricted])
+
+    def restricted_index(self, full: int) -> int:
+        return int(self.full_to_restricted[full])
+
+    def contains(self, full: int) -> bool:
+        return self.full_to_restricted[full] >= 0
+
+
+def build_subset(table: FrequencyTable, size: int, forced: Sequence[int] = ()) -> RankedSubset:
+    f = _i32(list(forced))
+    out = np.empty(max(size, 1), np.int32)
+    check(lib().frs_build_subset(_np_ptr(np.ascontiguousarray(table.counts, np.uint64)), table.vocab_size, size,
+                                 _np_ptr(f), f.size, _np_ptr(out)), "build_subset")
+    return RankedSubset(table.vocab_size, out[:size])
+
+
+def subset_from_ranking(ranked_desc, size: int, vocab_size: int, forced: Sequence[int] = ()) -> RankedSubset:
+    r, f = _i32(ranked_desc), _i32(list(forced))
+    out = np.empty(max(size, 1), np.int32)
+    check(lib().frs_subset_from_ranking(_np_ptr(r), r.size, size, vocab_size, _np_ptr(f), f.size, _np_ptr(out)),
+          "subset_from_ranking")
+    return RankedSubset(vocab_size, out[:size])
+
+
+def coverage(table: FrequencyTable, subset: RankedSubset) -> float:
+    if subset.vocab_size != table.vocab_size:
+        raise InvalidArgument("coverage: subset does not match the table vocabulary")
+    out = C.c_double()
+    check(lib().frs_coverage(_np_ptr(np.ascontiguousarray(table.counts, np.uint64)), table.vocab_size,
+                             _np_ptr(subset.ordered_ids), subset.size(), C.byref(out)), "coverage")
+    return out.value
+
+
+def flops_ratio(full_size: int, restricted_size: int) -> float:
+    out = C.c_double()
+    check(lib().frs_flops_ratio(full_size, restricted_size, C.byref(out)), "flops_ratio")
+    return out.value
+
+
+# ---------------------------------------------------------------- K1: restrict_lm_head
+@dataclass
+class RestrictedHead:
+    """Device-resident row-gathered LM head slice (vocab.h:49-52). ``slab`` is row-major
+    [V_sub x d] in ``dtype``; ``ordered_dev`` is the restricted->full id map on the device."""
+    slab: torch.Tensor
+    ordered_dev: torch.Tensor
+    subset: RankedSubset
+    dtype: int
+
+    @property
+    def v_sub(self) -> int:
+        return int(self.slab.shape[0])
+
+    @property
+    def d(self) -> int:
+        return int(self.slab.shape[1])
+
+
+def restrict_lm_head(ctx: Context, lm_head: torch.Tensor, subset: RankedSubset, dtype="bf16",
+                     stream=None) -> RestrictedHead:
+    if lm_head.dtype != torch.float32 or not lm_head.is_cuda or lm_head.dim() != 2:
+        raise InvalidArgument("restrict_lm_head: lm_head must be a CUDA float32 [V x d] tensor")
+    lm_head = lm_head.contiguous()
+    dt = _dtype(dtype)
+    V, d = lm_head.shape
+    ordered_dev = torch.from_numpy(subset.ordered_ids).to(lm_head.device)
+    slab = torch.empty((subset.size(), d), dtype=torch.bfloat16 if dt == DTYPE_BF16 else torch.float32,
+                       device=lm_head.device)
+    check(lib().frs_slab_build(ctx.handle, _ptr(lm_head), V, d, _ptr(ordered_dev), subset.size(), dt, _ptr(slab),
+                               _stream(stream)), "restrict_lm_head")
+    return RestrictedHead(slab, ordered_dev, subset, dt)
+
+
+# ---------------------------------------------------------------- K2: draft head + top-k
+@dataclass
+class DraftLevel:
+    ridx: torch.Tensor     # [n, k] int32 restricted index
+    full: torch.Tensor     # [n, k] int32 full-vocabulary id
+    prob: torch.Tensor     # [n, k] float32
+    rowmax: torch.Tensor   # [n] float32
+    total: torch.Tensor    # [n] float64
+    flags: torch.Tensor    # [n] int32 (FRS_FLAG_*)
+    logits: Optional[torch.Tensor] = None
+
+
+def draft_head_topk(ctx: Context, h: torch.Tensor, head: RestrictedHead, k: int, temperature: float = 1.0,
+                    mode="exact", want_logits: bool = False, stream=None, out: Optional[DraftLevel] = None) -> DraftLevel:
+    if h.dtype != torch.float32 or not h.is_cuda:
+        raise InvalidArgument("draft head: h must be a CUDA float32 tensor")
+    h = h.contiguous()
+    n, d = h.shape
+    dev = h.device
+    if out is None:
+        out = DraftLevel(torch.empty((n, k), dtype=torch.int32, device=dev), torch.empty((n, k), dtype=torch.int32, device=dev),
+                         torch.empty((n, k), dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.float32, device=dev),
+                         torch.empty(n, dtype=torch.float64, device=dev), torch.zeros(n, dtype=torch.int32, device=dev),
+                         torch.empty((n, head.v_sub), dtype=torch.float32, device=dev) if want_logits else None)
+    check(lib().frs_draft_head_topk(ctx.handle, _ptr(h), n, d, _ptr(head.slab), head.v_sub, head.dtype,
+                                    _ptr(head.ordered_dev), k, temperature, _mode(mode), _ptr(out.ridx), _ptr(out.full),
+                                    _ptr(out.prob), _ptr(out.rowmax), _ptr(out.total), _ptr(out.logits),
+                                    _ptr(out.flags), _stream(stream)), "draft_head_topk")
+    return out
+
+
+# ---------------------------------------------------------------- K3/K4/K5
+def verify_head_argmax(ctx: Context, h: torch.Tensor, W: torch.Tensor, id_offset: int = 0, mode="exact",
+                       stream=None):
+    """Per-row argmax of h . W^T with ties to the lowest id; W is a CUDA fp32/bf16 shard."""
+    h = h.contiguous()
+    m, d = h.shape
+    dt = DTYPE_BF16 if W.dtype == torch.bfloat16 else DTYPE_F32
+    ids = torch.empty(m, dtype=torch.int32, device=h.device)
+    vals = torch.empty(m, dtype=torch.float32, device=h.device)
+    flags = torch.zeros(m, dtype=torch.int32, device=h.device)
+    check(lib().frs_verify_head_argmax(ctx.handle, _ptr(h), m, d, _ptr(W), W.shape[0], dt, id_offset, _mode(mode),
+                                       _ptr(ids), _ptr(vals), _ptr(flags), _stream(stream)), "verify_head_argmax")
+    return ids, vals, flags
+
+
+def accept_greedy(ctx: Context, argmax_ids: torch.Tensor, tokens: torch.Tensor, parents: torch.Tensor, stream=None):
+    k = int(tokens.numel())
+    dev = argmax_ids.device
+    emitted = torch.empty(k + 1, dtype=torch.int32, device=dev)
+    path = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    counts = torch.empty(2, dtype=torch.int32, device=dev)
+    check(lib().frs_accept_greedy(ctx.handle, _ptr(argmax_ids), _ptr(tokens), _ptr(parents), k, _ptr(emitted),
+                                  _ptr(path), _ptr(counts), _stream(stream)), "accept_greedy")
+    return emitted, path, counts
+
+
+def argmax_merge(ctx: Context, vals: torch.Tensor, ids: torch.Tensor, stream=None):
+    G, m = vals.shape
+    ov = torch.empty(m, dtype=torch.float32, device=vals.device)
+    oi = torch.empty(m, dtype=torch.int32, device=vals.device)
+    check(lib().frs_argmax_merge(ctx.handle, _ptr(vals.contiguous()), _ptr(ids.contiguous()), G, m, _ptr(ov), _ptr(oi),
+                                 _stream(stream)), "argmax_merge")
+    return ov, oi
+
+
+def gather_rows(ctx: Context, table: torch.Tensor, tokens: torch.Tensor, out: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
+    n = int(tokens.numel())
+    if out is None:
+        out = torch.empty((n, table.shape[1]), dtype=torch.float32, device=table.device)
+    check(lib().frs_gather_rows(ctx.handle, _ptr(table), table.shape[0], table.shape[1], _ptr(tokens), n, _ptr(out),
+                                _stream(stream)), "gather_rows")
+    return out
+
+
+# ---------------------------------------------------------------- drafting / verification
+@dataclass
+class DraftParams:  # drafting.h:13-17
+    beam_width: int = 10
+    search_depth: int = 6
+    total_draft_tokens: int = 60
+
+
+@dataclass
+class DraftTree:  # drafting.h:21-29 as parallel arrays
+    tokens: np.ndarray
+    parents: np.ndarray
+    depths: np.ndarray
+    log_joint: np.ndarray
+
+    def __len__(self) -> int:
+        return int(self.tokens.size)
+
+
+def build_tree_mask(parents) -> np.ndarray:
+    """verification.cpp:13-27: words[i] = words[parent] | 1 << i."""
+    p = _i32(parents)
+    w = np.zeros(max(p.size, 1), np.uint64)
+    check(lib().frs_tree_mask(_np_ptr(p), p.size, _np_ptr(w)), "build_tree_mask")
+    return w[: p.size]
+
+
+class DeviceHead:
+    """frs_head: a device-resident RestrictedHead owned by the library (host-buffer API)."""
+
+    def __init__(self, ctx: Context, lm_head, subset: RankedSubset, dtype="bf16"):
+        self.ctx, self.subset, self.dtype = ctx, subset, _dtype(dtype)
+        self._keep = lm_head
+        if isinstance(lm_head, torch.Tensor) and lm_head.is_cuda:
+            W, on_dev, V, d = _ptr(lm_head.contiguous()), 1, lm_head.shape[0], lm_head.shape[1]
+        else:
+            arr = np.ascontiguousarray(lm_head, np.float32)
+            self._keep = arr
+            W, on_dev, (V, d) = _np_ptr(arr), 0, arr.shape
+        self.vocab, self.d = int(V), int(d)
+        p = C.c_void_p()
+        check(lib().frs_head_create(ctx.handle, W, V, d, on_dev, _np_ptr(subset.ordered_ids), subset.size(),
+                                    self.dtype, C.byref(p)), "restrict_lm_head")
+        self.handle = p
+        self._keep = None
+
+    def close(self):
+        if self.handle:
+            lib().frs_head_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def draft_host(self, h: np.ndarray, k: int, mode="exact"):
+        """One level with HOST buffers (H2D, K2, D2H, sync): the e2e call."""
+        h = np.ascontiguousarray(h, np.float32)
+        n = h.shape[0]
+        ridx, full, prob = np.empty((n, k), np.int32), np.empty((n, k), np.int32), np.empty((n, k), np.float32)
+        check(lib().frs_head_draft_host(self.handle, _np_ptr(h), n, k, _mode(mode), _np_ptr(ridx), _np_ptr(full),
+                                        _np_ptr(prob)), "draft_host")
+        return ridx, full, prob
+
+    def build_draft_tree(self, root_token: int, params: DraftParams = DraftParams(), mode="exact",
+                         provider: Optional[Callable] = None, hidden_table: Optional[torch.Tensor] = None) -> DraftTree:
+        """Head-path build_draft_tree (drafting.cpp:122-245, greedy). provider(level, tokens,
+        parent_cands) -> CUDA float32 [n x d] tensor of the forwarded rows' hidden states."""
+        keep = {}
+
+        def cb(_user, level, n, tok_p, par_p, hidden_dev, stream):
+            try:
+                toks = np.ctypeslib.as_array(tok_p, (n,)).copy()
+                pars = np.ctypeslib.as_array(par_p, (n,)).copy()
+                hid = provider(level, toks, pars).to(torch.float32).contiguous()
+                dst = torch.as_tensor(_DeviceView(hidden_dev, (n, self.d)), device=hid.device)
+                dst.copy_(hid)
+                torch.cuda.current_stream(hid.device).synchronize()  # library stream reads it next
+                return 0
+            except Exception as exc:  # surfaced as FRS_ELOGIC by the library
+                keep["exc"] = exc
+                return 9
+
+        fn = _lib.HIDDEN_FN(cb) if provider is not None else C.cast(None, _lib.HIDDEN_FN)
+        total = params.total_draft_tokens
+        tok, par, dep = (np.empty(max(total, 1), np.int32) for _ in range(3))
+        lj, cnt = np.empty(max(total, 1), np.float64), C.c_int()
+        st = lib().frs_draft_tree(self.handle, root_token, fn, None, _ptr(hidden_table), params.beam_width,
+                                  params.search_depth, total, _mode(mode), _np_ptr(tok), _np_ptr(par), _np_ptr(dep),
+                                  _np_ptr(lj), C.byref(cnt))
+        if "exc" in keep:
+            raise keep["exc"]
+        check(st, "build_draft_tree")
+        n = cnt.value
+        return DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy())
+
+
+class _DeviceView:
+    """__cuda_array_interface__ view of a library-owned float32 device buffer."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+@dataclass
+class VerifyOutcome:  # verification.h:25-30
+    accepted_path: np.ndarray
+    emitted: np.ndarray
+
+    def accepted_length(self) -> int:
+        return int(self.emitted.size)
+
+
+def verify_greedy(ctx: Context, h_dev: torch.Tensor, lm_head: torch.Tensor, tree: DraftTree, mode="exact") -> VerifyOutcome:
+    """verification.cpp:42-71 with the target head on the device. h_dev: [1 + K, d] CUDA
+    float32 (row 0 = root position, row 1 + i = node i)."""
+    k = len(tree)
+    dt = DTYPE_BF16 if lm_head.dtype == torch.bfloat16 else DTYPE_F32
+    em, path = np.empty(k + 1, np.int32), np.empty(max(k, 1), np.int32)
+    ne, npth = C.c_int(), C.c_int()
+    tok, par = _i32(tree.tokens), _i32(tree.parents)
+    check(lib().frs_verify_greedy(ctx.handle, _ptr(h_dev.contiguous()), _ptr(lm_head), lm_head.shape[0],
+                                  lm_head.shape[1], dt, _mode(mode), _np_ptr(tok), _np_ptr(par), k, _np_ptr(em),
+                                  C.byref(ne), _np_ptr(path), C.byref(npth)), "verify_greedy")
+    return VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy())
+
+
+@dataclass
+class AcceptanceStats:  # verification.h:52-62, verification.cpp:180-206
+    iterations: int = 0
+    emitted: int = 0
+    mean_accepted_length: float = 0.0
+    histogram: list = field(default_factory=list)
+
+    def add(self, accepted_length: int) -> None:
+        self.iterations += 1
+        self.emitted += accepted_length
+        if len(self.histogram) <= accepted_length:
+            self.histogram.extend([0] * (accepted_length + 1 - len(self.histogram)))
+        self.histogram[accepted_length] += 1
+        self.mean_accepted_length = self.emitted / self.iterations
+
+    def merge(self, other: "AcceptanceStats") -> None:
+        self.iterations += other.iterations
+        self.emitted += other.emitted
+        if len(self.histogram) < len(other.histogram):
+            self.histogram.extend([0] * (len(other.histogram) - len(self.histogram)))
+        for i, v in enumerate(other.histogram):
+            self.histogram[i] += v
+        self.mean_accepted_length = self.emitted / self.iterations if self.iterations else 0.0
+
+
+def accepted_length_stats(outcomes: Sequence[VerifyOutcome]) -> AcceptanceStats:
+    if not outcomes:
+        raise InvalidArgument("accepted_length_stats: empty outcome list")
+    s = AcceptanceStats()
+    for o in outcomes:
+        s.add(o.accepted_length())
+    return s
+
+
+__all__ = [n for n in dir() if not n.startswith("_")] + ["CapacityError"]

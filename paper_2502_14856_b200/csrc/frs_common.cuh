@@ -1,0 +1,73 @@
+// Shared internals of libfrspec_cuda.so: context, error plumbing, device helpers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "frspec_cuda.h"
+
+namespace frs {
+
+// ---- error plumbing: status codes + thread-local message (frspec_cuda.h) ----
+void set_error(const std::string &msg);
+int fail(int status, const std::string &msg);
+#define FRS_CUDA_TRY(expr)                                                                   \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return ::frs::fail(FRS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define FRS_REQUIRE(cond, msg)                                  \
+    do {                                                        \
+        if (!(cond)) return ::frs::fail(FRS_EINVAL, (msg));     \
+    } while (0)
+
+// Grow-only device scratch buffer.
+struct DevBuf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    int ensure(size_t need);
+    ~DevBuf();
+};
+
+}  // namespace frs
+
+struct frs_ctx {
+    int device = 0;
+    int sm_count = 148;
+    size_t smem_optin = 0;
+    frs::DevBuf logits;    // [rows x vocab] fp32 logits (EXACT)
+    frs::DevBuf scratch;   // [rows x vocab] fp32 exp values (EXACT softmax)
+    frs::DevBuf counters;  // work-queue counters for persistent kernels
+    frs::DevBuf flags;     // uint32 status flags
+    frs::DevBuf fast_ws;   // FAST path candidate/partials workspace
+    frs::DevBuf hbuf;      // host-API staging of hidden rows
+    frs::DevBuf obuf;      // host-API staging of outputs
+    void *pinned = nullptr;
+    size_t pinned_bytes = 0;
+    cudaStream_t stream = nullptr;  // owned stream for the host-buffer conveniences
+};
+
+namespace frs {
+
+constexpr int kMaxK = 64;  // width <= total_draft_tokens <= 64 (drafting.cpp:14-20)
+
+// Launchers (defined in the .cu files); all return frs_status.
+int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *W, int w_dtype,
+                        int v_rows, float *logits, cudaStream_t s);
+int launch_softmax_topk(frs_ctx *ctx, const float *logits, int n, int v, int k, float temperature,
+                        const int32_t *ordered_ids, int32_t *out_ridx, int32_t *out_full,
+                        float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags,
+                        cudaStream_t s);
+int launch_argmax_rows(frs_ctx *ctx, const float *logits, int m, int v, int32_t id_offset,
+                       int32_t *out_id, float *out_val, uint32_t *out_flags, cudaStream_t s);
+int launch_fast_draft(frs_ctx *ctx, const float *h, int n, int d, const void *slab, int v_sub,
+                      const int32_t *ordered_ids, int k, float temperature, int32_t *out_ridx,
+                      int32_t *out_full, float *out_prob, float *out_rowmax, double *out_total,
+                      uint32_t *out_flags, cudaStream_t s);
+int launch_fast_verify(frs_ctx *ctx, const float *h, int m, int d, const void *W, int v_rows,
+                       int32_t id_offset, int32_t *out_id, float *out_val, uint32_t *out_flags,
+                       cudaStream_t s);
+
+}  // namespace frs

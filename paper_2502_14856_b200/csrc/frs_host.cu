@@ -1,0 +1,434 @@
+// Host side of the boundary (C++20 over the C ABI): the one-time FR vocabulary build
+// (vocab.cpp:23-178 semantics), the device-resident RestrictedHead, and the head-path
+// build_draft_tree / verify_greedy drivers (drafting.cpp:122-245, verification.cpp:13-71).
+// Integer / bookkeeping work stays on the host exactly as in the reference (std::log on the
+// same libm, std::sort comparators identical), so the device only runs the HBM-bound heads.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "frs_common.cuh"
+
+struct frs_head {
+    frs_ctx *ctx = nullptr;
+    void *slab = nullptr;
+    int32_t *ordered_dev = nullptr;
+    std::vector<int32_t> ordered;
+    int64_t vocab = 0;
+    int v_sub = 0, d = 0, dtype = FRS_DTYPE_F32;
+    // per-level staging (device + pinned host)
+    frs::DevBuf lvl_ridx, lvl_full, lvl_prob, lvl_tok, hidden;
+    int32_t *h_ridx = nullptr, *h_full = nullptr, *h_tok = nullptr;
+    float *h_prob = nullptr;
+};
+
+namespace frs {
+namespace {
+
+int check_forced(const int32_t *forced, int n_forced, int vocab_size) {
+    for (int f = 0; f < n_forced; ++f)
+        if (forced[f] < 0 || forced[f] >= vocab_size)
+            return fail(FRS_EINVAL, "subset: forced id " + std::to_string(forced[f]) + " out of range");
+    return FRS_OK;
+}
+
+struct Cand {
+    int32_t token, ridx, parent, depth;
+    double log_joint;
+};
+
+// (log_joint desc, candidate index asc) — drafting.cpp:83-86 / 167-172
+struct ByLogJoint {
+    const std::vector<Cand> *c;
+    bool operator()(int a, int b) const {
+        if ((*c)[a].log_joint != (*c)[b].log_joint) return (*c)[a].log_joint > (*c)[b].log_joint;
+        return a < b;
+    }
+};
+
+}  // namespace
+}  // namespace frs
+
+using namespace frs;
+
+extern "C" {
+
+// vocab.cpp:23-38
+int frs_count_frequencies(const int32_t *stream, int64_t count, int vocab_size, uint64_t *counts) {
+    FRS_REQUIRE(vocab_size >= 1, "count_frequencies: vocab_size must be >= 1");
+    FRS_REQUIRE(counts && (count == 0 || stream), "count_frequencies: null pointer");
+    std::fill(counts, counts + vocab_size, 0ull);
+    for (int64_t i = 0; i < count; ++i) {
+        const int32_t t = stream[i];
+        if (t < 0 || t >= vocab_size)
+            return fail(FRS_EINVAL, "count_frequencies: token id " + std::to_string(t) + " out of range at offset " +
+                                        std::to_string(i));
+        ++counts[t];
+    }
+    return FRS_OK;
+}
+
+// vocab.cpp:70-102 (+ finalize_subset 42-58)
+int frs_build_subset(const uint64_t *counts, int vocab_size, int size, const int32_t *forced, int n_forced,
+                     int32_t *ordered_out) {
+    FRS_REQUIRE(counts && ordered_out, "build_subset: null pointer");
+    if (size < 1 || size > vocab_size)
+        return fail(FRS_EINVAL, "build_subset: size " + std::to_string(size) + " out of range");
+    int st = check_forced(forced, n_forced, vocab_size);
+    if (st) return st;
+    std::vector<char> is_member(vocab_size, 0);
+    std::vector<int32_t> members;
+    for (int f = 0; f < n_forced; ++f)
+        if (!is_member[forced[f]]) {
+            is_member[forced[f]] = 1;
+            members.push_back(forced[f]);
+        }
+    if (static_cast<int>(members.size()) > size)
+        return fail(FRS_EINVAL, "build_subset: size smaller than the forced id count");
+    auto by_count = [&](int32_t a, int32_t b) {
+        if (counts[a] != counts[b]) return counts[a] > counts[b];
+        return a < b;
+    };
+    std::vector<int32_t> order(vocab_size);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), by_count);
+    for (int32_t t : order) {
+        if (static_cast<int>(members.size()) >= size) break;
+        if (!is_member[t]) {
+            is_member[t] = 1;
+            members.push_back(t);
+        }
+    }
+    std::sort(members.begin(), members.end(), by_count);
+    std::copy(members.begin(), members.end(), ordered_out);
+    return FRS_OK;
+}
+
+// vocab.cpp:104-138
+int frs_subset_from_ranking(const int32_t *ranked, int n_ranked, int size, int vocab_size, const int32_t *forced,
+                            int n_forced, int32_t *ordered_out) {
+    FRS_REQUIRE(ranked && ordered_out, "subset_from_ranking: null pointer");
+    if (size < 1 || size > n_ranked) return fail(FRS_EINVAL, "subset_from_ranking: size out of range");
+    int st = check_forced(forced, n_forced, vocab_size);
+    if (st) return st;
+    std::vector<char> seen(vocab_size, 0);
+    for (int i = 0; i < n_ranked; ++i) {
+        const int32_t t = ranked[i];
+        if (t < 0 || t >= vocab_size)
+            return fail(FRS_EINVAL, "subset_from_ranking: id " + std::to_string(t) + " out of range");
+        if (seen[t]) return fail(FRS_EINVAL, "subset_from_ranking: duplicate id " + std::to_string(t));
+        seen[t] = 1;
+    }
+    std::vector<int32_t> members(ranked, ranked + size);
+    std::vector<char> is_member(vocab_size, 0);
+    for (int32_t t : members) is_member[t] = 1;
+    std::vector<int32_t> missing;
+    for (int f = 0; f < n_forced; ++f)
+        if (!is_member[forced[f]]) {
+            is_member[forced[f]] = 1;
+            missing.push_back(forced[f]);
+        }
+    if (static_cast<int>(missing.size()) > size)
+        return fail(FRS_EINVAL, "subset_from_ranking: size smaller than the forced id count");
+    for (size_t i = 0; i < missing.size(); ++i) members[members.size() - 1 - i] = missing[missing.size() - 1 - i];
+    std::copy(members.begin(), members.end(), ordered_out);
+    return FRS_OK;
+}
+
+// vocab.cpp:140-150
+int frs_coverage(const uint64_t *counts, int vocab_size, const int32_t *ordered, int v_sub, double *out) {
+    FRS_REQUIRE(counts && ordered && out, "coverage: null pointer");
+    uint64_t total = 0, covered = 0;
+    for (int t = 0; t < vocab_size; ++t) total += counts[t];
+    if (total == 0) return fail(FRS_ELOGIC, "coverage: undefined for an empty corpus");
+    for (int i = 0; i < v_sub; ++i) {
+        FRS_REQUIRE(ordered[i] >= 0 && ordered[i] < vocab_size, "coverage: subset does not match the table vocabulary");
+        covered += counts[ordered[i]];
+    }
+    *out = static_cast<double>(covered) / static_cast<double>(total);
+    return FRS_OK;
+}
+
+// vocab.cpp:170-178
+int frs_flops_ratio(int full_size, int restricted_size, double *out) {
+    FRS_REQUIRE(out, "flops_ratio: null pointer");
+    FRS_REQUIRE(full_size >= 1 && restricted_size >= 1, "flops_ratio: sizes must be positive");
+    FRS_REQUIRE(restricted_size <= full_size, "flops_ratio: restricted size exceeds full size");
+    *out = static_cast<double>(restricted_size) / static_cast<double>(full_size);
+    return FRS_OK;
+}
+
+// verification.cpp:13-27
+int frs_tree_mask(const int32_t *parents, int k, uint64_t *words) {
+    if (k > 64) return fail(FRS_ECAPACITY, "build_tree_mask: " + std::to_string(k) + " nodes exceed the 64-bit mask");
+    FRS_REQUIRE(k == 0 || (parents && words), "build_tree_mask: null pointer");
+    for (int i = 0; i < k; ++i) {
+        if (parents[i] >= i) return fail(FRS_EINVAL, "build_tree_mask: tree is not topological");
+        words[i] = (parents[i] >= 0 ? words[parents[i]] : 0ull) | (1ull << i);
+    }
+    return FRS_OK;
+}
+
+int frs_head_create(frs_ctx *ctx, const float *W, int64_t V, int d, int w_on_device, const int32_t *ordered_ids,
+                    int v_sub, int slab_dtype, frs_head **out) {
+    FRS_REQUIRE(ctx && W && ordered_ids && out, "restrict_lm_head: null pointer");
+    FRS_REQUIRE(V >= 1 && d >= 1 && v_sub >= 1 && v_sub <= V, "restrict_lm_head: bad sizes");
+    FRS_REQUIRE(slab_dtype == FRS_DTYPE_F32 || slab_dtype == FRS_DTYPE_BF16, "restrict_lm_head: unknown dtype");
+    for (int i = 0; i < v_sub; ++i)  // vocab.cpp:154-159
+        if (ordered_ids[i] < 0 || ordered_ids[i] >= V)
+            return fail(FRS_EINVAL, "restrict_lm_head: id " + std::to_string(ordered_ids[i]) +
+                                        " out of range for the LM head");
+    FRS_CUDA_TRY(cudaSetDevice(ctx->device));
+    frs_head *h = new frs_head();
+    h->ctx = ctx;
+    h->vocab = V;
+    h->v_sub = v_sub;
+    h->d = d;
+    h->dtype = slab_dtype;
+    h->ordered.assign(ordered_ids, ordered_ids + v_sub);
+    auto cleanup = [&](int st) {
+        frs_head_destroy(h);
+        return st;
+    };
+    if (cudaMalloc(&h->slab, frs_slab_bytes(v_sub, d, slab_dtype)) != cudaSuccess ||
+        cudaMalloc(&h->ordered_dev, sizeof(int32_t) * v_sub) != cudaSuccess)
+        return cleanup(fail(FRS_ECUDA, "restrict_lm_head: cudaMalloc failed"));
+    cudaStream_t s = ctx->stream;
+    if (cudaMemcpyAsync(h->ordered_dev, ordered_ids, sizeof(int32_t) * v_sub, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return cleanup(fail(FRS_ECUDA, "restrict_lm_head: copy of ids failed"));
+    const float *Wd = W;
+    float *tmp = nullptr;
+    if (!w_on_device) {  // stage only the subset rows: the gather happens on the host side of the copy
+        if (cudaMalloc(&tmp, sizeof(float) * (size_t)v_sub * d) != cudaSuccess)
+            return cleanup(fail(FRS_ECUDA, "restrict_lm_head: cudaMalloc failed"));
+        for (int i = 0; i < v_sub; ++i)
+            cudaMemcpyAsync(tmp + (size_t)i * d, W + (size_t)ordered_ids[i] * d, sizeof(float) * d,
+                            cudaMemcpyHostToDevice, s);
+        std::vector<int32_t> iota(v_sub);
+        std::iota(iota.begin(), iota.end(), 0);
+        int32_t *iota_dev = nullptr;
+        cudaMalloc(&iota_dev, sizeof(int32_t) * v_sub);
+        cudaMemcpyAsync(iota_dev, iota.data(), sizeof(int32_t) * v_sub, cudaMemcpyHostToDevice, s);
+        int st = frs_slab_build(ctx, tmp, v_sub, d, iota_dev, v_sub, slab_dtype, h->slab, s);
+        cudaFree(iota_dev);
+        cudaFree(tmp);
+        if (st) return cleanup(st);
+    } else {
+        int st = frs_slab_build(ctx, Wd, V, d, h->ordered_dev, v_sub, slab_dtype, h->slab, s);
+        if (st) return cleanup(st);
+    }
+    *out = h;
+    return FRS_OK;
+}
+
+int frs_head_destroy(frs_head *h) {
+    if (!h) return FRS_OK;
+    cudaSetDevice(h->ctx->device);
+    if (h->slab) cudaFree(h->slab);
+    if (h->ordered_dev) cudaFree(h->ordered_dev);
+    if (h->h_ridx) cudaFreeHost(h->h_ridx);
+    if (h->h_full) cudaFreeHost(h->h_full);
+    if (h->h_prob) cudaFreeHost(h->h_prob);
+    if (h->h_tok) cudaFreeHost(h->h_tok);
+    delete h;
+    return FRS_OK;
+}
+
+int frs_head_info(const frs_head *h, const void **slab, const int32_t **ordered_dev, int *v_sub, int *d,
+                  int *slab_dtype) {
+    FRS_REQUIRE(h, "null frs_head");
+    if (slab) *slab = h->slab;
+    if (ordered_dev) *ordered_dev = h->ordered_dev;
+    if (v_sub) *v_sub = h->v_sub;
+    if (d) *d = h->d;
+    if (slab_dtype) *slab_dtype = h->dtype;
+    return FRS_OK;
+}
+
+static int head_staging(frs_head *h, int rows, int k) {
+    const size_t cells = (size_t)rows * k;
+    int st;
+    if ((st = h->lvl_ridx.ensure(cells * 4)) || (st = h->lvl_full.ensure(cells * 4)) ||
+        (st = h->lvl_prob.ensure(cells * 4)) || (st = h->lvl_tok.ensure(64 * 4)) ||
+        (st = h->hidden.ensure((size_t)std::max(rows, 64) * h->d * sizeof(float))))
+        return st;
+    if (!h->h_ridx) {
+        const size_t cap = (size_t)64 * 64 * 4;
+        if (cudaMallocHost(&h->h_ridx, cap) != cudaSuccess || cudaMallocHost(&h->h_full, cap) != cudaSuccess ||
+            cudaMallocHost(&h->h_prob, cap) != cudaSuccess || cudaMallocHost(&h->h_tok, 64 * 4) != cudaSuccess)
+            return fail(FRS_ECUDA, "pinned staging allocation failed");
+    }
+    FRS_REQUIRE(cells <= (size_t)64 * 64, "host draft step: at most 64 rows x 64 children");
+    return FRS_OK;
+}
+
+int frs_head_draft_host(frs_head *h, const float *h_host, int n, int k, int mode, int32_t *ridx, int32_t *full,
+                        float *prob) {
+    FRS_REQUIRE(h && h_host && ridx && full && prob, "host draft step: null pointer");
+    FRS_REQUIRE(n >= 1 && n <= 64 && k >= 1 && k <= 64, "host draft step: 1 <= n, k <= 64");
+    FRS_CUDA_TRY(cudaSetDevice(h->ctx->device));
+    int st = head_staging(h, n, k);
+    if (st) return st;
+    cudaStream_t s = h->ctx->stream;
+    float *hd = static_cast<float *>(h->hidden.ptr);
+    FRS_CUDA_TRY(cudaMemcpyAsync(hd, h_host, sizeof(float) * (size_t)n * h->d, cudaMemcpyHostToDevice, s));
+    st = frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode,
+                             static_cast<int32_t *>(h->lvl_ridx.ptr), static_cast<int32_t *>(h->lvl_full.ptr),
+                             static_cast<float *>(h->lvl_prob.ptr), nullptr, nullptr, nullptr, nullptr, s);
+    if (st) return st;
+    const size_t cells = (size_t)n * k;
+    FRS_CUDA_TRY(cudaMemcpyAsync(ridx, h->lvl_ridx.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaMemcpyAsync(full, h->lvl_full.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaMemcpyAsync(prob, h->lvl_prob.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaStreamSynchronize(s));
+    return FRS_OK;
+}
+
+// drafting.cpp:122-245, greedy, head path: per level the provider supplies the forwarded
+// rows' hidden states, the device runs K2, the host keeps the reference's beam bookkeeping.
+int frs_draft_tree(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user, const float *hidden_table,
+                   int width, int depth, int total, int mode, int32_t *tokens, int32_t *parents, int32_t *depths,
+                   double *log_joint, int *count) {
+    FRS_REQUIRE(h && tokens && parents && depths && log_joint && count, "build_draft_tree: null pointer");
+    if (width < 1) return fail(FRS_EINVAL, "draft params: beam_width must be >= 1");
+    if (depth < 1) return fail(FRS_EINVAL, "draft params: search_depth must be >= 1");
+    if (total < width || total > 64)
+        return fail(FRS_EINVAL, "draft params: total_draft_tokens must lie in [beam_width, 64]");
+    FRS_REQUIRE(fn || hidden_table, "build_draft_tree: need a hidden provider or a hidden table");
+    FRS_CUDA_TRY(cudaSetDevice(h->ctx->device));
+    const int w = std::min(width, h->v_sub);  // drafting.cpp:40
+    int st = head_staging(h, width, w);
+    if (st) return st;
+    cudaStream_t s = h->ctx->stream;
+    float *hd = static_cast<float *>(h->hidden.ptr);
+    int32_t *tok_dev = static_cast<int32_t *>(h->lvl_tok.ptr);
+
+    std::vector<Cand> cands;
+    std::vector<int> beam;
+    std::vector<int32_t> btok, bpar;
+    auto run_level = [&](int level, int nb) -> int {
+        if (fn) {
+            const int rc = fn(user, level, nb, btok.data(), bpar.data(), hd, s);
+            if (rc) return fail(FRS_ELOGIC, "hidden provider failed with code " + std::to_string(rc));
+        } else {
+            std::memcpy(h->h_tok, btok.data(), sizeof(int32_t) * nb);
+            FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, h->h_tok, sizeof(int32_t) * nb, cudaMemcpyHostToDevice, s));
+            const int rc = frs_gather_rows(h->ctx, hidden_table, h->vocab, h->d, tok_dev, nb, hd, s);
+            if (rc) return rc;
+        }
+        int rc = frs_draft_head_topk(h->ctx, hd, nb, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, w, 1.0f, mode,
+                                     static_cast<int32_t *>(h->lvl_ridx.ptr), static_cast<int32_t *>(h->lvl_full.ptr),
+                                     static_cast<float *>(h->lvl_prob.ptr), nullptr, nullptr, nullptr, nullptr, s);
+        if (rc) return rc;
+        const size_t cells = (size_t)nb * w;
+        FRS_CUDA_TRY(cudaMemcpyAsync(h->h_ridx, h->lvl_ridx.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaMemcpyAsync(h->h_full, h->lvl_full.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaMemcpyAsync(h->h_prob, h->lvl_prob.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaStreamSynchronize(s));
+        return FRS_OK;
+    };
+
+    // Forward 1 of search_depth: the root row (drafting.cpp:133-160).
+    btok.assign(1, root_token);
+    bpar.assign(1, -1);
+    if ((st = run_level(0, 1))) return st;
+    for (int c = 0; c < w; ++c) {
+        beam.push_back(static_cast<int>(cands.size()));
+        cands.push_back({h->h_full[c], h->h_ridx[c], -1, 1, std::log(static_cast<double>(h->h_prob[c]))});
+    }
+    for (int level = 1; level < depth && !beam.empty(); ++level) {
+        if (static_cast<int>(beam.size()) > width) {  // drafting.cpp:164-176
+            std::sort(beam.begin(), beam.end(), ByLogJoint{&cands});
+            beam.resize(width);
+            std::sort(beam.begin(), beam.end());
+        }
+        const int nb = static_cast<int>(beam.size());
+        btok.resize(nb);
+        bpar.resize(nb);
+        for (int i = 0; i < nb; ++i) {
+            btok[i] = cands[beam[i]].token;
+            bpar[i] = cands[beam[i]].parent;
+        }
+        if ((st = run_level(level, nb))) return st;
+        std::vector<int> next;
+        for (int i = 0; i < nb; ++i) {  // drafting.cpp:199-220 (parent fields read by value)
+            const int pidx = beam[i];
+            const int pdepth = cands[pidx].depth;
+            const double plj = cands[pidx].log_joint;
+            for (int c = 0; c < w; ++c) {
+                const size_t o = (size_t)i * w + c;
+                next.push_back(static_cast<int>(cands.size()));
+                cands.push_back({h->h_full[o], h->h_ridx[o], pidx, pdepth + 1,
+                                 plj + std::log(static_cast<double>(h->h_prob[o]))});
+            }
+        }
+        beam = std::move(next);
+    }
+    // select_top_k (drafting.cpp:93-118, prefix_closed = false) and emit (230-244)
+    std::vector<int> order(cands.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), ByLogJoint{&cands});
+    std::vector<char> sel(cands.size(), 0);
+    int cnt = 0;
+    for (int c : order) {
+        if (sel[c]) continue;
+        if (cands[c].parent >= 0 && !sel[cands[c].parent]) continue;
+        if (cnt + 1 > total) continue;
+        sel[c] = 1;
+        ++cnt;
+    }
+    std::vector<int> remap(cands.size(), -1);
+    int out = 0;
+    for (size_t i = 0; i < cands.size(); ++i) {
+        if (!sel[i]) continue;
+        remap[i] = out;
+        tokens[out] = cands[i].token;
+        parents[out] = cands[i].parent >= 0 ? remap[cands[i].parent] : -1;
+        depths[out] = cands[i].depth;
+        log_joint[out] = cands[i].log_joint;
+        ++out;
+    }
+    *count = out;
+    return FRS_OK;
+}
+
+int frs_verify_greedy(frs_ctx *ctx, const float *h_dev, const void *W, int V, int d, int w_dtype, int mode,
+                      const int32_t *tokens, const int32_t *parents, int k, int32_t *emitted, int *n_emitted,
+                      int32_t *path, int *n_path) {
+    FRS_REQUIRE(ctx && h_dev && W && emitted && n_emitted && path && n_path, "verify_greedy: null pointer");
+    if (k > 64) return fail(FRS_ECAPACITY, "build_tree_mask: nodes exceed the 64-bit mask");
+    FRS_REQUIRE(k >= 0 && (k == 0 || (tokens && parents)), "verify_greedy: bad tree");
+    for (int i = 0; i < k; ++i)
+        if (parents[i] >= i || parents[i] < -1) return fail(FRS_EINVAL, "verify_greedy: tree is not topological");
+    FRS_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    // device scratch: argmax ids [65] | tokens [64] | parents [64] | emitted [65] | path [64] | counts [2]
+    int st = ctx->obuf.ensure(sizeof(int32_t) * 324);
+    if (st) return st;
+    int32_t *ids = static_cast<int32_t *>(ctx->obuf.ptr);
+    int32_t *tt = ids + 65, *pp = tt + 64, *d_em = pp + 64, *d_path = d_em + 65, *d_cnt = d_path + 64;
+    if (k > 0) {
+        FRS_CUDA_TRY(cudaMemcpyAsync(tt, tokens, sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
+        FRS_CUDA_TRY(cudaMemcpyAsync(pp, parents, sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
+    }
+    st = frs_verify_head_argmax(ctx, h_dev, 1 + k, d, W, V, w_dtype, 0, mode, ids, nullptr, nullptr, s);
+    if (st) return st;
+    st = frs_accept_greedy(ctx, ids, tt, pp, k, d_em, d_path, d_cnt, s);
+    if (st) return st;
+    int32_t cnt[2] = {0, 0};
+    std::vector<int32_t> em(65), pth(64);
+    FRS_CUDA_TRY(cudaMemcpyAsync(em.data(), d_em, sizeof(int32_t) * 65, cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaMemcpyAsync(pth.data(), d_path, sizeof(int32_t) * 64, cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaStreamSynchronize(s));
+    *n_emitted = cnt[0];
+    *n_path = cnt[1];
+    std::copy(em.begin(), em.begin() + cnt[0], emitted);
+    std::copy(pth.begin(), pth.begin() + cnt[1], path);
+    return FRS_OK;
+}
+
+}  // extern "C"

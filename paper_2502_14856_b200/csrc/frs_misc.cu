@@ -1,0 +1,159 @@
+// K1 slab build, K4 greedy accept, K5 vocab-parallel argmax merge, row gather.
+#include <cuda_bf16.h>
+
+#include "frs_common.cuh"
+
+namespace frs {
+namespace {
+
+// K1 — restrict_lm_head (vocab.cpp:152-168) on the device: one CTA per slab row (grid-stride),
+// 16-byte vector loads/stores. fp32 -> fp32 is a bitwise copy; fp32 -> bf16 rounds to nearest
+// even (exact when W is bf16-representable, which the bf16 parity fixtures guarantee).
+template <bool BF16>
+__global__ void __launch_bounds__(256)
+    k_slab_build(const float *__restrict__ W, long long V, int d, const int32_t *__restrict__ ids,
+                 int v_sub, void *__restrict__ slab, int *__restrict__ err) {
+    for (int row = blockIdx.x; row < v_sub; row += gridDim.x) {
+        const int src = ids[row];
+        if (src < 0 || src >= V) {
+            if (threadIdx.x == 0) atomicExch(err, 1);
+            continue;
+        }
+        const float *s = W + (size_t)src * d;
+        if (!BF16) {
+            float *o = static_cast<float *>(slab) + (size_t)row * d;
+            if ((d & 3) == 0) {
+                const float4 *s4 = reinterpret_cast<const float4 *>(s);
+                float4 *o4 = reinterpret_cast<float4 *>(o);
+                for (int c = threadIdx.x; c < d / 4; c += blockDim.x) o4[c] = __ldg(s4 + c);
+            } else {
+                for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = s[c];
+            }
+        } else {
+            __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(slab) + (size_t)row * d;
+            if ((d & 3) == 0) {
+                const float4 *s4 = reinterpret_cast<const float4 *>(s);
+                for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+                    const float4 v = __ldg(s4 + c);
+                    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+                    uint2 packed;
+                    packed.x = *reinterpret_cast<uint32_t *>(&a);
+                    packed.y = *reinterpret_cast<uint32_t *>(&b);
+                    reinterpret_cast<uint2 *>(o)[c] = packed;
+                }
+            } else {
+                for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = __float2bfloat16_rn(s[c]);
+            }
+        }
+    }
+}
+
+// K4 — verify_greedy walk (verification.cpp:42-71) in one warp: children of `node` are the
+// indices c with parents[c] == node in ascending order (children_by_node, :31-38); the first
+// whose token equals the target argmax is accepted, otherwise the argmax is the bonus token.
+__global__ void k_accept_greedy(const int32_t *__restrict__ argmax_ids, const int32_t *__restrict__ tokens,
+                                const int32_t *__restrict__ parents, int k, int32_t *__restrict__ emitted,
+                                int32_t *__restrict__ path, int32_t *__restrict__ counts) {
+    const int lane = threadIdx.x;
+    int node = -1, ne = 0, np = 0;
+    for (int step = 0; step <= k; ++step) {  // a path has at most k nodes
+        const int32_t best = argmax_ids[node + 1];
+        int match = -1;
+        for (int base = 0; base < k && match < 0; base += 32) {
+            const int c = base + lane;
+            const bool hit = c < k && parents[c] == node && tokens[c] == best;
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (m) match = base + __ffs(m) - 1;
+        }
+        if (lane == 0) emitted[ne] = best;
+        ++ne;
+        if (match < 0) break;
+        if (lane == 0) path[np] = match;
+        ++np;
+        node = match;
+    }
+    if (lane == 0) {
+        counts[0] = ne;
+        counts[1] = np;
+    }
+}
+
+__device__ __forceinline__ uint32_t ord_bits(float x) {
+    if (x == 0.0f) x = 0.0f;
+    const uint32_t b = __float_as_uint(x);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// K5 — merge shard-major (value, id) pairs by (value desc, id asc).
+__global__ void k_argmax_merge(const float *__restrict__ vals, const int32_t *__restrict__ ids, int shards,
+                               int m, float *__restrict__ out_val, int32_t *__restrict__ out_id) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= m) return;
+    unsigned long long best = 0ull;
+    int bs = 0;
+    for (int g = 0; g < shards; ++g) {
+        const unsigned long long key = (static_cast<unsigned long long>(ord_bits(vals[(size_t)g * m + row])) << 32) |
+                                       (0xffffffffu - static_cast<uint32_t>(ids[(size_t)g * m + row]));
+        if (key > best) {
+            best = key;
+            bs = g;
+        }
+    }
+    out_val[row] = vals[(size_t)bs * m + row];
+    out_id[row] = ids[(size_t)bs * m + row];
+}
+
+__global__ void __launch_bounds__(256)
+    k_gather_rows(const float *__restrict__ table, long long rows, int d, const int32_t *__restrict__ tokens,
+                  int n, float *__restrict__ out) {
+    const int i = blockIdx.x;
+    if (i >= n) return;
+    const int t = tokens[i];
+    const bool ok = t >= 0 && t < rows;
+    for (int c = threadIdx.x; c < d; c += blockDim.x)
+        out[(size_t)i * d + c] = ok ? table[(size_t)t * d + c] : 0.0f;
+}
+
+}  // namespace
+
+int slab_build(frs_ctx *ctx, const float *W, long long V, int d, const int32_t *ids, int v_sub, int dtype,
+               void *slab, cudaStream_t s) {
+    int st = ctx->flags.ensure(256);
+    if (st) return st;
+    int *err = static_cast<int *>(ctx->flags.ptr);
+    FRS_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int), s));
+    const int grid = ctx->sm_count * 8;
+    if (dtype == FRS_DTYPE_BF16)
+        k_slab_build<true><<<grid, 256, 0, s>>>(W, V, d, ids, v_sub, slab, err);
+    else
+        k_slab_build<false><<<grid, 256, 0, s>>>(W, V, d, ids, v_sub, slab, err);
+    FRS_CUDA_TRY(cudaGetLastError());
+    int host_err = 0;
+    FRS_CUDA_TRY(cudaMemcpyAsync(&host_err, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaStreamSynchronize(s));
+    if (host_err) return fail(FRS_EINVAL, "restrict_lm_head: subset id out of range for the LM head");
+    return FRS_OK;
+}
+
+int accept_greedy(const int32_t *argmax_ids, const int32_t *tokens, const int32_t *parents, int k,
+                  int32_t *emitted, int32_t *path, int32_t *counts, cudaStream_t s) {
+    k_accept_greedy<<<1, 32, 0, s>>>(argmax_ids, tokens, parents, k, emitted, path, counts);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+int argmax_merge(const float *vals, const int32_t *ids, int shards, int m, float *out_val, int32_t *out_id,
+                 cudaStream_t s) {
+    k_argmax_merge<<<(m + 127) / 128, 128, 0, s>>>(vals, ids, shards, m, out_val, out_id);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+int gather_rows(const float *table, long long rows, int d, const int32_t *tokens, int n, float *out,
+                cudaStream_t s) {
+    k_gather_rows<<<n, 256, 0, s>>>(table, rows, d, tokens, n, out);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+}  // namespace frs
