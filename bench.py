@@ -1,0 +1,300 @@
+#!/usr/bin/env python3
+"""bench.py — FR-Spec draft LM head + softmax + top-k + id remap (K2) on B200.
+
+Step = one draft level: n=10 beam rows against the FR slab at the Llama-3-8B shape
+(d=4096, V=128256 -> V_sub=32768, k=10), BASELINE.json configs[1]. The slab (268 MB bf16 /
+537 MB fp32) is larger than the 126 MB L2, so every step streams it from HBM (no flush
+needed). Multi-GPU: independent decode streams, one replica per rank, no collective
+(weak scaling).
+
+  python bench.py [--gpus N --steps K --warmup W] [--mode auto|fast|exact] [--dtype bf16|f32]
+  python bench.py --impl reference     # the reference's own CPU draft level on the host cores
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FR draft LM-head+top-k µs/step & HBM GB/s; decode tokens/s, Llama-3-8B shape"
+C2 = dict(d=4096, vocab=128256, v_sub=32768, rows=10, k=10)
+NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=2000)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--mode", choices=["auto", "fast", "exact"], default="auto")
+    p.add_argument("--dtype", choices=["bf16", "f32"], default="bf16")
+    p.add_argument("--v-sub", type=int, default=C2["v_sub"])
+    p.add_argument("--rows", type=int, default=C2["rows"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler(threading.Thread):
+    """NVML sampling of SM clock and throttle reasons DURING the timed region."""
+
+    def __init__(self, index: int, period: float = 0.005):
+        super().__init__(daemon=True)
+        self.period, self.samples, self.reasons, self.stop_flag = period, [], 0, threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def run(self):
+        while self.nv and not self.stop_flag.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                break
+            time.sleep(self.period)
+
+    def summary(self):
+        self.stop_flag.set()
+        self.join(timeout=1.0)
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz, "samples": len(s),
+                "reasons": [n for b, n in NVML_REASONS.items() if self.reasons & b and b != 0x1]}
+
+
+def rmsnorm_rows(x):
+    import torch
+    return (x * torch.rsqrt(x.double().pow(2).mean(dim=1, keepdim=True) + 1e-5).float()).contiguous()
+
+
+def synth(device, d, V, v_sub, seed):
+    """Random-init LM head (bf16-representable fp32) and a permuted frequency ranking."""
+    import numpy as np
+    import torch
+    from paper_2502_14856_b200 import api
+    g = torch.Generator(device=device).manual_seed(seed)
+    W = (torch.randn(V, d, generator=g, device=device) * 0.02).to(torch.bfloat16).float()
+    ranked = np.random.default_rng(seed).permutation(V).astype(np.int32)
+    subset = api.subset_from_ranking(ranked, v_sub, V, forced=[0, 1])
+    return W, subset
+
+
+def cpu_reference_rate(slab_f32, h_rows, k, seconds, threads):
+    """The compiled reference (oracle/_ref) draft level — matmul + softmax + topk per row — on
+    `threads` host threads, each running whole levels until the time budget is spent."""
+    from oracle.oracle import REFERENCE_SO, Reference, Restatement
+    if os.path.exists(REFERENCE_SO):
+        head, kind = Reference().head(slab_f32), "reference"
+        run = lambda h: head.draft_level(h, k)  # noqa: E731
+    else:  # the restatement (port) of the same arithmetic
+        R, kind = Restatement(), "port"
+        run = lambda h: R.draft_level(h, slab_f32, None, k)  # noqa: E731
+    counts = [0] * threads
+    barrier = threading.Barrier(threads + 1)
+    deadline = [0.0]
+
+    def worker(i):
+        barrier.wait()
+        while time.perf_counter() < deadline[0]:
+            run(h_rows)
+            counts[i] += 1
+
+    ths = [threading.Thread(target=worker, args=(i,), daemon=True) for i in range(threads)]
+    for t in ths:
+        t.start()
+    t0 = time.perf_counter()
+    deadline[0] = t0 + seconds
+    barrier.wait()
+    for t in ths:
+        t.join()
+    el = time.perf_counter() - t0
+    total = sum(counts)
+    return total / el, kind, total, el
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path, all host threads."""
+    import numpy as np
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(1234)
+    slab = (rng.standard_normal((args.v_sub, C2["d"]), dtype=np.float32) * 0.02).astype(np.float32)
+    h = rng.standard_normal((args.rows, C2["d"])).astype(np.float32)
+    h /= np.sqrt((h.astype(np.float64) ** 2).mean(axis=1, keepdims=True) + 1e-5).astype(np.float32)
+    budget = min(120.0, max(20.0, 0.3 * (args.steps + args.warmup)))
+    rate, kind, levels, el = cpu_reference_rate(slab, h, C2["k"], budget, threads)
+    line = {"metric": METRIC, "value": rate, "unit": "draft-steps/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": levels, "warmup": 0, "ms_per_step": 1000.0 * threads / rate if rate else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (N(0,0.02) fp32 slab, rmsnorm'd N(0,1) hidden rows)",
+            "config": {"workload": "draft LM-head+top-k level (model.cpp:278 + drafting.cpp:204,37-43), "
+                                   "Llama-3-8B shape", "d": C2["d"], "v_sub": args.v_sub, "rows": args.rows,
+                       "k": C2["k"], "slab_dtype": "f32 (reference dtype)"},
+            "cpu_baseline": {"value": rate, "unit": "draft-steps/s", "cores": threads, "kind": kind,
+                             "sample": f"{levels} whole levels over {el:.1f} s on {threads} threads "
+                                       f"(independent streams, one level at a time per thread)"},
+            "e2e": {"value": rate, "unit": "draft-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2502_14856_b200 import api
+
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    d, V, v_sub, n, k = C2["d"], C2["vocab"], args.v_sub, args.rows, C2["k"]
+
+    ctx = api.Context(local)
+    W, subset = synth(dev, d, V, v_sub, seed=1234)
+    t0 = time.perf_counter()
+    head = api.restrict_lm_head(ctx, W, subset, dtype=args.dtype)
+    torch.cuda.synchronize()
+    slab_build_ms = 1000 * (time.perf_counter() - t0)
+
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    pool = [rmsnorm_rows(torch.randn(n, d, generator=g, device=dev)) for _ in range(16)]
+    mode = args.mode
+    if mode == "auto":
+        mode = "exact"
+        if args.dtype == "bf16":
+            try:
+                api.draft_head_topk(ctx, pool[0], head, k, mode="fast")
+                mode = "fast"
+            except api._lib.NotSupported:
+                pass
+    out = api.draft_head_topk(ctx, pool[0], head, k, mode=mode)
+    for i in range(args.warmup):
+        api.draft_head_topk(ctx, pool[i % len(pool)], head, k, mode=mode, out=out)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    ctx.set_timing(True)
+    launches0 = ctx.launch_count
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        api.draft_head_topk(ctx, pool[i % len(pool)], head, k, mode=mode, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.summary()
+    elapsed_ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count - launches0
+    kern_ms, kern_n = ctx.timing_read()
+    ctx.set_timing(False)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+
+    bytes_w = 2 if args.dtype == "bf16" else 4
+    alg_bytes = v_sub * d * bytes_w + n * d * 4 + n * k * 12
+    hbm_peak, peak_kind = peaks()
+    kern_avg_s = (kern_ms / max(kern_n, 1)) / 1000.0
+    achieved = alg_bytes / kern_avg_s / 1e9 if kern_n else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_{mode}_{args.dtype}_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+
+    # e2e through the public host-buffer API: pinned H2D of h, K2, D2H of ids/probs, sync.
+    dh = api.DeviceHead(ctx, W, subset, dtype=args.dtype)
+    pinned = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+    pinned.copy_(pool[0].cpu())
+    h_host = pinned.numpy()
+    for _ in range(3):
+        dh.draft_host(h_host, k, mode=mode)
+    e2e_steps = max(20, min(args.steps, 500))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dh.draft_host(h_host, k, mode=mode)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        slab32 = head.slab.float().cpu().numpy()
+        threads = len(os.sched_getaffinity(0))
+        rate, kind, levels, el = cpu_reference_rate(slab32, pool[0].cpu().numpy(), k, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": "draft-steps/s", "cores": threads, "kind": kind,
+               "sample": f"{levels} whole draft levels (n={n}, V_sub={v_sub}, d={d}, fp32 slab = the bf16 "
+                         f"values widened) in {el:.1f} s across {threads} threads"}
+
+    if rank == 0:
+        ms_per_step = elapsed_ms / args.steps
+        line = {
+            "metric": METRIC, "value": world * args.steps / (elapsed_ms / 1000.0), "unit": "draft-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "us_per_step": 1000.0 * ms_per_step, "hbm_gbs_per_gpu": alg_bytes / (ms_per_step / 1000.0) / 1e9,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if args.dtype == "bf16" else "f32",
+            "data": "synthetic: random-init bf16-representable LM head N(0,0.02), permuted FR ranking, "
+                    "rmsnorm'd N(0,1) hidden rows",
+            "config": {"workload": "FR draft LM-head + softmax + top-k + id remap, one draft level "
+                                   "(BASELINE configs[1], Llama-3-8B shape)",
+                       "d": d, "vocab": V, "v_sub": v_sub, "rows": n, "k": k, "slab_dtype": args.dtype,
+                       "mode": mode, "l2": "inputs larger than L2: the slab streamed each step exceeds 126 MB",
+                       "parallelism": f"replicas x{world} (independent decode streams, no collective)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
+                         "peak_source": peak_kind, "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel_us": kern_avg_s * 1e6, "timed_calls": kern_n},
+            "cpu_baseline": cpu,
+            "e2e": {"value": world * e2e_steps / e2e_s, "unit": "draft-steps/s",
+                    "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": 3 * n * k * 4,
+                    "api": "frs_head_draft_host (C ABI, pinned host buffers, synchronous)"},
+            "clocks": clocks, "gpu_launches": launches, "slab_build_ms": slab_build_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

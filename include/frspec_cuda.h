@@ -74,6 +74,16 @@ FRS_API const char *frs_last_error(void);
 FRS_API int frs_ctx_create(int device, frs_ctx **out);
 FRS_API int frs_ctx_destroy(frs_ctx *ctx);
 FRS_API int frs_ctx_sm_count(const frs_ctx *ctx);
+/* Live device timing of each call's dominant kernel (CUDA events on the launch stream), for
+ * the roofline measurement: enable, run, then read the summed milliseconds and call count. */
+FRS_API int frs_ctx_set_timing(frs_ctx *ctx, int enable);
+FRS_API int frs_ctx_timing_read(frs_ctx *ctx, double *total_ms, int *count);
+/* Diagnostic: copy the per-CTA partials of the last FAST call ([n][G] max / sum-exp / bound,
+ * [n][G][4] candidate keys, [G] max |W_j|^2; G = frs_ctx_sm_count) to host buffers. */
+FRS_API int frs_debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float *pth,
+                                    uint64_t *pkey, float *pw2);
+/* Number of kernels this library has launched on ctx (evidence for bench gpu_launches). */
+FRS_API int frs_ctx_launch_count(const frs_ctx *ctx, uint64_t *out);
 /* Pre-size workspaces for up to max_rows hidden rows against up to max_vocab head rows. */
 FRS_API int frs_ctx_reserve(frs_ctx *ctx, int max_rows, int64_t max_vocab, int d);
 

@@ -227,6 +227,12 @@ class Reference:
         L.ref_build_tree_mask.argtypes = [_i32p, C.c_int, _u64p]
         L.ref_verify_greedy.argtypes = [_f32p, C.c_int, _f32p, C.c_int, _i32p, _i32p, _i32p, _ip, _i32p, _ip]
         L.ref_model_lm_head.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _f32p]
+        L.ref_head_new.restype = C.c_void_p
+        L.ref_head_new.argtypes = [_f32p, C.c_int, C.c_int]
+        L.ref_head_free.restype = None
+        L.ref_head_free.argtypes = [C.c_void_p]
+        L.ref_draft_level.argtypes = [C.c_void_p, _f32p, C.c_int, C.c_int, C.c_int, _i32p, _f32p]
+        L.ref_verify_argmax.argtypes = [C.c_void_p, _f32p, C.c_int, C.c_int, _i32p]
         L.ref_model_draft_tree.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_void_p, C.c_int, _i32p, C.c_int,
                                                            C.c_int, C.c_int, C.c_int, _i32p, _i32p, _i32p, _f64p, _ip]
         L.ref_model_draft_capture.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_void_p, C.c_int, _i32p, C.c_int,
@@ -320,6 +326,9 @@ class Reference:
                     "verify_greedy")
         return em[: ne.value].copy(), path[: npth.value].copy()
 
+    def head(self, W) -> "RefHead":
+        return RefHead(self, W)
+
     def model_lm_head(self, V, d, layers, heads, seed):
         out = np.empty((V, d), np.float32)
         self._check(self.lib.ref_model_lm_head(V, d, layers, heads, seed, out), "model_lm_head")
@@ -354,3 +363,32 @@ class Reference:
         return dict(hidden=hid[:r].copy(), row_token=rtok[:r].copy(), row_level=rlev[:r].copy(),
                     tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(),
                     log_joint=lj[:n].copy())
+
+
+class RefHead:
+    """A reference ``Matrix`` LM head kept resident, for timing the reference's own draft level
+    (model.cpp:278 + drafting.cpp:204, 37-43) and verify head (model.cpp:278 + kernels.cpp:113)."""
+
+    def __init__(self, ref: Reference, W):
+        self.ref = ref
+        W = _c32(W)
+        self.rows, self.d = W.shape
+        self.ptr = ref.lib.ref_head_new(W, self.rows, self.d)
+
+    def draft_level(self, h, k: int):
+        h = _c32(np.atleast_2d(h))
+        n = h.shape[0]
+        ridx, prob = np.zeros((n, k), np.int32), np.zeros((n, k), np.float32)
+        self.ref._check(self.ref.lib.ref_draft_level(self.ptr, h, n, self.d, k, ridx, prob), "draft_level")
+        return ridx, prob
+
+    def verify_argmax(self, h):
+        h = _c32(np.atleast_2d(h))
+        ids = np.zeros(h.shape[0], np.int32)
+        self.ref._check(self.ref.lib.ref_verify_argmax(self.ptr, h, h.shape[0], self.d, ids), "verify_argmax")
+        return ids
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            self.ref.lib.ref_head_free(self.ptr)
+            self.ptr = None

@@ -230,6 +230,37 @@ int ref_verify_greedy(const float * root_logits, int V, const float * node_logit
     });
 }
 
+// A persistent reference Matrix for timing the reference's own draft level without per-call
+// copies of the head (the CPU baseline in bench.py).
+void * ref_head_new(const float * W, int rows, int d) { return new Matrix(to_matrix(W, rows, d)); }
+void ref_head_free(void * head) { delete static_cast<Matrix *>(head); }
+
+// One draft level exactly as the reference runs it: LM-head matmul (model.cpp:278), then per
+// row softmax (drafting.cpp:204) and pick_children -> topk(min(width, V_sub)) (drafting.cpp:37-43).
+int ref_draft_level(const void * head, const float * h, int n, int d, int k, int32_t * ridx, float * prob) {
+    return guarded([&] {
+        const Matrix & W = *static_cast<const Matrix *>(head);
+        Matrix logits = matmul(to_matrix(h, n, d), W);
+        const int w = std::min(k, W.rows);
+        for (int i = 0; i < n; ++i) {
+            ProbVector p = softmax(logits.row_span(i), 1.0f);
+            auto r = topk(p.probs, w);
+            for (int c = 0; c < w; ++c) {
+                ridx[(size_t)i * k + c] = r[c].first;
+                prob[(size_t)i * k + c] = r[c].second;
+            }
+        }
+    });
+}
+
+// Verify head as the reference runs it: matmul over the full head, argmax per row.
+int ref_verify_argmax(const void * head, const float * h, int m, int d, int32_t * ids) {
+    return guarded([&] {
+        Matrix logits = matmul(to_matrix(h, m, d), *static_cast<const Matrix *>(head));
+        for (int i = 0; i < m; ++i) ids[i] = argmax(logits.row_span(i));
+    });
+}
+
 // Exports the seeded toy model's LM head [V x d] (model.cpp:93-128).
 int ref_model_lm_head(int V, int d, int layers, int heads, uint64_t seed, float * out) {
     return guarded([&] {

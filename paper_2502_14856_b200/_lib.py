@@ -59,6 +59,10 @@ SIGNATURES = [
     ("frs_ctx_destroy", _I, [_P]),
     ("frs_ctx_sm_count", _I, [_P]),
     ("frs_ctx_reserve", _I, [_P, _I, _I64, _I]),
+    ("frs_ctx_set_timing", _I, [_P, _I]),
+    ("frs_ctx_timing_read", _I, [_P, C.POINTER(C.c_double), C.POINTER(_I)]),
+    ("frs_ctx_launch_count", _I, [_P, C.POINTER(_U64)]),
+    ("frs_debug_fast_partials", _I, [_P, _I, _I, _P, _P, _P, _P, _P]),
     ("frs_slab_build", _I, [_P, _P, _I64, _I, _P, _I, _I, _P, _P]),
     ("frs_slab_bytes", C.c_size_t, [_I, _I, _I]),
     ("frs_draft_head_topk", _I, [_P, _P, _I, _I, _P, _I, _I, _P, _I, _F, _I, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -71,6 +71,22 @@ class Context:
     def reserve(self, max_rows: int, max_vocab: int, d: int) -> None:
         check(lib().frs_ctx_reserve(self.handle, max_rows, max_vocab, d), "frs_ctx_reserve")
 
+    def set_timing(self, enable: bool) -> None:
+        """Record CUDA events around each call's dominant kernel (on its launch stream)."""
+        check(lib().frs_ctx_set_timing(self.handle, int(enable)), "set_timing")
+
+    def timing_read(self):
+        """-> (summed milliseconds, number of timed calls); resets the record."""
+        ms, cnt = C.c_double(), C.c_int()
+        check(lib().frs_ctx_timing_read(self.handle, C.byref(ms), C.byref(cnt)), "timing_read")
+        return ms.value, cnt.value
+
+    @property
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        check(lib().frs_ctx_launch_count(self.handle, C.byref(v)), "launch_count")
+        return int(v.value)
+
     def close(self) -> None:
         if self.handle:
             lib().frs_ctx_destroy(self.handle)

@@ -54,6 +54,24 @@ static int check_device(frs_ctx *ctx) {
 
 static bool valid_dtype(int dt) { return dt == FRS_DTYPE_F32 || dt == FRS_DTYPE_BF16; }
 
+void timing_begin(frs_ctx *ctx, cudaStream_t s) {
+    if (!ctx->timing) return;
+    if (ctx->ev_used + 2 > ctx->ev.size()) {
+        for (int i = 0; i < 256; ++i) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return;
+            ctx->ev.push_back(e);
+        }
+    }
+    cudaEventRecord(ctx->ev[ctx->ev_used], s);
+}
+
+void timing_end(frs_ctx *ctx, cudaStream_t s) {
+    if (!ctx->timing || ctx->ev_used + 2 > ctx->ev.size()) return;
+    cudaEventRecord(ctx->ev[ctx->ev_used + 1], s);
+    ctx->ev_used += 2;
+}
+
 }  // namespace frs
 
 using namespace frs;
@@ -89,6 +107,7 @@ int frs_ctx_create(int device, frs_ctx **out) {
 int frs_ctx_destroy(frs_ctx *ctx) {
     if (!ctx) return FRS_OK;
     cudaSetDevice(ctx->device);
+    for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;
@@ -96,6 +115,41 @@ int frs_ctx_destroy(frs_ctx *ctx) {
 }
 
 int frs_ctx_sm_count(const frs_ctx *ctx) { return ctx ? ctx->sm_count : 0; }
+
+int frs_ctx_set_timing(frs_ctx *ctx, int enable) {
+    FRS_REQUIRE(ctx, "null frs_ctx");
+    ctx->timing = enable != 0;
+    ctx->ev_used = 0;
+    return FRS_OK;
+}
+
+int frs_ctx_timing_read(frs_ctx *ctx, double *total_ms, int *count) {
+    FRS_REQUIRE(ctx && total_ms && count, "frs_ctx_timing_read: null pointer");
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < ctx->ev_used; i += 2) {
+        FRS_CUDA_TRY(cudaEventSynchronize(ctx->ev[i + 1]));
+        float ms = 0.0f;
+        FRS_CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]));
+        tot += ms;
+    }
+    *total_ms = tot;
+    *count = static_cast<int>(ctx->ev_used / 2);
+    ctx->ev_used = 0;
+    return FRS_OK;
+}
+
+int frs_debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float *pth, uint64_t *pkey,
+                            float *pw2) {
+    int st = check_device(ctx);
+    if (st) return st;
+    return frs::debug_fast_partials(ctx, n, d, pm, ps, pth, reinterpret_cast<unsigned long long *>(pkey), pw2);
+}
+
+int frs_ctx_launch_count(const frs_ctx *ctx, uint64_t *out) {
+    FRS_REQUIRE(ctx && out, "frs_ctx_launch_count: null pointer");
+    *out = ctx->launches;
+    return FRS_OK;
+}
 
 int frs_ctx_reserve(frs_ctx *ctx, int max_rows, int64_t max_vocab, int d) {
     int st = check_device(ctx);
@@ -121,6 +175,7 @@ int frs_slab_build(frs_ctx *ctx, const float *W, int64_t V, int d, const int32_t
     FRS_REQUIRE(W && ordered_ids && slab, "restrict_lm_head: null pointer");
     FRS_REQUIRE(V >= 1 && d >= 1 && v_sub >= 1, "restrict_lm_head: sizes must be positive");
     FRS_REQUIRE(valid_dtype(slab_dtype), "restrict_lm_head: unknown slab dtype");
+    ++ctx->launches;
     return slab_build(ctx, W, V, d, ordered_ids, v_sub, slab_dtype, slab, static_cast<cudaStream_t>(stream));
 }
 
@@ -184,6 +239,7 @@ int frs_accept_greedy(frs_ctx *ctx, const int32_t *argmax_ids, const int32_t *to
     FRS_REQUIRE(k >= 0, "verify_greedy: negative node count");
     if (k > 64) return fail(FRS_ECAPACITY, "build_tree_mask: nodes exceed the 64-bit mask");
     FRS_REQUIRE(k == 0 || (tokens && parents), "verify_greedy: null tree arrays");
+    ++ctx->launches;
     return accept_greedy(argmax_ids, tokens, parents, k, out_emitted, out_path, out_counts,
                          static_cast<cudaStream_t>(stream));
 }
@@ -194,6 +250,7 @@ int frs_argmax_merge(frs_ctx *ctx, const float *vals, const int32_t *ids, int sh
     if (st) return st;
     FRS_REQUIRE(vals && ids && out_val && out_id, "argmax merge: null pointer");
     FRS_REQUIRE(shards >= 1 && m >= 1, "argmax merge: sizes must be positive");
+    ++ctx->launches;
     return argmax_merge(vals, ids, shards, m, out_val, out_id, static_cast<cudaStream_t>(stream));
 }
 
@@ -203,6 +260,7 @@ int frs_gather_rows(frs_ctx *ctx, const float *table, int64_t rows, int d, const
     if (st) return st;
     FRS_REQUIRE(table && tokens && out, "gather: null pointer");
     FRS_REQUIRE(rows >= 1 && d >= 1 && n >= 1, "gather: sizes must be positive");
+    ++ctx->launches;
     return gather_rows(table, rows, d, tokens, n, out, static_cast<cudaStream_t>(stream));
 }
 

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "frspec_cuda.h"
 
@@ -42,14 +43,23 @@ struct frs_ctx {
     frs::DevBuf counters;  // work-queue counters for persistent kernels
     frs::DevBuf flags;     // uint32 status flags
     frs::DevBuf fast_ws;   // FAST path candidate/partials workspace
+    frs::DevBuf fast_ctr;  // FAST finalize per-row arrival counters (monotonic, zeroed once)
     frs::DevBuf hbuf;      // host-API staging of hidden rows
     frs::DevBuf obuf;      // host-API staging of outputs
     void *pinned = nullptr;
     size_t pinned_bytes = 0;
     cudaStream_t stream = nullptr;  // owned stream for the host-buffer conveniences
+    // live timing of the dominant kernel of each call (bench roofline), on its own stream
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;  // start/stop pairs
+    size_t ev_used = 0;
+    unsigned long long launches = 0;  // kernels launched by this library on this ctx
 };
 
 namespace frs {
+
+void timing_begin(frs_ctx *ctx, cudaStream_t s);
+void timing_end(frs_ctx *ctx, cudaStream_t s);
 
 constexpr int kMaxK = 64;  // width <= total_draft_tokens <= 64 (drafting.cpp:14-20)
 
@@ -66,6 +76,8 @@ int launch_fast_draft(frs_ctx *ctx, const float *h, int n, int d, const void *sl
                       const int32_t *ordered_ids, int k, float temperature, int32_t *out_ridx,
                       int32_t *out_full, float *out_prob, float *out_rowmax, double *out_total,
                       uint32_t *out_flags, cudaStream_t s);
+int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float *pth, unsigned long long *pkey,
+                        float *pw2);
 int launch_fast_verify(frs_ctx *ctx, const float *h, int m, int d, const void *W, int v_rows,
                        int32_t id_offset, int32_t *out_id, float *out_val, uint32_t *out_flags,
                        cudaStream_t s);

@@ -1,0 +1,228 @@
+// Device helpers shared by the EXACT and FAST kernels: the glibc expf port, order-preserving
+// float keys, block reductions and the exact per-row softmax + top-k (kernels.cpp:62-122).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "frspec_cuda.h"
+
+namespace frs {
+namespace dev {
+
+// ---- glibc 2.39 expf, FMA ifunc ----
+__device__ __forceinline__ float expf_glibc(float x, const unsigned long long *tab) {
+    const uint32_t ux = __float_as_uint(x);
+    const uint32_t abstop = (ux >> 20) & 0x7ffu;
+    if (abstop >= 0x42bu) {
+        if (ux == 0xff800000u) return 0.0f;
+        if (abstop >= 0x7f8u) return x + x;
+        if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);
+        if (x < -0x1.9fe368p6f) return 0.0f;
+    }
+    const double xd = static_cast<double>(x);
+    double kd = __fma_rn(0x1.71547652b82fep+5, xd, 0x1.8p+52);
+    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
+    kd = __dsub_rn(kd, 0x1.8p+52);
+    const double r = __fma_rn(0x1.71547652b82fep+5, xd, -kd);
+    const unsigned long long tt = tab[ki & 31ull] + (ki << 47);
+    const double s = __longlong_as_double(static_cast<long long>(tt));
+    const double z = __fma_rn(0x1.c6af84b912394p-20, r, 0x1.ebfce50fac4f3p-13);
+    const double r2 = __dmul_rn(r, r);
+    double y = __fma_rn(0x1.62e42ff0c52d6p-6, r, 1.0);
+    y = __fma_rn(z, r2, y);
+    y = __dmul_rn(y, s);
+    return __double2float_rn(y);
+}
+
+static __device__ const unsigned long long kExp2fTable[32] = {
+        0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
+        0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,
+        0x3fef06fe0a31b715ULL, 0x3feef1a7373aa9cbULL, 0x3feedea64c123422ULL, 0x3feece086061892dULL,
+        0x3feebfdad5362a27ULL, 0x3feeb42b569d4f82ULL, 0x3feeab07dd485429ULL, 0x3feea47eb03a5585ULL,
+        0x3feea09e667f3bcdULL, 0x3fee9f75e8ec5f74ULL, 0x3feea11473eb0187ULL, 0x3feea589994cce13ULL,
+        0x3feeace5422aa0dbULL, 0x3feeb737b0cdc5e5ULL, 0x3feec49182a3f090ULL, 0x3feed503b23e255dULL,
+        0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
+        0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
+
+__device__ __forceinline__ void load_exp_table(unsigned long long *tab) {
+    if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTable[threadIdx.x];
+}
+
+// Exponent of the lowest set bit of a non-negative float (INT_MAX for 0).
+__device__ __forceinline__ int lsb_exponent(float v) {
+    const uint32_t b = __float_as_uint(v);
+    const uint32_t ex = (b >> 23) & 0xffu;
+    uint32_t m = b & 0x7fffffu;
+    if (ex != 0) m |= 0x800000u;
+    if (m == 0) return 0x7fffffff;
+    return (ex != 0 ? static_cast<int>(ex) - 150 : -149) + (__ffs(m) - 1);
+}
+
+// Order-preserving map float -> uint32 (with -0 == +0, as under the reference's '>').
+__device__ __forceinline__ uint32_t ordered_bits(float x) {
+    if (x == 0.0f) x = 0.0f;
+    const uint32_t b = __float_as_uint(x);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float from_ordered(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+// (value desc, index asc) as one descending uint64 key; 0 is below every real key.
+__device__ __forceinline__ unsigned long long value_key(float v, int idx) {
+    return (static_cast<unsigned long long>(ordered_bits(v)) << 32) | (0xffffffffu - static_cast<uint32_t>(idx));
+}
+__device__ __forceinline__ int key_index(unsigned long long k) {
+    return static_cast<int>(0xffffffffu - static_cast<uint32_t>(k & 0xffffffffull));
+}
+__device__ __forceinline__ float key_value(unsigned long long k) { return from_ordered(static_cast<uint32_t>(k >> 32)); }
+// probabilities are >= +0: their raw bits already order them
+__device__ __forceinline__ unsigned long long prob_key(float p, int j) {
+    return (static_cast<unsigned long long>(__float_as_uint(p)) << 32) | (0xffffffffu - static_cast<uint32_t>(j));
+}
+
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, Op op, T *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // serial over the (<= 32) warp partials: no identity element needed
+        v = red[0];
+        for (int w = 1; w < nw; ++w) v = op(v, red[w]);
+        red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+struct MaxF { __device__ float operator()(float a, float b) const { return fmaxf(a, b); } };
+struct SumD { __device__ double operator()(double a, double b) const { return a + b; } };
+struct MinI { __device__ int operator()(int a, int b) const { return min(a, b); } };
+struct OrI { __device__ int operator()(int a, int b) const { return a | b; } };
+struct MaxU64 {
+    __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const { return a > b ? a : b; }
+};
+
+struct ReduceScratch {
+    unsigned long long tab[32];
+    double d[32];
+    float f[32];
+    int i[32];
+    unsigned long long k[32];
+};
+
+// Exact softmax (kernels.cpp:62-91) + top-kk (kernels.cpp:93-111) + remap for ONE row whose
+// exact logits are L[0..v): the whole block cooperates; E is a [v] float scratch. Writes
+// out[0..k) (entries past min(k, v) get -1 / 0). Returns flags (thread 0's copy is valid).
+static __device__ __noinline__ uint32_t softmax_topk_row(const float *__restrict__ L, int v, int k,
+                                                         float temperature, const int32_t *__restrict__ ordered,
+                                                         float *__restrict__ E, int32_t *out_ridx, int32_t *out_full,
+                                                         float *out_prob, float *out_rowmax, double *out_total,
+                                                         ReduceScratch &rs) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    load_exp_table(rs.tab);
+    float mx = -__int_as_float(0x7f800000);
+    int bad = 0;
+    for (int j = tid; j < v; j += nt) {
+        const float x = L[j];
+        if (!isfinite(x)) bad = 1;
+        const float y = __fdiv_rn(x, temperature);
+        mx = (mx < y) ? y : mx;
+    }
+    mx = block_reduce(mx, MaxF(), rs.f);
+    bad = block_reduce(bad, OrI(), rs.i);
+    uint32_t flags = bad ? FRS_FLAG_NONFINITE : 0u;
+
+    double part = 0.0;
+    int lsb = 0x7fffffff;
+    for (int j = tid; j < v; j += nt) {
+        const float e = expf_glibc(__fsub_rn(__fdiv_rn(L[j], temperature), mx), rs.tab);
+        E[j] = e;
+        part += static_cast<double>(e);
+        lsb = min(lsb, lsb_exponent(e));
+    }
+    double total = block_reduce(part, SumD(), rs.d);
+    lsb = block_reduce(lsb, MinI(), rs.i);
+    // Every partial sum (in any order) is exact iff all e_j are multiples of
+    // 2^(ilogb(total)-51) (one bit of slack keeps it rigorous): then the tree sum equals the
+    // reference's index-order sum. Otherwise replay the reference order (kernels.cpp:80-85).
+    const bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
+    if (!exact) {
+        flags |= FRS_FLAG_SEQ_SUM;
+        __syncthreads();
+        if (tid == 0) {
+            double acc = 0.0;
+            for (int j = 0; j < v; ++j) acc += static_cast<double>(E[j]);
+            rs.d[0] = acc;
+        }
+        __syncthreads();
+        total = rs.d[0];
+    }
+    const float inv = __double2float_rn(1.0 / total);
+
+    unsigned long long cand = 0ull;
+    for (int j = tid; j < v; j += nt) {
+        const unsigned long long key = prob_key(__fmul_rn(E[j], inv), j);
+        cand = key > cand ? key : cand;
+    }
+    const int kk = min(k, v);
+    for (int r = 0; r < kk; ++r) {
+        const unsigned long long best = block_reduce(cand, MaxU64(), rs.k);
+        const int j = key_index(best);
+        if (tid == 0) {
+            out_ridx[r] = j;
+            out_full[r] = ordered ? ordered[j] : j;
+            out_prob[r] = __uint_as_float(static_cast<uint32_t>(best >> 32));
+        }
+        if (j % nt == tid) {  // the owner rescans for its best key below `best`
+            cand = 0ull;
+            for (int jj = tid; jj < v; jj += nt) {
+                const unsigned long long key = prob_key(__fmul_rn(E[jj], inv), jj);
+                if (key < best && key > cand) cand = key;
+            }
+        }
+    }
+    if (tid == 0) {
+        for (int r = kk; r < k; ++r) {
+            out_ridx[r] = -1;
+            out_full[r] = -1;
+            out_prob[r] = 0.0f;
+        }
+        if (out_rowmax) *out_rowmax = mx;
+        if (out_total) *out_total = total;
+    }
+    return flags;
+}
+
+// Exact dot_f32 (kernels.cpp:13-32) of h (fp32) with a bf16/fp32 row, computed by the 8
+// lanes l = threadIdx.x % 8 of an aligned 8-lane group; the result is valid in lane l == 0.
+// Requires the 8 lanes of the group to be converged; d % 8 == 0 handled by the lane chains,
+// the scalar tail by lane 0.
+template <typename WT>
+__device__ __forceinline__ float w_at(const WT *w, int i);
+template <>
+__device__ __forceinline__ float w_at<float>(const float *w, int i) { return w[i]; }
+template <>
+__device__ __forceinline__ float w_at<unsigned short>(const unsigned short *w, int i) {
+    return __uint_as_float(static_cast<uint32_t>(w[i]) << 16);
+}
+
+template <typename WT>
+__device__ __forceinline__ float dot_f32_lanes8(const float *h, const WT *w, int d) {
+    const int l = threadIdx.x & 7;
+    const int T = d >> 3;
+    float s = 0.0f;
+#pragma unroll 8
+    for (int t = 0; t < T; ++t) s = __fadd_rn(s, __fmul_rn(h[8 * t + l], w_at(w, 8 * t + l)));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+    if (l == 0)
+        for (int e = 8 * T; e < d; ++e) s = __fadd_rn(s, __fmul_rn(h[e], w_at(w, e)));
+    return s;
+}
+
+}  // namespace dev
+}  // namespace frs

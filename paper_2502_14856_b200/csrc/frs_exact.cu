@@ -21,6 +21,7 @@
 #include <algorithm>
 
 #include "frs_common.cuh"
+#include "frs_device.cuh"
 
 namespace frs {
 namespace {
@@ -105,188 +106,25 @@ __global__ void __launch_bounds__(1024, 1)
     }
 }
 
-// ---- glibc 2.39 expf, FMA ifunc, device port ----
-__constant__ unsigned long long kExp2fT[32] = {
-    0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
-    0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,
-    0x3fef06fe0a31b715ULL, 0x3feef1a7373aa9cbULL, 0x3feedea64c123422ULL, 0x3feece086061892dULL,
-    0x3feebfdad5362a27ULL, 0x3feeb42b569d4f82ULL, 0x3feeab07dd485429ULL, 0x3feea47eb03a5585ULL,
-    0x3feea09e667f3bcdULL, 0x3fee9f75e8ec5f74ULL, 0x3feea11473eb0187ULL, 0x3feea589994cce13ULL,
-    0x3feeace5422aa0dbULL, 0x3feeb737b0cdc5e5ULL, 0x3feec49182a3f090ULL, 0x3feed503b23e255dULL,
-    0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
-    0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
-
-__device__ __forceinline__ float expf_glibc(float x, const unsigned long long *tab) {
-    const uint32_t ux = __float_as_uint(x);
-    const uint32_t abstop = (ux >> 20) & 0x7ffu;
-    if (abstop >= 0x42bu) {
-        if (ux == 0xff800000u) return 0.0f;
-        if (abstop >= 0x7f8u) return x + x;
-        if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);
-        if (x < -0x1.9fe368p6f) return 0.0f;
-    }
-    const double xd = static_cast<double>(x);
-    double kd = __fma_rn(0x1.71547652b82fep+5, xd, 0x1.8p+52);
-    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
-    kd = __dsub_rn(kd, 0x1.8p+52);
-    const double r = __fma_rn(0x1.71547652b82fep+5, xd, -kd);
-    const unsigned long long tt = tab[ki & 31ull] + (ki << 47);
-    const double s = __longlong_as_double(static_cast<long long>(tt));
-    const double z = __fma_rn(0x1.c6af84b912394p-20, r, 0x1.ebfce50fac4f3p-13);
-    const double r2 = __dmul_rn(r, r);
-    double y = __fma_rn(0x1.62e42ff0c52d6p-6, r, 1.0);
-    y = __fma_rn(z, r2, y);
-    y = __dmul_rn(y, s);
-    return __double2float_rn(y);
-}
-
-// Exponent of the lowest set bit of a positive float (INT_MAX for 0).
-__device__ __forceinline__ int lsb_exponent(float v) {
-    const uint32_t b = __float_as_uint(v);
-    const uint32_t ex = (b >> 23) & 0xffu;
-    uint32_t m = b & 0x7fffffu;
-    if (ex != 0) m |= 0x800000u;
-    if (m == 0) return 0x7fffffff;
-    return (ex != 0 ? static_cast<int>(ex) - 150 : -149) + (__ffs(m) - 1);
-}
-
-template <typename T, typename Op>
-__device__ __forceinline__ T block_reduce(T v, Op op, T *red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-    __syncthreads();
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-        v = lane < nw ? red[lane] : red[0];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0) red[0] = v;
-    }
-    __syncthreads();
-    return red[0];
-}
-
-struct MaxF { __device__ float operator()(float a, float b) const { return fmaxf(a, b); } };
-struct SumD { __device__ double operator()(double a, double b) const { return a + b; } };
-struct MinI { __device__ int operator()(int a, int b) const { return min(a, b); } };
-struct OrI { __device__ int operator()(int a, int b) const { return a | b; } };
-struct MaxU64 {
-    __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const {
-        return a > b ? a : b;
-    }
-};
-
-__device__ __forceinline__ unsigned long long prob_key(float p, int j) {
-    return (static_cast<unsigned long long>(__float_as_uint(p)) << 32) | (0xffffffffu - static_cast<uint32_t>(j));
-}
-
-// One CTA per row: exact softmax (kernels.cpp:62-91) + top-kk by (prob desc, idx asc)
-// (kernels.cpp:93-111) + restricted->full remap (drafting.cpp:151/210).
+// One CTA per row: exact softmax + top-k + remap (dev::softmax_topk_row).
 __global__ void __launch_bounds__(1024)
     k_softmax_topk(const float *__restrict__ logits, int ld, int v, int k, float temperature,
-                   const int32_t *__restrict__ ordered, float *__restrict__ ework,
-                   int32_t *__restrict__ out_ridx, int32_t *__restrict__ out_full,
-                   float *__restrict__ out_prob, float *__restrict__ out_rowmax,
+                   const int32_t *__restrict__ ordered, float *__restrict__ ework, int32_t *__restrict__ out_ridx,
+                   int32_t *__restrict__ out_full, float *__restrict__ out_prob, float *__restrict__ out_rowmax,
                    double *__restrict__ out_total, uint32_t *__restrict__ out_flags) {
-    __shared__ unsigned long long tab[32];
-    __shared__ double red_d[32];
-    __shared__ float red_f[32];
-    __shared__ int red_i[32];
-    __shared__ unsigned long long red_k[32];
-    const int row = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    if (tid < 32) tab[tid] = kExp2fT[tid];
-    const float *L = logits + (size_t)row * ld;
-    float *E = ework + (size_t)row * ld;
-
-    float mx = -__int_as_float(0x7f800000);
-    int bad = 0;
-    for (int j = tid; j < v; j += nt) {
-        const float x = L[j];
-        if (!isfinite(x)) bad = 1;
-        const float y = __fdiv_rn(x, temperature);
-        mx = (mx < y) ? y : mx;
-    }
-    mx = block_reduce(mx, MaxF(), red_f);
-    bad = block_reduce(bad, OrI(), red_i);
-    uint32_t flags = bad ? FRS_FLAG_NONFINITE : 0u;
-
-    double part = 0.0;
-    int lsb = 0x7fffffff;
-    for (int j = tid; j < v; j += nt) {
-        const float e = expf_glibc(__fsub_rn(__fdiv_rn(L[j], temperature), mx), tab);
-        E[j] = e;
-        part += static_cast<double>(e);
-        lsb = min(lsb, lsb_exponent(e));
-    }
-    double total = block_reduce(part, SumD(), red_d);
-    lsb = block_reduce(lsb, MinI(), red_i);
-    // Every partial sum (any order) is exact iff all e_j are multiples of 2^(ilogb(total)-51)
-    // (one bit of slack keeps the claim rigorous); then the tree sum equals the reference's
-    // index-order sum. Otherwise replay the reference order (kernels.cpp:80-85).
-    const bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
-    if (!exact) {
-        flags |= FRS_FLAG_SEQ_SUM;
-        __syncthreads();
-        if (tid == 0) {
-            double acc = 0.0;
-            for (int j = 0; j < v; ++j) acc += static_cast<double>(E[j]);
-            red_d[0] = acc;
-        }
-        __syncthreads();
-        total = red_d[0];
-    }
-    const float inv = __double2float_rn(1.0 / total);
-
-    unsigned long long cand = 0ull;
-    for (int j = tid; j < v; j += nt) {
-        const unsigned long long key = prob_key(__fmul_rn(E[j], inv), j);
-        cand = key > cand ? key : cand;
-    }
-    const int kk = min(k, v);
-    for (int r = 0; r < kk; ++r) {
-        const unsigned long long best = block_reduce(cand, MaxU64(), red_k);
-        const int j = static_cast<int>(0xffffffffu - static_cast<uint32_t>(best & 0xffffffffull));
-        if (tid == 0) {
-            out_ridx[(size_t)row * k + r] = j;
-            out_full[(size_t)row * k + r] = ordered ? ordered[j] : j;
-            out_prob[(size_t)row * k + r] = __uint_as_float(static_cast<uint32_t>(best >> 32));
-        }
-        if (j % nt == tid) {  // owner rescans for its best key below `best`
-            cand = 0ull;
-            for (int jj = tid; jj < v; jj += nt) {
-                const unsigned long long key = prob_key(__fmul_rn(E[jj], inv), jj);
-                if (key < best && key > cand) cand = key;
-            }
-        }
-    }
-    if (tid == 0) {
-        for (int r = kk; r < k; ++r) {
-            out_ridx[(size_t)row * k + r] = -1;
-            out_full[(size_t)row * k + r] = -1;
-            out_prob[(size_t)row * k + r] = 0.0f;
-        }
-        if (out_rowmax) out_rowmax[row] = mx;
-        if (out_total) out_total[row] = total;
-        if (out_flags) out_flags[row] = flags;
-    }
-}
-
-__device__ __forceinline__ uint32_t ordered_bits(float x) {
-    if (x == 0.0f) x = 0.0f;  // -0 == +0 under the reference's '>' (kernels.cpp:119)
-    const uint32_t b = __float_as_uint(x);
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float from_ordered(uint32_t o) {
-    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+    __shared__ dev::ReduceScratch rs;
+    const int row = blockIdx.x;
+    const uint32_t flags = dev::softmax_topk_row(
+        logits + (size_t)row * ld, v, k, temperature, ordered, ework + (size_t)row * ld, out_ridx + (size_t)row * k,
+        out_full + (size_t)row * k, out_prob + (size_t)row * k, out_rowmax ? out_rowmax + row : nullptr,
+        out_total ? out_total + row : nullptr, rs);
+    if (threadIdx.x == 0 && out_flags) out_flags[row] = flags;
 }
 
 // One CTA per row: argmax with ties to the lowest index (kernels.cpp:113-122).
 __global__ void __launch_bounds__(1024)
-    k_argmax_rows(const float *__restrict__ logits, int ld, int v, int32_t id_offset,
-                  int32_t *__restrict__ out_id, float *__restrict__ out_val,
-                  uint32_t *__restrict__ out_flags) {
+    k_argmax_rows(const float *__restrict__ logits, int ld, int v, int32_t id_offset, int32_t *__restrict__ out_id,
+                  float *__restrict__ out_val, uint32_t *__restrict__ out_flags) {
     __shared__ unsigned long long red_k[32];
     __shared__ int red_i[32];
     const int row = blockIdx.x;
@@ -296,14 +134,13 @@ __global__ void __launch_bounds__(1024)
     for (int j = threadIdx.x; j < v; j += blockDim.x) {
         const float x = L[j];
         if (!isfinite(x)) bad = 1;
-        const unsigned long long key =
-            (static_cast<unsigned long long>(ordered_bits(x)) << 32) | (0xffffffffu - static_cast<uint32_t>(j));
+        const unsigned long long key = dev::value_key(x, j);
         cand = key > cand ? key : cand;
     }
-    cand = block_reduce(cand, MaxU64(), red_k);
-    bad = block_reduce(bad, OrI(), red_i);
+    cand = dev::block_reduce(cand, dev::MaxU64(), red_k);
+    bad = dev::block_reduce(bad, dev::OrI(), red_i);
     if (threadIdx.x == 0) {
-        const int j = static_cast<int>(0xffffffffu - static_cast<uint32_t>(cand & 0xffffffffull));
+        const int j = dev::key_index(cand);
         out_id[row] = id_offset + j;
         if (out_val) out_val[row] = L[j];
         if (out_flags) out_flags[row] = bad ? FRS_FLAG_NONFINITE : 0u;
@@ -311,21 +148,22 @@ __global__ void __launch_bounds__(1024)
 }
 
 template <int NB, typename WT>
-int launch_nb(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_rows, float *logits,
-              unsigned *counter, cudaStream_t s) {
+int launch_nb(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_rows, float *logits, unsigned *counter,
+              cudaStream_t s) {
     constexpr int NBS = (NB + 3) & ~3;
     const size_t smem = (size_t)(d & ~7) * NBS * sizeof(float);
     auto kern = k_exact_logits<NB, WT>;
     FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FRS_CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
     kern<<<ctx->sm_count, 1024, smem, s>>>(h, n, d, W, v_rows, logits, v_rows, counter);
+    ++ctx->launches;
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }
 
 template <typename WT>
-int launch_pass(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_rows, float *logits,
-                unsigned *counter, cudaStream_t s) {
+int launch_pass(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_rows, float *logits, unsigned *counter,
+                cudaStream_t s) {
     switch (n) {
 #define FRS_NB_CASE(N) \
     case N: return launch_nb<N, WT>(ctx, h, n, d, W, v_rows, logits, counter, s);
@@ -338,8 +176,8 @@ int launch_pass(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_r
 
 }  // namespace
 
-int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *W, int w_dtype,
-                        int v_rows, float *logits, cudaStream_t s) {
+int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *W, int w_dtype, int v_rows,
+                        float *logits, cudaStream_t s) {
     // Rows per pass: as many as fit (<= 12) with the hidden rows resident in shared memory.
     const size_t per_row = (size_t)(d & ~7) * sizeof(float);
     int nb_cap = static_cast<int>(std::min<size_t>(12, ctx->smem_optin / std::max<size_t>(per_row, 1)));
@@ -349,6 +187,12 @@ int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *
     if (st) return st;
     unsigned *counters = static_cast<unsigned *>(ctx->counters.ptr);
     int pass = 0;
+    timing_begin(ctx, s);
+    struct EndTiming {
+        frs_ctx *c;
+        cudaStream_t s;
+        ~EndTiming() { timing_end(c, s); }
+    } end_timing{ctx, s};
     for (int r0 = 0; r0 < n; r0 += nb_cap, ++pass) {
         const int nb = std::min(nb_cap, n - r0);
         unsigned *counter = counters + (pass % 64);
@@ -363,21 +207,20 @@ int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *
 }
 
 int launch_softmax_topk(frs_ctx *ctx, const float *logits, int n, int v, int k, float temperature,
-                        const int32_t *ordered_ids, int32_t *out_ridx, int32_t *out_full,
-                        float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags,
-                        cudaStream_t s) {
+                        const int32_t *ordered_ids, int32_t *out_ridx, int32_t *out_full, float *out_prob,
+                        float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
     int st = ctx->scratch.ensure((size_t)n * v * sizeof(float));
     if (st) return st;
-    k_softmax_topk<<<n, 1024, 0, s>>>(logits, v, v, k, temperature, ordered_ids,
-                                      static_cast<float *>(ctx->scratch.ptr), out_ridx, out_full,
-                                      out_prob, out_rowmax, out_total, out_flags);
+    ++ctx->launches;
+    k_softmax_topk<<<n, 1024, 0, s>>>(logits, v, v, k, temperature, ordered_ids, static_cast<float *>(ctx->scratch.ptr),
+                                      out_ridx, out_full, out_prob, out_rowmax, out_total, out_flags);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }
 
-int launch_argmax_rows(frs_ctx *ctx, const float *logits, int m, int v, int32_t id_offset,
-                       int32_t *out_id, float *out_val, uint32_t *out_flags, cudaStream_t s) {
-    (void)ctx;
+int launch_argmax_rows(frs_ctx *ctx, const float *logits, int m, int v, int32_t id_offset, int32_t *out_id,
+                       float *out_val, uint32_t *out_flags, cudaStream_t s) {
+    ++ctx->launches;
     k_argmax_rows<<<m, 1024, 0, s>>>(logits, v, v, id_offset, out_id, out_val, out_flags);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;

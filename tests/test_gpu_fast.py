@@ -1,0 +1,127 @@
+"""GPU parity of the FAST (tcgen05) path: draft ids / FR remaps / argmax bit-exact vs the
+oracle; probabilities within a stated tolerance (PROB_RTOL) because the softmax denominator
+is accumulated from the tensor-core logits; rows that fall back to the exact kernel
+(FLAG_RECOMPUTED) must be bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2502_14856_b200 import api
+from paper_2502_14856_b200._lib import FLAG_NONFINITE, FLAG_RECOMPUTED, FLAG_UNCERTIFIED
+
+pytestmark = pytest.mark.gpu
+PROB_RTOL = 1e-4  # relative tolerance on FAST probabilities (approximate Σexp denominator)
+
+
+def rmsnorm(x):
+    x = x.astype(np.float32)
+    ms = (x.astype(np.float64) ** 2).mean(axis=1, keepdims=True)
+    return (x * (1.0 / np.sqrt(ms + 1e-5)).astype(np.float32)).astype(np.float32)
+
+
+def case(seed, n, d, v_sub, V=None):
+    rng = np.random.default_rng(seed)
+    V = V or v_sub + 1000
+    W = torch.from_numpy((rng.standard_normal((V, d)) * 0.02).astype(np.float32)).to(torch.bfloat16).float().numpy()
+    ids = rng.permutation(V)[:v_sub].astype(np.int32)
+    h = rmsnorm(rng.standard_normal((n, d)))
+    return W, ids, h
+
+
+def check_fast(ctx, restatement, W, ids, h, k, temperature=1.0):
+    head = api.restrict_lm_head(ctx, torch.from_numpy(W).cuda(), api.RankedSubset(W.shape[0], ids), dtype="bf16")
+    out = api.draft_head_topk(ctx, torch.from_numpy(h).cuda(), head, k, temperature, mode="fast")
+    torch.cuda.synchronize()
+    ref = restatement.draft_level(h, restatement.restrict(W, ids), ids, k, temperature)
+    kk = min(k, ids.size)
+    flags = out.flags.cpu().numpy()
+    assert (flags & FLAG_UNCERTIFIED).sum() == 0
+    assert np.array_equal(out.ridx.cpu().numpy()[:, :kk], ref["ridx"][:, :kk])
+    assert np.array_equal(out.full.cpu().numpy()[:, :kk], ref["full"][:, :kk])
+    assert np.array_equal(out.rowmax.cpu().numpy(), ref["mx"])
+    prob = out.prob.cpu().numpy()[:, :kk]
+    np.testing.assert_allclose(prob, ref["prob"][:, :kk], rtol=PROB_RTOL, atol=0)
+    rec = (flags & FLAG_RECOMPUTED) != 0
+    if rec.any():  # fallback rows are the exact path: bit-identical
+        assert np.array_equal(prob[rec], ref["prob"][rec, :kk])
+    return flags
+
+
+@pytest.mark.parametrize("n,d,v_sub,k", [
+    (4, 512, 8192, 4),        # C1 shape
+    (10, 4096, 32768, 10),    # C2 shape
+    (1, 4096, 32768, 10),     # level-0 root row
+    (16, 256, 3000, 16),
+    (7, 1024, 300, 10),       # V_sub smaller than one CTA wave
+    (10, 2048, 20000, 32),    # k > 16: 64 recomputed candidates
+    (20, 512, 8192, 10),      # 17..32 rows
+    (3, 3584, 32768, 10),     # Qwen-2.5-7B hidden size
+])
+def test_fast_draft_ids_exact(cuda_ctx, restatement, n, d, v_sub, k):
+    W, ids, h = case(n * 7 + d + v_sub, n, d, v_sub)
+    check_fast(cuda_ctx, restatement, W, ids, h, k)
+
+
+@pytest.mark.parametrize("temperature", [0.6, 1.8])
+def test_fast_temperature(cuda_ctx, restatement, temperature):
+    W, ids, h = case(21, 5, 1024, 5000)
+    check_fast(cuda_ctx, restatement, W, ids, h, 10, temperature)
+
+
+def test_fast_exact_ties_and_forced_fallback(cuda_ctx, restatement):
+    """Identical slab rows give exactly equal logits (ties by restricted index); a fully flat
+    row cannot be certified and must fall back to the exact full-row path."""
+    W, ids, h = case(22, 3, 512, 4000)
+    W[ids[5]] = W[ids[3000]]           # exact duplicates at both ends of the ranking
+    W[ids[7]] = W[ids[2999]]
+    h[2] = 0.0                          # all logits 0: every prob ties -> flat row
+    flags = check_fast(cuda_ctx, restatement, W, ids, h, 10)
+    assert flags[2] & FLAG_RECOMPUTED
+
+
+def test_fast_nonfinite_flag(cuda_ctx):
+    W, ids, h = case(23, 2, 256, 1000)
+    h[0, 1] = np.nan
+    head = api.restrict_lm_head(cuda_ctx, torch.from_numpy(W).cuda(), api.RankedSubset(W.shape[0], ids), dtype="bf16")
+    out = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, 4, mode="fast")
+    flags = out.flags.cpu().numpy()
+    assert flags[0] & FLAG_NONFINITE and not flags[1] & FLAG_NONFINITE
+
+
+@pytest.mark.parametrize("m,d,V", [(61, 4096, 32000), (8, 4096, 128256), (33, 512, 7000), (5, 3584, 20000)])
+def test_fast_verify_argmax_exact(cuda_ctx, restatement, m, d, V):
+    rng = np.random.default_rng(m + d)
+    W = torch.from_numpy((rng.standard_normal((V, d)) * 0.02).astype(np.float32)).to(torch.bfloat16)
+    Wn = W.float().numpy()
+    h = rmsnorm(rng.standard_normal((m, d)))
+    ids, vals, flags = api.verify_head_argmax(cuda_ctx, torch.from_numpy(h).cuda(), W.cuda(), mode="fast")
+    rid, rval = restatement.verify_argmax(h, Wn)
+    assert np.array_equal(ids.cpu().numpy(), rid)
+    assert np.array_equal(vals.cpu().numpy(), rval)
+
+
+def test_fast_verify_ties_lowest_id(cuda_ctx, restatement):
+    rng = np.random.default_rng(31)
+    V, d = 5000, 256
+    Wf = (rng.standard_normal((V, d)) * 0.02).astype(np.float32)
+    h = rmsnorm(rng.standard_normal((4, d)))
+    best = restatement.verify_argmax(h, torch.from_numpy(Wf).to(torch.bfloat16).float().numpy())[0]
+    Wf[4999] = Wf[best[0]]  # duplicate the winner of row 0 at a higher id
+    Wf[0] = Wf[best[1]]     # and the winner of row 1 at a lower id
+    W = torch.from_numpy(Wf).to(torch.bfloat16)
+    ids, _, _ = api.verify_head_argmax(cuda_ctx, torch.from_numpy(h).cuda(), W.cuda(), id_offset=100, mode="fast")
+    rid, _ = restatement.verify_argmax(h, W.float().numpy())
+    assert np.array_equal(ids.cpu().numpy(), rid + 100)
+
+
+def test_fast_repeated_calls_stable(cuda_ctx, restatement):
+    """Monotonic per-row counters and reused workspaces: many back-to-back calls agree."""
+    W, ids, h = case(41, 10, 1024, 8192)
+    head = api.restrict_lm_head(cuda_ctx, torch.from_numpy(W).cuda(), api.RankedSubset(W.shape[0], ids), dtype="bf16")
+    hd = torch.from_numpy(h).cuda()
+    first = api.draft_head_topk(cuda_ctx, hd, head, 10, mode="fast")
+    f0 = first.full.clone()
+    for _ in range(50):
+        o = api.draft_head_topk(cuda_ctx, hd, head, 10, mode="fast", out=first)
+    torch.cuda.synchronize()
+    assert torch.equal(o.full, f0)
