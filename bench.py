@@ -220,6 +220,15 @@ def main():
     clocks = sampler.summary()
     elapsed_ms = e0.elapsed_time(e1)
     launches = ctx.launch_count - launches0
+    # certification outcome over the whole input pool (untimed): FAST rows that fell back
+    flag_counts = {"rows": 0, "recomputed": 0, "uncertified": 0, "seq_sum": 0}
+    for hp in pool:
+        o = api.draft_head_topk(ctx, hp, head, k, mode=mode)
+        f = o.flags.cpu().numpy()
+        flag_counts["rows"] += int(f.size)
+        flag_counts["recomputed"] += int(((f & api._lib.FLAG_RECOMPUTED) != 0).sum())
+        flag_counts["uncertified"] += int(((f & api._lib.FLAG_UNCERTIFIED) != 0).sum())
+        flag_counts["seq_sum"] += int(((f & api._lib.FLAG_SEQ_SUM) != 0).sum())
     kern_ms, kern_n = ctx.timing_read()
     ctx.set_timing(False)
     if world > 1:
@@ -289,7 +298,7 @@ def main():
             "e2e": {"value": world * e2e_steps / e2e_s, "unit": "draft-steps/s",
                     "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": 3 * n * k * 4,
                     "api": "frs_head_draft_host (C ABI, pinned host buffers, synchronous)"},
-            "clocks": clocks, "gpu_launches": launches, "slab_build_ms": slab_build_ms,
+            "clocks": clocks, "gpu_launches": launches, "slab_build_ms": slab_build_ms, "row_flags": flag_counts,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

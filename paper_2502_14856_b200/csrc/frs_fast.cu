@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "frs_common.cuh"
@@ -44,9 +45,8 @@ namespace {
 
 constexpr int BM = 128;      // slab rows per tile (UMMA M)
 constexpr int BK = 64;       // k elements per stage: 128-byte bf16 rows, SWIZZLE_128B
-constexpr int R = 4;         // per-CTA candidates per hidden row
+constexpr int R = 8;         // per-CTA candidates per hidden row
 constexpr int RL = R + 1;    // tracked per warp / CTA: the (R+1)-th bounds the CTA's other rows
-constexpr int kMainThreads = 256;
 constexpr int kFinThreads = 256;
 constexpr int kCandPerFinCta = 8;  // exact recomputes per finalize CTA (8 lanes each)
 
@@ -156,25 +156,22 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 }
 
 // Warp-wide merge of 32 new keys (one per lane) into a sorted top-RL list held in smem.
-__device__ __forceinline__ void warp_list_merge(unsigned long long *list, unsigned long long key, int lane) {
-    const unsigned long long theta = list[RL - 1];
-    if (!__any_sync(0xffffffffu, key > theta)) return;
-    unsigned long long old = lane < RL ? list[lane] : 0ull;
-    bool used_new = false, used_old = lane >= RL;
-    unsigned long long mine = 0ull;
+// Bitonic sort (descending) of one 64-bit key per lane across the warp, for NR independent
+// rows at once so the shuffle chains of different rows interleave (ILP instead of latency).
+template <int NR>
+__device__ __forceinline__ void warp_sort_desc(unsigned long long (&v)[NR], int lane) {
 #pragma unroll
-    for (int r = 0; r < RL; ++r) {
-        const unsigned long long c1 = used_new ? 0ull : key, c2 = used_old ? 0ull : old;
-        const unsigned long long best = warp_max_u64(c1 > c2 ? c1 : c2);
-        if (best != 0ull) {
-            if (!used_new && key == best) used_new = true;
-            else if (!used_old && old == best) used_old = true;
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const bool keep_max = ((lane & j) == 0) == ((lane & k) == 0);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                const unsigned long long p = __shfl_xor_sync(0xffffffffu, v[r], j);
+                v[r] = keep_max ? (v[r] > p ? v[r] : p) : (v[r] < p ? v[r] : p);
+            }
         }
-        if (lane == r) mine = best;
     }
-    __syncwarp();
-    if (lane < RL) list[lane] = mine;
-    __syncwarp();
 }
 
 // ------------------------------------------------------------------ kernels
@@ -185,7 +182,18 @@ struct Partials {
     unsigned long long *pkey;  // [NP][G][R] the CTA's best R (approx value, index) keys, descending
     float *pw2;                // [G] max squared L2 norm of the CTA's slab rows
     int G;
+    unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define FRS_TRACE(P, slot)                                                       \
+    do {                                                                         \
+        if ((P).trace) (P).trace[(size_t)blockIdx.x * 16 + (slot)] = gtimer();   \
+    } while (0)
 
 // hs rows [0,NP) = bf16(h), rows [NP,2NP) = bf16(h - bf16(h)); padded rows are zero.
 __global__ void __launch_bounds__(256) k_hsplit(const float *__restrict__ h, int n, int d, int NP,
@@ -204,34 +212,61 @@ __global__ void __launch_bounds__(256) k_hsplit(const float *__restrict__ h, int
 
 template <int NP, bool SOFTMAX>
 struct MainCfg {
-    static constexpr int N = 2 * NP;
+    static constexpr int N = 2 * NP;                       // MMA N: hi rows then lo rows
+    static constexpr int EPI_WARPS = NP <= 32 ? 4 : 8;     // 4 TMEM lane quarters x column halves
+    static constexpr int RPW = NP / (EPI_WARPS / 4);       // hidden rows per epilogue warp
+    static constexpr int TOPK = SOFTMAX ? 2 : 1;           // per-thread kept candidates per hidden row
+    static constexpr int THREADS = (4 + EPI_WARPS) * 32;
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = N * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 12 ? 12 : (196 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 12 ? 12 : (200 * 1024) / STAGE_BYTES;
     static constexpr int TMEM_COLS = (2 * N) < 32 ? 32 : 2 * N;
-    static constexpr int LIST_BYTES = 4 * NP * RL * 8;
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + LIST_BYTES + 4 * NP * 8 + 256;
+    // end-of-kernel candidate scratch, reusing the (then idle) stage ring
+    static constexpr int CAND_KEYS = NP * 128 * TOPK;
+    static constexpr int CAND_BYTES = CAND_KEYS * 8 + NP * 128 * 4;
+    static_assert(CAND_BYTES <= STAGES * STAGE_BYTES, "candidate scratch must fit the stage ring");
+    static_assert(!SOFTMAX || NP == 16, "the fused softmax path handles up to 16 hidden rows per call");
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 4 * NP * 8 + 256;
 };
 
+#define FRS_TMEM_LD16(taddr, r)                                                                                 \
+    asm volatile(                                                                                               \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) \
+        : "r"(taddr))
+
+// Warp max of a (value, index) key with 2 REDUX instead of 10 shuffles: max over the ordered
+// value bits, then max over ~index among the lanes holding that value.
+__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k) {
+    const unsigned hi = static_cast<unsigned>(k >> 32);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? static_cast<unsigned>(k) : 0u);
+    return (static_cast<unsigned long long>(mh) << 32) | ml;
+}
+
 template <int NP, bool SOFTMAX>
-__global__ void __launch_bounds__(kMainThreads, 1)
+__global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     k_fast_main(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapH, int n,
                 int v_rows, int d, float inv_t, Partials P) {
     using C = MainCfg<NP, SOFTMAX>;
-    constexpr int N = C::N, STAGES = C::STAGES;
+    constexpr int N = C::N, STAGES = C::STAGES, RPW = C::RPW, TOPK = C::TOPK, EPI = C::EPI_WARPS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;                                   // STAGES x 16 KB
     uint8_t *sB = smem + STAGES * C::A_BYTES;             // STAGES x B_BYTES
-    unsigned long long *lists = reinterpret_cast<unsigned long long *>(smem + STAGES * C::STAGE_BYTES);
-    float2 *red = reinterpret_cast<float2 *>(lists + 4 * NP * RL);  // [4][NP] (m, s)
+    unsigned long long *cand = reinterpret_cast<unsigned long long *>(smem);  // end-of-kernel reuse
+    float *cbound = reinterpret_cast<float *>(cand + C::CAND_KEYS);
+    float2 *red = reinterpret_cast<float2 *>(smem + STAGES * C::STAGE_BYTES);  // [4][NP] (m, s)
     uint64_t *bars = reinterpret_cast<uint64_t *>(red + 4 * NP);
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
     float *wred = reinterpret_cast<float *>(tmem_slot + 1);  // [2] norm-warp maxima
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index broadcast from lane 0: provably warp-uniform, so the role branches below
+    // keep their shuffles convergent (no WARPSYNC.COLLECTIVE emulation)
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int G = gridDim.x, cta = blockIdx.x;
     const int T = (v_rows + BM - 1) / BM, KB = (d + BK - 1) / BK;
     const int t_begin = static_cast<int>((static_cast<long long>(cta) * T) / G);
@@ -244,12 +279,11 @@ __global__ void __launch_bounds__(kMainThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], 4 * (EPI / 4));  // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    for (int i = threadIdx.x; i < 4 * NP * RL; i += blockDim.x) lists[i] = 0ull;
     if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&mapW);
@@ -259,6 +293,7 @@ __global__ void __launch_bounds__(kMainThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) FRS_TRACE(P, 0);
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -272,7 +307,9 @@ __global__ void __launch_bounds__(kMainThreads, 1)
                     mbar_expect_tx(&full[stage], C::STAGE_BYTES);
                     tma_load_2d(sA + stage * C::A_BYTES, &mapW, &full[stage], kb * BK, t * BM, pol_w);
                     if (!waited) {  // hs is produced by k_hsplit (programmatic dependency)
+                        FRS_TRACE(P, 1);
                         griddep_wait();
+                        FRS_TRACE(P, 9);
                         waited = true;
                     }
                     tma_load_2d(sB + stage * C::B_BYTES, &mapH, &full[stage], kb * BK, 0, pol_h);
@@ -282,6 +319,7 @@ __global__ void __launch_bounds__(kMainThreads, 1)
                     }
                 }
             }
+            FRS_TRACE(P, 2);
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
@@ -295,6 +333,7 @@ __global__ void __launch_bounds__(kMainThreads, 1)
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * N);
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&full[stage], phase);
+                    if (lt == 0 && kb == 0) FRS_TRACE(P, 3);
                     tc_fence_after();
                     const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
                     const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
@@ -309,6 +348,7 @@ __global__ void __launch_bounds__(kMainThreads, 1)
                 }
                 umma_commit(&tfull[acc]);
             }
+            FRS_TRACE(P, 4);
         }
     } else if (warp < 4) {  // ---------------- row-norm warps: max_j |W_j|^2 for the error bound
         const int r0 = threadIdx.x - 64;  // 0..63: rows r0 and r0 + 64 of every tile
@@ -321,8 +361,9 @@ __global__ void __launch_bounds__(kMainThreads, 1)
                 const uint4 *a0 = reinterpret_cast<const uint4 *>(sA + stage * C::A_BYTES + r0 * 128);
                 const uint4 *a1 = reinterpret_cast<const uint4 *>(sA + stage * C::A_BYTES + (r0 + 64) * 128);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {  // order within a row is irrelevant for a sum of squares
-                    const uint4 u = a0[c], w = a1[c];
+                for (int c = 0; c < 8; ++c) {   // order within a row is irrelevant for a sum of squares;
+                    const int pc = c ^ (r0 & 7);  // rotate chunks by row so 8 lanes cover all 32 banks
+                    const uint4 u = a0[pc], w = a1[pc];
                     const uint32_t uu[4] = {u.x, u.y, u.z, u.w}, ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -345,97 +386,165 @@ __global__ void __launch_bounds__(kMainThreads, 1)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         if (lane == 0) wred[warp - 2] = wmax;
-    } else {  // ---------------- epilogue warps 4..7
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        unsigned long long *my_lists = lists + q * NP * RL;
-        constexpr int NS = SOFTMAX ? NP : 1;
+        if (threadIdx.x == 64) FRS_TRACE(P, 8);
+        asm volatile("bar.sync 2, %0;" ::"r"((2 + EPI) * 32) : "memory");  // stage ring now idle
+    } else {  // ---------------- epilogue warps: TMEM -> (softmax stats, per-thread candidates)
+        const int we = warp - 4;         // 0 .. EPI-1
+        const int q = warp & 3;          // TMEM lane quarter this warp may access
+        const int cbase = (we / 4) * RPW;  // first hidden row handled by this warp
+        constexpr int NS = SOFTMAX ? RPW : 1;
+        const float kNegInf = __int_as_float(0xff800000u);
         float m[NS], s[NS];
+        unsigned long long b1[RPW], b2[TOPK == 2 ? RPW : 1];
+        float bnd[RPW];
 #pragma unroll
-        for (int i = 0; i < NS; ++i) {
-            m[i] = -__int_as_float(0x7f800000);
-            s[i] = 0.0f;
+        for (int r = 0; r < RPW; ++r) {
+            if constexpr (SOFTMAX) {
+                m[r] = kNegInf;
+                s[r] = 0.0f;
+            }
+            b1[r] = 0ull;
+            if constexpr (TOPK == 2) b2[r] = 0ull;
+            bnd[r] = kNegInf;
         }
         for (int t = t_begin, lt = 0; t < t_end; ++t, ++lt) {
             const int acc = lt & 1;
+            if (threadIdx.x == 128 && lt == 0) FRS_TRACE(P, 10);
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
+            if (threadIdx.x == 128 && lt == 0) FRS_TRACE(P, 11);
             tc_fence_after();
             const int row = t * BM + q * 32 + lane;
             const bool valid = row < v_rows;
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * N);
-            constexpr int GROUPS = NP / 16 > 1 ? NP / 32 : 1;  // 32-row hidden groups (NP=16 -> one group of 16)
-#pragma unroll 1
-            for (int g = 0; g < GROUPS; ++g) {
-                uint32_t hi[32], lo[32];
+#pragma unroll
+            for (int cg = 0; cg < RPW / 16; ++cg) {
+                const int c0 = cbase + cg * 16;
+                uint32_t hi[16], lo[16];
                 if constexpr (NP == 16) {
-                    FRS_TMEM_LD32(tbase, hi);  // cols 0..15 hi, 16..31 lo
+                    uint32_t both[32];
+                    FRS_TMEM_LD32(tbase, both);  // cols 0..15 hi, 16..31 lo
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) {
+                        hi[r] = both[r];
+                        lo[r] = both[16 + r];
+                    }
                 } else {
-                    FRS_TMEM_LD32(tbase + g * 32, hi);
-                    FRS_TMEM_LD32(tbase + NP + g * 32, lo);
+                    FRS_TMEM_LD16(tbase + c0, hi);
+                    FRS_TMEM_LD16(tbase + NP + c0, lo);
+                    tmem_wait_ld();
                 }
-                tmem_wait_ld();
-                if (g == GROUPS - 1) {  // accumulator drained: hand it back to the MMA warp
+                if (cg == RPW / 16 - 1) {  // accumulator drained: hand it back to the MMA warp
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
-                constexpr int PER = NP == 16 ? 16 : 32;
 #pragma unroll
-                for (int ii = 0; ii < PER; ++ii) {
-                    const int i = g * 32 + ii;
-                    if (i >= n) break;
-                    const float a = NP == 16 ? __uint_as_float(hi[ii]) + __uint_as_float(hi[16 + ii])
-                                             : __uint_as_float(hi[ii]) + __uint_as_float(lo[ii]);
-                    if constexpr (SOFTMAX) {
-                        if (valid) {
-                            const float x = a * inv_t;
-                            const float mn = fmaxf(m[i], x);
-                            s[i] = s[i] * exp2f((m[i] - mn) * 1.4426950408889634f) + exp2f((x - mn) * 1.4426950408889634f);
-                            m[i] = mn;
+                for (int r = 0; r < 16; ++r) {
+                    const int rr = cg * 16 + r, i = c0 + r;
+                    if (!valid || i >= n) continue;
+                    const float a = __uint_as_float(hi[r]) + __uint_as_float(lo[r]);
+                    if constexpr (SOFTMAX) {  // online sum exp(x - m), one MUFU per value
+                        const float x = a * inv_t;
+                        if (x <= m[rr]) {
+                            s[rr] += exp2f((x - m[rr]) * 1.4426950408889634f);
+                        } else {
+                            s[rr] = s[rr] * exp2f((m[rr] - x) * 1.4426950408889634f) + 1.0f;
+                            m[rr] = x;
                         }
                     }
-                    warp_list_merge(my_lists + i * RL, valid ? dev::value_key(a, row) : 0ull, lane);
+                    // per-thread top-TOPK keys; everything dropped is bounded by bnd
+                    const unsigned long long k = dev::value_key(a, row);
+                    if constexpr (TOPK == 2) {
+                        if (k > b1[rr]) {
+                            if (b2[rr]) bnd[rr] = fmaxf(bnd[rr], dev::key_value(b2[rr]));
+                            b2[rr] = b1[rr];
+                            b1[rr] = k;
+                        } else if (k > b2[rr]) {
+                            if (b2[rr]) bnd[rr] = fmaxf(bnd[rr], dev::key_value(b2[rr]));
+                            b2[rr] = k;
+                        } else {
+                            bnd[rr] = fmaxf(bnd[rr], a);
+                        }
+                    } else {
+                        if (k > b1[rr]) {
+                            if (b1[rr]) bnd[rr] = fmaxf(bnd[rr], dev::key_value(b1[rr]));
+                            b1[rr] = k;
+                        } else {
+                            bnd[rr] = fmaxf(bnd[rr], a);
+                        }
+                    }
                 }
             }
         }
-        // ---- CTA reduction of the softmax statistics and the candidate lists
+        if (threadIdx.x == 128) FRS_TRACE(P, 13);
+        // ---- publish per-thread state, then the CTA top-R per hidden row
         if constexpr (SOFTMAX) {
 #pragma unroll
-            for (int i = 0; i < NP; ++i) {
-                if (i >= n) break;
-                float mi = m[i], si = s[i];
+            for (int r = 0; r < RPW; ++r) {
+                const int i = cbase + r;
+                if (i >= n) continue;  // uniform
+                float mi = m[r], si = s[r];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     const float mo = __shfl_xor_sync(0xffffffffu, mi, o), so = __shfl_xor_sync(0xffffffffu, si, o);
                     const float mn = fmaxf(mi, mo);
-                    si = (mn == -__int_as_float(0x7f800000))
-                             ? 0.0f
-                             : si * exp2f((mi - mn) * 1.4426950408889634f) + so * exp2f((mo - mn) * 1.4426950408889634f);
+                    si = (mn == kNegInf) ? 0.0f
+                                         : si * exp2f((mi - mn) * 1.4426950408889634f) +
+                                               so * exp2f((mo - mn) * 1.4426950408889634f);
                     mi = mn;
                 }
                 if (lane == 0) red[q * NP + i] = make_float2(mi, si);
             }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
-        for (int i = q; i < n; i += 4) {
-            // merge the 4 warps' top-RL lists of hidden row i
-            unsigned long long key = lane < 4 * RL ? lists[(lane / RL) * NP * RL + i * RL + (lane % RL)] : 0ull;
-            bool used = false;
-            unsigned long long out = 0ull;
+        asm volatile("bar.sync 2, %0;" ::"r"((2 + EPI) * 32) : "memory");  // norm warps done with the ring
+        const int slot = q * 32 + lane;  // 0..127: the thread's slab-row position within a tile
 #pragma unroll
-            for (int r = 0; r < RL; ++r) {
-                const unsigned long long best = warp_max_u64(used ? 0ull : key);
-                if (!used && best != 0ull && key == best) used = true;
-                if (lane == r) out = best;
+        for (int r = 0; r < RPW; ++r) {
+            const int i = cbase + r;
+            cand[(size_t)i * 128 * TOPK + slot * TOPK] = b1[r];
+            if constexpr (TOPK == 2) cand[(size_t)i * 128 * TOPK + slot * TOPK + 1] = b2[r];
+            cbound[i * 128 + slot] = bnd[r];
+        }
+        if (threadIdx.x == 128) FRS_TRACE(P, 5);
+        asm volatile("bar.sync 1, %0;" ::"r"(EPI * 32) : "memory");  // the epilogue warps only
+        for (int i = we; i < n; i += EPI) {
+            constexpr int PL = 4 * TOPK;  // keys per lane
+            unsigned long long kk[PL];
+            float bmax = kNegInf;
+#pragma unroll
+            for (int j = 0; j < PL; ++j) kk[j] = cand[(size_t)i * 128 * TOPK + lane + 32 * j];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bmax = fmaxf(bmax, cbound[i * 128 + lane + 32 * j]);
+            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 16));
+            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 8));
+            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 4));
+            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 2));
+            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 1));
+            unsigned long long prev = ~0ull, out = 0ull;
+#pragma unroll
+            for (int rnd = 0; rnd < RL; ++rnd) {  // CTA top-RL by rounds of warp max
+                unsigned long long mine = 0ull;
+#pragma unroll
+                for (int j = 0; j < PL; ++j)
+                    if (kk[j] < prev && kk[j] > mine) mine = kk[j];
+                const unsigned long long best = warp_max_key(mine);
+                if (lane == rnd) out = best;
+                prev = best ? best : prev;
+                if (!best) break;  // uniform
             }
             if (lane < R) P.pkey[((size_t)i * G + cta) * R + lane] = out;
-            if (lane == R) P.pth[(size_t)i * G + cta] = out ? dev::key_value(out) : -__int_as_float(0x7f800000);
+            if (lane == R) {
+                const float th = out ? dev::key_value(out) : kNegInf;
+                P.pth[(size_t)i * G + cta] = fmaxf(th, bmax);
+            }
             if constexpr (SOFTMAX) {
                 if (lane == 0) {
-                    float mi = -__int_as_float(0x7f800000), si = 0.0f;
+                    float mi = kNegInf, si = 0.0f;
                     for (int w = 0; w < 4; ++w) {
                         const float2 v = red[w * NP + i];
                         const float mn = fmaxf(mi, v.x);
-                        if (mn != -__int_as_float(0x7f800000))
+                        if (mn != kNegInf)
                             si = si * exp2f((mi - mn) * 1.4426950408889634f) + v.y * exp2f((v.x - mn) * 1.4426950408889634f);
                         mi = mn;
                     }
@@ -446,7 +555,10 @@ __global__ void __launch_bounds__(kMainThreads, 1)
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) P.pw2[cta] = fmaxf(wred[0], wred[1]);
+    if (threadIdx.x == 0) {
+        P.pw2[cta] = fmaxf(wred[0], wred[1]);
+        FRS_TRACE(P, 7);
+    }
     __threadfence();
     griddep_launch();
     __syncthreads();
@@ -466,22 +578,25 @@ __device__ __forceinline__ float fast_gamma(int d) {
     return static_cast<float>(g * 1.01);
 }
 
-// Finalize (draft): grid (n, CSB). See the file comment.
+constexpr int kFinKPT = 8;    // union keys held per finalize thread: G * R <= 256 * 8
+constexpr int kCsMax = 64;    // max exactly-recomputed candidates per row (kFinCtas x 8)
+constexpr int kFinCtas = kCsMax / kCandPerFinCta;
+
 struct FinArgs {
     const float *h;
-    int n, d, v_rows, k, CS, CSB;
+    int n, d, v_rows, k;
     float temperature;
     const unsigned short *slab;
     const int32_t *ordered;
     Partials P;
-    float *fin;                      // [n][CS] exact logits of the candidates
+    float *fin;                      // [n][kCsMax] exact logits of the selected candidates
     unsigned long long *row_ctr;     // [64] monotonic per-row arrival counters
-    float *scratch;                  // [n][v_rows] fallback buffer
+    float *scratch;                  // [n][2 v_rows] fallback buffer
     int32_t *out_ridx, *out_full;
     float *out_prob, *out_rowmax;
     double *out_total;
     uint32_t *out_flags;
-    int argmax;                      // verify mode: argmax only, outputs (out_full = id, out_prob = value)
+    int argmax;                      // verify mode: out_full = id_offset + argmax id, out_prob = its logit
     int32_t id_offset;
 };
 
@@ -496,39 +611,71 @@ __device__ void fallback_exact_logits(const float *sh, const unsigned short *sla
     }
 }
 
-struct SumI {
-    __device__ int operator()(int a, int b) const { return a + b; }
-};
-
-template <int SORTN>
+// Finalize: grid (n, kFinCtas). Every CTA of row i merges the CTA partials (identically),
+// selects S = {union keys with approx >= approx_(k) - 2 eps - margin} (typically ~k..2k
+// entries), recomputes its slice of S exactly, and the last CTA to arrive selects the top-k
+// by (prob desc, index asc) and certifies it (see the file comment).
 __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     extern __shared__ uint8_t fsm_raw[];
-    float *sh = reinterpret_cast<float *>(fsm_raw);                                         // [d]
-    unsigned long long *keys = reinterpret_cast<unsigned long long *>(sh + ((A.d + 3) & ~3));  // [SORTN]
-    unsigned short *wrows = reinterpret_cast<unsigned short *>(keys + SORTN);               // [8][d]
+    float *sh = reinterpret_cast<float *>(fsm_raw);                                   // [d]
+    unsigned short *wrows = reinterpret_cast<unsigned short *>(sh + ((A.d + 7) & ~7));  // [8][d]
     __shared__ dev::ReduceScratch rs;
-    __shared__ int s_last;
+    __shared__ int s_nsel, s_last, s_cert;
     __shared__ float s_mx;
-    __shared__ float s_ex[64];
-    __shared__ unsigned long long s_ek[64];
+    __shared__ unsigned long long s_sel[kCsMax];
+    __shared__ unsigned long long s_ek[kCsMax];
 
     const int i = blockIdx.x, b = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
-    const int G = A.P.G;
+    const int warp_u = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);  // warp-uniform
+    const int G = A.P.G, E = G * R;
     // ---- prologue (independent of the main kernel): the hidden row and its norm
     double hn2 = 0.0;
     int bad = 0;
-    for (int c = tid; c < A.d; c += nt) {
-        const float x = A.h[(size_t)i * A.d + c];
-        sh[c] = x;
-        if (!isfinite(x)) bad = 1;
-        hn2 += static_cast<double>(x) * x;
+    {  // batch the global loads (all in flight) before the shared stores
+        const float4 *hv = reinterpret_cast<const float4 *>(A.h + (size_t)i * A.d);
+        const int d4 = A.d / 4;  // d % 8 == 0 on the FAST path
+        constexpr int MAXV = 8;  // up to 8 float4 per thread: d <= 8192
+        float4 v[MAXV];
+#pragma unroll
+        for (int u = 0; u < MAXV; ++u) {
+            const int e = tid + u * kFinThreads;
+            v[u] = e < d4 ? __ldg(hv + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int e = tid + MAXV * kFinThreads; e < d4; e += kFinThreads) {  // d > 8192
+            const float4 w = __ldg(hv + e);
+            reinterpret_cast<float4 *>(sh)[e] = w;
+            const float xs[4] = {w.x, w.y, w.z, w.w};
+            for (int q = 0; q < 4; ++q) {
+                if (!isfinite(xs[q])) bad = 1;
+                hn2 += static_cast<double>(xs[q]) * xs[q];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < MAXV; ++u) {
+            const int e = tid + u * kFinThreads;
+            if (e < d4) {
+                reinterpret_cast<float4 *>(sh)[e] = v[u];
+                const float xs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (!isfinite(xs[q])) bad = 1;
+                    hn2 += static_cast<double>(xs[q]) * xs[q];
+                }
+            }
+        }
     }
+    if (tid == 0) s_nsel = 0;
     hn2 = dev::block_reduce(hn2, dev::SumD(), rs.d);
     bad = dev::block_reduce(bad, dev::OrI(), rs.i);
     griddep_wait();
 
     // ---- merge the CTA partials (identically in every CTA of this row)
-    for (int e = tid; e < SORTN; e += nt) keys[e] = e < G * R ? A.P.pkey[(size_t)i * G * R + e] : 0ull;
+    unsigned long long kr[kFinKPT];
+#pragma unroll
+    for (int j = 0; j < kFinKPT; ++j) {
+        const int e = tid + j * nt;
+        kr[j] = e < E ? A.P.pkey[(size_t)i * E + e] : 0ull;
+    }
     float th = -__int_as_float(0x7f800000), w2 = 0.0f, mmax = -__int_as_float(0x7f800000);
     for (int c = tid; c < G; c += nt) {
         th = fmaxf(th, A.P.pth[(size_t)i * G + c]);
@@ -542,193 +689,205 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         mmax = dev::block_reduce(mmax, dev::MaxF(), rs.f);
         for (int c = tid; c < G; c += nt) {
             const float pm = A.P.pm[(size_t)i * G + c];
-            if (pm != -__int_as_float(0x7f800000)) tot += static_cast<double>(A.P.ps[(size_t)i * G + c]) * exp(static_cast<double>(pm) - mmax);
+            if (pm != -__int_as_float(0x7f800000))
+                tot += static_cast<double>(A.P.ps[(size_t)i * G + c]) * exp(static_cast<double>(pm) - mmax);
         }
         tot = dev::block_reduce(tot, dev::SumD(), rs.d);
     }
-    // bitonic sort, descending
-    for (int kk = 2; kk <= SORTN; kk <<= 1) {
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-            __syncthreads();
-            for (int e = tid; e < SORTN; e += nt) {
-                const int p = e ^ j;
-                if (p > e) {
-                    const unsigned long long x = keys[e], y = keys[p];
-                    const bool desc_blk = (e & kk) == 0;
-                    if (desc_blk ? (x < y) : (x > y)) {
-                        keys[e] = y;
-                        keys[p] = x;
-                    }
-                }
-            }
+    const float eps = static_cast<float>(sqrt(hn2) * sqrt(static_cast<double>(w2) * 1.001)) * fast_gamma(A.d) * 1.01f;
+
+    // approx_(kk): the kk-th largest union key, by kk rounds of block max
+    const int kk = min(A.k, A.v_rows);
+    unsigned long long prev = ~0ull, kth = 0ull;
+    for (int r = 0; r < kk; ++r) {
+        unsigned long long mine = 0ull;
+#pragma unroll
+        for (int j = 0; j < kFinKPT; ++j)
+            if (kr[j] < prev && kr[j] > mine) mine = kr[j];
+        const unsigned long long best = dev::block_reduce(mine, dev::MaxU64(), rs.k);
+        if (best == 0ull) break;
+        prev = kth = best;
+    }
+    const float vk = kth ? dev::key_value(kth) : -__int_as_float(0x7f800000);
+    const float t_s = vk - 2.0f * eps - (fabsf(vk) * 0x1p-18f + 0x1p-20f);
+    // S = union keys at or above t_s; a_below = best union value left out
+    float a_below = -__int_as_float(0x7f800000);
+#pragma unroll
+    for (int j = 0; j < kFinKPT; ++j) {
+        if (kr[j] == 0ull) continue;
+        const float v = dev::key_value(kr[j]);
+        if (v >= t_s) {
+            const int pos = atomicAdd(&s_nsel, 1);
+            if (pos < kCsMax) s_sel[pos] = kr[j];
+        } else {
+            a_below = fmaxf(a_below, v);
         }
     }
+    a_below = dev::block_reduce(a_below, dev::MaxF(), rs.f);
+    const int nsel = s_nsel;  // block_reduce synchronized
+    const int ns = min(nsel, kCsMax);
+    // canonical (descending) order, so every CTA of the row indexes S identically
+    unsigned long long my_sel = tid < ns ? s_sel[tid] : 0ull;
+    int my_rank = 0;
+    for (int c = 0; c < ns; ++c) my_rank += s_sel[c] > my_sel;
     __syncthreads();
-    int n_keys = 0;  // candidates actually present
-    for (int e = tid; e < SORTN; e += nt) n_keys += keys[e] != 0ull;
-    n_keys = dev::block_reduce(n_keys, SumI(), rs.i);
-    const int cs = min(A.CS, n_keys);
+    if (tid < ns) s_sel[my_rank] = my_sel;
+    __syncthreads();
 
-    // ---- exact recompute of candidates [8b, 8b + 8)
-    const int c0 = b * kCandPerFinCta, c1 = min(cs, c0 + kCandPerFinCta);
-    for (int c = c0; c < c1; ++c) {
-        const int j = dev::key_index(keys[c]);
-        const uint4 *src = reinterpret_cast<const uint4 *>(A.slab + (size_t)j * A.d);
-        uint4 *dst = reinterpret_cast<uint4 *>(wrows + (size_t)(c - c0) * A.d);
-        for (int e = tid; e < A.d / 8; e += nt) dst[e] = src[e];
-    }
-    __syncthreads();
-    if (tid < kCandPerFinCta * 8) {
-        const int c = c0 + tid / 8;
-        const int cc = c < c1 ? c : c0;
-        const float v = dev::dot_f32_lanes8(sh, wrows + (size_t)(cc - c0) * A.d, A.d);
-        if ((tid & 7) == 0 && c < c1) A.fin[(size_t)i * A.CS + c] = v;
+    // ---- exact recompute of my slice S[8b, 8b + 8)
+    const int c0 = b * kCandPerFinCta, c1 = min(ns, c0 + kCandPerFinCta);
+    if (c0 < c1) {
+        {  // all candidate-row loads in flight at once: 8 rows x d/8 uint4 over the CTA
+            const int per_row = A.d / 8, total = (c1 - c0) * per_row;
+            constexpr int MAXV = 16;  // 8 rows x 512 uint4 / 256 threads for d = 4096
+            uint4 v[MAXV];
+#pragma unroll
+            for (int u = 0; u < MAXV; ++u) {
+                const int e = tid + u * kFinThreads;
+                if (e < total) {
+                    const int c = c0 + e / per_row, off = e % per_row;
+                    v[u] = __ldg(reinterpret_cast<const uint4 *>(A.slab + (size_t)dev::key_index(s_sel[c]) * A.d) + off);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < MAXV; ++u) {
+                const int e = tid + u * kFinThreads;
+                if (e < total) reinterpret_cast<uint4 *>(wrows)[e] = v[u];
+            }
+            for (int e = tid + MAXV * kFinThreads; e < total; e += kFinThreads) {  // d > 4096
+                const int c = c0 + e / per_row, off = e % per_row;
+                reinterpret_cast<uint4 *>(wrows)[e] =
+                    __ldg(reinterpret_cast<const uint4 *>(A.slab + (size_t)dev::key_index(s_sel[c]) * A.d) + off);
+            }
+        }
+        __syncthreads();
+        if (warp_u < kCandPerFinCta * 8 / 32) {
+            const int c = c0 + tid / 8;
+            const int cc = c < c1 ? c : c0;
+            const float v = dev::dot_f32_lanes8(sh, wrows + (size_t)(cc - c0) * A.d, A.d);
+            if ((tid & 7) == 0 && c < c1) A.fin[(size_t)i * kCsMax + c] = v;
+        }
     }
     __threadfence();
     __syncthreads();
     if (tid == 0) {
         const unsigned long long old = atomicAdd(&A.row_ctr[i], 1ull);
-        s_last = (old % A.CSB) == static_cast<unsigned long long>(A.CSB - 1);
+        s_last = (old % kFinCtas) == static_cast<unsigned long long>(kFinCtas - 1);
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
 
-    // ---- selection + certification (last CTA of this row)
-    const float gamma = fast_gamma(A.d);
-    const float eps = static_cast<float>(sqrt(hn2) * sqrt(static_cast<double>(w2) * 1.001)) * gamma * 1.01f;
-    // largest approximate value NOT recomputed: the CTA bounds and the first skipped union entry
-    float a_bound = th;
-    if (cs < n_keys) a_bound = fmaxf(a_bound, dev::key_value(keys[cs]));
-    const bool all_rows = cs >= A.v_rows;  // every slab row was recomputed exactly
+    // ---- selection + certification (the last CTA of this row)
+    const float a_bound = fmaxf(th, a_below);  // every row not recomputed has approx <= a_bound
     uint32_t flags = bad ? FRS_FLAG_NONFINITE : 0u;
-    bool ok = !bad;
-
-    if (A.argmax) {
-        if (tid < 32) {
-            unsigned long long best = 0ull;
-            for (int c = tid; c < cs; c += 32) {
-                const unsigned long long kk2 = dev::value_key(A.fin[(size_t)i * A.CS + c], dev::key_index(keys[c]));
-                best = kk2 > best ? kk2 : best;
-            }
-            best = warp_max_u64(best);
-            if (tid == 0) {
-                const float lb = dev::key_value(best);
-                const bool cert = all_rows || (a_bound + eps < lb);
-                s_ek[0] = best;
-                s_last = cert && ok;
-            }
-        }
-        __syncthreads();
-        unsigned long long best = s_ek[0];
-        if (!s_last && !bad) {  // fallback: exact full-row argmax
-            flags |= FRS_FLAG_RECOMPUTED;
-            float *L = A.scratch + (size_t)i * A.v_rows;
-            fallback_exact_logits(sh, A.slab, A.v_rows, A.d, L);
-            __syncthreads();
-            unsigned long long cand = 0ull;
-            for (int j = tid; j < A.v_rows; j += nt) {
-                const unsigned long long kk2 = dev::value_key(L[j], j);
-                cand = kk2 > cand ? kk2 : cand;
-            }
-            best = dev::block_reduce(cand, dev::MaxU64(), rs.k);
-        }
-        if (tid == 0) {
-            A.out_full[i] = A.id_offset + dev::key_index(best);
-            if (A.out_prob) A.out_prob[i] = dev::key_value(best);
-            if (A.out_flags) A.out_flags[i] = flags;
-        }
-        return;
-    }
-
-    // draft: exact softmax numerators of the candidates, (e desc, idx asc) order
     dev::load_exp_table(rs.tab);
     __syncthreads();
-    if (tid < 32) {
+    if (warp_u == 0) {
+        const bool overflow = nsel > kCsMax;
         float mx = -__int_as_float(0x7f800000);
-        for (int c = tid; c < cs; c += 32) {
-            const float x = __fdiv_rn(A.fin[(size_t)i * A.CS + c], A.temperature);
-            s_ex[c] = x;
+        unsigned long long best_val = 0ull;
+        for (int c = tid; c < ns; c += 32) {
+            const float l = A.fin[(size_t)i * kCsMax + c];
+            const float x = __fdiv_rn(l, A.temperature);
             mx = fmaxf(mx, x);
+            const unsigned long long vkey = dev::value_key(l, dev::key_index(s_sel[c]));
+            best_val = vkey > best_val ? vkey : best_val;
+            s_ek[c] = __float_as_uint(x);  // stash x; replaced by the e-key below
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        for (int c = tid; c < cs; c += 32) {
-            const float e = dev::expf_glibc(__fsub_rn(s_ex[c], mx), rs.tab);
-            s_ek[c] = dev::prob_key(e, dev::key_index(keys[c]));
-        }
-        __syncwarp();
-        // selection sort of the top kk+1 keys into s_ek order (cs <= 64)
-        const int kk = min(A.k, A.v_rows);
-        const int want = min(cs, kk + 1);
-        for (int r = 0; r < want; ++r) {
-            unsigned long long best = 0ull;
-            int where = -1;
-            for (int c = r + tid; c < cs; c += 32)
-                if (s_ek[c] > best) {
-                    best = s_ek[c];
-                    where = c;
-                }
-            unsigned long long wbest = warp_max_u64(best);
-            const unsigned ball = __ballot_sync(0xffffffffu, where >= 0 && best == wbest);
-            const int src_lane = __ffs(ball) - 1;
-            const int w = __shfl_sync(0xffffffffu, where, src_lane);
-            if (tid == 0 && w != r) {
-                const unsigned long long tmp = s_ek[r];
-                s_ek[r] = s_ek[w];
-                s_ek[w] = tmp;
+        best_val = warp_max_u64(best_val);
+        bool cert = !bad && !overflow && ns >= kk;
+        if (A.argmax) {
+            // every non-recomputed row: exact <= a_bound + eps < the best exact logit
+            if (tid == 0) {
+                const float lb = dev::key_value(best_val);
+                cert = cert && (a_bound + eps < lb || a_bound == -__int_as_float(0x7f800000));
+                s_ek[0] = best_val;
+                s_cert = cert;
+            }
+        } else {
+            __syncwarp();
+            for (int c = tid; c < ns; c += 32) {
+                const float x = __uint_as_float(static_cast<uint32_t>(s_ek[c]));
+                s_ek[c] = dev::prob_key(dev::expf_glibc(__fsub_rn(x, mx), rs.tab), dev::key_index(s_sel[c]));
             }
             __syncwarp();
-        }
-        if (tid == 0) {
-            bool cert = ok;
-            if (cs < kk) cert = false;
-            // near ties among the selected and at the boundary (4-ulp separation)
-            for (int r = 0; cert && r + 1 < want; ++r) {
-                const float ea = __uint_as_float(static_cast<uint32_t>(s_ek[r] >> 32));
-                const float eb = __uint_as_float(static_cast<uint32_t>(s_ek[r + 1] >> 32));
-                if (ea != eb && ea <= eb * (1.0f + 0x1p-21f)) cert = false;
-            }
-            if (cert && !all_rows) {
-                const float x_ub = __fdiv_ru(a_bound + eps, A.temperature) * (1.0f + 0x1p-20f) + 0x1p-20f;
-                if (!(x_ub < mx)) {
-                    cert = false;
-                } else {
-                    const float e_ub = dev::expf_glibc(x_ub - mx, rs.tab) * (1.0f + 0x1p-20f);
-                    const float e_k = __uint_as_float(static_cast<uint32_t>(s_ek[kk - 1] >> 32));
-                    if (!(e_ub * (1.0f + 0x1p-21f) < e_k)) cert = false;
+            const int want = min(ns, kk + 1);
+            for (int r = 0; r < want; ++r) {  // selection sort of the leading (kk + 1) e-keys
+                unsigned long long best = 0ull;
+                int where = -1;
+                for (int c = r + tid; c < ns; c += 32)
+                    if (s_ek[c] > best) {
+                        best = s_ek[c];
+                        where = c;
+                    }
+                const unsigned long long wbest = warp_max_u64(best);
+                const unsigned ball = __ballot_sync(0xffffffffu, where >= 0 && best == wbest);
+                const int w = __shfl_sync(0xffffffffu, where, __ffs(ball) - 1);
+                if (tid == 0 && w != r) {
+                    const unsigned long long tmp = s_ek[r];
+                    s_ek[r] = s_ek[w];
+                    s_ek[w] = tmp;
                 }
+                __syncwarp();
             }
-            s_last = cert;
-            s_mx = mx;
+            if (tid == 0) {
+                // near ties (within 4 ulps) among the selected and at the k boundary: the
+                // reference's (prob, index) order could depend on the exact denominator
+                for (int r = 0; cert && r + 1 < want; ++r) {
+                    const float ea = __uint_as_float(static_cast<uint32_t>(s_ek[r] >> 32));
+                    const float eb = __uint_as_float(static_cast<uint32_t>(s_ek[r + 1] >> 32));
+                    if (ea != eb && ea <= eb * (1.0f + 0x1p-21f)) cert = false;
+                }
+                if (cert && a_bound != -__int_as_float(0x7f800000)) {
+                    const float x_ub = __fdiv_ru(a_bound + eps, A.temperature) * (1.0f + 0x1p-20f) + 0x1p-20f;
+                    if (!(x_ub < mx)) {
+                        cert = false;
+                    } else {
+                        const float e_ub = dev::expf_glibc(x_ub - mx, rs.tab) * (1.0f + 0x1p-20f);
+                        const float e_k = __uint_as_float(static_cast<uint32_t>(s_ek[kk - 1] >> 32));
+                        if (!(e_ub * (1.0f + 0x1p-21f) < e_k)) cert = false;
+                    }
+                }
+                s_cert = cert;
+                s_mx = mx;
+            }
         }
     }
     __syncthreads();
-    const int kk = min(A.k, A.v_rows);
-    if (s_last) {
+    if (s_cert) {
         if (tid == 0) {
-            const float mx = s_mx;
-            // tot = sum exp(x_j - M) in the approximate x domain; rescale to the exact max
-            const double total = tot * exp(static_cast<double>(mmax) - static_cast<double>(mx));
-            const float inv = __double2float_rn(1.0 / total);
-            for (int r = 0; r < kk; ++r) {
-                const int j = dev::key_index(s_ek[r]);
-                A.out_ridx[(size_t)i * A.k + r] = j;
-                A.out_full[(size_t)i * A.k + r] = A.ordered ? A.ordered[j] : j;
-                A.out_prob[(size_t)i * A.k + r] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(s_ek[r] >> 32)), inv);
+            if (A.argmax) {
+                const unsigned long long best = s_ek[0];
+                A.out_full[i] = A.id_offset + dev::key_index(best);
+                if (A.out_prob) A.out_prob[i] = dev::key_value(best);
+            } else {
+                const float mx = s_mx;
+                // tot = sum exp(x_j - M) in the approximate domain; rescale to the exact max
+                const double total = tot * exp(static_cast<double>(mmax) - static_cast<double>(mx));
+                const float inv = __double2float_rn(1.0 / total);
+                for (int r = 0; r < kk; ++r) {
+                    const int j = dev::key_index(s_ek[r]);
+                    A.out_ridx[(size_t)i * A.k + r] = j;
+                    A.out_full[(size_t)i * A.k + r] = A.ordered ? A.ordered[j] : j;
+                    A.out_prob[(size_t)i * A.k + r] =
+                        __fmul_rn(__uint_as_float(static_cast<uint32_t>(s_ek[r] >> 32)), inv);
+                }
+                for (int r = kk; r < A.k; ++r) {
+                    A.out_ridx[(size_t)i * A.k + r] = -1;
+                    A.out_full[(size_t)i * A.k + r] = -1;
+                    A.out_prob[(size_t)i * A.k + r] = 0.0f;
+                }
+                if (A.out_rowmax) A.out_rowmax[i] = mx;
+                if (A.out_total) A.out_total[i] = total;
             }
-            for (int r = kk; r < A.k; ++r) {
-                A.out_ridx[(size_t)i * A.k + r] = -1;
-                A.out_full[(size_t)i * A.k + r] = -1;
-                A.out_prob[(size_t)i * A.k + r] = 0.0f;
-            }
-            if (A.out_rowmax) A.out_rowmax[i] = mx;
-            if (A.out_total) A.out_total[i] = total;
             if (A.out_flags) A.out_flags[i] = flags;
         }
         return;
     }
-    // fallback: the exact row (bit-identical to the EXACT path)
+    // ---- fallback: the exact full row in this CTA (bit-identical to the EXACT path)
     float *L = A.scratch + (size_t)i * 2 * A.v_rows;
     if (!bad) {
         fallback_exact_logits(sh, A.slab, A.v_rows, A.d, L);
@@ -737,6 +896,20 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         for (int j = tid; j < A.v_rows; j += nt) L[j] = __int_as_float(0x7fc00000);
     }
     __syncthreads();
+    if (A.argmax) {
+        unsigned long long cand = 0ull;
+        for (int j = tid; j < A.v_rows; j += nt) {
+            const unsigned long long kk2 = dev::value_key(L[j], j);
+            cand = kk2 > cand ? kk2 : cand;
+        }
+        const unsigned long long best = dev::block_reduce(cand, dev::MaxU64(), rs.k);
+        if (tid == 0) {
+            A.out_full[i] = A.id_offset + dev::key_index(best);
+            if (A.out_prob) A.out_prob[i] = L[dev::key_index(best)];
+            if (A.out_flags) A.out_flags[i] = flags;
+        }
+        return;
+    }
     const uint32_t f2 = dev::softmax_topk_row(L, A.v_rows, A.k, A.temperature, A.ordered, L + A.v_rows,
                                               A.out_ridx + (size_t)i * A.k, A.out_full + (size_t)i * A.k,
                                               A.out_prob + (size_t)i * A.k, A.out_rowmax ? A.out_rowmax + i : nullptr,
@@ -779,7 +952,8 @@ struct FastWs {
     float *scratch;
 };
 
-int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, int CS, FastWs &w) {
+int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
+    const int CS = kCsMax;
     const int G = ctx->sm_count;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -804,6 +978,12 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, int CS, FastW
     w.P.G = G;
     w.fin = reinterpret_cast<float *>(base + o_fin);
     w.scratch = reinterpret_cast<float *>(base + o_scr);
+    w.P.trace = nullptr;
+    static const bool tracing = std::getenv("FRS_TRACE") != nullptr;
+    if (tracing) {
+        if ((st = ctx->trace.ensure((size_t)G * 16 * 8))) return st;
+        w.P.trace = static_cast<unsigned long long *>(ctx->trace.ptr);
+    }
     if (!ctx->fast_ctr.ptr) {
         if ((st = ctx->fast_ctr.ensure(64 * sizeof(unsigned long long)))) return st;
         FRS_CUDA_TRY(cudaMemset(ctx->fast_ctr.ptr, 0, 64 * sizeof(unsigned long long)));
@@ -819,7 +999,7 @@ int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapH, 
     FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctx->sm_count);
-    cfg.blockDim = dim3(kMainThreads);
+    cfg.blockDim = dim3(C::THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -832,14 +1012,13 @@ int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapH, 
     return FRS_OK;
 }
 
-template <int SORTN>
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
-    auto kern = k_fast_finalize<SORTN>;
-    const size_t smem = (size_t)((A.d + 3) & ~3) * 4 + (size_t)SORTN * 8 + (size_t)kCandPerFinCta * A.d * 2 + 64;
+    auto kern = k_fast_finalize;
+    const size_t smem = (size_t)((A.d + 7) & ~7) * 4 + (size_t)kCandPerFinCta * A.d * 2 + 64;
     if (smem > ctx->smem_optin) return fail(FRS_ENOTSUP, "FAST finalize: hidden_dim too large");
     FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(rows, A.CSB);
+    cfg.gridDim = dim3(rows, kFinCtas);
     cfg.blockDim = dim3(kFinThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -858,14 +1037,23 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
     if (d % 8 != 0) return fail(FRS_ENOTSUP, "FAST head: hidden_dim must be a multiple of 8 (TMA row pitch)");
     if (n > 64) return fail(FRS_ENOTSUP, "FAST head: at most 64 hidden rows per call");
-    if (!argmax && n > 32) return fail(FRS_ENOTSUP, "FAST draft head: at most 32 hidden rows per call");
+    if (!argmax && n > 16) {  // the fused softmax path takes 16 hidden rows per pass
+        for (int r0 = 0; r0 < n; r0 += 16) {
+            const int nr = std::min(16, n - r0);
+            const int st = launch_fast(ctx, h + (size_t)r0 * d, nr, d, W, v_rows, ordered_ids, k, temperature, false, 0,
+                                       out_ridx + (size_t)r0 * k, out_full + (size_t)r0 * k, out_prob + (size_t)r0 * k,
+                                       out_rowmax ? out_rowmax + r0 : nullptr, out_total ? out_total + r0 : nullptr,
+                                       out_flags ? out_flags + r0 : nullptr, s);
+            if (st) return st;
+        }
+        return FRS_OK;
+    }
     if (!argmax && k > 64) return fail(FRS_ENOTSUP, "FAST draft head: k <= 64");
     const int NP = n <= 16 ? 16 : (n <= 32 ? 32 : 64);
     const int G = ctx->sm_count;
-    if (G * R > 1024) return fail(FRS_ENOTSUP, "FAST head: too many SMs for the candidate merge");
-    const int CS = argmax ? 8 : (k <= 16 ? 32 : 64);
+    if (G * R > kFinThreads * kFinKPT) return fail(FRS_ENOTSUP, "FAST head: too many SMs for the candidate merge");
     FastWs w;
-    int st = fast_workspace(ctx, NP, d, n, v_rows, CS, w);
+    int st = fast_workspace(ctx, NP, d, n, v_rows, w);
     if (st) return st;
     CUtensorMap mapW, mapH;
     if ((st = make_map(&mapW, W, v_rows, d, BM))) return st;
@@ -886,8 +1074,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
              : NP == 32 ? launch_main<32, false>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s)
                         : launch_main<64, false>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s);
     } else {
-        st = NP == 16 ? launch_main<16, true>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s)
-                      : launch_main<32, true>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s);
+        st = launch_main<16, true>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s);
     }
     if (st) return st;
     FinArgs A{};
@@ -896,8 +1083,6 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     A.d = d;
     A.v_rows = v_rows;
     A.k = argmax ? 1 : k;
-    A.CS = CS;
-    A.CSB = argmax ? 1 : CS / kCandPerFinCta;
     A.temperature = temperature;
     A.slab = static_cast<const unsigned short *>(W);
     A.ordered = ordered_ids;
@@ -913,7 +1098,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     A.out_flags = out_flags;
     A.argmax = argmax ? 1 : 0;
     A.id_offset = id_offset;
-    return G * R <= 512 ? launch_fin<512>(ctx, A, n, s) : launch_fin<1024>(ctx, A, n, s);
+    return launch_fin(ctx, A, n, s);
 }
 
 }  // namespace
@@ -923,7 +1108,7 @@ int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float 
                         float *pw2) {
     FastWs w;
     const int NP = n <= 16 ? 16 : (n <= 32 ? 32 : 64);
-    int st = fast_workspace(ctx, NP, d, n, 1, 64, w);
+    int st = fast_workspace(ctx, NP, d, n, 1, w);
     if (st) return st;
     const int G = ctx->sm_count;
     FRS_CUDA_TRY(cudaDeviceSynchronize());
@@ -932,6 +1117,9 @@ int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float 
     FRS_CUDA_TRY(cudaMemcpy(pth, w.P.pth, sizeof(float) * n * G, cudaMemcpyDeviceToHost));
     FRS_CUDA_TRY(cudaMemcpy(pkey, w.P.pkey, sizeof(unsigned long long) * n * G * R, cudaMemcpyDeviceToHost));
     FRS_CUDA_TRY(cudaMemcpy(pw2, w.P.pw2, sizeof(float) * G, cudaMemcpyDeviceToHost));
+    if (w.P.trace && ctx->trace.bytes >= (size_t)G * 16 * 8) {  // trailing [G][16] stamps
+        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * G * R, w.P.trace, (size_t)G * 16 * 8, cudaMemcpyDeviceToHost));
+    }
     return FRS_OK;
 }
 
