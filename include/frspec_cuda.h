@@ -64,6 +64,10 @@ typedef enum { FRS_MODE_EXACT = 0, FRS_MODE_FAST = 1 } frs_mode;
 #define FRS_FLAG_SEQ_SUM 0x2u    /* Σ exp took the index-order sequential path                  */
 #define FRS_FLAG_UNCERTIFIED 0x4u /* FAST: candidate set could not be certified (ids may differ) */
 #define FRS_FLAG_RECOMPUTED 0x8u /* FAST: row fell back to the exact kernel                     */
+/* FAST: why a row fell back (set together with FRS_FLAG_RECOMPUTED) — "ties at tolerance". */
+#define FRS_FLAG_CERT_TIE 0x10u      /* two selected probabilities within 4 ulps: order needs exact Σ  */
+#define FRS_FLAG_CERT_BOUND 0x20u    /* the rigorous error bound did not separate the k-th candidate   */
+#define FRS_FLAG_CERT_OVERFLOW 0x40u /* more near-boundary candidates than the exact-recompute set     */
 
 typedef struct frs_ctx frs_ctx;
 typedef struct frs_head frs_head;

@@ -15,6 +15,7 @@ FRS_OK, FRS_EINVAL, FRS_ECAPACITY, FRS_EDATA, FRS_ELOGIC, FRS_ECUDA, FRS_ENCCL, 
 DTYPE_F32, DTYPE_BF16 = 0, 1
 MODE_EXACT, MODE_FAST = 0, 1
 FLAG_NONFINITE, FLAG_SEQ_SUM, FLAG_UNCERTIFIED, FLAG_RECOMPUTED = 0x1, 0x2, 0x4, 0x8
+FLAG_CERT_TIE, FLAG_CERT_BOUND, FLAG_CERT_OVERFLOW = 0x10, 0x20, 0x40
 
 
 class FrsError(RuntimeError):

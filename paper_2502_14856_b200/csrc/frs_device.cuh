@@ -224,5 +224,44 @@ __device__ __forceinline__ float dot_f32_lanes8(const float *h, const WT *w, int
     return s;
 }
 
+// Same arithmetic as dot_f32_lanes8 (bf16 row w in shared memory), with the operands of the
+// next 16 steps loaded into registers while the current 16 dependent adds run: the chain is
+// bound by the FADD latency (d/8 steps) instead of the shared-memory load latency.
+__device__ __forceinline__ float dot_f32_lanes8_pf(const float *h, const unsigned short *w, int d) {
+    const int l = threadIdx.x & 7;
+    const int T = d >> 3;
+    constexpr int B = 16;
+    float hb[B], wb[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+        hb[u] = u < T ? h[8 * u + l] : 0.0f;
+        wb[u] = u < T ? w_at(w, 8 * u + l) : 0.0f;
+    }
+    float s = 0.0f;
+    for (int t0 = 0; t0 < T; t0 += B) {
+        float hn[B], wn[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int t = t0 + B + u;
+            hn[u] = t < T ? h[8 * t + l] : 0.0f;
+            wn[u] = t < T ? w_at(w, 8 * t + l) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            if (t0 + u < T) s = __fadd_rn(s, __fmul_rn(hb[u], wb[u]));
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            hb[u] = hn[u];
+            wb[u] = wn[u];
+        }
+    }
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+    if (l == 0)
+        for (int e = 8 * T; e < d; ++e) s = __fadd_rn(s, __fmul_rn(h[e], w_at(w, e)));
+    return s;
+}
+
 }  // namespace dev
 }  // namespace frs

@@ -44,10 +44,14 @@ namespace frs {
 namespace {
 
 constexpr int BM = 128;      // slab rows per tile (UMMA M)
+constexpr int CH = 32;       // slab rows per TMA box = partition granule: CTAs own contiguous
+                             // runs of 32-row chunks (<= 1 chunk of imbalance instead of 1 tile)
+constexpr int CPT = BM / CH; // chunks per tile
 constexpr int BK = 64;       // k elements per stage: 128-byte bf16 rows, SWIZZLE_128B
 constexpr int R = 8;         // per-CTA candidates per hidden row
 constexpr int RL = R + 1;    // tracked per warp / CTA: the (R+1)-th bounds the CTA's other rows
 constexpr int kFinThreads = 256;
+constexpr int kFbThreads = 256;
 constexpr int kCandPerFinCta = 8;  // exact recomputes per finalize CTA (8 lanes each)
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -123,17 +127,6 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-#define FRS_TMEM_LD32(taddr, r)                                                                                   \
-    asm volatile(                                                                                                 \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"          \
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),       \
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), \
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),            \
-          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),            \
-          "=r"(r[30]), "=r"(r[31])                                                                              \
-        : "r"(taddr))
-
 // UMMA shared-memory descriptor, K-major, SWIZZLE_128B canonical layout: 8-row x 128-byte
 // atoms, SBO = 1024 B between atoms, LBO unused (1), version 1 (sm_100), layout type 2.
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -146,34 +139,6 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
            (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = w > v ? w : v;
-    }
-    return v;
-}
-
-// Warp-wide merge of 32 new keys (one per lane) into a sorted top-RL list held in smem.
-// Bitonic sort (descending) of one 64-bit key per lane across the warp, for NR independent
-// rows at once so the shuffle chains of different rows interleave (ILP instead of latency).
-template <int NR>
-__device__ __forceinline__ void warp_sort_desc(unsigned long long (&v)[NR], int lane) {
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const bool keep_max = ((lane & j) == 0) == ((lane & k) == 0);
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const unsigned long long p = __shfl_xor_sync(0xffffffffu, v[r], j);
-                v[r] = keep_max ? (v[r] > p ? v[r] : p) : (v[r] < p ? v[r] : p);
-            }
-        }
-    }
-}
-
 // ------------------------------------------------------------------ kernels
 struct Partials {
     float *pm;                 // [NP][G] running max of x = logit / t (softmax only)
@@ -183,6 +148,7 @@ struct Partials {
     float *pw2;                // [G] max squared L2 norm of the CTA's slab rows
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
+    int tiled;                 // EXPERIMENT: W map addresses [chunk][kb][32 x 64] pieces
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -198,6 +164,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // hs rows [0,NP) = bf16(h), rows [NP,2NP) = bf16(h - bf16(h)); padded rows are zero.
 __global__ void __launch_bounds__(256) k_hsplit(const float *__restrict__ h, int n, int d, int NP,
                                                 __nv_bfloat16 *__restrict__ hs) {
+    // launched programmatically after whatever precedes it on the stream: wait for it (h is
+    // final, the previous call's fallback queue is drained), then let the main kernel launch
+    griddep_wait();
+    griddep_launch();
     const int total = NP * d;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
         const int i = idx / d, c = idx - i * d;
@@ -207,13 +177,12 @@ __global__ void __launch_bounds__(256) k_hsplit(const float *__restrict__ h, int
         hs[(size_t)i * d + c] = hi;
         hs[(size_t)(NP + i) * d + c] = lo;
     }
-    griddep_launch();
 }
 
 template <int NP, bool SOFTMAX>
 struct MainCfg {
     static constexpr int N = 2 * NP;                       // MMA N: hi rows then lo rows
-    static constexpr int EPI_WARPS = NP <= 32 ? 4 : 8;     // 4 TMEM lane quarters x column halves
+    static constexpr int EPI_WARPS = 8;                    // 4 TMEM lane quarters x 2 column halves
     static constexpr int RPW = NP / (EPI_WARPS / 4);       // hidden rows per epilogue warp
     static constexpr int TOPK = SOFTMAX ? 2 : 1;           // per-thread kept candidates per hidden row
     static constexpr int THREADS = (4 + EPI_WARPS) * 32;
@@ -236,6 +205,11 @@ struct MainCfg {
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) \
         : "r"(taddr))
+
+#define FRS_TMEM_LD8(taddr, r)                                                                          \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                    \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]) \
+                 : "r"(taddr))
 
 // Warp max of a (value, index) key with 2 REDUX instead of 10 shuffles: max over the ordered
 // value bits, then max over ~index among the lanes holding that value.
@@ -268,9 +242,16 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     // keep their shuffles convergent (no WARPSYNC.COLLECTIVE emulation)
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int G = gridDim.x, cta = blockIdx.x;
-    const int T = (v_rows + BM - 1) / BM, KB = (d + BK - 1) / BK;
-    const int t_begin = static_cast<int>((static_cast<long long>(cta) * T) / G);
-    const int t_end = static_cast<int>((static_cast<long long>(cta + 1) * T) / G);
+    const int KB = (d + BK - 1) / BK;
+    // balanced partition: this CTA owns 32-row chunks [c_begin, c_end); tile t covers chunks
+    // c_begin + CPT t .. (at most CPT), so the A tile of a short tile is partly stale (ignored)
+    const int NCH = (v_rows + CH - 1) / CH;
+    const int c_begin = static_cast<int>((static_cast<long long>(cta) * NCH) / G);
+    const int c_end = static_cast<int>((static_cast<long long>(cta + 1) * NCH) / G);
+    const int t_begin = 0, t_end = (c_end - c_begin + CPT - 1) / CPT;
+    auto tile_chunks = [&](int t) { return min(CPT, c_end - (c_begin + t * CPT)); };
+    auto tile_row0 = [&](int t) { return (c_begin + t * CPT) * CH; };
+    auto tile_rows = [&](int t) { return min(v_rows - tile_row0(t), tile_chunks(t) * CH); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -294,6 +275,9 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) FRS_TRACE(P, 0);
+    // let the finalize grid launch now: its CTAs take SMs as ours retire and run their
+    // prologue; griddepcontrol.wait there still waits for this whole grid (and its writes)
+    griddep_launch();
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -302,10 +286,14 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             uint32_t phase = 0;
             bool waited = false;
             for (int t = t_begin; t < t_end; ++t) {
+                const int nch = tile_chunks(t), r0 = tile_row0(t);
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-                    tma_load_2d(sA + stage * C::A_BYTES, &mapW, &full[stage], kb * BK, t * BM, pol_w);
+                    mbar_expect_tx(&full[stage], nch * (CH * BK * 2) + C::B_BYTES);
+                    for (int c = 0; c < nch; ++c)
+                        tma_load_2d(sA + stage * C::A_BYTES + c * (CH * BK * 2), &mapW, &full[stage],
+                                    P.tiled ? 0 : kb * BK,
+                                    P.tiled ? ((r0 / CH + c) * KB + kb) * CH : r0 + c * CH, pol_w);
                     if (!waited) {  // hs is produced by k_hsplit (programmatic dependency)
                         FRS_TRACE(P, 1);
                         griddep_wait();
@@ -356,6 +344,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         int stage = 0;
         uint32_t phase = 0;
         for (int t = t_begin; t < t_end; ++t) {
+            const int nrows = tile_rows(t);  // rows past it are stale smem: keep them out of the max
             for (int kb = 0; kb < KB; ++kb) {
                 mbar_wait(&full[stage], phase);
                 const uint4 *a0 = reinterpret_cast<const uint4 *>(sA + stage * C::A_BYTES + r0 * 128);
@@ -380,7 +369,8 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                     phase ^= 1;
                 }
             }
-            wmax = fmaxf(wmax, fmaxf(acc0, acc1));
+            if (r0 < nrows) wmax = fmaxf(wmax, acc0);
+            if (r0 + 64 < nrows) wmax = fmaxf(wmax, acc1);
             acc0 = acc1 = 0.0f;
         }
 #pragma unroll
@@ -413,35 +403,30 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             if (threadIdx.x == 128 && lt == 0) FRS_TRACE(P, 11);
             tc_fence_after();
-            const int row = t * BM + q * 32 + lane;
-            const bool valid = row < v_rows;
+            const int row = tile_row0(t) + q * 32 + lane;
+            const bool valid = q * 32 + lane < tile_rows(t);
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * N);
+            constexpr int CG = RPW < 16 ? RPW : 16;  // hidden rows per TMEM load group
 #pragma unroll
-            for (int cg = 0; cg < RPW / 16; ++cg) {
-                const int c0 = cbase + cg * 16;
-                uint32_t hi[16], lo[16];
-                if constexpr (NP == 16) {
-                    uint32_t both[32];
-                    FRS_TMEM_LD32(tbase, both);  // cols 0..15 hi, 16..31 lo
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int r = 0; r < 16; ++r) {
-                        hi[r] = both[r];
-                        lo[r] = both[16 + r];
-                    }
+            for (int cg = 0; cg < RPW / CG; ++cg) {
+                const int c0 = cbase + cg * CG;
+                uint32_t hi[CG], lo[CG];
+                if constexpr (CG == 8) {
+                    FRS_TMEM_LD8(tbase + c0, hi);
+                    FRS_TMEM_LD8(tbase + NP + c0, lo);
                 } else {
                     FRS_TMEM_LD16(tbase + c0, hi);
                     FRS_TMEM_LD16(tbase + NP + c0, lo);
-                    tmem_wait_ld();
                 }
-                if (cg == RPW / 16 - 1) {  // accumulator drained: hand it back to the MMA warp
+                tmem_wait_ld();
+                if (cg == RPW / CG - 1) {  // accumulator drained: hand it back to the MMA warp
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
 #pragma unroll
-                for (int r = 0; r < 16; ++r) {
-                    const int rr = cg * 16 + r, i = c0 + r;
+                for (int r = 0; r < CG; ++r) {
+                    const int rr = cg * CG + r, i = c0 + r;
                     if (!valid || i >= n) continue;
                     const float a = __uint_as_float(hi[r]) + __uint_as_float(lo[r]);
                     if constexpr (SOFTMAX) {  // online sum exp(x - m), one MUFU per value
@@ -559,8 +544,6 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         P.pw2[cta] = fmaxf(wred[0], wred[1]);
         FRS_TRACE(P, 7);
     }
-    __threadfence();
-    griddep_launch();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
@@ -578,7 +561,6 @@ __device__ __forceinline__ float fast_gamma(int d) {
     return static_cast<float>(g * 1.01);
 }
 
-constexpr int kFinKPT = 8;    // union keys held per finalize thread: G * R <= 256 * 8
 constexpr int kCsMax = 64;    // max exactly-recomputed candidates per row (kFinCtas x 8)
 constexpr int kFinCtas = kCsMax / kCandPerFinCta;
 
@@ -598,176 +580,301 @@ struct FinArgs {
     uint32_t *out_flags;
     int argmax;                      // verify mode: out_full = id_offset + argmax id, out_prob = its logit
     int32_t id_offset;
+    unsigned *fb_count;              // fallback queue: count, entries row | reasons << 16
+    uint32_t *fb_rows;               // [64]
+    unsigned long long *fb_arrive;   // monotonic CTA arrival counter of k_fast_fallback
 };
 
-__device__ void fallback_exact_logits(const float *sh, const unsigned short *slab, int v_rows, int d, float *L) {
-    // The whole CTA: 8-lane groups each compute exact dot_f32 for rows g, g + groups, ...
-    const int groups = blockDim.x / 8, g = threadIdx.x / 8;
-    for (int base = 0; base < v_rows; base += groups) {
-        const int j = base + g;
-        const int jj = j < v_rows ? j : v_rows - 1;
-        const float v = dev::dot_f32_lanes8(sh, slab + (size_t)jj * d, d);
-        if ((threadIdx.x & 7) == 0 && j < v_rows) L[j] = v;
-    }
-}
+#define FRS_FTRACE(A, slot)                                                                              \
+    do {                                                                                                  \
+        if ((A).P.trace && threadIdx.x == 0)                                                              \
+            (A).P.trace[(size_t)(A).P.G * 16 + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + (slot)] = gtimer(); \
+    } while (0)
 
-// Finalize: grid (n, kFinCtas). Every CTA of row i merges the CTA partials (identically),
-// selects S = {union keys with approx >= approx_(k) - 2 eps - margin} (typically ~k..2k
-// entries), recomputes its slice of S exactly, and the last CTA to arrive selects the top-k
-// by (prob desc, index asc) and certifies it (see the file comment).
+// Finalize: grid (n, kFinCtas). The work per row is tiny, so the kernel is written for
+// latency: every step is spread over the whole CTA (a single warp running serial code sits at
+// CPI ~4 and was the bottleneck). Every CTA of row i rebuilds the same candidate set S:
+//   1. stage the row's union of per-CTA top-R keys (G lists, each sorted descending) and the
+//      hidden row (transposed per dot_f32 lane chain) in shared memory; warp 0 merges the
+//      softmax partials, warp 1 the bounds.
+//   2. v' = the kk-th largest key among the top-2 of every list (a lower bound of the kk-th
+//      largest union key), by parallel rank counting; S = {union keys >= v' - 2 eps - margin}
+//      (a superset of every row that can reach the top-k), in canonical descending order.
+//   3. the CTA recomputes its slice S[8b, 8b + 8) EXACTLY (dot_f32 order) into A.fin, each
+//      8-lane group reading its chain's operands as 16-byte vectors from transposed tiles.
+//   4. the last CTA of the row to arrive selects the top-k by (prob desc, index asc) and
+//      certifies it (see the file comment); rows that cannot be certified are queued for the
+//      grid-wide exact fallback (k_fast_fallback).
+constexpr int kMaxLists = 256;  // G <= 256 CTA lists of R keys
+
 __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
-    extern __shared__ uint8_t fsm_raw[];
-    float *sh = reinterpret_cast<float *>(fsm_raw);                                   // [d]
-    unsigned short *wrows = reinterpret_cast<unsigned short *>(sh + ((A.d + 7) & ~7));  // [8][d]
-    __shared__ dev::ReduceScratch rs;
-    __shared__ int s_nsel, s_last, s_cert;
-    __shared__ float s_mx;
-    __shared__ unsigned long long s_sel[kCsMax];
-    __shared__ unsigned long long s_ek[kCsMax];
+    extern __shared__ __align__(16) uint8_t fsm_raw[];
+    const int T = A.d >> 3;           // dot_f32 steps per lane chain (d % 8 == 0 on FAST)
+    const int TP = T + 8;             // padded chain pitch (elements): 16-byte aligned rows
+    unsigned long long *ukeys = reinterpret_cast<unsigned long long *>(fsm_raw);       // [G*R]
+    float *ht = reinterpret_cast<float *>(ukeys + (size_t)A.P.G * R);                 // [8][TP]
+    unsigned short *wt = reinterpret_cast<unsigned short *>(ht + 8 * TP);            // [8 cand][8][TP]
+    __shared__ unsigned long long s_S[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
+    __shared__ double s_hn2[kFinThreads / 32], s_tot;
+    __shared__ float s_mmax, s_th, s_eps, s_abw[kFinThreads / 32];
+    __shared__ unsigned long long s_vk, s_wtop[kFinThreads / 32][kMaxK];
+    __shared__ int s_nsel, s_last, s_badw[kFinThreads / 32];
+    FRS_FTRACE(A, 0);
+    griddep_launch();  // the fallback grid may become resident now; it waits for this grid
 
-    const int i = blockIdx.x, b = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
-    const int warp_u = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);  // warp-uniform
+    const int i = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = tid & 31;
     const int G = A.P.G, E = G * R;
-    // ---- prologue (independent of the main kernel): the hidden row and its norm
-    double hn2 = 0.0;
-    int bad = 0;
-    {  // batch the global loads (all in flight) before the shared stores
+    const float kNegInf = -__int_as_float(0x7f800000);
+    // ---- 1a. the hidden row (independent of the main kernel): transposed ht[l][t] = h[8t + l]
+    {
         const float4 *hv = reinterpret_cast<const float4 *>(A.h + (size_t)i * A.d);
-        const int d4 = A.d / 4;  // d % 8 == 0 on the FAST path
-        constexpr int MAXV = 8;  // up to 8 float4 per thread: d <= 8192
-        float4 v[MAXV];
+        double hn2 = 0.0;
+        int bad = 0;
+        for (int e0 = tid; e0 < 2 * T; e0 += 4 * kFinThreads) {  // float4 e holds h[4e .. 4e + 3]
+            float4 w[4];
 #pragma unroll
-        for (int u = 0; u < MAXV; ++u) {
-            const int e = tid + u * kFinThreads;
-            v[u] = e < d4 ? __ldg(hv + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        for (int e = tid + MAXV * kFinThreads; e < d4; e += kFinThreads) {  // d > 8192
-            const float4 w = __ldg(hv + e);
-            reinterpret_cast<float4 *>(sh)[e] = w;
-            const float xs[4] = {w.x, w.y, w.z, w.w};
-            for (int q = 0; q < 4; ++q) {
-                if (!isfinite(xs[q])) bad = 1;
-                hn2 += static_cast<double>(xs[q]) * xs[q];
+            for (int u = 0; u < 4; ++u) {  // all loads in flight before any use
+                const int e = e0 + u * kFinThreads;
+                w[u] = e < 2 * T ? __ldg(hv + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * kFinThreads;
+                if (e >= 2 * T) continue;
+                const int t = e >> 1, l0 = (e & 1) * 4;
+                ht[(l0 + 0) * TP + t] = w[u].x;
+                ht[(l0 + 1) * TP + t] = w[u].y;
+                ht[(l0 + 2) * TP + t] = w[u].z;
+                ht[(l0 + 3) * TP + t] = w[u].w;
+                bad |= !isfinite(w[u].x) | !isfinite(w[u].y) | !isfinite(w[u].z) | !isfinite(w[u].w);
+                hn2 += static_cast<double>(w[u].x) * w[u].x + static_cast<double>(w[u].y) * w[u].y +
+                       static_cast<double>(w[u].z) * w[u].z + static_cast<double>(w[u].w) * w[u].w;
             }
         }
 #pragma unroll
-        for (int u = 0; u < MAXV; ++u) {
-            const int e = tid + u * kFinThreads;
-            if (e < d4) {
-                reinterpret_cast<float4 *>(sh)[e] = v[u];
-                const float xs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (!isfinite(xs[q])) bad = 1;
-                    hn2 += static_cast<double>(xs[q]) * xs[q];
-                }
-            }
+        for (int o = 16; o > 0; o >>= 1) hn2 += __shfl_xor_sync(0xffffffffu, hn2, o);
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            s_hn2[warp] = hn2;
+            s_badw[warp] = bad;
+        }
+        if (tid == 0) {
+            s_nsel = 0;
+            s_vk = 0ull;
         }
     }
-    if (tid == 0) s_nsel = 0;
-    hn2 = dev::block_reduce(hn2, dev::SumD(), rs.d);
-    bad = dev::block_reduce(bad, dev::OrI(), rs.i);
+    __syncthreads();  // s_hn2 / s_badw complete (read by warp 1 below)
+    FRS_FTRACE(A, 1);
     griddep_wait();
-
-    // ---- merge the CTA partials (identically in every CTA of this row)
-    unsigned long long kr[kFinKPT];
+    FRS_FTRACE(A, 2);
+    // ---- 1b. partials of the main kernel: every load of a thread issued before any use
+    constexpr int KPT = kMaxLists * R / kFinThreads;  // union keys per thread (8)
+    unsigned long long kr[KPT];
+    {
+        const unsigned long long *src = A.P.pkey + (size_t)i * E;
 #pragma unroll
-    for (int j = 0; j < kFinKPT; ++j) {
-        const int e = tid + j * nt;
-        kr[j] = e < E ? A.P.pkey[(size_t)i * E + e] : 0ull;
-    }
-    float th = -__int_as_float(0x7f800000), w2 = 0.0f, mmax = -__int_as_float(0x7f800000);
-    for (int c = tid; c < G; c += nt) {
-        th = fmaxf(th, A.P.pth[(size_t)i * G + c]);
-        w2 = fmaxf(w2, A.P.pw2[c]);
-        if (!A.argmax) mmax = fmaxf(mmax, A.P.pm[(size_t)i * G + c]);
-    }
-    th = dev::block_reduce(th, dev::MaxF(), rs.f);
-    w2 = dev::block_reduce(w2, dev::MaxF(), rs.f);
-    double tot = 0.0;
-    if (!A.argmax) {
-        mmax = dev::block_reduce(mmax, dev::MaxF(), rs.f);
-        for (int c = tid; c < G; c += nt) {
-            const float pm = A.P.pm[(size_t)i * G + c];
-            if (pm != -__int_as_float(0x7f800000))
-                tot += static_cast<double>(A.P.ps[(size_t)i * G + c]) * exp(static_cast<double>(pm) - mmax);
+        for (int u = 0; u < KPT; ++u) {
+            const int e = tid + u * kFinThreads;
+            kr[u] = e < E ? __ldcg(src + e) : 0ull;
         }
-        tot = dev::block_reduce(tot, dev::SumD(), rs.d);
+#pragma unroll
+        for (int u = 0; u < KPT; ++u) {
+            const int e = tid + u * kFinThreads;
+            if (e < E) ukeys[e] = kr[u];
+        }
     }
-    const float eps = static_cast<float>(sqrt(hn2) * sqrt(static_cast<double>(w2) * 1.001)) * fast_gamma(A.d) * 1.01f;
+    constexpr int LPL = kMaxLists / 32;  // CTA partials per lane (8)
+    if (warp == 0 && !A.argmax) {        // softmax partials: M = max m_c, T = sum s_c exp(m_c - M)
+        float pm[LPL], ps[LPL];
+#pragma unroll
+        for (int u = 0; u < LPL; ++u) {
+            const int c = lane + 32 * u;
+            pm[u] = c < G ? __ldcg(A.P.pm + (size_t)i * G + c) : kNegInf;
+            ps[u] = c < G ? __ldcg(A.P.ps + (size_t)i * G + c) : 0.0f;
+        }
+        float mm = kNegInf;
+#pragma unroll
+        for (int u = 0; u < LPL; ++u) mm = fmaxf(mm, pm[u]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+        double t = 0.0;
+#pragma unroll
+        for (int u = 0; u < LPL; ++u)  // approximate domain anyway: one MUFU per partial
+            if (pm[u] != kNegInf) t += static_cast<double>(ps[u] * exp2f((pm[u] - mm) * 1.4426950408889634f));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) {
+            s_mmax = mm;
+            s_tot = t;
+        }
+    } else if (warp == 1) {  // bounds: th = max (R+1)-th key value, w2 = max |W_j|^2; then eps
+        float th = kNegInf, w2 = 0.0f;
+        float a[LPL], w[LPL];
+#pragma unroll
+        for (int u = 0; u < LPL; ++u) {
+            const int c = lane + 32 * u;
+            a[u] = c < G ? __ldcg(A.P.pth + (size_t)i * G + c) : kNegInf;
+            w[u] = c < G ? __ldcg(A.P.pw2 + c) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < LPL; ++u) {
+            th = fmaxf(th, a[u]);
+            w2 = fmaxf(w2, w[u]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            th = fmaxf(th, __shfl_xor_sync(0xffffffffu, th, o));
+            w2 = fmaxf(w2, __shfl_xor_sync(0xffffffffu, w2, o));
+        }
+        if (lane == 0) {
+            double h2 = 0.0;
+            for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
+            s_th = th;
+            s_eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(w2) * 1.001)) * fast_gamma(A.d) * 1.01f;
+        }
+    }
+    __syncthreads();
+    FRS_FTRACE(A, 3);
 
-    // approx_(kk): the kk-th largest union key, by kk rounds of block max
+    // ---- 2a. the kk-th largest union key by a two-level tournament over the sorted lists:
+    //          warp w merges lists [32w, 32w + 32) (one per lane) into its top-kk, then warp 0
+    //          merges the 8 warp lists. Each round is one warp max (2 REDUX) + one head advance.
     const int kk = min(A.k, A.v_rows);
-    unsigned long long prev = ~0ull, kth = 0ull;
-    for (int r = 0; r < kk; ++r) {
-        unsigned long long mine = 0ull;
-#pragma unroll
-        for (int j = 0; j < kFinKPT; ++j)
-            if (kr[j] < prev && kr[j] > mine) mine = kr[j];
-        const unsigned long long best = dev::block_reduce(mine, dev::MaxU64(), rs.k);
-        if (best == 0ull) break;
-        prev = kth = best;
-    }
-    const float vk = kth ? dev::key_value(kth) : -__int_as_float(0x7f800000);
-    const float t_s = vk - 2.0f * eps - (fabsf(vk) * 0x1p-18f + 0x1p-20f);
-    // S = union keys at or above t_s; a_below = best union value left out
-    float a_below = -__int_as_float(0x7f800000);
-#pragma unroll
-    for (int j = 0; j < kFinKPT; ++j) {
-        if (kr[j] == 0ull) continue;
-        const float v = dev::key_value(kr[j]);
-        if (v >= t_s) {
-            const int pos = atomicAdd(&s_nsel, 1);
-            if (pos < kCsMax) s_sel[pos] = kr[j];
-        } else {
-            a_below = fmaxf(a_below, v);
+    {
+        const int g = warp * 32 + lane;
+        int hp = 0;
+        unsigned long long hk = g < G ? ukeys[g * R] : 0ull;
+        for (int r = 0; r < kk; ++r) {
+            const unsigned long long best = warp_max_key(hk);
+            if (lane == 0) s_wtop[warp][r] = best;
+            if (hk == best && best != 0ull) {  // keys are unique: a single owner lane
+                ++hp;
+                hk = hp < R ? ukeys[g * R + hp] : 0ull;
+            }
         }
     }
-    a_below = dev::block_reduce(a_below, dev::MaxF(), rs.f);
-    const int nsel = s_nsel;  // block_reduce synchronized
-    const int ns = min(nsel, kCsMax);
-    // canonical (descending) order, so every CTA of the row indexes S identically
-    unsigned long long my_sel = tid < ns ? s_sel[tid] : 0ull;
-    int my_rank = 0;
-    for (int c = 0; c < ns; ++c) my_rank += s_sel[c] > my_sel;
     __syncthreads();
-    if (tid < ns) s_sel[my_rank] = my_sel;
+    if (warp == 0) {
+        int hp = 0;
+        unsigned long long hk = lane < kFinThreads / 32 ? s_wtop[lane][0] : 0ull;
+        unsigned long long kth = 0ull;
+        for (int r = 0; r < kk; ++r) {
+            const unsigned long long best = warp_max_key(hk);
+            if (best == 0ull) break;
+            kth = best;
+            if (hk == best) {
+                ++hp;
+                hk = hp < kk ? s_wtop[lane][hp] : 0ull;
+            }
+        }
+        if (lane == 0) s_vk = kth;
+    }
     __syncthreads();
-
-    // ---- exact recompute of my slice S[8b, 8b + 8)
-    const int c0 = b * kCandPerFinCta, c1 = min(ns, c0 + kCandPerFinCta);
-    if (c0 < c1) {
-        {  // all candidate-row loads in flight at once: 8 rows x d/8 uint4 over the CTA
-            const int per_row = A.d / 8, total = (c1 - c0) * per_row;
-            constexpr int MAXV = 16;  // 8 rows x 512 uint4 / 256 threads for d = 4096
-            uint4 v[MAXV];
+    FRS_FTRACE(A, 8);
+    // ---- 2b. S = union keys at or above t_s (fewer than kk pool keys: t_s = -inf)
+    {
+        const float eps = s_eps;
+        const float vk = s_vk ? dev::key_value(s_vk) : kNegInf;
+        const float t_s = vk - 2.0f * eps - (fabsf(vk) * 0x1p-18f + 0x1p-20f);
+        float a_below = kNegInf;
 #pragma unroll
-            for (int u = 0; u < MAXV; ++u) {
-                const int e = tid + u * kFinThreads;
-                if (e < total) {
-                    const int c = c0 + e / per_row, off = e % per_row;
-                    v[u] = __ldg(reinterpret_cast<const uint4 *>(A.slab + (size_t)dev::key_index(s_sel[c]) * A.d) + off);
+        for (int u = 0; u < KPT; ++u) {
+            if (kr[u] == 0ull) continue;
+            const float v = dev::key_value(kr[u]);
+            if (v >= t_s) {
+                const int pos = atomicAdd(&s_nsel, 1);
+                if (pos < kCsMax) s_S[pos] = kr[u];
+            } else {
+                a_below = fmaxf(a_below, v);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a_below = fmaxf(a_below, __shfl_xor_sync(0xffffffffu, a_below, o));
+        if (lane == 0) s_abw[warp] = a_below;
+    }
+    __syncthreads();
+    FRS_FTRACE(A, 9);
+    const int nsel = s_nsel, ns = min(nsel, kCsMax);
+    if (tid < ns) {  // canonical (descending) order, so every CTA of the row indexes S identically
+        const unsigned long long mine = s_S[tid];
+        int rank = 0;
+#pragma unroll 16
+        for (int c = 0; c < kCsMax; ++c) rank += (c < ns) & (s_S[c] > mine);
+        s_sel[rank] = mine;
+    }
+    __syncthreads();
+    FRS_FTRACE(A, 4);
+
+    // ---- 3. exact recompute of my candidates c = b, b + 8, ... (round-robin over the row's
+    //         CTAs): stage the rows transposed per lane chain (wt[c][l][t] = W_c[8t + l]),
+    //         then one 8-lane group per candidate
+    const int nmine = ns > b ? (ns - b + kFinCtas - 1) / kFinCtas : 0;
+    if (nmine > 0) {
+        constexpr int TPT = 2;  // uint4 per thread per row and batch: T <= 512 in one batch
+        for (int t0 = 0; t0 < T; t0 += TPT * kFinThreads) {
+            uint4 v[kCandPerFinCta][TPT];
+#pragma unroll
+            for (int c = 0; c < kCandPerFinCta; ++c) {
+                const uint4 *row = reinterpret_cast<const uint4 *>(
+                    A.slab + (size_t)dev::key_index(s_sel[c < nmine ? b + c * kFinCtas : 0]) * A.d);
+#pragma unroll
+                for (int u = 0; u < TPT; ++u) {
+                    const int t = t0 + tid + u * kFinThreads;
+                    if (c < nmine && t < T) v[c][u] = __ldg(row + t);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < MAXV; ++u) {
-                const int e = tid + u * kFinThreads;
-                if (e < total) reinterpret_cast<uint4 *>(wrows)[e] = v[u];
-            }
-            for (int e = tid + MAXV * kFinThreads; e < total; e += kFinThreads) {  // d > 4096
-                const int c = c0 + e / per_row, off = e % per_row;
-                reinterpret_cast<uint4 *>(wrows)[e] =
-                    __ldg(reinterpret_cast<const uint4 *>(A.slab + (size_t)dev::key_index(s_sel[c]) * A.d) + off);
+            for (int c = 0; c < kCandPerFinCta; ++c) {
+#pragma unroll
+                for (int u = 0; u < TPT; ++u) {
+                    const int t = t0 + tid + u * kFinThreads;
+                    if (!(c < nmine && t < T)) continue;
+                    unsigned short *dst = wt + (size_t)c * 8 * TP + t;
+                    const uint32_t w4[4] = {v[c][u].x, v[c][u].y, v[c][u].z, v[c][u].w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        dst[(2 * q) * TP] = static_cast<unsigned short>(w4[q] & 0xffffu);
+                        dst[(2 * q + 1) * TP] = static_cast<unsigned short>(w4[q] >> 16);
+                    }
+                }
             }
         }
+        FRS_FTRACE(A, 12);
         __syncthreads();
-        if (warp_u < kCandPerFinCta * 8 / 32) {
-            const int c = c0 + tid / 8;
-            const int cc = c < c1 ? c : c0;
-            const float v = dev::dot_f32_lanes8(sh, wrows + (size_t)(cc - c0) * A.d, A.d);
-            if ((tid & 7) == 0 && c < c1) A.fin[(size_t)i * kCsMax + c] = v;
+        if (tid < ((nmine * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
+            const int cl = (tid >> 3) < nmine ? tid >> 3 : 0, l = tid & 7;
+            const float4 *hp = reinterpret_cast<const float4 *>(ht + l * TP);
+            const uint4 *wp = reinterpret_cast<const uint4 *>(wt + ((size_t)cl * 8 + l) * TP);
+            float s = 0.0f;
+            const int T8 = T / 8;
+            uint4 wv = wp[0];
+            float4 h0 = hp[0], h1 = hp[1];
+            for (int t8 = 0; t8 < T8; ++t8) {  // 8 steps per iteration; next operands prefetched
+                const int tn = t8 + 1 < T8 ? t8 + 1 : t8;
+                const uint4 wn = wp[tn];
+                const float4 g0 = hp[2 * tn], g1 = hp[2 * tn + 1];
+                const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                const uint32_t wu[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float w = __uint_as_float(q & 1 ? (wu[q >> 1] & 0xffff0000u) : (wu[q >> 1] << 16));
+                    s = __fadd_rn(s, __fmul_rn(hv[q], w));  // kernels.cpp:17-26 lane chain
+                }
+                wv = wn;
+                h0 = g0;
+                h1 = g1;
+            }
+            for (int t = T8 * 8; t < T; ++t)  // T % 8 steps
+                s = __fadd_rn(s, __fmul_rn(ht[l * TP + t],
+                                           __uint_as_float(static_cast<uint32_t>(wt[((size_t)cl * 8 + l) * TP + t]) << 16)));
+            s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));  // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7))
+            s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+            s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+            if (l == 0 && (tid >> 3) < nmine) A.fin[(size_t)i * kCsMax + b + cl * kFinCtas] = s;
         }
     }
+    FRS_FTRACE(A, 5);
     __threadfence();
     __syncthreads();
     if (tid == 0) {
@@ -775,146 +882,213 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         s_last = (old % kFinCtas) == static_cast<unsigned long long>(kFinCtas - 1);
     }
     __syncthreads();
-    if (!s_last) return;
+    if (!s_last || warp != 0) return;
     __threadfence();
 
-    // ---- selection + certification (the last CTA of this row)
-    const float a_bound = fmaxf(th, a_below);  // every row not recomputed has approx <= a_bound
-    uint32_t flags = bad ? FRS_FLAG_NONFINITE : 0u;
-    dev::load_exp_table(rs.tab);
-    __syncthreads();
-    if (warp_u == 0) {
-        const bool overflow = nsel > kCsMax;
-        float mx = -__int_as_float(0x7f800000);
-        unsigned long long best_val = 0ull;
-        for (int c = tid; c < ns; c += 32) {
-            const float l = A.fin[(size_t)i * kCsMax + c];
-            const float x = __fdiv_rn(l, A.temperature);
-            mx = fmaxf(mx, x);
-            const unsigned long long vkey = dev::value_key(l, dev::key_index(s_sel[c]));
-            best_val = vkey > best_val ? vkey : best_val;
-            s_ek[c] = __float_as_uint(x);  // stash x; replaced by the e-key below
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        best_val = warp_max_u64(best_val);
-        bool cert = !bad && !overflow && ns >= kk;
-        if (A.argmax) {
-            // every non-recomputed row: exact <= a_bound + eps < the best exact logit
-            if (tid == 0) {
-                const float lb = dev::key_value(best_val);
-                cert = cert && (a_bound + eps < lb || a_bound == -__int_as_float(0x7f800000));
-                s_ek[0] = best_val;
-                s_cert = cert;
-            }
-        } else {
-            __syncwarp();
-            for (int c = tid; c < ns; c += 32) {
-                const float x = __uint_as_float(static_cast<uint32_t>(s_ek[c]));
-                s_ek[c] = dev::prob_key(dev::expf_glibc(__fsub_rn(x, mx), rs.tab), dev::key_index(s_sel[c]));
-            }
-            __syncwarp();
-            const int want = min(ns, kk + 1);
-            for (int r = 0; r < want; ++r) {  // selection sort of the leading (kk + 1) e-keys
-                unsigned long long best = 0ull;
-                int where = -1;
-                for (int c = r + tid; c < ns; c += 32)
-                    if (s_ek[c] > best) {
-                        best = s_ek[c];
-                        where = c;
-                    }
-                const unsigned long long wbest = warp_max_u64(best);
-                const unsigned ball = __ballot_sync(0xffffffffu, where >= 0 && best == wbest);
-                const int w = __shfl_sync(0xffffffffu, where, __ffs(ball) - 1);
-                if (tid == 0 && w != r) {
-                    const unsigned long long tmp = s_ek[r];
-                    s_ek[r] = s_ek[w];
-                    s_ek[w] = tmp;
-                }
-                __syncwarp();
-            }
-            if (tid == 0) {
-                // near ties (within 4 ulps) among the selected and at the k boundary: the
-                // reference's (prob, index) order could depend on the exact denominator
-                for (int r = 0; cert && r + 1 < want; ++r) {
-                    const float ea = __uint_as_float(static_cast<uint32_t>(s_ek[r] >> 32));
-                    const float eb = __uint_as_float(static_cast<uint32_t>(s_ek[r + 1] >> 32));
-                    if (ea != eb && ea <= eb * (1.0f + 0x1p-21f)) cert = false;
-                }
-                if (cert && a_bound != -__int_as_float(0x7f800000)) {
-                    const float x_ub = __fdiv_ru(a_bound + eps, A.temperature) * (1.0f + 0x1p-20f) + 0x1p-20f;
-                    if (!(x_ub < mx)) {
-                        cert = false;
-                    } else {
-                        const float e_ub = dev::expf_glibc(x_ub - mx, rs.tab) * (1.0f + 0x1p-20f);
-                        const float e_k = __uint_as_float(static_cast<uint32_t>(s_ek[kk - 1] >> 32));
-                        if (!(e_ub * (1.0f + 0x1p-21f) < e_k)) cert = false;
-                    }
-                }
-                s_cert = cert;
-                s_mx = mx;
-            }
-        }
+    // ---- 4. the last CTA of the row, warp 0: selection + certification
+    float a_bound = s_th;  // every row not recomputed has approx <= a_bound
+    int any_bad = 0;
+    for (int w = 0; w < kFinThreads / 32; ++w) {
+        a_bound = fmaxf(a_bound, s_abw[w]);
+        any_bad |= s_badw[w];
     }
-    __syncthreads();
-    if (s_cert) {
-        if (tid == 0) {
-            if (A.argmax) {
-                const unsigned long long best = s_ek[0];
-                A.out_full[i] = A.id_offset + dev::key_index(best);
-                if (A.out_prob) A.out_prob[i] = dev::key_value(best);
-            } else {
-                const float mx = s_mx;
-                // tot = sum exp(x_j - M) in the approximate domain; rescale to the exact max
-                const double total = tot * exp(static_cast<double>(mmax) - static_cast<double>(mx));
-                const float inv = __double2float_rn(1.0 / total);
-                for (int r = 0; r < kk; ++r) {
-                    const int j = dev::key_index(s_ek[r]);
-                    A.out_ridx[(size_t)i * A.k + r] = j;
-                    A.out_full[(size_t)i * A.k + r] = A.ordered ? A.ordered[j] : j;
-                    A.out_prob[(size_t)i * A.k + r] =
-                        __fmul_rn(__uint_as_float(static_cast<uint32_t>(s_ek[r] >> 32)), inv);
-                }
-                for (int r = kk; r < A.k; ++r) {
-                    A.out_ridx[(size_t)i * A.k + r] = -1;
-                    A.out_full[(size_t)i * A.k + r] = -1;
-                    A.out_prob[(size_t)i * A.k + r] = 0.0f;
-                }
-                if (A.out_rowmax) A.out_rowmax[i] = mx;
-                if (A.out_total) A.out_total[i] = total;
-            }
-            if (A.out_flags) A.out_flags[i] = flags;
-        }
-        return;
-    }
-    // ---- fallback: the exact full row in this CTA (bit-identical to the EXACT path)
-    float *L = A.scratch + (size_t)i * 2 * A.v_rows;
-    if (!bad) {
-        fallback_exact_logits(sh, A.slab, A.v_rows, A.d, L);
-        flags |= FRS_FLAG_RECOMPUTED;
-    } else {
-        for (int j = tid; j < A.v_rows; j += nt) L[j] = __int_as_float(0x7fc00000);
-    }
-    __syncthreads();
+    const float eps = s_eps;
+    uint32_t why = (nsel > kCsMax || ns < kk) ? FRS_FLAG_CERT_OVERFLOW : 0u;
+    if (any_bad) why |= FRS_FLAG_NONFINITE;
+    const bool have0 = lane < ns, have1 = lane + 32 < ns;
+    const float l0 = have0 ? __ldcg(A.fin + (size_t)i * kCsMax + lane) : kNegInf;  // written by the row's
+    const float l1 = have1 ? __ldcg(A.fin + (size_t)i * kCsMax + lane + 32) : kNegInf;  // other CTAs: L2
+    const int j0 = have0 ? dev::key_index(s_sel[lane]) : 0, j1 = have1 ? dev::key_index(s_sel[lane + 32]) : 0;
     if (A.argmax) {
-        unsigned long long cand = 0ull;
-        for (int j = tid; j < A.v_rows; j += nt) {
-            const unsigned long long kk2 = dev::value_key(L[j], j);
-            cand = kk2 > cand ? kk2 : cand;
+        unsigned long long bv = 0ull;
+        if (have0) bv = dev::value_key(l0, j0);
+        if (have1) {
+            const unsigned long long k1 = dev::value_key(l1, j1);
+            bv = k1 > bv ? k1 : bv;
         }
-        const unsigned long long best = dev::block_reduce(cand, dev::MaxU64(), rs.k);
-        if (tid == 0) {
+        const unsigned long long best = warp_max_key(bv);
+        const float lb = dev::key_value(best);
+        if (!(a_bound + eps < lb || a_bound == kNegInf)) why |= FRS_FLAG_CERT_BOUND;
+        if (why) {
+            if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
+            return;
+        }
+        if (lane == 0) {
             A.out_full[i] = A.id_offset + dev::key_index(best);
-            if (A.out_prob) A.out_prob[i] = L[dev::key_index(best)];
-            if (A.out_flags) A.out_flags[i] = flags;
+            if (A.out_prob) A.out_prob[i] = lb;
+            if (A.out_flags) A.out_flags[i] = 0u;
         }
+        FRS_FTRACE(A, 7);
         return;
     }
-    const uint32_t f2 = dev::softmax_topk_row(L, A.v_rows, A.k, A.temperature, A.ordered, L + A.v_rows,
-                                              A.out_ridx + (size_t)i * A.k, A.out_full + (size_t)i * A.k,
-                                              A.out_prob + (size_t)i * A.k, A.out_rowmax ? A.out_rowmax + i : nullptr,
-                                              A.out_total ? A.out_total + i : nullptr, rs);
-    if (tid == 0 && A.out_flags) A.out_flags[i] = flags | f2;
+    s_tab[lane] = dev::kExp2fTable[lane];
+    __syncwarp();
+    const unsigned long long *tab = s_tab;
+    const float x0 = __fdiv_rn(l0, A.temperature), x1 = __fdiv_rn(l1, A.temperature);
+    float mx = fmaxf(x0, x1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const unsigned long long e0 = have0 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x0, mx), tab), j0) : 0ull;
+    const unsigned long long e1 = have1 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x1, mx), tab), j1) : 0ull;
+    // rank of each e-key among the ns (distinct: the index is part of the key)
+    int r0 = 0, r1 = 0;
+    for (int c = 0; c < ns; ++c) {
+        const unsigned long long o = __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31);
+        r0 += o > e0;
+        r1 += o > e1;
+    }
+    if (have0) s_sorted[r0] = e0;
+    if (have1) s_sorted[r1] = e1;
+    __syncwarp();
+    const int want = min(ns, kk + 1);
+    // near ties (within 4 ulps) among the selected and at the k boundary: the reference's
+    // (prob, index) order could depend on the exact denominator
+    bool tie = false;
+    if (lane + 1 < want) {
+        const float ea = __uint_as_float(static_cast<uint32_t>(s_sorted[lane] >> 32));
+        const float eb = __uint_as_float(static_cast<uint32_t>(s_sorted[lane + 1] >> 32));
+        tie = ea != eb && ea <= eb * (1.0f + 0x1p-21f);
+    }
+    if (__any_sync(0xffffffffu, tie)) why |= FRS_FLAG_CERT_TIE;
+    if (!why && a_bound != kNegInf) {  // every non-recomputed row stays strictly below the k-th
+        const float x_ub = __fdiv_ru(a_bound + eps, A.temperature) * (1.0f + 0x1p-20f) + 0x1p-20f;
+        if (!(x_ub < mx)) {
+            why |= FRS_FLAG_CERT_BOUND;
+        } else {
+            const float e_ub = dev::expf_glibc(x_ub - mx, tab) * (1.0f + 0x1p-20f);
+            const float e_k = __uint_as_float(static_cast<uint32_t>(s_sorted[kk - 1] >> 32));
+            if (!(e_ub * (1.0f + 0x1p-21f) < e_k)) why |= FRS_FLAG_CERT_BOUND;
+        }
+    }
+    if (why) {
+        if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
+        return;
+    }
+    // tot = sum exp(x_j - M) over the approximate logits; rescale to the exact max
+    const double total = s_tot * exp(static_cast<double>(s_mmax) - static_cast<double>(mx));
+    const float inv = __double2float_rn(1.0 / total);
+    if (lane < A.k) {
+        const size_t o = (size_t)i * A.k + lane;
+        if (lane < kk) {
+            const unsigned long long key = s_sorted[lane];
+            const int j = dev::key_index(key);
+            A.out_ridx[o] = j;
+            A.out_full[o] = A.ordered ? A.ordered[j] : j;
+            A.out_prob[o] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(key >> 32)), inv);
+        } else {
+            A.out_ridx[o] = -1;
+            A.out_full[o] = -1;
+            A.out_prob[o] = 0.0f;
+        }
+    }
+    if (A.k > 32) {  // k up to 64
+        const int r = lane + 32;
+        if (r < A.k) {
+            const size_t o = (size_t)i * A.k + r;
+            if (r < kk) {
+                const unsigned long long key = s_sorted[r];
+                const int j = dev::key_index(key);
+                A.out_ridx[o] = j;
+                A.out_full[o] = A.ordered ? A.ordered[j] : j;
+                A.out_prob[o] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(key >> 32)), inv);
+            } else {
+                A.out_ridx[o] = -1;
+                A.out_full[o] = -1;
+                A.out_prob[o] = 0.0f;
+            }
+        }
+    }
+    if (lane == 0) {
+        if (A.out_rowmax) A.out_rowmax[i] = mx;
+        if (A.out_total) A.out_total[i] = total;
+        if (A.out_flags) A.out_flags[i] = 0u;
+    }
+    FRS_FTRACE(A, 7);
+}
+
+// Grid-wide exact fallback for the rows the finalize could not certify. Launched after every
+// FAST finalize (programmatic dependent launch), it exits at once when the queue is empty.
+// Otherwise every CTA computes exact dot_f32 logits for its slice of slab rows of each queued
+// hidden row — one thread per slab row carrying the reference's 8 lane chains, 16-byte slab
+// loads — and the last CTA to finish runs the exact softmax + top-k (or argmax) of those rows,
+// bit-identical to the EXACT path, then empties the queue.
+__global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
+    extern __shared__ uint8_t fbs_raw[];
+    float *sh = reinterpret_cast<float *>(fbs_raw);  // [d]
+    __shared__ dev::ReduceScratch rs;
+    __shared__ int s_last;
+    griddep_wait();
+    const unsigned nfb = *reinterpret_cast<volatile unsigned *>(A.fb_count);
+    if (nfb == 0) return;
+    const int tid = threadIdx.x, G = gridDim.x;
+    const int T = A.d >> 3;  // d % 8 == 0 on the FAST path
+    for (unsigned f = 0; f < nfb; ++f) {
+        const int i = static_cast<int>(A.fb_rows[f] & 0xffffu);
+        float *L = A.scratch + (size_t)i * 2 * A.v_rows;
+        __syncthreads();
+        for (int e = tid; e < A.d; e += blockDim.x) sh[e] = A.h[(size_t)i * A.d + e];
+        __syncthreads();
+        for (int j = blockIdx.x * blockDim.x + tid; j < A.v_rows; j += G * blockDim.x) {
+            const uint4 *w = reinterpret_cast<const uint4 *>(A.slab + (size_t)j * A.d);
+            float c[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+            for (int t = 0; t < T; ++t) {
+                const uint4 u = __ldg(w + t);
+                const float4 h0 = reinterpret_cast<const float4 *>(sh)[2 * t];
+                const float4 h1 = reinterpret_cast<const float4 *>(sh)[2 * t + 1];
+                const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int l = 0; l < 8; ++l) {
+                    const float wv = __uint_as_float(l & 1 ? (uw[l >> 1] & 0xffff0000u) : (uw[l >> 1] << 16));
+                    c[l] = __fadd_rn(c[l], __fmul_rn(hv[l], wv));
+                }
+            }
+            L[j] = __fadd_rn(__fadd_rn(__fadd_rn(c[0], c[1]), __fadd_rn(c[2], c[3])),
+                             __fadd_rn(__fadd_rn(c[4], c[5]), __fadd_rn(c[6], c[7])));  // kernels.cpp:27
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned long long old = atomicAdd(A.fb_arrive, 1ull);
+        s_last = (old % G) == static_cast<unsigned long long>(G - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (unsigned f = 0; f < nfb; ++f) {
+        const uint32_t ent = A.fb_rows[f];
+        const int i = static_cast<int>(ent & 0xffffu);
+        const uint32_t flags = FRS_FLAG_RECOMPUTED | (ent >> 16);
+        float *L = A.scratch + (size_t)i * 2 * A.v_rows;
+        __syncthreads();
+        if (A.argmax) {
+            unsigned long long cand = 0ull;
+            int bad = 0;
+            for (int j = tid; j < A.v_rows; j += blockDim.x) {
+                if (!isfinite(L[j])) bad = 1;
+                const unsigned long long kk2 = dev::value_key(L[j], j);
+                cand = kk2 > cand ? kk2 : cand;
+            }
+            const unsigned long long best = dev::block_reduce(cand, dev::MaxU64(), rs.k);
+            bad = dev::block_reduce(bad, dev::OrI(), rs.i);
+            if (tid == 0) {
+                A.out_full[i] = A.id_offset + dev::key_index(best);
+                if (A.out_prob) A.out_prob[i] = L[dev::key_index(best)];
+                if (A.out_flags) A.out_flags[i] = flags | (bad ? FRS_FLAG_NONFINITE : 0u);
+            }
+            continue;
+        }
+        const uint32_t f2 = dev::softmax_topk_row(L, A.v_rows, A.k, A.temperature, A.ordered, L + A.v_rows,
+                                                  A.out_ridx + (size_t)i * A.k, A.out_full + (size_t)i * A.k,
+                                                  A.out_prob + (size_t)i * A.k,
+                                                  A.out_rowmax ? A.out_rowmax + i : nullptr,
+                                                  A.out_total ? A.out_total + i : nullptr, rs);
+        if (tid == 0 && A.out_flags) A.out_flags[i] = flags | f2;
+    }
+    __syncthreads();
+    if (tid == 0) *A.fb_count = 0u;
 }
 
 // ------------------------------------------------------------------ host side
@@ -944,6 +1118,8 @@ int make_map(CUtensorMap *map, const void *base, int rows, int cols, int box_row
     if (r != CUDA_SUCCESS) return fail(FRS_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
     return FRS_OK;
 }
+
+constexpr size_t kCtrBytes = 64 * 8 + 8 + 4 + 64 * 4;
 
 struct FastWs {
     __nv_bfloat16 *hs;
@@ -981,12 +1157,12 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.P.trace = nullptr;
     static const bool tracing = std::getenv("FRS_TRACE") != nullptr;
     if (tracing) {
-        if ((st = ctx->trace.ensure((size_t)G * 16 * 8))) return st;
+        if ((st = ctx->trace.ensure((size_t)(G * 16 + 64 * kFinCtas * 16) * 8))) return st;
         w.P.trace = static_cast<unsigned long long *>(ctx->trace.ptr);
     }
-    if (!ctx->fast_ctr.ptr) {
-        if ((st = ctx->fast_ctr.ensure(64 * sizeof(unsigned long long)))) return st;
-        FRS_CUDA_TRY(cudaMemset(ctx->fast_ctr.ptr, 0, 64 * sizeof(unsigned long long)));
+    if (!ctx->fast_ctr.ptr) {  // row_ctr[64] u64 | fb_arrive u64 | fb_count u32 | fb_rows[64] u32
+        if ((st = ctx->fast_ctr.ensure(kCtrBytes))) return st;
+        FRS_CUDA_TRY(cudaMemset(ctx->fast_ctr.ptr, 0, kCtrBytes));
     }
     return FRS_OK;
 }
@@ -1014,7 +1190,8 @@ int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapH, 
 
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     auto kern = k_fast_finalize;
-    const size_t smem = (size_t)((A.d + 7) & ~7) * 4 + (size_t)kCandPerFinCta * A.d * 2 + 64;
+    const int TP = A.d / 8 + 8;
+    const size_t smem = (size_t)A.P.G * R * 8 + (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 2 + 64;
     if (smem > ctx->smem_optin) return fail(FRS_ENOTSUP, "FAST finalize: hidden_dim too large");
     FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg{};
@@ -1028,6 +1205,17 @@ int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
+    ++ctx->launches;
+    // the grid-wide exact fallback: exits at once unless the finalize queued a row
+    auto fb = k_fast_fallback;
+    const int fsmem = ((A.d + 7) & ~7) * 4;
+    FRS_CUDA_TRY(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
+    cfg.gridDim = dim3(ctx->sm_count);
+    cfg.blockDim = dim3(kFbThreads);
+    cfg.dynamicSmemBytes = fsmem;
+    static const bool no_pdl_fb = std::getenv("FRS_EXP_NO_PDL_FB") != nullptr;  // EXPERIMENT
+    if (no_pdl_fb) cfg.numAttrs = 0;
+    FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, fb, A));
     ++ctx->launches;
     return FRS_OK;
 }
@@ -1051,12 +1239,15 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     if (!argmax && k > 64) return fail(FRS_ENOTSUP, "FAST draft head: k <= 64");
     const int NP = n <= 16 ? 16 : (n <= 32 ? 32 : 64);
     const int G = ctx->sm_count;
-    if (G * R > kFinThreads * kFinKPT) return fail(FRS_ENOTSUP, "FAST head: too many SMs for the candidate merge");
+    if (G > kMaxLists) return fail(FRS_ENOTSUP, "FAST head: too many SMs for the candidate merge");
     FastWs w;
     int st = fast_workspace(ctx, NP, d, n, v_rows, w);
     if (st) return st;
     CUtensorMap mapW, mapH;
-    if ((st = make_map(&mapW, W, v_rows, d, BM))) return st;
+    static const bool exp_tiled = std::getenv("FRS_EXPERIMENT_TILED") != nullptr;
+    w.P.tiled = exp_tiled && d % 64 == 0 && v_rows % CH == 0;
+    if ((st = w.P.tiled ? make_map(&mapW, W, v_rows / CH * (d / 64) * CH, 64, CH) : make_map(&mapW, W, v_rows, d, CH)))
+        return st;
     if ((st = make_map(&mapH, w.hs, 2 * NP, d, 2 * NP))) return st;
 
     timing_begin(ctx, s);
@@ -1065,9 +1256,19 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
         cudaStream_t s;
         ~EndTiming() { timing_end(c, s); }
     } end_timing{ctx, s};
-    k_hsplit<<<std::min(ctx->sm_count, (NP * d + 255) / 256), 256, 0, s>>>(h, n, d, NP, w.hs);
-    ++ctx->launches;
-    FRS_CUDA_TRY(cudaGetLastError());
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(std::min(ctx->sm_count, (NP * d + 255) / 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs));
+        ++ctx->launches;
+    }
     const float inv_t = 1.0f / temperature;
     if (argmax) {
         st = NP == 16   ? launch_main<16, false>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s)
@@ -1089,6 +1290,9 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     A.P = w.P;
     A.fin = w.fin;
     A.row_ctr = static_cast<unsigned long long *>(ctx->fast_ctr.ptr);
+    A.fb_arrive = A.row_ctr + 64;
+    A.fb_count = reinterpret_cast<unsigned *>(A.row_ctr + 65);
+    A.fb_rows = reinterpret_cast<uint32_t *>(A.fb_count + 1);
     A.scratch = w.scratch;
     A.out_ridx = out_ridx;
     A.out_full = out_full;
@@ -1117,8 +1321,9 @@ int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float 
     FRS_CUDA_TRY(cudaMemcpy(pth, w.P.pth, sizeof(float) * n * G, cudaMemcpyDeviceToHost));
     FRS_CUDA_TRY(cudaMemcpy(pkey, w.P.pkey, sizeof(unsigned long long) * n * G * R, cudaMemcpyDeviceToHost));
     FRS_CUDA_TRY(cudaMemcpy(pw2, w.P.pw2, sizeof(float) * G, cudaMemcpyDeviceToHost));
-    if (w.P.trace && ctx->trace.bytes >= (size_t)G * 16 * 8) {  // trailing [G][16] stamps
-        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * G * R, w.P.trace, (size_t)G * 16 * 8, cudaMemcpyDeviceToHost));
+    if (w.P.trace) {  // trailing [G][16] main stamps, then [64][kFinCtas][8] finalize stamps
+        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * G * R, w.P.trace, (size_t)(G * 16 + 64 * kFinCtas * 16) * 8,
+                                cudaMemcpyDeviceToHost));
     }
     return FRS_OK;
 }

@@ -1,0 +1,81 @@
+#!/usr/bin/env python3
+"""Per-CTA globaltimer trace of the FAST main kernel (FRS_TRACE=1 must be set before the
+library allocates its workspace). Prints, per stamp slot, min/median/max microseconds
+relative to the earliest slot-0 stamp across CTAs.
+
+  FRS_TRACE=1 python tools/fast_trace.py [--v-sub 32768] [--rows 10]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2502_14856_b200 import api, _lib  # noqa: E402
+
+SLOTS = {0: "setup done", 1: "producer: before griddep_wait", 9: "producer: after griddep_wait",
+         3: "mma: first stage full", 2: "producer: all TMA issued", 4: "mma: all issued", 8: "norm warps done",
+         10: "epi: first tfull wait", 11: "epi: first tile ready", 13: "epi: loop done", 5: "cand published",
+         7: "cta end"}
+FSLOTS = {0: "fin start", 1: "fin h loaded", 2: "fin after griddep_wait", 3: "fin partials merged",
+          4: "fin S selected", 5: "fin recompute done", 6: "fin last: certified?", 7: "fin last: written",
+          8: "fin v' ranked", 9: "fin S collected",
+          12: "fin cand rows staged"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--v-sub", type=int, default=32768)
+    ap.add_argument("--rows", type=int, default=10)
+    ap.add_argument("--d", type=int, default=4096)
+    ap.add_argument("--reps", type=int, default=5)
+    a = ap.parse_args()
+    assert os.environ.get("FRS_TRACE"), "set FRS_TRACE=1"
+    dev = torch.device("cuda", 0)
+    ctx = api.Context(0)
+    g = torch.Generator(device=dev).manual_seed(1)
+    W = (torch.randn(a.v_sub, a.d, generator=g, device=dev) * 0.02).float()
+    head = api.restrict_lm_head(ctx, W, api.RankedSubset(a.v_sub, np.arange(a.v_sub)), dtype="bf16")
+    h = torch.randn(a.rows, a.d, generator=g, device=dev)
+    out = api.draft_head_topk(ctx, h, head, 10, mode="fast")
+    G = ctx.sm_count
+    res = []
+    for _ in range(a.reps):
+        api.draft_head_topk(ctx, h, head, 10, mode="fast", out=out)
+        torch.cuda.synchronize()
+        n = a.rows
+        pm, ps, pth = (np.empty(n * G, np.float32) for _ in range(3))
+        pkey = np.empty(n * G * 8 + G * 16 + 64 * 8 * 16, np.uint64)
+        pw2 = np.empty(G, np.float32)
+        _lib.check(_lib.lib().frs_debug_fast_partials(ctx.handle, n, a.d, pm.ctypes.data, ps.ctypes.data,
+                                                      pth.ctypes.data, pkey.ctypes.data, pw2.ctypes.data))
+        st = pkey[n * G * 8:n * G * 8 + G * 16].reshape(G, 16).astype(np.int64)
+        ft = pkey[n * G * 8 + G * 16:].reshape(64 * 8, 16).astype(np.int64)[: n * 8]
+        t0 = st[:, 0][st[:, 0] > 0].min()
+        row = {}
+        for s, name in SLOTS.items():
+            v = st[:, s]
+            v = v[v > 0]
+            if v.size:
+                us = (v - t0) / 1000.0
+                row[f"{s:02d} {name}"] = [round(float(us.min()), 2), round(float(np.median(us)), 2),
+                                          round(float(us.max()), 2)]
+        for s, name in FSLOTS.items():
+            v = ft[:, s]
+            v = v[v > 0]
+            if v.size:
+                us = (v - t0) / 1000.0
+                row[f"F{s} {name}"] = [round(float(us.min()), 2), round(float(np.median(us)), 2),
+                                       round(float(us.max()), 2)]
+        res.append(row)
+    for k in res[-1]:
+        print(k.ljust(40), res[-1][k])
+    print(json.dumps(res[-1]))
+
+
+if __name__ == "__main__":
+    main()
