@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfrspec_cuda.so")
+LIB_PATH = os.environ.get("FRS_LIB_PATH") or os.path.join(HERE, "libfrspec_cuda.so")  # override: A/B runs
 
 FRS_OK, FRS_EINVAL, FRS_ECAPACITY, FRS_EDATA, FRS_ELOGIC, FRS_ECUDA, FRS_ENCCL, FRS_ENOTSUP = range(8)
 DTYPE_F32, DTYPE_BF16 = 0, 1

@@ -2,32 +2,39 @@
 // statistics and per-CTA top-R candidate tracking, then an exact-recompute finalize that
 // certifies the top-k ids against the reference arithmetic.
 //
-// Per call (one draft level, or one verify head), three kernels on one stream, chained with
-// programmatic dependent launch so each kernel's prologue overlaps its predecessor's tail:
+// Per call (one draft level, or one verify head), four kernels on one stream, chained with
+// programmatic dependent launch (PDL) so each kernel's prologue overlaps its predecessor's tail:
 //
-//  k_hsplit      h[n x d] fp32 -> hs[2NP x d] bf16 with rows [0,NP) = hi = bf16(h) and
-//                rows [NP,2NP) = lo = bf16(h - hi): h = hi + lo + O(2^-16 |h|).
-//  k_fast_main   persistent, one CTA per SM, each CTA owns a contiguous range of 128-row slab
-//                tiles. Warp 0 streams (slab tile k-block, hs k-block) pairs with TMA
-//                (SWIZZLE_128B, 16 KB + 2NP*128 B per stage) into a multi-stage mbarrier ring;
-//                warp 1 issues tcgen05.mma (M=128 slab rows, N=2NP, K=16, bf16 -> fp32 in TMEM,
-//                double-buffered accumulator); warps 2-3 read the same smem stages to accumulate
-//                each slab row's squared L2 norm (for the error bound, always fresh); warps 4-7
-//                drain TMEM (tcgen05.ld 32x32b), form logit = hi + lo per (slab row, hidden row),
-//                update the online (max, sum-exp) statistics and a per-warp top-(R+1) list in
-//                shared memory. Logits never leave the SM. Each CTA publishes (m, s), its top-R
-//                candidate keys, the (R+1)-th value (bound for all its other rows) and max |W_j|^2.
-//  k_fast_finalize  per hidden row: merge the CTA partials, take the CS best candidates by
-//                approximate logit, recompute them EXACTLY (dot_f32 order, glibc expf), select
-//                the top-k by (prob desc, index asc) and certify that no other row can enter:
-//                every non-candidate's exact logit is <= bound + eps with eps a rigorous
-//                error bound (reference dot_f32 error + tensor-core accumulation + hi/lo
-//                truncation, Cauchy-Schwarz with |h|_2 |W_j|_2). Rows that cannot be certified
-//                (near-ties within 4 ulps, or a bound too loose) fall back to the exact
-//                full-row computation inside the same kernel, so ids are always the reference's.
+//  k_hsplit         the hi / lo bf16 split of the hidden rows (tiny).
+//  k_fast_main      persistent, one CTA per SM; each CTA owns a contiguous run of 32-row slab
+//                   chunks (tiles of up to 128 rows), so no CTA streams more than one chunk
+//                   beyond the average. Its B operand is hs[2NP x d] bf16 written by k_hsplit
+//                   (rows [0,NP) = hi = bf16(h), rows [NP,2NP) = lo = bf16(h - hi):
+//                   h = hi + lo + O(2^-16 |h|)); the first ring pass of slab tiles is issued
+//                   before waiting for that grid.
+//                   Warp 0 streams (slab k-block, hs k-block) stages with TMA (SWIZZLE_128B,
+//                   32-row boxes) into a multi-stage mbarrier ring; warp 1 issues tcgen05.mma
+//                   (M=128 slab rows, N=2NP, K=16, bf16 -> fp32 in TMEM, double-buffered
+//                   accumulator); warps 2-3 accumulate each slab row's squared L2 norm from the
+//                   same stages (for the error bound, always fresh); warps 4-11 drain TMEM
+//                   (tcgen05.ld 32x32b), form logit = hi + lo per (slab row, hidden row), update
+//                   the online (max, sum-exp) statistics and per-thread top-2 keys. Logits never
+//                   leave the SM. Each CTA publishes (m, s), its top-R candidate keys per hidden
+//                   row, the bound for all its other rows and max |W_j|^2.
+//  k_fast_finalize  grid (n, 8) in clusters of 8 (one cluster per hidden row): merge the CTA
+//                   partials, find the kk-th largest candidate key (two-level tournament), take
+//                   S = {keys >= v_kk - 2 eps - margin}, recompute S EXACTLY (dot_f32 order;
+//                   results gathered in the cluster leader through DSMEM), select the top-k by
+//                   (prob desc, index asc) with the glibc expf port, and certify that no other
+//                   row can enter: every row outside S has exact logit <= bound + eps, eps a
+//                   rigorous error bound (reference dot_f32 error + tensor-core accumulation +
+//                   hi/lo truncation, Cauchy-Schwarz with |h|_2 |W_j|_2). Rows that cannot be
+//                   certified (near-ties within 4 ulps, bound too loose, S overflow) are queued.
+//  k_fast_fallback  grid-wide exact recompute of the queued rows (bit-identical to the EXACT
+//                   path); exits at once when the queue is empty (the common case).
 //
 // Memory bound: the slab is read exactly once per call (268,435,456 B for V_sub=32768,
-// d=4096); hs (<= 1 MB) and candidate rows are L2 traffic.
+// d=4096); hs (<= 1 MB), partials and candidate rows are L2 traffic.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -36,6 +43,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "frs_common.cuh"
 #include "frs_device.cuh"
@@ -97,6 +106,11 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -148,7 +162,6 @@ struct Partials {
     float *pw2;                // [G] max squared L2 norm of the CTA's slab rows
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
-    int tiled;                 // EXPERIMENT: W map addresses [chunk][kb][32 x 64] pieces
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -162,21 +175,32 @@ __device__ __forceinline__ unsigned long long gtimer() {
     } while (0)
 
 // hs rows [0,NP) = bf16(h), rows [NP,2NP) = bf16(h - bf16(h)); padded rows are zero.
-__global__ void __launch_bounds__(256) k_hsplit(const float *__restrict__ h, int n, int d, int NP,
-                                                __nv_bfloat16 *__restrict__ hs) {
+// 128 threads, no shared memory: it co-resides with the main kernel's CTAs, which PDL lets
+// launch (and run their prologue and first slab loads) while this grid is still running.
+__global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int n, int d, int NP,
+                                                __nv_bfloat16 *__restrict__ hs, unsigned long long *xtrace) {
     // launched programmatically after whatever precedes it on the stream: wait for it (h is
     // final, the previous call's fallback queue is drained), then let the main kernel launch
     griddep_wait();
     griddep_launch();
-    const int total = NP * d;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-        const int i = idx / d, c = idx - i * d;
-        const float x = i < n ? h[(size_t)i * d + c] : 0.0f;
-        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-        const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
-        hs[(size_t)i * d + c] = hi;
-        hs[(size_t)(NP + i) * d + c] = lo;
+    if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[0] = gtimer();
+    const int total4 = NP * d / 4;  // d % 8 == 0 on the FAST path
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total4; idx += gridDim.x * blockDim.x) {
+        const int e = idx * 4, i = e / d, c = e - i * d;
+        const float4 x = i < n ? __ldg(reinterpret_cast<const float4 *>(h + (size_t)i * d + c))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        const __nv_bfloat162 h01 = __floats2bfloat162_rn(x.x, x.y), h23 = __floats2bfloat162_rn(x.z, x.w);
+        const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+        const __nv_bfloat162 l01 = __floats2bfloat162_rn(x.x - f01.x, x.y - f01.y);
+        const __nv_bfloat162 l23 = __floats2bfloat162_rn(x.z - f23.x, x.w - f23.y);
+        __nv_bfloat162 *hi = reinterpret_cast<__nv_bfloat162 *>(hs + (size_t)i * d + c);
+        __nv_bfloat162 *lo = reinterpret_cast<__nv_bfloat162 *>(hs + (size_t)(NP + i) * d + c);
+        hi[0] = h01;
+        hi[1] = h23;
+        lo[0] = l01;
+        lo[1] = l23;
     }
+    if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[1] = gtimer();
 }
 
 template <int NP, bool SOFTMAX>
@@ -222,7 +246,8 @@ __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k)
 
 template <int NP, bool SOFTMAX>
 __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
-    k_fast_main(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapH, int n,
+    k_fast_main(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapW32,
+                const __grid_constant__ CUtensorMap mapH, int n,
                 int v_rows, int d, float inv_t, Partials P) {
     using C = MainCfg<NP, SOFTMAX>;
     constexpr int N = C::N, STAGES = C::STAGES, RPW = C::RPW, TOPK = C::TOPK, EPI = C::EPI_WARPS;
@@ -268,6 +293,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&mapW);
+        prefetch_tmap(&mapW32);
         prefetch_tmap(&mapH);
     }
     tc_fence_before();
@@ -281,6 +307,9 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
+            // Straight-line issue loop: the producer thread's issue rate is on the critical
+            // path (a lambda-based version of this loop streamed 15 % slower). A full tile is
+            // one 128-row box; a short tile (the CTA's last) is loaded as 32-row boxes.
             const uint64_t pol_w = policy_evict_first(), pol_h = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
@@ -290,11 +319,14 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], nch * (CH * BK * 2) + C::B_BYTES);
-                    for (int c = 0; c < nch; ++c)
-                        tma_load_2d(sA + stage * C::A_BYTES + c * (CH * BK * 2), &mapW, &full[stage],
-                                    P.tiled ? 0 : kb * BK,
-                                    P.tiled ? ((r0 / CH + c) * KB + kb) * CH : r0 + c * CH, pol_w);
-                    if (!waited) {  // hs is produced by k_hsplit (programmatic dependency)
+                    if (nch == CPT) {
+                        tma_load_2d(sA + stage * C::A_BYTES, &mapW, &full[stage], kb * BK, r0, pol_w);
+                    } else {
+                        for (int c = 0; c < nch; ++c)
+                            tma_load_2d(sA + stage * C::A_BYTES + c * (CH * BK * 2), &mapW32, &full[stage], kb * BK,
+                                        r0 + c * CH, pol_w);
+                    }
+                    if (!waited) {  // hs is written by k_hsplit (programmatic dependency)
                         FRS_TRACE(P, 1);
                         griddep_wait();
                         FRS_TRACE(P, 9);
@@ -618,7 +650,9 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     __shared__ double s_hn2[kFinThreads / 32], s_tot;
     __shared__ float s_mmax, s_th, s_eps, s_abw[kFinThreads / 32];
     __shared__ unsigned long long s_vk, s_wtop[kFinThreads / 32][kMaxK];
-    __shared__ int s_nsel, s_last, s_badw[kFinThreads / 32];
+    __shared__ float s_fin[kCsMax];             // exact logits of S (cluster leader; DSMEM-written)
+    __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
+    __shared__ int s_nsel, s_badw[kFinThreads / 32];
     FRS_FTRACE(A, 0);
     griddep_launch();  // the fallback grid may become resident now; it waits for this grid
 
@@ -871,21 +905,24 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));  // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7))
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
-            if (l == 0 && (tid >> 3) < nmine) A.fin[(size_t)i * kCsMax + b + cl * kFinCtas] = s;
+            if (l == 0 && (tid >> 3) < nmine) {  // into the cluster leader's s_fin (DSMEM)
+                const uint32_t local = smem_u32(&s_fin[b + cl * kFinCtas]);
+                uint32_t remote;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(local));
+                asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(s) : "memory");
+            }
         }
     }
+    // the leader prefetches the remap of S while the exact dots run
+    if (cluster_rank() == 0 && tid < ns && A.ordered) s_ord[tid] = __ldg(A.ordered + dev::key_index(s_sel[tid]));
     FRS_FTRACE(A, 5);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-        const unsigned long long old = atomicAdd(&A.row_ctr[i], 1ull);
-        s_last = (old % kFinCtas) == static_cast<unsigned long long>(kFinCtas - 1);
-    }
-    __syncthreads();
-    if (!s_last || warp != 0) return;
-    __threadfence();
+    // cluster barrier: release our DSMEM stores, acquire everyone's in the leader
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if (cluster_rank() != 0) return;
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (warp != 0) return;
 
-    // ---- 4. the last CTA of the row, warp 0: selection + certification
+    // ---- 4. the cluster leader, warp 0: selection + certification
     float a_bound = s_th;  // every row not recomputed has approx <= a_bound
     int any_bad = 0;
     for (int w = 0; w < kFinThreads / 32; ++w) {
@@ -896,8 +933,8 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     uint32_t why = (nsel > kCsMax || ns < kk) ? FRS_FLAG_CERT_OVERFLOW : 0u;
     if (any_bad) why |= FRS_FLAG_NONFINITE;
     const bool have0 = lane < ns, have1 = lane + 32 < ns;
-    const float l0 = have0 ? __ldcg(A.fin + (size_t)i * kCsMax + lane) : kNegInf;  // written by the row's
-    const float l1 = have1 ? __ldcg(A.fin + (size_t)i * kCsMax + lane + 32) : kNegInf;  // other CTAs: L2
+    const float l0 = have0 ? s_fin[lane] : kNegInf;
+    const float l1 = have1 ? s_fin[lane + 32] : kNegInf;
     const int j0 = have0 ? dev::key_index(s_sel[lane]) : 0, j1 = have1 ? dev::key_index(s_sel[lane + 32]) : 0;
     if (A.argmax) {
         unsigned long long bv = 0ull;
@@ -937,8 +974,14 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         r0 += o > e0;
         r1 += o > e1;
     }
-    if (have0) s_sorted[r0] = e0;
-    if (have1) s_sorted[r1] = e1;
+    if (have0) {
+        s_sorted[r0] = e0;
+        s_spos[r0] = lane;
+    }
+    if (have1) {
+        s_sorted[r1] = e1;
+        s_spos[r1] = lane + 32;
+    }
     __syncwarp();
     const int want = min(ns, kk + 1);
     // near ties (within 4 ulps) among the selected and at the k boundary: the reference's
@@ -965,7 +1008,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         return;
     }
     // tot = sum exp(x_j - M) over the approximate logits; rescale to the exact max
-    const double total = s_tot * exp(static_cast<double>(s_mmax) - static_cast<double>(mx));
+    const double total = s_tot * static_cast<double>(exp2f((s_mmax - mx) * 1.4426950408889634f));
     const float inv = __double2float_rn(1.0 / total);
     if (lane < A.k) {
         const size_t o = (size_t)i * A.k + lane;
@@ -973,7 +1016,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             const unsigned long long key = s_sorted[lane];
             const int j = dev::key_index(key);
             A.out_ridx[o] = j;
-            A.out_full[o] = A.ordered ? A.ordered[j] : j;
+            A.out_full[o] = A.ordered ? s_ord[s_spos[lane]] : j;
             A.out_prob[o] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(key >> 32)), inv);
         } else {
             A.out_ridx[o] = -1;
@@ -989,7 +1032,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
                 const unsigned long long key = s_sorted[r];
                 const int j = dev::key_index(key);
                 A.out_ridx[o] = j;
-                A.out_full[o] = A.ordered ? A.ordered[j] : j;
+                A.out_full[o] = A.ordered ? s_ord[s_spos[lane]] : j;
                 A.out_prob[o] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(key >> 32)), inv);
             } else {
                 A.out_ridx[o] = -1;
@@ -1018,8 +1061,14 @@ __global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
     __shared__ dev::ReduceScratch rs;
     __shared__ int s_last;
     griddep_wait();
+    griddep_launch();  // the next call's main kernel may become resident as we retire
+    unsigned long long *xtrace = A.P.trace ? A.P.trace + (size_t)A.P.G * 16 + 64 * kFinCtas * 16 : nullptr;
+    if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[2] = gtimer();
     const unsigned nfb = *reinterpret_cast<volatile unsigned *>(A.fb_count);
-    if (nfb == 0) return;
+    if (nfb == 0) {
+        if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[3] = gtimer();
+        return;
+    }
     const int tid = threadIdx.x, G = gridDim.x;
     const int T = A.d >> 3;  // d % 8 == 0 on the FAST path
     for (unsigned f = 0; f < nfb; ++f) {
@@ -1119,7 +1168,7 @@ int make_map(CUtensorMap *map, const void *base, int rows, int cols, int box_row
     return FRS_OK;
 }
 
-constexpr size_t kCtrBytes = 64 * 8 + 8 + 4 + 64 * 4;
+constexpr size_t kCtrBytes = 64 * 8 + 8 + 4 + 64 * 4;  // row_ctr | fb_arrive | fb_count | fb_rows
 
 struct FastWs {
     __nv_bfloat16 *hs;
@@ -1157,7 +1206,7 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.P.trace = nullptr;
     static const bool tracing = std::getenv("FRS_TRACE") != nullptr;
     if (tracing) {
-        if ((st = ctx->trace.ensure((size_t)(G * 16 + 64 * kFinCtas * 16) * 8))) return st;
+        if ((st = ctx->trace.ensure((size_t)(G * 16 + 64 * kFinCtas * 16 + 8) * 8))) return st;
         w.P.trace = static_cast<unsigned long long *>(ctx->trace.ptr);
     }
     if (!ctx->fast_ctr.ptr) {  // row_ctr[64] u64 | fb_arrive u64 | fb_count u32 | fb_rows[64] u32
@@ -1167,12 +1216,34 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     return FRS_OK;
 }
 
+// Per-kernel attributes, set once (and again only when a call needs more dynamic smem):
+// every FAST kernel prefers the maximum shared-memory carveout, so consecutive kernels of the
+// PDL chain never force an SM to drain for an L1/shared reconfiguration and can co-reside.
+template <typename K>
+int configure(K *kern, size_t smem) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void *, size_t>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto &e : done)
+        if (e.first == reinterpret_cast<const void *>(kern) && e.second >= smem) return FRS_OK;
+    FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    for (auto &e : done)
+        if (e.first == reinterpret_cast<const void *>(kern)) {
+            e.second = smem;
+            return FRS_OK;
+        }
+    done.emplace_back(reinterpret_cast<const void *>(kern), smem);
+    return FRS_OK;
+}
+
 template <int NP, bool SOFTMAX>
-int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapH, int n, int v_rows, int d,
+int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapW32, const CUtensorMap &mapH, int n,
+                int v_rows, int d,
                 float inv_t, const Partials &P, cudaStream_t s) {
     using C = MainCfg<NP, SOFTMAX>;
     auto kern = k_fast_main<NP, SOFTMAX>;
-    FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    if (int st = configure(kern, C::SMEM)) return st;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctx->sm_count);
     cfg.blockDim = dim3(C::THREADS);
@@ -1183,7 +1254,7 @@ int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapH, 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mapW, mapH, n, v_rows, d, inv_t, P));
+    FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mapW, mapW32, mapH, n, v_rows, d, inv_t, P));
     ++ctx->launches;
     return FRS_OK;
 }
@@ -1193,28 +1264,31 @@ int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     const int TP = A.d / 8 + 8;
     const size_t smem = (size_t)A.P.G * R * 8 + (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 2 + 64;
     if (smem > ctx->smem_optin) return fail(FRS_ENOTSUP, "FAST finalize: hidden_dim too large");
-    FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (int st = configure(kern, smem)) return st;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(rows, kFinCtas);
     cfg.blockDim = dim3(kFinThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;  // the row's CTAs meet in one cluster
+    at[1].val.clusterDim.x = 1;
+    at[1].val.clusterDim.y = kFinCtas;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
     ++ctx->launches;
     // the grid-wide exact fallback: exits at once unless the finalize queued a row
     auto fb = k_fast_fallback;
     const int fsmem = ((A.d + 7) & ~7) * 4;
-    FRS_CUDA_TRY(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
+    if (int st = configure(fb, fsmem)) return st;
     cfg.gridDim = dim3(ctx->sm_count);
     cfg.blockDim = dim3(kFbThreads);
     cfg.dynamicSmemBytes = fsmem;
-    static const bool no_pdl_fb = std::getenv("FRS_EXP_NO_PDL_FB") != nullptr;  // EXPERIMENT
-    if (no_pdl_fb) cfg.numAttrs = 0;
+    cfg.numAttrs = 1;  // programmatic dependency only (no cluster)
     FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, fb, A));
     ++ctx->launches;
     return FRS_OK;
@@ -1244,10 +1318,8 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     int st = fast_workspace(ctx, NP, d, n, v_rows, w);
     if (st) return st;
     CUtensorMap mapW, mapH;
-    static const bool exp_tiled = std::getenv("FRS_EXPERIMENT_TILED") != nullptr;
-    w.P.tiled = exp_tiled && d % 64 == 0 && v_rows % CH == 0;
-    if ((st = w.P.tiled ? make_map(&mapW, W, v_rows / CH * (d / 64) * CH, 64, CH) : make_map(&mapW, W, v_rows, d, CH)))
-        return st;
+    CUtensorMap mapW32;
+    if ((st = make_map(&mapW, W, v_rows, d, BM)) || (st = make_map(&mapW32, W, v_rows, d, CH))) return st;
     if ((st = make_map(&mapH, w.hs, 2 * NP, d, 2 * NP))) return st;
 
     timing_begin(ctx, s);
@@ -1258,24 +1330,26 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     } end_timing{ctx, s};
     {
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(std::min(ctx->sm_count, (NP * d + 255) / 256));
-        cfg.blockDim = dim3(256);
+        cfg.gridDim = dim3(std::min(ctx->sm_count, (NP * d / 4 + 127) / 128));
+        cfg.blockDim = dim3(128);
         cfg.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs));
+        unsigned long long *xtrace = w.P.trace ? w.P.trace + (size_t)G * 16 + 64 * kFinCtas * 16 : nullptr;
+        if ((st = configure(k_hsplit, 0))) return st;
+        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, xtrace));
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;
     if (argmax) {
-        st = NP == 16   ? launch_main<16, false>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s)
-             : NP == 32 ? launch_main<32, false>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s)
-                        : launch_main<64, false>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s);
+        st = NP == 16   ? launch_main<16, false>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s)
+             : NP == 32 ? launch_main<32, false>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s)
+                        : launch_main<64, false>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s);
     } else {
-        st = launch_main<16, true>(ctx, mapW, mapH, n, v_rows, d, inv_t, w.P, s);
+        st = launch_main<16, true>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s);
     }
     if (st) return st;
     FinArgs A{};
@@ -1322,7 +1396,7 @@ int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float 
     FRS_CUDA_TRY(cudaMemcpy(pkey, w.P.pkey, sizeof(unsigned long long) * n * G * R, cudaMemcpyDeviceToHost));
     FRS_CUDA_TRY(cudaMemcpy(pw2, w.P.pw2, sizeof(float) * G, cudaMemcpyDeviceToHost));
     if (w.P.trace) {  // trailing [G][16] main stamps, then [64][kFinCtas][8] finalize stamps
-        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * G * R, w.P.trace, (size_t)(G * 16 + 64 * kFinCtas * 16) * 8,
+        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * G * R, w.P.trace, (size_t)(G * 16 + 64 * kFinCtas * 16 + 8) * 8,
                                 cudaMemcpyDeviceToHost));
     }
     return FRS_OK;

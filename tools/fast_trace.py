@@ -49,12 +49,13 @@ def main():
         torch.cuda.synchronize()
         n = a.rows
         pm, ps, pth = (np.empty(n * G, np.float32) for _ in range(3))
-        pkey = np.empty(n * G * 8 + G * 16 + 64 * 8 * 16, np.uint64)
+        pkey = np.empty(n * G * 8 + G * 16 + 64 * 8 * 16 + 8, np.uint64)
         pw2 = np.empty(G, np.float32)
         _lib.check(_lib.lib().frs_debug_fast_partials(ctx.handle, n, a.d, pm.ctypes.data, ps.ctypes.data,
                                                       pth.ctypes.data, pkey.ctypes.data, pw2.ctypes.data))
         st = pkey[n * G * 8:n * G * 8 + G * 16].reshape(G, 16).astype(np.int64)
-        ft = pkey[n * G * 8 + G * 16:].reshape(64 * 8, 16).astype(np.int64)[: n * 8]
+        ft = pkey[n * G * 8 + G * 16:n * G * 8 + G * 16 + 64 * 8 * 16].reshape(64 * 8, 16).astype(np.int64)[: n * 8]
+        xt = pkey[n * G * 8 + G * 16 + 64 * 8 * 16:].astype(np.int64)
         t0 = st[:, 0][st[:, 0] > 0].min()
         row = {}
         for s, name in SLOTS.items():
@@ -71,6 +72,9 @@ def main():
                 us = (v - t0) / 1000.0
                 row[f"F{s} {name}"] = [round(float(us.min()), 2), round(float(np.median(us)), 2),
                                        round(float(us.max()), 2)]
+        for s_, name in {0: "hsplit start", 1: "hsplit cta0 end", 2: "fallback start", 3: "fallback exit"}.items():
+            if xt[s_] > 0:
+                row[f"X{s_} {name}"] = round(float((xt[s_] - t0) / 1000.0), 2)
         res.append(row)
     for k in res[-1]:
         print(k.ljust(40), res[-1][k])
