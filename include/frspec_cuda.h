@@ -82,8 +82,10 @@ FRS_API int frs_ctx_sm_count(const frs_ctx *ctx);
  * the roofline measurement: enable, run, then read the summed milliseconds and call count. */
 FRS_API int frs_ctx_set_timing(frs_ctx *ctx, int enable);
 FRS_API int frs_ctx_timing_read(frs_ctx *ctx, double *total_ms, int *count);
-/* Diagnostic: copy the per-CTA partials of the last FAST call ([n][G] max / sum-exp / bound,
- * [n][G][4] candidate keys, [G] max |W_j|^2; G = frs_ctx_sm_count) to host buffers. */
+/* Diagnostic: copy the partials of the last FAST call to host buffers: per hidden row one list
+ * per (CTA, TMEM lane quarter), L = 4 G lists (G = frs_ctx_sm_count): [n][L] max / sum-exp /
+ * bound, [n][L][3] candidate keys, [2 G] max |W_j|^2. With FRS_TRACE set, pkey must have room
+ * for the globaltimer trace after the keys (see tools/fast_trace.py). */
 FRS_API int frs_debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float *pth,
                                     uint64_t *pkey, float *pw2);
 /* Number of kernels this library has launched on ctx (evidence for bench gpu_launches). */

@@ -56,9 +56,10 @@ constexpr int BM = 128;      // slab rows per tile (UMMA M)
 constexpr int CH = 32;       // slab rows per TMA box = partition granule: CTAs own contiguous
                              // runs of 32-row chunks (<= 1 chunk of imbalance instead of 1 tile)
 constexpr int CPT = BM / CH; // chunks per tile
+constexpr int kTrMain = 32;  // globaltimer trace slots per main-kernel CTA (FRS_TRACE diagnostics)
 constexpr int BK = 64;       // k elements per stage: 128-byte bf16 rows, SWIZZLE_128B
-constexpr int R = 8;         // per-CTA candidates per hidden row
-constexpr int RL = R + 1;    // tracked per warp / CTA: the (R+1)-th bounds the CTA's other rows
+constexpr int R = 3;         // candidate keys per list (per epilogue warp and hidden row)
+constexpr int kListsPerCta = 4;  // one list per TMEM lane quarter (32 slab rows of every tile)
 constexpr int kFinThreads = 256;
 constexpr int kFbThreads = 256;
 constexpr int kCandPerFinCta = 8;  // exact recomputes per finalize CTA (8 lanes each)
@@ -154,12 +155,13 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
 }
 
 // ------------------------------------------------------------------ kernels
+// Per hidden row, one "list" per (CTA, TMEM lane quarter): L = 4 G lists.
 struct Partials {
-    float *pm;                 // [NP][G] running max of x = logit / t (softmax only)
-    float *ps;                 // [NP][G] sum exp(x - pm)
-    float *pth;                // [NP][G] the CTA's (R+1)-th best approximate logit (-inf if none)
-    unsigned long long *pkey;  // [NP][G][R] the CTA's best R (approx value, index) keys, descending
-    float *pw2;                // [G] max squared L2 norm of the CTA's slab rows
+    float *pm;                 // [NP][L] max of x = logit / t over the list's slab rows (softmax only)
+    float *ps;                 // [NP][L] sum exp(x - pm)
+    float *pth;                // [NP][L] bound: every list row not in pkey has approx logit <= pth
+    unsigned long long *pkey;  // [NP][L][R] the list's best R (approx value, index) keys, descending
+    float *pw2;                // [2G] max squared L2 norm of slab rows (per CTA and norm warp)
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
 };
@@ -171,7 +173,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define FRS_TRACE(P, slot)                                                       \
     do {                                                                         \
-        if ((P).trace) (P).trace[(size_t)blockIdx.x * 16 + (slot)] = gtimer();   \
+        if ((P).trace) (P).trace[(size_t)blockIdx.x * kTrMain + (slot)] = gtimer();   \
     } while (0)
 
 // hs rows [0,NP) = bf16(h), rows [NP,2NP) = bf16(h - bf16(h)); padded rows are zero.
@@ -215,10 +217,6 @@ struct MainCfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 12 ? 12 : (200 * 1024) / STAGE_BYTES;
     static constexpr int TMEM_COLS = (2 * N) < 32 ? 32 : 2 * N;
-    // end-of-kernel candidate scratch, reusing the (then idle) stage ring
-    static constexpr int CAND_KEYS = NP * 128 * TOPK;
-    static constexpr int CAND_BYTES = CAND_KEYS * 8 + NP * 128 * 4;
-    static_assert(CAND_BYTES <= STAGES * STAGE_BYTES, "candidate scratch must fit the stage ring");
     static_assert(!SOFTMAX || NP == 16, "the fused softmax path handles up to 16 hidden rows per call");
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 4 * NP * 8 + 256;
 };
@@ -255,13 +253,9 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;                                   // STAGES x 16 KB
     uint8_t *sB = smem + STAGES * C::A_BYTES;             // STAGES x B_BYTES
-    unsigned long long *cand = reinterpret_cast<unsigned long long *>(smem);  // end-of-kernel reuse
-    float *cbound = reinterpret_cast<float *>(cand + C::CAND_KEYS);
-    float2 *red = reinterpret_cast<float2 *>(smem + STAGES * C::STAGE_BYTES);  // [4][NP] (m, s)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(red + 4 * NP);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE_BYTES);
     uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
-    float *wred = reinterpret_cast<float *>(tmem_slot + 1);  // [2] norm-warp maxima
 
     // warp index broadcast from lane 0: provably warp-uniform, so the role branches below
     // keep their shuffles convergent (no WARPSYNC.COLLECTIVE emulation)
@@ -341,6 +335,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             }
             FRS_TRACE(P, 2);
         }
+        __syncwarp();  // reconverge before the CTA-wide (aligned) barriers below
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
             constexpr uint32_t idesc = umma_idesc_bf16(BM, N);
@@ -370,6 +365,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             }
             FRS_TRACE(P, 4);
         }
+        __syncwarp();
     } else if (warp < 4) {  // ---------------- row-norm warps: max_j |W_j|^2 for the error bound
         const int r0 = threadIdx.x - 64;  // 0..63: rows r0 and r0 + 64 of every tile
         float acc0 = 0.0f, acc1 = 0.0f, wmax = 0.0f;
@@ -407,9 +403,8 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-        if (lane == 0) wred[warp - 2] = wmax;
+        if (lane == 0) P.pw2[cta * 2 + (warp - 2)] = wmax;
         if (threadIdx.x == 64) FRS_TRACE(P, 8);
-        asm volatile("bar.sync 2, %0;" ::"r"((2 + EPI) * 32) : "memory");  // stage ring now idle
     } else {  // ---------------- epilogue warps: TMEM -> (softmax stats, per-thread candidates)
         const int we = warp - 4;         // 0 .. EPI-1
         const int q = warp & 3;          // TMEM lane quarter this warp may access
@@ -434,6 +429,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             if (threadIdx.x == 128 && lt == 0) FRS_TRACE(P, 10);
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             if (threadIdx.x == 128 && lt == 0) FRS_TRACE(P, 11);
+            if (threadIdx.x == 128 && t == t_end - 1) FRS_TRACE(P, 14);
             tc_fence_after();
             const int row = tile_row0(t) + q * 32 + lane;
             const bool valid = q * 32 + lane < tile_rows(t);
@@ -495,88 +491,65 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             }
         }
         if (threadIdx.x == 128) FRS_TRACE(P, 13);
-        // ---- publish per-thread state, then the CTA top-R per hidden row
+        if (lane == 0) FRS_TRACE(P, 20 + we);
+        // ---- publish, per hidden row, this warp's list: the softmax partial (m, s) over its
+        //      slab rows and their top-R keys + a bound for the rest. Warp-local only: the
+        //      max by one REDUX on order-preserving bits, the list by R + 1 tournament rounds
+        //      over the lanes' sorted (b1, b2) heads.
+        const int list = cta * kListsPerCta + q, L = G * kListsPerCta;
+        // rows outer-unrolled inside every step, so the RPW independent REDUX chains overlap
         if constexpr (SOFTMAX) {
+            float M[RPW], e[RPW];
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) M[r] = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(m[r])));
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) e[r] = m[r] == kNegInf ? 0.0f : s[r] * exp2f((m[r] - M[r]) * 1.4426950408889634f);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int r = 0; r < RPW; ++r) e[r] += __shfl_xor_sync(0xffffffffu, e[r], o);
 #pragma unroll
             for (int r = 0; r < RPW; ++r) {
                 const int i = cbase + r;
-                if (i >= n) continue;  // uniform
-                float mi = m[r], si = s[r];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const float mo = __shfl_xor_sync(0xffffffffu, mi, o), so = __shfl_xor_sync(0xffffffffu, si, o);
-                    const float mn = fmaxf(mi, mo);
-                    si = (mn == kNegInf) ? 0.0f
-                                         : si * exp2f((mi - mn) * 1.4426950408889634f) +
-                                               so * exp2f((mo - mn) * 1.4426950408889634f);
-                    mi = mn;
+                if (lane == 0 && i < n) {
+                    P.pm[(size_t)i * L + list] = M[r];
+                    P.ps[(size_t)i * L + list] = e[r];
                 }
-                if (lane == 0) red[q * NP + i] = make_float2(mi, si);
             }
         }
-        asm volatile("bar.sync 2, %0;" ::"r"((2 + EPI) * 32) : "memory");  // norm warps done with the ring
-        const int slot = q * 32 + lane;  // 0..127: the thread's slab-row position within a tile
+        unsigned long long h1[RPW], h2[RPW], out[RPW];
+        float bmax[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            bmax[r] = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(bnd[r])));
+            h1[r] = b1[r];
+            if constexpr (TOPK == 2) h2[r] = b2[r];
+            else h2[r] = 0ull;
+            out[r] = 0ull;
+        }
+#pragma unroll
+        for (int rnd = 0; rnd <= R; ++rnd) {
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) {
+                const unsigned long long best = warp_max_key(h1[r]);
+                if (lane == rnd) out[r] = best;
+                if (h1[r] == best && best != 0ull) {  // unique keys: one owner pops its head
+                    h1[r] = h2[r];
+                    h2[r] = 0ull;
+                }
+            }
+        }
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
             const int i = cbase + r;
-            cand[(size_t)i * 128 * TOPK + slot * TOPK] = b1[r];
-            if constexpr (TOPK == 2) cand[(size_t)i * 128 * TOPK + slot * TOPK + 1] = b2[r];
-            cbound[i * 128 + slot] = bnd[r];
+            if (i >= n) continue;
+            if (lane < R) P.pkey[((size_t)i * L + list) * R + lane] = out[r];
+            if (lane == R) P.pth[(size_t)i * L + list] = fmaxf(out[r] ? dev::key_value(out[r]) : kNegInf, bmax[r]);
         }
-        if (threadIdx.x == 128) FRS_TRACE(P, 5);
-        asm volatile("bar.sync 1, %0;" ::"r"(EPI * 32) : "memory");  // the epilogue warps only
-        for (int i = we; i < n; i += EPI) {
-            constexpr int PL = 4 * TOPK;  // keys per lane
-            unsigned long long kk[PL];
-            float bmax = kNegInf;
-#pragma unroll
-            for (int j = 0; j < PL; ++j) kk[j] = cand[(size_t)i * 128 * TOPK + lane + 32 * j];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) bmax = fmaxf(bmax, cbound[i * 128 + lane + 32 * j]);
-            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 16));
-            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 8));
-            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 4));
-            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 2));
-            bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, 1));
-            unsigned long long prev = ~0ull, out = 0ull;
-#pragma unroll
-            for (int rnd = 0; rnd < RL; ++rnd) {  // CTA top-RL by rounds of warp max
-                unsigned long long mine = 0ull;
-#pragma unroll
-                for (int j = 0; j < PL; ++j)
-                    if (kk[j] < prev && kk[j] > mine) mine = kk[j];
-                const unsigned long long best = warp_max_key(mine);
-                if (lane == rnd) out = best;
-                prev = best ? best : prev;
-                if (!best) break;  // uniform
-            }
-            if (lane < R) P.pkey[((size_t)i * G + cta) * R + lane] = out;
-            if (lane == R) {
-                const float th = out ? dev::key_value(out) : kNegInf;
-                P.pth[(size_t)i * G + cta] = fmaxf(th, bmax);
-            }
-            if constexpr (SOFTMAX) {
-                if (lane == 0) {
-                    float mi = kNegInf, si = 0.0f;
-                    for (int w = 0; w < 4; ++w) {
-                        const float2 v = red[w * NP + i];
-                        const float mn = fmaxf(mi, v.x);
-                        if (mn != kNegInf)
-                            si = si * exp2f((mi - mn) * 1.4426950408889634f) + v.y * exp2f((v.x - mn) * 1.4426950408889634f);
-                        mi = mn;
-                    }
-                    P.pm[(size_t)i * G + cta] = mi;
-                    P.ps[(size_t)i * G + cta] = si;
-                }
-            }
-        }
+        if (threadIdx.x == 128) FRS_TRACE(P, 18);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        P.pw2[cta] = fmaxf(wred[0], wred[1]);
-        FRS_TRACE(P, 7);
-    }
-    __syncthreads();
+    __syncthreads();  // every TMEM read is done
+    if (threadIdx.x == 0) FRS_TRACE(P, 7);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, C::TMEM_COLS);
@@ -620,7 +593,7 @@ struct FinArgs {
 #define FRS_FTRACE(A, slot)                                                                              \
     do {                                                                                                  \
         if ((A).P.trace && threadIdx.x == 0)                                                              \
-            (A).P.trace[(size_t)(A).P.G * 16 + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + (slot)] = gtimer(); \
+            (A).P.trace[(size_t)(A).P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + (slot)] = gtimer(); \
     } while (0)
 
 // Finalize: grid (n, kFinCtas). The work per row is tiny, so the kernel is written for
@@ -637,18 +610,19 @@ struct FinArgs {
 //   4. the last CTA of the row to arrive selects the top-k by (prob desc, index asc) and
 //      certifies it (see the file comment); rows that cannot be certified are queued for the
 //      grid-wide exact fallback (k_fast_fallback).
-constexpr int kMaxLists = 256;  // G <= 256 CTA lists of R keys
+constexpr int kMaxLists = 1024;  // L = 4 G <= 1024 lists of R keys per hidden row
 
 __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     extern __shared__ __align__(16) uint8_t fsm_raw[];
     const int T = A.d >> 3;           // dot_f32 steps per lane chain (d % 8 == 0 on FAST)
     const int TP = T + 8;             // padded chain pitch (elements): 16-byte aligned rows
-    unsigned long long *ukeys = reinterpret_cast<unsigned long long *>(fsm_raw);       // [G*R]
-    float *ht = reinterpret_cast<float *>(ukeys + (size_t)A.P.G * R);                 // [8][TP]
+    unsigned long long *ukeys = reinterpret_cast<unsigned long long *>(fsm_raw);       // [L*R]
+    float *ht = reinterpret_cast<float *>(ukeys + (size_t)A.P.G * kListsPerCta * R);  // [8][TP]
     unsigned short *wt = reinterpret_cast<unsigned short *>(ht + 8 * TP);            // [8 cand][8][TP]
     __shared__ unsigned long long s_S[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
     __shared__ double s_hn2[kFinThreads / 32], s_tot;
-    __shared__ float s_mmax, s_th, s_eps, s_abw[kFinThreads / 32];
+    __shared__ float s_mmax, s_th, s_eps, s_abw[kFinThreads / 32], s_pmw[4], s_thw[2], s_w2w[2];
+    __shared__ double s_psw[4];
     __shared__ unsigned long long s_vk, s_wtop[kFinThreads / 32][kMaxK];
     __shared__ float s_fin[kCsMax];             // exact logits of S (cluster leader; DSMEM-written)
     __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
@@ -658,7 +632,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
 
     const int i = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = tid & 31;
-    const int G = A.P.G, E = G * R;
+    const int G = A.P.G, L = G * kListsPerCta, E = L * R;
     const float kNegInf = -__int_as_float(0x7f800000);
     // ---- 1a. the hidden row (independent of the main kernel): transposed ht[l][t] = h[8t + l]
     {
@@ -703,7 +677,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     griddep_wait();
     FRS_FTRACE(A, 2);
     // ---- 1b. partials of the main kernel: every load of a thread issued before any use
-    constexpr int KPT = kMaxLists * R / kFinThreads;  // union keys per thread (8)
+    constexpr int KPT = kMaxLists * R / kFinThreads;  // union keys per thread
     unsigned long long kr[KPT];
     {
         const unsigned long long *src = A.P.pkey + (size_t)i * E;
@@ -718,74 +692,101 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             if (e < E) ukeys[e] = kr[u];
         }
     }
-    constexpr int LPL = kMaxLists / 32;  // CTA partials per lane (8)
-    if (warp == 0 && !A.argmax) {        // softmax partials: M = max m_c, T = sum s_c exp(m_c - M)
-        float pm[LPL], ps[LPL];
+    constexpr int SW = 4;                        // warps merging the softmax partials
+    constexpr int PPL = kMaxLists / (32 * SW);   // partials per lane
+    if (warp < SW && !A.argmax) {  // softmax partials: M = max m_c, T = sum s_c exp(m_c - M)
+        float pm[PPL], ps[PPL];
 #pragma unroll
-        for (int u = 0; u < LPL; ++u) {
-            const int c = lane + 32 * u;
-            pm[u] = c < G ? __ldcg(A.P.pm + (size_t)i * G + c) : kNegInf;
-            ps[u] = c < G ? __ldcg(A.P.ps + (size_t)i * G + c) : 0.0f;
+        for (int u = 0; u < PPL; ++u) {
+            const int c = warp * 32 + lane + 32 * SW * u;
+            pm[u] = c < L ? __ldcg(A.P.pm + (size_t)i * L + c) : kNegInf;
+            ps[u] = c < L ? __ldcg(A.P.ps + (size_t)i * L + c) : 0.0f;
         }
         float mm = kNegInf;
 #pragma unroll
-        for (int u = 0; u < LPL; ++u) mm = fmaxf(mm, pm[u]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+        for (int u = 0; u < PPL; ++u) mm = fmaxf(mm, pm[u]);
+        mm = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(mm)));
         double t = 0.0;
 #pragma unroll
-        for (int u = 0; u < LPL; ++u)  // approximate domain anyway: one MUFU per partial
+        for (int u = 0; u < PPL; ++u)  // approximate domain anyway: one MUFU per partial
             if (pm[u] != kNegInf) t += static_cast<double>(ps[u] * exp2f((pm[u] - mm) * 1.4426950408889634f));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (lane == 0) {
-            s_mmax = mm;
-            s_tot = t;
+            s_pmw[warp] = mm;
+            s_psw[warp] = t;
         }
-    } else if (warp == 1) {  // bounds: th = max (R+1)-th key value, w2 = max |W_j|^2; then eps
+    } else if (warp >= SW && warp < SW + 2) {  // bounds: th over the lists, w2 over the norm warps
+        const int wb = warp - SW;
         float th = kNegInf, w2 = 0.0f;
-        float a[LPL], w[LPL];
+        constexpr int TPL = kMaxLists / 64;
+        float a[TPL], w[TPL];
 #pragma unroll
-        for (int u = 0; u < LPL; ++u) {
-            const int c = lane + 32 * u;
-            a[u] = c < G ? __ldcg(A.P.pth + (size_t)i * G + c) : kNegInf;
-            w[u] = c < G ? __ldcg(A.P.pw2 + c) : 0.0f;
+        for (int u = 0; u < TPL; ++u) {
+            const int c = wb * 32 + lane + 64 * u;
+            a[u] = c < L ? __ldcg(A.P.pth + (size_t)i * L + c) : kNegInf;
+            w[u] = c < 2 * G ? __ldcg(A.P.pw2 + c) : 0.0f;
         }
 #pragma unroll
-        for (int u = 0; u < LPL; ++u) {
+        for (int u = 0; u < TPL; ++u) {
             th = fmaxf(th, a[u]);
             w2 = fmaxf(w2, w[u]);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            th = fmaxf(th, __shfl_xor_sync(0xffffffffu, th, o));
-            w2 = fmaxf(w2, __shfl_xor_sync(0xffffffffu, w2, o));
-        }
+        th = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(th)));
+        w2 = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(w2)));
         if (lane == 0) {
-            double h2 = 0.0;
-            for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
-            s_th = th;
-            s_eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(w2) * 1.001)) * fast_gamma(A.d) * 1.01f;
+            s_thw[wb] = th;
+            s_w2w[wb] = w2;
         }
     }
     __syncthreads();
+    if (tid == 0) {
+        double h2 = 0.0;
+        for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
+        const float w2 = fmaxf(s_w2w[0], s_w2w[1]);
+        s_th = fmaxf(s_thw[0], s_thw[1]);
+        s_eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(w2) * 1.001)) * fast_gamma(A.d) * 1.01f;
+        if (!A.argmax) {
+            float mm = kNegInf;
+            for (int w = 0; w < SW; ++w) mm = fmaxf(mm, s_pmw[w]);
+            double t = 0.0;
+            for (int w = 0; w < SW; ++w)
+                if (s_pmw[w] != kNegInf) t += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
+            s_mmax = mm;
+            s_tot = t;
+        }
+    }
     FRS_FTRACE(A, 3);
 
     // ---- 2a. the kk-th largest union key by a two-level tournament over the sorted lists:
-    //          warp w merges lists [32w, 32w + 32) (one per lane) into its top-kk, then warp 0
-    //          merges the 8 warp lists. Each round is one warp max (2 REDUX) + one head advance.
+    //          warp w merges its share of the lists (heads in its lanes) into its top-kk, then
+    //          warp 0 merges the 8 warp lists. Each round is one warp max (2 REDUX) + one head
+    //          advance in the owner lane.
     const int kk = min(A.k, A.v_rows);
     {
-        const int g = warp * 32 + lane;
-        int hp = 0;
-        unsigned long long hk = g < G ? ukeys[g * R] : 0ull;
+        constexpr int HPL = kMaxLists / kFinThreads;  // lists per lane
+        const int LW = (L + kFinThreads / 32 - 1) / (kFinThreads / 32);
+        int hp[HPL];
+        unsigned long long hk[HPL];
+#pragma unroll
+        for (int u = 0; u < HPL; ++u) {
+            const int g = warp * LW + lane + 32 * u;
+            hp[u] = 0;
+            hk[u] = (lane + 32 * u < LW && g < L) ? ukeys[g * R] : 0ull;
+        }
         for (int r = 0; r < kk; ++r) {
-            const unsigned long long best = warp_max_key(hk);
+            unsigned long long mine = 0ull;
+#pragma unroll
+            for (int u = 0; u < HPL; ++u) mine = hk[u] > mine ? hk[u] : mine;
+            const unsigned long long best = warp_max_key(mine);
             if (lane == 0) s_wtop[warp][r] = best;
-            if (hk == best && best != 0ull) {  // keys are unique: a single owner lane
-                ++hp;
-                hk = hp < R ? ukeys[g * R + hp] : 0ull;
-            }
+#pragma unroll
+            for (int u = 0; u < HPL; ++u)
+                if (hk[u] == best && best != 0ull) {  // keys are unique: a single owner
+                    const int g = warp * LW + lane + 32 * u;
+                    ++hp[u];
+                    hk[u] = hp[u] < R ? ukeys[g * R + hp[u]] : 0ull;
+                }
         }
     }
     __syncthreads();
@@ -1062,7 +1063,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
     __shared__ int s_last;
     griddep_wait();
     griddep_launch();  // the next call's main kernel may become resident as we retire
-    unsigned long long *xtrace = A.P.trace ? A.P.trace + (size_t)A.P.G * 16 + 64 * kFinCtas * 16 : nullptr;
+    unsigned long long *xtrace = A.P.trace ? A.P.trace + (size_t)A.P.G * kTrMain + 64 * kFinCtas * 16 : nullptr;
     if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[2] = gtimer();
     const unsigned nfb = *reinterpret_cast<volatile unsigned *>(A.fb_count);
     if (nfb == 0) {
@@ -1187,8 +1188,9 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
         return o;
     };
     const size_t o_hs = take((size_t)2 * NP * d * 2);
-    const size_t o_pm = take((size_t)NP * G * 4), o_ps = take((size_t)NP * G * 4), o_pth = take((size_t)NP * G * 4);
-    const size_t o_pkey = take((size_t)NP * G * R * 8), o_pw2 = take((size_t)G * 4);
+    const int L = G * kListsPerCta;
+    const size_t o_pm = take((size_t)NP * L * 4), o_ps = take((size_t)NP * L * 4), o_pth = take((size_t)NP * L * 4);
+    const size_t o_pkey = take((size_t)NP * L * R * 8), o_pw2 = take((size_t)G * 2 * 4);
     const size_t o_fin = take((size_t)NP * CS * 4);
     const size_t o_scr = take((size_t)n * v_rows * 2 * 4);
     int st = ctx->fast_ws.ensure(off);
@@ -1206,7 +1208,7 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.P.trace = nullptr;
     static const bool tracing = std::getenv("FRS_TRACE") != nullptr;
     if (tracing) {
-        if ((st = ctx->trace.ensure((size_t)(G * 16 + 64 * kFinCtas * 16 + 8) * 8))) return st;
+        if ((st = ctx->trace.ensure((size_t)(G * kTrMain + 64 * kFinCtas * 16 + 8) * 8))) return st;
         w.P.trace = static_cast<unsigned long long *>(ctx->trace.ptr);
     }
     if (!ctx->fast_ctr.ptr) {  // row_ctr[64] u64 | fb_arrive u64 | fb_count u32 | fb_rows[64] u32
@@ -1262,7 +1264,7 @@ int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapW32
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     auto kern = k_fast_finalize;
     const int TP = A.d / 8 + 8;
-    const size_t smem = (size_t)A.P.G * R * 8 + (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 2 + 64;
+    const size_t smem = (size_t)A.P.G * kListsPerCta * R * 8 + (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 2 + 64;
     if (smem > ctx->smem_optin) return fail(FRS_ENOTSUP, "FAST finalize: hidden_dim too large");
     if (int st = configure(kern, smem)) return st;
     cudaLaunchConfig_t cfg{};
@@ -1313,7 +1315,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     if (!argmax && k > 64) return fail(FRS_ENOTSUP, "FAST draft head: k <= 64");
     const int NP = n <= 16 ? 16 : (n <= 32 ? 32 : 64);
     const int G = ctx->sm_count;
-    if (G > kMaxLists) return fail(FRS_ENOTSUP, "FAST head: too many SMs for the candidate merge");
+    if (G * kListsPerCta > kMaxLists) return fail(FRS_ENOTSUP, "FAST head: too many SMs for the candidate merge");
     FastWs w;
     int st = fast_workspace(ctx, NP, d, n, v_rows, w);
     if (st) return st;
@@ -1338,7 +1340,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        unsigned long long *xtrace = w.P.trace ? w.P.trace + (size_t)G * 16 + 64 * kFinCtas * 16 : nullptr;
+        unsigned long long *xtrace = w.P.trace ? w.P.trace + (size_t)G * kTrMain + 64 * kFinCtas * 16 : nullptr;
         if ((st = configure(k_hsplit, 0))) return st;
         FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, xtrace));
         ++ctx->launches;
@@ -1390,13 +1392,14 @@ int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float 
     if (st) return st;
     const int G = ctx->sm_count;
     FRS_CUDA_TRY(cudaDeviceSynchronize());
-    FRS_CUDA_TRY(cudaMemcpy(pm, w.P.pm, sizeof(float) * n * G, cudaMemcpyDeviceToHost));
-    FRS_CUDA_TRY(cudaMemcpy(ps, w.P.ps, sizeof(float) * n * G, cudaMemcpyDeviceToHost));
-    FRS_CUDA_TRY(cudaMemcpy(pth, w.P.pth, sizeof(float) * n * G, cudaMemcpyDeviceToHost));
-    FRS_CUDA_TRY(cudaMemcpy(pkey, w.P.pkey, sizeof(unsigned long long) * n * G * R, cudaMemcpyDeviceToHost));
-    FRS_CUDA_TRY(cudaMemcpy(pw2, w.P.pw2, sizeof(float) * G, cudaMemcpyDeviceToHost));
-    if (w.P.trace) {  // trailing [G][16] main stamps, then [64][kFinCtas][8] finalize stamps
-        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * G * R, w.P.trace, (size_t)(G * 16 + 64 * kFinCtas * 16 + 8) * 8,
+    const int L = G * kListsPerCta;
+    FRS_CUDA_TRY(cudaMemcpy(pm, w.P.pm, sizeof(float) * n * L, cudaMemcpyDeviceToHost));
+    FRS_CUDA_TRY(cudaMemcpy(ps, w.P.ps, sizeof(float) * n * L, cudaMemcpyDeviceToHost));
+    FRS_CUDA_TRY(cudaMemcpy(pth, w.P.pth, sizeof(float) * n * L, cudaMemcpyDeviceToHost));
+    FRS_CUDA_TRY(cudaMemcpy(pkey, w.P.pkey, sizeof(unsigned long long) * n * L * R, cudaMemcpyDeviceToHost));
+    FRS_CUDA_TRY(cudaMemcpy(pw2, w.P.pw2, sizeof(float) * 2 * G, cudaMemcpyDeviceToHost));
+    if (w.P.trace) {  // trailing [G][kTrMain] main stamps, [64][kFinCtas][16] finalize stamps, [8] extra
+        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * L * R, w.P.trace, (size_t)(G * kTrMain + 64 * kFinCtas * 16 + 8) * 8,
                                 cudaMemcpyDeviceToHost));
     }
     return FRS_OK;

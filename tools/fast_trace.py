@@ -19,8 +19,11 @@ from paper_2502_14856_b200 import api, _lib  # noqa: E402
 
 SLOTS = {0: "setup done", 1: "producer: before griddep_wait", 9: "producer: after griddep_wait",
          3: "mma: first stage full", 2: "producer: all TMA issued", 4: "mma: all issued", 8: "norm warps done",
-         10: "epi: first tfull wait", 11: "epi: first tile ready", 13: "epi: loop done", 5: "cand published",
-         7: "cta end"}
+         10: "epi: first tfull wait", 11: "epi: first tile ready", 14: "epi w4: last tile ready",
+         13: "epi: loop done", 15: "epi w4: softmax merged", 16: "epi w4: after bar2", 5: "cand published",
+         17: "epi w4: after bar1", 18: "epi w4: rows done", 19: "cta: final sync", 7: "cta end",
+         20: "loop done w0", 21: "loop done w1", 22: "loop done w2", 23: "loop done w3", 24: "loop done w4",
+         25: "loop done w5", 26: "loop done w6", 27: "loop done w7"}
 FSLOTS = {0: "fin start", 1: "fin h loaded", 2: "fin after griddep_wait", 3: "fin partials merged",
           4: "fin S selected", 5: "fin recompute done", 6: "fin last: certified?", 7: "fin last: written",
           8: "fin v' ranked", 9: "fin S collected",
@@ -48,14 +51,15 @@ def main():
         api.draft_head_topk(ctx, h, head, 10, mode="fast", out=out)
         torch.cuda.synchronize()
         n = a.rows
-        pm, ps, pth = (np.empty(n * G, np.float32) for _ in range(3))
-        pkey = np.empty(n * G * 8 + G * 16 + 64 * 8 * 16 + 8, np.uint64)
-        pw2 = np.empty(G, np.float32)
+        L = 4 * G
+        pm, ps, pth = (np.empty(n * L, np.float32) for _ in range(3))
+        pkey = np.empty(n * L * 3 + G * 32 + 64 * 8 * 16 + 8, np.uint64)
+        pw2 = np.empty(2 * G, np.float32)
         _lib.check(_lib.lib().frs_debug_fast_partials(ctx.handle, n, a.d, pm.ctypes.data, ps.ctypes.data,
                                                       pth.ctypes.data, pkey.ctypes.data, pw2.ctypes.data))
-        st = pkey[n * G * 8:n * G * 8 + G * 16].reshape(G, 16).astype(np.int64)
-        ft = pkey[n * G * 8 + G * 16:n * G * 8 + G * 16 + 64 * 8 * 16].reshape(64 * 8, 16).astype(np.int64)[: n * 8]
-        xt = pkey[n * G * 8 + G * 16 + 64 * 8 * 16:].astype(np.int64)
+        st = pkey[n * L * 3:n * L * 3 + G * 32].reshape(G, 32).astype(np.int64)
+        ft = pkey[n * L * 3 + G * 32:n * L * 3 + G * 32 + 64 * 8 * 16].reshape(64 * 8, 16).astype(np.int64)[: n * 8]
+        xt = pkey[n * L * 3 + G * 32 + 64 * 8 * 16:].astype(np.int64)
         t0 = st[:, 0][st[:, 0] > 0].min()
         row = {}
         for s, name in SLOTS.items():
