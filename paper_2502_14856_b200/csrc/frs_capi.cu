@@ -108,6 +108,9 @@ int frs_ctx_destroy(frs_ctx *ctx) {
     if (!ctx) return FRS_OK;
     cudaSetDevice(ctx->device);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+    for (auto &g : ctx->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;

@@ -32,6 +32,23 @@ struct DevBuf {
     ~DevBuf();
 };
 
+// CUDA-graph cache of repeated FAST calls (frs_fast.cu): the key is every pointer, size and
+// parameter the captured chain bakes in.
+constexpr int kGraphKeyWords = 19;
+struct GraphKey {
+    uint64_t w[kGraphKeyWords];
+    bool operator==(const GraphKey &o) const {
+        for (int i = 0; i < kGraphKeyWords; ++i)
+            if (w[i] != o.w[i]) return false;
+        return true;
+    }
+};
+struct GraphEntry {
+    GraphKey key{};
+    cudaGraphExec_t exec = nullptr;
+    uint64_t last_use = 0;
+};
+
 }  // namespace frs
 
 struct frs_ctx {
@@ -55,6 +72,9 @@ struct frs_ctx {
     std::vector<cudaEvent_t> ev;  // start/stop pairs
     size_t ev_used = 0;
     unsigned long long launches = 0;  // kernels launched by this library on this ctx
+    std::vector<frs::GraphEntry> graphs;  // captured FAST chains (LRU)
+    uint64_t graph_clock = 0;
+    cudaStream_t cap_stream = nullptr;    // private stream for graph capture
 };
 
 namespace frs {

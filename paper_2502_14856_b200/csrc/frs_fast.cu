@@ -42,6 +42,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -611,19 +612,33 @@ struct FinArgs {
 //      certifies it (see the file comment); rows that cannot be certified are queued for the
 //      grid-wide exact fallback (k_fast_fallback).
 constexpr int kMaxLists = 1024;  // L = 4 G <= 1024 lists of R keys per hidden row
+constexpr int kHistBins = 64;     // threshold histogram of (M - v) / bw: 48 linear bins, then
+                                  // 4 bins per octave, the last one a catch-all
+__device__ __forceinline__ int hist_bin(float r) {  // r >= 0
+    if (!(r < 48.0f)) {
+        if (!(r < 48.0f * 0x1p15f)) return kHistBins - 1;  // also NaN
+        const int b = 48 + static_cast<int>(4.0f * log2f(r * (1.0f / 48.0f)));
+        return b < kHistBins - 1 ? b : kHistBins - 1;
+    }
+    return static_cast<int>(r);
+}
+// upper edge of bin j - 1 (= lower bound of r over bins >= j), with slack for log2f rounding
+__device__ __forceinline__ float hist_edge(int j) {
+    return j <= 48 ? static_cast<float>(j) : 48.0f * exp2f(0.25f * static_cast<float>(j - 48)) * (1.0f + 0x1p-10f);
+}
 
 __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     extern __shared__ __align__(16) uint8_t fsm_raw[];
     const int T = A.d >> 3;           // dot_f32 steps per lane chain (d % 8 == 0 on FAST)
     const int TP = T + 8;             // padded chain pitch (elements): 16-byte aligned rows
-    unsigned long long *ukeys = reinterpret_cast<unsigned long long *>(fsm_raw);       // [L*R]
-    float *ht = reinterpret_cast<float *>(ukeys + (size_t)A.P.G * kListsPerCta * R);  // [8][TP]
+    float *ht = reinterpret_cast<float *>(fsm_raw);                                   // [8][TP]
     unsigned short *wt = reinterpret_cast<unsigned short *>(ht + 8 * TP);            // [8 cand][8][TP]
     __shared__ unsigned long long s_S[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
     __shared__ double s_hn2[kFinThreads / 32], s_tot;
-    __shared__ float s_mmax, s_th, s_eps, s_abw[kFinThreads / 32], s_pmw[4], s_thw[2], s_w2w[2];
-    __shared__ double s_psw[4];
-    __shared__ unsigned long long s_vk, s_wtop[kFinThreads / 32][kMaxK];
+    __shared__ float s_mmax, s_th, s_abw[kFinThreads / 32], s_pmw[4], s_thw[2], s_w2w[2];
+    __shared__ float s_psw[4];
+    __shared__ unsigned s_hist[kHistBins];
+    __shared__ uint32_t s_kmax[kFinThreads / 32];
     __shared__ float s_fin[kCsMax];             // exact logits of S (cluster leader; DSMEM-written)
     __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
     __shared__ int s_nsel, s_badw[kFinThreads / 32];
@@ -667,10 +682,8 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             s_hn2[warp] = hn2;
             s_badw[warp] = bad;
         }
-        if (tid == 0) {
-            s_nsel = 0;
-            s_vk = 0ull;
-        }
+        if (tid == 0) s_nsel = 0;
+        if (tid < kHistBins) s_hist[tid] = 0u;
     }
     __syncthreads();  // s_hn2 / s_badw complete (read by warp 1 below)
     FRS_FTRACE(A, 1);
@@ -686,11 +699,11 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             const int e = tid + u * kFinThreads;
             kr[u] = e < E ? __ldcg(src + e) : 0ull;
         }
+        unsigned long long km = 0ull;
 #pragma unroll
-        for (int u = 0; u < KPT; ++u) {
-            const int e = tid + u * kFinThreads;
-            if (e < E) ukeys[e] = kr[u];
-        }
+        for (int u = 0; u < KPT; ++u) km = kr[u] > km ? kr[u] : km;
+        const uint32_t kv = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(km >> 32));  // value bits
+        if (lane == 0) s_kmax[warp] = kv;
     }
     constexpr int SW = 4;                        // warps merging the softmax partials
     constexpr int PPL = kMaxLists / (32 * SW);   // partials per lane
@@ -706,10 +719,10 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
 #pragma unroll
         for (int u = 0; u < PPL; ++u) mm = fmaxf(mm, pm[u]);
         mm = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(mm)));
-        double t = 0.0;
+        float t = 0.0f;
 #pragma unroll
         for (int u = 0; u < PPL; ++u)  // approximate domain anyway: one MUFU per partial
-            if (pm[u] != kNegInf) t += static_cast<double>(ps[u] * exp2f((pm[u] - mm) * 1.4426950408889634f));
+            if (pm[u] != kNegInf) t += ps[u] * exp2f((pm[u] - mm) * 1.4426950408889634f);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (lane == 0) {
@@ -740,78 +753,52 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         }
     }
     __syncthreads();
-    if (tid == 0) {
-        double h2 = 0.0;
-        for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
-        const float w2 = fmaxf(s_w2w[0], s_w2w[1]);
-        s_th = fmaxf(s_thw[0], s_thw[1]);
-        s_eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(w2) * 1.001)) * fast_gamma(A.d) * 1.01f;
-        if (!A.argmax) {
-            float mm = kNegInf;
-            for (int w = 0; w < SW; ++w) mm = fmaxf(mm, s_pmw[w]);
-            double t = 0.0;
-            for (int w = 0; w < SW; ++w)
-                if (s_pmw[w] != kNegInf) t += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
-            s_mmax = mm;
-            s_tot = t;
-        }
-    }
     FRS_FTRACE(A, 3);
-
-    // ---- 2a. the kk-th largest union key by a two-level tournament over the sorted lists:
-    //          warp w merges its share of the lists (heads in its lanes) into its top-kk, then
-    //          warp 0 merges the 8 warp lists. Each round is one warp max (2 REDUX) + one head
-    //          advance in the owner lane.
+    // every thread: eps, the largest key value M, the histogram of (M - v) in half-eps bins
     const int kk = min(A.k, A.v_rows);
+    float eps, Mv, bw;
     {
-        constexpr int HPL = kMaxLists / kFinThreads;  // lists per lane
-        const int LW = (L + kFinThreads / 32 - 1) / (kFinThreads / 32);
-        int hp[HPL];
-        unsigned long long hk[HPL];
+        double h2 = 0.0;
 #pragma unroll
-        for (int u = 0; u < HPL; ++u) {
-            const int g = warp * LW + lane + 32 * u;
-            hp[u] = 0;
-            hk[u] = (lane + 32 * u < LW && g < L) ? ukeys[g * R] : 0ull;
-        }
-        for (int r = 0; r < kk; ++r) {
-            unsigned long long mine = 0ull;
+        for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
+        eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(fmaxf(s_w2w[0], s_w2w[1])) * 1.001)) *
+              fast_gamma(A.d) * 1.01f;
+        uint32_t kv = 0u;
 #pragma unroll
-            for (int u = 0; u < HPL; ++u) mine = hk[u] > mine ? hk[u] : mine;
-            const unsigned long long best = warp_max_key(mine);
-            if (lane == 0) s_wtop[warp][r] = best;
+        for (int q = 0; q < kFinThreads / 32; ++q) kv = max(kv, s_kmax[q]);
+        Mv = dev::from_ordered(kv);
+        bw = fmaxf(0.5f * eps, fabsf(Mv) * 0x1p-20f + 0x1p-30f);
 #pragma unroll
-            for (int u = 0; u < HPL; ++u)
-                if (hk[u] == best && best != 0ull) {  // keys are unique: a single owner
-                    const int g = warp * LW + lane + 32 * u;
-                    ++hp[u];
-                    hk[u] = hp[u] < R ? ukeys[g * R + hp[u]] : 0ull;
-                }
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        int hp = 0;
-        unsigned long long hk = lane < kFinThreads / 32 ? s_wtop[lane][0] : 0ull;
-        unsigned long long kth = 0ull;
-        for (int r = 0; r < kk; ++r) {
-            const unsigned long long best = warp_max_key(hk);
-            if (best == 0ull) break;
-            kth = best;
-            if (hk == best) {
-                ++hp;
-                hk = hp < kk ? s_wtop[lane][hp] : 0ull;
-            }
-        }
-        if (lane == 0) s_vk = kth;
+        for (int u = 0; u < KPT; ++u)
+            if (kr[u] != 0ull) atomicAdd(&s_hist[hist_bin((Mv - dev::key_value(kr[u])) / bw)], 1u);
     }
     __syncthreads();
     FRS_FTRACE(A, 8);
-    // ---- 2b. S = union keys at or above t_s (fewer than kk pool keys: t_s = -inf)
+    // ---- 2. S = union keys >= t_s: the kk-th key lies in the first bin whose cumulative count
+    //         reaches kk (every warp scans the 64 bins redundantly: no extra barrier), so
+    //         v_kk > M - bw g(bin + 1) and t_s = that edge - 2 eps - margin keeps every row that
+    //         can reach the top-k (the catch-all last bin: t_s = -inf).
     {
-        const float eps = s_eps;
-        const float vk = s_vk ? dev::key_value(s_vk) : kNegInf;
-        const float t_s = vk - 2.0f * eps - (fabsf(vk) * 0x1p-18f + 0x1p-20f);
+        const unsigned c0 = s_hist[2 * lane], c1 = s_hist[2 * lane + 1];
+        unsigned incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const unsigned excl = incl - c0 - c1;
+        const bool hit0 = excl < static_cast<unsigned>(kk) && excl + c0 >= static_cast<unsigned>(kk);
+        const bool hit1 = !hit0 && excl + c0 < static_cast<unsigned>(kk) && incl >= static_cast<unsigned>(kk);
+        const unsigned ball = __ballot_sync(0xffffffffu, hit0 || hit1);
+        int bk = kHistBins - 1;
+        if (ball) {
+            const int src = __ffs(ball) - 1;
+            bk = 2 * src + (__shfl_sync(0xffffffffu, hit0 ? 0 : 1, src));
+        }
+        const float t_s = bk >= kHistBins - 1
+                              ? kNegInf
+                              : Mv - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
+                                    (fabsf(Mv) * 0x1p-18f + 0x1p-20f);
         float a_below = kNegInf;
 #pragma unroll
         for (int u = 0; u < KPT; ++u) {
@@ -824,9 +811,20 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
                 a_below = fmaxf(a_below, v);
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a_below = fmaxf(a_below, __shfl_xor_sync(0xffffffffu, a_below, o));
+        a_below = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_below)));
         if (lane == 0) s_abw[warp] = a_below;
+        if (tid == 0) {
+            s_th = fmaxf(s_thw[0], s_thw[1]);
+            if (!A.argmax) {
+                float mm = kNegInf;
+                for (int w = 0; w < SW; ++w) mm = fmaxf(mm, s_pmw[w]);
+                double t = 0.0;
+                for (int w = 0; w < SW; ++w)
+                    if (s_pmw[w] != kNegInf) t += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
+                s_mmax = mm;
+                s_tot = t;
+            }
+        }
     }
     __syncthreads();
     FRS_FTRACE(A, 9);
@@ -930,7 +928,6 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         a_bound = fmaxf(a_bound, s_abw[w]);
         any_bad |= s_badw[w];
     }
-    const float eps = s_eps;
     uint32_t why = (nsel > kCsMax || ns < kk) ? FRS_FLAG_CERT_OVERFLOW : 0u;
     if (any_bad) why |= FRS_FLAG_NONFINITE;
     const bool have0 = lane < ns, have1 = lane + 32 < ns;
@@ -1264,7 +1261,7 @@ int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapW32
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     auto kern = k_fast_finalize;
     const int TP = A.d / 8 + 8;
-    const size_t smem = (size_t)A.P.G * kListsPerCta * R * 8 + (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 2 + 64;
+    const size_t smem = (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 2 + 64;
     if (smem > ctx->smem_optin) return fail(FRS_ENOTSUP, "FAST finalize: hidden_dim too large");
     if (int st = configure(kern, smem)) return st;
     cudaLaunchConfig_t cfg{};
@@ -1296,6 +1293,41 @@ int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     return FRS_OK;
 }
 
+int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
+                 int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx, int32_t *out_full,
+                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, int NP, FastWs &w,
+                 cudaStream_t s);
+
+inline uint32_t __float_as_uint_host(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return u;
+}
+
+GraphEntry *graph_lookup(frs_ctx *ctx, const GraphKey &key) {
+    for (auto &e : ctx->graphs)
+        if (e.key == key) {
+            e.last_use = ++ctx->graph_clock;
+            return &e;
+        }
+    return nullptr;
+}
+
+void graph_insert(frs_ctx *ctx, const GraphKey &key) {
+    constexpr size_t kMaxGraphs = 64;
+    if (ctx->graphs.size() >= kMaxGraphs) {  // evict the least recently used
+        size_t lru = 0;
+        for (size_t q = 1; q < ctx->graphs.size(); ++q)
+            if (ctx->graphs[q].last_use < ctx->graphs[lru].last_use) lru = q;
+        if (ctx->graphs[lru].exec) cudaGraphExecDestroy(ctx->graphs[lru].exec);
+        ctx->graphs.erase(ctx->graphs.begin() + lru);
+    }
+    GraphEntry e;
+    e.key = key;
+    e.last_use = ++ctx->graph_clock;
+    ctx->graphs.push_back(e);
+}
+
 int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
                 int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx, int32_t *out_full,
                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
@@ -1319,17 +1351,85 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     FastWs w;
     int st = fast_workspace(ctx, NP, d, n, v_rows, w);
     if (st) return st;
-    CUtensorMap mapW, mapH;
-    CUtensorMap mapW32;
-    if ((st = make_map(&mapW, W, v_rows, d, BM)) || (st = make_map(&mapW32, W, v_rows, d, CH))) return st;
-    if ((st = make_map(&mapH, w.hs, 2 * NP, d, 2 * NP))) return st;
-
+    // Replay: the 4-kernel chain of a repeated call (same buffers, shapes and parameters) is
+    // captured once into a CUDA graph and relaunched with one cudaGraphLaunch, removing the
+    // per-call host cost of 3 tensor-map encodes and 4 kernel launches. A key is captured on
+    // its second use (the first runs eagerly and configures the kernels).
+    static const bool use_graphs = std::getenv("FRS_NO_GRAPH") == nullptr;
+    GraphKey key{};
+    if (use_graphs) {
+        const uint64_t vals[] = {reinterpret_cast<uint64_t>(h), static_cast<uint64_t>(n), static_cast<uint64_t>(d),
+                                 reinterpret_cast<uint64_t>(W), static_cast<uint64_t>(v_rows),
+                                 reinterpret_cast<uint64_t>(ordered_ids), static_cast<uint64_t>(k),
+                                 static_cast<uint64_t>(__float_as_uint_host(temperature)), static_cast<uint64_t>(argmax),
+                                 static_cast<uint64_t>(static_cast<uint32_t>(id_offset)),
+                                 reinterpret_cast<uint64_t>(out_ridx), reinterpret_cast<uint64_t>(out_full),
+                                 reinterpret_cast<uint64_t>(out_prob), reinterpret_cast<uint64_t>(out_rowmax),
+                                 reinterpret_cast<uint64_t>(out_total), reinterpret_cast<uint64_t>(out_flags),
+                                 reinterpret_cast<uint64_t>(ctx->fast_ws.ptr), reinterpret_cast<uint64_t>(ctx->fast_ctr.ptr),
+                                 reinterpret_cast<uint64_t>(ctx->trace.ptr)};
+        static_assert(sizeof(vals) / sizeof(vals[0]) == kGraphKeyWords, "graph key size");
+        for (int q = 0; q < kGraphKeyWords; ++q) key.w[q] = vals[q];
+        GraphEntry *e = graph_lookup(ctx, key);
+        if (e && e->exec) {
+            timing_begin(ctx, s);
+            FRS_CUDA_TRY(cudaGraphLaunch(e->exec, s));
+            timing_end(ctx, s);
+            ctx->launches += 4;
+            return FRS_OK;
+        }
+        if (e) {  // second use: capture the chain on the ctx's capture stream, then replay
+            if (!ctx->cap_stream) FRS_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+            FRS_CUDA_TRY(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+            const unsigned long long l0 = ctx->launches;
+            const bool timing = ctx->timing;
+            ctx->timing = false;
+            st = enqueue_fast(ctx, h, n, d, W, v_rows, ordered_ids, k, temperature, argmax, id_offset, out_ridx,
+                              out_full, out_prob, out_rowmax, out_total, out_flags, NP, w, ctx->cap_stream);
+            ctx->timing = timing;
+            ctx->launches = l0;
+            cudaGraph_t graph = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+            if (st) {
+                if (graph) cudaGraphDestroy(graph);
+                return st;
+            }
+            if (ce != cudaSuccess) return fail(FRS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+            const cudaError_t ie = cudaGraphInstantiate(&e->exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ie != cudaSuccess) {
+                e->exec = nullptr;
+                return fail(FRS_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+            }
+            timing_begin(ctx, s);
+            FRS_CUDA_TRY(cudaGraphLaunch(e->exec, s));
+            timing_end(ctx, s);
+            ctx->launches += 4;
+            return FRS_OK;
+        }
+        graph_insert(ctx, key);  // first use: eager below
+    }
     timing_begin(ctx, s);
     struct EndTiming {
         frs_ctx *c;
         cudaStream_t s;
         ~EndTiming() { timing_end(c, s); }
     } end_timing{ctx, s};
+    return enqueue_fast(ctx, h, n, d, W, v_rows, ordered_ids, k, temperature, argmax, id_offset, out_ridx, out_full,
+                        out_prob, out_rowmax, out_total, out_flags, NP, w, s);
+}
+
+// The FAST chain itself: k_hsplit -> k_fast_main -> k_fast_finalize -> k_fast_fallback.
+int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
+                 int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx, int32_t *out_full,
+                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, int NP, FastWs &w,
+                 cudaStream_t s) {
+    const int G = ctx->sm_count;
+    int st;
+    CUtensorMap mapW, mapH;
+    CUtensorMap mapW32;
+    if ((st = make_map(&mapW, W, v_rows, d, BM)) || (st = make_map(&mapW32, W, v_rows, d, CH))) return st;
+    if ((st = make_map(&mapH, w.hs, 2 * NP, d, 2 * NP))) return st;
     {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(std::min(ctx->sm_count, (NP * d / 4 + 127) / 128));
