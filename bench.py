@@ -38,6 +38,7 @@ def parse():
     p.add_argument("--v-sub", type=int, default=C2["v_sub"])
     p.add_argument("--rows", type=int, default=C2["rows"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-verify", action="store_true", help="skip the vocab-parallel verify measurement")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
 
@@ -279,6 +280,48 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # C4 (BASELINE configs[3]): vocab-parallel verify head at the Qwen-2.5-7B shape — each rank
+    # holds a contiguous vocabulary shard, computes its argmax pairs (K3), NCCL all-gathers them
+    # and merges (K5); at N=1 the single shard is the whole head (no collective).
+    verify_vp = None
+    if not args.no_verify:
+        qd, qV, qm = 3584, 152064, 61
+        start, count = api.vocab_shard(qV, world, rank)
+        gq = torch.Generator(device=dev).manual_seed(4242 + rank)
+        Wq = (torch.randn(count, qd, generator=gq, device=dev) * 0.02).to(torch.bfloat16)
+        hq = [rmsnorm_rows(torch.randn(qm, qd, generator=torch.Generator(device=dev).manual_seed(77 + j), device=dev))
+              for j in range(4)]
+
+        def vstep(j):
+            if world > 1:
+                return api.verify_head_argmax_vocab_parallel(ctx, hq[j % 4], Wq, qV, mode=mode)
+            return api.verify_head_argmax(ctx, hq[j % 4], Wq, id_offset=start, mode=mode)
+
+        for j in range(5):
+            vstep(j)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        vsteps = 50
+        v0.record()
+        for j in range(vsteps):
+            vstep(j)
+        v1.record()
+        torch.cuda.synchronize()
+        vus = v0.elapsed_time(v1) * 1000.0 / vsteps
+        if world > 1:
+            t = torch.tensor([vus], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            vus = float(t.item())
+        vbytes = count * qd * 2 + qm * qd * 4
+        verify_vp = {"workload": "vocab-parallel verify head, Qwen-2.5-7B shape (BASELINE configs[3])",
+                     "d": qd, "vocab": qV, "rows": qm, "shards": world, "shard_rows": count,
+                     "collective": "NCCL all_gather of (value, id) per row + K5 merge" if world > 1 else "none",
+                     "us_per_call": vus, "verify_calls_per_s": 1e6 / vus,
+                     "GBps_per_rank": vbytes / vus / 1e3, "frac_of_peak_per_rank": vbytes / vus / 1e3 / hbm_peak}
+        del Wq
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         slab32 = head.slab.float().cpu().numpy()
@@ -313,6 +356,7 @@ def main():
                     "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": 3 * n * k * 4,
                     "api": "frs_head_draft_host (C ABI, pinned host buffers, synchronous)"},
             "clocks": clocks, "gpu_launches": launches, "slab_build_ms": slab_build_ms, "row_flags": flag_counts,
+            "verify_vocab_parallel": verify_vp,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -130,6 +130,12 @@ FRS_API int frs_accept_greedy(frs_ctx *ctx, const int32_t *argmax_ids, const int
 FRS_API int frs_argmax_merge(frs_ctx *ctx, const float *vals, const int32_t *ids, int shards, int m,
                      float *out_val, int32_t *out_id, void *stream);
 
+/* Vocab-parallel verify helpers: the contiguous vocabulary shard of `rank`
+ * among `world` ranks, and the host twin of frs_argmax_merge for host-resident all-gathers. */
+FRS_API int frs_vocab_shard(int64_t V, int world, int rank, int64_t *start, int64_t *count);
+FRS_API int frs_argmax_merge_host(const float *vals, const int32_t *ids, int shards, int m, float *out_val,
+                                  int32_t *out_id);
+
 /* Row gather out[i,:] = table[tokens[i],:] (the identity draft layer of the head-path decode
  * loop). Device buffers. */
 FRS_API int frs_gather_rows(frs_ctx *ctx, const float *table, int64_t rows, int d, const int32_t *tokens,

@@ -71,6 +71,8 @@ SIGNATURES = [
     ("frs_accept_greedy", _I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
     ("frs_argmax_merge", _I, [_P, _P, _P, _I, _I, _P, _P, _P]),
     ("frs_gather_rows", _I, [_P, _P, _I64, _I, _P, _I, _P, _P]),
+    ("frs_vocab_shard", _I, [_I64, _I, _I, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("frs_argmax_merge_host", _I, [_P, _P, _I, _I, _P, _P]),
     ("frs_count_frequencies", _I, [_P, _I64, _I, _P]),
     ("frs_build_subset", _I, [_P, _I, _I, _P, _I, _P]),
     ("frs_subset_from_ranking", _I, [_P, _I, _I, _I, _P, _I, _P]),

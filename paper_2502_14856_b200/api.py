@@ -277,6 +277,46 @@ def argmax_merge(ctx: Context, vals: torch.Tensor, ids: torch.Tensor, stream=Non
     return ov, oi
 
 
+# ---------------------------------------------------------------- vocab-parallel verify
+def vocab_shard(vocab_size: int, world: int, rank: int):
+    """Contiguous vocabulary shard [start, start + count) of `rank` (frs_vocab_shard)."""
+    st, cnt = C.c_int64(), C.c_int64()
+    check(lib().frs_vocab_shard(vocab_size, world, rank, C.byref(st), C.byref(cnt)), "vocab_shard")
+    return int(st.value), int(cnt.value)
+
+
+def argmax_merge_host(vals: np.ndarray, ids: np.ndarray):
+    """Host twin of argmax_merge for host-resident gathered pairs [shards x m]."""
+    v = np.ascontiguousarray(vals, np.float32)
+    i = np.ascontiguousarray(ids, np.int32)
+    G, m = v.shape
+    ov, oi = np.empty(m, np.float32), np.empty(m, np.int32)
+    check(lib().frs_argmax_merge_host(_np_ptr(v), _np_ptr(i), G, m, _np_ptr(ov), _np_ptr(oi)), "argmax_merge_host")
+    return ov, oi
+
+
+def verify_head_argmax_vocab_parallel(ctx: Context, h: torch.Tensor, W_shard: torch.Tensor, vocab_size: int,
+                                      group=None, mode="fast", stream=None):
+    """Vocab-parallel verify head: this rank holds rows [start, start + count) of the LM head
+    (`vocab_shard`), computes the per-row argmax of its shard on the device (K3 with id_offset),
+    all-gathers the (value, id) pairs over `group` (NCCL on GPUs) and merges them by
+    (value desc, id asc) — argmax's lowest-id rule (kernels.cpp:117-121) — with K5."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    start, count = vocab_shard(vocab_size, world, rank)
+    if W_shard.shape[0] != count:
+        raise InvalidArgument(f"verify (vocab-parallel): rank {rank} holds {W_shard.shape[0]} rows, expected {count}")
+    ids, vals, flags = verify_head_argmax(ctx, h, W_shard, id_offset=start, mode=mode, stream=stream)
+    m = ids.numel()
+    gv = torch.empty((world, m), dtype=torch.float32, device=h.device)
+    gi = torch.empty((world, m), dtype=torch.int32, device=h.device)
+    dist.all_gather_into_tensor(gv, vals, group=group)
+    dist.all_gather_into_tensor(gi, ids, group=group)
+    ov, oi = argmax_merge(ctx, gv, gi, stream=stream)
+    return oi, ov, flags
+
+
 def gather_rows(ctx: Context, table: torch.Tensor, tokens: torch.Tensor, out: Optional[torch.Tensor] = None,
                 stream=None) -> torch.Tensor:
     n = int(tokens.numel())

@@ -874,6 +874,8 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             }
         }
         FRS_FTRACE(A, 12);
+        if (A.P.trace && threadIdx.x == 0)
+            A.P.trace[(size_t)A.P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + 13] = clock64();
         __syncthreads();
         if (tid < ((nmine * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
             const int cl = (tid >> 3) < nmine ? tid >> 3 : 0, l = tid & 7;
@@ -915,6 +917,8 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     // the leader prefetches the remap of S while the exact dots run
     if (cluster_rank() == 0 && tid < ns && A.ordered) s_ord[tid] = __ldg(A.ordered + dev::key_index(s_sel[tid]));
     FRS_FTRACE(A, 5);
+    if (A.P.trace && threadIdx.x == 0)
+        A.P.trace[(size_t)A.P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + 14] = clock64();
     // cluster barrier: release our DSMEM stores, acquire everyone's in the leader
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     if (cluster_rank() != 0) return;

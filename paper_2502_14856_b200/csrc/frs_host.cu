@@ -138,6 +138,37 @@ int frs_subset_from_ranking(const int32_t *ranked, int n_ranked, int size, int v
     return FRS_OK;
 }
 
+// Vocab-parallel verify: contiguous shard [start, start + count) of rank
+// `rank` among `world` (the first V % world ranks hold one extra row).
+int frs_vocab_shard(int64_t V, int world, int rank, int64_t *start, int64_t *count) {
+    FRS_REQUIRE(start && count, "vocab shard: null pointer");
+    FRS_REQUIRE(V >= 1 && world >= 1 && rank >= 0 && rank < world, "vocab shard: bad sizes");
+    const int64_t base = V / world, extra = V % world;
+    *count = base + (rank < extra ? 1 : 0);
+    *start = rank * base + std::min<int64_t>(rank, extra);
+    return FRS_OK;
+}
+
+// Host twin of K5 (frs_argmax_merge) for host-resident all-gather results: per row, the pair
+// with the largest value, ties to the lowest id — argmax's rule (kernels.cpp:117-121) over a
+// contiguous vocabulary split. -0 and +0 compare equal, NaN never wins over a number.
+int frs_argmax_merge_host(const float *vals, const int32_t *ids, int shards, int m, float *out_val,
+                          int32_t *out_id) {
+    FRS_REQUIRE(vals && ids && out_val && out_id, "argmax merge: null pointer");
+    FRS_REQUIRE(shards >= 1 && m >= 1, "argmax merge: sizes must be positive");
+    for (int r = 0; r < m; ++r) {
+        int bs = 0;
+        for (int g = 1; g < shards; ++g) {
+            const float v = vals[(size_t)g * m + r], b = vals[(size_t)bs * m + r];
+            const int32_t iv = ids[(size_t)g * m + r], ib = ids[(size_t)bs * m + r];
+            if (v > b || (v == b && iv < ib) || (b != b && v == v)) bs = g;
+        }
+        out_val[r] = vals[(size_t)bs * m + r];
+        out_id[r] = ids[(size_t)bs * m + r];
+    }
+    return FRS_OK;
+}
+
 // vocab.cpp:140-150
 int frs_coverage(const uint64_t *counts, int vocab_size, const int32_t *ordered, int v_sub, double *out) {
     FRS_REQUIRE(counts && ordered && out, "coverage: null pointer");

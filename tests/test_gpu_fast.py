@@ -176,3 +176,54 @@ def test_fast_certification_rate_c2(cuda_ctx, restatement):
             reasons[bit] = reasons.get(bit, 0) + int(((f & bit) != 0).sum())
     print(f"certification: {total - rec}/{total} rows certified; fallback reasons {reasons}")
     assert rec <= max(2, total // 20)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_vocab_parallel_emulated(cuda_ctx, restatement, G):
+    """emulate the G-GPU vocab-parallel verify on one GPU — each contiguous
+    shard through K3 with its id offset, the pairs stacked as an all-gather would, K5 merges —
+    bit-exact with the full-vocabulary argmax, including a tie straddling a shard boundary."""
+    rng = np.random.default_rng(40 + G)
+    V, d, m = 9001, 512, 13
+    Wf = (rng.standard_normal((V, d)) * 0.02).astype(np.float32)
+    h = rmsnorm(rng.standard_normal((m, d)))
+    best = restatement.verify_argmax(h, torch.from_numpy(Wf).to(torch.bfloat16).float().numpy())[0]
+    s_last, _ = api.vocab_shard(V, G, G - 1)
+    Wf[s_last + 5] = Wf[best[0]]  # the same max in the last shard: the lower id must win
+    W = torch.from_numpy(Wf).to(torch.bfloat16).cuda()
+    hd = torch.from_numpy(h).cuda()
+    vals, ids = [], []
+    for r in range(G):
+        st, cnt = api.vocab_shard(V, G, r)
+        i_, v_, _ = api.verify_head_argmax(cuda_ctx, hd, W[st:st + cnt].contiguous(), id_offset=st, mode="fast")
+        vals.append(v_)
+        ids.append(i_)
+    mv, mi = api.argmax_merge(cuda_ctx, torch.stack(vals), torch.stack(ids))
+    rid, rval = restatement.verify_argmax(h, W.float().cpu().numpy())
+    assert np.array_equal(mi.cpu().numpy(), rid)
+    assert np.array_equal(mv.cpu().numpy(), rval)
+
+
+def test_vocab_parallel_nccl_world1(cuda_ctx, restatement):
+    """The NCCL path of api.verify_head_argmax_vocab_parallel (all_gather + K5) on a 1-rank group."""
+    import socket
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(3)
+        V, d, m = 5000, 256, 7
+        W = torch.from_numpy((rng.standard_normal((V, d)) * 0.02).astype(np.float32)).to(torch.bfloat16)
+        h = rmsnorm(rng.standard_normal((m, d)))
+        ids, vals, _ = api.verify_head_argmax_vocab_parallel(cuda_ctx, torch.from_numpy(h).cuda(), W.cuda(), V)
+        rid, rval = restatement.verify_argmax(h, W.float().numpy())
+        assert np.array_equal(ids.cpu().numpy(), rid)
+        assert np.array_equal(vals.cpu().numpy(), rval)
+    finally:
+        dist.destroy_process_group()

@@ -26,7 +26,8 @@ SLOTS = {0: "setup done", 1: "producer: before griddep_wait", 9: "producer: afte
          25: "loop done w5", 26: "loop done w6", 27: "loop done w7"}
 FSLOTS = {0: "fin start", 1: "fin h loaded", 2: "fin after griddep_wait", 3: "fin partials merged",
           4: "fin S selected", 5: "fin recompute done", 6: "fin last: certified?", 7: "fin last: written",
-          8: "fin v' ranked", 9: "fin S collected",
+          8: "fin hist done", 9: "fin S collected", 10: "fin leader: after cluster wait",
+          11: "fin leader: mx", 13: "fin leader: e-keys ranked", 14: "fin leader: ties", 15: "fin leader: certified",
           12: "fin cand rows staged"}
 
 
@@ -79,6 +80,13 @@ def main():
         for s_, name in {0: "hsplit start", 1: "hsplit cta0 end", 2: "fallback start", 3: "fallback exit"}.items():
             if xt[s_] > 0:
                 row[f"X{s_} {name}"] = round(float((xt[s_] - t0) / 1000.0), 2)
+        # clock64 vs globaltimer over the exact-recompute phase (slots 12 -> 5; cycles in 13/14)
+        sel = (ft[:, 12] > 0) & (ft[:, 5] > ft[:, 12])
+        if sel.any():
+            ns_ = (ft[sel, 5] - ft[sel, 12]).astype(np.float64)
+            cyc = (ft[sel, 14] - ft[sel, 13]).astype(np.float64)
+            row["recompute cycles/ns (SM GHz)"] = [round(float(np.median(cyc / ns_)), 3), round(float(np.median(cyc)), 0),
+                                                   round(float(np.median(ns_)), 0)]
         res.append(row)
     for k in res[-1]:
         print(k.ljust(40), res[-1][k])

@@ -1,0 +1,156 @@
+#!/usr/bin/env python3
+"""Secondary measurements on one B200 (JSON lines to stdout), for SURVEY.md §8(d) rows the
+headline bench line does not carry:
+
+  draft   : FAST (and EXACT) draft level at the Llama-3-8B shape, V_sub sweep (C3)
+  verify  : FAST verify head (argmax over the full vocabulary) at C2 (61 rows, V=128256,
+            d=4096) and the C4 Qwen-2.5-7B shape split into 1/2/4/8 contiguous vocabulary
+            shards (per-shard device time = what one GPU of a vocab-parallel group spends)
+  decode  : head-path decode loop: build_draft_tree (6 levels, width 10,
+            60 tokens, hidden state = identity draft layer over an embedding table) +
+            verify_greedy over the full head, tokens/s and mean accepted length
+
+Device times are CUDA events over K back-to-back calls; slabs smaller than 4x L2 rotate
+over enough copies that each call streams from HBM.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2502_14856_b200 import api  # noqa: E402
+
+L2 = 126 * 2 ** 20
+PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6650.0
+
+
+def rms(x):
+    return (x * torch.rsqrt(x.double().pow(2).mean(dim=1, keepdim=True) + 1e-5).float()).contiguous()
+
+
+def timed(fn, iters, warm=5):
+    for _ in range(warm):
+        fn(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(iters):
+        fn(i)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1000.0 / iters
+
+
+def draft_sweep(ctx, dev, modes):
+    d, V, n, k = 4096, 128256, 10, 10
+    g = torch.Generator(device=dev).manual_seed(1234)
+    W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16).float()
+    ranked = np.random.default_rng(1234).permutation(V).astype(np.int32)
+    pool = [rms(torch.randn(n, d, generator=g, device=dev)) for _ in range(64)]
+    h_in = torch.empty((n, d), device=dev)
+    for v_sub in (8192, 16384, 32768, 65536, 128256):
+        sub = api.subset_from_ranking(ranked, v_sub, V, forced=[0, 1])
+        slab_bytes = v_sub * d * 2
+        copies = max(1, -(-4 * L2 // slab_bytes))
+        heads = [api.restrict_lm_head(ctx, W, sub, dtype="bf16") for _ in range(copies)]
+        for mode in modes:
+            out = api.draft_head_topk(ctx, pool[0], heads[0], k, mode=mode)
+
+            def step(i):
+                h_in.copy_(pool[i % len(pool)])
+                api.draft_head_topk(ctx, h_in, heads[i % copies], k, mode=mode, out=out)
+
+            us = timed(step, 200 if mode == "fast" else 20)
+            alg = slab_bytes + n * d * 4 + n * k * 12
+            print(json.dumps({"sweep": "draft", "mode": mode, "v_sub": v_sub, "d": d, "rows": n, "k": k,
+                              "slab_copies": copies, "us_per_level": us, "alg_bytes": alg,
+                              "GBps": alg / us / 1e3, "frac_of_peak": alg / us / 1e3 / PEAK}), flush=True)
+        del heads
+        torch.cuda.empty_cache()
+    del W
+
+
+def verify_sweep(ctx, dev):
+    for name, d, V, m in (("C2 Llama-3-8B", 4096, 128256, 61), ("C4 Qwen-2.5-7B", 3584, 152064, 61)):
+        g = torch.Generator(device=dev).manual_seed(7)
+        W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+        hs = [rms(torch.randn(m, d, generator=g, device=dev)) for _ in range(8)]
+        shard_list = (1,) if name.startswith("C2") else (1, 2, 4, 8)
+        for G in shard_list:
+            per = -(-V // G)
+            # shard 0 of G (all shards have the same size up to one row): per-GPU device time
+            Ws = W[:per].contiguous()
+            copies = max(1, -(-4 * L2 // (per * d * 2)))
+            shards = [Ws] + [Ws.clone() for _ in range(copies - 1)]
+
+            def step(i):
+                api.verify_head_argmax(ctx, hs[i % len(hs)], shards[i % copies], id_offset=0, mode="fast")
+
+            us = timed(step, 50)
+            alg = per * d * 2 + m * d * 4
+            print(json.dumps({"sweep": "verify", "shape": name, "shards": G, "rows": m, "d": d, "vocab": V,
+                              "shard_rows": per, "us_per_shard": us, "alg_bytes": alg, "GBps": alg / us / 1e3,
+                              "frac_of_peak": alg / us / 1e3 / PEAK}), flush=True)
+            del shards, Ws
+            torch.cuda.empty_cache()
+        del W
+
+
+def decode_loop(ctx, dev, iters):
+    d, V, v_sub = 4096, 128256, 32768
+    g = torch.Generator(device=dev).manual_seed(1234)
+    W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16).float()
+    ranked = np.random.default_rng(1234).permutation(V).astype(np.int32)
+    sub = api.subset_from_ranking(ranked, v_sub, V, forced=[0, 1])
+    head = api.DeviceHead(ctx, W, sub, dtype="bf16")
+    E = rms(torch.randn(V, d, generator=g, device=dev))  # identity draft layer: hidden = rmsnorm(E[token])
+    Wb = W.to(torch.bfloat16)
+    del W
+    params = api.DraftParams(10, 6, 60)
+    stats = api.AcceptanceStats()
+    token = 1
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    emitted_total = 0
+    for it in range(iters):
+        tree = head.build_draft_tree(token, params, mode="fast", hidden_table=E)
+        toks = torch.from_numpy(np.concatenate([[token], tree.tokens]).astype(np.int64)).to(dev)
+        hv = E.index_select(0, toks).contiguous()  # root + 60 node rows (same identity layer)
+        outc = api.verify_greedy(ctx, hv, Wb, tree, mode="fast")
+        stats.add(outc.accepted_length())
+        emitted_total += outc.accepted_length()
+        token = int(outc.emitted[-1])
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    print(json.dumps({"sweep": "decode", "config": "head path: draft tree depth 6 width 10, 60 draft tokens, "
+                      "verify 61 rows over V=128256 (bf16), identity draft layer", "iterations": iters,
+                      "tokens_per_s": emitted_total / el, "ms_per_iteration": 1000 * el / iters,
+                      "mean_accepted_length": stats.mean_accepted_length}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--what", default="draft,verify,decode")
+    ap.add_argument("--exact", action="store_true", help="also time the EXACT draft level")
+    ap.add_argument("--decode-iters", type=int, default=100)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    ctx = api.Context(0)
+    what = a.what.split(",")
+    if "draft" in what:
+        draft_sweep(ctx, dev, ["fast", "exact"] if a.exact else ["fast"])
+    if "verify" in what:
+        verify_sweep(ctx, dev)
+    if "decode" in what:
+        decode_loop(ctx, dev, a.decode_iters)
+
+
+if __name__ == "__main__":
+    main()
