@@ -611,6 +611,15 @@ struct FinArgs {
 //   4. the last CTA of the row to arrive selects the top-k by (prob desc, index asc) and
 //      certifies it (see the file comment); rows that cannot be certified are queued for the
 //      grid-wide exact fallback (k_fast_fallback).
+// Row pitch (floats) of the transposed per-lane-chain operand tiles of the exact recompute: a
+// multiple of 4 (16-byte vector loads) with pitch % 8 == 4, so the 8 lanes of a quarter-warp
+// hit 8 distinct 4-bank groups (a 2-way conflict at pitch % 8 == 0 doubled the loop time).
+__host__ __device__ inline int fin_pitch(int T) {
+    int tp = (T + 3) & ~3;
+    if ((tp & 7) != 4) tp += 4;
+    return tp;
+}
+
 constexpr int kMaxLists = 1024;  // L = 4 G <= 1024 lists of R keys per hidden row
 constexpr int kHistBins = 64;     // threshold histogram of (M - v) / bw: 48 linear bins, then
                                   // 4 bins per octave, the last one a catch-all
@@ -630,9 +639,9 @@ __device__ __forceinline__ float hist_edge(int j) {
 __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     extern __shared__ __align__(16) uint8_t fsm_raw[];
     const int T = A.d >> 3;           // dot_f32 steps per lane chain (d % 8 == 0 on FAST)
-    const int TP = T + 8;             // padded chain pitch (elements): 16-byte aligned rows
+    const int TP = fin_pitch(T);      // padded chain pitch (elements): 16-byte aligned rows
     float *ht = reinterpret_cast<float *>(fsm_raw);                                   // [8][TP]
-    unsigned short *wt = reinterpret_cast<unsigned short *>(ht + 8 * TP);            // [8 cand][8][TP]
+    float *wt = ht + 8 * TP;                        // [8 cand][8][TP] fp32 (bf16 widened, exact)
     __shared__ unsigned long long s_S[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
     __shared__ double s_hn2[kFinThreads / 32], s_tot;
     __shared__ float s_mmax, s_th, s_abw[kFinThreads / 32], s_pmw[4], s_thw[2], s_w2w[2];
@@ -863,12 +872,12 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
                 for (int u = 0; u < TPT; ++u) {
                     const int t = t0 + tid + u * kFinThreads;
                     if (!(c < nmine && t < T)) continue;
-                    unsigned short *dst = wt + (size_t)c * 8 * TP + t;
+                    float *dst = wt + (size_t)c * 8 * TP + t;
                     const uint32_t w4[4] = {v[c][u].x, v[c][u].y, v[c][u].z, v[c][u].w};
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        dst[(2 * q) * TP] = static_cast<unsigned short>(w4[q] & 0xffffu);
-                        dst[(2 * q + 1) * TP] = static_cast<unsigned short>(w4[q] >> 16);
+                    for (int q = 0; q < 4; ++q) {  // bf16 -> fp32 is exact
+                        dst[(2 * q) * TP] = __uint_as_float(w4[q] << 16);
+                        dst[(2 * q + 1) * TP] = __uint_as_float(w4[q] & 0xffff0000u);
                     }
                 }
             }
@@ -880,29 +889,24 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         if (tid < ((nmine * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
             const int cl = (tid >> 3) < nmine ? tid >> 3 : 0, l = tid & 7;
             const float4 *hp = reinterpret_cast<const float4 *>(ht + l * TP);
-            const uint4 *wp = reinterpret_cast<const uint4 *>(wt + ((size_t)cl * 8 + l) * TP);
+            const float4 *wp = reinterpret_cast<const float4 *>(wt + ((size_t)cl * 8 + l) * TP);
             float s = 0.0f;
             const int T8 = T / 8;
-            uint4 wv = wp[0];
-            float4 h0 = hp[0], h1 = hp[1];
+            float4 w0 = wp[0], w1 = wp[1], h0 = hp[0], h1 = hp[1];
             for (int t8 = 0; t8 < T8; ++t8) {  // 8 steps per iteration; next operands prefetched
                 const int tn = t8 + 1 < T8 ? t8 + 1 : t8;
-                const uint4 wn = wp[tn];
-                const float4 g0 = hp[2 * tn], g1 = hp[2 * tn + 1];
+                const float4 v0 = wp[2 * tn], v1 = wp[2 * tn + 1], g0 = hp[2 * tn], g1 = hp[2 * tn + 1];
                 const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-                const uint32_t wu[4] = {wv.x, wv.y, wv.z, wv.w};
+                const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float w = __uint_as_float(q & 1 ? (wu[q >> 1] & 0xffff0000u) : (wu[q >> 1] << 16));
-                    s = __fadd_rn(s, __fmul_rn(hv[q], w));  // kernels.cpp:17-26 lane chain
-                }
-                wv = wn;
+                for (int q = 0; q < 8; ++q) s = __fadd_rn(s, __fmul_rn(hv[q], wv[q]));  // kernels.cpp:17-26 lane chain
+                w0 = v0;
+                w1 = v1;
                 h0 = g0;
                 h1 = g1;
             }
             for (int t = T8 * 8; t < T; ++t)  // T % 8 steps
-                s = __fadd_rn(s, __fmul_rn(ht[l * TP + t],
-                                           __uint_as_float(static_cast<uint32_t>(wt[((size_t)cl * 8 + l) * TP + t]) << 16)));
+                s = __fadd_rn(s, __fmul_rn(ht[l * TP + t], wt[((size_t)cl * 8 + l) * TP + t]));
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));  // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7))
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
@@ -1264,8 +1268,8 @@ int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapW32
 
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     auto kern = k_fast_finalize;
-    const int TP = A.d / 8 + 8;
-    const size_t smem = (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 2 + 64;
+    const int TP = fin_pitch(A.d / 8);
+    const size_t smem = (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 4 + 64;
     if (smem > ctx->smem_optin) return fail(FRS_ENOTSUP, "FAST finalize: hidden_dim too large");
     if (int st = configure(kern, smem)) return st;
     cudaLaunchConfig_t cfg{};
