@@ -163,6 +163,8 @@ struct Partials {
     float *pth;                // [NP][L] bound: every list row not in pkey has approx logit <= pth
     unsigned long long *pkey;  // [NP][L][R] the list's best R (approx value, index) keys, descending
     float *pw2;                // [2G] max squared L2 norm of slab rows (per CTA and norm warp)
+    float *logits;             // LOGITS mode: approximate logits [n][ld_logits] (batched drafting)
+    int ld_logits;
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
 };
@@ -243,7 +245,9 @@ __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k)
     return (static_cast<unsigned long long>(mh) << 32) | ml;
 }
 
-template <int NP, bool SOFTMAX>
+// LOGITS: the epilogue writes the approximate logits of every (hidden row, slab row) to
+// P.logits instead of tracking lists (batched drafting with many hidden rows, k_fast_select).
+template <int NP, bool SOFTMAX, bool LOGITS = false>
 __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     k_fast_main(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapW32,
                 const __grid_constant__ CUtensorMap mapH, int n,
@@ -453,6 +457,15 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
+                if constexpr (LOGITS) {  // coalesced: the warp's 32 lanes are 32 consecutive slab rows
+#pragma unroll
+                    for (int r = 0; r < CG; ++r) {
+                        const int i = c0 + r;
+                        if (valid && i < n)
+                            P.logits[(size_t)i * P.ld_logits + row] = __uint_as_float(hi[r]) + __uint_as_float(lo[r]);
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int r = 0; r < CG; ++r) {
                     const int rr = cg * CG + r, i = c0 + r;
@@ -497,6 +510,10 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         //      slab rows and their top-R keys + a bound for the rest. Warp-local only: the
         //      max by one REDUX on order-preserving bits, the list by R + 1 tournament rounds
         //      over the lanes' sorted (b1, b2) heads.
+        if constexpr (LOGITS) {
+            (void)b1;
+            (void)bnd;
+        } else {
         const int list = cta * kListsPerCta + q, L = G * kListsPerCta;
         // rows outer-unrolled inside every step, so the RPW independent REDUX chains overlap
         if constexpr (SOFTMAX) {
@@ -547,6 +564,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             if (lane < R) P.pkey[((size_t)i * L + list) * R + lane] = out[r];
             if (lane == R) P.pth[(size_t)i * L + list] = fmaxf(out[r] ? dev::key_value(out[r]) : kNegInf, bmax[r]);
         }
+        }  // !LOGITS
         if (threadIdx.x == 128) FRS_TRACE(P, 18);
     }
     __syncthreads();  // every TMEM read is done
@@ -634,6 +652,137 @@ __device__ __forceinline__ int hist_bin(float r) {  // r >= 0
 // upper edge of bin j - 1 (= lower bound of r over bins >= j), with slack for log2f rounding
 __device__ __forceinline__ float hist_edge(int j) {
     return j <= 48 ? static_cast<float>(j) : 48.0f * exp2f(0.25f * static_cast<float>(j - 48)) * (1.0f + 0x1p-10f);
+}
+
+// Selection + certification of one hidden row (warp 0 only; the other lanes of the CTA are
+// gone). fin[0..ns) are the exact logits of the candidate set S (keys sel[], canonical order),
+// nsel the untruncated |S|; a_bound bounds every approximate logit outside S, eps the FAST
+// error. Writes the row's outputs, or queues it for k_fast_fallback with the reason.
+__device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int nsel, int kk, float a_bound, float eps,
+                                            bool any_bad, double tot_approx, float mmax_approx, const float *s_fin,
+                                            const unsigned long long *s_sel, unsigned long long *s_sorted,
+                                            unsigned long long *s_tab, int32_t *s_spos, const int32_t *s_ord) {
+    const int lane = threadIdx.x & 31;
+    const float kNegInf = -__int_as_float(0x7f800000);
+    const double s_tot = tot_approx;
+    const float s_mmax = mmax_approx;
+    uint32_t why = (nsel > kCsMax || ns < kk) ? FRS_FLAG_CERT_OVERFLOW : 0u;
+    if (any_bad) why |= FRS_FLAG_NONFINITE;
+    const bool have0 = lane < ns, have1 = lane + 32 < ns;
+    const float l0 = have0 ? s_fin[lane] : kNegInf;
+    const float l1 = have1 ? s_fin[lane + 32] : kNegInf;
+    const int j0 = have0 ? dev::key_index(s_sel[lane]) : 0, j1 = have1 ? dev::key_index(s_sel[lane + 32]) : 0;
+    if (A.argmax) {
+        unsigned long long bv = 0ull;
+        if (have0) bv = dev::value_key(l0, j0);
+        if (have1) {
+            const unsigned long long k1 = dev::value_key(l1, j1);
+            bv = k1 > bv ? k1 : bv;
+        }
+        const unsigned long long best = warp_max_key(bv);
+        const float lb = dev::key_value(best);
+        if (!(a_bound + eps < lb || a_bound == kNegInf)) why |= FRS_FLAG_CERT_BOUND;
+        if (why) {
+            if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
+            return;
+        }
+        if (lane == 0) {
+            A.out_full[i] = A.id_offset + dev::key_index(best);
+            if (A.out_prob) A.out_prob[i] = lb;
+            if (A.out_flags) A.out_flags[i] = 0u;
+        }
+        FRS_FTRACE(A, 7);
+        return;
+    }
+    s_tab[lane] = dev::kExp2fTable[lane];
+    __syncwarp();
+    const unsigned long long *tab = s_tab;
+    const float x0 = __fdiv_rn(l0, A.temperature), x1 = __fdiv_rn(l1, A.temperature);
+    float mx = fmaxf(x0, x1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const unsigned long long e0 = have0 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x0, mx), tab), j0) : 0ull;
+    const unsigned long long e1 = have1 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x1, mx), tab), j1) : 0ull;
+    // rank of each e-key among the ns (distinct: the index is part of the key)
+    int r0 = 0, r1 = 0;
+    for (int c = 0; c < ns; ++c) {
+        const unsigned long long o = __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31);
+        r0 += o > e0;
+        r1 += o > e1;
+    }
+    if (have0) {
+        s_sorted[r0] = e0;
+        s_spos[r0] = lane;
+    }
+    if (have1) {
+        s_sorted[r1] = e1;
+        s_spos[r1] = lane + 32;
+    }
+    __syncwarp();
+    const int want = min(ns, kk + 1);
+    // near ties (within 4 ulps) among the selected and at the k boundary: the reference's
+    // (prob, index) order could depend on the exact denominator
+    bool tie = false;
+    if (lane + 1 < want) {
+        const float ea = __uint_as_float(static_cast<uint32_t>(s_sorted[lane] >> 32));
+        const float eb = __uint_as_float(static_cast<uint32_t>(s_sorted[lane + 1] >> 32));
+        tie = ea != eb && ea <= eb * (1.0f + 0x1p-21f);
+    }
+    if (__any_sync(0xffffffffu, tie)) why |= FRS_FLAG_CERT_TIE;
+    if (!why && a_bound != kNegInf) {  // every non-recomputed row stays strictly below the k-th
+        const float x_ub = __fdiv_ru(a_bound + eps, A.temperature) * (1.0f + 0x1p-20f) + 0x1p-20f;
+        if (!(x_ub < mx)) {
+            why |= FRS_FLAG_CERT_BOUND;
+        } else {
+            const float e_ub = dev::expf_glibc(x_ub - mx, tab) * (1.0f + 0x1p-20f);
+            const float e_k = __uint_as_float(static_cast<uint32_t>(s_sorted[kk - 1] >> 32));
+            if (!(e_ub * (1.0f + 0x1p-21f) < e_k)) why |= FRS_FLAG_CERT_BOUND;
+        }
+    }
+    if (why) {
+        if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
+        return;
+    }
+    // tot = sum exp(x_j - M) over the approximate logits; rescale to the exact max
+    const double total = s_tot * static_cast<double>(exp2f((s_mmax - mx) * 1.4426950408889634f));
+    const float inv = __double2float_rn(1.0 / total);
+    if (lane < A.k) {
+        const size_t o = (size_t)i * A.k + lane;
+        if (lane < kk) {
+            const unsigned long long key = s_sorted[lane];
+            const int j = dev::key_index(key);
+            A.out_ridx[o] = j;
+            A.out_full[o] = A.ordered ? s_ord[s_spos[lane]] : j;
+            A.out_prob[o] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(key >> 32)), inv);
+        } else {
+            A.out_ridx[o] = -1;
+            A.out_full[o] = -1;
+            A.out_prob[o] = 0.0f;
+        }
+    }
+    if (A.k > 32) {  // k up to 64
+        const int r = lane + 32;
+        if (r < A.k) {
+            const size_t o = (size_t)i * A.k + r;
+            if (r < kk) {
+                const unsigned long long key = s_sorted[r];
+                const int j = dev::key_index(key);
+                A.out_ridx[o] = j;
+                A.out_full[o] = A.ordered ? s_ord[s_spos[r]] : j;
+                A.out_prob[o] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(key >> 32)), inv);
+            } else {
+                A.out_ridx[o] = -1;
+                A.out_full[o] = -1;
+                A.out_prob[o] = 0.0f;
+            }
+        }
+    }
+    if (lane == 0) {
+        if (A.out_rowmax) A.out_rowmax[i] = mx;
+        if (A.out_total) A.out_total[i] = total;
+        if (A.out_flags) A.out_flags[i] = 0u;
+    }
+    FRS_FTRACE(A, 7);
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
@@ -936,123 +1085,202 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         a_bound = fmaxf(a_bound, s_abw[w]);
         any_bad |= s_badw[w];
     }
-    uint32_t why = (nsel > kCsMax || ns < kk) ? FRS_FLAG_CERT_OVERFLOW : 0u;
-    if (any_bad) why |= FRS_FLAG_NONFINITE;
-    const bool have0 = lane < ns, have1 = lane + 32 < ns;
-    const float l0 = have0 ? s_fin[lane] : kNegInf;
-    const float l1 = have1 ? s_fin[lane + 32] : kNegInf;
-    const int j0 = have0 ? dev::key_index(s_sel[lane]) : 0, j1 = have1 ? dev::key_index(s_sel[lane + 32]) : 0;
-    if (A.argmax) {
-        unsigned long long bv = 0ull;
-        if (have0) bv = dev::value_key(l0, j0);
-        if (have1) {
-            const unsigned long long k1 = dev::value_key(l1, j1);
-            bv = k1 > bv ? k1 : bv;
+    select_certify(A, i, ns, nsel, kk, a_bound, eps, any_bad != 0, s_tot, s_mmax, s_fin, s_sel, s_sorted, s_tab,
+                   s_spos, s_ord);
+}
+
+// Batched drafting (n > 16 hidden rows): per hidden row one CTA over the approximate logits
+// row written by k_fast_main<NP,false,true> (L2-resident: n x V_sub x 4 B). Three passes over
+// the row (max; Σexp + threshold histogram; candidate set S), exact recompute of S in chunks
+// of 8 candidates (dot_f32 order), then the same selection + certification as the finalize
+// (select_certify). Every row outside S has approx <= a_below, so a_bound = a_below.
+constexpr int kSelThreads = 512;
+
+__global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
+    extern __shared__ __align__(16) uint8_t ssm_raw[];
+    const int T = A.d >> 3, TP = fin_pitch(T);
+    float *ht = reinterpret_cast<float *>(ssm_raw);  // [8][TP]
+    float *wt = ht + 8 * TP;                          // [8 cand][8][TP]
+    __shared__ unsigned long long s_S[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
+    __shared__ float s_fin[kCsMax], s_redf[kSelThreads / 32], s_abw[kSelThreads / 32];
+    __shared__ double s_redd[kSelThreads / 32], s_hn2[kSelThreads / 32];
+    __shared__ unsigned s_hist[kHistBins];
+    __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
+    __shared__ int s_nsel, s_badw[kSelThreads / 32];
+    __shared__ float s_ts;
+    griddep_launch();
+
+    const int i = blockIdx.x, tid = threadIdx.x;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = tid & 31;
+    constexpr int NW = kSelThreads / 32;
+    const float kNegInf = -__int_as_float(0x7f800000);
+    {  // the hidden row (independent of the main kernel): ht[l][t] = h[8t + l], |h|^2, finiteness
+        const float4 *hv = reinterpret_cast<const float4 *>(A.h + (size_t)i * A.d);
+        double hn2 = 0.0;
+        int bad = 0;
+        for (int e = tid; e < 2 * T; e += kSelThreads) {
+            const float4 w = __ldg(hv + e);
+            const int t = e >> 1, l0 = (e & 1) * 4;
+            ht[(l0 + 0) * TP + t] = w.x;
+            ht[(l0 + 1) * TP + t] = w.y;
+            ht[(l0 + 2) * TP + t] = w.z;
+            ht[(l0 + 3) * TP + t] = w.w;
+            bad |= !isfinite(w.x) | !isfinite(w.y) | !isfinite(w.z) | !isfinite(w.w);
+            hn2 += static_cast<double>(w.x) * w.x + static_cast<double>(w.y) * w.y +
+                   static_cast<double>(w.z) * w.z + static_cast<double>(w.w) * w.w;
         }
-        const unsigned long long best = warp_max_key(bv);
-        const float lb = dev::key_value(best);
-        if (!(a_bound + eps < lb || a_bound == kNegInf)) why |= FRS_FLAG_CERT_BOUND;
-        if (why) {
-            if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
-            return;
-        }
-        if (lane == 0) {
-            A.out_full[i] = A.id_offset + dev::key_index(best);
-            if (A.out_prob) A.out_prob[i] = lb;
-            if (A.out_flags) A.out_flags[i] = 0u;
-        }
-        FRS_FTRACE(A, 7);
-        return;
-    }
-    s_tab[lane] = dev::kExp2fTable[lane];
-    __syncwarp();
-    const unsigned long long *tab = s_tab;
-    const float x0 = __fdiv_rn(l0, A.temperature), x1 = __fdiv_rn(l1, A.temperature);
-    float mx = fmaxf(x0, x1);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const unsigned long long e0 = have0 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x0, mx), tab), j0) : 0ull;
-    const unsigned long long e1 = have1 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x1, mx), tab), j1) : 0ull;
-    // rank of each e-key among the ns (distinct: the index is part of the key)
-    int r0 = 0, r1 = 0;
-    for (int c = 0; c < ns; ++c) {
-        const unsigned long long o = __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31);
-        r0 += o > e0;
-        r1 += o > e1;
+        for (int o = 16; o > 0; o >>= 1) hn2 += __shfl_xor_sync(0xffffffffu, hn2, o);
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            s_hn2[warp] = hn2;
+            s_badw[warp] = bad;
+        }
+        if (tid == 0) s_nsel = 0;
+        if (tid < kHistBins) s_hist[tid] = 0u;
     }
-    if (have0) {
-        s_sorted[r0] = e0;
-        s_spos[r0] = lane;
+    griddep_wait();
+    const float *Lr = A.P.logits + (size_t)i * A.P.ld_logits;
+    const int v = A.v_rows;
+    const float inv_t = 1.0f / A.temperature;
+    // ---- pass 1: max approximate logit; max |W_j|^2 (norm warps of the main kernel)
+    float mx = kNegInf, w2 = 0.0f;
+    for (int j = tid; j < v; j += kSelThreads) mx = fmaxf(mx, __ldcg(Lr + j));
+    for (int c = tid; c < 2 * A.P.G; c += kSelThreads) w2 = fmaxf(w2, __ldcg(A.P.pw2 + c));
+    mx = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(mx)));
+    w2 = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(w2)));
+    if (lane == 0) {
+        s_redf[warp] = mx;
+        s_abw[warp] = w2;
     }
-    if (have1) {
-        s_sorted[r1] = e1;
-        s_spos[r1] = lane + 32;
+    __syncthreads();
+    float M = kNegInf, W2 = 0.0f;
+    double h2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        M = fmaxf(M, s_redf[w]);
+        W2 = fmaxf(W2, s_abw[w]);
+        h2 += s_hn2[w];
     }
-    __syncwarp();
-    const int want = min(ns, kk + 1);
-    // near ties (within 4 ulps) among the selected and at the k boundary: the reference's
-    // (prob, index) order could depend on the exact denominator
-    bool tie = false;
-    if (lane + 1 < want) {
-        const float ea = __uint_as_float(static_cast<uint32_t>(s_sorted[lane] >> 32));
-        const float eb = __uint_as_float(static_cast<uint32_t>(s_sorted[lane + 1] >> 32));
-        tie = ea != eb && ea <= eb * (1.0f + 0x1p-21f);
+    const float eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(W2) * 1.001)) * fast_gamma(A.d) * 1.01f;
+    const float bw = fmaxf(0.5f * eps, fabsf(M) * 0x1p-20f + 0x1p-30f), rbw = 1.0f / bw;
+    // ---- pass 2: Σ exp(x - max x) in the approximate domain + the threshold histogram
+    const float Mx = M * inv_t;
+    double tot = 0.0;
+    for (int j0 = 0; j0 < v; j0 += kSelThreads) {
+        const int j = j0 + tid;
+        const float a = j < v ? __ldcg(Lr + j) : kNegInf;
+        if (j < v) tot += static_cast<double>(exp2f((a * inv_t - Mx) * 1.4426950408889634f));
+        const int bin = j < v ? hist_bin((M - a) * rbw) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
     }
-    if (__any_sync(0xffffffffu, tie)) why |= FRS_FLAG_CERT_TIE;
-    if (!why && a_bound != kNegInf) {  // every non-recomputed row stays strictly below the k-th
-        const float x_ub = __fdiv_ru(a_bound + eps, A.temperature) * (1.0f + 0x1p-20f) + 0x1p-20f;
-        if (!(x_ub < mx)) {
-            why |= FRS_FLAG_CERT_BOUND;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) s_redd[warp] = tot;
+    __syncthreads();
+    const int kk = min(A.k, v);
+    if (warp == 0) {  // the first bin whose cumulative count reaches kk
+        const unsigned c0 = s_hist[2 * lane], c1 = s_hist[2 * lane + 1];
+        unsigned incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const unsigned excl = incl - c0 - c1;
+        const bool hit0 = excl < static_cast<unsigned>(kk) && excl + c0 >= static_cast<unsigned>(kk);
+        const bool hit1 = !hit0 && excl + c0 < static_cast<unsigned>(kk) && incl >= static_cast<unsigned>(kk);
+        const unsigned ball = __ballot_sync(0xffffffffu, hit0 || hit1);
+        int bk = kHistBins - 1;
+        if (ball) {
+            const int src = __ffs(ball) - 1;
+            bk = 2 * src + (__shfl_sync(0xffffffffu, hit0 ? 0 : 1, src));
+        }
+        if (lane == 0)
+            s_ts = bk >= kHistBins - 1 ? kNegInf
+                                       : M - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
+                                             (fabsf(M) * 0x1p-18f + 0x1p-20f);
+    }
+    __syncthreads();
+    // ---- pass 3: the candidate set S and the best value left out of it
+    const float t_s = s_ts;
+    float a_below = kNegInf;
+    for (int j = tid; j < v; j += kSelThreads) {
+        const float a = __ldcg(Lr + j);
+        if (a >= t_s) {
+            const int pos = atomicAdd(&s_nsel, 1);
+            if (pos < kCsMax) s_S[pos] = dev::value_key(a, j);
         } else {
-            const float e_ub = dev::expf_glibc(x_ub - mx, tab) * (1.0f + 0x1p-20f);
-            const float e_k = __uint_as_float(static_cast<uint32_t>(s_sorted[kk - 1] >> 32));
-            if (!(e_ub * (1.0f + 0x1p-21f) < e_k)) why |= FRS_FLAG_CERT_BOUND;
+            a_below = fmaxf(a_below, a);
         }
     }
-    if (why) {
-        if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
-        return;
+    a_below = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_below)));
+    if (lane == 0) s_abw[warp] = a_below;
+    __syncthreads();
+    const int nsel = s_nsel, ns = min(nsel, kCsMax);
+    if (tid < ns) {  // canonical (descending) order
+        const unsigned long long mine = s_S[tid];
+        int rank = 0;
+        for (int c = 0; c < ns; ++c) rank += s_S[c] > mine;
+        s_sel[rank] = mine;
     }
-    // tot = sum exp(x_j - M) over the approximate logits; rescale to the exact max
-    const double total = s_tot * static_cast<double>(exp2f((s_mmax - mx) * 1.4426950408889634f));
-    const float inv = __double2float_rn(1.0 / total);
-    if (lane < A.k) {
-        const size_t o = (size_t)i * A.k + lane;
-        if (lane < kk) {
-            const unsigned long long key = s_sorted[lane];
-            const int j = dev::key_index(key);
-            A.out_ridx[o] = j;
-            A.out_full[o] = A.ordered ? s_ord[s_spos[lane]] : j;
-            A.out_prob[o] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(key >> 32)), inv);
-        } else {
-            A.out_ridx[o] = -1;
-            A.out_full[o] = -1;
-            A.out_prob[o] = 0.0f;
-        }
-    }
-    if (A.k > 32) {  // k up to 64
-        const int r = lane + 32;
-        if (r < A.k) {
-            const size_t o = (size_t)i * A.k + r;
-            if (r < kk) {
-                const unsigned long long key = s_sorted[r];
-                const int j = dev::key_index(key);
-                A.out_ridx[o] = j;
-                A.out_full[o] = A.ordered ? s_ord[s_spos[lane]] : j;
-                A.out_prob[o] = __fmul_rn(__uint_as_float(static_cast<uint32_t>(key >> 32)), inv);
-            } else {
-                A.out_ridx[o] = -1;
-                A.out_full[o] = -1;
-                A.out_prob[o] = 0.0f;
+    __syncthreads();
+    if (tid < ns && A.ordered) s_ord[tid] = __ldg(A.ordered + dev::key_index(s_sel[tid]));
+    // ---- exact recompute of S, 8 candidates per round
+    for (int c0 = 0; c0 < ns; c0 += kCandPerFinCta) {
+        const int nc = min(kCandPerFinCta, ns - c0);
+        for (int e = tid; e < nc * T; e += kSelThreads) {
+            const int c = e / T, t = e - c * T;
+            const uint4 u = __ldg(reinterpret_cast<const uint4 *>(A.slab + (size_t)dev::key_index(s_sel[c0 + c]) * A.d) + t);
+            float *dst = wt + (size_t)c * 8 * TP + t;
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // bf16 -> fp32 is exact
+                dst[(2 * q) * TP] = __uint_as_float(w4[q] << 16);
+                dst[(2 * q + 1) * TP] = __uint_as_float(w4[q] & 0xffff0000u);
             }
         }
+        __syncthreads();
+        if (tid < ((nc * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
+            const int cl = (tid >> 3) < nc ? tid >> 3 : 0, l = tid & 7;
+            const float4 *hp = reinterpret_cast<const float4 *>(ht + l * TP);
+            const float4 *wp = reinterpret_cast<const float4 *>(wt + ((size_t)cl * 8 + l) * TP);
+            float s = 0.0f;
+            const int T8 = T / 8;
+            float4 w0 = wp[0], w1 = wp[1], h0 = hp[0], h1 = hp[1];
+            for (int t8 = 0; t8 < T8; ++t8) {
+                const int tn = t8 + 1 < T8 ? t8 + 1 : t8;
+                const float4 v0 = wp[2 * tn], v1 = wp[2 * tn + 1], g0 = hp[2 * tn], g1 = hp[2 * tn + 1];
+                const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s = __fadd_rn(s, __fmul_rn(hv[q], wv[q]));  // kernels.cpp:17-26
+                w0 = v0;
+                w1 = v1;
+                h0 = g0;
+                h1 = g1;
+            }
+            for (int t = T8 * 8; t < T; ++t) s = __fadd_rn(s, __fmul_rn(ht[l * TP + t], wt[((size_t)cl * 8 + l) * TP + t]));
+            s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));  // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7))
+            s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+            s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+            if (l == 0 && (tid >> 3) < nc) s_fin[c0 + cl] = s;
+        }
+        __syncthreads();
     }
-    if (lane == 0) {
-        if (A.out_rowmax) A.out_rowmax[i] = mx;
-        if (A.out_total) A.out_total[i] = total;
-        if (A.out_flags) A.out_flags[i] = 0u;
+    if (warp != 0) return;
+    float a_bound = kNegInf, mxx = kNegInf;
+    double total = 0.0;
+    int any_bad = 0;
+    for (int w = 0; w < NW; ++w) {
+        a_bound = fmaxf(a_bound, s_abw[w]);
+        total += s_redd[w];
+        any_bad |= s_badw[w];
     }
-    FRS_FTRACE(A, 7);
+    mxx = Mx;
+    select_certify(A, i, ns, nsel, kk, a_bound, eps, any_bad != 0, total, mxx, s_fin, s_sel, s_sorted, s_tab, s_spos,
+                   s_ord);
 }
 
 // Grid-wide exact fallback for the rows the finalize could not certify. Launched after every
@@ -1244,12 +1472,12 @@ int configure(K *kern, size_t smem) {
     return FRS_OK;
 }
 
-template <int NP, bool SOFTMAX>
+template <int NP, bool SOFTMAX, bool LOGITS = false>
 int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapW32, const CUtensorMap &mapH, int n,
                 int v_rows, int d,
                 float inv_t, const Partials &P, cudaStream_t s) {
     using C = MainCfg<NP, SOFTMAX>;
-    auto kern = k_fast_main<NP, SOFTMAX>;
+    auto kern = k_fast_main<NP, SOFTMAX, LOGITS>;
     if (int st = configure(kern, C::SMEM)) return st;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctx->sm_count);
@@ -1264,6 +1492,46 @@ int launch_main(frs_ctx *ctx, const CUtensorMap &mapW, const CUtensorMap &mapW32
     FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mapW, mapW32, mapH, n, v_rows, d, inv_t, P));
     ++ctx->launches;
     return FRS_OK;
+}
+
+// The grid-wide exact fallback: exits at once unless the finalize / select queued a row.
+int launch_fallback(frs_ctx *ctx, const FinArgs &A, cudaStream_t s) {
+    auto fb = k_fast_fallback;
+    const int fsmem = ((A.d + 7) & ~7) * 4;
+    if (int st = configure(fb, fsmem)) return st;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctx->sm_count);
+    cfg.blockDim = dim3(kFbThreads);
+    cfg.dynamicSmemBytes = fsmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, fb, A));
+    ++ctx->launches;
+    return FRS_OK;
+}
+
+int launch_select(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
+    auto kern = k_fast_select;
+    const int TP = fin_pitch(A.d / 8);
+    const size_t smem = (size_t)(8 + kCandPerFinCta * 8) * TP * 4;
+    if (int st = configure(kern, smem)) return st;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(rows);
+    cfg.blockDim = dim3(kSelThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
+    ++ctx->launches;
+    return launch_fallback(ctx, A, s);
 }
 
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
@@ -1288,17 +1556,7 @@ int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     cfg.numAttrs = 2;
     FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
     ++ctx->launches;
-    // the grid-wide exact fallback: exits at once unless the finalize queued a row
-    auto fb = k_fast_fallback;
-    const int fsmem = ((A.d + 7) & ~7) * 4;
-    if (int st = configure(fb, fsmem)) return st;
-    cfg.gridDim = dim3(ctx->sm_count);
-    cfg.blockDim = dim3(kFbThreads);
-    cfg.dynamicSmemBytes = fsmem;
-    cfg.numAttrs = 1;  // programmatic dependency only (no cluster)
-    FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, fb, A));
-    ++ctx->launches;
-    return FRS_OK;
+    return launch_fallback(ctx, A, s);
 }
 
 int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
@@ -1336,11 +1594,93 @@ void graph_insert(frs_ctx *ctx, const GraphKey &key) {
     ctx->graphs.push_back(e);
 }
 
+// Batched drafting chain (17..64 hidden rows): k_hsplit -> k_fast_main<NP,false,LOGITS> ->
+// k_fast_select -> k_fast_fallback. The approximate logits [n x V_sub] fp32 stay in L2.
+int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows,
+                    const int32_t *ordered_ids, int k, float temperature, int32_t *out_ridx, int32_t *out_full,
+                    float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
+    if (k > 64) return fail(FRS_ENOTSUP, "FAST draft head: k <= 64");
+    const int NP = 64;  // N = 128: the NP=32 variant measured slower (240 vs 133 us at C2)
+    const int G = ctx->sm_count;
+    FastWs w;
+    int st = fast_workspace(ctx, NP, d, n, v_rows, w);
+    if (st) return st;
+    const int ld = (v_rows + 3) & ~3;
+    if ((st = ctx->fast_logits.ensure((size_t)n * ld * sizeof(float)))) return st;
+    w.P.logits = static_cast<float *>(ctx->fast_logits.ptr);
+    w.P.ld_logits = ld;
+    CUtensorMap mapW, mapW32, mapH;
+    if ((st = make_map(&mapW, W, v_rows, d, BM)) || (st = make_map(&mapW32, W, v_rows, d, CH)) ||
+        (st = make_map(&mapH, w.hs, 2 * NP, d, 2 * NP)))
+        return st;
+    timing_begin(ctx, s);
+    struct EndTiming {
+        frs_ctx *c;
+        cudaStream_t s;
+        ~EndTiming() { timing_end(c, s); }
+    } end_timing{ctx, s};
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(std::min(G, (NP * d / 4 + 127) / 128));
+        cfg.blockDim = dim3(128);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if ((st = configure(k_hsplit, 0))) return st;
+        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, static_cast<unsigned long long *>(nullptr)));
+        ++ctx->launches;
+    }
+    const float inv_t = 1.0f / temperature;
+    st = launch_main<64, false, true>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s);
+    if (st) return st;
+    FinArgs A{};
+    A.h = h;
+    A.n = n;
+    A.d = d;
+    A.v_rows = v_rows;
+    A.k = k;
+    A.temperature = temperature;
+    A.slab = static_cast<const unsigned short *>(W);
+    A.ordered = ordered_ids;
+    A.P = w.P;
+    A.fin = w.fin;
+    A.row_ctr = static_cast<unsigned long long *>(ctx->fast_ctr.ptr);
+    A.fb_arrive = A.row_ctr + 64;
+    A.fb_count = reinterpret_cast<unsigned *>(A.row_ctr + 65);
+    A.fb_rows = reinterpret_cast<uint32_t *>(A.fb_count + 1);
+    A.scratch = w.scratch;
+    A.out_ridx = out_ridx;
+    A.out_full = out_full;
+    A.out_prob = out_prob;
+    A.out_rowmax = out_rowmax;
+    A.out_total = out_total;
+    A.out_flags = out_flags;
+    A.argmax = 0;
+    A.id_offset = 0;
+    return launch_select(ctx, A, n, s);
+}
+
 int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
                 int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx, int32_t *out_full,
                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
     if (d % 8 != 0) return fail(FRS_ENOTSUP, "FAST head: hidden_dim must be a multiple of 8 (TMA row pitch)");
-    if (n > 64) return fail(FRS_ENOTSUP, "FAST head: at most 64 hidden rows per call");
+    const int TPs = fin_pitch(d / 8);
+    const bool batched_ok = (size_t)(8 + kCandPerFinCta * 8) * TPs * 4 <= ctx->smem_optin;
+    if (!argmax && n > 16 && batched_ok) {  // batched drafting: up to 64 rows per slab pass
+        for (int r0 = 0; r0 < n; r0 += 64) {
+            const int nr = std::min(64, n - r0);
+            const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, v_rows, ordered_ids, k, temperature,
+                                           out_ridx + (size_t)r0 * k, out_full + (size_t)r0 * k,
+                                           out_prob + (size_t)r0 * k, out_rowmax ? out_rowmax + r0 : nullptr,
+                                           out_total ? out_total + r0 : nullptr, out_flags ? out_flags + r0 : nullptr, s);
+            if (st) return st;
+        }
+        return FRS_OK;
+    }
+    if (n > 64 && argmax) return fail(FRS_ENOTSUP, "FAST verify head: at most 64 hidden rows per call");
     if (!argmax && n > 16) {  // the fused softmax path takes 16 hidden rows per pass
         for (int r0 = 0; r0 < n; r0 += 16) {
             const int nr = std::min(16, n - r0);

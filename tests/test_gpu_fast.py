@@ -54,8 +54,11 @@ def check_fast(ctx, restatement, W, ids, h, k, temperature=1.0):
     (16, 256, 3000, 16),
     (7, 1024, 300, 10),       # V_sub smaller than one CTA wave
     (10, 2048, 20000, 32),    # k > 16: 64 recomputed candidates
-    (20, 512, 8192, 10),      # 17..32 rows
+    (20, 512, 8192, 10),      # 17..32 rows: batched path (NP=32)
     (3, 3584, 32768, 10),     # Qwen-2.5-7B hidden size
+    (64, 4096, 32768, 10),    # batched path, one full 64-row pass at the Llama shape
+    (100, 1024, 12000, 10),   # batched path, two passes (64 + 36)
+    (40, 2048, 5000, 40),     # batched path, k > 32
 ])
 def test_fast_draft_ids_exact(cuda_ctx, restatement, n, d, v_sub, k):
     W, ids, h = case(n * 7 + d + v_sub, n, d, v_sub)

@@ -77,6 +77,33 @@ def draft_sweep(ctx, dev, modes):
     del W
 
 
+def batched_draft(ctx, dev):
+    """C5-style batched drafting: many independent streams' beam rows in one call (one slab
+    pass per 64 rows); µs per call and aggregate rows/s at the Llama-3-8B shape."""
+    d, V, v_sub, k = 4096, 128256, 32768, 10
+    g = torch.Generator(device=dev).manual_seed(1234)
+    W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16).float()
+    ranked = np.random.default_rng(1234).permutation(V).astype(np.int32)
+    head = api.restrict_lm_head(ctx, W, api.subset_from_ranking(ranked, v_sub, V, forced=[0, 1]), dtype="bf16")
+    del W
+    for n in (10, 16, 32, 64, 128, 256, 640, 2560):
+        pool = [rms(torch.randn(n, d, generator=g, device=dev)) for _ in range(4)]
+        out = api.draft_head_topk(ctx, pool[0], head, k, mode="fast")
+
+        def step(i):
+            api.draft_head_topk(ctx, pool[i % 4], head, k, mode="fast", out=out)
+
+        iters = max(5, 2000 // n)
+        us = timed(step, iters)
+        f = out.flags.cpu().numpy()
+        print(json.dumps({"sweep": "batched_draft", "rows": n, "streams_x10": n / 10, "v_sub": v_sub, "d": d,
+                          "us_per_call": us, "rows_per_s": n / us * 1e6,
+                          "rows_recomputed_last_call": int(((f & 0x8) != 0).sum()),
+                          "reasons_last_call": [int(((f & b) != 0).sum()) for b in (0x10, 0x20, 0x40)],
+                          "slab_passes": -(-n // 64) if n > 16 else 1}), flush=True)
+    del head
+
+
 def verify_sweep(ctx, dev):
     for name, d, V, m in (("C2 Llama-3-8B", 4096, 128256, 61), ("C4 Qwen-2.5-7B", 3584, 152064, 61)):
         g = torch.Generator(device=dev).manual_seed(7)
@@ -137,7 +164,7 @@ def decode_loop(ctx, dev, iters):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="draft,verify,decode")
+    ap.add_argument("--what", default="draft,batched,verify,decode")
     ap.add_argument("--exact", action="store_true", help="also time the EXACT draft level")
     ap.add_argument("--decode-iters", type=int, default=100)
     a = ap.parse_args()
@@ -146,6 +173,8 @@ def main():
     what = a.what.split(",")
     if "draft" in what:
         draft_sweep(ctx, dev, ["fast", "exact"] if a.exact else ["fast"])
+    if "batched" in what:
+        batched_draft(ctx, dev)
     if "verify" in what:
         verify_sweep(ctx, dev)
     if "decode" in what:
