@@ -163,6 +163,8 @@ struct Partials {
     float *pth;                // [NP][L] bound: every list row not in pkey has approx logit <= pth
     unsigned long long *pkey;  // [NP][L][R] the list's best R (approx value, index) keys, descending
     float *pw2;                // [2G] max squared L2 norm of slab rows (per CTA and norm warp)
+    unsigned *rowmax_bits;     // [64] per hidden row: max approximate logit, order-preserving bits
+    unsigned *w2_bits;         // [1] max |W_j|^2 (float bits); both reset by k_hsplit, atomicMax here
     float *logits;             // LOGITS mode: approximate logits [n][ld_logits] (batched drafting)
     int ld_logits;
     int G;
@@ -183,11 +185,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // 128 threads, no shared memory: it co-resides with the main kernel's CTAs, which PDL lets
 // launch (and run their prologue and first slab loads) while this grid is still running.
 __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int n, int d, int NP,
-                                                __nv_bfloat16 *__restrict__ hs, unsigned long long *xtrace) {
+                                                __nv_bfloat16 *__restrict__ hs, unsigned *__restrict__ rowmax_bits,
+                                                unsigned *__restrict__ w2_bits, unsigned long long *xtrace) {
     // launched programmatically after whatever precedes it on the stream: wait for it (h is
     // final, the previous call's fallback queue is drained), then let the main kernel launch
     griddep_wait();
     griddep_launch();
+    if (blockIdx.x == 0) {  // this call's atomicMax targets (the previous call is complete)
+        if (threadIdx.x < 64) rowmax_bits[threadIdx.x] = 0u;  // below every ordered value
+        if (threadIdx.x == 0) *w2_bits = 0u;
+    }
     if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[0] = gtimer();
     const int total4 = NP * d / 4;  // d % 8 == 0 on the FAST path
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total4; idx += gridDim.x * blockDim.x) {
@@ -408,7 +415,10 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-        if (lane == 0) P.pw2[cta * 2 + (warp - 2)] = wmax;
+        if (lane == 0) {
+            P.pw2[cta * 2 + (warp - 2)] = wmax;
+            atomicMax(P.w2_bits, __float_as_uint(wmax));  // non-negative: raw bits order
+        }
         if (threadIdx.x == 64) FRS_TRACE(P, 8);
     } else {  // ---------------- epilogue warps: TMEM -> (softmax stats, per-thread candidates)
         const int we = warp - 4;         // 0 .. EPI-1
@@ -562,6 +572,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             const int i = cbase + r;
             if (i >= n) continue;
             if (lane < R) P.pkey[((size_t)i * L + list) * R + lane] = out[r];
+            if (lane == 0 && out[r]) atomicMax(P.rowmax_bits + i, static_cast<unsigned>(out[r] >> 32));
             if (lane == R) P.pth[(size_t)i * L + list] = fmaxf(out[r] ? dev::key_value(out[r]) : kNegInf, bmax[r]);
         }
         }  // !LOGITS
@@ -615,20 +626,6 @@ struct FinArgs {
             (A).P.trace[(size_t)(A).P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + (slot)] = gtimer(); \
     } while (0)
 
-// Finalize: grid (n, kFinCtas). The work per row is tiny, so the kernel is written for
-// latency: every step is spread over the whole CTA (a single warp running serial code sits at
-// CPI ~4 and was the bottleneck). Every CTA of row i rebuilds the same candidate set S:
-//   1. stage the row's union of per-CTA top-R keys (G lists, each sorted descending) and the
-//      hidden row (transposed per dot_f32 lane chain) in shared memory; warp 0 merges the
-//      softmax partials, warp 1 the bounds.
-//   2. v' = the kk-th largest key among the top-2 of every list (a lower bound of the kk-th
-//      largest union key), by parallel rank counting; S = {union keys >= v' - 2 eps - margin}
-//      (a superset of every row that can reach the top-k), in canonical descending order.
-//   3. the CTA recomputes its slice S[8b, 8b + 8) EXACTLY (dot_f32 order) into A.fin, each
-//      8-lane group reading its chain's operands as 16-byte vectors from transposed tiles.
-//   4. the last CTA of the row to arrive selects the top-k by (prob desc, index asc) and
-//      certifies it (see the file comment); rows that cannot be certified are queued for the
-//      grid-wide exact fallback (k_fast_fallback).
 // Row pitch (floats) of the transposed per-lane-chain operand tiles of the exact recompute: a
 // multiple of 4 (16-byte vector loads) with pitch % 8 == 4, so the 8 lanes of a quarter-warp
 // hit 8 distinct 4-bank groups (a 2-way conflict at pitch % 8 == 0 doubled the loop time).
@@ -785,29 +782,43 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
     FRS_FTRACE(A, 7);
 }
 
+// Finalize: grid (n, kFinCtas) in clusters of kFinCtas (one cluster per hidden row). The work
+// per row is tiny, so every step is spread over the CTA and the number of barrier-separated
+// phases is kept minimal:
+//   0. (before griddepcontrol.wait, overlapping the main kernel's tail) the hidden row,
+//      transposed per dot_f32 lane chain, and |h|^2; a cluster barrier orders the DSMEM
+//      counters' initialisation before any remote atomic.
+//   1. the row max M and max |W_j|^2 arrive as single words (atomics of the main kernel), so
+//      eps and the bin width are known at once: every thread bins its union keys (4G lists x
+//      R) into a histogram of (M - v) / bw; warps 0-3 merge the softmax partials, 4-5 the bounds.
+//   2. every warp scans the histogram (the kk-th key's bin gives t_s = bin edge - 2 eps -
+//      margin, so S = {keys >= t_s} holds every row that can reach the top-k); each CTA takes
+//      the keys of S with key_index % kFinCtas == its rank (no canonical order needed).
+//   3. the CTA recomputes its keys EXACTLY (dot_f32 order) and appends (key, exact logit,
+//      full id) to the cluster leader's arrays through DSMEM (remote atomic slot + stores).
+//   4. the leader, warp 0: selection + certification (select_certify).
 __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     extern __shared__ __align__(16) uint8_t fsm_raw[];
     const int T = A.d >> 3;           // dot_f32 steps per lane chain (d % 8 == 0 on FAST)
     const int TP = fin_pitch(T);      // padded chain pitch (elements): 16-byte aligned rows
-    float *ht = reinterpret_cast<float *>(fsm_raw);                                   // [8][TP]
-    float *wt = ht + 8 * TP;                        // [8 cand][8][TP] fp32 (bf16 widened, exact)
-    __shared__ unsigned long long s_S[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
-    __shared__ double s_hn2[kFinThreads / 32], s_tot;
-    __shared__ float s_mmax, s_th, s_abw[kFinThreads / 32], s_pmw[4], s_thw[2], s_w2w[2];
+    float *ht = reinterpret_cast<float *>(fsm_raw);  // [8][TP]
+    float *wt = ht + 8 * TP;                          // [8 cand][8][TP] fp32 (bf16 widened, exact)
+    __shared__ unsigned long long s_mine[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
+    __shared__ double s_hn2[kFinThreads / 32];
+    __shared__ float s_abw[kFinThreads / 32], s_pmw[4], s_thw[2];
     __shared__ float s_psw[4];
     __shared__ unsigned s_hist[kHistBins];
-    __shared__ uint32_t s_kmax[kFinThreads / 32];
-    __shared__ float s_fin[kCsMax];             // exact logits of S (cluster leader; DSMEM-written)
+    __shared__ float s_fin[kCsMax];      // leader: exact logits of S, in arrival (slot) order
     __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
-    __shared__ int s_nsel, s_badw[kFinThreads / 32];
+    __shared__ int s_nsel, s_nmine, s_cnt, s_badw[kFinThreads / 32];
     FRS_FTRACE(A, 0);
     griddep_launch();  // the fallback grid may become resident now; it waits for this grid
 
-    const int i = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+    const int i = blockIdx.x, b = static_cast<int>(cluster_rank()), tid = threadIdx.x;
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = tid & 31;
     const int G = A.P.G, L = G * kListsPerCta, E = L * R;
     const float kNegInf = -__int_as_float(0x7f800000);
-    // ---- 1a. the hidden row (independent of the main kernel): transposed ht[l][t] = h[8t + l]
+    // ---- 0. the hidden row (independent of the main kernel): transposed ht[l][t] = h[8t + l]
     {
         const float4 *hv = reinterpret_cast<const float4 *>(A.h + (size_t)i * A.d);
         double hn2 = 0.0;
@@ -840,32 +851,44 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             s_hn2[warp] = hn2;
             s_badw[warp] = bad;
         }
-        if (tid == 0) s_nsel = 0;
+        if (tid == 0) {
+            s_nsel = 0;
+            s_nmine = 0;
+            s_cnt = 0;
+        }
         if (tid < kHistBins) s_hist[tid] = 0u;
     }
-    __syncthreads();  // s_hn2 / s_badw complete (read by warp 1 below)
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     FRS_FTRACE(A, 1);
     griddep_wait();
     FRS_FTRACE(A, 2);
-    // ---- 1b. partials of the main kernel: every load of a thread issued before any use
+    // ---- 1. keys in registers, eps, histogram; softmax / bound partials
+    const int kk = min(A.k, A.v_rows);
     constexpr int KPT = kMaxLists * R / kFinThreads;  // union keys per thread
     unsigned long long kr[KPT];
-    {
-        const unsigned long long *src = A.P.pkey + (size_t)i * E;
+    const unsigned long long *src = A.P.pkey + (size_t)i * E;
 #pragma unroll
-        for (int u = 0; u < KPT; ++u) {
-            const int e = tid + u * kFinThreads;
-            kr[u] = e < E ? __ldcg(src + e) : 0ull;
-        }
-        unsigned long long km = 0ull;
+    for (int u = 0; u < KPT; ++u) {
+        const int e = tid + u * kFinThreads;
+        kr[u] = e < E ? __ldcg(src + e) : 0ull;
+    }
+    const float M = dev::from_ordered(__ldcg(A.P.rowmax_bits + i));
+    const float W2 = __uint_as_float(__ldcg(A.P.w2_bits));
+    double h2 = 0.0;
 #pragma unroll
-        for (int u = 0; u < KPT; ++u) km = kr[u] > km ? kr[u] : km;
-        const uint32_t kv = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(km >> 32));  // value bits
-        if (lane == 0) s_kmax[warp] = kv;
+    for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
+    const float eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(W2) * 1.001)) * fast_gamma(A.d) * 1.01f;
+    const float bw = fmaxf(0.5f * eps, fabsf(M) * 0x1p-20f + 0x1p-30f), rbw = 1.0f / bw;
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {  // warp-aggregated: one shared atomic per distinct bin
+        const int bin = kr[u] != 0ull ? hist_bin((M - dev::key_value(kr[u])) * rbw) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
     }
     constexpr int SW = 4;                        // warps merging the softmax partials
     constexpr int PPL = kMaxLists / (32 * SW);   // partials per lane
-    if (warp < SW && !A.argmax) {  // softmax partials: M = max m_c, T = sum s_c exp(m_c - M)
+    if (warp < SW && !A.argmax) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
         float pm[PPL], ps[PPL];
 #pragma unroll
         for (int u = 0; u < PPL; ++u) {
@@ -887,55 +910,23 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             s_pmw[warp] = mm;
             s_psw[warp] = t;
         }
-    } else if (warp >= SW && warp < SW + 2) {  // bounds: th over the lists, w2 over the norm warps
+    } else if (warp >= SW && warp < SW + 2) {  // th = max list bound
         const int wb = warp - SW;
-        float th = kNegInf, w2 = 0.0f;
         constexpr int TPL = kMaxLists / 64;
-        float a[TPL], w[TPL];
+        float a[TPL], th = kNegInf;
 #pragma unroll
         for (int u = 0; u < TPL; ++u) {
             const int c = wb * 32 + lane + 64 * u;
             a[u] = c < L ? __ldcg(A.P.pth + (size_t)i * L + c) : kNegInf;
-            w[u] = c < 2 * G ? __ldcg(A.P.pw2 + c) : 0.0f;
         }
 #pragma unroll
-        for (int u = 0; u < TPL; ++u) {
-            th = fmaxf(th, a[u]);
-            w2 = fmaxf(w2, w[u]);
-        }
+        for (int u = 0; u < TPL; ++u) th = fmaxf(th, a[u]);
         th = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(th)));
-        w2 = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(w2)));
-        if (lane == 0) {
-            s_thw[wb] = th;
-            s_w2w[wb] = w2;
-        }
+        if (lane == 0) s_thw[wb] = th;
     }
     __syncthreads();
     FRS_FTRACE(A, 3);
-    // every thread: eps, the largest key value M, the histogram of (M - v) in half-eps bins
-    const int kk = min(A.k, A.v_rows);
-    float eps, Mv, bw;
-    {
-        double h2 = 0.0;
-#pragma unroll
-        for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
-        eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(fmaxf(s_w2w[0], s_w2w[1])) * 1.001)) *
-              fast_gamma(A.d) * 1.01f;
-        uint32_t kv = 0u;
-#pragma unroll
-        for (int q = 0; q < kFinThreads / 32; ++q) kv = max(kv, s_kmax[q]);
-        Mv = dev::from_ordered(kv);
-        bw = fmaxf(0.5f * eps, fabsf(Mv) * 0x1p-20f + 0x1p-30f);
-#pragma unroll
-        for (int u = 0; u < KPT; ++u)
-            if (kr[u] != 0ull) atomicAdd(&s_hist[hist_bin((Mv - dev::key_value(kr[u])) / bw)], 1u);
-    }
-    __syncthreads();
-    FRS_FTRACE(A, 8);
-    // ---- 2. S = union keys >= t_s: the kk-th key lies in the first bin whose cumulative count
-    //         reaches kk (every warp scans the 64 bins redundantly: no extra barrier), so
-    //         v_kk > M - bw g(bin + 1) and t_s = that edge - 2 eps - margin keeps every row that
-    //         can reach the top-k (the catch-all last bin: t_s = -inf).
+    // ---- 2. threshold (every warp redundantly), S, my share of S, a_below
     {
         const unsigned c0 = s_hist[2 * lane], c1 = s_hist[2 * lane + 1];
         unsigned incl = c0 + c1;
@@ -950,69 +941,52 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         const unsigned ball = __ballot_sync(0xffffffffu, hit0 || hit1);
         int bk = kHistBins - 1;
         if (ball) {
-            const int src = __ffs(ball) - 1;
-            bk = 2 * src + (__shfl_sync(0xffffffffu, hit0 ? 0 : 1, src));
+            const int srcl = __ffs(ball) - 1;
+            bk = 2 * srcl + (__shfl_sync(0xffffffffu, hit0 ? 0 : 1, srcl));
         }
         const float t_s = bk >= kHistBins - 1
                               ? kNegInf
-                              : Mv - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
-                                    (fabsf(Mv) * 0x1p-18f + 0x1p-20f);
+                              : M - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
+                                    (fabsf(M) * 0x1p-18f + 0x1p-20f);
         float a_below = kNegInf;
+        int in_s = 0;
 #pragma unroll
         for (int u = 0; u < KPT; ++u) {
             if (kr[u] == 0ull) continue;
             const float v = dev::key_value(kr[u]);
             if (v >= t_s) {
-                const int pos = atomicAdd(&s_nsel, 1);
-                if (pos < kCsMax) s_S[pos] = kr[u];
+                ++in_s;
+                if ((dev::key_index(kr[u]) & (kFinCtas - 1)) == b) {
+                    const int pos = atomicAdd(&s_nmine, 1);
+                    if (pos < kCsMax) s_mine[pos] = kr[u];
+                }
             } else {
                 a_below = fmaxf(a_below, v);
             }
         }
+        in_s = __reduce_add_sync(0xffffffffu, in_s);
+        if (lane == 0 && in_s) atomicAdd(&s_nsel, in_s);
         a_below = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_below)));
         if (lane == 0) s_abw[warp] = a_below;
-        if (tid == 0) {
-            s_th = fmaxf(s_thw[0], s_thw[1]);
-            if (!A.argmax) {
-                float mm = kNegInf;
-                for (int w = 0; w < SW; ++w) mm = fmaxf(mm, s_pmw[w]);
-                double t = 0.0;
-                for (int w = 0; w < SW; ++w)
-                    if (s_pmw[w] != kNegInf) t += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
-                s_mmax = mm;
-                s_tot = t;
-            }
-        }
-    }
-    __syncthreads();
-    FRS_FTRACE(A, 9);
-    const int nsel = s_nsel, ns = min(nsel, kCsMax);
-    if (tid < ns) {  // canonical (descending) order, so every CTA of the row indexes S identically
-        const unsigned long long mine = s_S[tid];
-        int rank = 0;
-#pragma unroll 16
-        for (int c = 0; c < kCsMax; ++c) rank += (c < ns) & (s_S[c] > mine);
-        s_sel[rank] = mine;
     }
     __syncthreads();
     FRS_FTRACE(A, 4);
-
-    // ---- 3. exact recompute of my candidates c = b, b + 8, ... (round-robin over the row's
-    //         CTAs): stage the rows transposed per lane chain (wt[c][l][t] = W_c[8t + l]),
-    //         then one 8-lane group per candidate
-    const int nmine = ns > b ? (ns - b + kFinCtas - 1) / kFinCtas : 0;
-    if (nmine > 0) {
+    const int nsel = s_nsel;
+    // ---- 3. exact recompute of my share (none if S overflowed: the leader falls back)
+    const int nmine = nsel <= kCsMax ? min(s_nmine, kCsMax) : 0;
+    for (int r0 = 0; r0 < nmine; r0 += kCandPerFinCta) {
+        const int nc = min(kCandPerFinCta, nmine - r0);
         constexpr int TPT = 2;  // uint4 per thread per row and batch: T <= 512 in one batch
         for (int t0 = 0; t0 < T; t0 += TPT * kFinThreads) {
             uint4 v[kCandPerFinCta][TPT];
 #pragma unroll
             for (int c = 0; c < kCandPerFinCta; ++c) {
                 const uint4 *row = reinterpret_cast<const uint4 *>(
-                    A.slab + (size_t)dev::key_index(s_sel[c < nmine ? b + c * kFinCtas : 0]) * A.d);
+                    A.slab + (size_t)dev::key_index(s_mine[r0 + (c < nc ? c : 0)]) * A.d);
 #pragma unroll
                 for (int u = 0; u < TPT; ++u) {
                     const int t = t0 + tid + u * kFinThreads;
-                    if (c < nmine && t < T) v[c][u] = __ldg(row + t);
+                    if (c < nc && t < T) v[c][u] = __ldg(row + t);
                 }
             }
 #pragma unroll
@@ -1020,7 +994,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
 #pragma unroll
                 for (int u = 0; u < TPT; ++u) {
                     const int t = t0 + tid + u * kFinThreads;
-                    if (!(c < nmine && t < T)) continue;
+                    if (!(c < nc && t < T)) continue;
                     float *dst = wt + (size_t)c * 8 * TP + t;
                     const uint32_t w4[4] = {v[c][u].x, v[c][u].y, v[c][u].z, v[c][u].w};
 #pragma unroll
@@ -1032,11 +1006,9 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             }
         }
         FRS_FTRACE(A, 12);
-        if (A.P.trace && threadIdx.x == 0)
-            A.P.trace[(size_t)A.P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + 13] = clock64();
         __syncthreads();
-        if (tid < ((nmine * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
-            const int cl = (tid >> 3) < nmine ? tid >> 3 : 0, l = tid & 7;
+        if (tid < ((nc * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
+            const int cl = (tid >> 3) < nc ? tid >> 3 : 0, l = tid & 7;
             const float4 *hp = reinterpret_cast<const float4 *>(ht + l * TP);
             const float4 *wp = reinterpret_cast<const float4 *>(wt + ((size_t)cl * 8 + l) * TP);
             float s = 0.0f;
@@ -1059,34 +1031,49 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));  // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7))
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
-            if (l == 0 && (tid >> 3) < nmine) {  // into the cluster leader's s_fin (DSMEM)
-                const uint32_t local = smem_u32(&s_fin[b + cl * kFinCtas]);
-                uint32_t remote;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(local));
-                asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(s) : "memory");
+            if (l == 0 && (tid >> 3) < nc) {  // append to the cluster leader's arrays (DSMEM)
+                const unsigned long long key = s_mine[r0 + cl];
+                const int j = dev::key_index(key);
+                const int32_t full = A.ordered ? __ldg(A.ordered + j) : j;
+                uint32_t rc, slot;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rc) : "r"(smem_u32(&s_cnt)));
+                asm volatile("atom.shared::cluster.add.u32 %0, [%1], 1;" : "=r"(slot) : "r"(rc) : "memory");
+                uint32_t rf, rk, ro;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rf) : "r"(smem_u32(&s_fin[slot])));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rk) : "r"(smem_u32(&s_sel[slot])));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ro) : "r"(smem_u32(&s_ord[slot])));
+                asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(rf), "f"(s) : "memory");
+                asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(rk), "l"(key) : "memory");
+                asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ro), "r"(full) : "memory");
             }
         }
+        __syncthreads();
     }
-    // the leader prefetches the remap of S while the exact dots run
-    if (cluster_rank() == 0 && tid < ns && A.ordered) s_ord[tid] = __ldg(A.ordered + dev::key_index(s_sel[tid]));
     FRS_FTRACE(A, 5);
-    if (A.P.trace && threadIdx.x == 0)
-        A.P.trace[(size_t)A.P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + 14] = clock64();
     // cluster barrier: release our DSMEM stores, acquire everyone's in the leader
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    if (cluster_rank() != 0) return;
+    if (b != 0) return;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (warp != 0) return;
+    FRS_FTRACE(A, 10);
 
     // ---- 4. the cluster leader, warp 0: selection + certification
-    float a_bound = s_th;  // every row not recomputed has approx <= a_bound
+    float a_bound = fmaxf(s_thw[0], s_thw[1]);  // every row not recomputed has approx <= a_bound
     int any_bad = 0;
     for (int w = 0; w < kFinThreads / 32; ++w) {
         a_bound = fmaxf(a_bound, s_abw[w]);
         any_bad |= s_badw[w];
     }
-    select_certify(A, i, ns, nsel, kk, a_bound, eps, any_bad != 0, s_tot, s_mmax, s_fin, s_sel, s_sorted, s_tab,
-                   s_spos, s_ord);
+    float mm = kNegInf;
+    double tot = 0.0;
+    if (!A.argmax) {
+        for (int w = 0; w < SW; ++w) mm = fmaxf(mm, s_pmw[w]);
+        for (int w = 0; w < SW; ++w)
+            if (s_pmw[w] != kNegInf) tot += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
+    }
+    const int ns = nsel <= kCsMax ? s_cnt : 0;  // == nsel when nothing overflowed
+    select_certify(A, i, ns, nsel, kk, a_bound, eps, any_bad != 0, tot, mm, s_fin, s_sel, s_sorted, s_tab, s_spos,
+                   s_ord);
 }
 
 // Batched drafting (n > 16 hidden rows): per hidden row one CTA over the approximate logits
@@ -1402,7 +1389,9 @@ int make_map(CUtensorMap *map, const void *base, int rows, int cols, int box_row
     return FRS_OK;
 }
 
-constexpr size_t kCtrBytes = 64 * 8 + 8 + 4 + 64 * 4;  // row_ctr | fb_arrive | fb_count | fb_rows
+// row_ctr[64] u64 | fb_arrive u64 | fb_count u32 | fb_rows[64] u32 | rowmax_bits[64] u32 | w2_bits u32
+constexpr size_t kCtrRowmax = 64 * 8 + 8 + 4 + 64 * 4;
+constexpr size_t kCtrBytes = kCtrRowmax + 64 * 4 + 4;
 
 struct FastWs {
     __nv_bfloat16 *hs;
@@ -1439,15 +1428,19 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.fin = reinterpret_cast<float *>(base + o_fin);
     w.scratch = reinterpret_cast<float *>(base + o_scr);
     w.P.trace = nullptr;
+    w.P.rowmax_bits = nullptr;
+    w.P.w2_bits = nullptr;
     static const bool tracing = std::getenv("FRS_TRACE") != nullptr;
     if (tracing) {
         if ((st = ctx->trace.ensure((size_t)(G * kTrMain + 64 * kFinCtas * 16 + 8) * 8))) return st;
         w.P.trace = static_cast<unsigned long long *>(ctx->trace.ptr);
     }
-    if (!ctx->fast_ctr.ptr) {  // row_ctr[64] u64 | fb_arrive u64 | fb_count u32 | fb_rows[64] u32
+    if (!ctx->fast_ctr.ptr) {  // zeroed once: counters are monotonic or reset in-stream
         if ((st = ctx->fast_ctr.ensure(kCtrBytes))) return st;
         FRS_CUDA_TRY(cudaMemset(ctx->fast_ctr.ptr, 0, kCtrBytes));
     }
+    w.P.rowmax_bits = reinterpret_cast<unsigned *>(static_cast<uint8_t *>(ctx->fast_ctr.ptr) + kCtrRowmax);
+    w.P.w2_bits = w.P.rowmax_bits + 64;
     return FRS_OK;
 }
 
@@ -1630,7 +1623,8 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
         cfg.attrs = at;
         cfg.numAttrs = 1;
         if ((st = configure(k_hsplit, 0))) return st;
-        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, static_cast<unsigned long long *>(nullptr)));
+        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, w.P.rowmax_bits, w.P.w2_bits,
+                                        static_cast<unsigned long long *>(nullptr)));
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;
@@ -1791,7 +1785,7 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
         cfg.numAttrs = 1;
         unsigned long long *xtrace = w.P.trace ? w.P.trace + (size_t)G * kTrMain + 64 * kFinCtas * 16 : nullptr;
         if ((st = configure(k_hsplit, 0))) return st;
-        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, xtrace));
+        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, w.P.rowmax_bits, w.P.w2_bits, xtrace));
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;
