@@ -1157,7 +1157,7 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
     for (int j0 = 0; j0 < v; j0 += kSelThreads) {
         const int j = j0 + tid;
         const float a = j < v ? __ldcg(Lr + j) : kNegInf;
-        if (j < v) tot += static_cast<double>(exp2f((a * inv_t - Mx) * 1.4426950408889634f));
+        if (j < v && !A.argmax) tot += static_cast<double>(exp2f((a * inv_t - Mx) * 1.4426950408889634f));
         const int bin = j < v ? hist_bin((M - a) * rbw) : -1;
         const unsigned peers = __match_any_sync(0xffffffffu, bin);
         if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
@@ -1591,7 +1591,8 @@ void graph_insert(frs_ctx *ctx, const GraphKey &key) {
 // k_fast_select -> k_fast_fallback. The approximate logits [n x V_sub] fp32 stay in L2.
 int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows,
                     const int32_t *ordered_ids, int k, float temperature, int32_t *out_ridx, int32_t *out_full,
-                    float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
+                    float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s,
+                    bool argmax = false, int32_t id_offset = 0) {
     if (k > 64) return fail(FRS_ENOTSUP, "FAST draft head: k <= 64");
     const int NP = 64;  // N = 128: the NP=32 variant measured slower (240 vs 133 us at C2)
     const int G = ctx->sm_count;
@@ -1652,8 +1653,9 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
     A.out_rowmax = out_rowmax;
     A.out_total = out_total;
     A.out_flags = out_flags;
-    A.argmax = 0;
-    A.id_offset = 0;
+    A.argmax = argmax ? 1 : 0;
+    A.id_offset = id_offset;
+    if (argmax) A.k = 1;
     return launch_select(ctx, A, n, s);
 }
 
@@ -1670,6 +1672,17 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
                                            out_ridx + (size_t)r0 * k, out_full + (size_t)r0 * k,
                                            out_prob + (size_t)r0 * k, out_rowmax ? out_rowmax + r0 : nullptr,
                                            out_total ? out_total + r0 : nullptr, out_flags ? out_flags + r0 : nullptr, s);
+            if (st) return st;
+        }
+        return FRS_OK;
+    }
+    if (argmax && n > 64 && batched_ok) {  // verify of many rows: approximate logits + per-row argmax
+        // (the list path is faster up to 64 rows: 238 vs 354 us at C2's 61 rows)
+        for (int r0 = 0; r0 < n; r0 += 64) {
+            const int nr = std::min(64, n - r0);
+            const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, v_rows, nullptr, 1, 1.0f, nullptr,
+                                           out_full + r0, out_prob ? out_prob + r0 : nullptr, nullptr, nullptr,
+                                           out_flags ? out_flags + r0 : nullptr, s, true, id_offset);
             if (st) return st;
         }
         return FRS_OK;

@@ -230,3 +230,16 @@ def test_vocab_parallel_nccl_world1(cuda_ctx, restatement):
         assert np.array_equal(vals.cpu().numpy(), rval)
     finally:
         dist.destroy_process_group()
+
+
+def test_fast_verify_many_rows_batched(cuda_ctx, restatement):
+    """More than 64 verify rows (batched streams) go through the approximate-logits path."""
+    rng = np.random.default_rng(91)
+    V, d, m = 6000, 512, 150
+    W = torch.from_numpy((rng.standard_normal((V, d)) * 0.02).astype(np.float32)).to(torch.bfloat16)
+    h = rmsnorm(rng.standard_normal((m, d)))
+    h[7] = 0.0  # flat row: lowest id through the exact fallback
+    ids, vals, flags = api.verify_head_argmax(cuda_ctx, torch.from_numpy(h).cuda(), W.cuda(), id_offset=11, mode="fast")
+    rid, rval = restatement.verify_argmax(h, W.float().numpy())
+    assert np.array_equal(ids.cpu().numpy(), rid + 11)
+    assert np.array_equal(vals.cpu().numpy(), rval)
