@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     auto tile_rows = [&](int t) { return min(v_rows - tile_row0(t), tile_chunks(t) * CH); };
 
     if (threadIdx.x == 0) {
+        FRS_TRACE(P, 28);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1 + 2);  // MMA commit + the two norm warps
@@ -691,13 +692,10 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
         FRS_FTRACE(A, 7);
         return;
     }
-    s_tab[lane] = dev::kExp2fTable[lane];
-    __syncwarp();
-    const unsigned long long *tab = s_tab;
-    const float x0 = __fdiv_rn(l0, A.temperature), x1 = __fdiv_rn(l1, A.temperature);
-    float mx = fmaxf(x0, x1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const unsigned long long *tab = s_tab;  // glibc exp table, staged by the caller's prologue
+    const bool unit_t = A.temperature == 1.0f;  // x = l / 1 is exact: skip the IEEE divisions
+    const float x0 = unit_t ? l0 : __fdiv_rn(l0, A.temperature), x1 = unit_t ? l1 : __fdiv_rn(l1, A.temperature);
+    const float mx = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(fmaxf(x0, x1))));
     const unsigned long long e0 = have0 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x0, mx), tab), j0) : 0ull;
     const unsigned long long e1 = have1 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x1, mx), tab), j1) : 0ull;
     // rank of each e-key among the ns (distinct: the index is part of the key)
@@ -857,6 +855,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             s_cnt = 0;
         }
         if (tid < kHistBins) s_hist[tid] = 0u;
+        if (tid < 32) s_tab[tid] = dev::kExp2fTable[tid];
     }
     __syncthreads();
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1125,6 +1124,7 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
         }
         if (tid == 0) s_nsel = 0;
         if (tid < kHistBins) s_hist[tid] = 0u;
+        if (tid < 32) s_tab[tid] = dev::kExp2fTable[tid];
     }
     griddep_wait();
     const float *Lr = A.P.logits + (size_t)i * A.P.ld_logits;

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 
 from paper_2502_14856_b200 import api, _lib  # noqa: E402
 
-SLOTS = {0: "setup done", 1: "producer: before griddep_wait", 9: "producer: after griddep_wait",
+SLOTS = {28: "main entry", 0: "setup done", 1: "producer: before griddep_wait", 9: "producer: after griddep_wait",
          3: "mma: first stage full", 2: "producer: all TMA issued", 4: "mma: all issued", 8: "norm warps done",
          10: "epi: first tfull wait", 11: "epi: first tile ready", 14: "epi w4: last tile ready",
          13: "epi: loop done", 15: "epi w4: softmax merged", 16: "epi w4: after bar2", 5: "cand published",
@@ -61,7 +61,7 @@ def main():
         st = pkey[n * L * 3:n * L * 3 + G * 32].reshape(G, 32).astype(np.int64)
         ft = pkey[n * L * 3 + G * 32:n * L * 3 + G * 32 + 64 * 8 * 16].reshape(64 * 8, 16).astype(np.int64)[: n * 8]
         xt = pkey[n * L * 3 + G * 32 + 64 * 8 * 16:].astype(np.int64)
-        t0 = st[:, 0][st[:, 0] > 0].min()
+        t0 = st[:, 0][st[:, 0] > 0].min()  # earliest "setup done" of the main kernel
         row = {}
         for s, name in SLOTS.items():
             v = st[:, s]
