@@ -166,6 +166,7 @@ struct Partials {
     unsigned *rowmax_bits;     // [64] per hidden row: max approximate logit, order-preserving bits
     unsigned *w2_bits;         // [1] max |W_j|^2 (float bits); both reset by k_hsplit, atomicMax here
     float *logits;             // LOGITS mode: approximate logits [n][ld_logits] (batched drafting)
+    int late_trigger;          // DIAGNOSTIC (FRS_ABLATE=8): launch_dependents at the end, not the start
     int ld_logits;
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     if (threadIdx.x == 0) FRS_TRACE(P, 0);
     // let the finalize grid launch now: its CTAs take SMs as ours retire and run their
     // prologue; griddepcontrol.wait there still waits for this whole grid (and its writes)
-    griddep_launch();
+    if (!P.late_trigger) griddep_launch();
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -580,6 +581,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         if (threadIdx.x == 128) FRS_TRACE(P, 18);
     }
     __syncthreads();  // every TMEM read is done
+    if (P.late_trigger) griddep_launch();
     if (threadIdx.x == 0) FRS_TRACE(P, 7);
     if (warp == 1) {
         tc_fence_after();
@@ -618,6 +620,7 @@ struct FinArgs {
     int32_t id_offset;
     unsigned *fb_count;              // fallback queue: count, entries row | reasons << 16
     uint32_t *fb_rows;               // [64]
+    int ablate;                      // DIAGNOSTIC ONLY (FRS_ABLATE): skip finalize phases for timing
     unsigned long long *fb_arrive;   // monotonic CTA arrival counter of k_fast_fallback
 };
 
@@ -810,7 +813,8 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
     __shared__ int s_nsel, s_nmine, s_cnt, s_badw[kFinThreads / 32];
     FRS_FTRACE(A, 0);
-    griddep_launch();  // the fallback grid may become resident now; it waits for this grid
+    // no early griddepcontrol.launch_dependents here: 148 fallback CTAs parked in
+    // griddepcontrol.wait next to this grid slowed it by ~2.7 us per call (measured)
 
     const int i = blockIdx.x, b = static_cast<int>(cluster_rank()), tid = threadIdx.x;
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = tid & 31;
@@ -862,6 +866,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     FRS_FTRACE(A, 1);
     griddep_wait();
     FRS_FTRACE(A, 2);
+    if (A.ablate == 1) return;
     // ---- 1. keys in registers, eps, histogram; softmax / bound partials
     const int kk = min(A.k, A.v_rows);
     constexpr int KPT = kMaxLists * R / kFinThreads;  // union keys per thread
@@ -881,13 +886,14 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     const float bw = fmaxf(0.5f * eps, fabsf(M) * 0x1p-20f + 0x1p-30f), rbw = 1.0f / bw;
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {  // warp-aggregated: one shared atomic per distinct bin
+        if (A.ablate == 4) break;
         const int bin = kr[u] != 0ull ? hist_bin((M - dev::key_value(kr[u])) * rbw) : -1;
         const unsigned peers = __match_any_sync(0xffffffffu, bin);
         if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
     }
     constexpr int SW = 4;                        // warps merging the softmax partials
     constexpr int PPL = kMaxLists / (32 * SW);   // partials per lane
-    if (warp < SW && !A.argmax) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
+    if (warp < SW && !A.argmax && A.ablate != 5) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
         float pm[PPL], ps[PPL];
 #pragma unroll
         for (int u = 0; u < PPL; ++u) {
@@ -943,10 +949,11 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             const int srcl = __ffs(ball) - 1;
             bk = 2 * srcl + (__shfl_sync(0xffffffffu, hit0 ? 0 : 1, srcl));
         }
-        const float t_s = bk >= kHistBins - 1
-                              ? kNegInf
-                              : M - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
-                                    (fabsf(M) * 0x1p-18f + 0x1p-20f);
+        float t_s = bk >= kHistBins - 1
+                        ? kNegInf
+                        : M - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
+                              (fabsf(M) * 0x1p-18f + 0x1p-20f);
+        if (A.ablate == 4) t_s = M - 10.0f * eps;  // DIAGNOSTIC: no histogram
         float a_below = kNegInf;
         int in_s = 0;
 #pragma unroll
@@ -972,7 +979,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     FRS_FTRACE(A, 4);
     const int nsel = s_nsel;
     // ---- 3. exact recompute of my share (none if S overflowed: the leader falls back)
-    const int nmine = nsel <= kCsMax ? min(s_nmine, kCsMax) : 0;
+    const int nmine = (nsel <= kCsMax && A.ablate != 2) ? min(s_nmine, kCsMax) : 0;
     for (int r0 = 0; r0 < nmine; r0 += kCandPerFinCta) {
         const int nc = min(kCandPerFinCta, nmine - r0);
         constexpr int TPT = 2;  // uint4 per thread per row and batch: T <= 512 in one batch
@@ -1071,6 +1078,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             if (s_pmw[w] != kNegInf) tot += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
     }
     const int ns = nsel <= kCsMax ? s_cnt : 0;  // == nsel when nothing overflowed
+    if (A.ablate == 3) return;
     select_certify(A, i, ns, nsel, kk, a_bound, eps, any_bad != 0, tot, mm, s_fin, s_sel, s_sorted, s_tab, s_spos,
                    s_ord);
 }
@@ -1439,6 +1447,8 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
         if ((st = ctx->fast_ctr.ensure(kCtrBytes))) return st;
         FRS_CUDA_TRY(cudaMemset(ctx->fast_ctr.ptr, 0, kCtrBytes));
     }
+    static const int late = std::getenv("FRS_ABLATE") && std::atoi(std::getenv("FRS_ABLATE")) == 8;
+    w.P.late_trigger = late;
     w.P.rowmax_bits = reinterpret_cast<unsigned *>(static_cast<uint8_t *>(ctx->fast_ctr.ptr) + kCtrRowmax);
     w.P.w2_bits = w.P.rowmax_bits + 64;
     return FRS_OK;
@@ -1549,6 +1559,7 @@ int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     cfg.numAttrs = 2;
     FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
     ++ctx->launches;
+    if (A.ablate == 7) return FRS_OK;  // DIAGNOSTIC: no fallback kernel
     return launch_fallback(ctx, A, s);
 }
 
@@ -1834,6 +1845,8 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
     A.out_flags = out_flags;
     A.argmax = argmax ? 1 : 0;
     A.id_offset = id_offset;
+    static const int ablate = std::getenv("FRS_ABLATE") ? std::atoi(std::getenv("FRS_ABLATE")) : 0;
+    A.ablate = ablate;
     return launch_fin(ctx, A, n, s);
 }
 
