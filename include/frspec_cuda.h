@@ -68,6 +68,8 @@ typedef enum { FRS_MODE_EXACT = 0, FRS_MODE_FAST = 1 } frs_mode;
 #define FRS_FLAG_CERT_TIE 0x10u      /* two selected probabilities within 4 ulps: order needs exact Σ  */
 #define FRS_FLAG_CERT_BOUND 0x20u    /* the rigorous error bound did not separate the k-th candidate   */
 #define FRS_FLAG_CERT_OVERFLOW 0x40u /* more near-boundary candidates than the exact-recompute set     */
+/* FAST, certified rows: bits 8..15 hold the size of the exactly recomputed candidate set (info). */
+#define FRS_FLAG_CAND_SHIFT 8
 
 typedef struct frs_ctx frs_ctx;
 typedef struct frs_head frs_head;

@@ -690,7 +690,7 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
         if (lane == 0) {
             A.out_full[i] = A.id_offset + dev::key_index(best);
             if (A.out_prob) A.out_prob[i] = lb;
-            if (A.out_flags) A.out_flags[i] = 0u;
+            if (A.out_flags) A.out_flags[i] = static_cast<uint32_t>(min(ns, 255)) << 8;  // |S| (info)
         }
         FRS_FTRACE(A, 7);
         return;
@@ -778,7 +778,7 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
     if (lane == 0) {
         if (A.out_rowmax) A.out_rowmax[i] = mx;
         if (A.out_total) A.out_total[i] = total;
-        if (A.out_flags) A.out_flags[i] = 0u;
+        if (A.out_flags) A.out_flags[i] = static_cast<uint32_t>(min(ns, 255)) << 8;  // |S| (info)
     }
     FRS_FTRACE(A, 7);
 }

@@ -53,6 +53,8 @@ def main():
         flags_all.append(f)
         (rec_times if (f & _lib.FLAG_RECOMPUTED).any() else times).append(e0.elapsed_time(e1) * 1000)
     F = np.concatenate(flags_all)
+    ns = (F >> 8) & 0xff
+    cert = (F & _lib.FLAG_RECOMPUTED) == 0
     res = {
         "v_sub": a.v_sub, "rows": a.rows, "calls": a.calls,
         "us_certified_calls": {"median": float(np.median(times)) if times else None,
@@ -63,6 +65,8 @@ def main():
         "reason_tie": int(((F & 0x10) != 0).sum()), "reason_bound": int(((F & 0x20) != 0).sum()),
         "reason_overflow": int(((F & 0x40) != 0).sum()),
         "slab_bytes": a.v_sub * a.d * 2,
+        "cand_set_size": {"mean": float(ns[cert].mean()), "p50": float(np.median(ns[cert])),
+                          "p99": float(np.percentile(ns[cert], 99)), "max": int(ns[cert].max())},
     }
     med = res["us_certified_calls"]["median"]
     if med:
