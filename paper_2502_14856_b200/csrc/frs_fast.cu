@@ -63,7 +63,9 @@ constexpr int R = 3;         // candidate keys per list (per epilogue warp and h
 constexpr int kListsPerCta = 4;  // one list per TMEM lane quarter (32 slab rows of every tile)
 constexpr int kFinThreads = 256;
 constexpr int kFbThreads = 256;
-constexpr int kCandPerFinCta = 8;  // exact recomputes per finalize CTA (8 lanes each)
+constexpr int kCandPerFinCta = 8;  // exact recomputes per batched-select round (8 lanes each)
+constexpr int kFinStage = 8;       // max candidates staged per finalize round (runtime A.fin_stage:
+                                   // 8 for drafts (150 KB smem), 4 for verify (83 KB, 2 CTAs/SM))
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -621,6 +623,8 @@ struct FinArgs {
     unsigned *fb_count;              // fallback queue: count, entries row | reasons << 16
     uint32_t *fb_rows;               // [64]
     int ablate;                      // DIAGNOSTIC ONLY (FRS_ABLATE): skip finalize phases for timing
+    int fin_ctas;                    // finalize cluster width (power of 2, <= kFinCtas): 8 draft, 2 verify
+    int fin_stage;                   // candidates staged per round (<= kFinStage): 8 draft, 4 verify
     unsigned long long *fb_arrive;   // monotonic CTA arrival counter of k_fast_fallback
 };
 
@@ -962,7 +966,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             const float v = dev::key_value(kr[u]);
             if (v >= t_s) {
                 ++in_s;
-                if ((dev::key_index(kr[u]) & (kFinCtas - 1)) == b) {
+                if ((dev::key_index(kr[u]) & (A.fin_ctas - 1)) == b) {
                     const int pos = atomicAdd(&s_nmine, 1);
                     if (pos < kCsMax) s_mine[pos] = kr[u];
                 }
@@ -980,13 +984,13 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     const int nsel = s_nsel;
     // ---- 3. exact recompute of my share (none if S overflowed: the leader falls back)
     const int nmine = (nsel <= kCsMax && A.ablate != 2) ? min(s_nmine, kCsMax) : 0;
-    for (int r0 = 0; r0 < nmine; r0 += kCandPerFinCta) {
-        const int nc = min(kCandPerFinCta, nmine - r0);
+    for (int r0 = 0; r0 < nmine; r0 += A.fin_stage) {
+        const int nc = min(A.fin_stage, nmine - r0);
         constexpr int TPT = 2;  // uint4 per thread per row and batch: T <= 512 in one batch
         for (int t0 = 0; t0 < T; t0 += TPT * kFinThreads) {
-            uint4 v[kCandPerFinCta][TPT];
+            uint4 v[kFinStage][TPT];
 #pragma unroll
-            for (int c = 0; c < kCandPerFinCta; ++c) {
+            for (int c = 0; c < kFinStage; ++c) {
                 const uint4 *row = reinterpret_cast<const uint4 *>(
                     A.slab + (size_t)dev::key_index(s_mine[r0 + (c < nc ? c : 0)]) * A.d);
 #pragma unroll
@@ -996,7 +1000,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
                 }
             }
 #pragma unroll
-            for (int c = 0; c < kCandPerFinCta; ++c) {
+            for (int c = 0; c < kFinStage; ++c) {
 #pragma unroll
                 for (int u = 0; u < TPT; ++u) {
                     const int t = t0 + tid + u * kFinThreads;
@@ -1540,11 +1544,11 @@ int launch_select(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     auto kern = k_fast_finalize;
     const int TP = fin_pitch(A.d / 8);
-    const size_t smem = (size_t)8 * TP * 4 + (size_t)kCandPerFinCta * 8 * TP * 4 + 64;
+    const size_t smem = (size_t)8 * TP * 4 + (size_t)A.fin_stage * 8 * TP * 4 + 64;
     if (smem > ctx->smem_optin) return fail(FRS_ENOTSUP, "FAST finalize: hidden_dim too large");
     if (int st = configure(kern, smem)) return st;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(rows, kFinCtas);
+    cfg.gridDim = dim3(rows, A.fin_ctas);
     cfg.blockDim = dim3(kFinThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -1553,7 +1557,7 @@ int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     at[1].id = cudaLaunchAttributeClusterDimension;  // the row's CTAs meet in one cluster
     at[1].val.clusterDim.x = 1;
-    at[1].val.clusterDim.y = kFinCtas;
+    at[1].val.clusterDim.y = A.fin_ctas;
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
@@ -1847,6 +1851,8 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
     A.id_offset = id_offset;
     static const int ablate = std::getenv("FRS_ABLATE") ? std::atoi(std::getenv("FRS_ABLATE")) : 0;
     A.ablate = ablate;
+    A.fin_ctas = argmax ? 2 : kFinCtas;  // argmax rows need ~1-3 exact candidates
+    A.fin_stage = argmax ? 4 : kFinStage;
     return launch_fin(ctx, A, n, s);
 }
 
