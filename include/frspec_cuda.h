@@ -183,6 +183,13 @@ FRS_API int frs_verify_greedy(frs_ctx *ctx, const float *h_dev, const void *W, i
                       int mode, const int32_t *tokens, const int32_t *parents, int k,
                       int32_t *emitted, int *n_emitted, int32_t *path, int *n_path);
 
+/* verify_greedy with the hidden rows gathered on the device from table[V_table x d] by
+ * [root_token, tokens...] (the head-path decode loop's identity layer). Host outputs. */
+FRS_API int frs_verify_greedy_table(frs_ctx *ctx, const float *table, int64_t V_table, int32_t root_token,
+                                    const void *W, int V, int d, int w_dtype, int mode, const int32_t *tokens,
+                                    const int32_t *parents, int k, int32_t *emitted, int *n_emitted, int32_t *path,
+                                    int *n_path);
+
 #ifdef __cplusplus
 }
 #endif

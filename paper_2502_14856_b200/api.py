@@ -457,6 +457,21 @@ def verify_greedy(ctx: Context, h_dev: torch.Tensor, lm_head: torch.Tensor, tree
     return VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy())
 
 
+def verify_greedy_table(ctx: Context, table: torch.Tensor, root_token: int, lm_head: torch.Tensor, tree: DraftTree,
+                        mode="exact") -> VerifyOutcome:
+    """verify_greedy with hidden rows gathered on the device from table[V x d] (CUDA float32)
+    by [root_token, tree.tokens...] — the head-path decode loop's identity draft/target layer."""
+    k = len(tree)
+    dt = DTYPE_BF16 if lm_head.dtype == torch.bfloat16 else DTYPE_F32
+    em, path = np.empty(k + 1, np.int32), np.empty(max(k, 1), np.int32)
+    ne, npth = C.c_int(), C.c_int()
+    tok, par = _i32(tree.tokens), _i32(tree.parents)
+    check(lib().frs_verify_greedy_table(ctx.handle, _ptr(table), table.shape[0], root_token, _ptr(lm_head),
+                                        lm_head.shape[0], lm_head.shape[1], dt, _mode(mode), _np_ptr(tok), _np_ptr(par),
+                                        k, _np_ptr(em), C.byref(ne), _np_ptr(path), C.byref(npth)), "verify_greedy")
+    return VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy())
+
+
 @dataclass
 class AcceptanceStats:  # verification.h:52-62, verification.cpp:180-206
     iterations: int = 0

@@ -76,6 +76,7 @@ struct frs_ctx {
     std::vector<frs::GraphEntry> graphs;  // captured FAST chains (LRU)
     uint64_t graph_clock = 0;
     cudaStream_t cap_stream = nullptr;    // private stream for graph capture
+    bool prefer_graphs = false;           // set by host loops that wait on every call (frs_draft_tree)
 };
 
 namespace frs {

@@ -1726,7 +1726,8 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     // cudaGraphLaunch, removing the per-call host cost of 3 tensor-map encodes and 4 launches.
     // Off by default: eager launches keep the PDL overlap with the previous call's tail
     // (measured 76.7 vs 78.9 us per C2 level back to back), and the host keeps ahead anyway.
-    static const bool use_graphs = std::getenv("FRS_GRAPH") != nullptr;
+    static const bool env_graphs = std::getenv("FRS_GRAPH") != nullptr;
+    const bool use_graphs = env_graphs || ctx->prefer_graphs;  // latency-bound callers (draft tree loop)
     GraphKey key{};
     if (use_graphs) {
         const uint64_t vals[] = {reinterpret_cast<uint64_t>(h), static_cast<uint64_t>(n), static_cast<uint64_t>(d),

@@ -282,13 +282,13 @@ int frs_head_info(const frs_head *h, const void **slab, const int32_t **ordered_
 static int head_staging(frs_head *h, int rows, int k) {
     const size_t cells = (size_t)rows * k;
     int st;
-    if ((st = h->lvl_ridx.ensure(cells * 4)) || (st = h->lvl_full.ensure(cells * 4)) ||
+    if ((st = h->lvl_ridx.ensure(cells * 12)) || (st = h->lvl_full.ensure(cells * 4)) ||
         (st = h->lvl_prob.ensure(cells * 4)) || (st = h->lvl_tok.ensure(64 * 4)) ||
         (st = h->hidden.ensure((size_t)std::max(rows, 64) * h->d * sizeof(float))))
         return st;
     if (!h->h_ridx) {
         const size_t cap = (size_t)64 * 64 * 4;
-        if (cudaMallocHost(&h->h_ridx, cap) != cudaSuccess || cudaMallocHost(&h->h_full, cap) != cudaSuccess ||
+        if (cudaMallocHost(&h->h_ridx, 3 * cap) != cudaSuccess || cudaMallocHost(&h->h_full, cap) != cudaSuccess ||
             cudaMallocHost(&h->h_prob, cap) != cudaSuccess || cudaMallocHost(&h->h_tok, 64 * 4) != cudaSuccess)
             return fail(FRS_ECUDA, "pinned staging allocation failed");
     }
@@ -350,15 +350,17 @@ int frs_draft_tree(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user
             const int rc = frs_gather_rows(h->ctx, hidden_table, h->vocab, h->d, tok_dev, nb, hd, s);
             if (rc) return rc;
         }
-        int rc = frs_draft_head_topk(h->ctx, hd, nb, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, w, 1.0f, mode,
-                                     static_cast<int32_t *>(h->lvl_ridx.ptr), static_cast<int32_t *>(h->lvl_full.ptr),
-                                     static_cast<float *>(h->lvl_prob.ptr), nullptr, nullptr, nullptr, nullptr, s);
-        if (rc) return rc;
+        // outputs packed [ridx | full | prob] (cells each) in lvl_ridx: one D2H per level
         const size_t cells = (size_t)nb * w;
-        FRS_CUDA_TRY(cudaMemcpyAsync(h->h_ridx, h->lvl_ridx.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
-        FRS_CUDA_TRY(cudaMemcpyAsync(h->h_full, h->lvl_full.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
-        FRS_CUDA_TRY(cudaMemcpyAsync(h->h_prob, h->lvl_prob.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
+        int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
+        int rc = frs_draft_head_topk(h->ctx, hd, nb, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, w, 1.0f, mode,
+                                     pk, pk + cells, reinterpret_cast<float *>(pk + 2 * cells), nullptr, nullptr,
+                                     nullptr, nullptr, s);
+        if (rc) return rc;
+        FRS_CUDA_TRY(cudaMemcpyAsync(h->h_ridx, pk, cells * 12, cudaMemcpyDeviceToHost, s));
         FRS_CUDA_TRY(cudaStreamSynchronize(s));
+        std::memcpy(h->h_full, h->h_ridx + cells, cells * 4);
+        std::memcpy(h->h_prob, h->h_ridx + 2 * cells, cells * 4);
         return FRS_OK;
     };
 
@@ -426,40 +428,78 @@ int frs_draft_tree(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user
     return FRS_OK;
 }
 
-int frs_verify_greedy(frs_ctx *ctx, const float *h_dev, const void *W, int V, int d, int w_dtype, int mode,
-                      const int32_t *tokens, const int32_t *parents, int k, int32_t *emitted, int *n_emitted,
-                      int32_t *path, int *n_path) {
-    FRS_REQUIRE(ctx && h_dev && W && emitted && n_emitted && path && n_path, "verify_greedy: null pointer");
+// Pinned staging shared by the verify entry points (one H2D of the tree, one D2H of the result).
+static int ctx_pinned(frs_ctx *ctx, size_t bytes) {
+    if (ctx->pinned_bytes >= bytes) return FRS_OK;
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    if (cudaMallocHost(&ctx->pinned, bytes) != cudaSuccess) return fail(FRS_ECUDA, "pinned staging allocation failed");
+    ctx->pinned_bytes = bytes;
+    return FRS_OK;
+}
+
+// verify_greedy (verification.cpp:42-71) on the device: verify head argmax over the 1 + k rows
+// of h_dev (root first), the accept walk, one packed D2H. table != nullptr: h_dev is ignored
+// and the rows are gathered from table[V_table x d] by [root_token, tokens...] on the device.
+static int verify_greedy_impl(frs_ctx *ctx, const float *h_dev, const float *table, int64_t V_table, int32_t root_token,
+                              const void *W, int V, int d, int w_dtype, int mode, const int32_t *tokens,
+                              const int32_t *parents, int k, int32_t *emitted, int *n_emitted, int32_t *path,
+                              int *n_path) {
     if (k > 64) return fail(FRS_ECAPACITY, "build_tree_mask: nodes exceed the 64-bit mask");
     FRS_REQUIRE(k >= 0 && (k == 0 || (tokens && parents)), "verify_greedy: bad tree");
     for (int i = 0; i < k; ++i)
         if (parents[i] >= i || parents[i] < -1) return fail(FRS_EINVAL, "verify_greedy: tree is not topological");
     FRS_CUDA_TRY(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    // device scratch: argmax ids [65] | tokens [64] | parents [64] | emitted [65] | path [64] | counts [2]
-    int st = ctx->obuf.ensure(sizeof(int32_t) * 324);
+    // device: argmax ids [65] | root+tokens [65] | parents [64] | emitted [65] | path [64] | counts [2]
+    int st = ctx->obuf.ensure(sizeof(int32_t) * 336);
     if (st) return st;
+    if ((st = ctx_pinned(ctx, sizeof(int32_t) * 336))) return st;
     int32_t *ids = static_cast<int32_t *>(ctx->obuf.ptr);
-    int32_t *tt = ids + 65, *pp = tt + 64, *d_em = pp + 64, *d_path = d_em + 65, *d_cnt = d_path + 64;
-    if (k > 0) {
-        FRS_CUDA_TRY(cudaMemcpyAsync(tt, tokens, sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
-        FRS_CUDA_TRY(cudaMemcpyAsync(pp, parents, sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
+    int32_t *rt = ids + 65, *pp = rt + 65, *d_em = pp + 64, *d_path = d_em + 65, *d_cnt = d_path + 64;
+    int32_t *hp = static_cast<int32_t *>(ctx->pinned);  // same layout from rt on
+    hp[0] = root_token;
+    std::copy(tokens, tokens + k, hp + 1);
+    std::copy(parents, parents + k, hp + 65);
+    FRS_CUDA_TRY(cudaMemcpyAsync(rt, hp, sizeof(int32_t) * (65 + 64), cudaMemcpyHostToDevice, s));
+    const float *hd = h_dev;
+    if (table) {
+        if ((st = ctx->hbuf.ensure((size_t)(1 + k) * d * sizeof(float)))) return st;
+        if ((st = frs_gather_rows(ctx, table, V_table, d, rt, 1 + k, static_cast<float *>(ctx->hbuf.ptr), s))) return st;
+        hd = static_cast<const float *>(ctx->hbuf.ptr);
     }
-    st = frs_verify_head_argmax(ctx, h_dev, 1 + k, d, W, V, w_dtype, 0, mode, ids, nullptr, nullptr, s);
+    st = frs_verify_head_argmax(ctx, hd, 1 + k, d, W, V, w_dtype, 0, mode, ids, nullptr, nullptr, s);
     if (st) return st;
-    st = frs_accept_greedy(ctx, ids, tt, pp, k, d_em, d_path, d_cnt, s);
+    st = frs_accept_greedy(ctx, ids, rt + 1, pp, k, d_em, d_path, d_cnt, s);
     if (st) return st;
-    int32_t cnt[2] = {0, 0};
-    std::vector<int32_t> em(65), pth(64);
-    FRS_CUDA_TRY(cudaMemcpyAsync(em.data(), d_em, sizeof(int32_t) * 65, cudaMemcpyDeviceToHost, s));
-    FRS_CUDA_TRY(cudaMemcpyAsync(pth.data(), d_path, sizeof(int32_t) * 64, cudaMemcpyDeviceToHost, s));
-    FRS_CUDA_TRY(cudaMemcpyAsync(cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    int32_t *ho = hp + 129;  // emitted [65] | path [64] | counts [2]
+    FRS_CUDA_TRY(cudaMemcpyAsync(ho, d_em, sizeof(int32_t) * (65 + 64 + 2), cudaMemcpyDeviceToHost, s));
     FRS_CUDA_TRY(cudaStreamSynchronize(s));
-    *n_emitted = cnt[0];
-    *n_path = cnt[1];
-    std::copy(em.begin(), em.begin() + cnt[0], emitted);
-    std::copy(pth.begin(), pth.begin() + cnt[1], path);
+    *n_emitted = ho[129];
+    *n_path = ho[130];
+    std::copy(ho, ho + *n_emitted, emitted);
+    std::copy(ho + 65, ho + 65 + *n_path, path);
     return FRS_OK;
+}
+
+int frs_verify_greedy(frs_ctx *ctx, const float *h_dev, const void *W, int V, int d, int w_dtype, int mode,
+                      const int32_t *tokens, const int32_t *parents, int k, int32_t *emitted, int *n_emitted,
+                      int32_t *path, int *n_path) {
+    FRS_REQUIRE(ctx && h_dev && W && emitted && n_emitted && path && n_path, "verify_greedy: null pointer");
+    return verify_greedy_impl(ctx, h_dev, nullptr, 0, 0, W, V, d, w_dtype, mode, tokens, parents, k, emitted,
+                              n_emitted, path, n_path);
+}
+
+int frs_verify_greedy_table(frs_ctx *ctx, const float *table, int64_t V_table, int32_t root_token, const void *W,
+                            int V, int d, int w_dtype, int mode, const int32_t *tokens, const int32_t *parents, int k,
+                            int32_t *emitted, int *n_emitted, int32_t *path, int *n_path) {
+    FRS_REQUIRE(ctx && table && W && emitted && n_emitted && path && n_path, "verify_greedy: null pointer");
+    FRS_REQUIRE(root_token >= 0 && root_token < V_table, "verify_greedy: root token outside the hidden table");
+    for (int i = 0; i < k; ++i)
+        FRS_REQUIRE(tokens[i] >= 0 && tokens[i] < V_table, "verify_greedy: token outside the hidden table");
+    return verify_greedy_impl(ctx, nullptr, table, V_table, root_token, W, V, d, w_dtype, mode, tokens, parents, k,
+                              emitted, n_emitted, path, n_path);
 }
 
 }  // extern "C"

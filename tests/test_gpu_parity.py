@@ -227,3 +227,21 @@ def test_draft_tree_identity_layer_table(cuda_ctx, restatement):
     ref = restatement.draft_tree(provider, restatement.restrict(W, ids), ids, 10, 6, 60)
     for key in ("tokens", "parents", "depths", "log_joint"):
         assert np.array_equal(getattr(tree, key), ref[key]), key
+
+
+def test_verify_greedy_table_matches_gathered(cuda_ctx, restatement):
+    """frs_verify_greedy_table (device gather of [root, tokens]) == verify_greedy on gathered rows."""
+    rng = np.random.default_rng(14)
+    V, d = 3000, 128
+    W = (rng.standard_normal((V, d)) * 0.05).astype(np.float32)
+    E = rmsnorm(rng.standard_normal((V, d)))
+    tree = api.DraftTree(np.array([5, 9, 11, 2], np.int32), np.array([-1, 0, 0, 1], np.int32),
+                         np.array([1, 2, 2, 3], np.int32), np.zeros(4))
+    Ed, Wd = torch.from_numpy(E).cuda(), torch.from_numpy(W).cuda()
+    a = api.verify_greedy_table(cuda_ctx, Ed, 77, Wd, tree)
+    rows = np.concatenate([[77], tree.tokens])
+    b = api.verify_greedy(cuda_ctx, torch.from_numpy(E[rows]).cuda(), Wd, tree)
+    assert np.array_equal(a.emitted, b.emitted) and np.array_equal(a.accepted_path, b.accepted_path)
+    ids = restatement.verify_argmax(E[rows], W)[0]
+    em, path = restatement.verify_greedy_ids(ids, tree.tokens, tree.parents)
+    assert np.array_equal(a.emitted, em) and np.array_equal(a.accepted_path, path)
