@@ -148,7 +148,7 @@ def run_reference(args):
     budget = min(120.0, max(20.0, 0.3 * (args.steps + args.warmup)))
     rate, kind, levels, el = cpu_reference_rate(slab, h, C2["k"], budget, threads)
     line = {"metric": METRIC, "value": rate, "unit": "draft-steps/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": levels, "warmup": 0, "ms_per_step": 1000.0 * threads / rate if rate else None,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * threads / rate if rate else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (N(0,0.02) fp32 slab, rmsnorm'd N(0,1) hidden rows)",
             "config": {"workload": "draft LM-head+top-k level (model.cpp:278 + drafting.cpp:204,37-43), "
