@@ -644,19 +644,23 @@ __host__ __device__ inline int fin_pitch(int T) {
 }
 
 constexpr int kMaxLists = 1024;  // L = 4 G <= 1024 lists of R keys per hidden row
+constexpr int kSurvMax = 128;     // finalize fast path: keys within 16 eps of the row max
 constexpr int kHistBins = 64;     // threshold histogram of (M - v) / bw: 48 linear bins, then
                                   // 4 bins per octave, the last one a catch-all
-__device__ __forceinline__ int hist_bin(float r) {  // r >= 0
-    if (!(r < 48.0f)) {
-        if (!(r < 48.0f * 0x1p15f)) return kHistBins - 1;  // also NaN
-        const int b = 48 + static_cast<int>(4.0f * log2f(r * (1.0f / 48.0f)));
-        return b < kHistBins - 1 ? b : kHistBins - 1;
-    }
-    return static_cast<int>(r);
+__device__ __forceinline__ int hist_bin(float r) {  // r >= 0 (NaN -> the catch-all bin)
+    if (r < 48.0f) return static_cast<int>(r);
+    // far bins from the float representation of q = r / 48 >= 1: 4 per octave by the top two
+    // mantissa bits (no log2f: this runs for every key of every list)
+    const uint32_t b = __float_as_uint(r * (1.0f / 48.0f));
+    const int e = static_cast<int>((b >> 23) & 0xffu) - 127, m = static_cast<int>((b >> 21) & 3u);
+    const int bin = 48 + 4 * e + m;
+    return (e < 0 || bin >= kHistBins - 1) ? kHistBins - 1 : bin;
 }
-// upper edge of bin j - 1 (= lower bound of r over bins >= j), with slack for log2f rounding
+// lower edge of bin j (= upper edge of bin j - 1) in units of bw
 __device__ __forceinline__ float hist_edge(int j) {
-    return j <= 48 ? static_cast<float>(j) : 48.0f * exp2f(0.25f * static_cast<float>(j - 48)) * (1.0f + 0x1p-10f);
+    if (j <= 48) return static_cast<float>(j);
+    const int t = j - 48;
+    return 48.0f * ldexpf(1.0f + 0.25f * static_cast<float>(t & 3), t >> 2);
 }
 
 // Selection + certification of one hidden row (warp 0 only; the other lanes of the CTA are
@@ -815,7 +819,9 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     __shared__ unsigned s_hist[kHistBins];
     __shared__ float s_fin[kCsMax];      // leader: exact logits of S, in arrival (slot) order
     __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
-    __shared__ int s_nsel, s_nmine, s_cnt, s_badw[kFinThreads / 32];
+    __shared__ int s_nsel, s_nmine, s_cnt, s_nsurv, s_badw[kFinThreads / 32];
+    __shared__ unsigned long long s_surv[kSurvMax], s_vk;
+    __shared__ float s_afar[kFinThreads / 32];
     FRS_FTRACE(A, 0);
     // no early griddepcontrol.launch_dependents here: 148 fallback CTAs parked in
     // griddepcontrol.wait next to this grid slowed it by ~2.7 us per call (measured)
@@ -861,6 +867,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             s_nsel = 0;
             s_nmine = 0;
             s_cnt = 0;
+            s_nsurv = 0;
         }
         if (tid < kHistBins) s_hist[tid] = 0u;
         if (tid < 32) s_tab[tid] = dev::kExp2fTable[tid];
@@ -887,14 +894,26 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
 #pragma unroll
     for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
     const float eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(W2) * 1.001)) * fast_gamma(A.d) * 1.01f;
-    const float bw = fmaxf(0.5f * eps, fabsf(M) * 0x1p-20f + 0x1p-30f), rbw = 1.0f / bw;
+    // coarse filter: the keys within 16 eps of the row max (typically ~30 per row) are the only
+    // ones that can matter unless the top-k is spread wider (then the histogram path below)
+    const float t0 = M - 16.0f * eps - (fabsf(M) * 0x1p-18f + 0x1p-20f);
+    {
+        float a_far = kNegInf;
 #pragma unroll
-    for (int u = 0; u < KPT; ++u) {  // warp-aggregated: one shared atomic per distinct bin
-        if (A.ablate == 4) break;
-        const int bin = kr[u] != 0ull ? hist_bin((M - dev::key_value(kr[u])) * rbw) : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, bin);
-        if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
+        for (int u = 0; u < KPT; ++u) {
+            if (kr[u] == 0ull) continue;
+            const float v = dev::key_value(kr[u]);
+            if (v >= t0) {
+                const int pos = atomicAdd(&s_nsurv, 1);
+                if (pos < kSurvMax) s_surv[pos] = kr[u];
+            } else {
+                a_far = fmaxf(a_far, v);
+            }
+        }
+        a_far = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_far)));
+        if (lane == 0) s_afar[warp] = a_far;
     }
+    FRS_FTRACE(A, 11);  // filter done (thread 0's share)
     constexpr int SW = 4;                        // warps merging the softmax partials
     constexpr int PPL = kMaxLists / (32 * SW);   // partials per lane
     if (warp < SW && !A.argmax && A.ablate != 5) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
@@ -935,8 +954,54 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     }
     __syncthreads();
     FRS_FTRACE(A, 3);
-    // ---- 2. threshold (every warp redundantly), S, my share of S, a_below
-    {
+    // ---- 2. the kk-th largest key: rank counting among the survivors (fast path), or a
+    //         histogram of (M - v) / (eps / 2) over all keys (robust path: the top-k is spread
+    //         wider than the filter or there are too many survivors)
+    const int nsurv = s_nsurv;
+    bool robust = nsurv < kk || nsurv > kSurvMax;
+    if (!robust) {
+        if (tid < nsurv) {
+            const unsigned long long mine = s_surv[tid];
+            int rank = 0;
+#pragma unroll 8
+            for (int c = 0; c < kSurvMax; ++c) rank += (c < nsurv) & (s_surv[c] > mine);
+            if (rank == kk - 1) s_vk = mine;
+        }
+        __syncthreads();
+        const float vk = dev::key_value(s_vk);
+        const float t_s = vk - 2.0f * eps - (fabsf(vk) * 0x1p-18f + 0x1p-20f);
+        robust = t_s < t0;  // S would reach below the filter: uniform across the cluster
+        if (!robust) {
+            float a_below = kNegInf;
+            int in_s = 0;
+            if (tid < nsurv) {
+                const unsigned long long key = s_surv[tid];
+                const float v = dev::key_value(key);
+                if (v >= t_s) {
+                    in_s = 1;
+                    if ((dev::key_index(key) & (A.fin_ctas - 1)) == b) {
+                        const int pos = atomicAdd(&s_nmine, 1);
+                        if (pos < kCsMax) s_mine[pos] = key;
+                    }
+                } else {
+                    a_below = v;
+                }
+            }
+            in_s = __reduce_add_sync(0xffffffffu, in_s);
+            if (lane == 0 && in_s) atomicAdd(&s_nsel, in_s);
+            a_below = fmaxf(dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_below))), s_afar[warp]);
+            if (lane == 0) s_abw[warp] = a_below;
+        }
+    }
+    if (robust) {
+        const float bw = fmaxf(0.5f * eps, fabsf(M) * 0x1p-20f + 0x1p-30f), rbw = 1.0f / bw;
+#pragma unroll
+        for (int u = 0; u < KPT; ++u) {  // warp-aggregated: one shared atomic per distinct bin
+            const int bin = kr[u] != 0ull ? hist_bin((M - dev::key_value(kr[u])) * rbw) : -1;
+            const unsigned peers = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
+        }
+        __syncthreads();
         const unsigned c0 = s_hist[2 * lane], c1 = s_hist[2 * lane + 1];
         unsigned incl = c0 + c1;
 #pragma unroll
@@ -953,11 +1018,9 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             const int srcl = __ffs(ball) - 1;
             bk = 2 * srcl + (__shfl_sync(0xffffffffu, hit0 ? 0 : 1, srcl));
         }
-        float t_s = bk >= kHistBins - 1
-                        ? kNegInf
-                        : M - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
-                              (fabsf(M) * 0x1p-18f + 0x1p-20f);
-        if (A.ablate == 4) t_s = M - 10.0f * eps;  // DIAGNOSTIC: no histogram
+        const float t_s = bk >= kHistBins - 1 ? kNegInf
+                                              : M - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
+                                                    (fabsf(M) * 0x1p-18f + 0x1p-20f);
         float a_below = kNegInf;
         int in_s = 0;
 #pragma unroll
@@ -1814,7 +1877,9 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
         cfg.numAttrs = 1;
         unsigned long long *xtrace = w.P.trace ? w.P.trace + (size_t)G * kTrMain + 64 * kFinCtas * 16 : nullptr;
         if ((st = configure(k_hsplit, 0))) return st;
-        FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, w.P.rowmax_bits, w.P.w2_bits, xtrace));
+        static const bool skip_hs = std::getenv("FRS_ABLATE") && std::atoi(std::getenv("FRS_ABLATE")) == 10;
+        if (!skip_hs)  // DIAGNOSTIC (FRS_ABLATE=10): measure the chain without the split kernel
+            FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, w.P.rowmax_bits, w.P.w2_bits, xtrace));
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;

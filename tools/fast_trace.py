@@ -26,8 +26,7 @@ SLOTS = {28: "main entry", 0: "setup done", 1: "producer: before griddep_wait", 
          25: "loop done w5", 26: "loop done w6", 27: "loop done w7"}
 FSLOTS = {0: "fin start", 1: "fin h loaded", 2: "fin after griddep_wait", 3: "fin partials merged",
           4: "fin S selected", 5: "fin recompute done", 6: "fin last: certified?", 7: "fin last: written",
-          8: "fin hist done", 9: "fin S collected", 10: "fin leader: after cluster wait",
-          11: "fin leader: mx", 13: "fin leader: e-keys ranked", 14: "fin leader: ties", 15: "fin leader: certified",
+          6: "fin keys+M+eps ready", 11: "fin histogram issued", 10: "fin leader: after cluster wait",
           12: "fin cand rows staged"}
 
 
