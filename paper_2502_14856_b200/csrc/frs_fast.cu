@@ -709,13 +709,19 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
     const float mx = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(fmaxf(x0, x1))));
     const unsigned long long e0 = have0 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x0, mx), tab), j0) : 0ull;
     const unsigned long long e1 = have1 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x1, mx), tab), j1) : 0ull;
-    // rank of each e-key among the ns (distinct: the index is part of the key)
+    // rank of each e-key among the ns (distinct: the index is part of the key): the keys go to
+    // shared memory once, then every lane's loop is independent broadcast loads (no shuffle chain)
+    if (have0) s_sorted[lane] = e0;
+    if (have1) s_sorted[lane + 32] = e1;
+    __syncwarp();
     int r0 = 0, r1 = 0;
+#pragma unroll 8
     for (int c = 0; c < ns; ++c) {
-        const unsigned long long o = __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31);
+        const unsigned long long o = s_sorted[c];
         r0 += o > e0;
         r1 += o > e1;
     }
+    __syncwarp();
     if (have0) {
         s_sorted[r0] = e0;
         s_spos[r0] = lane;
