@@ -113,42 +113,109 @@ struct ReduceScratch {
     unsigned long long k[32];
 };
 
+// Calls f(j, p[j]) for j in [0, v) split over the block, with U loads in flight per thread:
+// float4 loads when p is 16-byte aligned (each thread takes 4 consecutive j), else scalar.
+// A one-load-per-iteration loop over an L2-resident row is latency-bound (~30 us per 32K).
+template <int U, typename F>
+__device__ __forceinline__ void row_pass(const float *p, int v, F &&f) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+        const float4 *p4 = reinterpret_cast<const float4 *>(p);
+        const int v4 = v >> 2;
+        for (int base = 0; base < v4; base += U * nt) {
+            float4 b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = base + u * nt + tid;
+                if (q < v4) b[u] = __ldcg(p4 + q);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = base + u * nt + tid;
+                if (q < v4) {
+                    f(4 * q, b[u].x);
+                    f(4 * q + 1, b[u].y);
+                    f(4 * q + 2, b[u].z);
+                    f(4 * q + 3, b[u].w);
+                }
+            }
+        }
+        for (int j = 4 * v4 + tid; j < v; j += nt) f(j, __ldcg(p + j));
+    } else {
+        for (int base = 0; base < v; base += 4 * U * nt) {
+            float b[4 * U];
+#pragma unroll
+            for (int u = 0; u < 4 * U; ++u) {
+                const int j = base + u * nt + tid;
+                if (j < v) b[u] = __ldcg(p + j);
+            }
+#pragma unroll
+            for (int u = 0; u < 4 * U; ++u) {
+                const int j = base + u * nt + tid;
+                if (j < v) f(j, b[u]);
+            }
+        }
+    }
+}
+
 // Exact softmax (kernels.cpp:62-91) + top-kk (kernels.cpp:93-111) + remap for ONE row whose
 // exact logits are L[0..v): the whole block cooperates; E is a [v] float scratch. Writes
 // out[0..k) (entries past min(k, v) get -1 / 0). Returns flags (thread 0's copy is valid).
+// tree_total_ok (FAST fallback rows): ids and probabilities stay bit-exact but *out_total may
+// be the tree sum (within v 2^-52 relative) when that pins the reference's 1 / total.
 static __device__ __noinline__ uint32_t softmax_topk_row(const float *__restrict__ L, int v, int k,
                                                          float temperature, const int32_t *__restrict__ ordered,
                                                          float *__restrict__ E, int32_t *out_ridx, int32_t *out_full,
                                                          float *out_prob, float *out_rowmax, double *out_total,
-                                                         ReduceScratch &rs) {
+                                                         ReduceScratch &rs, bool tree_total_ok = false,
+                                                         unsigned long long *stamps = nullptr) {
     const int tid = threadIdx.x, nt = blockDim.x;
+#define FRS_STAMP(q)                                                                                  \
+    do {                                                                                              \
+        if (stamps && tid == 0) {                                                                     \
+            unsigned long long t_;                                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
+            stamps[q] = t_;                                                                           \
+        }                                                                                             \
+    } while (0)
     load_exp_table(rs.tab);
     float mx = -__int_as_float(0x7f800000);
     int bad = 0;
-    for (int j = tid; j < v; j += nt) {
-        const float x = L[j];
+    const bool unit_t = temperature == 1.0f;  // x / 1 == x: skip the IEEE divisions
+    row_pass<8>(L, v, [&](int, float x) {
         if (!isfinite(x)) bad = 1;
-        const float y = __fdiv_rn(x, temperature);
+        const float y = unit_t ? x : __fdiv_rn(x, temperature);
         mx = (mx < y) ? y : mx;
-    }
+    });
     mx = block_reduce(mx, MaxF(), rs.f);
     bad = block_reduce(bad, OrI(), rs.i);
     uint32_t flags = bad ? FRS_FLAG_NONFINITE : 0u;
+    FRS_STAMP(0);
 
     double part = 0.0;
     int lsb = 0x7fffffff;
-    for (int j = tid; j < v; j += nt) {
-        const float e = expf_glibc(__fsub_rn(__fdiv_rn(L[j], temperature), mx), rs.tab);
+    row_pass<8>(L, v, [&](int j, float x) {
+        const float e = expf_glibc(__fsub_rn(unit_t ? x : __fdiv_rn(x, temperature), mx), rs.tab);
         E[j] = e;
         part += static_cast<double>(e);
         lsb = min(lsb, lsb_exponent(e));
-    }
+    });
     double total = block_reduce(part, SumD(), rs.d);
     lsb = block_reduce(lsb, MinI(), rs.i);
+    FRS_STAMP(1);
     // Every partial sum (in any order) is exact iff all e_j are multiples of
     // 2^(ilogb(total)-51) (one bit of slack keeps it rigorous): then the tree sum equals the
     // reference's index-order sum. Otherwise replay the reference order (kernels.cpp:80-85).
-    const bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
+    bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
+    if (!exact && tree_total_ok && total > 0.0) {
+        // FAST fallback rows need the reference's inv = float(1 / total) exactly, not total
+        // itself: the tree sum and the index-order sum both lie within gamma_v * S of the
+        // exact sum S of v positive terms, so |tree - seq| <= v 2^-52 S (slack: 2 nt more),
+        // and inv(x) = float(fl64(1 / x)) is monotone, so equal ends of the interval pin it.
+        const double del = static_cast<double>(v + 2 * nt) * 0x1p-52;
+        const double lo = __dmul_rd(total, 1.0 - del), hi = __dmul_ru(total, 1.0 + del);
+        exact = __double2float_rn(1.0 / lo) == __double2float_rn(1.0 / hi);
+    }
     if (!exact) {
         flags |= FRS_FLAG_SEQ_SUM;
         __syncthreads();
@@ -161,29 +228,68 @@ static __device__ __noinline__ uint32_t softmax_topk_row(const float *__restrict
         total = rs.d[0];
     }
     const float inv = __double2float_rn(1.0 / total);
+    FRS_STAMP(2);
 
-    unsigned long long cand = 0ull;
-    for (int j = tid; j < v; j += nt) {
-        const unsigned long long key = prob_key(__fmul_rn(E[j], inv), j);
-        cand = key > cand ? key : cand;
-    }
+    // top-kk: every thread keeps its KL best keys (descending, 0 = empty); each round the
+    // block max is popped from its owner's list, which rescans its slice below the popped key
+    // only when the list runs dry while the slice held more than KL keys
+    constexpr int KL = 4;
+    unsigned long long lst[KL];
+#pragma unroll
+    for (int q = 0; q < KL; ++q) lst[q] = 0ull;
+    int nmine = 0;
+    __syncthreads();  // E written by other threads of the block
+    row_pass<8>(E, v, [&](int j, float e) {
+        unsigned long long key = prob_key(__fmul_rn(e, inv), j);
+        ++nmine;
+#pragma unroll
+        for (int q = 0; q < KL; ++q) {  // insertion into the sorted list
+            const unsigned long long o = lst[q];
+            const bool gt = key > o;
+            lst[q] = gt ? key : o;
+            key = gt ? o : key;
+        }
+    });
+    FRS_STAMP(3);
+    int left = nmine;  // keys of this slice not yet popped
     const int kk = min(k, v);
     for (int r = 0; r < kk; ++r) {
-        const unsigned long long best = block_reduce(cand, MaxU64(), rs.k);
+        const unsigned long long best = block_reduce(lst[0], MaxU64(), rs.k);
         const int j = key_index(best);
         if (tid == 0) {
             out_ridx[r] = j;
             out_full[r] = ordered ? ordered[j] : j;
             out_prob[r] = __uint_as_float(static_cast<uint32_t>(best >> 32));
         }
-        if (j % nt == tid) {  // the owner rescans for its best key below `best`
-            cand = 0ull;
-            for (int jj = tid; jj < v; jj += nt) {
-                const unsigned long long key = prob_key(__fmul_rn(E[jj], inv), jj);
-                if (key < best && key > cand) cand = key;
+        if (lst[0] == best) {  // the owner (keys are distinct: the index is part of the key)
+#pragma unroll
+            for (int q = 0; q + 1 < KL; ++q) lst[q] = lst[q + 1];
+            lst[KL - 1] = 0ull;
+            --left;
+            if (lst[0] == 0ull && left > 0) {  // dry: rebuild from the slice below `best`
+                // (this thread's slice only: row_pass's split is a function of tid, v and E's
+                // alignment alone, so the scalar walk below visits the same j)
+                const bool vec = (reinterpret_cast<uintptr_t>(E) & 15u) == 0;
+                const int v4 = vec ? (v >> 2) : 0;
+                auto take = [&](int jj) {
+                    unsigned long long key = prob_key(__fmul_rn(E[jj], inv), jj);
+                    if (key >= best) return;
+#pragma unroll
+                    for (int q = 0; q < KL; ++q) {
+                        const unsigned long long o = lst[q];
+                        const bool gt = key > o;
+                        lst[q] = gt ? key : o;
+                        key = gt ? o : key;
+                    }
+                };
+                for (int q = tid; q < v4; q += nt)
+                    for (int c = 0; c < 4; ++c) take(4 * q + c);
+                for (int jj = 4 * v4 + tid; jj < v; jj += nt) take(jj);
             }
         }
     }
+    FRS_STAMP(4);
+#undef FRS_STAMP
     if (tid == 0) {
         for (int r = kk; r < k; ++r) {
             out_ridx[r] = -1;

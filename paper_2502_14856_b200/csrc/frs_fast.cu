@@ -63,7 +63,6 @@ constexpr int R = 3;         // candidate keys per list (per epilogue warp and h
 constexpr int kListsPerCta = 4;  // one list per TMEM lane quarter (32 slab rows of every tile)
 constexpr int kFinThreads = 256;
 constexpr int kFbThreads = 256;
-constexpr int kCandPerFinCta = 8;  // exact recomputes per batched-select round (8 lanes each)
 constexpr int kFinStage = 8;       // max candidates staged per finalize round (runtime A.fin_stage:
                                    // 8 for drafts (150 KB smem), 4 for verify (83 KB, 2 CTAs/SM))
 
@@ -601,8 +600,8 @@ __device__ __forceinline__ float fast_gamma(int d) {
     return static_cast<float>(g * 1.01);
 }
 
-constexpr int kCsMax = 64;    // max exactly-recomputed candidates per row (kFinCtas x 8)
-constexpr int kFinCtas = kCsMax / kCandPerFinCta;
+constexpr int kCsMax = 128;   // max exactly-recomputed candidates per row (overflow: fallback)
+constexpr int kFinCtas = 8;    // finalize cluster width for draft rows (portable cluster size)
 
 struct FinArgs {
     const float *h;
@@ -677,17 +676,25 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
     const float s_mmax = mmax_approx;
     uint32_t why = (nsel > kCsMax || ns < kk) ? FRS_FLAG_CERT_OVERFLOW : 0u;
     if (any_bad) why |= FRS_FLAG_NONFINITE;
-    const bool have0 = lane < ns, have1 = lane + 32 < ns;
-    const float l0 = have0 ? s_fin[lane] : kNegInf;
-    const float l1 = have1 ? s_fin[lane + 32] : kNegInf;
-    const int j0 = have0 ? dev::key_index(s_sel[lane]) : 0, j1 = have1 ? dev::key_index(s_sel[lane + 32]) : 0;
+    constexpr int CPL = kCsMax / 32;  // candidates per lane
+    bool hq[CPL];
+    float lq[CPL];
+    int jq[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+        const int c = lane + 32 * q;
+        hq[q] = c < ns;
+        lq[q] = hq[q] ? s_fin[c] : kNegInf;
+        jq[q] = hq[q] ? dev::key_index(s_sel[c]) : 0;
+    }
     if (A.argmax) {
         unsigned long long bv = 0ull;
-        if (have0) bv = dev::value_key(l0, j0);
-        if (have1) {
-            const unsigned long long k1 = dev::value_key(l1, j1);
-            bv = k1 > bv ? k1 : bv;
-        }
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+            if (hq[q]) {
+                const unsigned long long kq = dev::value_key(lq[q], jq[q]);
+                bv = kq > bv ? kq : bv;
+            }
         const unsigned long long best = warp_max_key(bv);
         const float lb = dev::key_value(best);
         if (!(a_bound + eps < lb || a_bound == kNegInf)) why |= FRS_FLAG_CERT_BOUND;
@@ -705,42 +712,57 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
     }
     const unsigned long long *tab = s_tab;  // glibc exp table, staged by the caller's prologue
     const bool unit_t = A.temperature == 1.0f;  // x = l / 1 is exact: skip the IEEE divisions
-    const float x0 = unit_t ? l0 : __fdiv_rn(l0, A.temperature), x1 = unit_t ? l1 : __fdiv_rn(l1, A.temperature);
-    const float mx = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(fmaxf(x0, x1))));
-    const unsigned long long e0 = have0 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x0, mx), tab), j0) : 0ull;
-    const unsigned long long e1 = have1 ? dev::prob_key(dev::expf_glibc(__fsub_rn(x1, mx), tab), j1) : 0ull;
-    // rank of each e-key among the ns (distinct: the index is part of the key): the keys go to
-    // shared memory once, then every lane's loop is independent broadcast loads (no shuffle chain)
-    if (have0) s_sorted[lane] = e0;
-    if (have1) s_sorted[lane + 32] = e1;
+    float xq[CPL], xm = kNegInf;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+        xq[q] = unit_t ? lq[q] : __fdiv_rn(lq[q], A.temperature);
+        xm = fmaxf(xm, xq[q]);
+    }
+    const float mx = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(xm)));
+    unsigned long long eq[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+        eq[q] = hq[q] ? dev::prob_key(dev::expf_glibc(__fsub_rn(xq[q], mx), tab), jq[q]) : 0ull;
+        if (hq[q]) s_sorted[lane + 32 * q] = eq[q];
+    }
+    // rank of each e-key among the ns (distinct: the index is part of the key): independent
+    // broadcast loads from shared memory (no shuffle chain)
     __syncwarp();
-    int r0 = 0, r1 = 0;
-#pragma unroll 8
+    int rq[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) rq[q] = 0;
+#pragma unroll 4
     for (int c = 0; c < ns; ++c) {
         const unsigned long long o = s_sorted[c];
-        r0 += o > e0;
-        r1 += o > e1;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) rq[q] += o > eq[q];
     }
     __syncwarp();
-    if (have0) {
-        s_sorted[r0] = e0;
-        s_spos[r0] = lane;
-    }
-    if (have1) {
-        s_sorted[r1] = e1;
-        s_spos[r1] = lane + 32;
-    }
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+        if (hq[q]) {
+            s_sorted[rq[q]] = eq[q];
+            s_spos[rq[q]] = lane + 32 * q;
+        }
     __syncwarp();
     const int want = min(ns, kk + 1);
-    // near ties (within 4 ulps) among the selected and at the k boundary: the reference's
-    // (prob, index) order could depend on the exact denominator
+    // near ties (within 4 ulps) among the selected and at the k boundary: the probabilities
+    // e * (1 / total) of such a pair may round to one value under the exact denominator, and
+    // the reference then orders by index. Rounding is monotone, so only a pair whose e-order
+    // disagrees with its index order can change places (a collapsed run that is not index-
+    // ascending has such an adjacent pair).
     bool tie = false;
-    if (lane + 1 < want) {
-        const float ea = __uint_as_float(static_cast<uint32_t>(s_sorted[lane] >> 32));
-        const float eb = __uint_as_float(static_cast<uint32_t>(s_sorted[lane + 1] >> 32));
-        tie = ea != eb && ea <= eb * (1.0f + 0x1p-21f);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {  // want <= kk + 1 <= 65 adjacent pairs
+        const int r = lane + 32 * q;
+        if (r + 1 < want) {
+            const float ea = __uint_as_float(static_cast<uint32_t>(s_sorted[r] >> 32));
+            const float eb = __uint_as_float(static_cast<uint32_t>(s_sorted[r + 1] >> 32));
+            tie |= ea != eb && ea <= eb * (1.0f + 0x1p-21f) &&
+                   dev::key_index(s_sorted[r]) > dev::key_index(s_sorted[r + 1]);
+        }
     }
-    if (__any_sync(0xffffffffu, tie)) why |= FRS_FLAG_CERT_TIE;
+    if (__any_sync(0xffffffffu, tie) || A.ablate == 11) why |= FRS_FLAG_CERT_TIE;  // 11: DIAGNOSTIC
     if (!why && a_bound != kNegInf) {  // every non-recomputed row stays strictly below the k-th
         const float x_ub = __fdiv_ru(a_bound + eps, A.temperature) * (1.0f + 0x1p-20f) + 0x1p-20f;
         if (!(x_ub < mx)) {
@@ -1157,24 +1179,66 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
 }
 
 // Batched drafting (n > 16 hidden rows): per hidden row one CTA over the approximate logits
-// row written by k_fast_main<NP,false,true> (L2-resident: n x V_sub x 4 B). Three passes over
-// the row (max; Σexp + threshold histogram; candidate set S), exact recompute of S in chunks
-// of 8 candidates (dot_f32 order), then the same selection + certification as the finalize
-// (select_certify). Every row outside S has approx <= a_below, so a_bound = a_below.
+// row written by k_fast_main<NP,false,true> (L2-resident: n x V_sub x 4 B). Two float4 passes
+// over the row (max; Σexp + the survivors above a bound from the threads' maxima), t_s from a
+// histogram of the survivors (a third pass over the row only when they cannot hold the top-k),
+// exact recompute of S in rounds of A.fin_stage candidates whose slab rows arrive by bulk
+// copies (cp.async.bulk, one mbarrier), then the same selection + certification as the
+// finalize (select_certify). Every row outside S has approx <= a_below, so a_bound = a_below.
 constexpr int kSelThreads = 512;
+constexpr int kSelSurv = 512;  // survivor keys kept per row (beyond: the row-scan path)
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Warp 0: the first histogram bin whose cumulative count reaches kk -> the S threshold t_s
+// (every key in bins <= bk is >= M - bw * edge(bk + 1), up to the rounding of the bin index).
+__device__ __forceinline__ float hist_threshold(const unsigned *s_hist, int kk, float M, float bw, float eps) {
+    const int lane = threadIdx.x & 31;
+    const unsigned c0 = s_hist[2 * lane], c1 = s_hist[2 * lane + 1];
+    unsigned incl = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const unsigned excl = incl - c0 - c1;
+    const bool hit0 = excl < static_cast<unsigned>(kk) && excl + c0 >= static_cast<unsigned>(kk);
+    const bool hit1 = !hit0 && excl + c0 < static_cast<unsigned>(kk) && incl >= static_cast<unsigned>(kk);
+    const unsigned ball = __ballot_sync(0xffffffffu, hit0 || hit1);
+    int bk = kHistBins - 1;
+    if (ball) {
+        const int src = __ffs(ball) - 1;
+        bk = 2 * src + (__shfl_sync(0xffffffffu, hit0 ? 0 : 1, src));
+    }
+    const float kNegInf = -__int_as_float(0x7f800000);
+    return bk >= kHistBins - 1 ? kNegInf
+                               : M - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
+                                     (fabsf(M) * 0x1p-18f + 0x1p-20f);
+}
 
 __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
     extern __shared__ __align__(16) uint8_t ssm_raw[];
     const int T = A.d >> 3, TP = fin_pitch(T);
-    float *ht = reinterpret_cast<float *>(ssm_raw);  // [8][TP]
-    float *wt = ht + 8 * TP;                          // [8 cand][8][TP]
+    float *ht = reinterpret_cast<float *>(ssm_raw);  // [8][TP]: the hidden row, lane chains
+    // [fin_stage][d + 8] bf16: the candidates' slab rows as stored (16-byte pad: the 4 rows a
+    // warp reads sit in distinct bank quads)
+    unsigned short *wrows = reinterpret_cast<unsigned short *>(ht + 8 * TP);
+    const int wpitch = A.d + 8;
     __shared__ unsigned long long s_S[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
     __shared__ float s_fin[kCsMax], s_redf[kSelThreads / 32], s_abw[kSelThreads / 32];
     __shared__ double s_redd[kSelThreads / 32], s_hn2[kSelThreads / 32];
     __shared__ unsigned s_hist[kHistBins];
     __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
-    __shared__ int s_nsel, s_badw[kSelThreads / 32];
-    __shared__ float s_ts;
+    __shared__ int s_nsel, s_nsurv, s_badw[kSelThreads / 32];
+    __shared__ float s_ts, s_afar[kSelThreads / 32];
+    __shared__ unsigned long long s_surv[kSelSurv];
+    __shared__ __align__(8) uint64_t s_bar;
+    FRS_FTRACE(A, 0);
     griddep_launch();
 
     const int i = blockIdx.x, tid = threadIdx.x;
@@ -1203,25 +1267,53 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
             s_hn2[warp] = hn2;
             s_badw[warp] = bad;
         }
-        if (tid == 0) s_nsel = 0;
+        if (tid == 0) {
+            s_nsel = 0;
+            mbar_init(&s_bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
         if (tid < kHistBins) s_hist[tid] = 0u;
         if (tid < 32) s_tab[tid] = dev::kExp2fTable[tid];
     }
     griddep_wait();
+    FRS_FTRACE(A, 2);
     const float *Lr = A.P.logits + (size_t)i * A.P.ld_logits;
     const int v = A.v_rows;
     const float inv_t = 1.0f / A.temperature;
+    // The row is read with float4 loads, UNR in flight per thread, in CTA-uniform trip counts
+    // (a scalar loop paid the L2 latency on every element).
+    const float4 *Lr4 = reinterpret_cast<const float4 *>(Lr);
+    const int v4 = (v + 3) >> 2;
+    constexpr int UNR = 4;
     // ---- pass 1: max approximate logit; max |W_j|^2 (norm warps of the main kernel)
     float mx = kNegInf, w2 = 0.0f;
-    for (int j = tid; j < v; j += kSelThreads) mx = fmaxf(mx, __ldcg(Lr + j));
+    for (int base = 0; base < v4; base += UNR * kSelThreads) {
+        float4 b4[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int q = base + tid + u * kSelThreads;
+            b4[u] = q < v4 ? __ldcg(Lr4 + q) : make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int j = 4 * (base + tid + u * kSelThreads);
+            const float e[4] = {b4[u].x, b4[u].y, b4[u].z, b4[u].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (j + c < v) mx = fmaxf(mx, e[c]);
+        }
+    }
     for (int c = tid; c < 2 * A.P.G; c += kSelThreads) w2 = fmaxf(w2, __ldcg(A.P.pw2 + c));
+    const float mx_own = mx;  // this thread's max over its 4 * UNR * trips keys
     mx = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(mx)));
     w2 = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(w2)));
     if (lane == 0) {
         s_redf[warp] = mx;
         s_abw[warp] = w2;
     }
+    if (tid == 0) s_nsurv = 0;
     __syncthreads();
+    FRS_FTRACE(A, 3);
     float M = kNegInf, W2 = 0.0f;
     double h2 = 0.0;
 #pragma unroll
@@ -1232,60 +1324,152 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
     }
     const float eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(W2) * 1.001)) * fast_gamma(A.d) * 1.01f;
     const float bw = fmaxf(0.5f * eps, fabsf(M) * 0x1p-20f + 0x1p-30f), rbw = 1.0f / bw;
-    // ---- pass 2: Σ exp(x - max x) in the approximate domain + the threshold histogram
-    const float Mx = M * inv_t;
-    double tot = 0.0;
-    for (int j0 = 0; j0 < v; j0 += kSelThreads) {
-        const int j = j0 + tid;
-        const float a = j < v ? __ldcg(Lr + j) : kNegInf;
-        if (j < v && !A.argmax) tot += static_cast<double>(exp2f((a * inv_t - Mx) * 1.4426950408889634f));
-        const int bin = j < v ? hist_bin((M - a) * rbw) : -1;
+    // The survivor threshold t0 from the threads' maxima: they are distinct keys of the row, so
+    // the kk-th largest of them bounds the kk-th largest key v_k from below, and t0 =
+    // hist_threshold(thread maxima) <= v_k - 2 eps keeps every key S can need.
+    {
+        const int bin = hist_bin((M - mx_own) * rbw);
         const unsigned peers = __match_any_sync(0xffffffffu, bin);
-        if (bin >= 0 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
+        if (bin < kHistBins - 1 && lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const float ts = hist_threshold(s_hist, min(A.k, v), M, bw, eps);
+        if (lane == 0) s_ts = ts;
+        s_hist[2 * lane] = 0u;  // each lane read only its own two bins
+        s_hist[2 * lane + 1] = 0u;
+    }
+    __syncthreads();
+    // ---- pass 2: Σ exp(x - max x) (approximate domain) and the survivors (keys >= t0)
+    const float Mx = M * inv_t;
+    const float t0 = s_ts;
+    double tot = 0.0;
+    float a_far = kNegInf;
+    for (int base = 0; base < v4; base += UNR * kSelThreads) {
+        float4 b4[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int q = base + tid + u * kSelThreads;
+            b4[u] = q < v4 ? __ldcg(Lr4 + q) : make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+        }
+        float part = 0.0f;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int j = 4 * (base + tid + u * kSelThreads);
+            const float e[4] = {b4[u].x, b4[u].y, b4[u].z, b4[u].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (j + c >= v) continue;
+                if (!A.argmax) part += exp2f((e[c] * inv_t - Mx) * 1.4426950408889634f);
+                if (e[c] >= t0) {
+                    const int pos = atomicAdd(&s_nsurv, 1);
+                    if (pos < kSelSurv) s_surv[pos] = dev::value_key(e[c], j + c);
+                } else {
+                    a_far = fmaxf(a_far, e[c]);
+                }
+            }
+        }
+        tot += static_cast<double>(part);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if (lane == 0) s_redd[warp] = tot;
+    a_far = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_far)));
+    if (lane == 0) {
+        s_redd[warp] = tot;
+        s_afar[warp] = a_far;
+    }
     __syncthreads();
+    FRS_FTRACE(A, 4);
     const int kk = min(A.k, v);
-    if (warp == 0) {  // the first bin whose cumulative count reaches kk
-        const unsigned c0 = s_hist[2 * lane], c1 = s_hist[2 * lane + 1];
-        unsigned incl = c0 + c1;
+    const int nsurv = s_nsurv;
+    bool robust = nsurv < kk || nsurv > kSelSurv || t0 == kNegInf;
+    if (!robust) {  // histogram of the survivors -> t_s; S = survivors >= t_s
+        for (int c = tid; c < nsurv; c += kSelThreads) {
+            const int bin = hist_bin((M - dev::key_value(s_surv[c])) * rbw);
+            if (bin < kHistBins - 1) atomicAdd(&s_hist[bin], 1u);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const float ts = hist_threshold(s_hist, kk, M, bw, eps);
+            if (lane == 0) s_ts = ts;
+        }
+        __syncthreads();
+        const float t_s = s_ts;
+        robust = t_s < t0;  // S would reach below the survivors
+        if (!robust) {
+            float a_below = kNegInf;
+            for (int c = tid; c < nsurv; c += kSelThreads) {
+                const unsigned long long key = s_surv[c];
+                if (dev::key_value(key) >= t_s) {
+                    const int pos = atomicAdd(&s_nsel, 1);
+                    if (pos < kCsMax) s_S[pos] = key;
+                } else {
+                    a_below = fmaxf(a_below, dev::key_value(key));
+                }
+            }
+            a_below = fmaxf(dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_below))), s_afar[warp]);
+            if (lane == 0) s_abw[warp] = a_below;
+        } else if (tid < kHistBins) {
+            s_hist[tid] = 0u;
+        }
+        __syncthreads();
+    }
+    if (robust) {  // histogram of (M - a) / bw over the whole row, then S from the row
+        for (int base = 0; base < v4; base += UNR * kSelThreads) {
+            float4 b4[UNR];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            for (int u = 0; u < UNR; ++u) {
+                const int q = base + tid + u * kSelThreads;
+                b4[u] = q < v4 ? __ldcg(Lr4 + q) : make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int j = 4 * (base + tid + u * kSelThreads);
+                const float e[4] = {b4[u].x, b4[u].y, b4[u].z, b4[u].w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int bin = j + c < v ? hist_bin((M - e[c]) * rbw) : kHistBins - 1;
+                    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+                    if (bin < kHistBins - 1 && lane == __ffs(peers) - 1)
+                        atomicAdd(&s_hist[bin], static_cast<unsigned>(__popc(peers)));
+                }
+            }
         }
-        const unsigned excl = incl - c0 - c1;
-        const bool hit0 = excl < static_cast<unsigned>(kk) && excl + c0 >= static_cast<unsigned>(kk);
-        const bool hit1 = !hit0 && excl + c0 < static_cast<unsigned>(kk) && incl >= static_cast<unsigned>(kk);
-        const unsigned ball = __ballot_sync(0xffffffffu, hit0 || hit1);
-        int bk = kHistBins - 1;
-        if (ball) {
-            const int src = __ffs(ball) - 1;
-            bk = 2 * src + (__shfl_sync(0xffffffffu, hit0 ? 0 : 1, src));
+        __syncthreads();
+        if (warp == 0) {
+            const float ts = hist_threshold(s_hist, kk, M, bw, eps);
+            if (lane == 0) s_ts = ts;
         }
-        if (lane == 0)
-            s_ts = bk >= kHistBins - 1 ? kNegInf
-                                       : M - bw * hist_edge(bk + 1) * (1.0f + 0x1p-20f) - 2.0f * eps -
-                                             (fabsf(M) * 0x1p-18f + 0x1p-20f);
+        __syncthreads();
+        const float t_s = s_ts;
+        float a_below = kNegInf;
+        for (int base = 0; base < v4; base += UNR * kSelThreads) {
+            float4 b4[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int q = base + tid + u * kSelThreads;
+                b4[u] = q < v4 ? __ldcg(Lr4 + q) : make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int j = 4 * (base + tid + u * kSelThreads);
+                const float e[4] = {b4[u].x, b4[u].y, b4[u].z, b4[u].w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (j + c >= v) continue;
+                    if (e[c] >= t_s) {
+                        const int pos = atomicAdd(&s_nsel, 1);
+                        if (pos < kCsMax) s_S[pos] = dev::value_key(e[c], j + c);
+                    } else {
+                        a_below = fmaxf(a_below, e[c]);
+                    }
+                }
+            }
+        }
+        a_below = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_below)));
+        if (lane == 0) s_abw[warp] = a_below;
+        __syncthreads();
     }
-    __syncthreads();
-    // ---- pass 3: the candidate set S and the best value left out of it
-    const float t_s = s_ts;
-    float a_below = kNegInf;
-    for (int j = tid; j < v; j += kSelThreads) {
-        const float a = __ldcg(Lr + j);
-        if (a >= t_s) {
-            const int pos = atomicAdd(&s_nsel, 1);
-            if (pos < kCsMax) s_S[pos] = dev::value_key(a, j);
-        } else {
-            a_below = fmaxf(a_below, a);
-        }
-    }
-    a_below = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_below)));
-    if (lane == 0) s_abw[warp] = a_below;
-    __syncthreads();
     const int nsel = s_nsel, ns = min(nsel, kCsMax);
     if (tid < ns) {  // canonical (descending) order
         const unsigned long long mine = s_S[tid];
@@ -1295,48 +1479,51 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
     }
     __syncthreads();
     if (tid < ns && A.ordered) s_ord[tid] = __ldg(A.ordered + dev::key_index(s_sel[tid]));
-    // ---- exact recompute of S, 8 candidates per round
-    for (int c0 = 0; c0 < ns; c0 += kCandPerFinCta) {
-        const int nc = min(kCandPerFinCta, ns - c0);
-        for (int e = tid; e < nc * T; e += kSelThreads) {
-            const int c = e / T, t = e - c * T;
-            const uint4 u = __ldg(reinterpret_cast<const uint4 *>(A.slab + (size_t)dev::key_index(s_sel[c0 + c]) * A.d) + t);
-            float *dst = wt + (size_t)c * 8 * TP + t;
-            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {  // bf16 -> fp32 is exact
-                dst[(2 * q) * TP] = __uint_as_float(w4[q] << 16);
-                dst[(2 * q + 1) * TP] = __uint_as_float(w4[q] & 0xffff0000u);
+    FRS_FTRACE(A, 6);
+    if (A.P.trace && tid == 0)
+        A.P.trace[(size_t)A.P.G * kTrMain + (size_t)blockIdx.x * kFinCtas * 16 + 8] =
+            static_cast<unsigned long long>(ns) | (robust ? 1ull << 32 : 0ull);
+    // ---- exact recompute of S, A.fin_stage candidates per round (dot_f32 order: lane chain l
+    //      of candidate c = 8-lane group c of the CTA runs over t = 0..T-1, kernels.cpp:17-26)
+    const uint32_t row_bytes = static_cast<uint32_t>(A.d) * 2u;
+    for (int c0 = 0, round = 0; c0 < ns; c0 += A.fin_stage, ++round) {
+        const int nc = min(A.fin_stage, ns - c0);
+        if (warp == 0) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the last round's reads
+                mbar_expect_tx(&s_bar, row_bytes * static_cast<uint32_t>(nc));
             }
+            __syncwarp();
+            for (int c = lane; c < nc; c += 32)
+                bulk_g2s(wrows + (size_t)c * wpitch, A.slab + (size_t)dev::key_index(s_sel[c0 + c]) * A.d, row_bytes,
+                         &s_bar);
         }
-        __syncthreads();
         if (tid < ((nc * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
-            const int cl = (tid >> 3) < nc ? tid >> 3 : 0, l = tid & 7;
-            const float4 *hp = reinterpret_cast<const float4 *>(ht + l * TP);
-            const float4 *wp = reinterpret_cast<const float4 *>(wt + ((size_t)cl * 8 + l) * TP);
+            mbar_wait(&s_bar, round & 1);
+            if (c0 == 0) FRS_FTRACE(A, 12);
+            const int g = tid >> 3, cl = g < nc ? g : 0, l = tid & 7;
+            const float *hp = ht + l * TP;
+            const unsigned short *wp = wrows + (size_t)cl * wpitch + l;
             float s = 0.0f;
-            const int T8 = T / 8;
-            float4 w0 = wp[0], w1 = wp[1], h0 = hp[0], h1 = hp[1];
-            for (int t8 = 0; t8 < T8; ++t8) {
-                const int tn = t8 + 1 < T8 ? t8 + 1 : t8;
-                const float4 v0 = wp[2 * tn], v1 = wp[2 * tn + 1], g0 = hp[2 * tn], g1 = hp[2 * tn + 1];
-                const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-                const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            int t = 0;
+            for (; t + 4 <= T; t += 4) {
+                const float4 hv = *reinterpret_cast<const float4 *>(hp + t);
+                const float h4[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-                for (int q = 0; q < 8; ++q) s = __fadd_rn(s, __fmul_rn(hv[q], wv[q]));  // kernels.cpp:17-26
-                w0 = v0;
-                w1 = v1;
-                h0 = g0;
-                h1 = g1;
+                for (int q = 0; q < 4; ++q) {
+                    const float w = __uint_as_float(static_cast<uint32_t>(wp[8 * (t + q)]) << 16);  // exact
+                    s = __fadd_rn(s, __fmul_rn(h4[q], w));
+                }
             }
-            for (int t = T8 * 8; t < T; ++t) s = __fadd_rn(s, __fmul_rn(ht[l * TP + t], wt[((size_t)cl * 8 + l) * TP + t]));
+            for (; t < T; ++t) s = __fadd_rn(s, __fmul_rn(hp[t], __uint_as_float(static_cast<uint32_t>(wp[8 * t]) << 16)));
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));  // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7))
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
-            if (l == 0 && (tid >> 3) < nc) s_fin[c0 + cl] = s;
+            if (l == 0 && g < nc) s_fin[c0 + cl] = s;
         }
         __syncthreads();
     }
+    FRS_FTRACE(A, 5);
     if (warp != 0) return;
     float a_bound = kNegInf, mxx = kNegInf;
     double total = 0.0;
@@ -1357,6 +1544,8 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
 // hidden row — one thread per slab row carrying the reference's 8 lane chains, 16-byte slab
 // loads — and the last CTA to finish runs the exact softmax + top-k (or argmax) of those rows,
 // bit-identical to the EXACT path, then empties the queue.
+constexpr int kFbBatch = 8;  // 16-byte slab loads per batch of the fallback's exact dots
+
 __global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
     extern __shared__ uint8_t fbs_raw[];
     float *sh = reinterpret_cast<float *>(fbs_raw);  // [d]
@@ -1379,14 +1568,15 @@ __global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
         __syncthreads();
         for (int e = tid; e < A.d; e += blockDim.x) sh[e] = A.h[(size_t)i * A.d + e];
         __syncthreads();
+        // one thread per slab row carrying the 8 lane chains; the row streams in batches of
+        // kFbBatch 16-byte loads, the next batch in flight while the current one is consumed
+        // (4 loads in flight per thread left this phase latency-bound at ~1/3 of HBM speed)
+        const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
         for (int j = blockIdx.x * blockDim.x + tid; j < A.v_rows; j += G * blockDim.x) {
             const uint4 *w = reinterpret_cast<const uint4 *>(A.slab + (size_t)j * A.d);
             float c[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-            for (int t = 0; t < T; ++t) {
-                const uint4 u = __ldg(w + t);
-                const float4 h0 = reinterpret_cast<const float4 *>(sh)[2 * t];
-                const float4 h1 = reinterpret_cast<const float4 *>(sh)[2 * t + 1];
+            auto step = [&](const uint4 &u, int t) {
+                const float4 h0 = sh4[2 * t], h1 = sh4[2 * t + 1];
                 const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
                 const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
@@ -1394,7 +1584,23 @@ __global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
                     const float wv = __uint_as_float(l & 1 ? (uw[l >> 1] & 0xffff0000u) : (uw[l >> 1] << 16));
                     c[l] = __fadd_rn(c[l], __fmul_rn(hv[l], wv));
                 }
+            };
+            const int TB = T - T % kFbBatch;
+            uint4 cur[kFbBatch], nxt[kFbBatch];
+            if (TB > 0) {
+#pragma unroll
+                for (int b = 0; b < kFbBatch; ++b) cur[b] = __ldcs(w + b);
             }
+            for (int t0 = 0; t0 < TB; t0 += kFbBatch) {
+                const bool more = t0 + kFbBatch < TB;
+#pragma unroll
+                for (int b = 0; b < kFbBatch; ++b) nxt[b] = more ? __ldcs(w + t0 + kFbBatch + b) : cur[b];
+#pragma unroll
+                for (int b = 0; b < kFbBatch; ++b) step(cur[b], t0 + b);
+#pragma unroll
+                for (int b = 0; b < kFbBatch; ++b) cur[b] = nxt[b];
+            }
+            for (int t = TB; t < T; ++t) step(__ldcs(w + t), t);
             L[j] = __fadd_rn(__fadd_rn(__fadd_rn(c[0], c[1]), __fadd_rn(c[2], c[3])),
                              __fadd_rn(__fadd_rn(c[4], c[5]), __fadd_rn(c[6], c[7])));  // kernels.cpp:27
         }
@@ -1408,6 +1614,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    if (xtrace && threadIdx.x == 0) xtrace[4] = gtimer();
     for (unsigned f = 0; f < nfb; ++f) {
         const uint32_t ent = A.fb_rows[f];
         const int i = static_cast<int>(ent & 0xffffu);
@@ -1435,11 +1642,13 @@ __global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
                                                   A.out_ridx + (size_t)i * A.k, A.out_full + (size_t)i * A.k,
                                                   A.out_prob + (size_t)i * A.k,
                                                   A.out_rowmax ? A.out_rowmax + i : nullptr,
-                                                  A.out_total ? A.out_total + i : nullptr, rs);
+                                                  A.out_total ? A.out_total + i : nullptr, rs, true,
+                                                  xtrace && f == 0 ? xtrace + 8 : nullptr);
         if (tid == 0 && A.out_flags) A.out_flags[i] = flags | f2;
     }
     __syncthreads();
     if (tid == 0) *A.fb_count = 0u;
+    if (xtrace && threadIdx.x == 0) xtrace[5] = gtimer();
 }
 
 // ------------------------------------------------------------------ host side
@@ -1513,7 +1722,7 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.P.w2_bits = nullptr;
     static const bool tracing = std::getenv("FRS_TRACE") != nullptr;
     if (tracing) {
-        if ((st = ctx->trace.ensure((size_t)(G * kTrMain + 64 * kFinCtas * 16 + 8) * 8))) return st;
+        if ((st = ctx->trace.ensure((size_t)(G * kTrMain + 64 * kFinCtas * 16 + 16) * 8))) return st;
         w.P.trace = static_cast<unsigned long long *>(ctx->trace.ptr);
     }
     if (!ctx->fast_ctr.ptr) {  // zeroed once: counters are monotonic or reset in-stream
@@ -1590,10 +1799,21 @@ int launch_fallback(frs_ctx *ctx, const FinArgs &A, cudaStream_t s) {
     return FRS_OK;
 }
 
-int launch_select(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
+// Candidates per exact-recompute round of k_fast_select: bulk-copied slab rows (2d + 16 B
+// each) next to the hidden row's lane-chain tile, up to 16, within the opt-in shared memory
+// (the static arrays take ~12 KB). 0 = the batched path does not fit this hidden size.
+int sel_stage(const frs_ctx *ctx, int d) {
+    const size_t fixed = (size_t)8 * fin_pitch(d / 8) * 4 + 12 * 1024;
+    if (fixed >= (size_t)ctx->smem_optin) return 0;
+    return (int)std::min<size_t>(16, ((size_t)ctx->smem_optin - fixed) / ((size_t)2 * d + 16));
+}
+
+int launch_select(frs_ctx *ctx, const FinArgs &A0, int rows, cudaStream_t s) {
     auto kern = k_fast_select;
-    const int TP = fin_pitch(A.d / 8);
-    const size_t smem = (size_t)(8 + kCandPerFinCta * 8) * TP * 4;
+    FinArgs A = A0;
+    A.fin_stage = sel_stage(ctx, A.d);
+    if (A.fin_stage < 1) return fail(FRS_ENOTSUP, "FAST batched draft: hidden_dim too large");
+    const size_t smem = (size_t)8 * fin_pitch(A.d / 8) * 4 + (size_t)A.fin_stage * (2 * A.d + 16);
     if (int st = configure(kern, smem)) return st;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(rows);
@@ -1740,6 +1960,8 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
     A.argmax = argmax ? 1 : 0;
     A.id_offset = id_offset;
     if (argmax) A.k = 1;
+    static const int ablate = std::getenv("FRS_ABLATE") ? std::atoi(std::getenv("FRS_ABLATE")) : 0;
+    A.ablate = ablate == 11 ? ablate : 0;
     return launch_select(ctx, A, n, s);
 }
 
@@ -1747,8 +1969,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
                 int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx, int32_t *out_full,
                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
     if (d % 8 != 0) return fail(FRS_ENOTSUP, "FAST head: hidden_dim must be a multiple of 8 (TMA row pitch)");
-    const int TPs = fin_pitch(d / 8);
-    const bool batched_ok = (size_t)(8 + kCandPerFinCta * 8) * TPs * 4 <= ctx->smem_optin;
+    const bool batched_ok = sel_stage(ctx, d) >= 4;
     if (!argmax && n > 16 && batched_ok) {  // batched drafting: up to 64 rows per slab pass
         for (int r0 = 0; r0 < n; r0 += 64) {
             const int nr = std::min(64, n - r0);
@@ -1946,7 +2167,7 @@ int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float 
     FRS_CUDA_TRY(cudaMemcpy(pkey, w.P.pkey, sizeof(unsigned long long) * n * L * R, cudaMemcpyDeviceToHost));
     FRS_CUDA_TRY(cudaMemcpy(pw2, w.P.pw2, sizeof(float) * 2 * G, cudaMemcpyDeviceToHost));
     if (w.P.trace) {  // trailing [G][kTrMain] main stamps, [64][kFinCtas][16] finalize stamps, [8] extra
-        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * L * R, w.P.trace, (size_t)(G * kTrMain + 64 * kFinCtas * 16 + 8) * 8,
+        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * L * R, w.P.trace, (size_t)(G * kTrMain + 64 * kFinCtas * 16 + 16) * 8,
                                 cudaMemcpyDeviceToHost));
     }
     return FRS_OK;

@@ -24,6 +24,8 @@ SLOTS = {28: "main entry", 0: "setup done", 1: "producer: before griddep_wait", 
          17: "epi w4: after bar1", 18: "epi w4: rows done", 19: "cta: final sync", 7: "cta end",
          20: "loop done w0", 21: "loop done w1", 22: "loop done w2", 23: "loop done w3", 24: "loop done w4",
          25: "loop done w5", 26: "loop done w6", 27: "loop done w7"}
+SSLOTS = {0: "sel start", 2: "sel after griddep_wait", 3: "sel pass1 (max)", 4: "sel pass2 (sum, survivors)",
+          6: "sel S chosen", 12: "sel first gather", 5: "sel recompute done", 7: "sel certified+written"}
 FSLOTS = {0: "fin start", 1: "fin h loaded", 2: "fin after griddep_wait", 3: "fin partials merged",
           4: "fin S selected", 5: "fin recompute done", 6: "fin last: certified?", 7: "fin last: written",
           6: "fin keys+M+eps ready", 11: "fin histogram issued", 10: "fin leader: after cluster wait",
@@ -53,7 +55,7 @@ def main():
         n = a.rows
         L = 4 * G
         pm, ps, pth = (np.empty(n * L, np.float32) for _ in range(3))
-        pkey = np.empty(n * L * 3 + G * 32 + 64 * 8 * 16 + 8, np.uint64)
+        pkey = np.empty(n * L * 3 + G * 32 + 64 * 8 * 16 + 16, np.uint64)
         pw2 = np.empty(2 * G, np.float32)
         _lib.check(_lib.lib().frs_debug_fast_partials(ctx.handle, n, a.d, pm.ctypes.data, ps.ctypes.data,
                                                       pth.ctypes.data, pkey.ctypes.data, pw2.ctypes.data))
@@ -69,16 +71,24 @@ def main():
                 us = (v - t0) / 1000.0
                 row[f"{s:02d} {name}"] = [round(float(us.min()), 2), round(float(np.median(us)), 2),
                                           round(float(us.max()), 2)]
-        for s, name in FSLOTS.items():
+        for s, name in (SSLOTS if n > 16 else FSLOTS).items():
             v = ft[:, s]
             v = v[v > 0]
             if v.size:
                 us = (v - t0) / 1000.0
                 row[f"F{s} {name}"] = [round(float(us.min()), 2), round(float(np.median(us)), 2),
                                        round(float(us.max()), 2)]
-        for s_, name in {0: "hsplit start", 1: "hsplit cta0 end", 2: "fallback start", 3: "fallback exit"}.items():
+        for s_, name in {0: "hsplit start", 1: "hsplit cta0 end", 2: "fallback start", 3: "fallback exit (empty)",
+                        4: "fallback dots done (last CTA)", 5: "fallback end", 8: "fb row0: max pass",
+                        9: "fb row0: exp+sum pass", 10: "fb row0: total (seq?)", 11: "fb row0: key lists",
+                        12: "fb row0: top-k done"}.items():
             if xt[s_] > 0:
                 row[f"X{s_} {name}"] = round(float((xt[s_] - t0) / 1000.0), 2)
+        if n > 16:  # batched path: k_fast_select stamps (row i at [i*8]); slot 8 = |S| | robust << 32
+            sel8 = ft[::8, 8][:n]
+            row["select |S| (min/med/max)"] = [int((sel8 & 0xffffffff).min()), int(np.median(sel8 & 0xffffffff)),
+                                               int((sel8 & 0xffffffff).max())]
+            row["select robust rows"] = int(((sel8 >> 32) & 1).sum())
         # clock64 vs globaltimer over the exact-recompute phase (slots 12 -> 5; cycles in 13/14)
         sel = (ft[:, 12] > 0) & (ft[:, 5] > ft[:, 12])
         if sel.any():
