@@ -34,6 +34,35 @@ __device__ __forceinline__ float expf_glibc(float x, const unsigned long long *t
     return __double2float_rn(y);
 }
 
+// expf_glibc without the special-case branch (bit-identical for every input): the main path
+// runs on x clamped into [-104, 89] (glibc's main path is valid on all of [-103.97, 88.72])
+// and the special cases are selected afterwards, so several calls interleave freely.
+__device__ __forceinline__ float expf_glibc_nb(float x, const unsigned long long *tab) {
+    const uint32_t ux = __float_as_uint(x);
+    const uint32_t abstop = (ux >> 20) & 0x7ffu;
+    const float xc = fminf(fmaxf(x, -104.0f), 89.0f);
+    const double xd = static_cast<double>(xc);
+    double kd = __fma_rn(0x1.71547652b82fep+5, xd, 0x1.8p+52);
+    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
+    kd = __dsub_rn(kd, 0x1.8p+52);
+    const double r = __fma_rn(0x1.71547652b82fep+5, xd, -kd);
+    const unsigned long long tt = tab[ki & 31ull] + (ki << 47);
+    const double s = __longlong_as_double(static_cast<long long>(tt));
+    const double z = __fma_rn(0x1.c6af84b912394p-20, r, 0x1.ebfce50fac4f3p-13);
+    const double r2 = __dmul_rn(r, r);
+    double y = __fma_rn(0x1.62e42ff0c52d6p-6, r, 1.0);
+    y = __fma_rn(z, r2, y);
+    y = __dmul_rn(y, s);
+    float res = __double2float_rn(y);
+    if (abstop >= 0x42bu) {  // selects, not a branch around the main path
+        res = x < -0x1.9fe368p6f ? 0.0f : res;
+        res = x > 0x1.62e42ep6f ? __int_as_float(0x7f800000) : res;
+        res = abstop >= 0x7f8u ? x + x : res;
+        res = ux == 0xff800000u ? 0.0f : res;
+    }
+    return res;
+}
+
 static __device__ const unsigned long long kExp2fTable[32] = {
         0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
         0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,

@@ -633,6 +633,14 @@ struct FinArgs {
             (A).P.trace[(size_t)(A).P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + (slot)] = gtimer(); \
     } while (0)
 
+// DIAGNOSTIC: clock64 probes of select_certify (FRS_TRACE): [64 rows][16] cycles since entry
+#define FRS_CPROBE(A, q)                                                                                 \
+    do {                                                                                                  \
+        if ((A).P.trace && (threadIdx.x & 31) == 0)                                                       \
+            (A).P.trace[(size_t)(A).P.G * kTrMain + 64 * kFinCtas * 16 + 16 + (size_t)i * 16 + (q)] =    \
+                static_cast<unsigned long long>(clock64() - c_entry_);                                    \
+    } while (0)
+
 // Row pitch (floats) of the transposed per-lane-chain operand tiles of the exact recompute: a
 // multiple of 4 (16-byte vector loads) with pitch % 8 == 4, so the 8 lanes of a quarter-warp
 // hit 8 distinct 4-bank groups (a 2-way conflict at pitch % 8 == 0 doubled the loop time).
@@ -666,12 +674,13 @@ __device__ __forceinline__ float hist_edge(int j) {
 // gone). fin[0..ns) are the exact logits of the candidate set S (keys sel[], canonical order),
 // nsel the untruncated |S|; a_bound bounds every approximate logit outside S, eps the FAST
 // error. Writes the row's outputs, or queues it for k_fast_fallback with the reason.
-__device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int nsel, int kk, float a_bound, float eps,
+__device__ __forceinline__ void select_certify(const FinArgs &A, int i, int ns, int nsel, int kk, float a_bound, float eps,
                                             bool any_bad, double tot_approx, float mmax_approx, const float *s_fin,
                                             const unsigned long long *s_sel, unsigned long long *s_sorted,
                                             unsigned long long *s_tab, int32_t *s_spos, const int32_t *s_ord) {
     const int lane = threadIdx.x & 31;
     const float kNegInf = -__int_as_float(0x7f800000);
+    const long long c_entry_ = clock64();
     const double s_tot = tot_approx;
     const float s_mmax = mmax_approx;
     uint32_t why = (nsel > kCsMax || ns < kk) ? FRS_FLAG_CERT_OVERFLOW : 0u;
@@ -712,39 +721,62 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
     }
     const unsigned long long *tab = s_tab;  // glibc exp table, staged by the caller's prologue
     const bool unit_t = A.temperature == 1.0f;  // x = l / 1 is exact: skip the IEEE divisions
+    const int nq = (ns + 31) >> 5;              // warp-uniform: candidate slots in use per lane
     float xq[CPL], xm = kNegInf;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
-        xq[q] = unit_t ? lq[q] : __fdiv_rn(lq[q], A.temperature);
+        xq[q] = (q >= nq || unit_t) ? lq[q] : __fdiv_rn(lq[q], A.temperature);
         xm = fmaxf(xm, xq[q]);
     }
     const float mx = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(xm)));
+    FRS_CPROBE(A, 0);
+    // Three independent latency chains, issued together: the e-keys (branch-free glibc expf),
+    // the bound on every non-recomputed row's e, and the denominator 1 / total.
+    const bool bnd_live = a_bound != kNegInf;
+    const float x_ub = (unit_t ? __fadd_ru(a_bound, eps) : __fdiv_ru(a_bound + eps, A.temperature)) *
+                           (1.0f + 0x1p-20f) + 0x1p-20f;
+    const float e_ub = dev::expf_glibc_nb(fminf(x_ub - mx, 0.0f), tab) * (1.0f + 0x1p-20f);
+    // tot = sum exp(x_j - M) over the approximate logits; rescale to the exact max
+    const double total = s_tot * static_cast<double>(exp2f((s_mmax - mx) * 1.4426950408889634f));
+    const float inv = __double2float_rn(1.0 / total);
     unsigned long long eq[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
-        eq[q] = hq[q] ? dev::prob_key(dev::expf_glibc(__fsub_rn(xq[q], mx), tab), jq[q]) : 0ull;
-        if (hq[q]) s_sorted[lane + 32 * q] = eq[q];
+        if (q < nq) {
+            const float e = dev::expf_glibc_nb(__fsub_rn(xq[q], mx), tab);
+            eq[q] = hq[q] ? dev::prob_key(e, jq[q]) : 0ull;
+            if (hq[q]) s_sorted[lane + 32 * q] = eq[q];
+        } else {
+            eq[q] = 0ull;
+        }
     }
+    FRS_CPROBE(A, 1);
     // rank of each e-key among the ns (distinct: the index is part of the key): independent
     // broadcast loads from shared memory (no shuffle chain)
     __syncwarp();
     int rq[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) rq[q] = 0;
+    if (nq == 1) {
+#pragma unroll 8
+        for (int c = 0; c < ns; ++c) rq[0] += s_sorted[c] > eq[0];
+    } else {
 #pragma unroll 4
-    for (int c = 0; c < ns; ++c) {
-        const unsigned long long o = s_sorted[c];
+        for (int c = 0; c < ns; ++c) {
+            const unsigned long long o = s_sorted[c];
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) rq[q] += o > eq[q];
+            for (int q = 0; q < CPL; ++q) rq[q] += o > eq[q];
+        }
     }
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < CPL; ++q)
-        if (hq[q]) {
+        if (q < nq && hq[q]) {
             s_sorted[rq[q]] = eq[q];
             s_spos[rq[q]] = lane + 32 * q;
         }
     __syncwarp();
+    FRS_CPROBE(A, 2);
     const int want = min(ns, kk + 1);
     // near ties (within 4 ulps) among the selected and at the k boundary: the probabilities
     // e * (1 / total) of such a pair may round to one value under the exact denominator, and
@@ -763,12 +795,11 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
         }
     }
     if (__any_sync(0xffffffffu, tie) || A.ablate == 11) why |= FRS_FLAG_CERT_TIE;  // 11: DIAGNOSTIC
-    if (!why && a_bound != kNegInf) {  // every non-recomputed row stays strictly below the k-th
-        const float x_ub = __fdiv_ru(a_bound + eps, A.temperature) * (1.0f + 0x1p-20f) + 0x1p-20f;
+    FRS_CPROBE(A, 3);
+    if (!why && bnd_live) {  // every non-recomputed row stays strictly below the k-th
         if (!(x_ub < mx)) {
             why |= FRS_FLAG_CERT_BOUND;
         } else {
-            const float e_ub = dev::expf_glibc(x_ub - mx, tab) * (1.0f + 0x1p-20f);
             const float e_k = __uint_as_float(static_cast<uint32_t>(s_sorted[kk - 1] >> 32));
             if (!(e_ub * (1.0f + 0x1p-21f) < e_k)) why |= FRS_FLAG_CERT_BOUND;
         }
@@ -777,9 +808,7 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
         if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
         return;
     }
-    // tot = sum exp(x_j - M) over the approximate logits; rescale to the exact max
-    const double total = s_tot * static_cast<double>(exp2f((s_mmax - mx) * 1.4426950408889634f));
-    const float inv = __double2float_rn(1.0 / total);
+    FRS_CPROBE(A, 4);
     if (lane < A.k) {
         const size_t o = (size_t)i * A.k + lane;
         if (lane < kk) {
@@ -816,6 +845,7 @@ __device__ __noinline__ void select_certify(const FinArgs &A, int i, int ns, int
         if (A.out_total) A.out_total[i] = total;
         if (A.out_flags) A.out_flags[i] = static_cast<uint32_t>(min(ns, 255)) << 8;  // |S| (info)
     }
+    FRS_CPROBE(A, 6);
     FRS_FTRACE(A, 7);
 }
 
@@ -1221,6 +1251,19 @@ __device__ __forceinline__ float hist_threshold(const unsigned *s_hist, int kk, 
                                      (fabsf(M) * 0x1p-18f + 0x1p-20f);
 }
 
+// Appends for the lanes with pred set (all 32 lanes must call): one shared atomic per warp
+// (per-lane atomics on one counter serialise when hundreds of keys survive). Returns the
+// lane's slot, or -1.
+__device__ __forceinline__ int warp_append(bool pred, int *counter) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (!m) return -1;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(counter, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return pred ? base + __popc(m & ((1u << lane) - 1u)) : -1;
+}
+
 __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
     extern __shared__ __align__(16) uint8_t ssm_raw[];
     const int T = A.d >> 3, TP = fin_pitch(T);
@@ -1358,15 +1401,13 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
             const int j = 4 * (base + tid + u * kSelThreads);
             const float e[4] = {b4[u].x, b4[u].y, b4[u].z, b4[u].w};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                if (j + c >= v) continue;
-                if (!A.argmax) part += exp2f((e[c] * inv_t - Mx) * 1.4426950408889634f);
-                if (e[c] >= t0) {
-                    const int pos = atomicAdd(&s_nsurv, 1);
-                    if (pos < kSelSurv) s_surv[pos] = dev::value_key(e[c], j + c);
-                } else {
-                    a_far = fmaxf(a_far, e[c]);
-                }
+            for (int c = 0; c < 4; ++c) {  // warp-uniform: survivors append warp-aggregated
+                const bool in = j + c < v;
+                if (in && !A.argmax) part += exp2f((e[c] * inv_t - Mx) * 1.4426950408889634f);
+                const bool sv = in && e[c] >= t0;
+                const int pos = warp_append(sv, &s_nsurv);
+                if (sv && pos < kSelSurv) s_surv[pos] = dev::value_key(e[c], j + c);
+                if (in && !sv) a_far = fmaxf(a_far, e[c]);
             }
         }
         tot += static_cast<double>(part);
@@ -1500,26 +1541,53 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
         }
         if (tid < ((nc * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
             mbar_wait(&s_bar, round & 1);
-            if (c0 == 0) FRS_FTRACE(A, 12);
+            if (round == 0) FRS_FTRACE(A, 12);
+            if (round == 1) FRS_FTRACE(A, 11);
             const int g = tid >> 3, cl = g < nc ? g : 0, l = tid & 7;
             const float *hp = ht + l * TP;
             const unsigned short *wp = wrows + (size_t)cl * wpitch + l;
             float s = 0.0f;
             int t = 0;
-            for (; t + 4 <= T; t += 4) {
-                const float4 hv = *reinterpret_cast<const float4 *>(hp + t);
-                const float h4[4] = {hv.x, hv.y, hv.z, hv.w};
+            // 16 steps per half-iteration over ping-pong operand buffers, each half's loads
+            // issued before the other half's add chain (4 warps alone on the SM: nothing else
+            // hides the shared-memory latency); bf16 words land in 32-bit registers
+            constexpr int ST = 16;
+            const int TS = T - T % ST;
+            float ha[ST], hb[ST];
+            uint32_t wa[ST], wb[ST];
+            auto load = [&](float(&hv)[ST], uint32_t(&wv)[ST], int t0) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float w = __uint_as_float(static_cast<uint32_t>(wp[8 * (t + q)]) << 16);  // exact
-                    s = __fadd_rn(s, __fmul_rn(h4[q], w));
+                for (int q = 0; q < ST; q += 4) {
+                    const float4 x = *reinterpret_cast<const float4 *>(hp + t0 + q);
+                    hv[q] = x.x, hv[q + 1] = x.y, hv[q + 2] = x.z, hv[q + 3] = x.w;
                 }
+#pragma unroll
+                for (int q = 0; q < ST; ++q) wv[q] = wp[8 * (t0 + q)];
+            };
+            auto chain = [&](const float(&hv)[ST], const uint32_t(&wv)[ST]) {
+#pragma unroll
+                for (int q = 0; q < ST; ++q) s = __fadd_rn(s, __fmul_rn(hv[q], __uint_as_float(wv[q] << 16)));  // exact
+            };
+            const long long c_begin = clock64();
+            if (TS > 0) load(ha, wa, 0);
+            for (; t < TS; t += 2 * ST) {
+                const bool second = t + ST < TS;
+                if (second) load(hb, wb, t + ST);
+                chain(ha, wa);
+                if (t + 2 * ST < TS) load(ha, wa, t + 2 * ST);
+                if (second) chain(hb, wb);
             }
+            t = TS;
+            if (A.P.trace && tid == 0 && round == 0)  // DIAGNOSTIC: dot cycles (trace row i*8+1)
+                A.P.trace[(size_t)A.P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + 1) * 16 + 15] =
+                    static_cast<unsigned long long>(clock64() - c_begin);
             for (; t < T; ++t) s = __fadd_rn(s, __fmul_rn(hp[t], __uint_as_float(static_cast<uint32_t>(wp[8 * t]) << 16)));
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));  // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7))
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
             s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
             if (l == 0 && g < nc) s_fin[c0 + cl] = s;
+            if (round == 0) FRS_FTRACE(A, 10);
+            if (round == 1) FRS_FTRACE(A, 1);
         }
         __syncthreads();
     }
@@ -1722,7 +1790,7 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.P.w2_bits = nullptr;
     static const bool tracing = std::getenv("FRS_TRACE") != nullptr;
     if (tracing) {
-        if ((st = ctx->trace.ensure((size_t)(G * kTrMain + 64 * kFinCtas * 16 + 16) * 8))) return st;
+        if ((st = ctx->trace.ensure((size_t)(G * kTrMain + 64 * kFinCtas * 16 + 16 + 64 * 16) * 8))) return st;
         w.P.trace = static_cast<unsigned long long *>(ctx->trace.ptr);
     }
     if (!ctx->fast_ctr.ptr) {  // zeroed once: counters are monotonic or reset in-stream
@@ -1831,6 +1899,7 @@ int launch_select(frs_ctx *ctx, const FinArgs &A0, int rows, cudaStream_t s) {
 }
 
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
+    if (A.ablate == 13) return FRS_OK;  // DIAGNOSTIC: main kernel only (outputs not written)
     auto kern = k_fast_finalize;
     const int TP = fin_pitch(A.d / 8);
     const size_t smem = (size_t)8 * TP * 4 + (size_t)A.fin_stage * 8 * TP * 4 + 64;
@@ -2167,7 +2236,7 @@ int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float 
     FRS_CUDA_TRY(cudaMemcpy(pkey, w.P.pkey, sizeof(unsigned long long) * n * L * R, cudaMemcpyDeviceToHost));
     FRS_CUDA_TRY(cudaMemcpy(pw2, w.P.pw2, sizeof(float) * 2 * G, cudaMemcpyDeviceToHost));
     if (w.P.trace) {  // trailing [G][kTrMain] main stamps, [64][kFinCtas][16] finalize stamps, [8] extra
-        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * L * R, w.P.trace, (size_t)(G * kTrMain + 64 * kFinCtas * 16 + 16) * 8,
+        FRS_CUDA_TRY(cudaMemcpy(pkey + (size_t)n * L * R, w.P.trace, (size_t)(G * kTrMain + 64 * kFinCtas * 16 + 16 + 64 * 16) * 8,
                                 cudaMemcpyDeviceToHost));
     }
     return FRS_OK;

@@ -25,11 +25,14 @@ SLOTS = {28: "main entry", 0: "setup done", 1: "producer: before griddep_wait", 
          20: "loop done w0", 21: "loop done w1", 22: "loop done w2", 23: "loop done w3", 24: "loop done w4",
          25: "loop done w5", 26: "loop done w6", 27: "loop done w7"}
 SSLOTS = {0: "sel start", 2: "sel after griddep_wait", 3: "sel pass1 (max)", 4: "sel pass2 (sum, survivors)",
-          6: "sel S chosen", 12: "sel first gather", 5: "sel recompute done", 7: "sel certified+written"}
+          6: "sel S chosen", 12: "sel round 0 gathered", 10: "sel round 0 dot done (tid 0)",
+          11: "sel round 1 gathered", 1: "sel round 1 dot done", 5: "sel recompute done", 13: "certify: entry",
+          14: "certify: e-keys", 15: "certify: sorted", 9: "certify: checks passed", 7: "sel certified+written"}
 FSLOTS = {0: "fin start", 1: "fin h loaded", 2: "fin after griddep_wait", 3: "fin partials merged",
           4: "fin S selected", 5: "fin recompute done", 6: "fin last: certified?", 7: "fin last: written",
           6: "fin keys+M+eps ready", 11: "fin histogram issued", 10: "fin leader: after cluster wait",
-          12: "fin cand rows staged"}
+          12: "fin cand rows staged", 13: "certify: entry", 14: "certify: e-keys", 15: "certify: sorted",
+          9: "certify: checks passed"}
 
 
 def main():
@@ -55,15 +58,22 @@ def main():
         n = a.rows
         L = 4 * G
         pm, ps, pth = (np.empty(n * L, np.float32) for _ in range(3))
-        pkey = np.empty(n * L * 3 + G * 32 + 64 * 8 * 16 + 16, np.uint64)
+        pkey = np.empty(n * L * 3 + G * 32 + 64 * 8 * 16 + 16 + 64 * 16, np.uint64)
         pw2 = np.empty(2 * G, np.float32)
         _lib.check(_lib.lib().frs_debug_fast_partials(ctx.handle, n, a.d, pm.ctypes.data, ps.ctypes.data,
                                                       pth.ctypes.data, pkey.ctypes.data, pw2.ctypes.data))
         st = pkey[n * L * 3:n * L * 3 + G * 32].reshape(G, 32).astype(np.int64)
         ft = pkey[n * L * 3 + G * 32:n * L * 3 + G * 32 + 64 * 8 * 16].reshape(64 * 8, 16).astype(np.int64)[: n * 8]
-        xt = pkey[n * L * 3 + G * 32 + 64 * 8 * 16:].astype(np.int64)
+        xt = pkey[n * L * 3 + G * 32 + 64 * 8 * 16:n * L * 3 + G * 32 + 64 * 8 * 16 + 16].astype(np.int64)
+
         t0 = st[:, 0][st[:, 0] > 0].min()  # earliest "setup done" of the main kernel
         row = {}
+        cp = pkey[n * L * 3 + G * 32 + 64 * 8 * 16 + 16:].reshape(64, 16).astype(np.int64)[:n]
+        for q, name in enumerate(["mx (redux)", "e-keys", "sorted", "tie", "bound", "inv", "written"]):
+            v = cp[:, q]
+            v = v[v > 0]
+            if v.size:
+                row[f"C{q} certify cycles: {name}"] = [int(v.min()), int(np.median(v)), int(v.max())]
         for s, name in SLOTS.items():
             v = st[:, s]
             v = v[v > 0]
@@ -72,7 +82,7 @@ def main():
                 row[f"{s:02d} {name}"] = [round(float(us.min()), 2), round(float(np.median(us)), 2),
                                           round(float(us.max()), 2)]
         for s, name in (SSLOTS if n > 16 else FSLOTS).items():
-            v = ft[:, s]
+            v = ft[::8, s] if n > 16 else ft[:, s]
             v = v[v > 0]
             if v.size:
                 us = (v - t0) / 1000.0
@@ -89,6 +99,8 @@ def main():
             row["select |S| (min/med/max)"] = [int((sel8 & 0xffffffff).min()), int(np.median(sel8 & 0xffffffff)),
                                                int((sel8 & 0xffffffff).max())]
             row["select robust rows"] = int(((sel8 >> 32) & 1).sum())
+            dc = ft[1::8, 15][:n]
+            row["select round-0 dot cycles (min/med/max)"] = [int(dc.min()), int(np.median(dc)), int(dc.max())]
         # clock64 vs globaltimer over the exact-recompute phase (slots 12 -> 5; cycles in 13/14)
         sel = (ft[:, 12] > 0) & (ft[:, 5] > ft[:, 12])
         if sel.any():
