@@ -106,6 +106,9 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {  // bytes % 16 == 0
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -168,6 +171,7 @@ struct Partials {
     unsigned *w2_bits;         // [1] max |W_j|^2 (float bits); both reset by k_hsplit, atomicMax here
     float *logits;             // LOGITS mode: approximate logits [n][ld_logits] (batched drafting)
     int late_trigger;          // DIAGNOSTIC (FRS_ABLATE=8): launch_dependents at the end, not the start
+    int ablate_main;           // DIAGNOSTIC (FRS_ABLATE=14/15): skip the publish / the epilogue math
     int ld_logits;
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
@@ -183,7 +187,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if ((P).trace) (P).trace[(size_t)blockIdx.x * kTrMain + (slot)] = gtimer();   \
     } while (0)
 
-// hs rows [0,NP) = bf16(h), rows [NP,2NP) = bf16(h - bf16(h)); padded rows are zero.
+// hs rows [0,NP) = bf16(h), rows [NP,2NP) = bf16(h - bf16(h)); padded rows are zero. Hidden
+// rows are interleaved over the two column halves (hs row p = hidden row 2 (p % (NP/2)) +
+// p / (NP/2)), so the two epilogue warps of a TMEM lane quarter share the valid rows evenly.
 // 128 threads, no shared memory: it co-resides with the main kernel's CTAs, which PDL lets
 // launch (and run their prologue and first slab loads) while this grid is still running.
 __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int n, int d, int NP,
@@ -200,15 +206,16 @@ __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int
     if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[0] = gtimer();
     const int total4 = NP * d / 4;  // d % 8 == 0 on the FAST path
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total4; idx += gridDim.x * blockDim.x) {
-        const int e = idx * 4, i = e / d, c = e - i * d;
+        const int e = idx * 4, p = e / d, c = e - p * d;
+        const int i = 2 * (p % (NP / 2)) + p / (NP / 2);  // hs row p holds hidden row i (see k_fast_main)
         const float4 x = i < n ? __ldg(reinterpret_cast<const float4 *>(h + (size_t)i * d + c))
                                : make_float4(0.f, 0.f, 0.f, 0.f);
         const __nv_bfloat162 h01 = __floats2bfloat162_rn(x.x, x.y), h23 = __floats2bfloat162_rn(x.z, x.w);
         const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
         const __nv_bfloat162 l01 = __floats2bfloat162_rn(x.x - f01.x, x.y - f01.y);
         const __nv_bfloat162 l23 = __floats2bfloat162_rn(x.z - f23.x, x.w - f23.y);
-        __nv_bfloat162 *hi = reinterpret_cast<__nv_bfloat162 *>(hs + (size_t)i * d + c);
-        __nv_bfloat162 *lo = reinterpret_cast<__nv_bfloat162 *>(hs + (size_t)(NP + i) * d + c);
+        __nv_bfloat162 *hi = reinterpret_cast<__nv_bfloat162 *>(hs + (size_t)p * d + c);
+        __nv_bfloat162 *lo = reinterpret_cast<__nv_bfloat162 *>(hs + (size_t)(NP + p) * d + c);
         hi[0] = h01;
         hi[1] = h23;
         lo[0] = l01;
@@ -231,6 +238,11 @@ struct MainCfg {
     static constexpr int TMEM_COLS = (2 * N) < 32 ? 32 : 2 * N;
     static_assert(!SOFTMAX || NP == 16, "the fused softmax path handles up to 16 hidden rows per call");
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 4 * NP * 8 + 256;
+    // publish scratch per epilogue warp, carved from the A stages once the MMAs are done
+    static constexpr int SCRATCH_PER_WARP = (STAGES * A_BYTES) / EPI_WARPS;
+    static constexpr int PUB_KSTRIDE = 8 * TOPK + 1, PUB_FSTRIDE = 8 + 1;  // 8 rows per pass, odd strides
+    static_assert(32 * PUB_KSTRIDE * 8 + 32 * PUB_FSTRIDE * 4 * (SOFTMAX ? 3 : 1) <= SCRATCH_PER_WARP,
+                  "publish scratch");
 };
 
 #define FRS_TMEM_LD16(taddr, r)                                                                                 \
@@ -247,6 +259,23 @@ struct MainCfg {
 
 // Warp max of a (value, index) key with 2 REDUX instead of 10 shuffles: max over the ordered
 // value bits, then max over ~index among the lanes holding that value.
+// a := top 4 of (a, b), both sorted descending: bitonic half-cleaner, then sort the bitonic 4
+__device__ __forceinline__ void top4_merge(unsigned long long (&a)[4], const unsigned long long (&b)[4]) {
+    unsigned long long c0 = a[0] > b[3] ? a[0] : b[3], c1 = a[1] > b[2] ? a[1] : b[2];
+    unsigned long long c2 = a[2] > b[1] ? a[2] : b[1], c3 = a[3] > b[0] ? a[3] : b[0];
+    auto ce = [](unsigned long long &x, unsigned long long &y) {
+        const bool sw = y > x;
+        const unsigned long long t = sw ? y : x;
+        y = sw ? x : y;
+        x = t;
+    };
+    ce(c0, c2);
+    ce(c1, c3);
+    ce(c0, c1);
+    ce(c2, c3);
+    a[0] = c0, a[1] = c1, a[2] = c2, a[3] = c3;
+}
+
 __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k) {
     const unsigned hi = static_cast<unsigned>(k >> 32);
     const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
@@ -286,6 +315,11 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     auto tile_row0 = [&](int t) { return (c_begin + t * CPT) * CH; };
     auto tile_rows = [&](int t) { return min(v_rows - tile_row0(t), tile_chunks(t) * CH); };
 
+    // per-CTA maxima, combined in shared memory: ONE global atomic per (CTA, row) and per CTA
+    // for |W|^2 (hundreds of same-address atomics per row at the tail cost ~3 us per call)
+    __shared__ unsigned s_rmax[64], s_w2max;
+    if (threadIdx.x < 64) s_rmax[threadIdx.x] = 0u;
+    if (threadIdx.x == 64) s_w2max = 0u;
     if (threadIdx.x == 0) {
         FRS_TRACE(P, 28);
         for (int s = 0; s < STAGES; ++s) {
@@ -420,13 +454,16 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         if (lane == 0) {
             P.pw2[cta * 2 + (warp - 2)] = wmax;
-            atomicMax(P.w2_bits, __float_as_uint(wmax));  // non-negative: raw bits order
+            atomicMax(&s_w2max, __float_as_uint(wmax));  // non-negative: raw bits order
         }
         if (threadIdx.x == 64) FRS_TRACE(P, 8);
+        if constexpr (!LOGITS) asm volatile("bar.arrive 1, %0;" ::"r"((2 + EPI) * 32) : "memory");  // sA reads done
     } else {  // ---------------- epilogue warps: TMEM -> (softmax stats, per-thread candidates)
         const int we = warp - 4;         // 0 .. EPI-1
         const int q = warp & 3;          // TMEM lane quarter this warp may access
-        const int cbase = (we / 4) * RPW;  // first hidden row handled by this warp
+        const int half = we >> 2;          // column half: TMEM columns [half RPW, (half + 1) RPW)
+        const int cbase = half * RPW;      // = hidden rows 2 r + half, r < RPW (k_hsplit's order)
+        const int nv = max(0, min(RPW, (n - half + 1) >> 1));  // valid hidden rows of this warp
         constexpr int NS = SOFTMAX ? RPW : 1;
         const float kNegInf = __int_as_float(0xff800000u);
         float m[NS], s[NS];
@@ -470,10 +507,11 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
+                if (!LOGITS && P.ablate_main == 15) continue;
                 if constexpr (LOGITS) {  // coalesced: the warp's 32 lanes are 32 consecutive slab rows
 #pragma unroll
                     for (int r = 0; r < CG; ++r) {
-                        const int i = c0 + r;
+                        const int i = 2 * (cg * CG + r) + half;
                         if (valid && i < n)
                             P.logits[(size_t)i * P.ld_logits + row] = __uint_as_float(hi[r]) + __uint_as_float(lo[r]);
                     }
@@ -481,7 +519,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                 }
 #pragma unroll
                 for (int r = 0; r < CG; ++r) {
-                    const int rr = cg * CG + r, i = c0 + r;
+                    const int rr = cg * CG + r, i = 2 * rr + half;
                     if (!valid || i >= n) continue;
                     const float a = __uint_as_float(hi[r]) + __uint_as_float(lo[r]);
                     if constexpr (SOFTMAX) {  // online sum exp(x - m), one MUFU per value
@@ -523,65 +561,123 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         //      slab rows and their top-R keys + a bound for the rest. Warp-local only: the
         //      max by one REDUX on order-preserving bits, the list by R + 1 tournament rounds
         //      over the lanes' sorted (b1, b2) heads.
+        const long long c_pub0 = clock64();
         if constexpr (LOGITS) {
             (void)b1;
             (void)bnd;
+        } else if (P.ablate_main >= 14) {
+            asm volatile("bar.sync 1, %0;" ::"r"((2 + EPI) * 32) : "memory");
         } else {
         const int list = cta * kListsPerCta + q, L = G * kListsPerCta;
-        // rows outer-unrolled inside every step, so the RPW independent REDUX chains overlap
-        if constexpr (SOFTMAX) {
-            float M[RPW], e[RPW];
+        // Lanes' states go through shared memory (the A stages: every MMA has completed and
+        // the norm warps have signalled barrier 1), then 4 lanes per hidden row merge 8 lanes'
+        // entries each and combine over 2 shuffle rounds. (Warp-wide REDUX/shuffle trees per
+        // row took ~3 us at the tail of every call.)
+        asm volatile("bar.sync 1, %0;" ::"r"((2 + EPI) * 32) : "memory");
+        if (P.trace && threadIdx.x == 128) P.trace[(size_t)blockIdx.x * kTrMain + 6] = static_cast<unsigned long long>(clock64() - c_pub0);
+        constexpr int SLOT = C::SCRATCH_PER_WARP;
+        uint8_t *scr = sA + we * SLOT;
+        // per pass of 8 rows, lane-major with odd strides: the 8 rows a reader instruction
+        // touches sit in distinct banks (row-major [row][lane] made every merge load 8-way
+        // bank-conflicted)
+        constexpr int KS = C::PUB_KSTRIDE, FS = C::PUB_FSTRIDE;
+        unsigned long long *sk = reinterpret_cast<unsigned long long *>(scr);  // [32][KS]: row k's keys at k TOPK
+        float *sbn = reinterpret_cast<float *>(scr + 32 * KS * 8);            // [32][FS]
+        float *smm = sbn + 32 * FS, *sss = smm + 32 * FS;                     // [32][FS] (SOFTMAX)
+        const int g = lane >> 2, u = lane & 3;
+        static_assert(R + 1 == 4, "the merge network keeps the top 4 keys");
 #pragma unroll
-            for (int r = 0; r < RPW; ++r) M[r] = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(m[r])));
+        for (int r0 = 0; r0 < RPW; r0 += 8) {  // warp-uniform passes of 8 rows
+            if (r0 >= nv) break;
+            if (r0 > 0) __syncwarp();  // the previous pass's reads are done
 #pragma unroll
-            for (int r = 0; r < RPW; ++r) e[r] = m[r] == kNegInf ? 0.0f : s[r] * exp2f((m[r] - M[r]) * 1.4426950408889634f);
+            for (int k = 0; k < 8; ++k) {
+                if (r0 + k >= RPW || r0 + k >= nv) continue;
+                sk[lane * KS + k * TOPK] = b1[r0 + k];
+                if constexpr (TOPK == 2) sk[lane * KS + k * TOPK + 1] = b2[r0 + k];
+                sbn[lane * FS + k] = bnd[r0 + k];
+                if constexpr (SOFTMAX) {
+                    smm[lane * FS + k] = m[r0 + k];
+                    sss[lane * FS + k] = s[r0 + k];
+                }
+            }
+            __syncwarp();
+            const int r = r0 + g;
+            const bool live = r < nv;
+            unsigned long long top[4] = {0ull, 0ull, 0ull, 0ull};
+            float bmx = kNegInf, mu = kNegInf, eu = 0.0f;
+            if (live) {
+                // lanes 8u .. 8u+7: their sorted (b1, b2) pairs -> four sorted 4-lists -> top 4
+                // by a bitonic merge tree (short dependent chains, unlike sequential insertion)
+                unsigned long long q4[4][4];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
+                for (int pq = 0; pq < 4; ++pq) {
+                    const int la = 8 * u + 2 * pq, lb = la + 1;
+                    const unsigned long long x0 = sk[la * KS + g * TOPK];
+                    const unsigned long long x1 = TOPK == 2 ? sk[la * KS + g * TOPK + (TOPK - 1)] : 0ull;
+                    const unsigned long long y0 = sk[lb * KS + g * TOPK];
+                    const unsigned long long y1 = TOPK == 2 ? sk[lb * KS + g * TOPK + (TOPK - 1)] : 0ull;
+                    const unsigned long long t1 = x0 > y0 ? y0 : x0, t2 = x1 > y1 ? x1 : y1;
+                    q4[pq][0] = x0 > y0 ? x0 : y0;
+                    q4[pq][1] = t1 > t2 ? t1 : t2;
+                    q4[pq][2] = t1 > t2 ? t2 : t1;
+                    q4[pq][3] = x1 > y1 ? y1 : x1;
+                }
+                top4_merge(q4[0], q4[1]);
+                top4_merge(q4[2], q4[3]);
+                top4_merge(q4[0], q4[2]);
 #pragma unroll
-                for (int r = 0; r < RPW; ++r) e[r] += __shfl_xor_sync(0xffffffffu, e[r], o);
+                for (int z = 0; z < 4; ++z) top[z] = q4[0][z];
 #pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                const int i = cbase + r;
-                if (lane == 0 && i < n) {
-                    P.pm[(size_t)i * L + list] = M[r];
-                    P.ps[(size_t)i * L + list] = e[r];
+                for (int l = 8 * u; l < 8 * u + 8; ++l) {
+                    bmx = fmaxf(bmx, sbn[l * FS + g]);
+                    if constexpr (SOFTMAX) mu = fmaxf(mu, smm[l * FS + g]);
+                }
+                if constexpr (SOFTMAX) {
+#pragma unroll
+                    for (int l = 8 * u; l < 8 * u + 8; ++l) {
+                        const float ml = smm[l * FS + g];
+                        if (ml != kNegInf) eu += sss[l * FS + g] * exp2f((ml - mu) * 1.4426950408889634f);
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {  // combine the 4 lanes of the row
+                unsigned long long pk[4];
+#pragma unroll
+                for (int z = 0; z < 4; ++z) pk[z] = __shfl_xor_sync(0xffffffffu, top[z], o);
+                top4_merge(top, pk);
+                bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
+                if constexpr (SOFTMAX) {
+                    const float mo = __shfl_xor_sync(0xffffffffu, mu, o), eo = __shfl_xor_sync(0xffffffffu, eu, o);
+                    const float mn = fmaxf(mu, mo);
+                    const float ea = mu == kNegInf ? 0.0f : eu * exp2f((mu - mn) * 1.4426950408889634f);
+                    const float eb = mo == kNegInf ? 0.0f : eo * exp2f((mo - mn) * 1.4426950408889634f);
+                    mu = mn;
+                    eu = ea + eb;
+                }
+            }
+            if (live && u == 0) {
+                const int i = 2 * r + half;
+#pragma unroll
+                for (int z = 0; z < R; ++z) P.pkey[((size_t)i * L + list) * R + z] = top[z];
+                P.pth[(size_t)i * L + list] = fmaxf(top[R] ? dev::key_value(top[R]) : kNegInf, bmx);
+                if (top[0]) atomicMax(&s_rmax[i], static_cast<unsigned>(top[0] >> 32));
+                if constexpr (SOFTMAX) {
+                    P.pm[(size_t)i * L + list] = mu;
+                    P.ps[(size_t)i * L + list] = eu;
                 }
             }
         }
-        unsigned long long h1[RPW], h2[RPW], out[RPW];
-        float bmax[RPW];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-            bmax[r] = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(bnd[r])));
-            h1[r] = b1[r];
-            if constexpr (TOPK == 2) h2[r] = b2[r];
-            else h2[r] = 0ull;
-            out[r] = 0ull;
-        }
-#pragma unroll
-        for (int rnd = 0; rnd <= R; ++rnd) {
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                const unsigned long long best = warp_max_key(h1[r]);
-                if (lane == rnd) out[r] = best;
-                if (h1[r] == best && best != 0ull) {  // unique keys: one owner pops its head
-                    h1[r] = h2[r];
-                    h2[r] = 0ull;
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-            const int i = cbase + r;
-            if (i >= n) continue;
-            if (lane < R) P.pkey[((size_t)i * L + list) * R + lane] = out[r];
-            if (lane == 0 && out[r]) atomicMax(P.rowmax_bits + i, static_cast<unsigned>(out[r] >> 32));
-            if (lane == R) P.pth[(size_t)i * L + list] = fmaxf(out[r] ? dev::key_value(out[r]) : kNegInf, bmax[r]);
-        }
+        if (P.trace && threadIdx.x == 128) P.trace[(size_t)blockIdx.x * kTrMain + 31] = static_cast<unsigned long long>(clock64() - c_pub0);
         }  // !LOGITS
         if (threadIdx.x == 128) FRS_TRACE(P, 18);
+        if (P.trace && lane == 0 && (we == 0 || we == 4))  // DIAGNOSTIC: publish cycles
+            P.trace[(size_t)blockIdx.x * kTrMain + (we == 0 ? 29 : 30)] = static_cast<unsigned long long>(clock64() - c_pub0);
     }
-    __syncthreads();  // every TMEM read is done
+    __syncthreads();  // every TMEM read is done; s_rmax / s_w2max complete
+    if (threadIdx.x < n && s_rmax[threadIdx.x]) atomicMax(P.rowmax_bits + threadIdx.x, s_rmax[threadIdx.x]);
+    if (threadIdx.x == 64) atomicMax(P.w2_bits, s_w2max);
     if (P.late_trigger) griddep_launch();
     if (threadIdx.x == 0) FRS_TRACE(P, 7);
     if (warp == 1) {
@@ -639,6 +735,14 @@ struct FinArgs {
         if ((A).P.trace && (threadIdx.x & 31) == 0)                                                       \
             (A).P.trace[(size_t)(A).P.G * kTrMain + 64 * kFinCtas * 16 + 16 + (size_t)i * 16 + (q)] =    \
                 static_cast<unsigned long long>(clock64() - c_entry_);                                    \
+    } while (0)
+
+// DIAGNOSTIC: finalize phase cycles (leader CTA, thread 0) since griddepcontrol.wait returned
+#define FRS_FPROBE(A, q)                                                                                 \
+    do {                                                                                                  \
+        if ((A).P.trace && threadIdx.x == 0 && cluster_rank() == 0)                                       \
+            (A).P.trace[(size_t)(A).P.G * kTrMain + 64 * kFinCtas * 16 + 16 + (size_t)blockIdx.x * 16 + (q)] = \
+                static_cast<unsigned long long>(clock64() - c_fin0_);                                     \
     } while (0)
 
 // Row pitch (floats) of the transposed per-lane-chain operand tiles of the exact recompute: a
@@ -935,6 +1039,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     FRS_FTRACE(A, 1);
     griddep_wait();
     FRS_FTRACE(A, 2);
+    const long long c_fin0_ = clock64();
     if (A.ablate == 1) return;
     // ---- 1. keys in registers, eps, histogram; softmax / bound partials
     const int kk = min(A.k, A.v_rows);
@@ -964,6 +1069,10 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             if (v >= t0) {
                 const int pos = atomicAdd(&s_nsurv, 1);
                 if (pos < kSurvMax) s_surv[pos] = kr[u];
+                // S is drawn from the survivors (fast path): pull my share's slab rows towards
+                // L2 now, so the staging after the selection phases reads L2, not HBM
+                if ((dev::key_index(kr[u]) & (A.fin_ctas - 1)) == b)
+                    prefetch_l2_bulk(A.slab + (size_t)dev::key_index(kr[u]) * A.d, static_cast<uint32_t>(A.d) * 2u);
             } else {
                 a_far = fmaxf(a_far, v);
             }
@@ -971,7 +1080,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         a_far = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(a_far)));
         if (lane == 0) s_afar[warp] = a_far;
     }
-    FRS_FTRACE(A, 11);  // filter done (thread 0's share)
+    FRS_FPROBE(A, 9);  // filter done (thread 0's share)
     constexpr int SW = 4;                        // warps merging the softmax partials
     constexpr int PPL = kMaxLists / (32 * SW);   // partials per lane
     if (warp < SW && !A.argmax && A.ablate != 5) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
@@ -1011,7 +1120,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         if (lane == 0) s_thw[wb] = th;
     }
     __syncthreads();
-    FRS_FTRACE(A, 3);
+    FRS_FPROBE(A, 10);
     // ---- 2. the kk-th largest key: rank counting among the survivors (fast path), or a
     //         histogram of (M - v) / (eps / 2) over all keys (robust path: the top-k is spread
     //         wider than the filter or there are too many survivors)
@@ -1101,7 +1210,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         if (lane == 0) s_abw[warp] = a_below;
     }
     __syncthreads();
-    FRS_FTRACE(A, 4);
+    FRS_FPROBE(A, 11);
     const int nsel = s_nsel;
     // ---- 3. exact recompute of my share (none if S overflowed: the leader falls back)
     const int nmine = (nsel <= kCsMax && A.ablate != 2) ? min(s_nmine, kCsMax) : 0;
@@ -1136,7 +1245,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
                 }
             }
         }
-        FRS_FTRACE(A, 12);
+        FRS_FPROBE(A, 12);
         __syncthreads();
         if (tid < ((nc * 8 + 31) & ~31)) {  // whole warps: the xor tree below is warp-wide
             const int cl = (tid >> 3) < nc ? tid >> 3 : 0, l = tid & 7;
@@ -1180,13 +1289,13 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         }
         __syncthreads();
     }
-    FRS_FTRACE(A, 5);
+    FRS_FPROBE(A, 13);
     // cluster barrier: release our DSMEM stores, acquire everyone's in the leader
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     if (b != 0) return;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (warp != 0) return;
-    FRS_FTRACE(A, 10);
+    FRS_FPROBE(A, 14);
 
     // ---- 4. the cluster leader, warp 0: selection + certification
     float a_bound = fmaxf(s_thw[0], s_thw[1]);  // every row not recomputed has approx <= a_bound
@@ -1799,6 +1908,8 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     }
     static const int late = std::getenv("FRS_ABLATE") && std::atoi(std::getenv("FRS_ABLATE")) == 8;
     w.P.late_trigger = late;
+    static const int abl = std::getenv("FRS_ABLATE") ? std::atoi(std::getenv("FRS_ABLATE")) : 0;
+    w.P.ablate_main = abl == 14 || abl == 15 ? abl : 0;
     w.P.rowmax_bits = reinterpret_cast<unsigned *>(static_cast<uint8_t *>(ctx->fast_ctr.ptr) + kCtrRowmax);
     w.P.w2_bits = w.P.rowmax_bits + 64;
     return FRS_OK;
@@ -1899,7 +2010,7 @@ int launch_select(frs_ctx *ctx, const FinArgs &A0, int rows, cudaStream_t s) {
 }
 
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
-    if (A.ablate == 13) return FRS_OK;  // DIAGNOSTIC: main kernel only (outputs not written)
+    if (A.ablate >= 13 && A.ablate <= 15) return FRS_OK;  // DIAGNOSTIC: main kernel only (outputs not written)
     auto kern = k_fast_finalize;
     const int TP = fin_pitch(A.d / 8);
     const size_t smem = (size_t)8 * TP * 4 + (size_t)A.fin_stage * 8 * TP * 4 + 64;

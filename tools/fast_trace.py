@@ -69,11 +69,19 @@ def main():
         t0 = st[:, 0][st[:, 0] > 0].min()  # earliest "setup done" of the main kernel
         row = {}
         cp = pkey[n * L * 3 + G * 32 + 64 * 8 * 16 + 16:].reshape(64, 16).astype(np.int64)[:n]
-        for q, name in enumerate(["mx (redux)", "e-keys", "sorted", "tie", "bound", "inv", "written"]):
+        for q, name in list(enumerate(["mx (redux)", "e-keys", "sorted", "tie", "bound", "inv", "written"])) + [
+                (9, "fin: keys filtered"), (10, "fin: partials merged"), (11, "fin: S selected"),
+                (12, "fin: cand rows staged"), (13, "fin: recompute done"), (14, "fin leader: cluster wait done")]:
             v = cp[:, q]
             v = v[v > 0]
             if v.size:
-                row[f"C{q} certify cycles: {name}"] = [int(v.min()), int(np.median(v)), int(v.max())]
+                row[f"C{q} cycles: {name}"] = [int(v.min()), int(np.median(v)), int(v.max())]
+        for s_, name in ((6, "publish: softmax done"), (12, "publish: bmax done"), (31, "publish: tournament done"),
+                         (29, "publish cycles w0 (half 0)"), (30, "publish cycles w4 (half 1)")):
+            v = st[:, s_]
+            v = v[v > 0]
+            if v.size:
+                row[f"M{s_} {name}"] = [int(v.min()), int(np.median(v)), int(v.max())]
         for s, name in SLOTS.items():
             v = st[:, s]
             v = v[v > 0]
