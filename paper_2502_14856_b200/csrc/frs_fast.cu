@@ -2324,7 +2324,8 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
     A.id_offset = id_offset;
     static const int ablate = std::getenv("FRS_ABLATE") ? std::atoi(std::getenv("FRS_ABLATE")) : 0;
     A.ablate = ablate;
-    A.fin_ctas = argmax ? 2 : kFinCtas;  // argmax rows need ~1-3 exact candidates
+    static const int fin_env = std::getenv("FRS_FIN_CTAS") ? std::atoi(std::getenv("FRS_FIN_CTAS")) : 0;  // DIAGNOSTIC
+    A.fin_ctas = argmax ? 2 : (fin_env == 2 || fin_env == 4 ? fin_env : kFinCtas);  // argmax rows: ~1-3 candidates
     A.fin_stage = argmax ? 4 : kFinStage;
     return launch_fin(ctx, A, n, s);
 }
