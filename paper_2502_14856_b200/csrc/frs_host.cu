@@ -306,15 +306,20 @@ int frs_head_draft_host(frs_head *h, const float *h_host, int n, int k, int mode
     cudaStream_t s = h->ctx->stream;
     float *hd = static_cast<float *>(h->hidden.ptr);
     FRS_CUDA_TRY(cudaMemcpyAsync(hd, h_host, sizeof(float) * (size_t)n * h->d, cudaMemcpyHostToDevice, s));
-    st = frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode,
-                             static_cast<int32_t *>(h->lvl_ridx.ptr), static_cast<int32_t *>(h->lvl_full.ptr),
-                             static_cast<float *>(h->lvl_prob.ptr), nullptr, nullptr, nullptr, nullptr, s);
-    if (st) return st;
+    // outputs packed [ridx | full | prob] on the device: ONE D2H into pinned staging (the
+    // caller's arrays may be pageable, where each async copy degrades to a staged sync copy)
     const size_t cells = (size_t)n * k;
-    FRS_CUDA_TRY(cudaMemcpyAsync(ridx, h->lvl_ridx.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
-    FRS_CUDA_TRY(cudaMemcpyAsync(full, h->lvl_full.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
-    FRS_CUDA_TRY(cudaMemcpyAsync(prob, h->lvl_prob.ptr, cells * 4, cudaMemcpyDeviceToHost, s));
+    int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
+    st = frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode, pk,
+                             pk + cells, reinterpret_cast<float *>(pk + 2 * cells), nullptr, nullptr, nullptr, nullptr,
+                             s);
+    if (st) return st;
+    FRS_CUDA_TRY(cudaMemcpyAsync(h->h_ridx, pk, cells * 12, cudaMemcpyDeviceToHost, s));
     FRS_CUDA_TRY(cudaStreamSynchronize(s));
+    const int32_t *hp = static_cast<const int32_t *>(h->h_ridx);
+    std::memcpy(ridx, hp, cells * 4);
+    std::memcpy(full, hp + cells, cells * 4);
+    std::memcpy(prob, hp + 2 * cells, cells * 4);
     return FRS_OK;
 }
 
