@@ -5,6 +5,7 @@
 // same libm, std::sort comparators identical), so the device only runs the HBM-bound heads.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -20,7 +21,7 @@ struct frs_head {
     int64_t vocab = 0;
     int v_sub = 0, d = 0, dtype = FRS_DTYPE_F32;
     // per-level staging (device + pinned host)
-    frs::DevBuf lvl_ridx, lvl_full, lvl_prob, lvl_tok, hidden;
+    frs::DevBuf lvl_ridx, lvl_full, lvl_prob, lvl_tok, hidden, tree_ws;
     int32_t *h_ridx = nullptr, *h_full = nullptr, *h_tok = nullptr;
     float *h_prob = nullptr;
 };
@@ -279,6 +280,14 @@ int frs_head_info(const frs_head *h, const void **slab, const int32_t **ordered_
     return FRS_OK;
 }
 
+extern "C++" namespace frs {  // frs_tree.cu (C++ linkage inside this file's extern "C" block)
+size_t tree_ws_bytes(int max_cand);
+int tree_begin(void *ws, int max_cand, cudaStream_t s);
+int tree_level(void *ws, int max_cand, const int32_t *pk, int nb, int w_children, int width, bool prune, int total,
+               int32_t *next_tok, cudaStream_t s);
+int tree_select(void *ws, int max_cand, int total, int32_t **out_dev, cudaStream_t s);
+}  // namespace frs
+
 static int head_staging(frs_head *h, int rows, int k) {
     const size_t cells = (size_t)rows * k;
     int st;
@@ -341,6 +350,59 @@ int frs_draft_tree(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user
     cudaStream_t s = h->ctx->stream;
     float *hd = static_cast<float *>(h->hidden.ptr);
     int32_t *tok_dev = static_cast<int32_t *>(h->lvl_tok.ptr);
+
+    // Device-resident beam bookkeeping (frs_tree.cu) when the hidden rows come from a table:
+    // every level runs gather -> K2 -> k_tree_level with no host round trip, then one D2H of
+    // the selected nodes. An uncertified ordering decision (see frs_tree.cu) falls through to
+    // the host bookkeeping below.
+    if (!fn && hidden_table && total <= 64 && (size_t)w * width <= 960) {
+        int max_cand = w, nb = std::min(w, width);
+        for (int level = 1; level < depth; ++level) {
+            max_cand += nb * w;
+            nb = std::min(nb * w, width);
+        }
+        static const bool no_dev_tree = std::getenv("FRS_HOST_TREE") != nullptr;  // DIAGNOSTIC
+        if (max_cand <= 2048 && !no_dev_tree) {
+            if ((st = h->tree_ws.ensure(frs::tree_ws_bytes(max_cand)))) return st;
+            void *ws = h->tree_ws.ptr;
+            if ((st = frs::tree_begin(ws, max_cand, s))) return st;
+            h->h_tok[0] = root_token;
+            FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, h->h_tok, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            int rows = 1;
+            int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
+            for (int level = 0; level < depth && rows > 0; ++level) {
+                if ((st = frs_gather_rows(h->ctx, hidden_table, h->vocab, h->d, tok_dev, rows, hd, s))) return st;
+                const size_t cells = (size_t)rows * w;
+                if ((st = frs_draft_head_topk(h->ctx, hd, rows, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, w,
+                                              1.0f, mode, pk, pk + cells, reinterpret_cast<float *>(pk + 2 * cells),
+                                              nullptr, nullptr, nullptr, nullptr, s)))
+                    return st;
+                if ((st = frs::tree_level(ws, max_cand, pk, rows, w, width, level + 1 < depth, total, tok_dev, s)))
+                    return st;
+                rows = std::min(rows * w, width);
+            }
+            int32_t *out_dev = nullptr;
+            if ((st = frs::tree_select(ws, max_cand, total, &out_dev, s))) return st;
+            int32_t *ho = h->h_ridx;  // pinned staging
+            FRS_CUDA_TRY(cudaMemcpyAsync(ho, out_dev, sizeof(int32_t) * (2 + 4 * 64), cudaMemcpyDeviceToHost, s));
+            FRS_CUDA_TRY(cudaStreamSynchronize(s));
+            if (ho[1] == 0) {
+                const int K = ho[0];
+                const int32_t *tk = ho + 2, *pa = tk + 64, *dp = pa + 64, *pr = dp + 64;
+                for (int i = 0; i < K; ++i) {  // the reference's log_joint, parents first
+                    float p;
+                    std::memcpy(&p, pr + i, 4);
+                    const double lg = std::log(static_cast<double>(p));
+                    tokens[i] = tk[i];
+                    parents[i] = pa[i];
+                    depths[i] = dp[i];
+                    log_joint[i] = pa[i] < 0 ? lg : log_joint[pa[i]] + lg;
+                }
+                *count = K;
+                return FRS_OK;
+            }
+        }
+    }
 
     std::vector<Cand> cands;
     std::vector<int> beam;

@@ -1,6 +1,9 @@
 // K1 slab build, K4 greedy accept, K5 vocab-parallel argmax merge, row gather.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdint>
+
 #include "frs_common.cuh"
 
 namespace frs {
@@ -103,6 +106,8 @@ __global__ void k_argmax_merge(const float *__restrict__ vals, const int32_t *__
     out_id[row] = ids[(size_t)bs * m + row];
 }
 
+// grid (n, splits): row i, one slice of it per CTA; float4 when rows are 16-byte aligned (one
+// load in flight per thread for d <= 4096: a latency-bound scalar loop took ~10 us per level)
 __global__ void __launch_bounds__(256)
     k_gather_rows(const float *__restrict__ table, long long rows, int d, const int32_t *__restrict__ tokens,
                   int n, float *__restrict__ out) {
@@ -110,8 +115,15 @@ __global__ void __launch_bounds__(256)
     if (i >= n) return;
     const int t = tokens[i];
     const bool ok = t >= 0 && t < rows;
-    for (int c = threadIdx.x; c < d; c += blockDim.x)
-        out[(size_t)i * d + c] = ok ? table[(size_t)t * d + c] : 0.0f;
+    const int tid = blockIdx.y * blockDim.x + threadIdx.x, nt = gridDim.y * blockDim.x;
+    const bool vec = (d & 3) == 0 && ((reinterpret_cast<uintptr_t>(table) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (vec) {
+        const float4 *src = reinterpret_cast<const float4 *>(table + (size_t)(ok ? t : 0) * d);
+        float4 *dst = reinterpret_cast<float4 *>(out + (size_t)i * d);
+        for (int c = tid; c < d / 4; c += nt) dst[c] = ok ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+        for (int c = tid; c < d; c += nt) out[(size_t)i * d + c] = ok ? table[(size_t)t * d + c] : 0.0f;
+    }
 }
 
 }  // namespace
@@ -151,7 +163,8 @@ int argmax_merge(const float *vals, const int32_t *ids, int shards, int m, float
 
 int gather_rows(const float *table, long long rows, int d, const int32_t *tokens, int n, float *out,
                 cudaStream_t s) {
-    k_gather_rows<<<n, 256, 0, s>>>(table, rows, d, tokens, n, out);
+    const int splits = std::max(1, std::min(16, (d / 4 + 255) / 256));
+    k_gather_rows<<<dim3(n, splits), 256, 0, s>>>(table, rows, d, tokens, n, out);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }
