@@ -39,6 +39,7 @@ def parse():
     p.add_argument("--rows", type=int, default=C2["rows"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-verify", action="store_true", help="skip the vocab-parallel verify measurement")
+    p.add_argument("--no-decode", action="store_true", help="skip the head-path decode loop measurement")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
 
@@ -318,6 +319,41 @@ def main():
                      "GBps_per_rank": vbytes / vus / 1e3, "frac_of_peak_per_rank": vbytes / vus / 1e3 / hbm_peak}
         del Wq
 
+    # Decode tokens/s (BASELINE metric's second half): the head-path loop through
+    # the public API — build_draft_tree (6 levels, width 10, 60 tokens; device-resident beam
+    # bookkeeping, identity draft layer: hidden(token) = rmsnorm(E[token])) + verify_greedy_table
+    # (61 rows over the full V = 128256 bf16 head, device gather + accept), one host sync each.
+    # Transformer layers are out of scope (stated); random-init heads accept ~1.4 tokens/iter.
+    decode = None
+    if not args.no_decode:
+        ge = torch.Generator(device=dev).manual_seed(555 + rank)
+        E = rmsnorm_rows(torch.randn(V, d, generator=ge, device=dev))
+        Wb = W.to(torch.bfloat16)
+        params = api.DraftParams(10, 6, 60)
+        token, emitted, iters = 1, 0, 40
+        for _ in range(3):
+            tree = dh.build_draft_tree(token, params, mode=mode, hidden_table=E)
+            token = int(api.verify_greedy_table(ctx, E, token, Wb, tree, mode=mode).emitted[-1])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            tree = dh.build_draft_tree(token, params, mode=mode, hidden_table=E)
+            outc = api.verify_greedy_table(ctx, E, token, Wb, tree, mode=mode)
+            emitted += outc.accepted_length()
+            token = int(outc.emitted[-1])
+        dec_s = time.perf_counter() - t0
+        rate = emitted / dec_s
+        if world > 1:
+            t = torch.tensor([rate, dec_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t[:1], op=dist.ReduceOp.SUM)
+            rate = float(t[0].item())
+        decode = {"workload": "head-path decode loop at C2: draft tree depth 6 / width 10 / 60 tokens (FR head, "
+                              "V_sub 32768) + greedy verify of 61 rows over V = 128256 (bf16), identity draft layer",
+                  "tokens_per_s": rate, "ms_per_iteration": 1000.0 * dec_s / iters,
+                  "mean_accepted_length": emitted / iters, "iterations": iters, "streams": world,
+                  "note": "transformer layers excluded (SURVEY.md §8(d)); random-init weights"}
+        del E, Wb
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         slab32 = head.slab.float().cpu().numpy()
@@ -353,6 +389,7 @@ def main():
                     "api": "frs_head_draft_host (C ABI, pinned host buffers, synchronous)"},
             "clocks": clocks, "gpu_launches": launches, "slab_build_ms": slab_build_ms, "row_flags": flag_counts,
             "verify_vocab_parallel": verify_vp,
+            "decode": decode,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
