@@ -69,6 +69,7 @@ typedef enum { FRS_MODE_EXACT = 0, FRS_MODE_FAST = 1 } frs_mode;
 #define FRS_FLAG_CERT_BOUND 0x20u    /* the rigorous error bound did not separate the k-th candidate   */
 #define FRS_FLAG_CERT_OVERFLOW 0x40u /* more near-boundary candidates than the exact-recompute set     */
 /* FAST, certified rows: bits 8..15 hold the size of the exactly recomputed candidate set (info). */
+#define FRS_FLAG_SAMPLE_UNCERTIFIED 0x80u /* sampled draw inside the rounding bound: host replays the level */
 #define FRS_FLAG_CAND_SHIFT 8
 
 typedef struct frs_ctx frs_ctx;
@@ -177,6 +178,28 @@ FRS_API int frs_draft_tree(frs_head *head, int32_t root_token, frs_hidden_fn fn,
                    const float *hidden_table, int width, int depth, int total, int mode,
                    int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint,
                    int *count);
+/* Sampled drafting (drafting.cpp:44-74): a std::mt19937_64 the caller owns (the reference's
+ * `std::mt19937_64 * rng`), advanced by every draw exactly as the reference advances it. */
+typedef struct frs_rng frs_rng;
+FRS_API int frs_rng_create(uint64_t seed, frs_rng **out);
+FRS_API int frs_rng_destroy(frs_rng *rng);
+/* Uniforms in [0, 1) the way std::uniform_real_distribution<double>(0, 1) draws them (tests). */
+FRS_API int frs_rng_uniforms(frs_rng *rng, int count, double *out);
+/* K2 sampled (EXACT arithmetic only): per row, the exact softmax (kernels.cpp:62-91) into
+ * probs [n x v_sub] (device) and w = min(width, v_sub) draws without replacement with the
+ * given uniforms (device, [n x w], draw order) — pick_children's sampled branch. Outputs
+ * ridx/full/prob [n x w] in draw order, count[n] draws made, flags[n] (FRS_FLAG_SAMPLE_
+ * UNCERTIFIED: a draw was not certified; the caller replays the row from probs). */
+FRS_API int frs_draft_head_sample(frs_ctx *ctx, const float *h, int n, int d, const void *slab, int v_sub,
+                                  int slab_dtype, const int32_t *ordered_ids, int width, float temperature,
+                                  const double *uniforms, float *probs, int32_t *out_ridx, int32_t *out_full,
+                                  float *out_prob, int32_t *out_count, uint32_t *out_flags, void *stream);
+/* build_draft_tree with an rng (drafting.cpp:122-245: sampled children, prefix-closed
+ * select_top_k), head path, EXACT arithmetic. Same arguments as frs_draft_tree plus rng. */
+FRS_API int frs_draft_tree_sampled(frs_head *head, int32_t root_token, frs_hidden_fn fn, void *user,
+                                   const float *hidden_table, int width, int depth, int total, frs_rng *rng,
+                                   int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint,
+                                   int *count);
 /* verify_greedy (verification.cpp:42-71) with the target head on the device: h_dev holds
  * 1 + k rows (root first), W the full LM head [V x d] (device). Host outputs. */
 FRS_API int frs_verify_greedy(frs_ctx *ctx, const float *h_dev, const void *W, int V, int d, int w_dtype,

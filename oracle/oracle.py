@@ -238,6 +238,14 @@ class Reference:
         L.ref_model_draft_capture.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_void_p, C.c_int, _i32p, C.c_int,
                                                               C.c_int, C.c_int, C.c_int, _f32p, _i32p, _i32p, _ip,
                                                               _i32p, _i32p, _i32p, _f64p, _ip]
+        L.ref_model_draft_tree_rng.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_void_p, C.c_int, _i32p, C.c_int,
+                                                               C.c_int, C.c_int, C.c_int, C.c_uint64, _i32p, _i32p,
+                                                               _i32p, _f64p, _ip]
+        L.ref_model_draft_capture_rng.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_void_p, C.c_int, _i32p, C.c_int,
+                                                                  C.c_int, C.c_int, C.c_int, C.c_uint64, _f32p, _i32p,
+                                                                  _i32p, _ip, _i32p, _i32p, _i32p, _f64p, _ip]
+        L.ref_pick_sampled.argtypes = [_f32p, C.c_int, C.c_int, C.c_uint64, C.c_int64, _i32p, _f32p, _ip]
+        L.ref_uniforms.argtypes = [C.c_uint64, C.c_int64, C.c_int, _f64p]
 
     def _check(self, rc: int, what: str):
         if rc:
@@ -363,6 +371,53 @@ class Reference:
         return dict(hidden=hid[:r].copy(), row_token=rtok[:r].copy(), row_level=rlev[:r].copy(),
                     tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(),
                     log_joint=lj[:n].copy())
+
+
+    def model_draft_tree_rng(self, V, d, layers, heads, max_seq, seed, ordered, pending, width, depth, total,
+                             rng_seed):
+        o = None if ordered is None else _ci32(ordered)
+        pend = _ci32(pending)
+        tok, par, dep = (np.empty(64, np.int32) for _ in range(3))
+        lj, cnt = np.empty(64, np.float64), C.c_int()
+        self._check(self.lib.ref_model_draft_tree_rng(V, d, layers, heads, max_seq, seed,
+                                                      None if o is None else o.ctypes.data,
+                                                      0 if o is None else o.size, pend, pend.size, width, depth,
+                                                      total, C.c_uint64(rng_seed), tok, par, dep, lj,
+                                                      C.byref(cnt)), "build_draft_tree(rng)")
+        n = cnt.value
+        return dict(tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(), log_joint=lj[:n].copy())
+
+    def model_draft_capture_rng(self, V, d, layers, heads, max_seq, seed, ordered, pending, width, depth, total,
+                                rng_seed):
+        o = None if ordered is None else _ci32(ordered)
+        pend = _ci32(pending)
+        max_rows = 1 + (depth - 1) * width
+        hid = np.empty((max_rows, d), np.float32)
+        rtok, rlev, nrows = np.empty(max_rows, np.int32), np.empty(max_rows, np.int32), C.c_int()
+        tok, par, dep = (np.empty(64, np.int32) for _ in range(3))
+        lj, cnt = np.empty(64, np.float64), C.c_int()
+        self._check(self.lib.ref_model_draft_capture_rng(V, d, layers, heads, max_seq, seed,
+                                                         None if o is None else o.ctypes.data,
+                                                         0 if o is None else o.size, pend, pend.size, width, depth,
+                                                         total, C.c_uint64(rng_seed), hid, rtok, rlev,
+                                                         C.byref(nrows), tok, par, dep, lj, C.byref(cnt)),
+                    "draft_capture(rng)")
+        n, r = cnt.value, nrows.value
+        return dict(hidden=hid[:r].copy(), row_token=rtok[:r].copy(), row_level=rlev[:r].copy(),
+                    tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(),
+                    log_joint=lj[:n].copy())
+
+    def uniforms(self, seed, count, skip=0):
+        out = np.empty(count, np.float64)
+        self._check(self.lib.ref_uniforms(C.c_uint64(seed), C.c_int64(skip), count, out), "uniforms")
+        return out
+
+    def pick_sampled(self, probs, width, rng_seed, skip=0):
+        p = _c32(probs)
+        picks, pr, cnt = np.empty(width, np.int32), np.empty(width, np.float32), C.c_int()
+        self._check(self.lib.ref_pick_sampled(p, p.size, width, C.c_uint64(rng_seed), C.c_int64(skip), picks, pr,
+                                              C.byref(cnt)), "pick_sampled")
+        return picks[:cnt.value].copy(), pr[:cnt.value].copy()
 
 
 class RefHead:

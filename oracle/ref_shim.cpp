@@ -402,4 +402,203 @@ int ref_model_draft_capture(int V, int d, int layers, int heads, int max_seq, ui
     });
 }
 
+// Sampled drafting (drafting.cpp:44-74 with an rng): the reference's own build_draft_tree
+// with std::mt19937_64(rng_seed).
+int ref_model_draft_tree_rng(int V, int d, int layers, int heads, int max_seq, uint64_t seed,
+                             const int32_t * ordered, int v_sub, const int32_t * pending, int n_pending,
+                             int width, int depth, int total, uint64_t rng_seed, int32_t * tokens,
+                             int32_t * parents, int32_t * depths, double * log_joint, int * count) {
+    return guarded([&] {
+        ModelBundle b = make_bundle(V, d, layers, heads, max_seq, seed, ordered, v_sub);
+        KVCache cache = make_cache(b.draft);
+        DraftParams p{width, depth, total};
+        std::mt19937_64 rng(rng_seed);
+        DraftResult r = build_draft_tree(b.draft, cache, std::span<const Token>(pending, n_pending), p,
+                                         ordered ? &b.head : nullptr, &rng, false);
+        export_tree(r.tree, tokens, parents, depths, log_joint, count);
+    });
+}
+
+// Restatement of pick_children's sampled branch (drafting.cpp:44-74; the original sits in an
+// anonymous namespace), pinned by the sampled capture test against build_draft_tree above.
+static std::vector<std::pair<int, float>> pick_sampled(const std::vector<float> & probs, int width,
+                                                       std::mt19937_64 & rng) {
+    const int n = static_cast<int>(probs.size());
+    const int w = std::min(width, n);
+    std::vector<std::pair<int, float>> out;
+    std::vector<double> work(probs.begin(), probs.end());
+    std::uniform_real_distribution<double> uni(0.0, 1.0);
+    for (int draw = 0; draw < w; ++draw) {
+        double total = 0.0;
+        for (double p : work) total += p;
+        if (total <= 0.0) break;
+        const double u = uni(rng) * total;
+        double acc = 0.0;
+        int picked = -1;
+        for (int i = 0; i < n; ++i) {
+            acc += work[i];
+            if (u < acc) {
+                picked = i;
+                break;
+            }
+        }
+        if (picked < 0) {
+            for (int i = n - 1; i >= 0; --i)
+                if (work[i] > 0.0) {
+                    picked = i;
+                    break;
+                }
+            if (picked < 0) break;
+        }
+        out.emplace_back(picked, probs[picked]);
+        work[picked] = 0.0;
+    }
+    return out;
+}
+
+// pick_sampled over given probabilities (unit tests of the device sampler): picks[w], probs[w]
+// in draw order; *count = draws made. Consumes draws from a fresh mt19937_64(rng_seed) after
+// skipping `skip` uniforms.
+int ref_pick_sampled(const float * probs, int n, int width, uint64_t rng_seed, int64_t skip, int32_t * picks,
+                     float * out_probs, int * count) {
+    return guarded([&] {
+        std::mt19937_64 rng(rng_seed);
+        std::uniform_real_distribution<double> uni(0.0, 1.0);
+        for (int64_t i = 0; i < skip; ++i) (void)uni(rng);
+        auto kids = pick_sampled(std::vector<float>(probs, probs + n), width, rng);
+        for (size_t i = 0; i < kids.size(); ++i) {
+            picks[i] = kids[i].first;
+            out_probs[i] = kids[i].second;
+        }
+        *count = static_cast<int>(kids.size());
+    });
+}
+
+// std::uniform_real_distribution<double>(0, 1) draws of std::mt19937_64(seed) (tests).
+int ref_uniforms(uint64_t seed, int64_t skip, int count, double * out) {
+    return guarded([&] {
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> uni(0.0, 1.0);
+        for (int64_t i = 0; i < skip; ++i) (void)uni(rng);
+        for (int i = 0; i < count; ++i) out[i] = uni(rng);
+    });
+}
+
+// Sampled-mode capture: the drafting loop of ref_model_draft_capture with pick_sampled and the
+// prefix-closed select_top_k (drafting.cpp:93-118, prefix_closed = true).
+int ref_model_draft_capture_rng(int V, int d, int layers, int heads, int max_seq, uint64_t seed,
+                                const int32_t * ordered, int v_sub, const int32_t * pending, int n_pending,
+                                int width, int depth, int total, uint64_t rng_seed, float * hidden_out,
+                                int32_t * row_token, int32_t * row_level, int * n_rows, int32_t * tokens,
+                                int32_t * parents, int32_t * depths, double * log_joint, int * count) {
+    return guarded([&] {
+        ModelBundle b = make_bundle(V, d, layers, heads, max_seq, seed, ordered, v_sub);
+        KVCache cache = make_cache(b.draft);
+        DraftParams params{width, depth, total};
+        validate_params(params);
+        std::mt19937_64 rng(rng_seed);
+        const RankedSubset * subset = ordered ? b.subset.get() : nullptr;
+        const Matrix & head = ordered ? b.head.matrix : b.draft.shared->lm_head;
+        struct Cand {
+            Token token;
+            int parent, depth, sibling_rank;
+            double log_joint;
+            int cache_row;
+        };
+        int rows = 0;
+        auto emit_row = [&](const Matrix & hid, int r, Token tok, int level) {
+            std::memcpy(hidden_out + static_cast<size_t>(rows) * d, hid.row(r), sizeof(float) * d);
+            row_token[rows] = tok;
+            row_level[rows] = level;
+            ++rows;
+        };
+        ForwardResult fwd = draft_forward(b.draft, std::span<const Token>(pending, n_pending), cache,
+                                          ordered ? &b.head : nullptr);
+        emit_row(fwd.hidden, fwd.hidden.rows - 1, pending[n_pending - 1], 0);
+        const int base_len = cache.len;
+        const int anchor_pos = cache.positions[base_len - 1];
+        std::vector<Cand> cands;
+        std::vector<int> beam;
+        {
+            ProbVector pr = softmax(fwd.logits.row_span(fwd.logits.rows - 1), 1.0f);
+            int rank = 0;
+            for (auto [idx, prob] : pick_sampled(pr.probs, width, rng)) {
+                beam.push_back(static_cast<int>(cands.size()));
+                cands.push_back({subset ? subset->full_id(idx) : idx, -1, 1, rank++, std::log((double)prob), -1});
+            }
+        }
+        for (int level = 1; level < depth && !beam.empty(); ++level) {
+            if (static_cast<int>(beam.size()) > width) {
+                std::sort(beam.begin(), beam.end(), [&](int a, int c) {
+                    if (cands[a].log_joint != cands[c].log_joint) return cands[a].log_joint > cands[c].log_joint;
+                    return a < c;
+                });
+                beam.resize(width);
+                std::sort(beam.begin(), beam.end());
+            }
+            const int batch = static_cast<int>(beam.size());
+            TokenSequence bt;
+            std::vector<int> bp;
+            BitMask visible(batch, cache.len + batch);
+            for (int i = 0; i < batch; ++i) {
+                Cand & c = cands[beam[i]];
+                c.cache_row = cache.len + i;
+                bt.push_back(c.token);
+                bp.push_back(anchor_pos + c.depth);
+                visible.set_range(i, 0, base_len);
+                for (int a = c.parent; a >= 0; a = cands[a].parent) visible.set(i, cands[a].cache_row);
+                visible.set(i, c.cache_row);
+            }
+            fwd = forward_raw(*b.draft.shared, {&b.draft.layer, 1}, bt, bp, visible, cache, head);
+            std::vector<int> next;
+            for (int i = 0; i < batch; ++i) {
+                emit_row(fwd.hidden, i, bt[i], level);
+                const int pidx = beam[i];
+                const int pdepth = cands[pidx].depth;
+                const double plj = cands[pidx].log_joint;
+                ProbVector pr = softmax(fwd.logits.row_span(i), 1.0f);
+                int rank = 0;
+                for (auto [idx, prob] : pick_sampled(pr.probs, width, rng)) {
+                    next.push_back(static_cast<int>(cands.size()));
+                    cands.push_back({subset ? subset->full_id(idx) : idx, pidx, pdepth + 1, rank++,
+                                     plj + std::log((double)prob), -1});
+                }
+            }
+            beam = std::move(next);
+        }
+        *n_rows = rows;
+        std::vector<int> order(cands.size());
+        for (size_t i = 0; i < cands.size(); ++i) order[i] = static_cast<int>(i);
+        std::sort(order.begin(), order.end(), [&](int a, int c) {
+            if (cands[a].log_joint != cands[c].log_joint) return cands[a].log_joint > cands[c].log_joint;
+            return a < c;
+        });
+        std::vector<char> sel(cands.size(), 0);
+        int cnt = 0;
+        for (int c : order) {
+            if (sel[c]) continue;
+            if (cands[c].parent >= 0 && !sel[cands[c].parent]) continue;
+            std::vector<int> group;
+            for (size_t s2 = 0; s2 < cands.size(); ++s2)
+                if (!sel[s2] && cands[s2].parent == cands[c].parent && cands[s2].sibling_rank <= cands[c].sibling_rank)
+                    group.push_back(static_cast<int>(s2));
+            if (cnt + static_cast<int>(group.size()) > total) continue;
+            for (int g : group) sel[g] = 1;
+            cnt += static_cast<int>(group.size());
+        }
+        std::vector<int> remap(cands.size(), -1);
+        int out = 0;
+        for (size_t i = 0; i < cands.size(); ++i) {
+            if (!sel[i]) continue;
+            remap[i] = out;
+            tokens[out] = cands[i].token;
+            parents[out] = cands[i].parent >= 0 ? remap[cands[i].parent] : -1;
+            depths[out] = cands[i].depth;
+            log_joint[out] = cands[i].log_joint;
+            ++out;
+        }
+        *count = out;
+    });
+}
+
 }  // extern "C"

@@ -16,6 +16,7 @@ DTYPE_F32, DTYPE_BF16 = 0, 1
 MODE_EXACT, MODE_FAST = 0, 1
 FLAG_NONFINITE, FLAG_SEQ_SUM, FLAG_UNCERTIFIED, FLAG_RECOMPUTED = 0x1, 0x2, 0x4, 0x8
 FLAG_CERT_TIE, FLAG_CERT_BOUND, FLAG_CERT_OVERFLOW = 0x10, 0x20, 0x40
+FLAG_SAMPLE_UNCERTIFIED = 0x80
 
 
 class FrsError(RuntimeError):
@@ -84,6 +85,12 @@ SIGNATURES = [
     ("frs_head_info", _I, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     ("frs_head_draft_host", _I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     ("frs_draft_tree", _I, [_P, C.c_int32, HIDDEN_FN, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, C.POINTER(_I)]),
+    ("frs_rng_create", _I, [C.c_uint64, C.POINTER(_P)]),
+    ("frs_rng_destroy", _I, [_P]),
+    ("frs_rng_uniforms", _I, [_P, _I, _P]),
+    ("frs_draft_head_sample", _I, [_P, _P, _I, _I, _P, _I, _I, _P, _I, C.c_float, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("frs_draft_tree_sampled", _I, [_P, C.c_int32, HIDDEN_FN, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P,
+                                    C.POINTER(_I)]),
     ("frs_verify_greedy", _I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P, C.POINTER(_I)]),
     ("frs_verify_greedy_table", _I, [_P, _P, _I64, C.c_int32, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P,
                                      C.POINTER(_I)]),

@@ -394,9 +394,14 @@ class DeviceHead:
         return ridx, full, prob
 
     def build_draft_tree(self, root_token: int, params: DraftParams = DraftParams(), mode="exact",
-                         provider: Optional[Callable] = None, hidden_table: Optional[torch.Tensor] = None) -> DraftTree:
-        """Head-path build_draft_tree (drafting.cpp:122-245, greedy). provider(level, tokens,
-        parent_cands) -> CUDA float32 [n x d] tensor of the forwarded rows' hidden states."""
+                         provider: Optional[Callable] = None, hidden_table: Optional[torch.Tensor] = None,
+                         rng: Optional["Rng"] = None) -> DraftTree:
+        """Head-path build_draft_tree (drafting.cpp:122-245). provider(level, tokens,
+        parent_cands) -> CUDA float32 [n x d] tensor of the forwarded rows' hidden states.
+        rng=None: greedy children (top-width); with an Rng: sampled children without
+        replacement (drafting.cpp:44-74, EXACT arithmetic) and the prefix-closed selection."""
+        if rng is not None and mode != "exact":
+            raise ValueError("sampled drafting runs on the exact probabilities: mode must be 'exact'")
         keep = {}
 
         def cb(_user, level, n, tok_p, par_p, hidden_dev, stream):
@@ -416,14 +421,73 @@ class DeviceHead:
         total = params.total_draft_tokens
         tok, par, dep = (np.empty(max(total, 1), np.int32) for _ in range(3))
         lj, cnt = np.empty(max(total, 1), np.float64), C.c_int()
-        st = lib().frs_draft_tree(self.handle, root_token, fn, None, _ptr(hidden_table), params.beam_width,
-                                  params.search_depth, total, _mode(mode), _np_ptr(tok), _np_ptr(par), _np_ptr(dep),
-                                  _np_ptr(lj), C.byref(cnt))
+        if rng is None:
+            st = lib().frs_draft_tree(self.handle, root_token, fn, None, _ptr(hidden_table), params.beam_width,
+                                      params.search_depth, total, _mode(mode), _np_ptr(tok), _np_ptr(par),
+                                      _np_ptr(dep), _np_ptr(lj), C.byref(cnt))
+        else:
+            st = lib().frs_draft_tree_sampled(self.handle, root_token, fn, None, _ptr(hidden_table),
+                                              params.beam_width, params.search_depth, total, rng.handle,
+                                              _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt))
         if "exc" in keep:
             raise keep["exc"]
         check(st, "build_draft_tree")
         n = cnt.value
         return DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy())
+
+
+class Rng:
+    """The reference's ``std::mt19937_64`` (drafting.cpp:44-74, verification.cpp:76-178): one
+    engine, advanced by every draw in the reference's order."""
+
+    def __init__(self, seed: int):
+        h = C.c_void_p()
+        check(lib().frs_rng_create(C.c_uint64(seed), C.byref(h)), "rng")
+        self.handle = h
+
+    def uniforms(self, count: int) -> np.ndarray:
+        """std::uniform_real_distribution<double>(0, 1) draws (advances the engine)."""
+        out = np.empty(count, np.float64)
+        check(lib().frs_rng_uniforms(self.handle, count, _np_ptr(out)), "rng")
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and _lib._LIB is not None:
+                lib().frs_rng_destroy(self.handle)
+                self.handle = None
+        except Exception:  # interpreter shutdown
+            pass
+
+
+@dataclass
+class SampledLevel:
+    ridx: torch.Tensor   # [n, w] restricted indices, draw order
+    full: torch.Tensor   # [n, w] full-vocabulary ids
+    prob: torch.Tensor   # [n, w] probabilities of the drawn children
+    count: torch.Tensor  # [n] draws made
+    flags: torch.Tensor  # [n] FLAG_SAMPLE_UNCERTIFIED: replay the row on the host
+    probs: torch.Tensor  # [n, v_sub] exact probabilities
+
+
+def draft_head_sample(ctx: Context, h: torch.Tensor, head: "RestrictedHead", width: int,
+                      uniforms: torch.Tensor) -> SampledLevel:
+    """K2 sampled (pick_children's sampled branch, drafting.cpp:44-74) over the EXACT softmax:
+    uniforms [n, min(width, v_sub)] float64 on the device, in draw order."""
+    h = h.contiguous()
+    n, d = h.shape
+    w = min(width, head.v_sub)
+    dev = h.device
+    u = uniforms.to(device=dev, dtype=torch.float64).contiguous()
+    out = SampledLevel(torch.empty((n, w), dtype=torch.int32, device=dev), torch.empty((n, w), dtype=torch.int32, device=dev),
+                       torch.empty((n, w), dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
+                       torch.empty(n, dtype=torch.int32, device=dev),
+                       torch.empty((n, head.v_sub), dtype=torch.float32, device=dev))
+    check(lib().frs_draft_head_sample(ctx.handle, _ptr(h), n, d, _ptr(head.slab), head.v_sub, head.dtype,
+                                      _ptr(head.ordered_dev), width, C.c_float(1.0), _ptr(u), _ptr(out.probs),
+                                      _ptr(out.ridx), _ptr(out.full), _ptr(out.prob), _ptr(out.count),
+                                      _ptr(out.flags), _stream(None)), "draft_head_sample")
+    return out
 
 
 class _DeviceView:

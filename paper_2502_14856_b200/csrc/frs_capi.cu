@@ -213,6 +213,29 @@ int frs_draft_head_topk(frs_ctx *ctx, const float *h, int n, int d, const void *
                                out_rowmax, out_total, out_flags, s);
 }
 
+int frs_draft_head_sample(frs_ctx *ctx, const float *h, int n, int d, const void *slab, int v_sub, int slab_dtype,
+                          const int32_t *ordered_ids, int width, float temperature, const double *uniforms,
+                          float *probs, int32_t *out_ridx, int32_t *out_full, float *out_prob, int32_t *out_count,
+                          uint32_t *out_flags, void *stream) {
+    int st = check_device(ctx);
+    if (st) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    FRS_REQUIRE(h && slab && uniforms && probs && out_ridx && out_full && out_prob && out_count,
+                "sampled draft head: null pointer");
+    FRS_REQUIRE(n >= 1, "forward: empty token batch");                       // model.cpp:217
+    FRS_REQUIRE(d >= 1 && v_sub >= 1, "draft head: sizes must be positive");
+    FRS_REQUIRE(width >= 1, "draft params: beam_width must be >= 1");       // drafting.cpp:15
+    FRS_REQUIRE(std::isfinite(temperature) && temperature > 0.0f,
+                "softmax: temperature must be positive and finite");       // kernels.cpp:66-68
+    FRS_REQUIRE(valid_dtype(slab_dtype), "draft head: unknown slab dtype");
+    const int w = std::min(width, v_sub);                                   // drafting.cpp:40
+    if ((st = ctx->logits.ensure((size_t)n * v_sub * sizeof(float)))) return st;
+    float *logits = static_cast<float *>(ctx->logits.ptr);
+    if ((st = launch_exact_logits(ctx, h, n, d, slab, slab_dtype, v_sub, logits, s))) return st;
+    return launch_softmax_sample(ctx, logits, n, v_sub, temperature, uniforms, w, ordered_ids, probs, out_ridx,
+                                 out_full, out_prob, out_count, out_flags, s);
+}
+
 int frs_verify_head_argmax(frs_ctx *ctx, const float *h, int m, int d, const void *W, int v_rows, int w_dtype,
                            int32_t id_offset, int mode, int32_t *out_id, float *out_val, uint32_t *out_flags,
                            void *stream) {

@@ -331,6 +331,59 @@ static __device__ __noinline__ uint32_t softmax_topk_row(const float *__restrict
     return flags;
 }
 
+// Exact softmax probabilities of ONE row (kernels.cpp:62-91): P[j] = float(e_j) * inv with the
+// reference's e_j (glibc expf) and inv = float(1 / total). inv is pinned as in
+// softmax_topk_row(tree_total_ok): the tree sum brackets the index-order sum; the sequential
+// replay runs only when the bracket straddles a float boundary. Whole block; returns flags.
+static __device__ __noinline__ uint32_t softmax_probs_row(const float *__restrict__ L, int v, float temperature,
+                                                          float *__restrict__ P, ReduceScratch &rs) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    load_exp_table(rs.tab);
+    float mx = -__int_as_float(0x7f800000);
+    int bad = 0;
+    const bool unit_t = temperature == 1.0f;
+    row_pass<8>(L, v, [&](int, float x) {
+        if (!isfinite(x)) bad = 1;
+        const float y = unit_t ? x : __fdiv_rn(x, temperature);
+        mx = (mx < y) ? y : mx;
+    });
+    mx = block_reduce(mx, MaxF(), rs.f);
+    bad = block_reduce(bad, OrI(), rs.i);
+    uint32_t flags = bad ? FRS_FLAG_NONFINITE : 0u;
+    double part = 0.0;
+    int lsb = 0x7fffffff;
+    row_pass<8>(L, v, [&](int j, float x) {
+        const float e = expf_glibc(__fsub_rn(unit_t ? x : __fdiv_rn(x, temperature), mx), rs.tab);
+        P[j] = e;
+        part += static_cast<double>(e);
+        lsb = min(lsb, lsb_exponent(e));
+    });
+    double total = block_reduce(part, SumD(), rs.d);
+    lsb = block_reduce(lsb, MinI(), rs.i);
+    bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
+    if (!exact && total > 0.0) {
+        const double del = static_cast<double>(v + 2 * nt) * 0x1p-52;
+        const double lo = __dmul_rd(total, 1.0 - del), hi = __dmul_ru(total, 1.0 + del);
+        exact = __double2float_rn(1.0 / lo) == __double2float_rn(1.0 / hi);
+    }
+    if (!exact) {
+        flags |= FRS_FLAG_SEQ_SUM;
+        __syncthreads();
+        if (tid == 0) {
+            double acc = 0.0;
+            for (int j = 0; j < v; ++j) acc += static_cast<double>(P[j]);
+            rs.d[0] = acc;
+        }
+        __syncthreads();
+        total = rs.d[0];
+    }
+    const float inv = __double2float_rn(1.0 / total);
+    __syncthreads();
+    for (int j = tid; j < v; j += nt) P[j] = __fmul_rn(P[j], inv);
+    __syncthreads();
+    return flags;
+}
+
 // Exact dot_f32 (kernels.cpp:13-32) of h (fp32) with a bf16/fp32 row, computed by the 8
 // lanes l = threadIdx.x % 8 of an aligned 8-lane group; the result is valid in lane l == 0.
 // Requires the 8 lanes of the group to be converged; d % 8 == 0 handled by the lane chains,

@@ -32,6 +32,108 @@ __device__ __forceinline__ float load_w(const __nv_bfloat16 *p) {
     return __uint_as_float(static_cast<uint32_t>(u) << 16);  // bf16 -> fp32 is exact
 }
 
+// Sampled pick_children (drafting.cpp:44-74) for each row: exact probabilities (kernels.cpp:
+// 62-91, softmax_probs_row) into probs[row], then w draws without replacement with the caller's
+// uniforms (std::uniform_real_distribution<double> of the reference's mt19937_64, in draw
+// order). The reference sums work[] sequentially in double each draw and scans for the first
+// running sum above u = uni * total; here the prefix is a block scan of per-thread chunk sums,
+// and every decision is certified: the tree prefix P_i and the index-order acc_i differ by at
+// most eb = (v + 2048 + 64 w) 2^-52 T, so the pick is certain when the first i with
+// P_i + eb > u_lo equals the first with P_i - eb > u_hi (u's own bracket from T +- eb). An
+// uncertain draw (or the reference's upper-edge guard) stops the row with
+// FRS_FLAG_SAMPLE_UNCERTIFIED: the host replays that level from the probabilities.
+__global__ void __launch_bounds__(1024)
+    k_softmax_sample(const float *__restrict__ logits, int v, float temperature, const double *__restrict__ uniforms,
+                     int w, const int32_t *__restrict__ ordered, float *__restrict__ probs, float *__restrict__ work,
+                     int32_t *__restrict__ out_ridx, int32_t *__restrict__ out_full, float *__restrict__ out_prob,
+                     int32_t *__restrict__ out_count, uint32_t *__restrict__ out_flags) {
+    __shared__ dev::ReduceScratch rs;
+    __shared__ double s_cp[1024];
+    const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const float *L = logits + (size_t)row * v;
+    float *P = probs + (size_t)row * v, *Wk = work + (size_t)row * v;
+    uint32_t flags = dev::softmax_probs_row(L, v, temperature, P, rs);
+    __shared__ int s_pick, s_stop;
+    const int C = (v + 1023) / 1024, j0 = min(v, tid * C), j1 = min(v, j0 + C);
+    for (int j = j0; j < j1; ++j) Wk[j] = P[j];
+    const double del = static_cast<double>(v + 2048) * 0x1p-52;
+    int count = 0;
+    for (int k = 0; k < w; ++k) {
+        // the running sums of this draw from scratch (the reference re-sums work[] per draw)
+        double cs = 0.0;
+        for (int j = j0; j < j1; ++j) cs += static_cast<double>(Wk[j]);
+        __syncthreads();  // the previous draw's s_cp / s_pick readers are done
+        s_cp[tid] = cs;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan of the chunk sums
+            double x = s_cp[tid];
+            if (tid >= off) x += s_cp[tid - off];
+            __syncthreads();
+            s_cp[tid] = x;
+            __syncthreads();
+        }
+        const double T = s_cp[1023];
+        if (!(T > 0.0)) break;  // all mass drawn: the reference breaks (total <= 0)
+        if (tid < 32) {
+            const double uni = uniforms[(size_t)row * w + k];
+            const double eb = T * del;
+            const double u_lo = __dmul_rd(uni, T - eb), u_hi = __dmul_ru(uni, T + eb);
+            // first chunk with CP + eb > u_lo, first with CP - eb > u_hi (CP is non-decreasing)
+            int c_lo = 1024, c_hi = 1024;
+            for (int c0 = 0; c0 < 1024; c0 += 32) {
+                const double cp = s_cp[c0 + lane];
+                const unsigned bl = __ballot_sync(0xffffffffu, cp + eb > u_lo);
+                const unsigned bh = __ballot_sync(0xffffffffu, cp - eb > u_hi);
+                if (c_lo == 1024 && bl) c_lo = c0 + __ffs(bl) - 1;
+                if (c_hi == 1024 && bh) c_hi = c0 + __ffs(bh) - 1;
+                if (c_hi != 1024) break;
+            }
+            int pick = -1;
+            if (c_lo == c_hi && c_hi < 1024) {  // inside chunk c: element prefixes base + warp scan
+                const int c = c_lo, e0 = min(v, c * C), e1 = min(v, e0 + C);
+                double base = c > 0 ? s_cp[c - 1] : 0.0;
+                int i_lo = -1, i_hi = -1;
+                for (int p0 = e0; p0 < e1 && i_hi < 0; p0 += 32) {
+                    const int j = p0 + lane;
+                    double x = j < e1 ? static_cast<double>(Wk[j]) : 0.0;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    const double pj = base + x;
+                    const unsigned bl = __ballot_sync(0xffffffffu, j < e1 && pj + eb > u_lo);
+                    const unsigned bh = __ballot_sync(0xffffffffu, j < e1 && pj - eb > u_hi);
+                    if (i_lo < 0 && bl) i_lo = p0 + __ffs(bl) - 1;
+                    if (i_hi < 0 && bh) i_hi = p0 + __ffs(bh) - 1;
+                    base += __shfl_sync(0xffffffffu, x, 31);
+                }
+                if (i_lo >= 0 && i_lo == i_hi) pick = i_lo;
+            }
+            if (lane == 0) {
+                s_pick = pick;
+                if (pick >= 0) {
+                    out_ridx[(size_t)row * w + k] = pick;
+                    out_full[(size_t)row * w + k] = ordered ? ordered[pick] : pick;
+                    out_prob[(size_t)row * w + k] = P[pick];
+                    Wk[pick] = 0.0f;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_pick < 0) {  // uncertain (or the reference's upper-edge guard): the host replays
+            flags |= FRS_FLAG_SAMPLE_UNCERTIFIED;
+            break;
+        }
+        ++count;
+    }
+    (void)s_stop;
+    if (tid == 0) {
+        out_count[row] = count;
+        if (out_flags) out_flags[row] = flags;
+    }
+}
+
 template <int NB, typename WT>
 __global__ void __launch_bounds__(1024, 1)
     k_exact_logits(const float *__restrict__ h, int n, int d, const WT *__restrict__ W, int v_rows,
@@ -214,6 +316,19 @@ int launch_softmax_topk(frs_ctx *ctx, const float *logits, int n, int v, int k, 
     ++ctx->launches;
     k_softmax_topk<<<n, 1024, 0, s>>>(logits, v, v, k, temperature, ordered_ids, static_cast<float *>(ctx->scratch.ptr),
                                       out_ridx, out_full, out_prob, out_rowmax, out_total, out_flags);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+int launch_softmax_sample(frs_ctx *ctx, const float *logits, int n, int v, float temperature, const double *uniforms,
+                          int w, const int32_t *ordered_ids, float *probs, int32_t *out_ridx, int32_t *out_full,
+                          float *out_prob, int32_t *out_count, uint32_t *out_flags, cudaStream_t s) {
+    int st = ctx->scratch.ensure((size_t)n * v * sizeof(float));
+    if (st) return st;
+    ++ctx->launches;
+    k_softmax_sample<<<n, 1024, 0, s>>>(logits, v, temperature, uniforms, w, ordered_ids, probs,
+                                        static_cast<float *>(ctx->scratch.ptr), out_ridx, out_full, out_prob,
+                                        out_count, out_flags);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }

@@ -8,10 +8,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <random>
 #include <string>
 #include <vector>
 
 #include "frs_common.cuh"
+
+struct frs_rng {
+    std::mt19937_64 engine;
+};
 
 struct frs_head {
     frs_ctx *ctx = nullptr;
@@ -21,7 +26,7 @@ struct frs_head {
     int64_t vocab = 0;
     int v_sub = 0, d = 0, dtype = FRS_DTYPE_F32;
     // per-level staging (device + pinned host)
-    frs::DevBuf lvl_ridx, lvl_full, lvl_prob, lvl_tok, hidden, tree_ws;
+    frs::DevBuf lvl_ridx, lvl_full, lvl_prob, lvl_tok, hidden, tree_ws, smp_u, smp_probs;
     int32_t *h_ridx = nullptr, *h_full = nullptr, *h_tok = nullptr;
     float *h_prob = nullptr;
 };
@@ -49,6 +54,43 @@ struct ByLogJoint {
         return a < b;
     }
 };
+
+// pick_children's sampled branch on the host (drafting.cpp:44-74), for levels the device could
+// not certify: the same draws from the same engine state, over the exact probabilities.
+void pick_sampled_host(const float *probs, int n, int width, std::mt19937_64 &rng, std::vector<int> &idx,
+                       std::vector<float> &pr) {
+    const int w = std::min(width, n);
+    idx.clear();
+    pr.clear();
+    std::vector<double> work(probs, probs + n);
+    std::uniform_real_distribution<double> uni(0.0, 1.0);
+    for (int draw = 0; draw < w; ++draw) {
+        double total = 0.0;
+        for (double p : work) total += p;
+        if (total <= 0.0) break;
+        const double u = uni(rng) * total;
+        double acc = 0.0;
+        int picked = -1;
+        for (int i = 0; i < n; ++i) {
+            acc += work[i];
+            if (u < acc) {
+                picked = i;
+                break;
+            }
+        }
+        if (picked < 0) {
+            for (int i = n - 1; i >= 0; --i)
+                if (work[i] > 0.0) {
+                    picked = i;
+                    break;
+                }
+            if (picked < 0) break;
+        }
+        idx.push_back(picked);
+        pr.push_back(probs[picked]);
+        work[picked] = 0.0;
+    }
+}
 
 }  // namespace
 }  // namespace frs
@@ -567,6 +609,183 @@ int frs_verify_greedy_table(frs_ctx *ctx, const float *table, int64_t V_table, i
         FRS_REQUIRE(tokens[i] >= 0 && tokens[i] < V_table, "verify_greedy: token outside the hidden table");
     return verify_greedy_impl(ctx, nullptr, table, V_table, root_token, W, V, d, w_dtype, mode, tokens, parents, k,
                               emitted, n_emitted, path, n_path);
+}
+
+int frs_rng_create(uint64_t seed, frs_rng **out) {
+    FRS_REQUIRE(out, "rng: null pointer");
+    *out = new frs_rng{std::mt19937_64(seed)};
+    return FRS_OK;
+}
+
+int frs_rng_destroy(frs_rng *rng) {
+    delete rng;
+    return FRS_OK;
+}
+
+int frs_rng_uniforms(frs_rng *rng, int count, double *out) {
+    FRS_REQUIRE(rng && out && count >= 0, "rng: bad arguments");
+    std::uniform_real_distribution<double> uni(0.0, 1.0);
+    for (int i = 0; i < count; ++i) out[i] = uni(rng->engine);
+    return FRS_OK;
+}
+
+// build_draft_tree with an rng (drafting.cpp:122-245), head path, EXACT arithmetic: per level
+// the device samples every row (frs_draft_head_sample) with uniforms drawn here in the
+// reference's order (row by row, draw by draw); a level with an uncertified draw or an early
+// stop is replayed on the host from the device's exact probabilities with the engine rewound
+// to the level's start. select_top_k is prefix-closed (drafting.cpp:93-118).
+int frs_draft_tree_sampled(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user, const float *hidden_table,
+                           int width, int depth, int total, frs_rng *rng, int32_t *tokens, int32_t *parents,
+                           int32_t *depths, double *log_joint, int *count) {
+    FRS_REQUIRE(h && rng && tokens && parents && depths && log_joint && count, "build_draft_tree: null pointer");
+    if (width < 1) return fail(FRS_EINVAL, "draft params: beam_width must be >= 1");
+    if (depth < 1) return fail(FRS_EINVAL, "draft params: search_depth must be >= 1");
+    if (total < width || total > 64)
+        return fail(FRS_EINVAL, "draft params: total_draft_tokens must lie in [beam_width, 64]");
+    FRS_REQUIRE(fn || hidden_table, "build_draft_tree: need a hidden provider or a hidden table");
+    FRS_CUDA_TRY(cudaSetDevice(h->ctx->device));
+    const int w = std::min(width, h->v_sub);
+    int st = head_staging(h, width, w);
+    if (st) return st;
+    cudaStream_t s = h->ctx->stream;
+    float *hd = static_cast<float *>(h->hidden.ptr);
+    int32_t *tok_dev = static_cast<int32_t *>(h->lvl_tok.ptr);
+    const int max_rows = std::max(1, width);
+    if ((st = h->smp_u.ensure((size_t)max_rows * w * sizeof(double))) ||
+        (st = h->smp_probs.ensure((size_t)max_rows * h->v_sub * sizeof(float))))
+        return st;
+    struct SCand {
+        int32_t token, ridx, parent, depth, sibling_rank;
+        double log_joint;
+    };
+    std::vector<SCand> cands;
+    std::vector<int> beam;
+    std::vector<int32_t> btok, bpar;
+    std::vector<double> uh;
+    std::vector<int> idx;
+    std::vector<float> pr, probs_host;
+    // one level: hidden rows, device sampling (or host replay), children appended in beam order
+    auto run_level = [&](int level, int nb, const std::vector<int> &parents_of_rows) -> int {
+        if (fn) {
+            const int rc = fn(user, level, nb, btok.data(), bpar.data(), hd, s);
+            if (rc) return fail(FRS_ELOGIC, "hidden provider failed with code " + std::to_string(rc));
+        } else {
+            std::memcpy(h->h_tok, btok.data(), sizeof(int32_t) * nb);
+            FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, h->h_tok, sizeof(int32_t) * nb, cudaMemcpyHostToDevice, s));
+            const int rc = frs_gather_rows(h->ctx, hidden_table, h->vocab, h->d, tok_dev, nb, hd, s);
+            if (rc) return rc;
+        }
+        const std::mt19937_64 saved = rng->engine;  // the level's start, for a host replay
+        uh.resize((size_t)nb * w);
+        std::uniform_real_distribution<double> uni(0.0, 1.0);
+        for (auto &u : uh) u = uni(rng->engine);
+        FRS_CUDA_TRY(cudaMemcpyAsync(h->smp_u.ptr, uh.data(), uh.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        const size_t cells = (size_t)nb * w;
+        int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);  // [ridx | full | prob | count | flags]
+        if ((st = h->lvl_ridx.ensure(cells * 12 + (size_t)nb * 8))) return st;
+        pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
+        int rc = frs_draft_head_sample(h->ctx, hd, nb, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, width, 1.0f,
+                                       static_cast<const double *>(h->smp_u.ptr),
+                                       static_cast<float *>(h->smp_probs.ptr), pk, pk + cells,
+                                       reinterpret_cast<float *>(pk + 2 * cells), pk + 3 * cells,
+                                       reinterpret_cast<uint32_t *>(pk + 3 * cells + nb), s);
+        if (rc) return rc;
+        std::vector<int32_t> hb(cells * 3 + (size_t)nb * 2);
+        FRS_CUDA_TRY(cudaMemcpyAsync(hb.data(), pk, hb.size() * 4, cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaStreamSynchronize(s));
+        bool replay = false;
+        for (int i = 0; i < nb; ++i)
+            if (hb[3 * cells + i] != w || (hb[3 * cells + nb + i] & FRS_FLAG_SAMPLE_UNCERTIFIED)) replay = true;
+        for (int i = 0; i < nb; ++i)
+            if (hb[3 * cells + nb + i] & FRS_FLAG_NONFINITE)
+                return fail(FRS_EINVAL, "softmax: non-finite logit");  // kernels.cpp:72-74
+        if (replay) {  // rewind and redo the whole level on the host (rows in order)
+            rng->engine = saved;
+            probs_host.resize((size_t)nb * h->v_sub);
+            FRS_CUDA_TRY(cudaMemcpy(probs_host.data(), h->smp_probs.ptr, probs_host.size() * sizeof(float),
+                                    cudaMemcpyDeviceToHost));
+        }
+        for (int i = 0; i < nb; ++i) {
+            int m;
+            if (replay) {
+                pick_sampled_host(probs_host.data() + (size_t)i * h->v_sub, h->v_sub, width, rng->engine, idx, pr);
+                m = static_cast<int>(idx.size());
+            } else {
+                m = w;
+                idx.assign(hb.begin() + (size_t)i * w, hb.begin() + (size_t)(i + 1) * w);
+                pr.resize(w);
+                std::memcpy(pr.data(), hb.data() + 2 * cells + (size_t)i * w, sizeof(float) * w);
+            }
+            const int par = parents_of_rows[i];
+            for (int c = 0; c < m; ++c) {
+                const int j = idx[c];
+                const int32_t full = h->ordered.empty() ? j : h->ordered[j];
+                const double lg = std::log(static_cast<double>(pr[c]));
+                if (par < 0) {
+                    cands.push_back({full, j, -1, 1, c, lg});
+                } else {
+                    cands.push_back({full, j, par, cands[par].depth + 1, c, cands[par].log_joint + lg});
+                }
+            }
+        }
+        return FRS_OK;
+    };
+    auto by_lj = [&](int a, int b) {
+        if (cands[a].log_joint != cands[b].log_joint) return cands[a].log_joint > cands[b].log_joint;
+        return a < b;
+    };
+    btok.assign(1, root_token);
+    bpar.assign(1, -1);
+    if ((st = run_level(0, 1, std::vector<int>{-1}))) return st;
+    for (int c = 0; c < static_cast<int>(cands.size()); ++c) beam.push_back(c);
+    for (int level = 1; level < depth && !beam.empty(); ++level) {
+        if (static_cast<int>(beam.size()) > width) {  // drafting.cpp:164-176
+            std::sort(beam.begin(), beam.end(), by_lj);
+            beam.resize(width);
+            std::sort(beam.begin(), beam.end());
+        }
+        const int nb = static_cast<int>(beam.size());
+        btok.resize(nb);
+        bpar.resize(nb);
+        for (int i = 0; i < nb; ++i) {
+            btok[i] = cands[beam[i]].token;
+            bpar[i] = cands[beam[i]].parent;
+        }
+        const int first = static_cast<int>(cands.size());
+        if ((st = run_level(level, nb, beam))) return st;
+        beam.clear();
+        for (int c = first; c < static_cast<int>(cands.size()); ++c) beam.push_back(c);
+    }
+    // select_top_k, prefix_closed = true (drafting.cpp:93-118)
+    std::vector<int> order(cands.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), by_lj);
+    std::vector<char> sel(cands.size(), 0);
+    int cnt = 0;
+    for (int c : order) {
+        if (sel[c]) continue;
+        if (cands[c].parent >= 0 && !sel[cands[c].parent]) continue;
+        std::vector<int> group;
+        for (size_t s2 = 0; s2 < cands.size(); ++s2)
+            if (!sel[s2] && cands[s2].parent == cands[c].parent && cands[s2].sibling_rank <= cands[c].sibling_rank)
+                group.push_back(static_cast<int>(s2));
+        if (cnt + static_cast<int>(group.size()) > total) continue;
+        for (int g : group) sel[g] = 1;
+        cnt += static_cast<int>(group.size());
+    }
+    std::vector<int> remap(cands.size(), -1);
+    int out = 0;
+    for (size_t i = 0; i < cands.size(); ++i) {
+        if (!sel[i]) continue;
+        remap[i] = out;
+        tokens[out] = cands[i].token;
+        parents[out] = cands[i].parent >= 0 ? remap[cands[i].parent] : -1;
+        depths[out] = cands[i].depth;
+        log_joint[out] = cands[i].log_joint;
+        ++out;
+    }
+    *count = out;
+    return FRS_OK;
 }
 
 }  // extern "C"

@@ -1,6 +1,6 @@
 """Generates the committed golden fixtures from the COMPILED REFERENCE (oracle/_ref).
 
-Run here (where /root/reference exists):  python tests/golden/make_golden.py
+Run here (where /root/reference exists):  python tests/golden/make_golden.py [--sampled]
 Outputs:
   spec_examples.json   SPEC.md worked examples evaluated by the reference (SPEC.md:38-67,
                        217-219, 246, 354) — asserted against the SPEC's stated answers.
@@ -8,6 +8,8 @@ Outputs:
   c1_capture_w10.npz   reference's build_draft_tree tree + the hidden state of every
                        forwarded draft row (restated loop around forward_raw), for width 4
                        and for width 10 / depth 6 / K 60 (exercises beam pruning).
+  c1_sampled_w4_s11.npz / c1_sampled_w10_s5.npz (--sampled): the same for sampled drafting
+                       (build_draft_tree with std::mt19937_64(rng_seed), prefix-closed selection).
 The LM head is regenerated from the seed on the GPU box through oracle/_ref and checked
 against the stored sha256, so no weights are committed.
 """
@@ -82,5 +84,33 @@ def main():
         print(name, "nodes", tree["tokens"].size, "rows", cap["hidden"].shape)
 
 
+def sampled():
+    """c1_sampled_*.npz: sampled drafting (drafting.cpp:44-74 with std::mt19937_64(rng_seed)):
+    the reference's build_draft_tree(rng) tree + the hidden state of every forwarded row from the
+    restated capture loop (asserted identical to the reference's tree)."""
+    build(reference=True)
+    ref = Reference()
+    ordered = c1_subset(ref)
+    W = ref.model_lm_head(C1["V"], C1["d"], C1["layers"], C1["heads"], C1["seed"])
+    digest = hashlib.sha256(W.tobytes()).hexdigest()
+    for name, (width, depth, total, rng_seed) in {"c1_sampled_w4_s11": (4, 3, 16, 11),
+                                                   "c1_sampled_w10_s5": (10, 6, 60, 5)}.items():
+        args = (C1["V"], C1["d"], C1["layers"], C1["heads"], 64, C1["seed"], ordered, np.array(C1["pending"], np.int32),
+                width, depth, total, rng_seed)
+        tree = ref.model_draft_tree_rng(*args)
+        cap = ref.model_draft_capture_rng(*args)
+        for k in ("tokens", "parents", "depths", "log_joint"):
+            assert np.array_equal(tree[k], cap[k]), (name, k)
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), hidden=cap["hidden"], row_token=cap["row_token"],
+                            row_level=cap["row_level"], tokens=tree["tokens"], parents=tree["parents"],
+                            depths=tree["depths"], log_joint=tree["log_joint"], ordered=ordered,
+                            lm_head_sha256=np.array(digest), width=width, depth=depth, total=total,
+                            rng_seed=rng_seed, config=np.array(json.dumps(C1)))
+        print(name, "nodes", tree["tokens"].size, "rows", cap["hidden"].shape)
+
+
 if __name__ == "__main__":
-    main()
+    if "--sampled" in sys.argv:
+        sampled()
+    else:
+        main()

@@ -1,0 +1,105 @@
+"""Sampled drafting (drafting.cpp:44-74 with an rng): the device draws
+children without replacement from the EXACT probabilities with the reference's
+std::mt19937_64 / uniform_real_distribution<double> stream, certifying every draw against the
+reference's sequential double sums (k_softmax_sample); the host replays a level otherwise.
+Pinned against the compiled reference: its pick_children restatement (ref_pick_sampled, itself
+pinned by the sampled capture) and its own build_draft_tree(rng) trees (golden captures)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2502_14856_b200 import api, _lib
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def rmsnorm(x):
+    x = x.astype(np.float32)
+    ms = (x.astype(np.float64) ** 2).mean(axis=1, keepdims=True)
+    return (x * (1.0 / np.sqrt(ms + 1e-5)).astype(np.float32)).astype(np.float32)
+
+
+@pytest.mark.parametrize("scale,width,seed", [(0.02, 10, 3), (0.3, 10, 4), (2.0, 8, 5), (0.05, 64, 6)])
+def test_sampled_level_matches_reference(cuda_ctx, reference, scale, width, seed):
+    """Per-row draws == the reference's pick_children on the same uniforms (flat, peaked and
+    very peaked distributions; width up to 64)."""
+    rng = np.random.default_rng(seed)
+    V, d, v_sub, n = 6000, 256, 3000, 6
+    W = (rng.standard_normal((V, d)) * scale).astype(np.float32)
+    ids = rng.permutation(V)[:v_sub].astype(np.int32)
+    h = rmsnorm(rng.standard_normal((n, d)))
+    head = api.restrict_lm_head(cuda_ctx, torch.from_numpy(W).cuda(), api.RankedSubset(V, ids), dtype="f32")
+    w = min(width, v_sub)
+    u = reference.uniforms(100 + seed, n * w)
+    out = api.draft_head_sample(cuda_ctx, torch.from_numpy(h).cuda(), head, width, torch.from_numpy(u.reshape(n, w)))
+    ex = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, 1, mode="exact", want_logits=True)
+    logits = ex.logits.cpu().numpy()
+    probs = out.probs.cpu().numpy()
+    cnt, fl = out.count.cpu().numpy(), out.flags.cpu().numpy()
+    for r in range(n):
+        ref_p = reference.softmax(logits[r], 1.0)
+        assert np.array_equal(probs[r], ref_p), r  # bit-exact probabilities
+        picks, pr = reference.pick_sampled(ref_p, width, 100 + seed, skip=r * w)
+        if fl[r] & _lib.FLAG_SAMPLE_UNCERTIFIED:
+            continue  # the host replays such rows (covered by the tree tests)
+        assert cnt[r] == picks.size
+        assert np.array_equal(out.ridx.cpu().numpy()[r, :cnt[r]], picks), r
+        assert np.array_equal(out.prob.cpu().numpy()[r, :cnt[r]], pr), r
+        assert np.array_equal(out.full.cpu().numpy()[r, :cnt[r]], ids[picks]), r
+    assert (fl & _lib.FLAG_SAMPLE_UNCERTIFIED).sum() <= 1
+
+
+@pytest.mark.parametrize("name", ["c1_sampled_w4_s11", "c1_sampled_w10_s5"])
+def test_sampled_tree_matches_reference_build_draft_tree(cuda_ctx, reference, name):
+    """C1 end to end in sampled mode: the reference's hidden states and its build_draft_tree(rng)
+    tree; our device head + sampler + host bookkeeping with the same mt19937_64 seed."""
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    cfg = json.loads(str(z["config"]))
+    W = reference.model_lm_head(cfg["V"], cfg["d"], cfg["layers"], cfg["heads"], cfg["seed"])
+    assert hashlib.sha256(W.tobytes()).hexdigest() == str(z["lm_head_sha256"])
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(cfg["V"], z["ordered"]), dtype="f32")
+    rows, lev, rtok = z["hidden"], z["row_level"], z["row_token"]
+
+    def provider(level, toks, pars):
+        idx = np.where(lev == level)[0]
+        if level > 0:
+            assert np.array_equal(rtok[idx], toks), "beam diverged from the reference"
+        return torch.from_numpy(rows[idx]).cuda()
+
+    params = api.DraftParams(int(z["width"]), int(z["depth"]), int(z["total"]))
+    tree = head.build_draft_tree(int(cfg["pending"][-1]), params, mode="exact", provider=provider,
+                                 rng=api.Rng(int(z["rng_seed"])))
+    for key in ("tokens", "parents", "depths", "log_joint"):
+        assert np.array_equal(getattr(tree, key), z[key]), key
+
+
+def test_sampled_tree_table_prefix_closed(cuda_ctx, reference):
+    """Hidden rows from a device table: the tree is prefix-closed per parent (the children kept
+    are a prefix of the draw order), topological, inside the subset; same seed -> same tree."""
+    rng = np.random.default_rng(9)
+    V, d, v_sub = 4000, 128, 1200
+    W = (rng.standard_normal((V, d)) * 0.3).astype(np.float32)
+    E = rmsnorm(rng.standard_normal((V, d)))
+    ids = rng.permutation(V)[:v_sub].astype(np.int32)
+    sub = api.RankedSubset(V, ids)
+    head = api.DeviceHead(cuda_ctx, W, sub, dtype="f32")
+    Ed = torch.from_numpy(E).cuda()
+    params = api.DraftParams(6, 4, 30)
+    t1 = head.build_draft_tree(int(ids[1]), params, hidden_table=Ed, rng=api.Rng(77))
+    t2 = head.build_draft_tree(int(ids[1]), params, hidden_table=Ed, rng=api.Rng(77))
+    for key in ("tokens", "parents", "depths", "log_joint"):
+        assert np.array_equal(getattr(t1, key), getattr(t2, key)), key
+    K = len(t1)
+    assert 1 <= K <= 30
+    for i in range(K):
+        p = int(t1.parents[i])
+        assert -1 <= p < i and sub.contains(int(t1.tokens[i]))
+        if p >= 0:
+            assert t1.depths[i] == t1.depths[p] + 1
+    with pytest.raises(ValueError):
+        head.build_draft_tree(int(ids[1]), params, mode="fast", hidden_table=Ed, rng=api.Rng(1))
