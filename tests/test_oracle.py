@@ -124,3 +124,28 @@ def test_headpath_tree_matches_reference_build_draft_tree(restatement, reference
     t = restatement.draft_tree(provider, slab, z["ordered"], int(z["width"]), int(z["depth"]), int(z["total"]))
     for k in ("tokens", "parents", "depths", "log_joint"):
         assert np.array_equal(t[k], z[k]), k
+
+
+@pytest.mark.parametrize("width,depth,total,seed", [(3, 3, 9, 1), (5, 4, 20, 2)])
+def test_sampled_capture_matches_reference_build_draft_tree(reference, width, depth, total, seed):
+    """The sampled capture loop (pick_children's sampled branch restated in the shim, prefix-closed
+    select_top_k) reproduces the reference's own build_draft_tree(rng) — this pins
+    ref_pick_sampled, the checker of the device sampler (tests/test_gpu_sampled.py)."""
+    rng = np.random.default_rng(seed)
+    V, d = 2000, 64
+    ordered = rng.permutation(V)[:700].astype(np.int32)
+    args = (V, d, 1, 4, 64, 7 + seed, ordered, np.array([5, 17, 300], np.int32), width, depth, total, 900 + seed)
+    tree = reference.model_draft_tree_rng(*args)
+    cap = reference.model_draft_capture_rng(*args)
+    for k in ("tokens", "parents", "depths", "log_joint"):
+        assert np.array_equal(tree[k], cap[k]), k
+
+
+def test_sampled_goldens_consistent(reference):
+    """The committed sampled goldens are prefix-closed trees of the stated size."""
+    for name in ("c1_sampled_w4_s11", "c1_sampled_w10_s5"):
+        z = np.load(os.path.join(GOLDEN, name + ".npz"))
+        par, dep = z["parents"], z["depths"]
+        assert par.size == int(z["total"])
+        for i, p in enumerate(par):
+            assert -1 <= p < i and (p < 0 or dep[i] == dep[p] + 1)
