@@ -56,27 +56,37 @@ __global__ void __launch_bounds__(1024)
     __shared__ int s_pick, s_stop;
     const int C = (v + 1023) / 1024, j0 = min(v, tid * C), j1 = min(v, j0 + C);
     for (int j = j0; j < j1; ++j) Wk[j] = P[j];
-    const double del = static_cast<double>(v + 2048) * 0x1p-52;
+    // Prefix bookkeeping: a fresh scan (chunk sums + block scan) is within errP = 2^-46 T of the
+    // exact prefix; each later pick is subtracted in place (one rounding each, errP grows by
+    // 2^-52 T). The reference's running sums are within (v + 64) 2^-53 T of the exact ones.
+    // Rescan when the remaining mass halves, so the bounds stay relative to it.
+    double errP = 0.0, t_scan = 0.0;
+    bool need_scan = true;
+    __shared__ int s_pchunk;
     int count = 0;
     for (int k = 0; k < w; ++k) {
-        // the running sums of this draw from scratch (the reference re-sums work[] per draw)
-        double cs = 0.0;
-        for (int j = j0; j < j1; ++j) cs += static_cast<double>(Wk[j]);
-        __syncthreads();  // the previous draw's s_cp / s_pick readers are done
-        s_cp[tid] = cs;
-        __syncthreads();
-        for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan of the chunk sums
-            double x = s_cp[tid];
-            if (tid >= off) x += s_cp[tid - off];
+        if (need_scan) {
+            double cs = 0.0;
+            for (int j = j0; j < j1; ++j) cs += static_cast<double>(Wk[j]);
+            __syncthreads();  // readers of the previous s_cp are done
+            s_cp[tid] = cs;
             __syncthreads();
-            s_cp[tid] = x;
-            __syncthreads();
+            for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan of the chunk sums
+                double x = s_cp[tid];
+                if (tid >= off) x += s_cp[tid - off];
+                __syncthreads();
+                s_cp[tid] = x;
+                __syncthreads();
+            }
+            t_scan = s_cp[1023];
+            errP = t_scan * 0x1p-46;
+            need_scan = false;
         }
         const double T = s_cp[1023];
         if (!(T > 0.0)) break;  // all mass drawn: the reference breaks (total <= 0)
         if (tid < 32) {
             const double uni = uniforms[(size_t)row * w + k];
-            const double eb = T * del;
+            const double eb = errP + static_cast<double>(v + 64) * 0x1p-53 * T;
             const double u_lo = __dmul_rd(uni, T - eb), u_hi = __dmul_ru(uni, T + eb);
             // first chunk with CP + eb > u_lo, first with CP - eb > u_hi (CP is non-decreasing)
             int c_lo = 1024, c_hi = 1024;
@@ -112,6 +122,7 @@ __global__ void __launch_bounds__(1024)
             }
             if (lane == 0) {
                 s_pick = pick;
+                s_pchunk = c_lo;
                 if (pick >= 0) {
                     out_ridx[(size_t)row * w + k] = pick;
                     out_full[(size_t)row * w + k] = ordered ? ordered[pick] : pick;
@@ -126,6 +137,11 @@ __global__ void __launch_bounds__(1024)
             break;
         }
         ++count;
+        // subtract the drawn mass from the prefixes at and after its chunk
+        if (tid >= s_pchunk) s_cp[tid] -= static_cast<double>(P[s_pick]);
+        errP += T * 0x1p-52;
+        __syncthreads();
+        need_scan = s_cp[1023] < 0.5 * t_scan;
     }
     (void)s_stop;
     if (tid == 0) {

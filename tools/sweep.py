@@ -6,6 +6,7 @@ headline bench line does not carry:
   verify  : FAST verify head (argmax over the full vocabulary) at C2 (61 rows, V=128256,
             d=4096) and the C4 Qwen-2.5-7B shape split into 1/2/4/8 contiguous vocabulary
             shards (per-shard device time = what one GPU of a vocab-parallel group spends)
+  sampled : sampled drafting (EXACT arithmetic) — one level and a whole sampled tree
   decode  : head-path decode loop: build_draft_tree (6 levels, width 10,
             60 tokens, hidden state = identity draft layer over an embedding table) +
             verify_greedy over the full head, tokens/s and mean accepted length
@@ -167,9 +168,38 @@ def decode_loop(ctx, dev, iters):
                       "ms_draft_tree": 1000 * t_tree / iters, "ms_verify": 1000 * t_ver / iters}), flush=True)
 
 
+def sampled_draft(ctx, dev, iters=20):
+    """Sampled drafting (drafting.cpp:44-74, EXACT arithmetic) at C2: one 10-row level of
+    k_exact_logits + k_softmax_sample, and a whole sampled tree (6 levels, width 10, 60 tokens)."""
+    d, V, v_sub, n, w = 4096, 128256, 32768, 10, 10
+    g = torch.Generator(device=dev).manual_seed(1234)
+    W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16).float()
+    ranked = np.random.default_rng(1234).permutation(V).astype(np.int32)
+    sub = api.subset_from_ranking(ranked, v_sub, V, forced=[0, 1])
+    head = api.restrict_lm_head(ctx, W, sub, dtype="bf16")
+    dh = api.DeviceHead(ctx, W, sub, dtype="bf16")
+    E = rms(torch.randn(V, d, generator=g, device=dev))
+    del W
+    h = rms(torch.randn(n, d, generator=g, device=dev))
+    rng = api.Rng(2024)
+    u = torch.from_numpy(rng.uniforms(n * w).reshape(n, w)).to(dev)
+    us = timed(lambda i: api.draft_head_sample(ctx, h, head, w, u), iters)
+    out = api.draft_head_sample(ctx, h, head, w, u)
+    unc = int(((out.flags.cpu().numpy() & 0x80) != 0).sum())
+    dh.build_draft_tree(1, api.DraftParams(10, 6, 60), mode="exact", hidden_table=E, rng=rng)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(5):
+        dh.build_draft_tree(2 + i, api.DraftParams(10, 6, 60), mode="exact", hidden_table=E, rng=rng)
+    ms = (time.perf_counter() - t0) * 1000 / 5
+    print(json.dumps({"sweep": "sampled_draft", "v_sub": v_sub, "d": d, "rows": n, "width": w,
+                      "us_per_level_exact_sampled": us, "rows_uncertified_last_level": unc,
+                      "ms_per_sampled_tree_6x10_60": ms}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="draft,batched,verify,decode")
+    ap.add_argument("--what", default="draft,batched,verify,decode,sampled")
     ap.add_argument("--exact", action="store_true", help="also time the EXACT draft level")
     ap.add_argument("--decode-iters", type=int, default=100)
     a = ap.parse_args()
@@ -184,6 +214,8 @@ def main():
         verify_sweep(ctx, dev)
     if "decode" in what:
         decode_loop(ctx, dev, a.decode_iters)
+    if "sampled" in what:
+        sampled_draft(ctx, dev)
 
 
 if __name__ == "__main__":
