@@ -200,6 +200,18 @@ FRS_API int frs_draft_tree_sampled(frs_head *head, int32_t root_token, frs_hidde
                                    const float *hidden_table, int width, int depth, int total, frs_rng *rng,
                                    int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint,
                                    int *count);
+/* verify_stochastic (verification.cpp:76-178): h_dev holds 1 + k target rows (root first),
+ * W the full target head [V x d]. The device computes the EXACT target logits and softmax
+ * probabilities (kernels.cpp:13-32, 62-91); the residual walk (accept with probability
+ * min(1, p/q), p <- norm(max(0, p - q)) on rejection, bonus token from the residual) runs on the
+ * host in the reference's double arithmetic over those probabilities, drawing from rng. The
+ * draft distributions: q_root [v_sub], q_nodes [k x v_sub] with has_q[i] = 0 for nodes that
+ * were not expanded; ordered (host, v_sub ids) maps draft indices to tokens (NULL: identity). */
+FRS_API int frs_verify_stochastic(frs_ctx *ctx, const float *h_dev, const void *W, int V, int d, int w_dtype,
+                                  const int32_t *tokens, const int32_t *parents, int k, const float *q_root,
+                                  int v_sub, const float *q_nodes, const int32_t *has_q, const int32_t *ordered,
+                                  float temperature, frs_rng *rng, int32_t *emitted, int *n_emitted, int32_t *path,
+                                  int *n_path);
 /* verify_greedy (verification.cpp:42-71) with the target head on the device: h_dev holds
  * 1 + k rows (root first), W the full LM head [V x d] (device). Host outputs. */
 FRS_API int frs_verify_greedy(frs_ctx *ctx, const float *h_dev, const void *W, int V, int d, int w_dtype,

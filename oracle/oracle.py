@@ -246,6 +246,8 @@ class Reference:
                                                                   _i32p, _ip, _i32p, _i32p, _i32p, _f64p, _ip]
         L.ref_pick_sampled.argtypes = [_f32p, C.c_int, C.c_int, C.c_uint64, C.c_int64, _i32p, _f32p, _ip]
         L.ref_uniforms.argtypes = [C.c_uint64, C.c_int64, C.c_int, _f64p]
+        L.ref_verify_stochastic.argtypes = [_f32p, C.c_int, _f32p, C.c_int, _i32p, _i32p, _f32p, C.c_int, _f32p, _i32p,
+                                            C.c_void_p, C.c_float, C.c_uint64, _i32p, _ip, _i32p, _ip]
 
     def _check(self, rc: int, what: str):
         if rc:
@@ -406,6 +408,21 @@ class Reference:
         return dict(hidden=hid[:r].copy(), row_token=rtok[:r].copy(), row_level=rlev[:r].copy(),
                     tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(),
                     log_joint=lj[:n].copy())
+
+    def verify_stochastic(self, root_logits, node_logits, tokens, parents, q_root, q_nodes, has_q, ordered,
+                          temperature, rng_seed):
+        rl, nl = _c32(root_logits), _c32(node_logits)
+        k = nl.shape[0]
+        tok, par = _ci32(tokens), _ci32(parents)
+        qr, qn, hq = _c32(q_root), _c32(q_nodes), _ci32(has_q)
+        o = None if ordered is None else _ci32(ordered)
+        em, pa = np.empty(70, np.int32), np.empty(70, np.int32)
+        ne, npth = C.c_int(), C.c_int()
+        self._check(self.lib.ref_verify_stochastic(rl, rl.size, nl, k, tok, par, qr, qr.size, qn, hq,
+                                                   None if o is None else o.ctypes.data, temperature,
+                                                   C.c_uint64(rng_seed), em, C.byref(ne), pa, C.byref(npth)),
+                    "verify_stochastic")
+        return em[:ne.value].copy(), pa[:npth.value].copy()
 
     def uniforms(self, seed, count, skip=0):
         out = np.empty(count, np.float64)

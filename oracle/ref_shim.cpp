@@ -230,6 +230,37 @@ int ref_verify_greedy(const float * root_logits, int V, const float * node_logit
     });
 }
 
+// verify_stochastic (verification.cpp:76-178) of the compiled reference. q_root [v_sub] and
+// q_nodes [k][v_sub] are the draft distributions (node rows with has_q[i] == 0 are empty, as
+// for unexpanded nodes); ordered (v_sub ids) is the drafting subset (NULL: full vocabulary).
+int ref_verify_stochastic(const float * root_logits, int V, const float * node_logits, int k,
+                          const int32_t * tokens, const int32_t * parents, const float * q_root, int v_sub,
+                          const float * q_nodes, const int32_t * has_q, const int32_t * ordered,
+                          float temperature, uint64_t rng_seed, int32_t * emitted, int * n_emitted,
+                          int32_t * path, int * n_path) {
+    return guarded([&] {
+        DraftResult dr;
+        dr.tree = tree_from(tokens, parents, nullptr, k);
+        dr.root_probs.assign(q_root, q_root + v_sub);
+        dr.node_probs.resize(k);
+        for (int i = 0; i < k; ++i)
+            if (has_q[i]) dr.node_probs[i].assign(q_nodes + static_cast<size_t>(i) * v_sub,
+                                                  q_nodes + static_cast<size_t>(i + 1) * v_sub);
+        std::shared_ptr<const RankedSubset> sub;
+        if (ordered) {
+            std::vector<Token> ids(ordered, ordered + v_sub);
+            sub = std::make_shared<const RankedSubset>(subset_from_ranking(ids, v_sub, V, {}));
+        }
+        std::mt19937_64 rng(rng_seed);
+        VerifyOutcome o = verify_stochastic(std::span<const float>(root_logits, V), to_matrix(node_logits, k, V), dr,
+                                            sub.get(), temperature, rng);
+        *n_emitted = static_cast<int>(o.emitted.size());
+        *n_path = static_cast<int>(o.accepted_path.size());
+        std::copy(o.emitted.begin(), o.emitted.end(), emitted);
+        std::copy(o.accepted_path.begin(), o.accepted_path.end(), path);
+    });
+}
+
 // A persistent reference Matrix for timing the reference's own draft level without per-call
 // copies of the head (the CPU baseline in bench.py).
 void * ref_head_new(const float * W, int rows, int d) { return new Matrix(to_matrix(W, rows, d)); }

@@ -89,6 +89,8 @@ SIGNATURES = [
     ("frs_rng_destroy", _I, [_P]),
     ("frs_rng_uniforms", _I, [_P, _I, _P]),
     ("frs_draft_head_sample", _I, [_P, _P, _I, _I, _P, _I, _I, _P, _I, C.c_float, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("frs_verify_stochastic", _I, [_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _I, _P, _P, _P, C.c_float, _P, _P,
+                                   C.POINTER(_I), _P, C.POINTER(_I)]),
     ("frs_draft_tree_sampled", _I, [_P, C.c_int32, HIDDEN_FN, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P,
                                     C.POINTER(_I)]),
     ("frs_verify_greedy", _I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P, C.POINTER(_I)]),

@@ -521,6 +521,29 @@ def verify_greedy(ctx: Context, h_dev: torch.Tensor, lm_head: torch.Tensor, tree
     return VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy())
 
 
+def verify_stochastic(ctx: Context, h_dev: torch.Tensor, lm_head: torch.Tensor, tree: DraftTree, q_root,
+                      q_nodes, has_q, ordered, rng: "Rng", temperature: float = 1.0) -> VerifyOutcome:
+    """verification.cpp:76-178: exact target probabilities on the device (rows of h_dev: root
+    first, then one per node), the reference's residual walk on the host with ``rng``. q_root
+    [v_sub] / q_nodes [K, v_sub] / has_q [K]: the draft distributions (DraftResult root_probs /
+    node_probs; has_q[i] = 0 where node i was not expanded); ordered: the drafting subset's ids
+    (None: the draft head is the full vocabulary)."""
+    k = len(tree)
+    dt = DTYPE_BF16 if lm_head.dtype == torch.bfloat16 else DTYPE_F32
+    qr = np.ascontiguousarray(q_root, np.float32)
+    qn = np.ascontiguousarray(q_nodes, np.float32).reshape(k, qr.size) if k else np.zeros((1, qr.size), np.float32)
+    hq = _i32(has_q) if k else np.zeros(1, np.int32)
+    od = None if ordered is None else _i32(ordered)
+    em, path = np.empty(k + 1, np.int32), np.empty(max(k, 1), np.int32)
+    ne, npth = C.c_int(), C.c_int()
+    tok, par = _i32(tree.tokens), _i32(tree.parents)
+    check(lib().frs_verify_stochastic(ctx.handle, _ptr(h_dev.contiguous()), _ptr(lm_head), lm_head.shape[0],
+                                      lm_head.shape[1], dt, _np_ptr(tok), _np_ptr(par), k, _np_ptr(qr), qr.size,
+                                      _np_ptr(qn), _np_ptr(hq), _np_ptr(od), C.c_float(temperature), rng.handle,
+                                      _np_ptr(em), C.byref(ne), _np_ptr(path), C.byref(npth)), "verify_stochastic")
+    return VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy())
+
+
 def verify_greedy_table(ctx: Context, table: torch.Tensor, root_token: int, lm_head: torch.Tensor, tree: DraftTree,
                         mode="exact") -> VerifyOutcome:
     """verify_greedy with hidden rows gathered on the device from table[V x d] (CUDA float32)

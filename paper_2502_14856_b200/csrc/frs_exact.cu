@@ -32,6 +32,17 @@ __device__ __forceinline__ float load_w(const __nv_bfloat16 *p) {
     return __uint_as_float(static_cast<uint32_t>(u) << 16);  // bf16 -> fp32 is exact
 }
 
+// One CTA per row: the exact softmax probabilities (kernels.cpp:62-91) of full-vocabulary
+// target logits (verify_stochastic's Residual::init, verification.cpp:80-87); flags per row.
+__global__ void __launch_bounds__(1024)
+    k_softmax_probs_rows(const float *__restrict__ logits, int v, float temperature, float *__restrict__ probs,
+                         uint32_t *__restrict__ out_flags) {
+    __shared__ dev::ReduceScratch rs;
+    const int row = blockIdx.x;
+    const uint32_t flags = dev::softmax_probs_row(logits + (size_t)row * v, v, temperature, probs + (size_t)row * v, rs);
+    if (threadIdx.x == 0) out_flags[row] = flags;
+}
+
 // Sampled pick_children (drafting.cpp:44-74) for each row: exact probabilities (kernels.cpp:
 // 62-91, softmax_probs_row) into probs[row], then w draws without replacement with the caller's
 // uniforms (std::uniform_real_distribution<double> of the reference's mt19937_64, in draw
@@ -345,6 +356,14 @@ int launch_softmax_sample(frs_ctx *ctx, const float *logits, int n, int v, float
     k_softmax_sample<<<n, 1024, 0, s>>>(logits, v, temperature, uniforms, w, ordered_ids, probs,
                                         static_cast<float *>(ctx->scratch.ptr), out_ridx, out_full, out_prob,
                                         out_count, out_flags);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+int launch_softmax_probs(frs_ctx *ctx, const float *logits, int n, int v, float temperature, float *probs,
+                         uint32_t *flags, cudaStream_t s) {
+    ++ctx->launches;
+    k_softmax_probs_rows<<<n, 1024, 0, s>>>(logits, v, temperature, probs, flags);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }

@@ -788,4 +788,130 @@ int frs_draft_tree_sampled(frs_head *h, int32_t root_token, frs_hidden_fn fn, vo
     return FRS_OK;
 }
 
+int frs_verify_stochastic(frs_ctx *ctx, const float *h_dev, const void *W, int V, int d, int w_dtype,
+                          const int32_t *tokens, const int32_t *parents, int k, const float *q_root, int v_sub,
+                          const float *q_nodes, const int32_t *has_q, const int32_t *ordered, float temperature,
+                          frs_rng *rng, int32_t *emitted, int *n_emitted, int32_t *path, int *n_path) {
+    FRS_REQUIRE(ctx && h_dev && W && rng && q_root && emitted && n_emitted && path && n_path,
+                "verify_stochastic: null pointer");
+    FRS_REQUIRE(k >= 0 && (k == 0 || (tokens && parents && q_nodes && has_q)), "verify_stochastic: bad tree");
+    if (k > 64) return fail(FRS_ECAPACITY, "build_tree_mask: nodes exceed the 64-bit mask");
+    for (int i = 0; i < k; ++i)
+        if (parents[i] >= i || parents[i] < -1) return fail(FRS_EINVAL, "verify_stochastic: tree is not topological");
+    FRS_REQUIRE(std::isfinite(temperature) && temperature > 0.0f, "softmax: temperature must be positive and finite");
+    FRS_REQUIRE(V >= 1 && d >= 1 && v_sub >= 1, "verify_stochastic: sizes must be positive");
+    FRS_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int rows = 1 + k;
+    int st;
+    if ((st = ctx->logits.ensure((size_t)rows * V * sizeof(float))) ||
+        (st = ctx->scratch.ensure((size_t)rows * V * sizeof(float) + 64 * sizeof(uint32_t) + 256)))
+        return st;
+    float *logits = static_cast<float *>(ctx->logits.ptr), *probs = static_cast<float *>(ctx->scratch.ptr);
+    uint32_t *fl = reinterpret_cast<uint32_t *>(probs + (size_t)rows * V);
+    if ((st = launch_exact_logits(ctx, h_dev, rows, d, W, w_dtype, V, logits, s))) return st;
+    if ((st = launch_softmax_probs(ctx, logits, rows, V, temperature, probs, fl, s))) return st;
+    std::vector<uint32_t> hfl(rows);
+    FRS_CUDA_TRY(cudaMemcpyAsync(hfl.data(), fl, rows * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int r = 0; r < rows; ++r)
+        if (hfl[r] & FRS_FLAG_NONFINITE) return fail(FRS_EINVAL, "softmax: non-finite logit");  // kernels.cpp:72-74
+    std::vector<float> prow(V);
+    auto fetch = [&](int r) -> int {  // the exact probabilities of target row r (0 = root)
+        FRS_CUDA_TRY(cudaMemcpy(prow.data(), probs + (size_t)r * V, sizeof(float) * V, cudaMemcpyDeviceToHost));
+        return FRS_OK;
+    };
+    // children_by_node (verification.cpp:31-38)
+    std::vector<std::vector<int>> kids(k + 1);
+    for (int i = 0; i < k; ++i) kids[parents[i] + 1].push_back(i);
+    std::vector<int32_t> full_to_r;
+    if (ordered) {
+        full_to_r.assign(V, -1);
+        for (int j = 0; j < v_sub; ++j)
+            if (ordered[j] >= 0 && ordered[j] < V) full_to_r[ordered[j]] = j;
+    }
+    // Residual (verification.cpp:76-128) in the reference's double arithmetic
+    std::vector<double> p;
+    double total = 1.0;
+    auto init = [&](int r) -> int {
+        if ((st = fetch(r))) return st;
+        p.assign(prow.begin(), prow.end());
+        total = 0.0;
+        for (double x : p) total += x;
+        return FRS_OK;
+    };
+    auto subtract = [&](const std::vector<double> &q, double q_total) {
+        for (int j = 0; j < static_cast<int>(q.size()); ++j) {
+            if (q[j] <= 0.0) continue;
+            const int t = ordered ? ordered[j] : j;
+            p[t] = std::max(0.0, p[t] - (q[j] / q_total) * total);
+        }
+        double sum = 0.0;
+        for (double x : p) sum += x;
+        if (sum <= 0.0) {
+            p.assign(p.size(), 1.0);
+            sum = static_cast<double>(p.size());
+        }
+        for (double &x : p) x /= sum;
+        total = 1.0;
+    };
+    auto sample = [&]() -> int32_t {
+        std::uniform_real_distribution<double> uni(0.0, 1.0);
+        const double u = uni(rng->engine) * total;
+        double acc = 0.0;
+        int32_t last_positive = 0;
+        for (size_t t = 0; t < p.size(); ++t) {
+            if (p[t] <= 0.0) continue;
+            acc += p[t];
+            last_positive = static_cast<int32_t>(t);
+            if (u < acc) return last_positive;
+        }
+        return last_positive;
+    };
+    std::uniform_real_distribution<double> uni(0.0, 1.0);
+    std::vector<int32_t> em, pa;
+    if ((st = init(0))) return st;
+    int node = -1;
+    for (;;) {
+        const auto &ch = kids[node + 1];
+        int accepted = -1;
+        if (!ch.empty()) {
+            if (node >= 0 && !has_q[node])
+                return fail(FRS_ELOGIC, "verify_stochastic: expanded node is missing its draft distribution");
+            const float *qs = node < 0 ? q_root : q_nodes + (size_t)node * v_sub;
+            std::vector<double> q(qs, qs + v_sub);
+            double q_total = 0.0;
+            for (double x : q) q_total += x;
+            for (int child : ch) {
+                const int32_t t = tokens[child];
+                const int j = ordered ? (t >= 0 && t < V ? full_to_r[t] : -1) : t;
+                if (j < 0 || j >= v_sub || q[j] <= 0.0 || q_total <= 0.0)
+                    return fail(FRS_ELOGIC, "verify_stochastic: drafted token has zero draft probability");
+                const double q_t = q[j] / q_total;
+                const double ratio = (p[t] / total) / q_t;
+                if (uni(rng->engine) < std::min(1.0, ratio)) {
+                    accepted = child;
+                    break;
+                }
+                subtract(q, q_total);
+                q_total -= q[j];
+                q[j] = 0.0;
+            }
+        }
+        if (accepted < 0) {
+            em.push_back(sample());  // bonus token
+            break;
+        }
+        pa.push_back(accepted);
+        em.push_back(tokens[accepted]);
+        node = accepted;
+        if ((st = init(1 + accepted))) return st;
+    }
+    *n_emitted = static_cast<int>(em.size());
+    *n_path = static_cast<int>(pa.size());
+    std::copy(em.begin(), em.end(), emitted);
+    std::copy(pa.begin(), pa.end(), path);
+    return FRS_OK;
+}
+
 }  // extern "C"

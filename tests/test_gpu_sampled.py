@@ -103,3 +103,63 @@ def test_sampled_tree_table_prefix_closed(cuda_ctx, reference):
             assert t1.depths[i] == t1.depths[p] + 1
     with pytest.raises(ValueError):
         head.build_draft_tree(int(ids[1]), params, mode="fast", hidden_table=Ed, rng=api.Rng(1))
+
+
+def _softmax64(x):
+    x = x.astype(np.float64)
+    e = np.exp(x - x.max())
+    return (e / e.sum()).astype(np.float32)
+
+
+@pytest.mark.parametrize("seed,scale,temperature", [(1, 0.05, 1.0), (2, 0.3, 1.0), (3, 0.3, 0.7), (4, 1.5, 1.0)])
+def test_verify_stochastic_matches_reference(cuda_ctx, reference, seed, scale, temperature):
+    """verification.cpp:76-178 end to end: exact target probabilities on the device + the
+    residual walk; emitted tokens and accepted path == the reference's verify_stochastic on
+    the same logits, draft distributions, subset and mt19937_64 seed. Targets correlated with
+    the drafts so paths get accepted as well as rejected."""
+    rng = np.random.default_rng(seed)
+    V, d, v_sub, k = 3000, 128, 900, 20
+    W = (rng.standard_normal((V, d)) * scale).astype(np.float32)
+    ordered = rng.permutation(V)[:v_sub].astype(np.int32)
+    parents = np.array([-1, -1, -1, 0, 0, 1, 3, 3, 4, 6, 6, 2, 2, 11, 9, 9, 14, 7, 7, 17], np.int32)
+    # draft distributions over the subset; tokens drawn from them (so q > 0)
+    q_root = _softmax64(rng.standard_normal(v_sub) * 3.0)
+    q_nodes = np.stack([_softmax64(rng.standard_normal(v_sub) * 3.0) for _ in range(k)])
+    has_q = np.zeros(k, np.int32)
+    has_q[np.unique(parents[parents >= 0])] = 1
+    tokens = np.empty(k, np.int32)
+    for i in range(k):
+        q = q_root if parents[i] < 0 else q_nodes[parents[i]]
+        sib = tokens[:i][parents[:i] == parents[i]]
+        order = np.argsort(-q, kind="stable")
+        cand = [int(ordered[j]) for j in order[:8] if int(ordered[j]) not in sib]
+        tokens[i] = cand[rng.integers(0, 3)]
+    h = rmsnorm(rng.standard_normal((1 + k, d)))
+    # align about half of the target rows with one of their drafted children (that child then
+    # carries most of the target mass: accepted), leave the others random (rejections)
+    for row in range(1 + k):
+        kids = np.where(parents == row - 1)[0]
+        if kids.size and rng.random() < 0.6:
+            t = tokens[kids[rng.integers(0, kids.size)]]
+            h[row] = (12.0 / (np.linalg.norm(W[t]) + 1e-6)) * W[t] / (np.linalg.norm(W[t]) + 1e-6) * np.float32(
+                min(1.0, 1.0 / scale))
+    Wd = torch.from_numpy(W).cuda()
+    tree = api.DraftTree(tokens, parents, np.ones(k, np.int32), np.zeros(k))
+    logits = reference.matmul(h, W)  # the reference's dot_f32 logits
+    for rs in (11, 12, 13):
+        out = api.verify_stochastic(cuda_ctx, torch.from_numpy(h).cuda(), Wd, tree, q_root, q_nodes, has_q, ordered,
+                                    api.Rng(1000 * seed + rs), temperature)
+        em, path = reference.verify_stochastic(logits[0], logits[1:], tokens, parents, q_root, q_nodes, has_q,
+                                               ordered, temperature, 1000 * seed + rs)
+        assert np.array_equal(out.emitted, em) and np.array_equal(out.accepted_path, path), rs
+        _LENS.append(int(path.size))
+
+
+_LENS = []
+
+
+def test_verify_stochastic_paths_cover_accept_and_reject():
+    """The parity cases above covered both outcomes: rejected at the root and accepted paths."""
+    if not _LENS:
+        pytest.skip("parity cases did not run")
+    assert min(_LENS) == 0 and max(_LENS) >= 2, _LENS
