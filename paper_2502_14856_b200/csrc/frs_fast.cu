@@ -720,6 +720,7 @@ struct FinArgs {
     int ablate;                      // DIAGNOSTIC ONLY (FRS_ABLATE): skip finalize phases for timing
     int fin_ctas;                    // finalize cluster width (power of 2, <= kFinCtas): 8 draft, 2 verify
     int fin_stage;                   // candidates staged per round (<= kFinStage): 8 draft, 4 verify
+    int surv_eps;                    // finalize survivor window (units of eps below the row max)
     unsigned long long *fb_arrive;   // monotonic CTA arrival counter of k_fast_fallback
 };
 
@@ -1059,7 +1060,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     const float eps = static_cast<float>(sqrt(h2) * sqrt(static_cast<double>(W2) * 1.001)) * fast_gamma(A.d) * 1.01f;
     // coarse filter: the keys within 16 eps of the row max (typically ~30 per row) are the only
     // ones that can matter unless the top-k is spread wider (then the histogram path below)
-    const float t0 = M - 16.0f * eps - (fabsf(M) * 0x1p-18f + 0x1p-20f);
+    const float t0 = M - static_cast<float>(A.surv_eps) * eps - (fabsf(M) * 0x1p-18f + 0x1p-20f);
     {
         float a_far = kNegInf;
 #pragma unroll
@@ -2327,6 +2328,8 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
     static const int fin_env = std::getenv("FRS_FIN_CTAS") ? std::atoi(std::getenv("FRS_FIN_CTAS")) : 0;  // DIAGNOSTIC
     A.fin_ctas = argmax ? 2 : (fin_env == 2 || fin_env == 4 ? fin_env : kFinCtas);  // argmax rows: ~1-3 candidates
     A.fin_stage = argmax ? 4 : kFinStage;
+    static const int surv_env = std::getenv("FRS_SURV_EPS") ? std::atoi(std::getenv("FRS_SURV_EPS")) : 0;  // DIAGNOSTIC
+    A.surv_eps = surv_env >= 4 ? surv_env : 16;
     return launch_fin(ctx, A, n, s);
 }
 
