@@ -7,6 +7,7 @@ headline bench line does not carry:
             d=4096) and the C4 Qwen-2.5-7B shape split into 1/2/4/8 contiguous vocabulary
             shards (per-shard device time = what one GPU of a vocab-parallel group spends)
   sampled : sampled drafting (EXACT arithmetic) — one level and a whole sampled tree
+  stochastic: verify_stochastic at C2 (exact target probabilities + the residual walk)
   decode  : head-path decode loop: build_draft_tree (6 levels, width 10,
             60 tokens, hidden state = identity draft layer over an embedding table) +
             verify_greedy over the full head, tokens/s and mean accepted length
@@ -197,9 +198,41 @@ def sampled_draft(ctx, dev, iters=20):
                       "ms_per_sampled_tree_6x10_60": ms}), flush=True)
 
 
+def stochastic_verify(ctx, dev, iters=5):
+    """verify_stochastic at C2 (verification.cpp:76-178): 61 target rows over V = 128256 (fp32
+    head: the exact path's dtype), a synthetic sampled draft (tree of 60 nodes, q over V_sub)."""
+    d, V, v_sub, k = 4096, 128256, 32768, 60
+    g = torch.Generator(device=dev).manual_seed(99)
+    W = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16).float()
+    rs = np.random.default_rng(99)
+    ordered = rs.permutation(V)[:v_sub].astype(np.int32)
+    parents = np.array([-1] * 10 + [i // 10 for i in range(50)], np.int32)
+    q_root = rs.dirichlet(np.ones(v_sub)).astype(np.float32)
+    q_nodes = rs.dirichlet(np.ones(v_sub), size=k).astype(np.float32)
+    has_q = np.zeros(k, np.int32)
+    has_q[:10] = 1
+    tokens = np.empty(k, np.int32)
+    for i in range(k):
+        q = q_root if parents[i] < 0 else q_nodes[parents[i]]
+        top = np.argsort(-q)[:20]
+        tokens[i] = ordered[top[i % 10]]
+    h = rms(torch.randn(1 + k, d, generator=g, device=dev))
+    tree = api.DraftTree(tokens, parents, np.ones(k, np.int32), np.zeros(k))
+    rng = api.Rng(5)
+    api.verify_stochastic(ctx, h, W, tree, q_root, q_nodes, has_q, ordered, rng)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    lens = []
+    for _ in range(iters):
+        lens.append(len(api.verify_stochastic(ctx, h, W, tree, q_root, q_nodes, has_q, ordered, rng).accepted_path))
+    ms = (time.perf_counter() - t0) * 1000 / iters
+    print(json.dumps({"sweep": "verify_stochastic", "rows": 1 + k, "d": d, "vocab": V, "v_sub": v_sub,
+                      "head_dtype": "f32", "ms_per_call": ms, "accepted_lengths": lens}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="draft,batched,verify,decode,sampled")
+    ap.add_argument("--what", default="draft,batched,verify,decode,sampled,stochastic")
     ap.add_argument("--exact", action="store_true", help="also time the EXACT draft level")
     ap.add_argument("--decode-iters", type=int, default=100)
     a = ap.parse_args()
@@ -216,6 +249,8 @@ def main():
         decode_loop(ctx, dev, a.decode_iters)
     if "sampled" in what:
         sampled_draft(ctx, dev)
+    if "stochastic" in what:
+        stochastic_verify(ctx, dev)
 
 
 if __name__ == "__main__":
