@@ -802,23 +802,25 @@ int frs_verify_stochastic(frs_ctx *ctx, const float *h_dev, const void *W, int V
     FRS_REQUIRE(V >= 1 && d >= 1 && v_sub >= 1, "verify_stochastic: sizes must be positive");
     FRS_CUDA_TRY(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
-    const int rows = 1 + k;
     int st;
-    if ((st = ctx->logits.ensure((size_t)rows * V * sizeof(float))) ||
-        (st = ctx->scratch.ensure((size_t)rows * V * sizeof(float) + 64 * sizeof(uint32_t) + 256)))
+    if ((st = ctx->logits.ensure((size_t)V * sizeof(float))) ||
+        (st = ctx->scratch.ensure((size_t)V * sizeof(float) + 256)))
         return st;
     float *logits = static_cast<float *>(ctx->logits.ptr), *probs = static_cast<float *>(ctx->scratch.ptr);
-    uint32_t *fl = reinterpret_cast<uint32_t *>(probs + (size_t)rows * V);
-    if ((st = launch_exact_logits(ctx, h_dev, rows, d, W, w_dtype, V, logits, s))) return st;
-    if ((st = launch_softmax_probs(ctx, logits, rows, V, temperature, probs, fl, s))) return st;
-    std::vector<uint32_t> hfl(rows);
-    FRS_CUDA_TRY(cudaMemcpyAsync(hfl.data(), fl, rows * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    FRS_CUDA_TRY(cudaStreamSynchronize(s));
-    for (int r = 0; r < rows; ++r)
-        if (hfl[r] & FRS_FLAG_NONFINITE) return fail(FRS_EINVAL, "softmax: non-finite logit");  // kernels.cpp:72-74
+    uint32_t *fl = reinterpret_cast<uint32_t *>(probs + V);
     std::vector<float> prow(V);
+    // The walk visits the root row and then only accepted nodes' rows: each row's exact
+    // logits + probabilities are computed when the walk reaches it (one head pass per visited
+    // row; typically 1-3 of the 1 + k).
     auto fetch = [&](int r) -> int {  // the exact probabilities of target row r (0 = root)
-        FRS_CUDA_TRY(cudaMemcpy(prow.data(), probs + (size_t)r * V, sizeof(float) * V, cudaMemcpyDeviceToHost));
+        int rc;
+        if ((rc = launch_exact_logits(ctx, h_dev + (size_t)r * d, 1, d, W, w_dtype, V, logits, s))) return rc;
+        if ((rc = launch_softmax_probs(ctx, logits, 1, V, temperature, probs, fl, s))) return rc;
+        uint32_t hf = 0;
+        FRS_CUDA_TRY(cudaMemcpyAsync(prow.data(), probs, sizeof(float) * V, cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaMemcpyAsync(&hf, fl, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaStreamSynchronize(s));
+        if (hf & FRS_FLAG_NONFINITE) return fail(FRS_EINVAL, "softmax: non-finite logit");  // kernels.cpp:72-74
         return FRS_OK;
     };
     // children_by_node (verification.cpp:31-38)
