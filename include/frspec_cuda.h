@@ -146,6 +146,22 @@ FRS_API int frs_gather_rows(frs_ctx *ctx, const float *table, int64_t rows, int 
 
 /* ---- host-side FR vocabulary (vocab.cpp:23-138) and tree mask (verification.cpp:13-27) ---- */
 FRS_API int frs_count_frequencies(const int32_t *stream, int64_t count, int vocab_size, uint64_t *counts);
+/* count_frequencies (vocab.cpp:23-38) on the device: tokens and counts [vocab_size] are device
+ * buffers; synchronises `stream` to report the first out-of-range id (FRS_EINVAL, the
+ * reference's message). */
+FRS_API int frs_count_frequencies_device(frs_ctx *ctx, const int32_t *tokens, int64_t count, int vocab_size,
+                                         uint64_t *counts, void *stream);
+/* Token-stream files (vocab.cpp:198-286): binary "FRTK" v1 (u32 vocab_size, u64 count, u32
+ * ids, little endian) and whitespace-separated text; ranked-id files (vocab.cpp:288-308).
+ * Readers: pass tokens/ids = NULL to get the count, then a buffer of that capacity.
+ * Errors: FRS_EDATA with the reference's DataError messages. */
+FRS_API int frs_write_token_stream(const char *path, int vocab_size, const int32_t *tokens, int64_t count);
+FRS_API int frs_read_token_stream(const char *path, int32_t *tokens, int64_t capacity, int *vocab_size,
+                                  int64_t *count);
+FRS_API int frs_read_token_stream_text(const char *path, int vocab_size, int32_t *tokens, int64_t capacity,
+                                       int64_t *count);
+FRS_API int frs_write_ranked_file(const char *path, const int32_t *ids, int64_t n);
+FRS_API int frs_read_ranked_file(const char *path, int32_t *ids, int64_t capacity, int64_t *n);
 FRS_API int frs_build_subset(const uint64_t *counts, int vocab_size, int size, const int32_t *forced,
                      int n_forced, int32_t *ordered_out);
 FRS_API int frs_subset_from_ranking(const int32_t *ranked, int n_ranked, int size, int vocab_size,

@@ -246,6 +246,11 @@ class Reference:
                                                                   _i32p, _ip, _i32p, _i32p, _i32p, _f64p, _ip]
         L.ref_pick_sampled.argtypes = [_f32p, C.c_int, C.c_int, C.c_uint64, C.c_int64, _i32p, _f32p, _ip]
         L.ref_uniforms.argtypes = [C.c_uint64, C.c_int64, C.c_int, _f64p]
+        L.ref_write_token_stream.argtypes = [C.c_char_p, C.c_int, _i32p, C.c_int64]
+        L.ref_read_token_stream.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, _ip, C.POINTER(C.c_int64)]
+        L.ref_read_token_stream_text.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.ref_write_ranked_file.argtypes = [C.c_char_p, _i32p, C.c_int64]
+        L.ref_read_ranked_file.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
         L.ref_verify_stochastic.argtypes = [_f32p, C.c_int, _f32p, C.c_int, _i32p, _i32p, _f32p, C.c_int, _f32p, _i32p,
                                             C.c_void_p, C.c_float, C.c_uint64, _i32p, _ip, _i32p, _ip]
 
@@ -423,6 +428,21 @@ class Reference:
                                                    C.c_uint64(rng_seed), em, C.byref(ne), pa, C.byref(npth)),
                     "verify_stochastic")
         return em[:ne.value].copy(), pa[:npth.value].copy()
+
+    def write_token_stream(self, path, vocab, tokens):
+        t = _ci32(tokens)
+        self._check(self.lib.ref_write_token_stream(path.encode(), vocab, t, t.size), "write_token_stream")
+
+    def read_token_stream(self, path):
+        v, n = C.c_int(), C.c_int64()
+        self._check(self.lib.ref_read_token_stream(path.encode(), None, 0, C.byref(v), C.byref(n)), "read_token_stream")
+        out = np.empty(n.value, np.int32)
+        self._check(self.lib.ref_read_token_stream(path.encode(), out.ctypes.data, out.size, C.byref(v), C.byref(n)),
+                    "read_token_stream")
+        return v.value, out
+
+    # (the text / ranked-file readers of the reference parse with iostreams, whose libstdc++
+    # differs from the one numpy loads into this process: they are not wrapped here)
 
     def uniforms(self, seed, count, skip=0):
         out = np.empty(count, np.float64)

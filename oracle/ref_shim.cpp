@@ -261,6 +261,36 @@ int ref_verify_stochastic(const float * root_logits, int V, const float * node_l
     });
 }
 
+// Token-stream / ranked files through the reference (vocab.cpp:198-308), for cross-checks.
+int ref_write_token_stream(const char * path, int vocab, const int32_t * tokens, int64_t n) {
+    return guarded([&] { write_token_stream(path, vocab, std::span<const Token>(tokens, n)); });
+}
+int ref_read_token_stream(const char * path, int32_t * out, int64_t cap, int * vocab, int64_t * n) {
+    return guarded([&] {
+        TokenStreamData d = read_token_stream(path);
+        *vocab = d.vocab_size;
+        *n = static_cast<int64_t>(d.tokens.size());
+        if (out) std::copy(d.tokens.begin(), d.tokens.begin() + std::min<int64_t>(cap, *n), out);
+    });
+}
+int ref_read_token_stream_text(const char * path, int vocab, int32_t * out, int64_t cap, int64_t * n) {
+    return guarded([&] {
+        TokenStreamData d = read_token_stream_text(path, vocab);
+        *n = static_cast<int64_t>(d.tokens.size());
+        if (out) std::copy(d.tokens.begin(), d.tokens.begin() + std::min<int64_t>(cap, *n), out);
+    });
+}
+int ref_write_ranked_file(const char * path, const int32_t * ids, int64_t n) {
+    return guarded([&] { write_ranked_file(path, std::span<const Token>(ids, n)); });
+}
+int ref_read_ranked_file(const char * path, int32_t * out, int64_t cap, int64_t * n) {
+    return guarded([&] {
+        std::vector<Token> ids = read_ranked_file(path);
+        *n = static_cast<int64_t>(ids.size());
+        if (out) std::copy(ids.begin(), ids.begin() + std::min<int64_t>(cap, *n), out);
+    });
+}
+
 // A persistent reference Matrix for timing the reference's own draft level without per-call
 // copies of the head (the CPU baseline in bench.py).
 void * ref_head_new(const float * W, int rows, int d) { return new Matrix(to_matrix(W, rows, d)); }

@@ -89,6 +89,12 @@ SIGNATURES = [
     ("frs_rng_destroy", _I, [_P]),
     ("frs_rng_uniforms", _I, [_P, _I, _P]),
     ("frs_draft_head_sample", _I, [_P, _P, _I, _I, _P, _I, _I, _P, _I, C.c_float, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("frs_count_frequencies_device", _I, [_P, _P, _I64, _I, _P, _P]),
+    ("frs_write_token_stream", _I, [C.c_char_p, _I, _P, _I64]),
+    ("frs_read_token_stream", _I, [C.c_char_p, _P, _I64, C.POINTER(_I), C.POINTER(_I64)]),
+    ("frs_read_token_stream_text", _I, [C.c_char_p, _I, _P, _I64, C.POINTER(_I64)]),
+    ("frs_write_ranked_file", _I, [C.c_char_p, _P, _I64]),
+    ("frs_read_ranked_file", _I, [C.c_char_p, _P, _I64, C.POINTER(_I64)]),
     ("frs_verify_stochastic", _I, [_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _I, _P, _P, _P, C.c_float, _P, _P,
                                    C.POINTER(_I), _P, C.POINTER(_I)]),
     ("frs_draft_tree_sampled", _I, [_P, C.c_int32, HIDDEN_FN, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P,

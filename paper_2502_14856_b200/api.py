@@ -120,6 +120,56 @@ def count_frequencies(stream, vocab_size: int) -> FrequencyTable:
     return FrequencyTable(vocab_size, counts, int(s.size))
 
 
+def count_frequencies_device(ctx: "Context", tokens: torch.Tensor, vocab_size: int) -> FrequencyTable:
+    """count_frequencies (vocab.cpp:23-38) on the device (int32 CUDA token tensor)."""
+    t = tokens.to(torch.int32).contiguous()
+    counts = torch.empty(max(vocab_size, 1), dtype=torch.int64, device=t.device)
+    check(lib().frs_count_frequencies_device(ctx.handle, _ptr(t), t.numel(), vocab_size, _ptr(counts),
+                                             _stream(None)), "count_frequencies")
+    return FrequencyTable(vocab_size, counts.cpu().numpy().view(np.uint64), int(t.numel()))
+
+
+def write_token_stream(path: str, vocab_size: int, tokens) -> None:
+    """vocab.cpp:236-245: binary FRTK v1 token stream."""
+    t = _i32(tokens)
+    check(lib().frs_write_token_stream(path.encode(), vocab_size, _np_ptr(t), t.size), "write_token_stream")
+
+
+def read_token_stream(path: str):
+    """vocab.cpp:247-272 -> (vocab_size, tokens)."""
+    v, n = C.c_int(), C.c_int64()
+    check(lib().frs_read_token_stream(path.encode(), None, 0, C.byref(v), C.byref(n)), "read_token_stream")
+    out = np.empty(n.value, np.int32)
+    check(lib().frs_read_token_stream(path.encode(), _np_ptr(out), out.size, C.byref(v), C.byref(n)),
+          "read_token_stream")
+    return v.value, out
+
+
+def read_token_stream_text(path: str, vocab_size: int) -> np.ndarray:
+    """vocab.cpp:274-286: whitespace-separated ids."""
+    n = C.c_int64()
+    check(lib().frs_read_token_stream_text(path.encode(), vocab_size, None, 0, C.byref(n)), "read_token_stream_text")
+    out = np.empty(n.value, np.int32)
+    check(lib().frs_read_token_stream_text(path.encode(), vocab_size, _np_ptr(out), out.size, C.byref(n)),
+          "read_token_stream_text")
+    return out
+
+
+def write_ranked_file(path: str, ordered_ids) -> None:
+    """vocab.cpp:288-293: one id per line."""
+    t = _i32(ordered_ids)
+    check(lib().frs_write_ranked_file(path.encode(), _np_ptr(t), t.size), "write_ranked_file")
+
+
+def read_ranked_file(path: str) -> np.ndarray:
+    """vocab.cpp:295-306."""
+    n = C.c_int64()
+    check(lib().frs_read_ranked_file(path.encode(), None, 0, C.byref(n)), "read_ranked_file")
+    out = np.empty(n.value, np.int32)
+    check(lib().frs_read_ranked_file(path.encode(), _np_ptr(out), out.size, C.byref(n)), "read_ranked_file")
+    return out
+
+
 @dataclass
 class RankedSubset:
     vocab_size: int

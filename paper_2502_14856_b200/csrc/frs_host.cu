@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <numeric>
 #include <random>
 #include <string>
@@ -913,6 +914,146 @@ int frs_verify_stochastic(frs_ctx *ctx, const float *h_dev, const void *W, int V
     *n_path = static_cast<int>(pa.size());
     std::copy(em.begin(), em.end(), emitted);
     std::copy(pa.begin(), pa.end(), path);
+    return FRS_OK;
+}
+
+int frs_count_frequencies_device(frs_ctx *ctx, const int32_t *tokens, int64_t count, int vocab_size, uint64_t *counts,
+                                 void *stream) {
+    FRS_REQUIRE(ctx, "count_frequencies: null context");
+    FRS_REQUIRE(vocab_size >= 1, "count_frequencies: vocab_size must be >= 1");
+    FRS_REQUIRE(counts && (count == 0 || tokens) && count >= 0, "count_frequencies: null pointer");
+    FRS_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int st = ctx->flags.ensure(256);
+    if (st) return st;
+    auto *bad = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(ctx->flags.ptr) + 64);
+    if ((st = frs::count_tokens(ctx, tokens, count, vocab_size, reinterpret_cast<unsigned long long *>(counts), bad, s)))
+        return st;
+    unsigned long long hb = ~0ull;
+    FRS_CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hb != ~0ull) {
+        int32_t t = 0;
+        FRS_CUDA_TRY(cudaMemcpy(&t, tokens + hb, sizeof(t), cudaMemcpyDeviceToHost));
+        return fail(FRS_EINVAL, "count_frequencies: token id " + std::to_string(t) + " out of range at offset " +
+                                    std::to_string(hb));
+    }
+    return FRS_OK;
+}
+
+namespace {
+bool read_le(std::ifstream &f, uint64_t &v, int bytes) {
+    unsigned char b[8];
+    if (!f.read(reinterpret_cast<char *>(b), bytes)) return false;
+    v = 0;
+    for (int i = 0; i < bytes; ++i) v |= static_cast<uint64_t>(b[i]) << (8 * i);
+    return true;
+}
+void write_le(std::ofstream &f, uint64_t v, int bytes) {
+    unsigned char b[8];
+    for (int i = 0; i < bytes; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+    f.write(reinterpret_cast<const char *>(b), bytes);
+}
+}  // namespace
+
+// vocab.cpp:236-245
+int frs_write_token_stream(const char *path, int vocab_size, const int32_t *tokens, int64_t count) {
+    FRS_REQUIRE(path && (count == 0 || tokens) && count >= 0, "write_token_stream: bad arguments");
+    const std::string p(path);
+    std::ofstream f(p, std::ios::binary);
+    if (!f) return fail(FRS_EDATA, p + ": cannot open for writing");
+    f.write("FRTK", 4);
+    write_le(f, 1, 4);
+    write_le(f, static_cast<uint32_t>(vocab_size), 4);
+    write_le(f, static_cast<uint64_t>(count), 8);
+    for (int64_t i = 0; i < count; ++i) write_le(f, static_cast<uint32_t>(tokens[i]), 4);
+    if (!f) return fail(FRS_EDATA, p + ": write failed");
+    return FRS_OK;
+}
+
+// vocab.cpp:247-272
+int frs_read_token_stream(const char *path, int32_t *tokens, int64_t capacity, int *vocab_size, int64_t *count) {
+    FRS_REQUIRE(path && vocab_size && count, "read_token_stream: null pointer");
+    const std::string p(path);
+    std::ifstream f(p, std::ios::binary);
+    if (!f) return fail(FRS_EDATA, p + ": cannot open");
+    char magic[4];
+    if (!f.read(magic, 4) || std::memcmp(magic, "FRTK", 4) != 0)
+        return fail(FRS_EDATA, p + ": not a token-stream file (bad magic)");
+    uint64_t version = 0, vs = 0, n = 0;
+    if (!read_le(f, version, 4)) return fail(FRS_EDATA, p + ": truncated header");
+    if (version != 1) return fail(FRS_EDATA, p + ": unsupported version " + std::to_string(version));
+    if (!read_le(f, vs, 4)) return fail(FRS_EDATA, p + ": truncated header");
+    const int v = static_cast<int>(static_cast<uint32_t>(vs));
+    if (v < 1) return fail(FRS_EDATA, p + ": bad vocab_size");
+    if (!read_le(f, n, 8)) return fail(FRS_EDATA, p + ": truncated header");
+    *vocab_size = v;
+    *count = static_cast<int64_t>(n);
+    if (!tokens) return FRS_OK;  // size query
+    if (static_cast<int64_t>(n) > capacity) return fail(FRS_ECAPACITY, "read_token_stream: buffer too small");
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t raw = 0;
+        if (!read_le(f, raw, 4)) return fail(FRS_EDATA, p + ": truncated header");
+        if (raw >= static_cast<uint64_t>(static_cast<uint32_t>(v)))
+            return fail(FRS_EDATA, p + ": token id " + std::to_string(raw) + " out of range at offset " +
+                                       std::to_string(i));
+        tokens[i] = static_cast<int32_t>(raw);
+    }
+    return FRS_OK;
+}
+
+// vocab.cpp:274-286
+int frs_read_token_stream_text(const char *path, int vocab_size, int32_t *tokens, int64_t capacity, int64_t *count) {
+    FRS_REQUIRE(path && count, "read_token_stream_text: null pointer");
+    const std::string p(path);
+    std::ifstream f(p);
+    if (!f) return fail(FRS_EDATA, p + ": cannot open");
+    long long value = 0;
+    int64_t offset = 0;
+    while (f >> value) {
+        if (value < 0 || value >= vocab_size)
+            return fail(FRS_EDATA, p + ": token id " + std::to_string(value) + " out of range at offset " +
+                                       std::to_string(offset));
+        if (tokens) {
+            if (offset >= capacity) return fail(FRS_ECAPACITY, "read_token_stream_text: buffer too small");
+            tokens[offset] = static_cast<int32_t>(value);
+        }
+        ++offset;
+    }
+    if (!f.eof()) return fail(FRS_EDATA, p + ": unparsable token id at offset " + std::to_string(offset));
+    *count = offset;
+    return FRS_OK;
+}
+
+// vocab.cpp:288-293
+int frs_write_ranked_file(const char *path, const int32_t *ids, int64_t n) {
+    FRS_REQUIRE(path && (n == 0 || ids) && n >= 0, "write_ranked_file: bad arguments");
+    const std::string p(path);
+    std::ofstream f(p);
+    if (!f) return fail(FRS_EDATA, p + ": cannot open for writing");
+    for (int64_t i = 0; i < n; ++i) f << ids[i] << '\n';
+    if (!f) return fail(FRS_EDATA, p + ": write failed");
+    return FRS_OK;
+}
+
+// vocab.cpp:295-306
+int frs_read_ranked_file(const char *path, int32_t *ids, int64_t capacity, int64_t *n) {
+    FRS_REQUIRE(path && n, "read_ranked_file: null pointer");
+    const std::string p(path);
+    std::ifstream f(p);
+    if (!f) return fail(FRS_EDATA, p + ": cannot open");
+    long long value = 0;
+    int64_t k = 0;
+    while (f >> value) {
+        if (value < 0) return fail(FRS_EDATA, p + ": negative token id");
+        if (ids) {
+            if (k >= capacity) return fail(FRS_ECAPACITY, "read_ranked_file: buffer too small");
+            ids[k] = static_cast<int32_t>(value);
+        }
+        ++k;
+    }
+    if (!f.eof()) return fail(FRS_EDATA, p + ": unparsable token id at line " + std::to_string(k + 1));
+    *n = k;
     return FRS_OK;
 }
 

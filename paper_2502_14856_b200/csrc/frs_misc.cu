@@ -126,6 +126,43 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// count_frequencies (vocab.cpp:23-38) on the device: counts[t] = occurrences of t. Each CTA
+// privatises the ids below kSmemBins in a u32 shared histogram (Zipf-ranked corpora put most
+// of the mass there) and sends the rest to the u64 global counters; both with warp-aggregated
+// atomics (one per distinct id in the warp); the shared bins are flushed at the end. An id out
+// of range records the smallest offending offset (the reference throws at the first one).
+constexpr int kSmemBins = 24576;  // 96 KB of u32
+
+__global__ void __launch_bounds__(1024)
+    k_count_tokens(const int32_t *__restrict__ tokens, long long count, int vocab, unsigned long long *__restrict__ counts,
+                   unsigned long long *__restrict__ bad_offset) {
+    extern __shared__ unsigned s_bins[];
+    const int nb = min(vocab, kSmemBins);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) s_bins[b] = 0u;
+    __syncthreads();
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < count; base += stride) {  // warp-uniform
+        const long long i = base + threadIdx.x;
+        const bool in = i < count;
+        const int t = in ? __ldcs(tokens + i) : 0;
+        const bool ok = in && t >= 0 && t < vocab;
+        if (in && !ok) atomicMin(bad_offset, static_cast<unsigned long long>(i));
+        // one atomic per distinct id in the warp (Zipf corpora repeat the head ids constantly)
+        const int key = ok ? t : -1 - lane;  // distinct dummies for the other lanes
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (ok && lane == __ffs(peers) - 1) {
+            if (t < nb)
+                atomicAdd(&s_bins[t], static_cast<unsigned>(__popc(peers)));
+            else
+                atomicAdd(counts + t, static_cast<unsigned long long>(__popc(peers)));
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        if (s_bins[b]) atomicAdd(counts + b, static_cast<unsigned long long>(s_bins[b]));
+}
+
 }  // namespace
 
 int slab_build(frs_ctx *ctx, const float *W, long long V, int d, const int32_t *ids, int v_sub, int dtype,
@@ -157,6 +194,20 @@ int accept_greedy(const int32_t *argmax_ids, const int32_t *tokens, const int32_
 int argmax_merge(const float *vals, const int32_t *ids, int shards, int m, float *out_val, int32_t *out_id,
                  cudaStream_t s) {
     k_argmax_merge<<<(m + 127) / 128, 128, 0, s>>>(vals, ids, shards, m, out_val, out_id);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+int count_tokens(frs_ctx *ctx, const int32_t *tokens, long long count, int vocab, unsigned long long *counts,
+                 unsigned long long *bad_offset, cudaStream_t s) {
+    FRS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * (size_t)vocab, s));
+    FRS_CUDA_TRY(cudaMemsetAsync(bad_offset, 0xff, sizeof(unsigned long long), s));
+    if (count == 0) return FRS_OK;
+    const size_t smem = sizeof(unsigned) * (size_t)std::min(vocab, kSmemBins);
+    FRS_CUDA_TRY(cudaFuncSetAttribute(k_count_tokens, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const long long blocks = std::min<long long>(ctx->sm_count * 2, (count + 1023) / 1024);
+    ++ctx->launches;
+    k_count_tokens<<<(int)blocks, 1024, smem, s>>>(tokens, count, vocab, counts, bad_offset);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }

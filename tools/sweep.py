@@ -230,9 +230,25 @@ def stochastic_verify(ctx, dev, iters=5):
                       "head_dtype": "f32", "ms_per_call": ms, "accepted_lengths": lens}), flush=True)
 
 
+def corpus_count(ctx, dev):
+    """count_frequencies on the device (vocab.cpp:23-38): 256M-token Zipf-like corpus at the
+    Qwen vocabulary (ids rank-ordered, and permuted)."""
+    V, n = 152064, 1 << 28
+    g = torch.Generator(device=dev).manual_seed(3)
+    u = torch.rand(n, generator=g, device=dev)
+    ranks = torch.clamp((torch.exp(u * np.log(V)) - 1).to(torch.int32), 0, V - 1)  # ~ Zipf(1) ranks
+    perm = torch.from_numpy(np.random.default_rng(3).permutation(V).astype(np.int32)).to(dev)
+    for name, toks in (("rank_ordered_ids", ranks), ("permuted_ids", perm[ranks.long()])):
+        api.count_frequencies_device(ctx, toks, V)
+        torch.cuda.synchronize()
+        us = timed(lambda i: api.count_frequencies_device(ctx, toks, V), 5, warm=1)
+        print(json.dumps({"sweep": "count_frequencies", "ids": name, "tokens": n, "vocab": V, "us_per_call": us,
+                          "GBps": n * 4 / us / 1e3, "tokens_per_s": n / us * 1e6}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="draft,batched,verify,decode,sampled,stochastic")
+    ap.add_argument("--what", default="draft,batched,verify,decode,sampled,stochastic,count")
     ap.add_argument("--exact", action="store_true", help="also time the EXACT draft level")
     ap.add_argument("--decode-iters", type=int, default=100)
     a = ap.parse_args()
@@ -251,6 +267,8 @@ def main():
         sampled_draft(ctx, dev)
     if "stochastic" in what:
         stochastic_verify(ctx, dev)
+    if "count" in what:
+        corpus_count(ctx, dev)
 
 
 if __name__ == "__main__":
