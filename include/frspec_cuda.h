@@ -69,6 +69,7 @@ typedef enum { FRS_MODE_EXACT = 0, FRS_MODE_FAST = 1 } frs_mode;
 #define FRS_FLAG_CERT_BOUND 0x20u    /* the rigorous error bound did not separate the k-th candidate   */
 #define FRS_FLAG_CERT_OVERFLOW 0x40u /* more near-boundary candidates than the exact-recompute set     */
 /* FAST, certified rows: bits 8..15 hold the size of the exactly recomputed candidate set (info). */
+#define FRS_FLAG_EMPTY_ROW 0x100u          /* masked_attention: the row permits no key (reference throws)  */
 #define FRS_FLAG_SAMPLE_UNCERTIFIED 0x80u /* sampled draw inside the rounding bound: host replays the level */
 #define FRS_FLAG_CAND_SHIFT 8
 
@@ -194,6 +195,13 @@ FRS_API int frs_draft_tree(frs_head *head, int32_t root_token, frs_hidden_fn fn,
                    const float *hidden_table, int width, int depth, int total, int mode,
                    int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint,
                    int *count);
+/* masked_attention (kernels.cpp:124-171), the tree attention of the draft / target forwards:
+ * q [n x dh], k [m x dh], v [m x dv] fp32 and mask [n x ceil(m/64)] u64 (bit j of row r = key j
+ * visible to query r, the reference's BitMask words) on the device; out [n x dv]. Bit-exact with
+ * the reference (dot_f32 order, glibc expf, pinned 1/Σ, key-ordered accumulation). flags [n]:
+ * FRS_FLAG_EMPTY_ROW where a row permits no key (the reference throws; the row is zeros). */
+FRS_API int frs_masked_attention(frs_ctx *ctx, const float *q, const float *k, const float *v, const uint64_t *mask,
+                                 int n, int m, int dh, int dv, float *out, uint32_t *flags, void *stream);
 /* Sampled drafting (drafting.cpp:44-74): a std::mt19937_64 the caller owns (the reference's
  * `std::mt19937_64 * rng`), advanced by every draw exactly as the reference advances it. */
 typedef struct frs_rng frs_rng;

@@ -247,6 +247,7 @@ class Reference:
         L.ref_pick_sampled.argtypes = [_f32p, C.c_int, C.c_int, C.c_uint64, C.c_int64, _i32p, _f32p, _ip]
         L.ref_uniforms.argtypes = [C.c_uint64, C.c_int64, C.c_int, _f64p]
         L.ref_write_token_stream.argtypes = [C.c_char_p, C.c_int, _i32p, C.c_int64]
+        L.ref_masked_attention.argtypes = [_f32p, _f32p, _f32p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _f32p]
         L.ref_read_token_stream.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, _ip, C.POINTER(C.c_int64)]
         L.ref_read_token_stream_text.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
         L.ref_write_ranked_file.argtypes = [C.c_char_p, _i32p, C.c_int64]
@@ -428,6 +429,14 @@ class Reference:
                                                    C.c_uint64(rng_seed), em, C.byref(ne), pa, C.byref(npth)),
                     "verify_stochastic")
         return em[:ne.value].copy(), pa[:npth.value].copy()
+
+    def masked_attention(self, q, k, v, allow):
+        q, k, v = _c32(q), _c32(k), _c32(v)
+        a = np.ascontiguousarray(allow, np.uint8)
+        out = np.empty((q.shape[0], v.shape[1]), np.float32)
+        self._check(self.lib.ref_masked_attention(q, k, v, a.ctypes.data, q.shape[0], k.shape[0], q.shape[1],
+                                                  v.shape[1], out), "masked_attention")
+        return out
 
     def write_token_stream(self, path, vocab, tokens):
         t = _ci32(tokens)

@@ -261,6 +261,19 @@ int ref_verify_stochastic(const float * root_logits, int V, const float * node_l
     });
 }
 
+// masked_attention (kernels.cpp:124-171) with a dense 0/1 mask [n x m].
+int ref_masked_attention(const float * q, const float * k, const float * v, const uint8_t * allow, int n, int m,
+                         int dh, int dv, float * out) {
+    return guarded([&] {
+        BitMask bm(n, m);
+        for (int r = 0; r < n; ++r)
+            for (int j = 0; j < m; ++j)
+                if (allow[static_cast<size_t>(r) * m + j]) bm.set(r, j);
+        Matrix o = masked_attention(to_matrix(q, n, dh), to_matrix(k, m, dh), to_matrix(v, m, dv), bm);
+        std::memcpy(out, o.row(0), sizeof(float) * static_cast<size_t>(n) * dv);
+    });
+}
+
 // Token-stream / ranked files through the reference (vocab.cpp:198-308), for cross-checks.
 int ref_write_token_stream(const char * path, int vocab, const int32_t * tokens, int64_t n) {
     return guarded([&] { write_token_stream(path, vocab, std::span<const Token>(tokens, n)); });

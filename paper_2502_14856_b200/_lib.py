@@ -17,6 +17,7 @@ MODE_EXACT, MODE_FAST = 0, 1
 FLAG_NONFINITE, FLAG_SEQ_SUM, FLAG_UNCERTIFIED, FLAG_RECOMPUTED = 0x1, 0x2, 0x4, 0x8
 FLAG_CERT_TIE, FLAG_CERT_BOUND, FLAG_CERT_OVERFLOW = 0x10, 0x20, 0x40
 FLAG_SAMPLE_UNCERTIFIED = 0x80
+FLAG_EMPTY_ROW = 0x100
 
 
 class FrsError(RuntimeError):
@@ -90,6 +91,7 @@ SIGNATURES = [
     ("frs_rng_uniforms", _I, [_P, _I, _P]),
     ("frs_draft_head_sample", _I, [_P, _P, _I, _I, _P, _I, _I, _P, _I, C.c_float, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("frs_count_frequencies_device", _I, [_P, _P, _I64, _I, _P, _P]),
+    ("frs_masked_attention", _I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     ("frs_write_token_stream", _I, [C.c_char_p, _I, _P, _I64]),
     ("frs_read_token_stream", _I, [C.c_char_p, _P, _I64, C.POINTER(_I), C.POINTER(_I64)]),
     ("frs_read_token_stream_text", _I, [C.c_char_p, _I, _P, _I64, C.POINTER(_I64)]),

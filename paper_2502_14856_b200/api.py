@@ -129,6 +129,30 @@ def count_frequencies_device(ctx: "Context", tokens: torch.Tensor, vocab_size: i
     return FrequencyTable(vocab_size, counts.cpu().numpy().view(np.uint64), int(t.numel()))
 
 
+def masked_attention(ctx: "Context", q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, allow) -> torch.Tensor:
+    """kernels.cpp:124-171 (the tree attention): allow [n, m] bool/0-1 (numpy or tensor), packed
+    here into the reference's BitMask words. Raises InvalidArgument like the reference when a
+    query row permits no key."""
+    q, k, v = (t.to(torch.float32).contiguous() for t in (q, k, v))
+    n, dh = q.shape
+    m, dv = v.shape
+    a = np.asarray(allow.cpu() if isinstance(allow, torch.Tensor) else allow).astype(bool).reshape(n, m)
+    stride = (m + 63) // 64
+    bits = np.zeros((n, stride * 64), np.uint8)
+    bits[:, :m] = a
+    words = np.packbits(bits.reshape(n, stride, 64)[:, :, ::-1], axis=2, bitorder="big").reshape(n, stride, 8)
+    words = words[:, :, ::-1].copy().view(np.uint64).reshape(n, stride)  # little-endian u64, bit j = key j
+    wd = torch.from_numpy(words.view(np.int64)).to(q.device)
+    out = torch.empty((n, dv), dtype=torch.float32, device=q.device)
+    flags = torch.empty(n, dtype=torch.int32, device=q.device)
+    check(lib().frs_masked_attention(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(wd), n, m, dh, dv, _ptr(out),
+                                     _ptr(flags), _stream(None)), "masked_attention")
+    bad = np.nonzero(flags.cpu().numpy() & _lib.FLAG_EMPTY_ROW)[0]
+    if bad.size:
+        raise InvalidArgument(f"masked_attention: query row {int(bad[0])} permits no keys")
+    return out
+
+
 def write_token_stream(path: str, vocab_size: int, tokens) -> None:
     """vocab.cpp:236-245: binary FRTK v1 token stream."""
     t = _i32(tokens)

@@ -213,6 +213,16 @@ int frs_draft_head_topk(frs_ctx *ctx, const float *h, int n, int d, const void *
                                out_rowmax, out_total, out_flags, s);
 }
 
+int frs_masked_attention(frs_ctx *ctx, const float *q, const float *k, const float *v, const uint64_t *mask, int n,
+                         int m, int dh, int dv, float *out, uint32_t *flags, void *stream) {
+    int st = check_device(ctx);
+    if (st) return st;
+    FRS_REQUIRE(q && k && v && mask && out && flags, "masked_attention: null pointer");
+    FRS_REQUIRE(n >= 1 && m >= 1 && dh >= 1 && dv >= 1, "masked_attention: sizes must be positive");
+    return launch_masked_attention(ctx, q, k, v, reinterpret_cast<const unsigned long long *>(mask), n, m, dh, dv, out,
+                                   flags, static_cast<cudaStream_t>(stream));
+}
+
 int frs_draft_head_sample(frs_ctx *ctx, const float *h, int n, int d, const void *slab, int v_sub, int slab_dtype,
                           const int32_t *ordered_ids, int width, float temperature, const double *uniforms,
                           float *probs, int32_t *out_ridx, int32_t *out_full, float *out_prob, int32_t *out_count,

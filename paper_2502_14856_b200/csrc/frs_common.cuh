@@ -89,6 +89,9 @@ constexpr int kMaxK = 64;  // width <= total_draft_tokens <= 64 (drafting.cpp:14
 // Launchers (defined in the .cu files); all return frs_status.
 int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *W, int w_dtype,
                         int v_rows, float *logits, cudaStream_t s);
+int launch_masked_attention(frs_ctx *ctx, const float *q, const float *k, const float *v,
+                            const unsigned long long *mask, int n, int m, int dh, int dv, float *out, uint32_t *flags,
+                            cudaStream_t s);
 int count_tokens(frs_ctx *ctx, const int32_t *tokens, long long count, int vocab, unsigned long long *counts,
                  unsigned long long *bad_offset, cudaStream_t s);
 int launch_softmax_probs(frs_ctx *ctx, const float *logits, int n, int v, float temperature, float *probs,

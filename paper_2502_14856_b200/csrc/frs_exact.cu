@@ -32,6 +32,92 @@ __device__ __forceinline__ float load_w(const __nv_bfloat16 *p) {
     return __uint_as_float(static_cast<uint32_t>(u) << 16);  // bf16 -> fp32 is exact
 }
 
+// masked_attention (kernels.cpp:124-171) for one query row per CTA: scores over the allowed
+// keys = dot_f32(q, k_j) * (1 / sqrtf(dh)) (8 lane chains, reference order), e_j = expf(s_j -
+// max) (glibc port), inv = float(1 / Σ e_j) with the index-order double sum pinned as in
+// softmax_probs_row, then out[c] = Σ_j (e_j * inv) * v[j][c] accumulated in key order per
+// column (one thread per column). Rows that permit no key: FRS_FLAG_EMPTY_ROW (the reference
+// throws) and zeros.
+__global__ void __launch_bounds__(256)
+    k_masked_attention(const float *__restrict__ q, const float *__restrict__ k, const float *__restrict__ v,
+                       const unsigned long long *__restrict__ mask, int m, int dh, int dv, float *__restrict__ out,
+                       float *__restrict__ scratch, uint32_t *__restrict__ flags) {
+    extern __shared__ float s_q[];
+    __shared__ dev::ReduceScratch rs;
+    const int r = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    const int stride = (m + 63) >> 6;
+    const unsigned long long *words = mask + (size_t)r * stride;
+    auto allowed = [&](int j) { return ((words[j >> 6] >> (j & 63)) & 1ull) != 0; };
+    float *S = scratch + (size_t)r * m;
+    for (int c = tid; c < dh; c += nt) s_q[c] = q[(size_t)r * dh + c];
+    dev::load_exp_table(rs.tab);
+    __syncthreads();
+    const float scale = __fdiv_rn(1.0f, __fsqrt_rn(static_cast<float>(dh)));
+    for (int j0 = 0; j0 < m; j0 += nt / 8) {  // 8 lanes per key; whole warps in the dot
+        const int j = j0 + (tid >> 3);
+        const int jj = j < m ? j : m - 1;
+        const float d = dev::dot_f32_lanes8(s_q, k + (size_t)jj * dh, dh);
+        if ((tid & 7) == 0 && j < m && allowed(j)) S[j] = __fmul_rn(d, scale);
+    }
+    __syncthreads();
+    float mx = -__int_as_float(0x7f800000);
+    int any = 0;
+    for (int j = tid; j < m; j += nt)
+        if (allowed(j)) {
+            mx = fmaxf(mx, S[j]);
+            any = 1;
+        }
+    mx = dev::block_reduce(mx, dev::MaxF(), rs.f);
+    any = dev::block_reduce(any, dev::OrI(), rs.i);
+    if (!any) {
+        for (int c = tid; c < dv; c += nt) out[(size_t)r * dv + c] = 0.0f;
+        if (tid == 0) flags[r] = FRS_FLAG_EMPTY_ROW;
+        return;
+    }
+    double part = 0.0;
+    int lsb = 0x7fffffff;
+    for (int j = tid; j < m; j += nt)
+        if (allowed(j)) {
+            const float e = dev::expf_glibc(__fsub_rn(S[j], mx), rs.tab);
+            S[j] = e;
+            part += static_cast<double>(e);
+            lsb = min(lsb, dev::lsb_exponent(e));
+        }
+    double total = dev::block_reduce(part, dev::SumD(), rs.d);
+    lsb = dev::block_reduce(lsb, dev::MinI(), rs.i);
+    uint32_t fl = 0;
+    bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
+    if (!exact && total > 0.0) {
+        const double del = static_cast<double>(m + 2 * nt) * 0x1p-52;
+        const double lo = __dmul_rd(total, 1.0 - del), hi = __dmul_ru(total, 1.0 + del);
+        exact = __double2float_rn(1.0 / lo) == __double2float_rn(1.0 / hi);
+    }
+    if (!exact) {
+        fl |= FRS_FLAG_SEQ_SUM;
+        __syncthreads();
+        if (tid == 0) {
+            double acc = 0.0;
+            for (int j = 0; j < m; ++j)
+                if (allowed(j)) acc += static_cast<double>(S[j]);
+            rs.d[0] = acc;
+        }
+        __syncthreads();
+        total = rs.d[0];
+    }
+    const float inv = __double2float_rn(1.0 / total);
+    __syncthreads();
+    for (int j = tid; j < m; j += nt)
+        if (allowed(j)) S[j] = __fmul_rn(S[j], inv);
+    __syncthreads();
+    for (int c = tid; c < dv; c += nt) {  // key-ordered accumulation per column (kernels.cpp:162-167)
+        float acc = 0.0f;
+        for (int j = 0; j < m; ++j)
+            if (allowed(j)) acc = __fadd_rn(acc, __fmul_rn(S[j], __ldg(v + (size_t)j * dv + c)));
+        out[(size_t)r * dv + c] = acc;
+    }
+    if (tid == 0) flags[r] = fl;
+}
+
 // One CTA per row: the exact softmax probabilities (kernels.cpp:62-91) of full-vocabulary
 // target logits (verify_stochastic's Residual::init, verification.cpp:80-87); flags per row.
 __global__ void __launch_bounds__(1024)
@@ -356,6 +442,20 @@ int launch_softmax_sample(frs_ctx *ctx, const float *logits, int n, int v, float
     k_softmax_sample<<<n, 1024, 0, s>>>(logits, v, temperature, uniforms, w, ordered_ids, probs,
                                         static_cast<float *>(ctx->scratch.ptr), out_ridx, out_full, out_prob,
                                         out_count, out_flags);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+int launch_masked_attention(frs_ctx *ctx, const float *q, const float *k, const float *v,
+                            const unsigned long long *mask, int n, int m, int dh, int dv, float *out, uint32_t *flags,
+                            cudaStream_t s) {
+    int st = ctx->scratch.ensure((size_t)n * m * sizeof(float));
+    if (st) return st;
+    const size_t smem = (size_t)dh * sizeof(float);
+    if (smem > 48 * 1024) FRS_CUDA_TRY(cudaFuncSetAttribute(k_masked_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ++ctx->launches;
+    k_masked_attention<<<n, 256, smem, s>>>(q, k, v, mask, m, dh, dv, out, static_cast<float *>(ctx->scratch.ptr),
+                                            flags);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }
