@@ -202,6 +202,21 @@ FRS_API int frs_draft_tree(frs_head *head, int32_t root_token, frs_hidden_fn fn,
  * FRS_FLAG_EMPTY_ROW where a row permits no key (the reference throws; the row is zeros). */
 FRS_API int frs_masked_attention(frs_ctx *ctx, const float *q, const float *k, const float *v, const uint64_t *mask,
                                  int n, int m, int dh, int dv, float *out, uint32_t *flags, void *stream);
+/* The draft model's transformer layer (model.cpp:208-281 forward_raw, 1-layer draft) on the
+ * device, bit-exact with the reference: weights host fp32 (LayerWeights layout, x * W^T; NULL
+ * gains = 1), a device KV cache of max_seq rows. forward: tokens / positions host [n], visible
+ * host BitMask words [n x ceil((len + n) / 64)] over cache rows [0, len + n), hidden_out device
+ * [n x d] (post final norm); appends the rows to the cache. FRS_ECAPACITY past max_seq. */
+typedef struct frs_draft_model frs_draft_model;
+FRS_API int frs_draft_model_create(frs_ctx *ctx, int V, int d, int heads, int max_seq, const float *embedding,
+                                   const float *wq, const float *wk, const float *wv, const float *wo,
+                                   const float *w_up, const float *w_down, const float *attn_norm,
+                                   const float *mlp_norm, const float *final_norm, frs_draft_model **out);
+FRS_API int frs_draft_model_destroy(frs_draft_model *m);
+FRS_API int frs_draft_model_truncate(frs_draft_model *m, int new_len);
+FRS_API int frs_draft_model_length(const frs_draft_model *m, int *len);
+FRS_API int frs_draft_model_forward(frs_draft_model *m, const int32_t *tokens, const int32_t *positions, int n,
+                                    const uint64_t *visible, float *hidden_out, void *stream);
 /* Sampled drafting (drafting.cpp:44-74): a std::mt19937_64 the caller owns (the reference's
  * `std::mt19937_64 * rng`), advanced by every draw exactly as the reference advances it. */
 typedef struct frs_rng frs_rng;

@@ -247,6 +247,12 @@ class Reference:
         L.ref_pick_sampled.argtypes = [_f32p, C.c_int, C.c_int, C.c_uint64, C.c_int64, _i32p, _f32p, _ip]
         L.ref_uniforms.argtypes = [C.c_uint64, C.c_int64, C.c_int, _f64p]
         L.ref_write_token_stream.argtypes = [C.c_char_p, C.c_int, _i32p, C.c_int64]
+        L.ref_draft_session_new.restype = C.c_void_p
+        L.ref_draft_session_new.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64]
+        L.ref_draft_session_free.restype = None
+        L.ref_draft_session_free.argtypes = [C.c_void_p]
+        L.ref_draft_session_weights.argtypes = [C.c_void_p] + [_f32p] * 7
+        L.ref_draft_session_forward.argtypes = [C.c_void_p, _i32p, _i32p, C.c_int, C.c_void_p, _f32p]
         L.ref_masked_attention.argtypes = [_f32p, _f32p, _f32p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _f32p]
         L.ref_read_token_stream.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, _ip, C.POINTER(C.c_int64)]
         L.ref_read_token_stream_text.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
@@ -429,6 +435,33 @@ class Reference:
                                                    C.c_uint64(rng_seed), em, C.byref(ne), pa, C.byref(npth)),
                     "verify_stochastic")
         return em[:ne.value].copy(), pa[:npth.value].copy()
+
+    def draft_session(self, V, d, heads, max_seq, seed):
+        """A reference 1-layer draft model + KV cache (forward_raw parity)."""
+        ref = self
+
+        class Session:
+            def __init__(self):
+                self.h = ref.lib.ref_draft_session_new(V, d, heads, max_seq, seed)
+                assert self.h, "ref_draft_session_new failed"
+
+            def weights(self):
+                out = [np.empty((V, d), np.float32)] + [np.empty((d, d), np.float32) for _ in range(4)] + \
+                      [np.empty((4 * d, d), np.float32), np.empty((d, 4 * d), np.float32)]
+                ref._check(ref.lib.ref_draft_session_weights(self.h, *out), "weights")
+                return dict(zip(["embedding", "wq", "wk", "wv", "wo", "w_up", "w_down"], out))
+
+            def forward(self, tokens, positions, allow):
+                t, p = _ci32(tokens), _ci32(positions)
+                a = np.ascontiguousarray(allow, np.uint8)
+                out = np.empty((t.size, d), np.float32)
+                ref._check(ref.lib.ref_draft_session_forward(self.h, t, p, t.size, a.ctypes.data, out), "forward_raw")
+                return out
+
+            def __del__(self):
+                ref.lib.ref_draft_session_free(self.h)
+
+        return Session()
 
     def masked_attention(self, q, k, v, allow):
         q, k, v = _c32(q), _c32(k), _c32(v)

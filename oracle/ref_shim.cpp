@@ -261,6 +261,55 @@ int ref_verify_stochastic(const float * root_logits, int V, const float * node_l
     });
 }
 
+// A reference draft model (build_draft truncated, 1 layer) with its KV cache, for parity of
+// the device draft forward: weights export + forward_raw calls on the persistent cache.
+struct RefDraftSession {
+    ModelBundle b;
+    KVCache cache;
+};
+void * ref_draft_session_new(int V, int d, int heads, int max_seq, uint64_t seed) {
+    try {
+        ModelBundle b = make_bundle(V, d, 1, heads, max_seq, seed, nullptr, 0);
+        KVCache c = make_cache(b.draft);
+        return new RefDraftSession{std::move(b), std::move(c)};
+    } catch (...) {
+        return nullptr;
+    }
+}
+void ref_draft_session_free(void * s) { delete static_cast<RefDraftSession *>(s); }
+// embedding [V x d], wq wk wv wo [d x d], w_up [4d x d], w_down [d x 4d] (norm gains are 1)
+int ref_draft_session_weights(void * sp, float * emb, float * wq, float * wk, float * wv, float * wo, float * w_up,
+                              float * w_down) {
+    return guarded([&] {
+        auto * s = static_cast<RefDraftSession *>(sp);
+        const LayerWeights & L = s->b.draft.layer;
+        auto cp = [](const Matrix & m, float * out) { std::memcpy(out, m.data.data(), sizeof(float) * m.data.size()); };
+        cp(s->b.draft.shared->embedding, emb);
+        cp(L.wq, wq);
+        cp(L.wk, wk);
+        cp(L.wv, wv);
+        cp(L.wo, wo);
+        cp(L.w_up, w_up);
+        cp(L.w_down, w_down);
+    });
+}
+// forward_raw on the session cache: visible_allow [n x (len + n)] 0/1; hidden_out [n x d]
+int ref_draft_session_forward(void * sp, const int32_t * tokens, const int32_t * positions, int n,
+                              const uint8_t * allow, float * hidden_out) {
+    return guarded([&] {
+        auto * s = static_cast<RefDraftSession *>(sp);
+        const int m = s->cache.len + n;
+        BitMask vis(n, m);
+        for (int r = 0; r < n; ++r)
+            for (int j = 0; j < m; ++j)
+                if (allow[static_cast<size_t>(r) * m + j]) vis.set(r, j);
+        std::vector<int> pos(positions, positions + n);
+        ForwardResult f = forward_raw(*s->b.draft.shared, {&s->b.draft.layer, 1}, std::span<const Token>(tokens, n), pos,
+                                      vis, s->cache, s->b.draft.shared->lm_head);
+        std::memcpy(hidden_out, f.hidden.row(0), sizeof(float) * static_cast<size_t>(n) * f.hidden.cols);
+    });
+}
+
 // masked_attention (kernels.cpp:124-171) with a dense 0/1 mask [n x m].
 int ref_masked_attention(const float * q, const float * k, const float * v, const uint8_t * allow, int n, int m,
                          int dh, int dv, float * out) {

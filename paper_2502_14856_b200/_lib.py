@@ -91,6 +91,11 @@ SIGNATURES = [
     ("frs_rng_uniforms", _I, [_P, _I, _P]),
     ("frs_draft_head_sample", _I, [_P, _P, _I, _I, _P, _I, _I, _P, _I, C.c_float, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("frs_count_frequencies_device", _I, [_P, _P, _I64, _I, _P, _P]),
+    ("frs_draft_model_create", _I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.POINTER(_P)]),
+    ("frs_draft_model_destroy", _I, [_P]),
+    ("frs_draft_model_truncate", _I, [_P, _I]),
+    ("frs_draft_model_length", _I, [_P, C.POINTER(_I)]),
+    ("frs_draft_model_forward", _I, [_P, _P, _P, _I, _P, _P, _P]),
     ("frs_masked_attention", _I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     ("frs_write_token_stream", _I, [C.c_char_p, _I, _P, _I64]),
     ("frs_read_token_stream", _I, [C.c_char_p, _P, _I64, C.POINTER(_I), C.POINTER(_I64)]),

@@ -153,6 +153,61 @@ def masked_attention(ctx: "Context", q: torch.Tensor, k: torch.Tensor, v: torch.
     return out
 
 
+def _mask_words(allow) -> np.ndarray:
+    """[n, m] bool -> the reference's BitMask words [n, ceil(m / 64)] (bit j = column j)."""
+    a = np.asarray(allow).astype(bool)
+    n, m = a.shape
+    stride = (m + 63) // 64
+    bits = np.zeros((n, stride * 64), np.uint8)
+    bits[:, :m] = a
+    w = np.packbits(bits.reshape(n, stride, 64)[:, :, ::-1], axis=2, bitorder="big").reshape(n, stride, 8)
+    return np.ascontiguousarray(w[:, :, ::-1]).view(np.uint64).reshape(n, stride)
+
+
+class DraftModel:
+    """The draft model's transformer layer on the device (model.cpp:208-281, forward_raw of a
+    1-layer draft) with its KV cache; bit-exact with the reference. weights: host fp32 arrays
+    embedding [V, d], wq / wk / wv / wo [d, d], w_up [4d, d], w_down [d, 4d] (x W^T), optional
+    attn_norm / mlp_norm / final_norm gains [d]."""
+
+    def __init__(self, ctx: "Context", weights: dict, heads: int, max_seq: int):
+        self.ctx = ctx
+        self._w = {k: np.ascontiguousarray(v, np.float32) for k, v in weights.items()}
+        V, d = self._w["embedding"].shape
+        self.V, self.d, self.heads, self.max_seq = V, d, heads, max_seq
+        g = lambda k: _np_ptr(self._w[k]) if k in self._w else None  # noqa: E731
+        h = C.c_void_p()
+        check(lib().frs_draft_model_create(ctx.handle, V, d, heads, max_seq, g("embedding"), g("wq"), g("wk"), g("wv"),
+                                           g("wo"), g("w_up"), g("w_down"), g("attn_norm"), g("mlp_norm"),
+                                           g("final_norm"), C.byref(h)), "draft_model")
+        self.handle = h
+
+    def __len__(self) -> int:
+        n = C.c_int()
+        check(lib().frs_draft_model_length(self.handle, C.byref(n)), "draft_model")
+        return n.value
+
+    def truncate(self, new_len: int) -> None:
+        check(lib().frs_draft_model_truncate(self.handle, new_len), "truncate")
+
+    def forward(self, tokens, positions, allow) -> torch.Tensor:
+        """forward_raw: allow [n, len + n] (cache rows visible to each token)."""
+        t, p = _i32(tokens), _i32(positions)
+        words = _mask_words(allow)
+        out = torch.empty((t.size, self.d), dtype=torch.float32, device=torch.device("cuda", self.ctx.device))
+        check(lib().frs_draft_model_forward(self.handle, _np_ptr(t), _np_ptr(p), t.size, _np_ptr(words), _ptr(out),
+                                            _stream(None)), "forward")
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and _lib._LIB is not None:
+                lib().frs_draft_model_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 def write_token_stream(path: str, vocab_size: int, tokens) -> None:
     """vocab.cpp:236-245: binary FRTK v1 token stream."""
     t = _i32(tokens)

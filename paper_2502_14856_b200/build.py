@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["frs_capi.cu", "frs_host.cu", "frs_exact.cu", "frs_misc.cu", "frs_fast.cu", "frs_tree.cu"]
+SOURCES = ["frs_capi.cu", "frs_host.cu", "frs_exact.cu", "frs_misc.cu", "frs_fast.cu", "frs_tree.cu", "frs_layer.cu"]
 
 
 def _stale(src: str, obj: str) -> bool:

@@ -62,6 +62,7 @@ struct frs_ctx {
     frs::DevBuf fast_ws;   // FAST path candidate/partials workspace
     frs::DevBuf fast_ctr;  // FAST counters: fallback queue (zeroed once)
     frs::DevBuf fast_logits;  // FAST batched drafting: approximate logits [n x V_sub] fp32
+    frs::DevBuf attn_scratch;  // masked_attention: per (head, query row) scores [heads x n x m] fp32
     frs::DevBuf trace;     // FAST main-kernel globaltimer stamps when FRS_TRACE is set (diagnostics)
     frs::DevBuf hbuf;      // host-API staging of hidden rows
     frs::DevBuf obuf;      // host-API staging of outputs

@@ -39,24 +39,31 @@ __device__ __forceinline__ float load_w(const __nv_bfloat16 *p) {
 // column (one thread per column). Rows that permit no key: FRS_FLAG_EMPTY_ROW (the reference
 // throws) and zeros.
 __global__ void __launch_bounds__(256)
-    k_masked_attention(const float *__restrict__ q, const float *__restrict__ k, const float *__restrict__ v,
-                       const unsigned long long *__restrict__ mask, int m, int dh, int dv, float *__restrict__ out,
-                       float *__restrict__ scratch, uint32_t *__restrict__ flags) {
+    k_masked_attention(const float *__restrict__ q, int q_ld, const float *__restrict__ k, int k_ld,
+                       const float *__restrict__ v, int v_ld, const unsigned long long *__restrict__ mask, int m,
+                       int dh, int dv, float *__restrict__ out, int out_ld, float *__restrict__ scratch,
+                       uint32_t *__restrict__ flags) {
+    // blockIdx.y = head: columns [y dh, (y + 1) dh) of q / k (y dv of v / out) — cols_slice
+    // (model.cpp:255-258); the mask is shared by the heads
     extern __shared__ float s_q[];
     __shared__ dev::ReduceScratch rs;
-    const int r = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    const int r = blockIdx.x, hd = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
+    q += (size_t)hd * dh;
+    k += (size_t)hd * dh;
+    v += (size_t)hd * dv;
+    out += (size_t)hd * dv;
     const int stride = (m + 63) >> 6;
     const unsigned long long *words = mask + (size_t)r * stride;
     auto allowed = [&](int j) { return ((words[j >> 6] >> (j & 63)) & 1ull) != 0; };
-    float *S = scratch + (size_t)r * m;
-    for (int c = tid; c < dh; c += nt) s_q[c] = q[(size_t)r * dh + c];
+    float *S = scratch + ((size_t)hd * gridDim.x + r) * m;
+    for (int c = tid; c < dh; c += nt) s_q[c] = q[(size_t)r * q_ld + c];
     dev::load_exp_table(rs.tab);
     __syncthreads();
     const float scale = __fdiv_rn(1.0f, __fsqrt_rn(static_cast<float>(dh)));
     for (int j0 = 0; j0 < m; j0 += nt / 8) {  // 8 lanes per key; whole warps in the dot
         const int j = j0 + (tid >> 3);
         const int jj = j < m ? j : m - 1;
-        const float d = dev::dot_f32_lanes8(s_q, k + (size_t)jj * dh, dh);
+        const float d = dev::dot_f32_lanes8(s_q, k + (size_t)jj * k_ld, dh);
         if ((tid & 7) == 0 && j < m && allowed(j)) S[j] = __fmul_rn(d, scale);
     }
     __syncthreads();
@@ -70,7 +77,7 @@ __global__ void __launch_bounds__(256)
     mx = dev::block_reduce(mx, dev::MaxF(), rs.f);
     any = dev::block_reduce(any, dev::OrI(), rs.i);
     if (!any) {
-        for (int c = tid; c < dv; c += nt) out[(size_t)r * dv + c] = 0.0f;
+        for (int c = tid; c < dv; c += nt) out[(size_t)r * out_ld + c] = 0.0f;
         if (tid == 0) flags[r] = FRS_FLAG_EMPTY_ROW;
         return;
     }
@@ -112,8 +119,8 @@ __global__ void __launch_bounds__(256)
     for (int c = tid; c < dv; c += nt) {  // key-ordered accumulation per column (kernels.cpp:162-167)
         float acc = 0.0f;
         for (int j = 0; j < m; ++j)
-            if (allowed(j)) acc = __fadd_rn(acc, __fmul_rn(S[j], __ldg(v + (size_t)j * dv + c)));
-        out[(size_t)r * dv + c] = acc;
+            if (allowed(j)) acc = __fadd_rn(acc, __fmul_rn(S[j], __ldg(v + (size_t)j * v_ld + c)));
+        out[(size_t)r * out_ld + c] = acc;
     }
     if (tid == 0) flags[r] = fl;
 }
@@ -446,18 +453,25 @@ int launch_softmax_sample(frs_ctx *ctx, const float *logits, int n, int v, float
     return FRS_OK;
 }
 
+int launch_masked_attention_strided(frs_ctx *ctx, const float *q, int q_ld, const float *k, int k_ld, const float *v,
+                                    int v_ld, const unsigned long long *mask, int n, int m, int dh, int dv, int heads,
+                                    float *out, int out_ld, uint32_t *flags, cudaStream_t s) {
+    int st = ctx->attn_scratch.ensure((size_t)heads * n * m * sizeof(float));
+    if (st) return st;
+    const size_t smem = (size_t)dh * sizeof(float);
+    if (smem > 48 * 1024)
+        FRS_CUDA_TRY(cudaFuncSetAttribute(k_masked_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ++ctx->launches;
+    k_masked_attention<<<dim3(n, heads), 256, smem, s>>>(q, q_ld, k, k_ld, v, v_ld, mask, m, dh, dv, out, out_ld,
+                                                         static_cast<float *>(ctx->attn_scratch.ptr), flags);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
 int launch_masked_attention(frs_ctx *ctx, const float *q, const float *k, const float *v,
                             const unsigned long long *mask, int n, int m, int dh, int dv, float *out, uint32_t *flags,
                             cudaStream_t s) {
-    int st = ctx->scratch.ensure((size_t)n * m * sizeof(float));
-    if (st) return st;
-    const size_t smem = (size_t)dh * sizeof(float);
-    if (smem > 48 * 1024) FRS_CUDA_TRY(cudaFuncSetAttribute(k_masked_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ++ctx->launches;
-    k_masked_attention<<<n, 256, smem, s>>>(q, k, v, mask, m, dh, dv, out, static_cast<float *>(ctx->scratch.ptr),
-                                            flags);
-    FRS_CUDA_TRY(cudaGetLastError());
-    return FRS_OK;
+    return launch_masked_attention_strided(ctx, q, dh, k, dh, v, dv, mask, n, m, dh, dv, 1, out, dv, flags, s);
 }
 
 int launch_softmax_probs(frs_ctx *ctx, const float *logits, int n, int v, float temperature, float *probs,

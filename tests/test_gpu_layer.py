@@ -1,0 +1,63 @@
+"""The draft transformer layer on the device (model.cpp:208-281):
+forward_raw of the reference's 1-layer draft (build_draft truncated) reproduced bit for bit —
+the hidden states after a causal context forward and after tree-shaped beam forwards on the
+growing KV cache — against the compiled reference running the same calls on its own cache."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2502_14856_b200 import api
+from paper_2502_14856_b200._lib import CapacityError
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("V,d,heads,seed", [(500, 64, 4, 7), (2000, 128, 8, 11), (3000, 96, 3, 5)])
+def test_draft_layer_forward_matches_reference(cuda_ctx, reference, V, d, heads, seed):
+    max_seq = 48
+    ref = reference.draft_session(V, d, heads, max_seq, seed)
+    dev = api.DraftModel(cuda_ctx, ref.weights(), heads, max_seq)
+    rng = np.random.default_rng(seed)
+    # 1. the pending context, causal (draft_forward without a tree mask)
+    ctx_toks = rng.integers(0, V, 6)
+    pos = np.arange(6)
+    allow = np.tril(np.ones((6, 6), np.uint8))
+    h_ref = ref.forward(ctx_toks, pos, allow)
+    h_dev = dev.forward(ctx_toks, pos, allow).cpu().numpy()
+    assert np.array_equal(h_dev, h_ref)
+    # 2. two tree levels: each beam row sees the context, its forwarded ancestors and itself;
+    #    positions = anchor + depth (drafting.cpp:180-196)
+    base, anchor = 6, 5
+    parents_rows = []  # cache row of each forwarded beam row
+    beam = [(int(t), -1, 1) for t in rng.integers(0, V, 4)]  # (token, parent cache row, depth)
+    for level in range(2):
+        n = len(beam)
+        m = len(dev) + n
+        allow = np.zeros((n, m), np.uint8)
+        allow[:, :base] = 1
+        for i, (tok, par, depth) in enumerate(beam):
+            a = par
+            while a >= 0:
+                allow[i, a] = 1
+                a = parents_rows[a - base] if a - base < len(parents_rows) else -1
+            allow[i, len(dev) + i] = 1
+        toks = [b[0] for b in beam]
+        pos = [anchor + b[2] for b in beam]
+        h_ref = ref.forward(toks, pos, allow)
+        h_dev = dev.forward(toks, pos, allow).cpu().numpy()
+        assert np.array_equal(h_dev, h_ref), level
+        first = len(dev) - n
+        parents_rows += [b[1] for b in beam]
+        beam = [(int(rng.integers(0, V)), first + (i % n), beam[i % n][2] + 1) for i in range(5)]
+
+
+def test_draft_layer_capacity_and_truncate(cuda_ctx, reference):
+    ref = reference.draft_session(300, 32, 2, 8, 3)
+    dev = api.DraftModel(cuda_ctx, ref.weights(), 2, 8)
+    dev.forward(np.arange(6), np.arange(6), np.tril(np.ones((6, 6), np.uint8)))
+    with pytest.raises(CapacityError, match="exceeds max_seq_len 8"):
+        dev.forward(np.arange(3), np.arange(6, 9), np.ones((3, 9), np.uint8))
+    dev.truncate(2)
+    assert len(dev) == 2
+    h = dev.forward([7], [2], np.ones((1, 3), np.uint8))
+    assert h.shape == (1, 32)
