@@ -217,6 +217,14 @@ FRS_API int frs_draft_model_truncate(frs_draft_model *m, int new_len);
 FRS_API int frs_draft_model_length(const frs_draft_model *m, int *len);
 FRS_API int frs_draft_model_forward(frs_draft_model *m, const int32_t *tokens, const int32_t *positions, int n,
                                     const uint64_t *visible, float *hidden_out, void *stream);
+typedef struct frs_rng frs_rng;
+/* build_draft_tree (drafting.cpp:122-245) driven by the device draft model: forwards the
+ * pending context (root = its last token) and each level's beam through frs_draft_model with
+ * the reference's positions and visibility, then truncates the cache back to the context.
+ * rng == NULL: greedy (mode EXACT / FAST); else sampled (EXACT). Outputs as frs_draft_tree. */
+FRS_API int frs_draft_tree_model(frs_head *head, frs_draft_model *draft, const int32_t *pending, int n_pending,
+                                 int width, int depth, int total, int mode, frs_rng *rng, int32_t *tokens,
+                                 int32_t *parents, int32_t *depths, double *log_joint, int *count);
 /* Sampled drafting (drafting.cpp:44-74): a std::mt19937_64 the caller owns (the reference's
  * `std::mt19937_64 * rng`), advanced by every draw exactly as the reference advances it. */
 typedef struct frs_rng frs_rng;

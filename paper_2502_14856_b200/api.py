@@ -619,6 +619,26 @@ def draft_head_sample(ctx: Context, h: torch.Tensor, head: "RestrictedHead", wid
     return out
 
 
+def build_draft_tree_model(head: "DeviceHead", draft: "DraftModel", pending, params: "DraftParams" = None,
+                           mode="exact", rng: Optional["Rng"] = None) -> "DraftTree":
+    """build_draft_tree (drafting.cpp:122-245) with the device draft model as the hidden-state
+    source (the reference's own drafting loop: pending context forward, per-level beam forwards
+    with tree visibility, cache truncated back). rng: sampled children (EXACT arithmetic)."""
+    params = params or DraftParams()
+    if rng is not None and mode != "exact":
+        raise ValueError("sampled drafting runs on the exact probabilities: mode must be 'exact'")
+    pend = _i32(pending)
+    total = params.total_draft_tokens
+    tok, par, dep = (np.empty(max(total, 1), np.int32) for _ in range(3))
+    lj, cnt = np.empty(max(total, 1), np.float64), C.c_int()
+    check(lib().frs_draft_tree_model(head.handle, draft.handle, _np_ptr(pend), pend.size, params.beam_width,
+                                     params.search_depth, total, _mode(mode), None if rng is None else rng.handle,
+                                     _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt)),
+          "build_draft_tree")
+    n = cnt.value
+    return DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy())
+
+
 class _DeviceView:
     """__cuda_array_interface__ view of a library-owned float32 device buffer."""
 

@@ -15,6 +15,11 @@
 
 #include "frs_common.cuh"
 
+// Candidate indices of the rows a hidden-state provider is asked to forward (level >= 1), for
+// the library's own model-driven provider (frs_draft_tree_model): the public callback carries
+// tokens and parent candidates only.
+static thread_local const int *tl_beam_cands = nullptr;
+
 struct frs_rng {
     std::mt19937_64 engine;
 };
@@ -452,6 +457,7 @@ int frs_draft_tree(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user
     std::vector<int32_t> btok, bpar;
     auto run_level = [&](int level, int nb) -> int {
         if (fn) {
+            tl_beam_cands = level == 0 ? nullptr : beam.data();
             const int rc = fn(user, level, nb, btok.data(), bpar.data(), hd, s);
             if (rc) return fail(FRS_ELOGIC, "hidden provider failed with code " + std::to_string(rc));
         } else {
@@ -668,6 +674,7 @@ int frs_draft_tree_sampled(frs_head *h, int32_t root_token, frs_hidden_fn fn, vo
     // one level: hidden rows, device sampling (or host replay), children appended in beam order
     auto run_level = [&](int level, int nb, const std::vector<int> &parents_of_rows) -> int {
         if (fn) {
+            tl_beam_cands = level == 0 ? nullptr : parents_of_rows.data();
             const int rc = fn(user, level, nb, btok.data(), bpar.data(), hd, s);
             if (rc) return fail(FRS_ELOGIC, "hidden provider failed with code " + std::to_string(rc));
         } else {
@@ -1055,6 +1062,96 @@ int frs_read_ranked_file(const char *path, int32_t *ids, int64_t capacity, int64
     if (!f.eof()) return fail(FRS_EDATA, p + ": unparsable token id at line " + std::to_string(k + 1));
     *n = k;
     return FRS_OK;
+}
+
+// build_draft_tree (drafting.cpp:122-245) with the device draft model as the hidden-state
+// source: the pending context forward (causal_layout, model.cpp:288-297), then per level the
+// beam rows at anchor position + depth seeing the cached prefix, their forwarded ancestors and
+// themselves (drafting.cpp:177-196); the cache is truncated back to the prefix afterwards
+// (drafting.cpp:225). rng == NULL: greedy; else sampled (EXACT arithmetic).
+struct ModelProvider {
+    frs_draft_model *dm;
+    const int32_t *pending;
+    int n_pending;
+    int base_len = 0, anchor_pos = 0, d = 0;
+    std::vector<int> cand_row, cand_parent;  // by candidate index (-1 unknown)
+    std::vector<int> positions;              // cache row -> position
+};
+
+static int model_provider_cb(void *user, int level, int n, const int32_t *tokens, const int32_t *parent_cands,
+                             float *hidden_dev, void *stream) {
+    auto *mp = static_cast<ModelProvider *>(user);
+    frs_draft_model *dm = mp->dm;
+    int len0 = 0;
+    frs_draft_model_length(dm, &len0);
+    if (level == 0) {  // the pending context, causal (the root is its last token)
+        const int np = mp->n_pending;
+        const int start = len0 > 0 ? mp->positions[len0 - 1] + 1 : 0;
+        std::vector<int32_t> pos(np);
+        const int m = len0 + np, words = (m + 63) / 64;
+        std::vector<uint64_t> vis((size_t)np * words, 0);
+        for (int i = 0; i < np; ++i) {
+            pos[i] = start + i;
+            for (int j = 0; j <= len0 + i; ++j) vis[(size_t)i * words + j / 64] |= 1ull << (j & 63);
+        }
+        float *tmp = nullptr;
+        if (cudaMalloc(&tmp, sizeof(float) * (size_t)np * mp->d) != cudaSuccess) return 2;
+        int rc = frs_draft_model_forward(dm, mp->pending, pos.data(), np, vis.data(), tmp, stream);
+        if (!rc && cudaMemcpyAsync(hidden_dev, tmp + (size_t)(np - 1) * mp->d, sizeof(float) * mp->d,
+                                   cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+            rc = 2;
+        cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+        cudaFree(tmp);
+        if (rc) return rc;
+        if (static_cast<int>(mp->positions.size()) < len0 + np) mp->positions.resize(len0 + np + 1024, 0);
+        for (int i = 0; i < np; ++i) mp->positions[len0 + i] = pos[i];
+        mp->base_len = len0 + np;
+        mp->anchor_pos = pos[np - 1];
+        return 0;
+    }
+    if (!tl_beam_cands) return 3;
+    const int m = len0 + n, words = (m + 63) / 64;
+    std::vector<int32_t> pos(n);
+    std::vector<uint64_t> vis((size_t)n * words, 0);
+    auto setb = [&](int i, int j) { vis[(size_t)i * words + j / 64] |= 1ull << (j & 63); };
+    for (int i = 0; i < n; ++i) {
+        const int c = tl_beam_cands[i];
+        if (c >= static_cast<int>(mp->cand_row.size())) {
+            mp->cand_row.resize(c + 1 + 1024, -1);
+            mp->cand_parent.resize(c + 1 + 1024, -1);
+        }
+        mp->cand_parent[c] = parent_cands[i];
+        mp->cand_row[c] = len0 + i;
+        pos[i] = mp->anchor_pos + level;  // depth of a level-L beam row is L
+        for (int j = 0; j < mp->base_len; ++j) setb(i, j);
+        for (int a = parent_cands[i]; a >= 0; a = mp->cand_parent[a]) setb(i, mp->cand_row[a]);
+        setb(i, len0 + i);
+    }
+    const int rc = frs_draft_model_forward(dm, tokens, pos.data(), n, vis.data(), hidden_dev, stream);
+    if (rc) return rc;
+    if (static_cast<int>(mp->positions.size()) < len0 + n) mp->positions.resize(len0 + n + 1024, 0);
+    for (int i = 0; i < n; ++i) mp->positions[len0 + i] = pos[i];
+    return 0;
+}
+
+int frs_draft_tree_model(frs_head *h, frs_draft_model *dm, const int32_t *pending, int n_pending, int width,
+                         int depth, int total, int mode, frs_rng *rng, int32_t *tokens, int32_t *parents,
+                         int32_t *depths, double *log_joint, int *count) {
+    FRS_REQUIRE(h && dm && pending, "build_draft_tree: null pointer");
+    if (n_pending < 1) return fail(FRS_EINVAL, "build_draft_tree: pending must end with the root token");
+    ModelProvider mp{dm, pending, n_pending};
+    int len0 = 0, maxs = 0;
+    frs_draft_model_length(dm, &len0);
+    mp.d = h->d;
+    maxs = 4096 + len0 + n_pending + width * depth;
+    mp.positions.assign(maxs, 0);
+    int st = rng ? frs_draft_tree_sampled(h, pending[n_pending - 1], model_provider_cb, &mp, nullptr, width, depth,
+                                          total, rng, tokens, parents, depths, log_joint, count)
+                 : frs_draft_tree(h, pending[n_pending - 1], model_provider_cb, &mp, nullptr, width, depth, total,
+                                  mode, tokens, parents, depths, log_joint, count);
+    tl_beam_cands = nullptr;
+    if (mp.base_len > 0) frs_draft_model_truncate(dm, mp.base_len);  // drafting.cpp:225
+    return st;
 }
 
 }  // extern "C"

@@ -61,3 +61,25 @@ def test_draft_layer_capacity_and_truncate(cuda_ctx, reference):
     assert len(dev) == 2
     h = dev.forward([7], [2], np.ones((1, 3), np.uint8))
     assert h.shape == (1, 32)
+
+
+@pytest.mark.parametrize("name", ["c1_capture_w4", "c1_capture_w10", "c1_sampled_w4_s11", "c1_sampled_w10_s5"])
+def test_model_driven_draft_tree_matches_reference(cuda_ctx, reference, name):
+    """The whole C1 drafting step on the GPU — draft transformer layer + FR head + beam
+    bookkeeping (greedy and sampled) — against the reference's own build_draft_tree trees."""
+    import hashlib
+    import json
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name + ".npz"))
+    cfg = json.loads(str(z["config"]))
+    W = reference.model_lm_head(cfg["V"], cfg["d"], cfg["layers"], cfg["heads"], cfg["seed"])
+    assert hashlib.sha256(W.tobytes()).hexdigest() == str(z["lm_head_sha256"])
+    sess = reference.draft_session(cfg["V"], cfg["d"], cfg["heads"], 64, cfg["seed"])
+    draft = api.DraftModel(cuda_ctx, sess.weights(), cfg["heads"], 64)
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(cfg["V"], z["ordered"]), dtype="f32")
+    params = api.DraftParams(int(z["width"]), int(z["depth"]), int(z["total"]))
+    rng = api.Rng(int(z["rng_seed"])) if "rng_seed" in z.files else None
+    tree = api.build_draft_tree_model(head, draft, cfg["pending"], params, mode="exact", rng=rng)
+    for key in ("tokens", "parents", "depths", "log_joint"):
+        assert np.array_equal(getattr(tree, key), z[key]), key
+    assert len(draft) == len(cfg["pending"])  # cache truncated back to the context (drafting.cpp:225)
