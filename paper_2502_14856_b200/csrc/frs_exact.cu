@@ -398,13 +398,43 @@ int launch_pass(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_r
 
 }  // namespace
 
+namespace {
+// Wide inputs (fewer than 4 rows fit in shared memory, e.g. the 4d-wide MLP down projection):
+// one 8-lane group per (row, output), the hidden row read from global memory (L1 / L2), the
+// same dot_f32 arithmetic (dev::dot_f32_lanes8, kernels.cpp:13-32).
+template <typename WT>
+__global__ void __launch_bounds__(256)
+    k_exact_logits_wide(const float *__restrict__ h, int n, int d, const WT *__restrict__ W, int v_rows,
+                        float *__restrict__ logits) {
+    const long long groups = (long long)n * v_rows;
+    const int per_block = blockDim.x >> 3;
+    for (long long base = (long long)blockIdx.x * per_block; base < groups; base += (long long)gridDim.x * per_block) {
+        const long long g = base + (threadIdx.x >> 3);  // block-uniform trip count: whole warps in the dot
+        const long long gg = g < groups ? g : groups - 1;
+        const int i = static_cast<int>(gg / v_rows), j = static_cast<int>(gg % v_rows);
+        const float v = dev::dot_f32_lanes8(h + (size_t)i * d, W + (size_t)j * d, d);
+        if ((threadIdx.x & 7) == 0 && g < groups) logits[(size_t)i * v_rows + j] = v;
+    }
+}
+}  // namespace
+
 int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *W, int w_dtype, int v_rows,
                         float *logits, cudaStream_t s) {
     // Rows per pass: as many as fit (<= 12) with the hidden rows resident in shared memory.
     const size_t per_row = (size_t)(d & ~7) * sizeof(float);
     int nb_cap = static_cast<int>(std::min<size_t>(12, ctx->smem_optin / std::max<size_t>(per_row, 1)));
     nb_cap &= ~3;
-    if (nb_cap < 4) return fail(FRS_ENOTSUP, "exact logits: hidden_dim too large for shared memory");
+    if (nb_cap < 4) {
+        const long long groups = (long long)n * v_rows;
+        const int blocks = (int)std::min<long long>((long long)ctx->sm_count * 8, (groups * 8 + 255) / 256);
+        ++ctx->launches;
+        if (w_dtype == FRS_DTYPE_BF16)  // bf16 words read as raw u16 (w_at widens them exactly)
+            k_exact_logits_wide<<<blocks, 256, 0, s>>>(h, n, d, static_cast<const unsigned short *>(W), v_rows, logits);
+        else
+            k_exact_logits_wide<<<blocks, 256, 0, s>>>(h, n, d, static_cast<const float *>(W), v_rows, logits);
+        FRS_CUDA_TRY(cudaGetLastError());
+        return FRS_OK;
+    }
     int st = ctx->counters.ensure(64 * sizeof(unsigned));
     if (st) return st;
     unsigned *counters = static_cast<unsigned *>(ctx->counters.ptr);

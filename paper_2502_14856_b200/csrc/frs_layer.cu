@@ -190,7 +190,7 @@ int frs_draft_model_forward(frs_draft_model *m, const int32_t *tokens, const int
     const int d = m->d, dh = d / m->heads, len0 = m->len, mm = len0 + n, words = (mm + 63) / 64;
     // work: x | normed | q | k | v | attn | tmp | up (4d) | rope cs | mask | tokens
     const size_t nd = (size_t)n * d;
-    const size_t need = (7 * nd + 4 * nd + (size_t)n * dh + 64) * sizeof(float) + (size_t)n * words * 8 + n * 4 + 256;
+    const size_t need = (7 * nd + 4 * nd + (size_t)n * dh + 64) * sizeof(float) + (size_t)n * words * 8 + (size_t)n * 8 + 256;
     int st = m->work.ensure(need);
     if (st) return st;
     float *x = static_cast<float *>(m->work.ptr), *normed = x + nd, *q = normed + nd, *k = q + nd, *v = k + nd,

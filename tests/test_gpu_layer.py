@@ -83,3 +83,17 @@ def test_model_driven_draft_tree_matches_reference(cuda_ctx, reference, name):
     for key in ("tokens", "parents", "depths", "log_joint"):
         assert np.array_equal(getattr(tree, key), z[key]), key
     assert len(draft) == len(cfg["pending"])  # cache truncated back to the context (drafting.cpp:225)
+
+
+def test_exact_logits_wide_inputs(cuda_ctx, restatement):
+    """Hidden widths whose rows no longer fit four to a CTA in shared memory (the 4d MLP down
+    projection at d = 4096 reads 16384-wide rows) take the global-memory dot_f32 kernel: same
+    bits as the reference's matmul."""
+    rng = np.random.default_rng(2)
+    V, d, n = 300, 16384 + 5, 3  # a dot_f32 tail too
+    W = (rng.standard_normal((V, d)) * 0.01).astype(np.float32)
+    h = rng.standard_normal((n, d)).astype(np.float32)
+    head = api.restrict_lm_head(cuda_ctx, torch.from_numpy(W).cuda(), api.RankedSubset(V, np.arange(V, dtype=np.int32)),
+                                dtype="f32")
+    out = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, 4, mode="exact", want_logits=True)
+    assert np.array_equal(out.logits.cpu().numpy(), restatement.logits(h, W))

@@ -246,9 +246,45 @@ def corpus_count(ctx, dev):
                           "GBps": n * 4 / us / 1e3, "tokens_per_s": n / us * 1e6}), flush=True)
 
 
+def draft_layer(ctx, dev, iters=10):
+    """The draft transformer layer (model.cpp:208-281, EXACT arithmetic) at the Llama-3-8B
+    shape (d = 4096, 32 heads, 4d MLP; fp32 weights): one 10-row beam forward on a 512-row
+    cache, and the whole model-driven sampled-free drafting step (6 levels x 10 rows + head)."""
+    d, heads, V = 4096, 32, 128256
+    rs = np.random.default_rng(0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    wt = lambda r, c: (torch.randn(r, c, generator=g, device=dev) * 0.02).cpu().numpy()  # noqa: E731
+    weights = {"embedding": wt(V, d), "wq": wt(d, d), "wk": wt(d, d), "wv": wt(d, d), "wo": wt(d, d),
+               "w_up": wt(4 * d, d), "w_down": wt(d, 4 * d)}
+    model = api.DraftModel(ctx, weights, heads, 1024)
+    ctx_len = 512
+    model.forward(rs.integers(0, V, ctx_len), np.arange(ctx_len), np.tril(np.ones((ctx_len, ctx_len), np.uint8)))
+    n = 10
+    allow = np.zeros((n, ctx_len + n), np.uint8)
+    allow[:, :ctx_len] = 1
+    allow[np.arange(n), ctx_len + np.arange(n)] = 1
+    toks = rs.integers(0, V, n)
+
+    def step(i):
+        model.truncate(ctx_len)
+        model.forward(toks, np.full(n, ctx_len), allow)
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(iters):
+        step(i)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1000 / iters
+    flops = 2 * n * (4 * d * d + 8 * d * d)
+    print(json.dumps({"sweep": "draft_layer", "d": d, "heads": heads, "rows": n, "cache_rows": ctx_len,
+                      "ms_per_forward": ms, "weight_bytes": 12 * d * d * 4,
+                      "GBps_weights": 12 * d * d * 4 / (ms * 1e-3) / 1e9, "GFLOPs": flops / (ms * 1e-3) / 1e9}),
+          flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="draft,batched,verify,decode,sampled,stochastic,count")
+    ap.add_argument("--what", default="draft,batched,verify,decode,sampled,stochastic,count,layer")
     ap.add_argument("--exact", action="store_true", help="also time the EXACT draft level")
     ap.add_argument("--decode-iters", type=int, default=100)
     a = ap.parse_args()
@@ -269,6 +305,8 @@ def main():
         stochastic_verify(ctx, dev)
     if "count" in what:
         corpus_count(ctx, dev)
+    if "layer" in what:
+        draft_layer(ctx, dev)
 
 
 if __name__ == "__main__":
