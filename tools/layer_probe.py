@@ -24,3 +24,13 @@ for _ in range(2):
     model.forward(rs.integers(0, V, n), np.full(n, ctx_len), allow)
 torch.cuda.synchronize()
 print("ok")
+import time  # noqa: E402
+toks = rs.integers(0, V, n)
+for trial in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        model.truncate(ctx_len)
+        model.forward(toks, np.full(n, ctx_len), allow)
+    torch.cuda.synchronize()
+    print("forward ms", round((time.perf_counter() - t0) * 1000 / 5, 3), flush=True)

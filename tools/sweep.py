@@ -269,6 +269,7 @@ def draft_layer(ctx, dev, iters=10):
         model.truncate(ctx_len)
         model.forward(toks, np.full(n, ctx_len), allow)
 
+    step(0)  # warm-up: lazy module loading of the kernel variants
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for i in range(iters):
