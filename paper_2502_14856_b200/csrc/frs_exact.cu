@@ -258,7 +258,7 @@ template <int NB, typename WT>
 __global__ void __launch_bounds__(1024, 1)
     k_exact_logits(const float *__restrict__ h, int n, int d, const WT *__restrict__ W, int v_rows,
                    float *__restrict__ logits, int ld, unsigned *__restrict__ counter) {
-    constexpr int NBS = (NB + 3) & ~3;
+    constexpr int NBS = NB <= 2 ? NB : (NB + 3) & ~3;  // 1-2 rows: unpadded (wide inputs)
     constexpr int U = 16;  // W prefetch depth (loads in flight per thread)
     extern __shared__ float4 smem4[];
     float *sh = reinterpret_cast<float *>(smem4);
@@ -291,8 +291,12 @@ __global__ void __launch_bounds__(1024, 1)
             for (int u = 0; u < U; ++u) w[u] = load_w(wr + (size_t)(t + u) * 8);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const float4 *hp = reinterpret_cast<const float4 *>(sh + ((t + u) * 8 + l) * NBS);
                 float hv[NBS];
+                if constexpr (NBS < 4) {
+#pragma unroll
+                    for (int c = 0; c < NBS; ++c) hv[c] = sh[((t + u) * 8 + l) * NBS + c];
+                }
+                const float4 *hp = reinterpret_cast<const float4 *>(sh + ((t + u) * 8 + l) * NBS);
 #pragma unroll
                 for (int c = 0; c < NBS / 4; ++c) {
                     const float4 v = hp[c];
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(1024)
 template <int NB, typename WT>
 int launch_nb(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_rows, float *logits, unsigned *counter,
               cudaStream_t s) {
-    constexpr int NBS = (NB + 3) & ~3;
+    constexpr int NBS = NB <= 2 ? NB : (NB + 3) & ~3;
     const size_t smem = (size_t)(d & ~7) * NBS * sizeof(float);
     auto kern = k_exact_logits<NB, WT>;
     FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -423,8 +427,8 @@ int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *
     // Rows per pass: as many as fit (<= 12) with the hidden rows resident in shared memory.
     const size_t per_row = (size_t)(d & ~7) * sizeof(float);
     int nb_cap = static_cast<int>(std::min<size_t>(12, ctx->smem_optin / std::max<size_t>(per_row, 1)));
-    nb_cap &= ~3;
-    if (nb_cap < 4) {
+    nb_cap = nb_cap >= 4 ? (nb_cap & ~3) : std::min(nb_cap, 2);  // 1-2 unpadded rows for wide inputs
+    if (nb_cap < 1) {
         const long long groups = (long long)n * v_rows;
         const int blocks = (int)std::min<long long>((long long)ctx->sm_count * 8, (groups * 8 + 255) / 256);
         ++ctx->launches;
