@@ -39,6 +39,9 @@ __device__ __forceinline__ float load_w(const __nv_bfloat16 *p) {
 // softmax_probs_row, then out[c] = Σ_j (e_j * inv) * v[j][c] accumulated in key order per
 // column (one thread per column). Rows that permit no key: FRS_FLAG_EMPTY_ROW (the reference
 // throws) and zeros.
+constexpr int kAttnKeys = 64;  // value rows staged per chunk (one 64-bit mask word)
+constexpr int kAttnCols = 4;   // value columns per thread (dv <= 4 x 256)
+
 __global__ void __launch_bounds__(256)
     k_masked_attention(const float *__restrict__ q, int q_ld, const float *__restrict__ k, int k_ld,
                        const float *__restrict__ v, int v_ld, const unsigned long long *__restrict__ mask, int m,
@@ -117,12 +120,59 @@ __global__ void __launch_bounds__(256)
     for (int j = tid; j < m; j += nt)
         if (allowed(j)) S[j] = __fmul_rn(S[j], inv);
     __syncthreads();
-    for (int c = tid; c < dv; c += nt) {  // key-ordered accumulation per column (kernels.cpp:162-167)
-        float acc = 0.0f;
-        for (int j = 0; j < m; ++j)
-            if (allowed(j)) acc = __fadd_rn(acc, __fmul_rn(S[j], __ldg(v + (size_t)j * v_ld + c)));
-        out[(size_t)r * out_ld + c] = acc;
+    // key-ordered accumulation per column (kernels.cpp:162-167): the values arrive in chunks of
+    // kAttnKeys keys staged in shared memory by the whole CTA (coalesced rows), so the per-key
+    // dependent adds wait on shared-memory latency instead of one L2 round trip per key
+    float *s_v = s_q + ((dh + 3) & ~3), *s_p = s_v + (size_t)kAttnKeys * dv;
+    const bool vec4 = (dv & 3) == 0 && (v_ld & 3) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0;
+    float acc[kAttnCols];
+#pragma unroll
+    for (int u = 0; u < kAttnCols; ++u) acc[u] = 0.0f;
+    for (int j0 = 0; j0 < m; j0 += kAttnKeys) {
+        const int nk = min(kAttnKeys, m - j0);
+        __syncthreads();
+        if (vec4) {  // all of a thread's loads of the chunk in flight at once
+            const int dv4 = dv >> 2, n4 = nk * dv4;
+            for (int base = 0; base < n4; base += nt * 8) {
+                float4 tmp[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int idx = base + u * nt + tid;
+                    if (idx < n4) {
+                        const int jj = idx / dv4, c4 = idx - jj * dv4;
+                        tmp[u] = __ldg(reinterpret_cast<const float4 *>(v + (size_t)(j0 + jj) * v_ld) + c4);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int idx = base + u * nt + tid;
+                    if (idx < n4) reinterpret_cast<float4 *>(s_v)[idx] = tmp[u];
+                }
+            }
+        } else {
+            for (int idx = tid; idx < nk * dv; idx += nt) {
+                const int jj = idx / dv, c = idx - jj * dv;
+                s_v[idx] = __ldg(v + (size_t)(j0 + jj) * v_ld + c);
+            }
+        }
+        for (int jj = tid; jj < nk; jj += nt) s_p[jj] = S[j0 + jj];
+        __syncthreads();
+        const unsigned long long bits = words[j0 >> 6];  // kAttnKeys == 64: one mask word
+#pragma unroll
+        for (int u = 0; u < kAttnCols; ++u) {
+            const int c = tid + u * nt;
+            if (c < dv) {
+                float a = acc[u];
+#pragma unroll 8
+                for (int jj = 0; jj < nk; ++jj)
+                    if ((bits >> jj) & 1ull) a = __fadd_rn(a, __fmul_rn(s_p[jj], s_v[jj * dv + c]));
+                acc[u] = a;
+            }
+        }
     }
+#pragma unroll
+    for (int u = 0; u < kAttnCols; ++u)
+        if (tid + u * nt < dv) out[(size_t)r * out_ld + tid + u * nt] = acc[u];
     if (tid == 0) flags[r] = fl;
 }
 
@@ -706,7 +756,8 @@ int launch_masked_attention_strided(frs_ctx *ctx, const float *q, int q_ld, cons
                                     float *out, int out_ld, uint32_t *flags, cudaStream_t s) {
     int st = ctx->attn_scratch.ensure((size_t)heads * n * m * sizeof(float));
     if (st) return st;
-    const size_t smem = (size_t)dh * sizeof(float);
+    if (dv > kAttnCols * 256) return fail(FRS_ENOTSUP, "masked_attention: value width above 1024");
+    const size_t smem = (size_t)(((dh + 3) & ~3) + kAttnKeys * dv + kAttnKeys) * sizeof(float);
     if (smem > 48 * 1024)
         FRS_CUDA_TRY(cudaFuncSetAttribute(k_masked_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ++ctx->launches;
