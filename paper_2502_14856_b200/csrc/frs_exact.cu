@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256)
                 s_v[idx] = __ldg(v + (size_t)(j0 + jj) * v_ld + c);
             }
         }
-        for (int jj = tid; jj < nk; jj += nt) s_p[jj] = S[j0 + jj];
+        for (int jj = tid; jj < nk; jj += nt) s_p[jj] = allowed(j0 + jj) ? S[j0 + jj] : 0.0f;  // masked: never written
         __syncthreads();
         const unsigned long long bits = words[j0 >> 6];  // kAttnKeys == 64: one mask word
 #pragma unroll
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(32 + 64 * (gv::NMAX / 2))
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             bar_init(&full[s], 1);
-            bar_init(&empty[s], 2 * S);
+            bar_init(&empty[s], 2 * S * 32);  // every consumer lane releases its own reads
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -623,8 +623,7 @@ __global__ void __launch_bounds__(32 + 64 * (gv::NMAX / 2))
                     a1[j] = __fadd_rn(a1[j], __fmul_rn(y[j], w[j]));
                 }
             }
-            __syncwarp();
-            if (lane == 0) bar_arrive(&empty[st]);
+            bar_arrive(&empty[st]);
         }
         // ((s0+s1)+(s2+s3)) + ((s4+s5)+(s6+s7)): cq 0 holds s0..s3, cq 1 holds s4..s7
         float q0 = __fadd_rn(__fadd_rn(a0[0], a0[1]), __fadd_rn(a0[2], a0[3]));

@@ -28,6 +28,16 @@ def main():
     hv = torch.from_numpy(rng.standard_normal((5, d)).astype(np.float32)).cuda()
     api.verify_head_argmax(ctx, hv, W.to(torch.bfloat16), mode="fast")
     api.verify_head_argmax(ctx, hv, W, mode="exact")
+    # the draft layer (staged exact GEMV with a K tail chunk, tree attention, norms, RoPE, SiLU)
+    dm, heads, Vm = 264, 4, 500
+    wt = lambda r, c: (rng.standard_normal((r, c)) * 0.05).astype(np.float32)  # noqa: E731
+    model = api.DraftModel(ctx, {"embedding": wt(Vm, dm), "wq": wt(dm, dm), "wk": wt(dm, dm), "wv": wt(dm, dm),
+                                 "wo": wt(dm, dm), "w_up": wt(4 * dm, dm), "w_down": wt(dm, 4 * dm)}, heads, 256)
+    model.forward(rng.integers(0, Vm, 70), np.arange(70), np.tril(np.ones((70, 70), np.uint8)))
+    allow = np.zeros((3, 73), np.uint8)
+    allow[:, :70] = 1
+    allow[np.arange(3), 70 + np.arange(3)] = 1
+    model.forward(rng.integers(0, Vm, 3), np.full(3, 70), allow)
     torch.cuda.synchronize()
     print("sanitize workload done")
 
