@@ -281,6 +281,25 @@ def draft_layer(ctx, dev, iters=10):
                       "ms_per_forward": ms, "weight_bytes": 12 * d * d * 4,
                       "GBps_weights": 12 * d * d * 4 / (ms * 1e-3) / 1e9, "GFLOPs": flops / (ms * 1e-3) / 1e9}),
           flush=True)
+    # the whole drafting step (build_draft_tree with the draft model as the hidden-state source):
+    # pending forward + 5 beam-level forwards + 6 FR-head levels (V_sub 32768) + bookkeeping
+    model.truncate(ctx_len)
+    lm = (torch.randn(V, d, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    sub = api.RankedSubset(V, rs.permutation(V)[:32768].astype(np.int32))
+    pending = rs.integers(0, V, 4)
+    for mode, dtype in (("fast", "bf16"), ("exact", "f32")):
+        head = api.DeviceHead(ctx, lm if dtype == "bf16" else lm.float(), sub, dtype=dtype)
+        api.build_draft_tree_model(head, model, pending, api.DraftParams(10, 6, 60), mode=mode)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(iters):
+            tree = api.build_draft_tree_model(head, model, pending, api.DraftParams(10, 6, 60), mode=mode)
+        torch.cuda.synchronize()
+        ms_tree = (time.perf_counter() - t0) * 1000 / iters
+        print(json.dumps({"sweep": "model_draft_tree", "mode": mode, "head_dtype": dtype, "d": d, "vocab": V,
+                          "v_sub": 32768, "context_rows": ctx_len, "pending": int(pending.size),
+                          "width_depth_total": [10, 6, 60], "nodes": len(tree), "ms_per_tree": ms_tree}), flush=True)
+        del head
 
 
 def main():
