@@ -9,13 +9,14 @@
 //                                          index order; inv = (float)(1/total); p = e*inv.
 //   topk / argmax      kernels.cpp:93-122  (value desc, index asc); argmax strict '>' => lowest index.
 //
-// Layout: the LM-head slab is row-major [rows x d] (fp32 or bf16). One persistent CTA per SM
-// (1024 threads) keeps the NB hidden rows resident in shared memory as sh[e*NBS + i] =
-// h[i][e]; each warp pulls groups of 4 slab rows from an atomic work queue and maps lane =
-// 8*q + l to (row q of the group, dot_f32 lane chain l). The chain order is therefore the
-// reference's exactly; the final tree is three xor-shuffles (1, 2, 4) whose association is
-// the reference's tree. Bound: FP32 issue (2 instructions per MAC, __fmul_rn/__fadd_rn keep
-// ptxas from contracting into FFMA), ~72 us at 1965 MHz for n=10, V_sub=32768, d=4096.
+// Exact logits: k_exact_gemv (below; operands staged by bulk copies through an mbarrier ring,
+// one dot_f32 chain quad per lane) whenever d % 8 == 0 and the rows are 16-byte aligned, else
+// k_exact_logits: one persistent CTA per SM (1024 threads) keeps the NB hidden rows resident in
+// shared memory as sh[e*NBS + i] = h[i][e]; each warp pulls groups of 4 slab rows from an
+// atomic work queue and maps lane = 8*q + l to (row q of the group, dot_f32 lane chain l). In
+// both the chain order is the reference's exactly and the final tree has the reference's
+// association. __fmul_rn/__fadd_rn keep ptxas from contracting into FFMA (2 FP32 instructions
+// per MAC).
 #include <cuda_bf16.h>
 
 #include <algorithm>
