@@ -188,6 +188,17 @@ int frs_draft_model_forward(frs_draft_model *m, const int32_t *tokens, const int
     FRS_CUDA_TRY(cudaSetDevice(ctx->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int d = m->d, dh = d / m->heads, len0 = m->len, mm = len0 + n, words = (mm + 63) / 64;
+    // a query row that permits no key: the reference's masked_attention throws (kernels.cpp);
+    // the mask is host data, so this is decided here without a device round trip
+    for (int r = 0; r < n; ++r) {
+        bool any = false;
+        for (int w = 0; w < words && !any; ++w) {
+            uint64_t bits = visible[(size_t)r * words + w];
+            if (w == words - 1 && (mm & 63)) bits &= (1ull << (mm & 63)) - 1ull;
+            any = bits != 0;
+        }
+        if (!any) return fail(FRS_EINVAL, "masked_attention: query row " + std::to_string(r) + " permits no keys");
+    }
     // work: x | normed | q | k | v | attn | tmp | up (4d) | rope cs | mask | tokens
     const size_t nd = (size_t)n * d;
     const size_t need = (7 * nd + 4 * nd + (size_t)n * dh + 64) * sizeof(float) + (size_t)n * words * 8 + (size_t)n * 8 + 256;
@@ -237,12 +248,6 @@ int frs_draft_model_forward(frs_draft_model *m, const int32_t *tokens, const int
     frs::k_rmsnorm_rows<<<n, 256, 0, s>>>(x, d, m->fn, hidden_out);                  // model.cpp:271
     FRS_CUDA_TRY(cudaGetLastError());
     ctx->launches += 8;
-    std::vector<uint32_t> hf(n);
-    FRS_CUDA_TRY(cudaMemcpyAsync(hf.data(), fl, n * 4, cudaMemcpyDeviceToHost, s));
-    FRS_CUDA_TRY(cudaStreamSynchronize(s));
-    for (int r = 0; r < n; ++r)
-        if (hf[r] & FRS_FLAG_EMPTY_ROW)
-            return fail(FRS_EINVAL, "masked_attention: query row " + std::to_string(r) + " permits no keys");
     for (int i = 0; i < n; ++i) m->positions[len0 + i] = positions[i];
     m->len = mm;
     return FRS_OK;

@@ -61,6 +61,13 @@ def test_draft_layer_capacity_and_truncate(cuda_ctx, reference):
     assert len(dev) == 2
     h = dev.forward([7], [2], np.ones((1, 3), np.uint8))
     assert h.shape == (1, 32)
+    # a query row that permits no key: the reference's masked_attention rejects it; nothing is
+    # appended to the cache
+    allow = np.ones((2, 5), np.uint8)
+    allow[1] = 0
+    with pytest.raises(ValueError, match="permits no keys"):
+        dev.forward([1, 2], [3, 4], allow)
+    assert len(dev) == 3
 
 
 @pytest.mark.parametrize("name", ["c1_capture_w4", "c1_capture_w10", "c1_sampled_w4_s11", "c1_sampled_w10_s5"])
