@@ -105,6 +105,29 @@ struct frs_draft_model {
     frs::DevBuf kc, vc, work;
     float *emb, *wq, *wk, *wv, *wo, *wup, *wdown, *an, *mn, *fn;
     std::vector<int> positions;
+    // RoPE cos / sin per position (model.cpp:50-54 with the host's libm), filled on first use:
+    // the values depend only on (position, pair index), so a cache returns the same floats
+    std::vector<std::vector<float>> rope;
+    const float *rope_row(int pos) {
+        const int dh = d / heads;
+        auto fill = [&](std::vector<float> &cs) {
+            cs.resize((size_t)dh);
+            for (int i = 0; i + 1 < dh; i += 2) {
+                const float freq = std::pow(10000.0f, -static_cast<float>(i) / dh);
+                const float angle = static_cast<float>(pos) * freq;
+                cs[(size_t)(i / 2) * 2] = std::cos(angle);
+                cs[(size_t)(i / 2) * 2 + 1] = std::sin(angle);
+            }
+        };
+        if (pos < 0 || pos >= 4 * max_seq) {  // outside the cached range: computed each time
+            static thread_local std::vector<float> tmp;
+            fill(tmp);
+            return tmp.data();
+        }
+        if ((size_t)pos >= rope.size()) rope.resize((size_t)pos + 1);
+        if (rope[pos].empty()) fill(rope[pos]);
+        return rope[pos].data();
+    }
 };
 
 extern "C" {
@@ -211,15 +234,8 @@ int frs_draft_model_forward(frs_draft_model *m, const int32_t *tokens, const int
     auto *tok_dev = reinterpret_cast<int32_t *>(mask + (size_t)n * words);
     // host: the RoPE cos / sin with the reference's own libm calls (model.cpp:50-54)
     std::vector<float> hcs((size_t)n * dh);
-    for (int r = 0; r < n; ++r) {
-        const float pos = static_cast<float>(positions[r]);
-        for (int i = 0; i + 1 < dh; i += 2) {
-            const float freq = std::pow(10000.0f, -static_cast<float>(i) / dh);
-            const float angle = pos * freq;
-            hcs[((size_t)r * (dh / 2) + i / 2) * 2] = std::cos(angle);
-            hcs[((size_t)r * (dh / 2) + i / 2) * 2 + 1] = std::sin(angle);
-        }
-    }
+    const size_t rs = (size_t)(dh / 2) * 2;  // k_rope's row stride
+    for (int r = 0; r < n; ++r) std::memcpy(hcs.data() + (size_t)r * rs, m->rope_row(positions[r]), sizeof(float) * rs);
     FRS_CUDA_TRY(cudaMemcpyAsync(cs, hcs.data(), hcs.size() * sizeof(float), cudaMemcpyHostToDevice, s));
     FRS_CUDA_TRY(cudaMemcpyAsync(mask, visible, (size_t)n * words * 8, cudaMemcpyHostToDevice, s));
     FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, tokens, n * 4, cudaMemcpyHostToDevice, s));
