@@ -163,9 +163,19 @@ __global__ void __launch_bounds__(256)
         for (int u = 0; u < kAttnCols; ++u) {
             const int c = tid + u * nt;
             if (c < dv) {
+                // operands read unconditionally (shared memory), so the loads of a batch issue
+                // ahead of the key-ordered add chain; only the add is predicated on the mask
                 float a = acc[u];
-#pragma unroll 8
-                for (int jj = 0; jj < nk; ++jj)
+                int jj = 0;
+                for (; jj + 8 <= nk; jj += 8) {
+                    float pr[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) pr[e] = __fmul_rn(s_p[jj + e], s_v[(jj + e) * dv + c]);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if ((bits >> (jj + e)) & 1ull) a = __fadd_rn(a, pr[e]);
+                }
+                for (; jj < nk; ++jj)
                     if ((bits >> jj) & 1ull) a = __fadd_rn(a, __fmul_rn(s_p[jj], s_v[jj * dv + c]));
                 acc[u] = a;
             }
