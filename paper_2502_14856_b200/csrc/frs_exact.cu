@@ -40,6 +40,41 @@ __device__ __forceinline__ float load_w(const __nv_bfloat16 *p) {
 // softmax_probs_row, then out[c] = Σ_j (e_j * inv) * v[j][c] accumulated in key order per
 // column (one thread per column). Rows that permit no key: FRS_FLAG_EMPTY_ROW (the reference
 // throws) and zeros.
+// Two dot_f32 products (kernels.cpp:13-32: 8 lane chains, then the reference's tree) of h with
+// rows wa and wb, the words of both rows requested 16 chain steps at a time.
+__device__ __forceinline__ float2 dot2_lanes8(const float *h, const float *wa, const float *wb, int d) {
+    const int l = threadIdx.x & 7;
+    const int T = d >> 3;
+    float sa = 0.0f, sb = 0.0f;
+    for (int t0 = 0; t0 < T; t0 += 16) {
+        float va[16], vb[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const bool in = t0 + u < T;
+            va[u] = in ? __ldg(wa + 8 * (t0 + u) + l) : 0.0f;
+            vb[u] = in ? __ldg(wb + 8 * (t0 + u) + l) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (t0 + u < T) {
+                const float x = h[8 * (t0 + u) + l];
+                sa = __fadd_rn(sa, __fmul_rn(x, va[u]));
+                sb = __fadd_rn(sb, __fmul_rn(x, vb[u]));
+            }
+    }
+#pragma unroll
+    for (int o = 1; o <= 4; o <<= 1) {
+        sa = __fadd_rn(sa, __shfl_xor_sync(0xffffffffu, sa, o));
+        sb = __fadd_rn(sb, __shfl_xor_sync(0xffffffffu, sb, o));
+    }
+    if (l == 0)
+        for (int e = 8 * T; e < d; ++e) {
+            sa = __fadd_rn(sa, __fmul_rn(h[e], __ldg(wa + e)));
+            sb = __fadd_rn(sb, __fmul_rn(h[e], __ldg(wb + e)));
+        }
+    return make_float2(sa, sb);
+}
+
 constexpr int kAttnKeys = 64;  // value rows staged per chunk (one 64-bit mask word)
 constexpr int kAttnCols = 4;   // value columns per thread (dv <= 4 x 256)
 
@@ -65,11 +100,13 @@ __global__ void __launch_bounds__(256)
     dev::load_exp_table(rs.tab);
     __syncthreads();
     const float scale = __fdiv_rn(1.0f, __fsqrt_rn(static_cast<float>(dh)));
-    for (int j0 = 0; j0 < m; j0 += nt / 8) {  // 8 lanes per key; whole warps in the dot
-        const int j = j0 + (tid >> 3);
-        const int jj = j < m ? j : m - 1;
-        const float d = dev::dot_f32_lanes8(s_q, k + (size_t)jj * k_ld, dh);
-        if ((tid & 7) == 0 && j < m && allowed(j)) S[j] = __fmul_rn(d, scale);
+    for (int j0 = 0; j0 < m; j0 += nt / 4) {  // 8 lanes per key, two keys per lane group at once
+        const int ja = j0 + (tid >> 3), jb = ja + nt / 8;
+        const float2 dd = dot2_lanes8(s_q, k + (size_t)min(ja, m - 1) * k_ld, k + (size_t)min(jb, m - 1) * k_ld, dh);
+        if ((tid & 7) == 0) {
+            if (ja < m && allowed(ja)) S[ja] = __fmul_rn(dd.x, scale);
+            if (jb < m && allowed(jb)) S[jb] = __fmul_rn(dd.y, scale);
+        }
     }
     __syncthreads();
     float mx = -__int_as_float(0x7f800000);
