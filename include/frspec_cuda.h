@@ -217,6 +217,15 @@ FRS_API int frs_draft_model_truncate(frs_draft_model *m, int new_len);
 FRS_API int frs_draft_model_length(const frs_draft_model *m, int *len);
 FRS_API int frs_draft_model_forward(frs_draft_model *m, const int32_t *tokens, const int32_t *positions, int n,
                                     const uint64_t *visible, float *hidden_out, void *stream);
+/* KVCache::positions[row] (model.cpp:280, 288-297): the position cached row `row` was forwarded
+ * at; FRS_EINVAL outside [0, len). */
+FRS_API int frs_draft_model_position(const frs_draft_model *m, int row, int *pos);
+/* KVCache::compact (model.cpp:165-196): keeps cached rows keep_from + kept_offsets[i] (ascending,
+ * < len) at keep_from + i with their positions; len = keep_from + n_kept. FRS_EINVAL for a bad
+ * keep_from or offsets (nothing moved); FRS_ELOGIC when the kept positions are not contiguous
+ * (raised after the move, as the reference's std::logic_error is). */
+FRS_API int frs_draft_model_compact(frs_draft_model *m, int keep_from, const int32_t *kept_offsets, int n_kept,
+                                    void *stream);
 typedef struct frs_rng frs_rng;
 /* build_draft_tree (drafting.cpp:122-245) driven by the device draft model: forwards the
  * pending context (root = its last token) and each level's beam through frs_draft_model with

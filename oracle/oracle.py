@@ -253,6 +253,11 @@ class Reference:
         L.ref_draft_session_free.argtypes = [C.c_void_p]
         L.ref_draft_session_weights.argtypes = [C.c_void_p] + [_f32p] * 7
         L.ref_draft_session_forward.argtypes = [C.c_void_p, _i32p, _i32p, C.c_int, C.c_void_p, _f32p]
+        L.ref_draft_session_len.argtypes = [C.c_void_p]
+        L.ref_draft_session_position.argtypes = [C.c_void_p, C.c_int]
+        L.ref_draft_session_compact.argtypes = [C.c_void_p, C.c_int, _i32p, C.c_int]
+        L.ref_draft_session_draft_tree.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _i32p, C.c_int, C.c_int, C.c_int,
+                                                   C.c_int, _i32p, _i32p, _i32p, _f64p, _ip]
         L.ref_masked_attention.argtypes = [_f32p, _f32p, _f32p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _f32p]
         L.ref_read_token_stream.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, _ip, C.POINTER(C.c_int64)]
         L.ref_read_token_stream_text.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
@@ -457,6 +462,30 @@ class Reference:
                 out = np.empty((t.size, d), np.float32)
                 ref._check(ref.lib.ref_draft_session_forward(self.h, t, p, t.size, a.ctypes.data, out), "forward_raw")
                 return out
+
+            def __len__(self):
+                return ref.lib.ref_draft_session_len(self.h)
+
+            def position(self, row):
+                return ref.lib.ref_draft_session_position(self.h, row)
+
+            def compact(self, keep_from, offsets):
+                o = _ci32(offsets)
+                ref._check(ref.lib.ref_draft_session_compact(self.h, keep_from, o, o.size), "compact")
+
+            def draft_tree(self, ordered, pending, width, depth, total):
+                """build_draft_tree on this session's persistent cache (greedy)."""
+                o = None if ordered is None else _ci32(ordered)
+                p = _ci32(pending)
+                tok, par, dep = (np.empty(total, np.int32) for _ in range(3))
+                lj = np.empty(total, np.float64)
+                cnt = C.c_int()
+                ref._check(ref.lib.ref_draft_session_draft_tree(self.h, o, 0 if o is None else o.size, p, p.size, width,
+                                                                depth, total, tok, par, dep, lj, C.byref(cnt)),
+                           "build_draft_tree")
+                n = cnt.value
+                return dict(tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(),
+                            log_joint=lj[:n].copy())
 
             def __del__(self):
                 ref.lib.ref_draft_session_free(self.h)

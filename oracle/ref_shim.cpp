@@ -310,6 +310,38 @@ int ref_draft_session_forward(void * sp, const int32_t * tokens, const int32_t *
     });
 }
 
+int ref_draft_session_len(void * sp) { return static_cast<RefDraftSession *>(sp)->cache.len; }
+int ref_draft_session_position(void * sp, int row) { return static_cast<RefDraftSession *>(sp)->cache.positions[row]; }
+// KVCache::compact (model.cpp:165-196) on the session cache.
+int ref_draft_session_compact(void * sp, int keep_from, const int32_t * offs, int n) {
+    return guarded([&] {
+        auto * s = static_cast<RefDraftSession *>(sp);
+        std::vector<int> o(offs, offs + n);
+        s->cache.compact(keep_from, o);
+    });
+}
+// build_draft_tree (greedy, restricted head over `ordered` when non-null) on the session's
+// persistent cache: a second call drafts after the first call's context, as a decode loop does.
+int ref_draft_session_draft_tree(void * sp, const int32_t * ordered, int v_sub, const int32_t * pending, int n_pending,
+                                 int width, int depth, int total, int32_t * tokens, int32_t * parents,
+                                 int32_t * depths, double * log_joint, int * count) {
+    return guarded([&] {
+        auto * s = static_cast<RefDraftSession *>(sp);
+        const int V = s->b.draft.shared->lm_head.rows;
+        std::shared_ptr<const RankedSubset> sub;
+        RestrictedHead head;
+        if (ordered != nullptr) {
+            std::vector<Token> ids(ordered, ordered + v_sub);
+            sub = std::make_shared<const RankedSubset>(subset_from_ranking(ids, v_sub, V, {}));
+            head = restrict_lm_head(s->b.draft.shared->lm_head, sub);
+        }
+        DraftParams p{width, depth, total};
+        DraftResult r = build_draft_tree(s->b.draft, s->cache, std::span<const Token>(pending, n_pending), p,
+                                         ordered ? &head : nullptr, nullptr, false);
+        export_tree(r.tree, tokens, parents, depths, log_joint, count);
+    });
+}
+
 // masked_attention (kernels.cpp:124-171) with a dense 0/1 mask [n x m].
 int ref_masked_attention(const float * q, const float * k, const float * v, const uint8_t * allow, int n, int m,
                          int dh, int dv, float * out) {

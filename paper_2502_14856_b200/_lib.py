@@ -96,6 +96,8 @@ SIGNATURES = [
     ("frs_draft_model_truncate", _I, [_P, _I]),
     ("frs_draft_model_length", _I, [_P, C.POINTER(_I)]),
     ("frs_draft_model_forward", _I, [_P, _P, _P, _I, _P, _P, _P]),
+    ("frs_draft_model_position", _I, [_P, _I, C.POINTER(_I)]),
+    ("frs_draft_model_compact", _I, [_P, _I, _P, _I, _P]),
     ("frs_draft_tree_model", _I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, C.POINTER(_I)]),
     ("frs_masked_attention", _I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     ("frs_write_token_stream", _I, [C.c_char_p, _I, _P, _I64]),

@@ -136,6 +136,9 @@ def masked_attention(ctx: "Context", q: torch.Tensor, k: torch.Tensor, v: torch.
     q, k, v = (t.to(torch.float32).contiguous() for t in (q, k, v))
     n, dh = q.shape
     m, dv = v.shape
+    if tuple(k.shape) != (m, dh):  # kernels.cpp:124-130
+        raise InvalidArgument("masked_attention: q/k width mismatch" if k.shape[1] != dh
+                              else "masked_attention: k/v row mismatch")
     a = np.asarray(allow.cpu() if isinstance(allow, torch.Tensor) else allow).astype(bool).reshape(n, m)
     stride = (m + 63) // 64
     bits = np.zeros((n, stride * 64), np.uint8)
@@ -190,9 +193,29 @@ class DraftModel:
     def truncate(self, new_len: int) -> None:
         check(lib().frs_draft_model_truncate(self.handle, new_len), "truncate")
 
+    def position(self, row: int) -> int:
+        """KVCache::positions[row]: the position a cached row was forwarded at."""
+        p = C.c_int()
+        check(lib().frs_draft_model_position(self.handle, row, C.byref(p)), "position")
+        return p.value
+
+    def compact(self, keep_from: int, kept_offsets) -> None:
+        """KVCache::compact (model.cpp:165-196): keep rows keep_from + kept_offsets[i] at
+        keep_from + i (K, V and positions); ValueError / RuntimeError (logic_error) as the
+        reference."""
+        o = _i32(kept_offsets)
+        check(lib().frs_draft_model_compact(self.handle, keep_from, _np_ptr(o) if o.size else None, o.size,
+                                            _stream(None)), "compact")
+
     def forward(self, tokens, positions, allow) -> torch.Tensor:
         """forward_raw: allow [n, len + n] (cache rows visible to each token)."""
         t, p = _i32(tokens), _i32(positions)
+        n = t.size
+        allow = np.asarray(allow)
+        if p.size != n:  # model.cpp:216-225
+            raise InvalidArgument("forward: positions size mismatch")
+        if allow.ndim != 2 or allow.shape != (n, len(self) + n):
+            raise InvalidArgument("forward: visibility mask shape mismatch")
         words = _mask_words(allow)
         out = torch.empty((t.size, self.d), dtype=torch.float32, device=torch.device("cuda", self.ctx.device))
         check(lib().frs_draft_model_forward(self.handle, _np_ptr(t), _np_ptr(p), t.size, _np_ptr(words), _ptr(out),
@@ -357,6 +380,10 @@ def draft_head_topk(ctx: Context, h: torch.Tensor, head: RestrictedHead, k: int,
     if h.dtype != torch.float32 or not h.is_cuda:
         raise InvalidArgument("draft head: h must be a CUDA float32 tensor")
     h = h.contiguous()
+    if h.dim() != 2 or h.shape[1] != head.d:  # kernels.cpp:35-37 matmul: inner dimensions differ
+        raise InvalidArgument(f"matmul: inner dimensions differ ({tuple(h.shape)} vs head width {head.d})")
+    if not 1 <= k <= head.v_sub:  # kernels.cpp:95-98
+        raise InvalidArgument(f"topk: k={k} out of range for size {head.v_sub}")
     n, d = h.shape
     dev = h.device
     if out is None:
@@ -377,6 +404,8 @@ def verify_head_argmax(ctx: Context, h: torch.Tensor, W: torch.Tensor, id_offset
     """Per-row argmax of h . W^T with ties to the lowest id; W is a CUDA fp32/bf16 shard."""
     h = h.contiguous()
     m, d = h.shape
+    if W.dim() != 2 or W.shape[1] != d:
+        raise InvalidArgument(f"matmul: inner dimensions differ ({tuple(h.shape)} vs {tuple(W.shape)})")
     dt = DTYPE_BF16 if W.dtype == torch.bfloat16 else DTYPE_F32
     ids = torch.empty(m, dtype=torch.int32, device=h.device)
     vals = torch.empty(m, dtype=torch.float32, device=h.device)

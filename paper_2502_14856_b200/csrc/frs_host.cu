@@ -1075,7 +1075,6 @@ struct ModelProvider {
     int n_pending;
     int base_len = 0, anchor_pos = 0, d = 0;
     std::vector<int> cand_row, cand_parent;  // by candidate index (-1 unknown)
-    std::vector<int> positions;              // cache row -> position
 };
 
 static int model_provider_cb(void *user, int level, int n, const int32_t *tokens, const int32_t *parent_cands,
@@ -1086,7 +1085,12 @@ static int model_provider_cb(void *user, int level, int n, const int32_t *tokens
     frs_draft_model_length(dm, &len0);
     if (level == 0) {  // the pending context, causal (the root is its last token)
         const int np = mp->n_pending;
-        const int start = len0 > 0 ? mp->positions[len0 - 1] + 1 : 0;
+        int start = 0;  // causal_layout (model.cpp:288-297): after the cache's last position
+        if (len0 > 0) {
+            const int rc = frs_draft_model_position(dm, len0 - 1, &start);
+            if (rc) return rc;
+            ++start;
+        }
         std::vector<int32_t> pos(np);
         const int m = len0 + np, words = (m + 63) / 64;
         std::vector<uint64_t> vis((size_t)np * words, 0);
@@ -1103,8 +1107,6 @@ static int model_provider_cb(void *user, int level, int n, const int32_t *tokens
         cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
         cudaFree(tmp);
         if (rc) return rc;
-        if (static_cast<int>(mp->positions.size()) < len0 + np) mp->positions.resize(len0 + np + 1024, 0);
-        for (int i = 0; i < np; ++i) mp->positions[len0 + i] = pos[i];
         mp->base_len = len0 + np;
         mp->anchor_pos = pos[np - 1];
         return 0;
@@ -1129,8 +1131,6 @@ static int model_provider_cb(void *user, int level, int n, const int32_t *tokens
     }
     const int rc = frs_draft_model_forward(dm, tokens, pos.data(), n, vis.data(), hidden_dev, stream);
     if (rc) return rc;
-    if (static_cast<int>(mp->positions.size()) < len0 + n) mp->positions.resize(len0 + n + 1024, 0);
-    for (int i = 0; i < n; ++i) mp->positions[len0 + i] = pos[i];
     return 0;
 }
 
@@ -1140,11 +1140,7 @@ int frs_draft_tree_model(frs_head *h, frs_draft_model *dm, const int32_t *pendin
     FRS_REQUIRE(h && dm && pending, "build_draft_tree: null pointer");
     if (n_pending < 1) return fail(FRS_EINVAL, "build_draft_tree: pending must end with the root token");
     ModelProvider mp{dm, pending, n_pending};
-    int len0 = 0, maxs = 0;
-    frs_draft_model_length(dm, &len0);
     mp.d = h->d;
-    maxs = 4096 + len0 + n_pending + width * depth;
-    mp.positions.assign(maxs, 0);
     int st = rng ? frs_draft_tree_sampled(h, pending[n_pending - 1], model_provider_cb, &mp, nullptr, width, depth,
                                           total, rng, tokens, parents, depths, log_joint, count)
                  : frs_draft_tree(h, pending[n_pending - 1], model_provider_cb, &mp, nullptr, width, depth, total,

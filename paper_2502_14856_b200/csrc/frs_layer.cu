@@ -194,6 +194,48 @@ int frs_draft_model_length(const frs_draft_model *m, int *len) {
     return FRS_OK;
 }
 
+// KVCache::positions[row] (model.cpp: the position each cached row was forwarded at).
+int frs_draft_model_position(const frs_draft_model *m, int row, int *pos) {
+    FRS_REQUIRE(m && pos, "draft model: null pointer");
+    FRS_REQUIRE(row >= 0 && row < m->len, "position: row out of range");
+    *pos = m->positions[row];
+    return FRS_OK;
+}
+
+// KVCache::compact (model.cpp:165-196): keep rows keep_from + kept_offsets[i] (ascending, in
+// range) at keep_from + i, for K and V, and their positions; the same rejections in the same
+// order. As in the reference, the contiguity check runs after the move (the cache is already
+// compacted when it throws std::logic_error -> FRS_ELOGIC).
+int frs_draft_model_compact(frs_draft_model *m, int keep_from, const int32_t *kept_offsets, int n_kept, void *stream) {
+    FRS_REQUIRE(m && (kept_offsets || n_kept == 0), "draft model: null pointer");
+    if (keep_from < 0 || keep_from > m->len) return fail(FRS_EINVAL, "KVCache::compact: bad keep_from");
+    int prev = -1;
+    for (int i = 0; i < n_kept; ++i) {
+        const int off = kept_offsets[i];
+        if (off <= prev || keep_from + off >= m->len)
+            return fail(FRS_EINVAL, "KVCache::compact: offsets must be ascending and in range");
+        prev = off;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    FRS_CUDA_TRY(cudaSetDevice(m->ctx->device));
+    const int d = m->d;
+    // src = keep_from + off_i >= dst = keep_from + i and src_i < src_j for i < j, so a forward
+    // sweep of stream-ordered row copies never reads a row it already overwrote
+    float *kc = static_cast<float *>(m->kc.ptr), *vc = static_cast<float *>(m->vc.ptr);
+    for (int i = 0; i < n_kept; ++i) {
+        const size_t src = (size_t)keep_from + kept_offsets[i], dst = (size_t)keep_from + i;
+        if (src == dst) continue;
+        FRS_CUDA_TRY(cudaMemcpyAsync(kc + dst * d, kc + src * d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+        FRS_CUDA_TRY(cudaMemcpyAsync(vc + dst * d, vc + src * d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    }
+    for (int i = 0; i < n_kept; ++i) m->positions[keep_from + i] = m->positions[keep_from + kept_offsets[i]];
+    m->len = keep_from + n_kept;
+    for (int r = 1; r < m->len; ++r)
+        if (m->positions[r] != m->positions[r - 1] + 1)
+            return fail(FRS_ELOGIC, "KVCache::compact: kept positions are not contiguous");
+    return FRS_OK;
+}
+
 // forward_raw (model.cpp:208-281) for the draft layer: tokens / positions host [n]; visible
 // host BitMask words [n x ceil((len + n) / 64)] (bit j of row r: cache row j visible to token
 // r); hidden_out device [n x d] (post final norm). Appends the n rows to the cache.

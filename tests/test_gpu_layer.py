@@ -104,3 +104,76 @@ def test_exact_logits_wide_inputs(cuda_ctx, restatement):
                                 dtype="f32")
     out = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, 4, mode="exact", want_logits=True)
     assert np.array_equal(out.logits.cpu().numpy(), restatement.logits(h, W))
+
+
+def test_model_draft_tree_on_persistent_cache(cuda_ctx, reference):
+    """Two drafting steps on the same draft model, the second after the first's context (a
+    decode loop's cache): the pending tokens continue at the cache's last position + 1
+    (causal_layout, model.cpp:288-297) and both trees equal the reference's build_draft_tree on
+    its own persistent cache."""
+    V, d, heads, seed, max_seq = 700, 64, 4, 19, 96
+    sess = reference.draft_session(V, d, heads, max_seq, seed)
+    draft = api.DraftModel(cuda_ctx, sess.weights(), heads, max_seq)
+    W = reference.model_lm_head(V, d, 1, heads, seed)
+    ordered = np.random.default_rng(seed).permutation(V)[:256].astype(np.int32)
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(V, ordered), dtype="f32")
+    params = api.DraftParams(4, 3, 12)
+    for step, pending in enumerate(([3, 14, 15, 92], [65, 35], [89])):
+        ref = sess.draft_tree(ordered, pending, 4, 3, 12)
+        tree = api.build_draft_tree_model(head, draft, pending, params, mode="exact")
+        for key in ("tokens", "parents", "depths", "log_joint"):
+            assert np.array_equal(getattr(tree, key), ref[key]), (step, key)
+        assert len(draft) == len(sess)
+        assert [draft.position(r) for r in range(len(draft))] == [sess.position(r) for r in range(len(sess))]
+
+
+def test_kv_compact_matches_reference(cuda_ctx, reference):
+    """KVCache::compact (model.cpp:165-196) on the device cache: the kept rows move down with
+    their positions, a later forward sees exactly the reference's cache; the rejections."""
+    from paper_2502_14856_b200._lib import InvalidArgument, LogicError
+    V, d, heads, seed, max_seq = 400, 64, 4, 23, 40
+    sess = reference.draft_session(V, d, heads, max_seq, seed)
+    dev = api.DraftModel(cuda_ctx, sess.weights(), heads, max_seq)
+    rng = np.random.default_rng(seed)
+    toks = rng.integers(0, V, 5)
+    allow = np.tril(np.ones((5, 5), np.uint8))
+    sess.forward(toks, np.arange(5), allow)
+    dev.forward(toks, np.arange(5), allow)
+    # a tree level of 4 rows at positions 5, 6, 6, 7 (rows 5..8); accept rows 5 and 7 (offsets 0, 2)
+    tree_toks = rng.integers(0, V, 4)
+    tpos = np.array([5, 6, 6, 7])
+    tallow = np.ones((4, 9), np.uint8)
+    sess.forward(tree_toks, tpos, tallow)
+    dev.forward(tree_toks, tpos, tallow)
+    for bad_from, bad_offs, exc in ((-1, [0], InvalidArgument), (10, [0], InvalidArgument),
+                                    (5, [1, 0], InvalidArgument), (5, [4], InvalidArgument)):
+        with pytest.raises(exc):
+            dev.compact(bad_from, bad_offs)
+        with pytest.raises(ValueError):
+            sess.compact(bad_from, bad_offs)
+    assert len(dev) == 9
+    sess.compact(5, [0, 2])
+    dev.compact(5, [0, 2])
+    assert len(dev) == len(sess) == 7
+    assert [dev.position(r) for r in range(7)] == [sess.position(r) for r in range(7)] == list(range(7))
+    nxt = rng.integers(0, V, 2)
+    h_ref = sess.forward(nxt, [7, 8], np.tril(np.ones((2, 9), np.uint8), 7))
+    h_dev = dev.forward(nxt, [7, 8], np.tril(np.ones((2, 9), np.uint8), 7)).cpu().numpy()
+    assert np.array_equal(h_dev, h_ref)
+    # positions 0..8 then keeping offsets {1} of keep_from 7: position 8 lands at row 7 after 6
+    with pytest.raises(LogicError, match="not contiguous"):
+        dev.compact(6, [0, 2])
+    with pytest.raises(RuntimeError, match="not contiguous"):
+        sess.compact(6, [0, 2])
+    assert len(dev) == len(sess) == 8
+
+
+def test_forward_shape_rejections(cuda_ctx, reference):
+    from paper_2502_14856_b200._lib import InvalidArgument
+    sess = reference.draft_session(300, 32, 2, 8, 3)
+    dev = api.DraftModel(cuda_ctx, sess.weights(), 2, 8)
+    with pytest.raises(InvalidArgument, match="positions size mismatch"):
+        dev.forward([1, 2], [0], np.tril(np.ones((2, 2), np.uint8)))
+    with pytest.raises(InvalidArgument, match="visibility mask shape mismatch"):
+        dev.forward([1, 2], [0, 1], np.ones((2, 1), np.uint8))
+    assert len(dev) == 0
