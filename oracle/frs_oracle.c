@@ -6,6 +6,8 @@
 #include "frs_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
+#include <unistd.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -28,12 +30,46 @@ float frs_o_dot_f32(const float *a, const float *b, int n) {
     return s;
 }
 
+/* out[j - j0] = dot_f32(h, W_j) for j in [j0, j1), split over the host's cores: every element
+ * is one dot_f32 call, so the split cannot change a bit (test speed only). */
+typedef struct {
+    const float *h, *W;
+    int n, d, j0, j1, ld;
+    float *out;
+} dots_job;
+static void *dots_worker(void *arg) {  /* W row j read once for all n hidden rows */
+    const dots_job *J = (const dots_job *)arg;
+    for (int j = J->j0; j < J->j1; ++j)
+        for (int i = 0; i < J->n; ++i)
+            J->out[(size_t)i * J->ld + j] = frs_o_dot_f32(J->h + (size_t)i * J->d, J->W + (size_t)j * J->d, J->d);
+    return NULL;
+}
+/* out[i * ld + j] = dot_f32(h_i, W_j), i < n, j in [j0, j1) */
+static void par_dots_n(const float *h, int n, const float *W, int d, int j0, int j1, float *out, int ld) {
+    enum { kMaxT = 64 };
+    long nt = sysconf(_SC_NPROCESSORS_ONLN);
+    if (nt < 1) nt = 1;
+    if (nt > kMaxT) nt = kMaxT;
+    if ((long)(j1 - j0) * d * n < (1L << 22)) nt = 1;
+    pthread_t th[kMaxT];
+    dots_job jobs[kMaxT];
+    for (long t = 0; t < nt; ++t) {
+        jobs[t] = (dots_job){h, W, n, d, j0 + (int)((long)(j1 - j0) * t / nt),
+                             j0 + (int)((long)(j1 - j0) * (t + 1) / nt), ld, out};
+        th[t] = 0;
+        if (t > 0 && pthread_create(&th[t], NULL, dots_worker, &jobs[t]) != 0) {
+            th[t] = 0;
+            dots_worker(&jobs[t]);
+        }
+    }
+    dots_worker(&jobs[0]);
+    for (long t = 1; t < nt; ++t)
+        if (th[t]) pthread_join(th[t], NULL);
+}
+
 /* kernels.cpp:34-60 (both branches give identical values: per-element order is fixed) */
 void frs_o_logits(const float *h, int n, const float *W, int V, int d, float *out) {
-    for (int j = 0; j < V; ++j) {
-        const float *wj = W + (size_t)j * d;
-        for (int i = 0; i < n; ++i) out[(size_t)i * V + j] = frs_o_dot_f32(h + (size_t)i * d, wj, d);
-    }
+    par_dots_n(h, n, W, d, 0, V, out, V);
 }
 
 /* glibc 2.39 sysdeps/ieee754/flt-32/e_expf.c as dispatched to the FMA ifunc on x86-64
@@ -136,12 +172,12 @@ int frs_o_draft_level(const float *h, int n, const float *slab, int v_sub, int d
                       int32_t *out_full, float *out_prob, float *out_mx, double *out_total,
                       float *out_logits) {
     const int w = k < v_sub ? k : v_sub; /* drafting.cpp:40 */
-    float *logits = (float *)malloc(sizeof(float) * (size_t)v_sub);
+    float *all = (float *)malloc(sizeof(float) * (size_t)v_sub * n);
     float *probs = (float *)malloc(sizeof(float) * (size_t)v_sub);
     int rc = 0;
+    par_dots_n(h, n, slab, d, 0, v_sub, all, v_sub);
     for (int i = 0; i < n && rc == 0; ++i) {
-        const float *hi = h + (size_t)i * d;
-        for (int j = 0; j < v_sub; ++j) logits[j] = frs_o_dot_f32(hi, slab + (size_t)j * d, d);
+        const float *logits = all + (size_t)i * v_sub;
         if (out_logits) memcpy(out_logits + (size_t)i * v_sub, logits, sizeof(float) * (size_t)v_sub);
         rc = frs_o_softmax(logits, v_sub, temperature, probs, out_mx ? out_mx + i : NULL,
                            out_total ? out_total + i : NULL);
@@ -152,27 +188,27 @@ int frs_o_draft_level(const float *h, int n, const float *slab, int v_sub, int d
             out_full[(size_t)i * k + c] = ordered_ids ? ordered_ids[r] : r;
         }
     }
-    free(logits);
+    free(all);
     free(probs);
     return rc;
 }
 
 void frs_o_verify_argmax(const float *h, int m, const float *W, int V, int d, int32_t *out_id,
                          float *out_val) {
+    float *row = (float *)malloc(sizeof(float) * (size_t)V);
     for (int i = 0; i < m; ++i) {
-        const float *hi = h + (size_t)i * d;
-        float best = frs_o_dot_f32(hi, W, d);
+        par_dots_n(h + (size_t)i * d, 1, W, d, 0, V, row, V);
+        float best = row[0];
         int bi = 0;
-        for (int j = 1; j < V; ++j) {
-            const float v = frs_o_dot_f32(hi, W + (size_t)j * d, d);
-            if (v > best) {
-                best = v;
+        for (int j = 1; j < V; ++j)
+            if (row[j] > best) { /* kernels.cpp:117-121: strict '>' keeps the lowest id on ties */
+                best = row[j];
                 bi = j;
             }
-        }
         out_id[i] = bi;
         if (out_val) out_val[i] = best;
     }
+    free(row);
 }
 
 /* verification.cpp:31-71 */

@@ -480,7 +480,7 @@ class Reference:
                 tok, par, dep = (np.empty(total, np.int32) for _ in range(3))
                 lj = np.empty(total, np.float64)
                 cnt = C.c_int()
-                ref._check(ref.lib.ref_draft_session_draft_tree(self.h, o, 0 if o is None else o.size, p, p.size, width,
+                ref._check(ref.lib.ref_draft_session_draft_tree(self.h, None if o is None else o.ctypes.data, 0 if o is None else o.size, p, p.size, width,
                                                                 depth, total, tok, par, dep, lj, C.byref(cnt)),
                            "build_draft_tree")
                 n = cnt.value

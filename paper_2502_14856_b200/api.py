@@ -382,8 +382,8 @@ def draft_head_topk(ctx: Context, h: torch.Tensor, head: RestrictedHead, k: int,
     h = h.contiguous()
     if h.dim() != 2 or h.shape[1] != head.d:  # kernels.cpp:35-37 matmul: inner dimensions differ
         raise InvalidArgument(f"matmul: inner dimensions differ ({tuple(h.shape)} vs head width {head.d})")
-    if not 1 <= k <= head.v_sub:  # kernels.cpp:95-98
-        raise InvalidArgument(f"topk: k={k} out of range for size {head.v_sub}")
+    if k < 1:  # drafting.cpp:15; k > V_sub draws min(width, V_sub) (drafting.cpp:37-43)
+        raise InvalidArgument("draft params: beam_width must be >= 1")
     n, d = h.shape
     dev = h.device
     if out is None:

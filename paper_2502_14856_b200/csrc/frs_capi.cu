@@ -193,8 +193,6 @@ int frs_draft_head_topk(frs_ctx *ctx, const float *h, int n, int d, const void *
     FRS_REQUIRE(n >= 1, "forward: empty token batch");                       // model.cpp:217
     FRS_REQUIRE(d >= 1 && v_sub >= 1, "draft head: sizes must be positive");
     FRS_REQUIRE(k >= 1, "draft params: beam_width must be >= 1");           // drafting.cpp:15
-    if (k > v_sub)                                                            // kernels.cpp:95-98
-        return fail(FRS_EINVAL, "topk: k=" + std::to_string(k) + " out of range for size " + std::to_string(v_sub));
     FRS_REQUIRE(std::isfinite(temperature) && temperature > 0.0f,
                 "softmax: temperature must be positive and finite");       // kernels.cpp:66-68
     FRS_REQUIRE(valid_dtype(slab_dtype), "draft head: unknown slab dtype");

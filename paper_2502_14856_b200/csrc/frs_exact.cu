@@ -17,10 +17,14 @@
 // both the chain order is the reference's exactly and the final tree has the reference's
 // association. __fmul_rn/__fadd_rn keep ptxas from contracting into FFMA (2 FP32 instructions
 // per MAC).
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <string>
 
 #include "frs_common.cuh"
 #include "frs_device.cuh"
@@ -431,7 +435,10 @@ __global__ void __launch_bounds__(1024, 1)
     }
 }
 
-// One CTA per row: exact softmax + top-k + remap (dev::softmax_topk_row).
+// One CTA per row: exact softmax + top-k + remap (dev::softmax_topk_row). The probabilities
+// and ids are always the reference's; the index-order double Σ itself (kernels.cpp:80-85) is
+// replayed sequentially (one thread, ~40 us at V_sub 32768) only when the caller asks for it
+// (out_total): otherwise 1 / Σ is pinned by bracketing the tree sum.
 __global__ void __launch_bounds__(1024)
     k_softmax_topk(const float *__restrict__ logits, int ld, int v, int k, float temperature,
                    const int32_t *__restrict__ ordered, float *__restrict__ ework, int32_t *__restrict__ out_ridx,
@@ -442,7 +449,7 @@ __global__ void __launch_bounds__(1024)
     const uint32_t flags = dev::softmax_topk_row(
         logits + (size_t)row * ld, v, k, temperature, ordered, ework + (size_t)row * ld, out_ridx + (size_t)row * k,
         out_full + (size_t)row * k, out_prob + (size_t)row * k, out_rowmax ? out_rowmax + row : nullptr,
-        out_total ? out_total + row : nullptr, rs);
+        out_total ? out_total + row : nullptr, rs, /*tree_total_ok=*/out_total == nullptr);
     if (threadIdx.x == 0 && out_flags) out_flags[row] = flags;
 }
 
@@ -520,27 +527,30 @@ __global__ void __launch_bounds__(256)
     }
 }
 // ---------------------------------------------------------------- staged exact GEMV
-// The same dot_f32 arithmetic with the operands staged in shared memory by bulk copies
-// (cp.async.bulk + mbarrier ring) instead of per-thread loads, so the stream does not depend
-// on how many warps have rows to work on: a 4096-row projection at d = 4096 gives the
-// per-thread-load kernel 1024 busy warps out of 4736 (~0.8 TB/s); here every SM streams its
-// rows through a 4-6 stage ring (~100 KB in flight per SM).
-//  * CTA = one producer warp + 2 S consumer warps (S = ceil(n / 2) slices of 2 hidden rows).
-//    A block is RB <= 32 consecutive W rows; K is cut into KC-element chunks (rows chunk W[r,
-//    c KC .. +KC) and h[i, c KC .. +KC), one bulk copy per row; row pitch KC + 8 elements so
-//    the 128-bit (fp32) / 64-bit (bf16) reads of 4 rows x 2 lanes hit distinct banks).
-//  * consumer lane = (row rl = 16 (warp & 1) + lane / 2, chain quad cq = lane & 1): it owns
-//    the dot_f32 lane chains 4 cq .. 4 cq + 3 (kernels.cpp:19-26: s_l += a*b over indices = l
-//    mod 8) of its 2 hidden rows and walks the chunks in index order, so every chain's
-//    sequence of rounded mul / add is the reference's; the final tree ((s0+s1)+(s2+s3)) +
-//    ((s4+s5)+(s6+s7)) (kernels.cpp:27) is one xor-1 shuffle. Requires d % 8 == 0 (no scalar
-//    tail) and 16-byte aligned rows.
-// Bound: FP32 issue (2 instructions per MAC) for n >= ~6 at fp32 weights; HBM below.
+// The reference's dot_f32 (kernels.cpp:13-32) for every (hidden row, W row) pair on CUDA cores,
+// operands staged in shared memory by TMA (cp.async.bulk.tensor) through an mbarrier ring.
+//  * Persistent grid, one CTA per SM. W rows come in 32-row groups; CTA c owns the groups
+//    [c NG / G, (c+1) NG / G) and walks them in blocks of RW groups (one row warp per group),
+//    each block in KC-element chunks (256 B of every W row per chunk): per chunk one TMA box of
+//    32 rows x 128 B per (group, 128-byte panel), SWIZZLE_128B (16-byte chunk c of row r lands
+//    at c ^ (r & 7), so the 16-byte reads of 8 consecutive rows hit distinct banks), and one
+//    box [n rows x KC] of the hidden rows (dense, read as warp-uniform broadcasts). Per-row
+//    bulk copies cost ~100 cycles of TMA issue each (measured: 256 B copies ran at 0.55 TB/s);
+//    the boxes move 4 KB per request.
+//  * Consumer thread = (W row of the block, hidden group hg): it owns ALL 8 lane chains of its
+//    W row for the nrg hidden rows of its group (8 nrg accumulators). Per 8-element step it
+//    reads its W row's 8 words once and each hidden row's 8 words once, then does 8 nrg
+//    rounded multiplies + rounded adds: every chain sees the reference's sequence s_l += a*b
+//    over indices = l mod 8 in index order; the final ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)) is
+//    in-thread. __fmul_rn / __fadd_rn keep ptxas from fusing (2 FP32 instructions per MAC).
+//  * Warps = RW x HG, hidden groups of nrg <= NRT rows (NRT = template register tile).
+// Requires d % 8 == 0 (no scalar tail) and 16-byte aligned rows / row strides; other shapes
+// take k_exact_logits.
 namespace gv {
-constexpr int KC = 256;     // k elements per chunk
-constexpr int RBMAX = 32;   // W rows per block
-constexpr int NMAX = 16;    // hidden rows per launch
-constexpr int PAD = 8;      // row pitch padding (elements)
+constexpr int NPASS = 32;   // hidden rows per launch
+constexpr int GROUP = 32;   // W rows per TMA box (one row warp)
+constexpr int PANEL = 128;  // bytes per TMA box row (SWIZZLE_128B)
+constexpr int BOX = GROUP * PANEL;
 __device__ __forceinline__ uint32_t su32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void bar_init(uint64_t *b, uint32_t c) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
@@ -560,127 +570,157 @@ __device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b, uint64_t pol) {
+__device__ __forceinline__ void tma2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *b, uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            su32(dst)),
-        "l"(src), "r"(bytes), "r"(su32(b)), "l"(pol)
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(b)), "l"(pol)
         : "memory");
 }
-__device__ __forceinline__ void lds4(const float *p, float (&w)[4]) {
-    const float4 v = *reinterpret_cast<const float4 *>(p);
-    w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+// 8 consecutive W words (fp32 widening of bf16 is exact) at 16-byte chunks c0, c1 of a row
+__device__ __forceinline__ void ldw8(const unsigned char *row, int c, int sw, const float *, float (&w)[8]) {
+    const float4 a = *reinterpret_cast<const float4 *>(row + (((2 * c) ^ sw) << 4));
+    const float4 b = *reinterpret_cast<const float4 *>(row + (((2 * c + 1) ^ sw) << 4));
+    w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
 }
-__device__ __forceinline__ void lds4(const unsigned short *p, float (&w)[4]) {
-    const uint2 v = *reinterpret_cast<const uint2 *>(p);  // bf16 -> fp32 is exact
+__device__ __forceinline__ void ldw8(const unsigned char *row, int c, int sw, const unsigned short *, float (&w)[8]) {
+    const uint4 v = *reinterpret_cast<const uint4 *>(row + ((c ^ sw) << 4));
     w[0] = __uint_as_float(v.x << 16), w[1] = __uint_as_float(v.x & 0xffff0000u);
     w[2] = __uint_as_float(v.y << 16), w[3] = __uint_as_float(v.y & 0xffff0000u);
+    w[4] = __uint_as_float(v.z << 16), w[5] = __uint_as_float(v.z & 0xffff0000u);
+    w[6] = __uint_as_float(v.w << 16), w[7] = __uint_as_float(v.w & 0xffff0000u);
 }
+__device__ __forceinline__ void ldh8(const float *p, float (&x)[8]) {
+    const float4 a = reinterpret_cast<const float4 *>(p)[0], b = reinterpret_cast<const float4 *>(p)[1];
+    x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+}
+constexpr int MAXW = 16;  // consumer warps per CTA
+// register estimate (accumulators + one step's W and h words + addressing), for the warp budget
+constexpr int regs_of(int nrt, int jt) { return (8 * nrt * jt + 8 * jt + 8 + 64 + 7) & ~7; }
+// most consumer warps whose registers fit (warps are allocated per scheduler in fours)
+constexpr int maxw_of(int nrt, int jt) {
+    for (int w = MAXW; w > 1; --w)
+        if (((w + 1 + 3) / 4) * 32 * regs_of(nrt, jt) <= 16384) return w;
+    return 1;
+}
+template <typename WT> constexpr int kc_of() { return 256 / (int)sizeof(WT); }  // 2 panels per row per chunk
 }  // namespace gv
 
-template <typename WT>
-__global__ void __launch_bounds__(32 + 64 * (gv::NMAX / 2))
-    k_exact_gemv(const float *__restrict__ h, int n, int d, const WT *__restrict__ W, int v_rows, int rb, int nblocks,
-                 int stages, float *__restrict__ logits, int ld) {
+template <typename WT, int NRT, int JT>
+__global__ void __launch_bounds__(32 + 32 * gv::maxw_of(NRT, JT), 1)
+    k_exact_gemv(const __grid_constant__ CUtensorMap w_map, const __grid_constant__ CUtensorMap h_map, int h_row0,
+                 int n, int d, int v_rows, int RW, int HG, int stages, float *__restrict__ logits, int ld) {
     using namespace gv;
-    extern __shared__ __align__(128) unsigned char g_smem[];
-    const int S = (n + 1) >> 1;
-    const int pitch = KC + PAD;
-    const size_t w_bytes = (size_t)RBMAX * pitch * sizeof(WT);
-    const size_t h_bytes = (size_t)(2 * S) * KC * sizeof(float);
-    const size_t st_bytes = (w_bytes + h_bytes + 127) & ~size_t(127);
-    uint64_t *full = reinterpret_cast<uint64_t *>(g_smem + st_bytes * stages);
+    constexpr int KC = kc_of<WT>();
+    constexpr int P = KC * (int)sizeof(WT) / PANEL;       // panels per chunk
+    constexpr int SPP = PANEL / (8 * (int)sizeof(WT));     // 8-element steps per panel
+    extern __shared__ __align__(1024) unsigned char g_smem[];
+    // 1024-byte aligned for SWIZZLE_128B; pointer arithmetic on g_smem keeps the shared window (LDS)
+    unsigned char *smem = g_smem + ((1024u - (su32(g_smem) & 1023u)) & 1023u);
+    const int GB = RW * JT;  // 32-row groups per block
+    const size_t w_bytes = (size_t)GB * P * BOX;
+    const size_t st_bytes = (w_bytes + (size_t)HG * NRT * KC * sizeof(float) + 1023) & ~size_t(1023);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + st_bytes * stages);
     uint64_t *empty = full + stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cwarps = (blockDim.x >> 5) - 1;
     const int nchunks = (d + KC - 1) / KC;
+    const int NG = (v_rows + GROUP - 1) / GROUP;
+    const int g_begin = static_cast<int>((long long)blockIdx.x * NG / gridDim.x);
+    const int g_end = static_cast<int>((long long)(blockIdx.x + 1) * NG / gridDim.x);
+    const int nblk = (g_end - g_begin + GB - 1) / GB;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             bar_init(&full[s], 1);
-            bar_init(&empty[s], 2 * S * 32);  // every consumer lane releases its own reads
+            bar_init(&empty[s], cwarps);  // one arrival per consumer warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == 0) {  // producer
-        uint64_t pol_w, pol_h;
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_h));
-        int it = 0;
-        for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
-            const int r0 = blk * rb, nr = min(rb, v_rows - r0);
-            for (int c = 0; c < nchunks; ++c, ++it) {
-                const int st = it % stages;
-                const uint32_t ph = (it / stages) & 1;
-                const int k0 = c * KC, kc = min(KC, d - k0);
-                bar_wait(&empty[st], ph ^ 1);
-                unsigned char *base = g_smem + st_bytes * st;
-                if (lane == 0) bar_expect(&full[st], (uint32_t)((nr * sizeof(WT) + n * sizeof(float)) * kc));
-                __syncwarp();
-                if (lane < nr)
-                    g2s(reinterpret_cast<WT *>(base) + (size_t)lane * pitch, W + (size_t)(r0 + lane) * d + k0,
-                        (uint32_t)(kc * sizeof(WT)), &full[st], pol_w);
-                if (lane < n)
-                    g2s(reinterpret_cast<float *>(base + w_bytes) + (size_t)lane * KC, h + (size_t)lane * d + k0,
-                        (uint32_t)(kc * sizeof(float)), &full[st], pol_h);
+    if (warp == 0) {  // producer: one elected lane
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&w_map)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&h_map)) : "memory");
+            uint64_t pol_w, pol_h;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_h));
+            int it = 0;
+            for (int b = 0; b < nblk; ++b) {
+                const int g0 = g_begin + b * GB, ng = min(GB, g_end - g0);
+                for (int c = 0; c < nchunks; ++c, ++it) {
+                    const int st = it % stages;
+                    const uint32_t ph = (it / stages) & 1;
+                    bar_wait(&empty[st], ph ^ 1);
+                    unsigned char *base = smem + st_bytes * st;
+                    // full boxes always land (OOB rows / columns are zero-filled and counted)
+                    bar_expect(&full[st], (uint32_t)(ng * P * BOX + n * KC * sizeof(float)));
+                    for (int g = 0; g < ng; ++g)
+                        for (int p = 0; p < P; ++p)
+                            tma2d(base + (size_t)(g * P + p) * BOX, &w_map, c * KC + p * (PANEL / (int)sizeof(WT)),
+                                  (g0 + g) * GROUP, &full[st], pol_w);
+                    tma2d(base + w_bytes, &h_map, c * KC, h_row0, &full[st], pol_h);
+                }
             }
         }
         return;
     }
-    const int cw = warp - 1, slice = cw >> 1;
-    const int rl = 16 * (cw & 1) + (lane >> 1), cq = lane & 1;
-    const int i0 = 2 * slice;
+    const int cw = warp - 1, hg = cw / RW, rw = cw - hg * RW;
+    const int i0 = hg * NRT, nr_t = min(NRT, n - i0);  // this warp's hidden rows
+    const int sw = lane & 7;
     int it = 0;
-    for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
-        const int r0 = blk * rb;
-        float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int b = 0; b < nblk; ++b) {
+        const int gw = g_begin + b * GB + rw * JT;  // this warp's first group
+        float acc[JT][NRT][8];
+#pragma unroll
+        for (int j = 0; j < JT; ++j)
+#pragma unroll
+            for (int i = 0; i < NRT; ++i)
+#pragma unroll
+                for (int l = 0; l < 8; ++l) acc[j][i][l] = 0.0f;
         for (int c = 0; c < nchunks; ++c, ++it) {
             const int st = it % stages;
             const uint32_t ph = (it / stages) & 1;
-            const int kc = min(KC, d - c * KC);
+            const int T = min(KC, d - c * KC) >> 3;
             bar_wait(&full[st], ph);
-            const unsigned char *base = g_smem + st_bytes * st;
-            const WT *wr = reinterpret_cast<const WT *>(base) + (size_t)rl * pitch + 4 * cq;
-            const float *h0 = reinterpret_cast<const float *>(base + w_bytes) + (size_t)i0 * KC + 4 * cq;
-            const float *h1 = h0 + KC;
-            const int T = kc >> 3;
-            int t = 0;
-            for (; t + 4 <= T; t += 4) {
-                float w[4][4], x[4][4], y[4][4];
+            const unsigned char *base = smem + st_bytes * st;
+            const unsigned char *wb = base + (size_t)rw * JT * P * BOX + lane * PANEL;
+            const float *hb = reinterpret_cast<const float *>(base + w_bytes) + (size_t)i0 * KC;
+            if (gw < g_end) {  // a second group past g_end computes on stale words, never stored
+#pragma unroll 1
+                for (int t = 0; t < T; ++t) {
+                    const int p = t / SPP, cc = t - p * SPP;
+                    float w[JT][8];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    gv::lds4(wr + (t + u) * 8, w[u]);
-                    gv::lds4(h0 + (t + u) * 8, x[u]);
-                    gv::lds4(h1 + (t + u) * 8, y[u]);
+                    for (int j = 0; j < JT; ++j)
+                        ldw8(wb + (size_t)(j * P + p) * BOX, cc, sw, static_cast<const WT *>(nullptr), w[j]);
+#pragma unroll
+                    for (int i = 0; i < NRT; ++i) {  // rows past n (last group) compute on padding, never stored
+                        float x[8];
+                        ldh8(hb + (size_t)i * KC + 8 * t, x);
+#pragma unroll
+                        for (int j = 0; j < JT; ++j)
+#pragma unroll
+                            for (int l = 0; l < 8; ++l)
+                                acc[j][i][l] = __fadd_rn(acc[j][i][l], __fmul_rn(x[l], w[j][l]));
+                    }
                 }
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(&empty[st]);
+        }
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+        for (int j = 0; j < JT; ++j) {
+            const int row = (gw + j) * GROUP + lane;
+            if (gw + j < g_end && row < v_rows) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        a0[j] = __fadd_rn(a0[j], __fmul_rn(x[u][j], w[u][j]));
-                        a1[j] = __fadd_rn(a1[j], __fmul_rn(y[u][j], w[u][j]));
+                for (int i = 0; i < NRT; ++i)
+                    if (i < nr_t) {
+                        const float(&a)[8] = acc[j][i];
+                        const float s = __fadd_rn(__fadd_rn(__fadd_rn(a[0], a[1]), __fadd_rn(a[2], a[3])),
+                                                  __fadd_rn(__fadd_rn(a[4], a[5]), __fadd_rn(a[6], a[7])));
+                        logits[(size_t)(i0 + i) * ld + row] = s;
                     }
             }
-            for (; t < T; ++t) {
-                float w[4], x[4], y[4];
-                gv::lds4(wr + t * 8, w);
-                gv::lds4(h0 + t * 8, x);
-                gv::lds4(h1 + t * 8, y);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    a0[j] = __fadd_rn(a0[j], __fmul_rn(x[j], w[j]));
-                    a1[j] = __fadd_rn(a1[j], __fmul_rn(y[j], w[j]));
-                }
-            }
-            bar_arrive(&empty[st]);
-        }
-        // ((s0+s1)+(s2+s3)) + ((s4+s5)+(s6+s7)): cq 0 holds s0..s3, cq 1 holds s4..s7
-        float q0 = __fadd_rn(__fadd_rn(a0[0], a0[1]), __fadd_rn(a0[2], a0[3]));
-        float q1 = __fadd_rn(__fadd_rn(a1[0], a1[1]), __fadd_rn(a1[2], a1[3]));
-        const float p0 = __shfl_xor_sync(0xffffffffu, q0, 1), p1 = __shfl_xor_sync(0xffffffffu, q1, 1);
-        const int row = r0 + rl;
-        if (cq == 0 && rl < rb && row < v_rows) {
-            if (i0 < n) logits[(size_t)i0 * ld + row] = __fadd_rn(q0, p0);
-            if (i0 + 1 < n) logits[(size_t)(i0 + 1) * ld + row] = __fadd_rn(q1, p1);
         }
     }
 }
@@ -693,27 +733,149 @@ bool gemv_enabled() {
     return on != 0;
 }
 
-template <typename WT>
-int launch_gemv(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_rows, float *logits, int ld,
-                cudaStream_t s) {
+PFN_cuTensorMapEncodeTiled_v12000 gemv_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2D row-major [rows x cols] map, box [box_rows x box_cols]
+int gemv_map(CUtensorMap *map, const void *base, bool bf16, long long rows, long long cols, long long row_stride_elems,
+             int box_cols, int box_rows, bool swizzle) {
+    auto fn = gemv_encode_fn();
+    if (!fn) return fail(FRS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const int es = bf16 ? 2 : 4;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride_elems) * es};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                    const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FRS_ECUDA, "exact gemv: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return FRS_OK;
+}
+
+struct GemvCfg {
+    int nrt, jt, rw, hg;
+};
+
+// (JT W rows x NRT hidden rows) per thread, RW row warps, HG hidden groups: the configuration
+// with the least estimated issue time per SM (FP 2 per MAC incl. padding rows / groups, W and h
+// shared-memory reads, bf16 widening; x 8 / warps below 8 warps for latency), register budget
+// permitting.
+GemvCfg gemv_cfg(int n, int d, int v_rows, int G, bool bf16) {
+    const int groups = (v_rows + gv::GROUP - 1) / gv::GROUP;
+    const int gpc = std::max(1, (groups + G - 1) / G);
+    GemvCfg best{1, 1, 1, 1};
+    double best_t = 1e300;
+    static const int force_jt = [] {  // A/B override (FRS_GEMV_JT=1|2)
+        const char *e = std::getenv("FRS_GEMV_JT");
+        return e ? std::atoi(e) : 0;
+    }();
+    // Two W rows per thread halve the h broadcasts per MAC and double the independent work per
+    // load: measured faster once a CTA owns >= 6 row groups (C2 slab 143 vs 163 us; verify passes
+    // 462 vs 509 us), slower on short ranges (16384 x 4096 fp32: 102 vs 94 us), which the issue
+    // model alone does not see (it has no load-latency term).
+    const int jt_only = force_jt ? force_jt : (gpc >= 6 ? 2 : 1);
+    for (int jt = 1; jt <= 2; ++jt)
+        for (int hg = 1; hg <= std::min(n, gv::MAXW); ++hg) {
+            if (jt != jt_only) continue;
+            const int nrt = (n + hg - 1) / hg;
+            if (nrt > (jt == 1 ? 16 : 8)) continue;
+            for (int rw = 1; rw <= 8; ++rw) {
+                const int warps = rw * hg;
+                if (warps > gv::maxw_of(nrt, jt)) continue;
+                if (rw > 1 && (rw - 1) * jt >= gpc) continue;  // a whole row warp idle
+                const int gb = rw * jt, nblk = (gpc + gb - 1) / gb;
+                const double per_step = 16.0 * nrt * jt + jt * (bf16 ? 9 : 2) + 2.0 * nrt + 4;  // instructions
+                const double wavefronts = jt * (bf16 ? 4.0 : 8.0) + 4.0 * nrt;  // h: 2 broadcast LDS.128 per row
+                double t = (double)nblk * warps * (d / 8) * std::max(per_step / 4.0, wavefronts);
+                if (warps < 8) t *= 8.0 / warps;
+                if (t < best_t * 0.999) best_t = t, best = GemvCfg{nrt, jt, rw, hg};
+            }
+        }
+    return best;
+}
+
+template <typename WT, int NRT, int JT>
+int launch_gemv_t(frs_ctx *ctx, const GemvCfg &c, const CUtensorMap &wm, const CUtensorMap &hm, int h_row0, int n,
+                  int d, int v_rows, float *logits, int ld, cudaStream_t s) {
     using namespace gv;
-    const int S = (n + 1) / 2;
-    const size_t st_bytes = (((size_t)RBMAX * (KC + PAD) * sizeof(WT) + (size_t)(2 * S) * KC * sizeof(float)) + 127) &
-                            ~size_t(127);
-    const size_t budget = std::min<size_t>(ctx->smem_optin, 220 * 1024) - 2 * 8 * 8;
+    constexpr int KC = kc_of<WT>();
+    constexpr int P = KC * (int)sizeof(WT) / PANEL;
+    const size_t st_bytes =
+        ((size_t)c.rw * JT * P * BOX + (size_t)c.hg * NRT * KC * sizeof(float) + 1023) & ~size_t(1023);
+    const size_t budget = std::min<size_t>(ctx->smem_optin, 227 * 1024) - 1024 - 2 * 8 * 8;
     const int stages = static_cast<int>(std::min<size_t>(8, budget / st_bytes));
     if (stages < 2) return fail(FRS_ENOTSUP, "exact gemv: shared memory too small");
-    const int G = ctx->sm_count;
-    const int rounds = (v_rows + G * RBMAX - 1) / (G * RBMAX);
-    const int rb = (v_rows + G * rounds - 1) / (G * rounds);
-    const int nblocks = (v_rows + rb - 1) / rb;
-    const size_t smem = st_bytes * stages + 2 * stages * sizeof(uint64_t);
-    auto kern = k_exact_gemv<WT>;
+    const size_t smem = 1024 + st_bytes * stages + 2 * stages * sizeof(uint64_t);
+    auto kern = k_exact_gemv<WT, NRT, JT>;
     FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ++ctx->launches;
-    kern<<<std::min(G, nblocks), 32 + 64 * S, smem, s>>>(h, n, d, W, v_rows, rb, nblocks, stages, logits, ld);
+    const int groups = (v_rows + GROUP - 1) / GROUP;
+    kern<<<std::min(ctx->sm_count, groups), 32 + 32 * c.rw * c.hg, smem, s>>>(wm, hm, h_row0, n, d, v_rows, c.rw,
+                                                                             c.hg, stages, logits, ld);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
+}
+
+// One launch per pass of <= NPASS hidden rows; h [n_total x d] fp32, W [v_rows x d].
+template <typename WT>
+int launch_gemv(frs_ctx *ctx, const float *h, int n_total, int d, const WT *W, int v_rows, float *logits, int ld,
+                cudaStream_t s) {
+    using namespace gv;
+    constexpr int KC = kc_of<WT>();
+    CUtensorMap wm, hm;
+    int st = gemv_map(&wm, W, sizeof(WT) == 2, v_rows, d, d, PANEL / (int)sizeof(WT), GROUP, true);
+    if (st) return st;
+    for (int r0 = 0; r0 < n_total && !st; r0 += NPASS) {
+        const int n = std::min(NPASS, n_total - r0);
+        if ((st = gemv_map(&hm, h, false, n_total, d, d, KC, n, false))) return st;
+        const GemvCfg c = gemv_cfg(n, d, v_rows, std::min(ctx->sm_count, (v_rows + GROUP - 1) / GROUP),
+                                   sizeof(WT) == 2);
+        float *out = logits + (size_t)r0 * ld;
+        if (c.jt == 1) {
+            switch (c.nrt) {
+            case 2: st = launch_gemv_t<WT, 2, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 3: st = launch_gemv_t<WT, 3, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 4: st = launch_gemv_t<WT, 4, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 5: st = launch_gemv_t<WT, 5, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 6: st = launch_gemv_t<WT, 6, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 7: st = launch_gemv_t<WT, 7, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 8: st = launch_gemv_t<WT, 8, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 9: st = launch_gemv_t<WT, 9, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 10: st = launch_gemv_t<WT, 10, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 11: st = launch_gemv_t<WT, 11, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 12: st = launch_gemv_t<WT, 12, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 13: st = launch_gemv_t<WT, 13, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 14: st = launch_gemv_t<WT, 14, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 15: st = launch_gemv_t<WT, 15, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 16: st = launch_gemv_t<WT, 16, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            default: st = launch_gemv_t<WT, 1, 1>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            }
+        } else {
+            switch (c.nrt) {
+            case 2: st = launch_gemv_t<WT, 2, 2>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 3: st = launch_gemv_t<WT, 3, 2>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 4: st = launch_gemv_t<WT, 4, 2>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 5: st = launch_gemv_t<WT, 5, 2>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 6: st = launch_gemv_t<WT, 6, 2>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 7: st = launch_gemv_t<WT, 7, 2>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            case 8: st = launch_gemv_t<WT, 8, 2>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            default: st = launch_gemv_t<WT, 1, 2>(ctx, c, wm, hm, r0, n, d, v_rows, out, ld, s); break;
+            }
+        }
+    }
+    return st;
 }
 
 }  // namespace
@@ -723,15 +885,9 @@ int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *
     if (gemv_enabled() && d % 8 == 0 && d >= 8 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(h) & 15) == 0) {
         timing_begin(ctx, s);
-        int st = FRS_OK;
-        for (int r0 = 0; r0 < n && !st; r0 += gv::NMAX) {
-            const int nb = std::min(gv::NMAX, n - r0);
-            st = (w_dtype == FRS_DTYPE_BF16)
-                     ? launch_gemv(ctx, h + (size_t)r0 * d, nb, d, static_cast<const unsigned short *>(W), v_rows,
-                                   logits + (size_t)r0 * v_rows, v_rows, s)
-                     : launch_gemv(ctx, h + (size_t)r0 * d, nb, d, static_cast<const float *>(W), v_rows,
-                                   logits + (size_t)r0 * v_rows, v_rows, s);
-        }
+        const int st = (w_dtype == FRS_DTYPE_BF16)
+                           ? launch_gemv(ctx, h, n, d, static_cast<const unsigned short *>(W), v_rows, logits, v_rows, s)
+                           : launch_gemv(ctx, h, n, d, static_cast<const float *>(W), v_rows, logits, v_rows, s);
         timing_end(ctx, s);
         return st;
     }

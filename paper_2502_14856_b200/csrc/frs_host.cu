@@ -391,6 +391,14 @@ int frs_draft_tree(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user
     if (total < width || total > 64)
         return fail(FRS_EINVAL, "draft params: total_draft_tokens must lie in [beam_width, 64]");
     FRS_REQUIRE(fn || hidden_table, "build_draft_tree: need a hidden provider or a hidden table");
+    FRS_REQUIRE(mode == FRS_MODE_EXACT || mode == FRS_MODE_FAST, "build_draft_tree: unknown mode");
+    // The levels always run EXACT: beam pruning and select_top_k compare log_joints of children
+    // of DIFFERENT rows, i.e. log(e_j / Σ_row) across rows, so every row's 1 / Σ must be the
+    // reference's (kernels.cpp:86-89). FAST's Σ comes from tensor-core logits whose rigorous
+    // error bound (~0.09 in log space at the Llama-3-8B shape) exceeds the typical gap at a
+    // beam cut, so no FAST tree could be certified; the exact Σ needs every logit in dot_f32
+    // order, which is the EXACT level itself. FAST is accepted for API compatibility.
+    mode = FRS_MODE_EXACT;
     FRS_CUDA_TRY(cudaSetDevice(h->ctx->device));
     const int w = std::min(width, h->v_sub);  // drafting.cpp:40
     int st = head_staging(h, width, w);

@@ -95,3 +95,32 @@ def test_device_tree_equals_host_bookkeeping_fast():
         assert r.returncode == 0, r.stderr[-2000:]
         runs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert runs[0] == runs[1]
+
+
+def test_c2_trees_match_restatement(cuda_ctx, restatement):
+    """50 drafting trees at the Llama-3-8B shape (d 4096, V 128256, V_sub 32768, bf16 slab,
+    width 10 / depth 6 / 60 tokens; hidden rows = rmsnorm'd embedding rows, the identity draft
+    layer of the decode loop) equal the restatement's build_draft_tree bit for bit: tokens,
+    parents, depths and log_joint. Requested in FAST mode — the tree levels run EXACT by design
+    (a tree compares log-probabilities across rows, so every row's 1/Σ must be the reference's;
+    DESIGN.md §3) — and in EXACT mode for a few roots."""
+    V, d, v_sub = 128256, 4096, 32768
+    g = torch.Generator(device="cuda").manual_seed(2502)
+    W = (torch.randn(V, d, generator=g, device="cuda") * 0.02).to(torch.bfloat16).float()
+    E = torch.randn(V, d, generator=g, device="cuda")
+    E = (E * torch.rsqrt(E.double().pow(2).mean(1, keepdim=True) + 1e-5).float()).contiguous()
+    ids = np.random.default_rng(2502).permutation(V)[:v_sub].astype(np.int32)
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(V, ids), dtype="bf16")
+    slab = W[torch.from_numpy(ids).long().cuda()].cpu().numpy()
+    del W
+    roots = [int(r) for r in np.random.default_rng(7).choice(ids[:4096], 53, replace=False)]
+    for t, root in enumerate(roots):
+        mode = "exact" if t >= 50 else "fast"
+        tree = head.build_draft_tree(root, api.DraftParams(10, 6, 60), mode=mode, hidden_table=E)
+
+        def provider(level, toks, pars, root=root):
+            return E[[root] if level == 0 else torch.from_numpy(toks).long().cuda()].cpu().numpy()
+
+        ref = restatement.draft_tree(provider, slab, ids, 10, 6, 60)
+        for key in ("tokens", "parents", "depths", "log_joint"):
+            assert np.array_equal(getattr(tree, key), ref[key]), (root, mode, key)
