@@ -92,6 +92,12 @@ FRS_API int frs_ctx_timing_read(frs_ctx *ctx, double *total_ms, int *count);
  * for the globaltimer trace after the keys (see tools/fast_trace.py). */
 FRS_API int frs_debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float *pth,
                                     uint64_t *pkey, float *pw2);
+/* Known-answer check of the device glibc expf ports: for the float bit
+ * patterns first_bits + i, i < count, compare both device ports (branchy expf_glibc and
+ * branch-free expf_glibc_nb) with expected[i] (the host libm's expf, device buffer). out
+ * (device, 4 x u64, out[2..3] preset to ~0): mismatch counts, first mismatching i. */
+FRS_API int frs_debug_expf_check(frs_ctx *ctx, uint32_t first_bits, int64_t count, const float *expected,
+                                 uint64_t *out, void *stream);
 /* Number of kernels this library has launched on ctx (evidence for bench gpu_launches). */
 FRS_API int frs_ctx_launch_count(const frs_ctx *ctx, uint64_t *out);
 /* Pre-size workspaces for up to max_rows hidden rows against up to max_vocab head rows. */
@@ -280,6 +286,24 @@ FRS_API int frs_verify_greedy_table(frs_ctx *ctx, const float *table, int64_t V_
                                     const void *W, int V, int d, int w_dtype, int mode, const int32_t *tokens,
                                     const int32_t *parents, int k, int32_t *emitted, int *n_emitted, int32_t *path,
                                     int *n_path);
+
+/* AcceptanceStats (verification.h:52-62, verification.cpp:180-206): accepted lengths are
+ * VerifyOutcome::accepted_length() = |emitted| (accepted tokens + the bonus), at most 65 for a
+ * 64-node tree; histogram[len] counts iterations of that length, hist_len = the reference's
+ * histogram.size(). add: FRS_EINVAL outside [0, FRS_HIST_MAX). accepted_length_stats: FRS_EINVAL
+ * "accepted_length_stats: empty outcome list" for n == 0 (verification.cpp:199-201). */
+#define FRS_HIST_MAX 72
+typedef struct frs_acceptance_stats {
+    int64_t iterations;
+    int64_t emitted;
+    double mean_accepted_length;
+    int32_t hist_len;
+    int32_t pad_;
+    int64_t histogram[FRS_HIST_MAX];
+} frs_acceptance_stats;
+FRS_API int frs_acceptance_add(frs_acceptance_stats *s, int accepted_length);
+FRS_API int frs_acceptance_merge(frs_acceptance_stats *s, const frs_acceptance_stats *other);
+FRS_API int frs_accepted_length_stats(const int32_t *accepted_lengths, int n, frs_acceptance_stats *out);
 
 #ifdef __cplusplus
 }

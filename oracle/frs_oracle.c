@@ -449,3 +449,41 @@ int frs_o_draft_tree(frs_o_hidden_fn fn, void *user, const float *slab, int v_su
     free(prob);
     return rc;
 }
+
+/* The host libm's own expf (NOT the restatement above) over the float bit patterns
+ * first_bits + i, i < count: the known-answer values the device ports are checked against
+ * (SURVEY.md §4.4). Threads split the range; each value is one libm call. */
+typedef struct {
+    uint32_t first;
+    int64_t i0, i1;
+    float *out;
+} expf_job;
+static void *expf_worker(void *arg) {
+    const expf_job *J = (const expf_job *)arg;
+    for (int64_t i = J->i0; i < J->i1; ++i) {
+        const uint32_t b = J->first + (uint32_t)i;
+        float x;
+        memcpy(&x, &b, 4);
+        J->out[i] = expf(x);
+    }
+    return NULL;
+}
+void frs_o_libm_expf_range(uint32_t first_bits, int64_t count, float *out) {
+    enum { kMaxT = 64 };
+    long nt = sysconf(_SC_NPROCESSORS_ONLN);
+    if (nt < 1) nt = 1;
+    if (nt > kMaxT) nt = kMaxT;
+    pthread_t th[kMaxT];
+    expf_job jobs[kMaxT];
+    for (long t = 0; t < nt; ++t) {
+        jobs[t] = (expf_job){first_bits, count * t / nt, count * (t + 1) / nt, out};
+        th[t] = 0;
+        if (t > 0 && pthread_create(&th[t], NULL, expf_worker, &jobs[t]) != 0) {
+            th[t] = 0;
+            expf_worker(&jobs[t]);
+        }
+    }
+    expf_worker(&jobs[0]);
+    for (long t = 1; t < nt; ++t)
+        if (th[t]) pthread_join(th[t], NULL);
+}

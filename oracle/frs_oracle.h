@@ -73,4 +73,7 @@ int frs_o_draft_tree(frs_o_hidden_fn fn, void *user, const float *slab, int v_su
 #ifdef __cplusplus
 }
 #endif
+/* host libm expf over bit patterns first_bits + i, i < count (SURVEY.md §4.4 KAT values) */
+void frs_o_libm_expf_range(uint32_t first_bits, int64_t count, float *out);
+
 #endif

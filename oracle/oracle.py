@@ -55,6 +55,8 @@ class Restatement:
         L.frs_o_logits.argtypes = [_f32p, C.c_int, _f32p, C.c_int, C.c_int, _f32p]
         L.frs_o_expf_glibc.restype = C.c_float
         L.frs_o_expf_glibc.argtypes = [C.c_float]
+        L.frs_o_libm_expf_range.restype = None
+        L.frs_o_libm_expf_range.argtypes = [C.c_uint32, C.c_int64, _f32p]
         L.frs_o_softmax.argtypes = [_f32p, C.c_int, C.c_float, _f32p, C.POINTER(C.c_float),
                                     C.POINTER(C.c_double)]
         L.frs_o_topk.argtypes = [_f32p, C.c_int, C.c_int, _i32p, _f32p]
@@ -74,6 +76,12 @@ class Restatement:
     def dot_f32(self, a, b) -> np.float32:
         a, b = _c32(a), _c32(b)
         return np.float32(self.lib.frs_o_dot_f32(a, b, a.size))
+
+    def libm_expf_range(self, first_bits: int, count: int) -> np.ndarray:
+        """The host libm's expf over float bit patterns first_bits + i (not the restatement)."""
+        out = np.empty(count, np.float32)
+        self.lib.frs_o_libm_expf_range(first_bits, count, out)
+        return out
 
     def logits(self, h, W):
         h, W = _c32(h), _c32(W)
@@ -258,6 +266,9 @@ class Reference:
         L.ref_draft_session_compact.argtypes = [C.c_void_p, C.c_int, _i32p, C.c_int]
         L.ref_draft_session_draft_tree.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _i32p, C.c_int, C.c_int, C.c_int,
                                                    C.c_int, _i32p, _i32p, _i32p, _f64p, _ip]
+        L.ref_acceptance_stats.argtypes = [_i32p, C.c_int, _i32p, C.c_int, C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                           np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS"), C.c_int, _ip]
         L.ref_masked_attention.argtypes = [_f32p, _f32p, _f32p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _f32p]
         L.ref_read_token_stream.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, _ip, C.POINTER(C.c_int64)]
         L.ref_read_token_stream_text.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
@@ -491,6 +502,18 @@ class Reference:
                 ref.lib.ref_draft_session_free(self.h)
 
         return Session()
+
+    def acceptance_stats(self, lengths_a, lengths_b=None):
+        """accepted_length_stats(a) [.merge(accepted_length_stats(b))] -> (iterations, emitted,
+        mean, histogram); lengths_b=[] merges a default (empty) AcceptanceStats."""
+        a = _ci32(lengths_a)
+        b = _ci32(lengths_b if lengths_b is not None else [])
+        it, em, mean, hl = C.c_int64(), C.c_int64(), C.c_double(), C.c_int()
+        hist = np.zeros(128, np.int64)
+        self._check(self.lib.ref_acceptance_stats(a, a.size, b, -1 if lengths_b is None else b.size, C.byref(it),
+                                                  C.byref(em), C.byref(mean), hist, hist.size, C.byref(hl)),
+                    "accepted_length_stats")
+        return it.value, em.value, mean.value, hist[:hl.value].tolist()
 
     def masked_attention(self, q, k, v, allow):
         q, k, v = _c32(q), _c32(k), _c32(v)

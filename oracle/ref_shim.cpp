@@ -342,6 +342,32 @@ int ref_draft_session_draft_tree(void * sp, const int32_t * ordered, int v_sub, 
     });
 }
 
+// accepted_length_stats over outcomes with the given accepted lengths (|emitted| = len), then
+// (when nb >= 0) .merge() of the stats of a second list (nb == 0: a default AcceptanceStats).
+int ref_acceptance_stats(const int32_t * la, int na, const int32_t * lb, int nb, int64_t * iterations,
+                         int64_t * emitted, double * mean, int64_t * hist, int hist_cap, int * hist_len) {
+    return guarded([&] {
+        auto outcomes = [](const int32_t * l, int n) {
+            std::vector<VerifyOutcome> v(n);
+            for (int i = 0; i < n; ++i) v[i].emitted.assign(l[i], 0);
+            return v;
+        };
+        auto va = outcomes(la, na);
+        AcceptanceStats s = accepted_length_stats(va);
+        if (nb > 0) {
+            auto vb = outcomes(lb, nb);
+            s.merge(accepted_length_stats(vb));
+        } else if (nb == 0) {
+            s.merge(AcceptanceStats{});
+        }
+        *iterations = s.iterations;
+        *emitted = s.emitted;
+        *mean = s.mean_accepted_length;
+        *hist_len = static_cast<int>(s.histogram.size());
+        for (int i = 0; i < *hist_len && i < hist_cap; ++i) hist[i] = s.histogram[i];
+    });
+}
+
 // masked_attention (kernels.cpp:124-171) with a dense 0/1 mask [n x m].
 int ref_masked_attention(const float * q, const float * k, const float * v, const uint8_t * allow, int n, int m,
                          int dh, int dv, float * out) {

@@ -66,6 +66,7 @@ SIGNATURES = [
     ("frs_ctx_timing_read", _I, [_P, C.POINTER(C.c_double), C.POINTER(_I)]),
     ("frs_ctx_launch_count", _I, [_P, C.POINTER(_U64)]),
     ("frs_debug_fast_partials", _I, [_P, _I, _I, _P, _P, _P, _P, _P]),
+    ("frs_debug_expf_check", _I, [_P, C.c_uint32, _I64, _P, _P, _P]),
     ("frs_slab_build", _I, [_P, _P, _I64, _I, _P, _I, _I, _P, _P]),
     ("frs_slab_bytes", C.c_size_t, [_I, _I, _I]),
     ("frs_draft_head_topk", _I, [_P, _P, _I, _I, _P, _I, _I, _P, _I, _F, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
@@ -112,6 +113,20 @@ SIGNATURES = [
     ("frs_verify_greedy", _I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P, C.POINTER(_I)]),
     ("frs_verify_greedy_table", _I, [_P, _P, _I64, C.c_int32, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P,
                                      C.POINTER(_I)]),
+]
+
+
+
+class AcceptanceStatsC(C.Structure):  # frs_acceptance_stats (include/frspec_cuda.h)
+    HIST_MAX = 72
+    _fields_ = [("iterations", C.c_int64), ("emitted", C.c_int64), ("mean_accepted_length", C.c_double),
+                ("hist_len", C.c_int32), ("pad_", C.c_int32), ("histogram", C.c_int64 * 72)]
+
+
+SIGNATURES += [
+    ("frs_acceptance_add", _I, [C.POINTER(AcceptanceStatsC), _I]),
+    ("frs_acceptance_merge", _I, [C.POINTER(AcceptanceStatsC), C.POINTER(AcceptanceStatsC)]),
+    ("frs_accepted_length_stats", _I, [_P, _I, C.POINTER(AcceptanceStatsC)]),
 ]
 
 _LIB = None

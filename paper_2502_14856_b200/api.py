@@ -737,37 +737,42 @@ def verify_greedy_table(ctx: Context, table: torch.Tensor, root_token: int, lm_h
     return VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy())
 
 
-@dataclass
-class AcceptanceStats:  # verification.h:52-62, verification.cpp:180-206
-    iterations: int = 0
-    emitted: int = 0
-    mean_accepted_length: float = 0.0
-    histogram: list = field(default_factory=list)
+class AcceptanceStats:
+    """AcceptanceStats (verification.h:52-62, verification.cpp:180-206) over the C ABI
+    (frs_acceptance_add / frs_acceptance_merge / frs_accepted_length_stats)."""
+
+    def __init__(self):
+        self._c = _lib.AcceptanceStatsC()
+
+    @property
+    def iterations(self) -> int:
+        return int(self._c.iterations)
+
+    @property
+    def emitted(self) -> int:
+        return int(self._c.emitted)
+
+    @property
+    def mean_accepted_length(self) -> float:
+        return float(self._c.mean_accepted_length)
+
+    @property
+    def histogram(self) -> list:
+        return [int(self._c.histogram[i]) for i in range(self._c.hist_len)]
 
     def add(self, accepted_length: int) -> None:
-        self.iterations += 1
-        self.emitted += accepted_length
-        if len(self.histogram) <= accepted_length:
-            self.histogram.extend([0] * (accepted_length + 1 - len(self.histogram)))
-        self.histogram[accepted_length] += 1
-        self.mean_accepted_length = self.emitted / self.iterations
+        check(lib().frs_acceptance_add(C.byref(self._c), int(accepted_length)), "AcceptanceStats::add")
 
     def merge(self, other: "AcceptanceStats") -> None:
-        self.iterations += other.iterations
-        self.emitted += other.emitted
-        if len(self.histogram) < len(other.histogram):
-            self.histogram.extend([0] * (len(other.histogram) - len(self.histogram)))
-        for i, v in enumerate(other.histogram):
-            self.histogram[i] += v
-        self.mean_accepted_length = self.emitted / self.iterations if self.iterations else 0.0
+        check(lib().frs_acceptance_merge(C.byref(self._c), C.byref(other._c)), "AcceptanceStats::merge")
 
 
 def accepted_length_stats(outcomes: Sequence[VerifyOutcome]) -> AcceptanceStats:
-    if not outcomes:
-        raise InvalidArgument("accepted_length_stats: empty outcome list")
+    """verification.cpp:197-206 (raises InvalidArgument on an empty list, as the reference)."""
+    lens = np.array([o.accepted_length() for o in outcomes], np.int32)
     s = AcceptanceStats()
-    for o in outcomes:
-        s.add(o.accepted_length())
+    check(lib().frs_accepted_length_stats(_np_ptr(lens) if lens.size else None, int(lens.size), C.byref(s._c)),
+          "accepted_length_stats")
     return s
 
 

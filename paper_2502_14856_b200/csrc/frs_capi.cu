@@ -141,6 +141,15 @@ int frs_ctx_timing_read(frs_ctx *ctx, double *total_ms, int *count) {
     return FRS_OK;
 }
 
+int frs_debug_expf_check(frs_ctx *ctx, uint32_t first_bits, int64_t count, const float *expected, uint64_t *out,
+                         void *stream) {
+    int st = check_device(ctx);
+    if (st) return st;
+    FRS_REQUIRE(expected && out && count >= 0, "expf check: bad arguments");
+    return expf_kat(ctx, first_bits, count, expected, reinterpret_cast<unsigned long long *>(out),
+                    static_cast<cudaStream_t>(stream));
+}
+
 int frs_debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float *pth, uint64_t *pkey,
                             float *pw2) {
     int st = check_device(ctx);

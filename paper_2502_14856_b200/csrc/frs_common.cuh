@@ -95,6 +95,8 @@ int launch_masked_attention(frs_ctx *ctx, const float *q, const float *k, const 
                             cudaStream_t s);
 int count_tokens(frs_ctx *ctx, const int32_t *tokens, long long count, int vocab, unsigned long long *counts,
                  unsigned long long *bad_offset, cudaStream_t s);
+int expf_kat(frs_ctx *ctx, uint32_t first_bits, long long count, const float *expected, unsigned long long *out,
+             cudaStream_t s);
 int launch_softmax_probs(frs_ctx *ctx, const float *logits, int n, int v, float temperature, float *probs,
                          uint32_t *flags, cudaStream_t s);
 int launch_softmax_sample(frs_ctx *ctx, const float *logits, int n, int v, float temperature, const double *uniforms,

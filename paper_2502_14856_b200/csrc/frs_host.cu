@@ -1158,4 +1158,46 @@ int frs_draft_tree_model(frs_head *h, frs_draft_model *dm, const int32_t *pendin
     return st;
 }
 
+// AcceptanceStats::add / merge / accepted_length_stats (verification.cpp:180-206).
+int frs_acceptance_add(frs_acceptance_stats *s, int accepted_length) {
+    FRS_REQUIRE(s, "acceptance stats: null pointer");
+    if (accepted_length < 0 || accepted_length >= FRS_HIST_MAX)
+        return fail(FRS_EINVAL, "acceptance stats: accepted length " + std::to_string(accepted_length) + " out of range");
+    s->iterations += 1;
+    s->emitted += accepted_length;
+    if (s->hist_len <= accepted_length) {  // histogram.resize(accepted_length + 1, 0)
+        for (int i = std::max(s->hist_len, 0); i <= accepted_length; ++i) s->histogram[i] = 0;
+        s->hist_len = accepted_length + 1;
+    }
+    s->histogram[accepted_length] += 1;
+    s->mean_accepted_length = static_cast<double>(s->emitted) / static_cast<double>(s->iterations);
+    return FRS_OK;
+}
+
+int frs_acceptance_merge(frs_acceptance_stats *s, const frs_acceptance_stats *o) {
+    FRS_REQUIRE(s && o, "acceptance stats: null pointer");
+    FRS_REQUIRE(o->hist_len >= 0 && o->hist_len <= FRS_HIST_MAX, "acceptance stats: bad histogram length");
+    s->iterations += o->iterations;
+    s->emitted += o->emitted;
+    if (s->hist_len < o->hist_len) {
+        for (int i = std::max(s->hist_len, 0); i < o->hist_len; ++i) s->histogram[i] = 0;
+        s->hist_len = o->hist_len;
+    }
+    for (int i = 0; i < o->hist_len; ++i) s->histogram[i] += o->histogram[i];
+    s->mean_accepted_length =
+        s->iterations > 0 ? static_cast<double>(s->emitted) / static_cast<double>(s->iterations) : 0.0;
+    return FRS_OK;
+}
+
+int frs_accepted_length_stats(const int32_t *lengths, int n, frs_acceptance_stats *out) {
+    FRS_REQUIRE(out && (lengths || n == 0), "acceptance stats: null pointer");
+    if (n <= 0) return fail(FRS_EINVAL, "accepted_length_stats: empty outcome list");
+    std::memset(out, 0, sizeof(*out));
+    for (int i = 0; i < n; ++i) {
+        const int st = frs_acceptance_add(out, lengths[i]);
+        if (st) return st;
+    }
+    return FRS_OK;
+}
+
 }  // extern "C"

@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "frs_common.cuh"
+#include "frs_device.cuh"
 
 namespace frs {
 namespace {
@@ -216,6 +217,40 @@ int gather_rows(const float *table, long long rows, int d, const int32_t *tokens
                 cudaStream_t s) {
     const int splits = std::max(1, std::min(16, (d / 4 + 255) / 256));
     k_gather_rows<<<dim3(n, splits), 256, 0, s>>>(table, rows, d, tokens, n, out);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+// Known-answer check of the device glibc expf ports: for the
+// float bit patterns first_bits + i (i < count) compare expf_glibc and expf_glibc_nb with the
+// host libm's expf values `expected`; out[0..1] mismatch counts, out[2..3] first mismatching i
+// (atomicMin; preset to ~0 by the caller), variants 0 / 1.
+__global__ void k_expf_kat(uint32_t first_bits, long long count, const float *__restrict__ expected,
+                           unsigned long long *__restrict__ out) {
+    __shared__ unsigned long long tab[32];
+    dev::load_exp_table(tab);
+    __syncthreads();
+    unsigned long long bad0 = 0, bad1 = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+        const float x = __uint_as_float(first_bits + static_cast<uint32_t>(i));
+        const uint32_t want = __float_as_uint(expected[i]);
+        if (__float_as_uint(dev::expf_glibc(x, tab)) != want) {
+            ++bad0;
+            atomicMin(&out[2], static_cast<unsigned long long>(i));
+        }
+        if (__float_as_uint(dev::expf_glibc_nb(x, tab)) != want) {
+            ++bad1;
+            atomicMin(&out[3], static_cast<unsigned long long>(i));
+        }
+    }
+    if (bad0) atomicAdd(&out[0], bad0);
+    if (bad1) atomicAdd(&out[1], bad1);
+}
+
+int expf_kat(frs_ctx *ctx, uint32_t first_bits, long long count, const float *expected, unsigned long long *out,
+             cudaStream_t s) {
+    ++ctx->launches;
+    k_expf_kat<<<ctx->sm_count * 8, 256, 0, s>>>(first_bits, count, expected, out);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }

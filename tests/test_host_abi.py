@@ -69,3 +69,32 @@ def test_tree_mask(restatement):
         api.build_tree_mask(np.arange(-1, 64, dtype=np.int32))
     with pytest.raises(InvalidArgument):
         api.build_tree_mask(np.array([-1, 1], np.int32))
+
+
+def test_acceptance_stats_match_reference(reference):
+    """AcceptanceStats add / merge / accepted_length_stats through the C ABI against the
+    reference's own (verification.cpp:180-206), including the empty-list rejection."""
+    from paper_2502_14856_b200 import api
+    from paper_2502_14856_b200._lib import InvalidArgument
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        a = rng.integers(1, 8, rng.integers(1, 40)).tolist()
+        b = rng.integers(1, 12, rng.integers(0, 30)).tolist()
+        outs = [api.VerifyOutcome(np.zeros(max(x - 1, 0), np.int32), np.zeros(x, np.int32)) for x in a]
+        s = api.accepted_length_stats(outs)
+        if b:
+            s.merge(api.accepted_length_stats([api.VerifyOutcome(np.zeros(0, np.int32), np.zeros(x, np.int32))
+                                               for x in b]))
+        else:
+            s.merge(api.AcceptanceStats())
+        it, em, mean, hist = reference.acceptance_stats(a, b)
+        assert (s.iterations, s.emitted, s.histogram) == (it, em, hist)
+        assert s.mean_accepted_length == mean  # same double division
+    with pytest.raises(InvalidArgument, match="empty outcome list"):
+        api.accepted_length_stats([])
+    with pytest.raises(ValueError, match="empty outcome list"):
+        reference.acceptance_stats([])
+    s = api.AcceptanceStats()
+    s.add(3)
+    s.add(0)
+    assert s.histogram == [1, 0, 0, 1] and s.iterations == 2 and s.mean_accepted_length == 1.5

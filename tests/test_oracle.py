@@ -77,7 +77,8 @@ def test_rejections_match_reference(restatement, reference):
 
 def test_expf_port_matches_host_libm_sampled(restatement):
     """the glibc expf port equals host expf on [-104, 0]. Sampled here
-    (every 4099th float); the device port is checked exhaustively in the GPU tests."""
+    (every 4099th float); both device ports are checked exhaustively against host libm in
+    tests/test_gpu_expf_kat.py."""
     libm = ctypes.CDLL("libm.so.6")
     libm.expf.restype, libm.expf.argtypes = ctypes.c_float, [ctypes.c_float]
     lo = np.float32(-104.0).view(np.uint32)
