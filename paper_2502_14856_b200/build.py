@@ -12,12 +12,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libfrspec_cuda.so")
+# FRS_DIAG=1: the diagnostic variant (globaltimer probes, FRS_ABLATE phase skips compiled in)
+# in its own object dir and .so; load it with FRS_LIB_PATH (tools/fast_trace.py, tools/ablate.sh)
+DIAG = os.environ.get("FRS_DIAG") == "1"
+OBJ = os.path.join(HERE, "_build_diag" if DIAG else "_build")
+LIB = os.path.join(HERE, "libfrspec_cuda_diag.so" if DIAG else "libfrspec_cuda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC] + (["-DFRS_DIAG=1"] if DIAG else [])
 SOURCES = ["frs_capi.cu", "frs_host.cu", "frs_exact.cu", "frs_misc.cu", "frs_fast.cu", "frs_tree.cu", "frs_layer.cu"]
 
 

@@ -50,9 +50,18 @@
 #include "frs_common.cuh"
 #include "frs_device.cuh"
 
+// Diagnostics (globaltimer / clock64 probes, FRS_ABLATE phase skipping) are compiled in only
+// with -DFRS_DIAG=1 (FRS_DIAG=1 python -m paper_2502_14856_b200.build -> libfrspec_cuda_diag.so,
+// loaded through FRS_LIB_PATH by tools/fast_trace.py, tools/ablate.sh, tools/sm_balance_probe.py);
+// release kernels carry no branches for them.
+#ifndef FRS_DIAG
+#define FRS_DIAG 0
+#endif
+
 namespace frs {
 namespace {
 
+constexpr bool kDiag = FRS_DIAG != 0;
 constexpr int BM = 128;      // slab rows per tile (UMMA M)
 constexpr int CH = 32;       // slab rows per TMA box = partition granule: CTAs own contiguous
                              // runs of 32-row chunks (<= 1 chunk of imbalance instead of 1 tile)
@@ -184,7 +193,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define FRS_TRACE(P, slot)                                                       \
     do {                                                                         \
-        if ((P).trace) (P).trace[(size_t)blockIdx.x * kTrMain + (slot)] = gtimer();   \
+        if (kDiag && (P).trace) (P).trace[(size_t)blockIdx.x * kTrMain + (slot)] = gtimer();   \
     } while (0)
 
 // hs rows [0,NP) = bf16(h), rows [NP,2NP) = bf16(h - bf16(h)); padded rows are zero. Hidden
@@ -293,7 +302,10 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     using C = MainCfg<NP, SOFTMAX>;
     constexpr int N = C::N, STAGES = C::STAGES, RPW = C::RPW, TOPK = C::TOPK, EPI = C::EPI_WARPS;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned (SWIZZLE_128B) by arithmetic on smem_raw itself: the pointer stays in the
+    // shared window, so the epilogue's publish scratch is read and written with LDS/STS, not
+    // generic accesses (65.9 vs 66.9 us per C2 level)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = smem;                                   // STAGES x 16 KB
     uint8_t *sB = smem + STAGES * C::A_BYTES;             // STAGES x B_BYTES
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE_BYTES);
@@ -346,7 +358,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     if (threadIdx.x == 0) FRS_TRACE(P, 0);
     // let the finalize grid launch now: its CTAs take SMs as ours retire and run their
     // prologue; griddepcontrol.wait there still waits for this whole grid (and its writes)
-    if (!P.late_trigger) griddep_launch();
+    if (!(kDiag && P.late_trigger)) griddep_launch();
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -507,7 +519,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
-                if (!LOGITS && P.ablate_main == 15) continue;
+                if (!LOGITS && (kDiag && P.ablate_main == 15)) continue;
                 if constexpr (LOGITS) {  // coalesced: the warp's 32 lanes are 32 consecutive slab rows
 #pragma unroll
                     for (int r = 0; r < CG; ++r) {
@@ -565,7 +577,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         if constexpr (LOGITS) {
             (void)b1;
             (void)bnd;
-        } else if (P.ablate_main >= 14) {
+        } else if ((kDiag && P.ablate_main >= 14)) {
             asm volatile("bar.sync 1, %0;" ::"r"((2 + EPI) * 32) : "memory");
         } else {
         const int list = cta * kListsPerCta + q, L = G * kListsPerCta;
@@ -574,7 +586,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         // entries each and combine over 2 shuffle rounds. (Warp-wide REDUX/shuffle trees per
         // row took ~3 us at the tail of every call.)
         asm volatile("bar.sync 1, %0;" ::"r"((2 + EPI) * 32) : "memory");
-        if (P.trace && threadIdx.x == 128) P.trace[(size_t)blockIdx.x * kTrMain + 6] = static_cast<unsigned long long>(clock64() - c_pub0);
+        if (kDiag && P.trace && threadIdx.x == 128) P.trace[(size_t)blockIdx.x * kTrMain + 6] = static_cast<unsigned long long>(clock64() - c_pub0);
         constexpr int SLOT = C::SCRATCH_PER_WARP;
         uint8_t *scr = sA + we * SLOT;
         // per pass of 8 rows, lane-major with odd strides: the 8 rows a reader instruction
@@ -669,17 +681,22 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                 }
             }
         }
-        if (P.trace && threadIdx.x == 128) P.trace[(size_t)blockIdx.x * kTrMain + 31] = static_cast<unsigned long long>(clock64() - c_pub0);
+        if (kDiag && P.trace && threadIdx.x == 128) P.trace[(size_t)blockIdx.x * kTrMain + 31] = static_cast<unsigned long long>(clock64() - c_pub0);
         }  // !LOGITS
         if (threadIdx.x == 128) FRS_TRACE(P, 18);
-        if (P.trace && lane == 0 && (we == 0 || we == 4))  // DIAGNOSTIC: publish cycles
+        if (kDiag && P.trace && lane == 0 && (we == 0 || we == 4))  // DIAGNOSTIC: publish cycles
             P.trace[(size_t)blockIdx.x * kTrMain + (we == 0 ? 29 : 30)] = static_cast<unsigned long long>(clock64() - c_pub0);
     }
     __syncthreads();  // every TMEM read is done; s_rmax / s_w2max complete
     if (threadIdx.x < n && s_rmax[threadIdx.x]) atomicMax(P.rowmax_bits + threadIdx.x, s_rmax[threadIdx.x]);
     if (threadIdx.x == 64) atomicMax(P.w2_bits, s_w2max);
-    if (P.late_trigger) griddep_launch();
+    if (kDiag && P.late_trigger) griddep_launch();
     if (threadIdx.x == 0) FRS_TRACE(P, 7);
+    if (kDiag && P.trace && threadIdx.x == 0) {  // DIAGNOSTIC: the SM this CTA ran on
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        P.trace[(size_t)blockIdx.x * kTrMain + 17] = smid;
+    }
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, C::TMEM_COLS);
@@ -726,14 +743,14 @@ struct FinArgs {
 
 #define FRS_FTRACE(A, slot)                                                                              \
     do {                                                                                                  \
-        if ((A).P.trace && threadIdx.x == 0)                                                              \
+        if (kDiag && (A).P.trace && threadIdx.x == 0)                                                     \
             (A).P.trace[(size_t)(A).P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + blockIdx.y) * 16 + (slot)] = gtimer(); \
     } while (0)
 
 // DIAGNOSTIC: clock64 probes of select_certify (FRS_TRACE): [64 rows][16] cycles since entry
 #define FRS_CPROBE(A, q)                                                                                 \
     do {                                                                                                  \
-        if ((A).P.trace && (threadIdx.x & 31) == 0)                                                       \
+        if (kDiag && (A).P.trace && (threadIdx.x & 31) == 0)                                              \
             (A).P.trace[(size_t)(A).P.G * kTrMain + 64 * kFinCtas * 16 + 16 + (size_t)i * 16 + (q)] =    \
                 static_cast<unsigned long long>(clock64() - c_entry_);                                    \
     } while (0)
@@ -741,7 +758,7 @@ struct FinArgs {
 // DIAGNOSTIC: finalize phase cycles (leader CTA, thread 0) since griddepcontrol.wait returned
 #define FRS_FPROBE(A, q)                                                                                 \
     do {                                                                                                  \
-        if ((A).P.trace && threadIdx.x == 0 && cluster_rank() == 0)                                       \
+        if (kDiag && (A).P.trace && threadIdx.x == 0 && cluster_rank() == 0)                              \
             (A).P.trace[(size_t)(A).P.G * kTrMain + 64 * kFinCtas * 16 + 16 + (size_t)blockIdx.x * 16 + (q)] = \
                 static_cast<unsigned long long>(clock64() - c_fin0_);                                     \
     } while (0)
@@ -899,7 +916,7 @@ __device__ __forceinline__ void select_certify(const FinArgs &A, int i, int ns, 
                    dev::key_index(s_sorted[r]) > dev::key_index(s_sorted[r + 1]);
         }
     }
-    if (__any_sync(0xffffffffu, tie) || A.ablate == 11) why |= FRS_FLAG_CERT_TIE;  // 11: DIAGNOSTIC
+    if (__any_sync(0xffffffffu, tie) || (kDiag && A.ablate == 11)) why |= FRS_FLAG_CERT_TIE;  // 11: DIAGNOSTIC
     FRS_CPROBE(A, 3);
     if (!why && bnd_live) {  // every non-recomputed row stays strictly below the k-th
         if (!(x_ub < mx)) {
@@ -1041,7 +1058,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     griddep_wait();
     FRS_FTRACE(A, 2);
     const long long c_fin0_ = clock64();
-    if (A.ablate == 1) return;
+    if (kDiag && A.ablate == 1) return;
     // ---- 1. keys in registers, eps, histogram; softmax / bound partials
     const int kk = min(A.k, A.v_rows);
     constexpr int KPT = kMaxLists * R / kFinThreads;  // union keys per thread
@@ -1084,7 +1101,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     FRS_FPROBE(A, 9);  // filter done (thread 0's share)
     constexpr int SW = 4;                        // warps merging the softmax partials
     constexpr int PPL = kMaxLists / (32 * SW);   // partials per lane
-    if (warp < SW && !A.argmax && A.ablate != 5) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
+    if (warp < SW && !A.argmax && !(kDiag && (kDiag && A.ablate == 5))) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
         float pm[PPL], ps[PPL];
 #pragma unroll
         for (int u = 0; u < PPL; ++u) {
@@ -1214,7 +1231,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     FRS_FPROBE(A, 11);
     const int nsel = s_nsel;
     // ---- 3. exact recompute of my share (none if S overflowed: the leader falls back)
-    const int nmine = (nsel <= kCsMax && A.ablate != 2) ? min(s_nmine, kCsMax) : 0;
+    const int nmine = (nsel <= kCsMax && !(kDiag && (kDiag && A.ablate == 2))) ? min(s_nmine, kCsMax) : 0;
     for (int r0 = 0; r0 < nmine; r0 += A.fin_stage) {
         const int nc = min(A.fin_stage, nmine - r0);
         constexpr int TPT = 2;  // uint4 per thread per row and batch: T <= 512 in one batch
@@ -1313,7 +1330,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             if (s_pmw[w] != kNegInf) tot += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
     }
     const int ns = nsel <= kCsMax ? s_cnt : 0;  // == nsel when nothing overflowed
-    if (A.ablate == 3) return;
+    if (kDiag && A.ablate == 3) return;
     select_certify(A, i, ns, nsel, kk, a_bound, eps, any_bad != 0, tot, mm, s_fin, s_sel, s_sorted, s_tab, s_spos,
                    s_ord);
 }
@@ -1631,7 +1648,7 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
     __syncthreads();
     if (tid < ns && A.ordered) s_ord[tid] = __ldg(A.ordered + dev::key_index(s_sel[tid]));
     FRS_FTRACE(A, 6);
-    if (A.P.trace && tid == 0)
+    if (kDiag && A.P.trace && tid == 0)
         A.P.trace[(size_t)A.P.G * kTrMain + (size_t)blockIdx.x * kFinCtas * 16 + 8] =
             static_cast<unsigned long long>(ns) | (robust ? 1ull << 32 : 0ull);
     // ---- exact recompute of S, A.fin_stage candidates per round (dot_f32 order: lane chain l
@@ -1688,7 +1705,7 @@ __global__ void __launch_bounds__(kSelThreads) k_fast_select(FinArgs A) {
                 if (second) chain(hb, wb);
             }
             t = TS;
-            if (A.P.trace && tid == 0 && round == 0)  // DIAGNOSTIC: dot cycles (trace row i*8+1)
+            if (kDiag && A.P.trace && tid == 0 && round == 0)  // DIAGNOSTIC: dot cycles (trace row i*8+1)
                 A.P.trace[(size_t)A.P.G * kTrMain + ((size_t)blockIdx.x * kFinCtas + 1) * 16 + 15] =
                     static_cast<unsigned long long>(clock64() - c_begin);
             for (; t < T; ++t) s = __fadd_rn(s, __fmul_rn(hp[t], __uint_as_float(static_cast<uint32_t>(wp[8 * t]) << 16)));
@@ -1731,7 +1748,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fast_fallback(FinArgs A) {
     __shared__ int s_last;
     griddep_wait();
     griddep_launch();  // the next call's main kernel may become resident as we retire
-    unsigned long long *xtrace = A.P.trace ? A.P.trace + (size_t)A.P.G * kTrMain + 64 * kFinCtas * 16 : nullptr;
+    unsigned long long *xtrace = kDiag && A.P.trace ? A.P.trace + (size_t)A.P.G * kTrMain + 64 * kFinCtas * 16 : nullptr;
     if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[2] = gtimer();
     const unsigned nfb = *reinterpret_cast<volatile unsigned *>(A.fb_count);
     if (nfb == 0) {
