@@ -289,9 +289,11 @@ def main():
         hq = [rmsnorm_rows(torch.randn(qm, qd, generator=torch.Generator(device=dev).manual_seed(77 + j), device=dev))
               for j in range(4)]
 
+        vp_comm = api.NcclComm(ctx) if world > 1 else None  # the library's own NCCL communicator
+
         def vstep(j):
             if world > 1:
-                return api.verify_head_argmax_vocab_parallel(ctx, hq[j % 4], Wq, qV, mode=mode)
+                return api.verify_head_argmax_vocab_parallel(ctx, hq[j % 4], Wq, qV, vp_comm, mode=mode)
             return api.verify_head_argmax(ctx, hq[j % 4], Wq, id_offset=start, mode=mode)
 
         for j in range(5):

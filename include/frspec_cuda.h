@@ -236,10 +236,12 @@ typedef struct frs_rng frs_rng;
 /* build_draft_tree (drafting.cpp:122-245) driven by the device draft model: forwards the
  * pending context (root = its last token) and each level's beam through frs_draft_model with
  * the reference's positions and visibility, then truncates the cache back to the context.
- * rng == NULL: greedy (mode EXACT / FAST); else sampled (EXACT). Outputs as frs_draft_tree. */
+ * rng == NULL: greedy (levels EXACT); else sampled (EXACT). Outputs as frs_draft_tree; keep_probs
+ * outputs as frs_draft_tree_sampled (with an rng only, else FRS_ENOTSUP). */
 FRS_API int frs_draft_tree_model(frs_head *head, frs_draft_model *draft, const int32_t *pending, int n_pending,
                                  int width, int depth, int total, int mode, frs_rng *rng, int32_t *tokens,
-                                 int32_t *parents, int32_t *depths, double *log_joint, int *count);
+                                 int32_t *parents, int32_t *depths, double *log_joint, int *count, float *root_probs,
+                                 float *node_probs, int32_t *has_probs);
 /* Sampled drafting (drafting.cpp:44-74): a std::mt19937_64 the caller owns (the reference's
  * `std::mt19937_64 * rng`), advanced by every draw exactly as the reference advances it. */
 typedef struct frs_rng frs_rng;
@@ -257,11 +259,13 @@ FRS_API int frs_draft_head_sample(frs_ctx *ctx, const float *h, int n, int d, co
                                   const double *uniforms, float *probs, int32_t *out_ridx, int32_t *out_full,
                                   float *out_prob, int32_t *out_count, uint32_t *out_flags, void *stream);
 /* build_draft_tree with an rng (drafting.cpp:122-245: sampled children, prefix-closed
- * select_top_k), head path, EXACT arithmetic. Same arguments as frs_draft_tree plus rng. */
+ * select_top_k), head path, EXACT arithmetic. Same arguments as frs_draft_tree plus rng.
+ * keep_probs (drafting.h:31-37, DraftResult): root_probs [v_sub] and node_probs [total x v_sub]
+ * with has_probs [total] (0 = node not expanded, its row untouched), host buffers; NULL = off. */
 FRS_API int frs_draft_tree_sampled(frs_head *head, int32_t root_token, frs_hidden_fn fn, void *user,
                                    const float *hidden_table, int width, int depth, int total, frs_rng *rng,
                                    int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint,
-                                   int *count);
+                                   int *count, float *root_probs, float *node_probs, int32_t *has_probs);
 /* verify_stochastic (verification.cpp:76-178): h_dev holds 1 + k target rows (root first),
  * W the full target head [V x d]. The device computes the EXACT target logits and softmax
  * probabilities (kernels.cpp:13-32, 62-91); the residual walk (accept with probability
@@ -286,6 +290,22 @@ FRS_API int frs_verify_greedy_table(frs_ctx *ctx, const float *table, int64_t V_
                                     const void *W, int V, int d, int w_dtype, int mode, const int32_t *tokens,
                                     const int32_t *parents, int k, int32_t *emitted, int *n_emitted, int32_t *path,
                                     int *n_path);
+
+/* Vocab-parallel verify head (SURVEY.md §8(b) frs_allgather_merge, §8(e)): every rank of an NCCL
+ * communicator holds the contiguous LM-head shard [id_offset, id_offset + v_rows) (frs_vocab_shard)
+ * and calls this with the same 1 + k hidden rows h [m x d]: K3 over its shard, ncclAllGather of
+ * the per-row (value, id) pairs over NVLink / NVSwitch, K5 merge by (value desc, id asc) = the
+ * reference argmax's lowest-id rule over contiguous shards (kernels.cpp:113-122). out_id / out_val
+ * [m] (device) hold the global argmax on every rank; out_flags [m] this rank's K3 flags.
+ * comm is an ncclComm_t (NCCL resolved at run time: FRS_ENCCL when unavailable or failing,
+ * ncclCommGetAsyncError checked). frs_nccl_get_unique_id writes an ncclUniqueId (128 bytes) to be
+ * broadcast to every rank; frs_nccl_comm_init makes this rank's communicator on ctx's device. */
+FRS_API int frs_nccl_get_unique_id(void *id_out);
+FRS_API int frs_nccl_comm_init(frs_ctx *ctx, int nranks, const void *id, int rank, void **comm_out);
+FRS_API int frs_nccl_comm_destroy(void *comm);
+FRS_API int frs_verify_head_argmax_vp(frs_ctx *ctx, void *comm, const float *h, int m, int d, const void *W_shard,
+                                      int v_rows, int w_dtype, int32_t id_offset, int mode, int32_t *out_id,
+                                      float *out_val, uint32_t *out_flags, void *stream);
 
 /* AcceptanceStats (verification.h:52-62, verification.cpp:180-206): accepted lengths are
  * VerifyOutcome::accepted_length() = |emitted| (accepted tokens + the bonus), at most 65 for a

@@ -266,6 +266,10 @@ class Reference:
         L.ref_draft_session_compact.argtypes = [C.c_void_p, C.c_int, _i32p, C.c_int]
         L.ref_draft_session_draft_tree.argtypes = [C.c_void_p, C.c_void_p, C.c_int, _i32p, C.c_int, C.c_int, C.c_int,
                                                    C.c_int, _i32p, _i32p, _i32p, _f64p, _ip]
+        L.ref_draft_verify_rng.argtypes = [C.c_int] * 4 + [C.c_uint64, C.c_void_p, C.c_int, _i32p, C.c_int, C.c_int,
+                                                            C.c_int, C.c_int, C.c_uint64, _f32p, _f32p, C.c_float, _i32p,
+                                                            _i32p, _i32p, _f64p, _ip, _f32p, _f32p, _i32p, _i32p, _ip,
+                                                            _i32p, _ip]
         L.ref_acceptance_stats.argtypes = [_i32p, C.c_int, _i32p, C.c_int, C.POINTER(C.c_int64),
                                            C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                            np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS"), C.c_int, _ip]
@@ -502,6 +506,26 @@ class Reference:
                 ref.lib.ref_draft_session_free(self.h)
 
         return Session()
+
+    def draft_verify_rng(self, V, d, heads, max_seq, seed, ordered, pending, width, depth, total, rng_seed, h_t, W_t,
+                         temperature=1.0):
+        """Sampled build_draft_tree(keep_probs) then verify_stochastic with the same engine."""
+        o = _ci32(ordered)
+        p = _ci32(pending)
+        hv = o.size
+        tok, par, dep = (np.empty(total, np.int32) for _ in range(3))
+        lj = np.empty(total, np.float64)
+        rp, npb, hp = np.zeros(hv, np.float32), np.zeros((total, hv), np.float32), np.zeros(total, np.int32)
+        em, path = np.empty(total + 1, np.int32), np.empty(total + 1, np.int32)
+        cnt, ne, npth = C.c_int(), C.c_int(), C.c_int()
+        self._check(self.lib.ref_draft_verify_rng(V, d, heads, max_seq, seed, o.ctypes.data, hv, p, p.size, width, depth,
+                                                  total, rng_seed, _c32(h_t), _c32(W_t), temperature, tok, par, dep, lj,
+                                                  C.byref(cnt), rp, npb, hp, em, C.byref(ne), path, C.byref(npth)),
+                    "draft_verify_rng")
+        n = cnt.value
+        return dict(tokens=tok[:n].copy(), parents=par[:n].copy(), depths=dep[:n].copy(), log_joint=lj[:n].copy(),
+                    root_probs=rp, node_probs=npb[:n].copy(), has_probs=hp[:n].copy(), emitted=em[:ne.value].copy(),
+                    path=path[:npth.value].copy())
 
     def acceptance_stats(self, lengths_a, lengths_b=None):
         """accepted_length_stats(a) [.merge(accepted_length_stats(b))] -> (iterations, emitted,

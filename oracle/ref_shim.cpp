@@ -600,6 +600,43 @@ int ref_model_draft_tree_rng(int V, int d, int layers, int heads, int max_seq, u
     });
 }
 
+// Sampled drafting with keep_probs, then stochastic verification with the SAME engine (the
+// decode loop's order): build_draft_tree(rng, keep_probs = true) on a fresh cache, target logits
+// = matmul(h_t[0 .. K], W_t) (h_t: caller rows, root first), verify_stochastic(root, nodes, the
+// DraftResult, subset, temperature, rng). Exports the tree, its distributions and the outcome.
+int ref_draft_verify_rng(int V, int d, int heads, int max_seq, uint64_t seed, const int32_t * ordered, int v_sub,
+                         const int32_t * pending, int n_pending, int width, int depth, int total, uint64_t rng_seed,
+                         const float * h_t, const float * W_t, float temperature, int32_t * tokens,
+                         int32_t * parents, int32_t * depths, double * log_joint, int * count, float * root_probs,
+                         float * node_probs, int32_t * has_probs, int32_t * emitted, int * n_emitted, int32_t * path,
+                         int * n_path) {
+    return guarded([&] {
+        ModelBundle b = make_bundle(V, d, 1, heads, max_seq, seed, ordered, v_sub);
+        KVCache cache = make_cache(b.draft);
+        DraftParams p{width, depth, total};
+        std::mt19937_64 rng(rng_seed);
+        DraftResult r = build_draft_tree(b.draft, cache, std::span<const Token>(pending, n_pending), p,
+                                         ordered ? &b.head : nullptr, &rng, true);
+        export_tree(r.tree, tokens, parents, depths, log_joint, count);
+        const int K = *count;
+        const int hv = ordered ? v_sub : V;
+        std::copy(r.root_probs.begin(), r.root_probs.end(), root_probs);
+        for (int i = 0; i < K; ++i) {
+            has_probs[i] = r.node_probs[i].empty() ? 0 : 1;
+            if (has_probs[i]) std::copy(r.node_probs[i].begin(), r.node_probs[i].end(), node_probs + (size_t)i * hv);
+        }
+        Matrix logits = matmul(to_matrix(h_t, 1 + K, d), to_matrix(W_t, V, d));
+        Matrix node_logits(K, V);
+        if (K > 0) std::memcpy(node_logits.row(0), logits.row(1), sizeof(float) * (size_t)K * V);
+        VerifyOutcome o = verify_stochastic(logits.row_span(0), node_logits, r, ordered ? b.subset.get() : nullptr,
+                                            temperature, rng);
+        *n_emitted = static_cast<int>(o.emitted.size());
+        *n_path = static_cast<int>(o.accepted_path.size());
+        std::copy(o.emitted.begin(), o.emitted.end(), emitted);
+        std::copy(o.accepted_path.begin(), o.accepted_path.end(), path);
+    });
+}
+
 // Restatement of pick_children's sampled branch (drafting.cpp:44-74; the original sits in an
 // anonymous namespace), pinned by the sampled capture test against build_draft_tree above.
 static std::vector<std::pair<int, float>> pick_sampled(const std::vector<float> & probs, int width,

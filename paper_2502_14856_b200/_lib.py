@@ -99,7 +99,7 @@ SIGNATURES = [
     ("frs_draft_model_forward", _I, [_P, _P, _P, _I, _P, _P, _P]),
     ("frs_draft_model_position", _I, [_P, _I, C.POINTER(_I)]),
     ("frs_draft_model_compact", _I, [_P, _I, _P, _I, _P]),
-    ("frs_draft_tree_model", _I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, C.POINTER(_I)]),
+    ("frs_draft_tree_model", _I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, C.POINTER(_I), _P, _P, _P]),
     ("frs_masked_attention", _I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P]),
     ("frs_write_token_stream", _I, [C.c_char_p, _I, _P, _I64]),
     ("frs_read_token_stream", _I, [C.c_char_p, _P, _I64, C.POINTER(_I), C.POINTER(_I64)]),
@@ -109,7 +109,7 @@ SIGNATURES = [
     ("frs_verify_stochastic", _I, [_P, _P, _P, _I, _I, _I, _P, _P, _I, _P, _I, _P, _P, _P, C.c_float, _P, _P,
                                    C.POINTER(_I), _P, C.POINTER(_I)]),
     ("frs_draft_tree_sampled", _I, [_P, C.c_int32, HIDDEN_FN, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P,
-                                    C.POINTER(_I)]),
+                                    C.POINTER(_I), _P, _P, _P]),
     ("frs_verify_greedy", _I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P, C.POINTER(_I)]),
     ("frs_verify_greedy_table", _I, [_P, _P, _I64, C.c_int32, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P,
                                      C.POINTER(_I)]),
@@ -124,6 +124,10 @@ class AcceptanceStatsC(C.Structure):  # frs_acceptance_stats (include/frspec_cud
 
 
 SIGNATURES += [
+    ("frs_nccl_get_unique_id", _I, [_P]),
+    ("frs_nccl_comm_init", _I, [_P, _I, _P, _I, C.POINTER(_P)]),
+    ("frs_nccl_comm_destroy", _I, [_P]),
+    ("frs_verify_head_argmax_vp", _I, [_P, _P, _P, _I, _I, _P, _I, _I, C.c_int32, _I, _P, _P, _P, _P]),
     ("frs_acceptance_add", _I, [C.POINTER(AcceptanceStatsC), _I]),
     ("frs_acceptance_merge", _I, [C.POINTER(AcceptanceStatsC), C.POINTER(AcceptanceStatsC)]),
     ("frs_accepted_length_stats", _I, [_P, _I, C.POINTER(AcceptanceStatsC)]),

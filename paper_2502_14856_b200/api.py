@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (DTYPE_BF16, DTYPE_F32, MODE_EXACT, MODE_FAST, CapacityError, InvalidArgument, check,
+from ._lib import (DTYPE_BF16, DTYPE_F32, MODE_EXACT, MODE_FAST, CapacityError, InvalidArgument, NotSupported, check,
                    lib)
 
 _DTYPES = {"f32": DTYPE_F32, "fp32": DTYPE_F32, "float32": DTYPE_F32, "bf16": DTYPE_BF16, "bfloat16": DTYPE_BF16}
@@ -453,26 +453,57 @@ def argmax_merge_host(vals: np.ndarray, ids: np.ndarray):
     return ov, oi
 
 
+class NcclComm:
+    """An NCCL communicator owned by the library (frs_nccl_comm_init): rank 0 makes the
+    ncclUniqueId, `group` (any torch.distributed group, gloo or nccl) broadcasts it, every rank
+    joins on ctx's device. Used by verify_head_argmax_vocab_parallel."""
+
+    def __init__(self, ctx: Context, group=None):
+        import torch.distributed as dist
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = (C.c_ubyte * 128)()
+        if self.rank == 0:
+            check(lib().frs_nccl_get_unique_id(uid), "nccl unique id")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        check(lib().frs_nccl_comm_init(ctx.handle, self.world, uid, self.rank, C.byref(h)), "nccl comm init")
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            check(lib().frs_nccl_comm_destroy(self.handle), "nccl comm destroy")
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def verify_head_argmax_vocab_parallel(ctx: Context, h: torch.Tensor, W_shard: torch.Tensor, vocab_size: int,
-                                      group=None, mode="fast", stream=None):
-    """Vocab-parallel verify head: this rank holds rows [start, start + count) of the LM head
-    (`vocab_shard`), computes the per-row argmax of its shard on the device (K3 with id_offset),
-    all-gathers the (value, id) pairs over `group` (NCCL on GPUs) and merges them by
-    (value desc, id asc) — argmax's lowest-id rule (kernels.cpp:117-121) — with K5."""
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    start, count = vocab_shard(vocab_size, world, rank)
+                                      comm: NcclComm, mode="fast", stream=None):
+    """Vocab-parallel verify head through the C ABI (frs_verify_head_argmax_vp): this rank holds
+    rows [start, start + count) of the LM head (`vocab_shard`); K3 on its shard (id_offset =
+    start), ncclAllGather of every rank's (value, id) pairs, K5 merge by (value desc, id asc) —
+    argmax's lowest-id rule (kernels.cpp:117-121). Returns (ids, values, this rank's flags)."""
+    start, count = vocab_shard(vocab_size, comm.world, comm.rank)
     if W_shard.shape[0] != count:
-        raise InvalidArgument(f"verify (vocab-parallel): rank {rank} holds {W_shard.shape[0]} rows, expected {count}")
-    ids, vals, flags = verify_head_argmax(ctx, h, W_shard, id_offset=start, mode=mode, stream=stream)
-    m = ids.numel()
-    gv = torch.empty((world, m), dtype=torch.float32, device=h.device)
-    gi = torch.empty((world, m), dtype=torch.int32, device=h.device)
-    dist.all_gather_into_tensor(gv, vals, group=group)
-    dist.all_gather_into_tensor(gi, ids, group=group)
-    ov, oi = argmax_merge(ctx, gv, gi, stream=stream)
-    return oi, ov, flags
+        raise InvalidArgument(f"verify (vocab-parallel): rank {comm.rank} holds {W_shard.shape[0]} rows, expected {count}")
+    h = h.contiguous()
+    m, d = h.shape
+    if W_shard.dim() != 2 or W_shard.shape[1] != d:
+        raise InvalidArgument(f"matmul: inner dimensions differ ({tuple(h.shape)} vs {tuple(W_shard.shape)})")
+    dt = DTYPE_BF16 if W_shard.dtype == torch.bfloat16 else DTYPE_F32
+    ids = torch.empty(m, dtype=torch.int32, device=h.device)
+    vals = torch.empty(m, dtype=torch.float32, device=h.device)
+    flags = torch.zeros(m, dtype=torch.int32, device=h.device)
+    check(lib().frs_verify_head_argmax_vp(ctx.handle, comm.handle, _ptr(h), m, d, _ptr(W_shard), W_shard.shape[0], dt,
+                                          start, _mode(mode), _ptr(ids), _ptr(vals), _ptr(flags), _stream(stream)),
+          "verify_head_argmax_vp")
+    return ids, vals, flags
 
 
 def gather_rows(ctx: Context, table: torch.Tensor, tokens: torch.Tensor, out: Optional[torch.Tensor] = None,
@@ -494,11 +525,14 @@ class DraftParams:  # drafting.h:13-17
 
 
 @dataclass
-class DraftTree:  # drafting.h:21-29 as parallel arrays
+class DraftTree:  # drafting.h:21-29 as parallel arrays (+ DraftResult's distributions, drafting.h:31-37)
     tokens: np.ndarray
     parents: np.ndarray
     depths: np.ndarray
     log_joint: np.ndarray
+    root_probs: Optional[np.ndarray] = None  # keep_probs: [V_sub] root distribution
+    node_probs: Optional[np.ndarray] = None  # keep_probs: [K, V_sub], rows of unexpanded nodes zero
+    has_probs: Optional[np.ndarray] = None   # keep_probs: [K] 1 where node_probs[i] was recorded
 
     def __len__(self) -> int:
         return int(self.tokens.size)
@@ -553,13 +587,15 @@ class DeviceHead:
 
     def build_draft_tree(self, root_token: int, params: DraftParams = DraftParams(), mode="exact",
                          provider: Optional[Callable] = None, hidden_table: Optional[torch.Tensor] = None,
-                         rng: Optional["Rng"] = None) -> DraftTree:
+                         rng: Optional["Rng"] = None, keep_probs: bool = False) -> DraftTree:
         """Head-path build_draft_tree (drafting.cpp:122-245). provider(level, tokens,
         parent_cands) -> CUDA float32 [n x d] tensor of the forwarded rows' hidden states.
         rng=None: greedy children (top-width); with an Rng: sampled children without
         replacement (drafting.cpp:44-74, EXACT arithmetic) and the prefix-closed selection."""
         if rng is not None and mode != "exact":
             raise ValueError("sampled drafting runs on the exact probabilities: mode must be 'exact'")
+        if keep_probs and rng is None:
+            raise NotSupported("keep_probs is provided with an rng (sampled drafting)")
         keep = {}
 
         def cb(_user, level, n, tok_p, par_p, hidden_dev, stream):
@@ -584,14 +620,19 @@ class DeviceHead:
                                       params.search_depth, total, _mode(mode), _np_ptr(tok), _np_ptr(par),
                                       _np_ptr(dep), _np_ptr(lj), C.byref(cnt))
         else:
+            rp, npb, hp = _probs_buffers(keep_probs, total, self.subset.size())
             st = lib().frs_draft_tree_sampled(self.handle, root_token, fn, None, _ptr(hidden_table),
                                               params.beam_width, params.search_depth, total, rng.handle,
-                                              _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt))
+                                              _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt),
+                                              _np_ptr(rp), _np_ptr(npb), _np_ptr(hp))
         if "exc" in keep:
             raise keep["exc"]
         check(st, "build_draft_tree")
         n = cnt.value
-        return DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy())
+        tree = DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy())
+        if rng is not None and keep_probs:
+            tree.root_probs, tree.node_probs, tree.has_probs = rp, npb[:n].copy(), hp[:n].copy()
+        return tree
 
 
 class Rng:
@@ -648,11 +689,19 @@ def draft_head_sample(ctx: Context, h: torch.Tensor, head: "RestrictedHead", wid
     return out
 
 
+def _probs_buffers(keep_probs: bool, total: int, v_sub: int):
+    if not keep_probs:
+        return None, None, None
+    return (np.zeros(v_sub, np.float32), np.zeros((max(total, 1), v_sub), np.float32),
+            np.zeros(max(total, 1), np.int32))
+
+
 def build_draft_tree_model(head: "DeviceHead", draft: "DraftModel", pending, params: "DraftParams" = None,
-                           mode="exact", rng: Optional["Rng"] = None) -> "DraftTree":
+                           mode="exact", rng: Optional["Rng"] = None, keep_probs: bool = False) -> "DraftTree":
     """build_draft_tree (drafting.cpp:122-245) with the device draft model as the hidden-state
     source (the reference's own drafting loop: pending context forward, per-level beam forwards
-    with tree visibility, cache truncated back). rng: sampled children (EXACT arithmetic)."""
+    with tree visibility, cache truncated back). rng: sampled children (EXACT arithmetic);
+    keep_probs (with rng): the DraftResult distributions stochastic verification consumes."""
     params = params or DraftParams()
     if rng is not None and mode != "exact":
         raise ValueError("sampled drafting runs on the exact probabilities: mode must be 'exact'")
@@ -660,12 +709,17 @@ def build_draft_tree_model(head: "DeviceHead", draft: "DraftModel", pending, par
     total = params.total_draft_tokens
     tok, par, dep = (np.empty(max(total, 1), np.int32) for _ in range(3))
     lj, cnt = np.empty(max(total, 1), np.float64), C.c_int()
+    rp, npb, hp = _probs_buffers(keep_probs, total, head.subset.size())
     check(lib().frs_draft_tree_model(head.handle, draft.handle, _np_ptr(pend), pend.size, params.beam_width,
                                      params.search_depth, total, _mode(mode), None if rng is None else rng.handle,
-                                     _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt)),
+                                     _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt),
+                                     _np_ptr(rp), _np_ptr(npb), _np_ptr(hp)),
           "build_draft_tree")
     n = cnt.value
-    return DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy())
+    tree = DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy())
+    if keep_probs:
+        tree.root_probs, tree.node_probs, tree.has_probs = rp, npb[:n].copy(), hp[:n].copy()
+    return tree
 
 
 class _DeviceView:

@@ -21,7 +21,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC] + (["-DFRS_DIAG=1"] if DIAG else [])
-SOURCES = ["frs_capi.cu", "frs_host.cu", "frs_exact.cu", "frs_misc.cu", "frs_fast.cu", "frs_tree.cu", "frs_layer.cu"]
+SOURCES = ["frs_capi.cu", "frs_host.cu", "frs_exact.cu", "frs_misc.cu", "frs_fast.cu", "frs_tree.cu", "frs_layer.cu",
+           "frs_nccl.cu"]
 
 
 def _stale(src: str, obj: str) -> bool:
@@ -51,7 +52,7 @@ def build(verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda n: _compile(n, verbose), SOURCES))
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", LIB, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -66,6 +66,7 @@ struct frs_ctx {
     frs::DevBuf trace;     // FAST main-kernel globaltimer stamps when FRS_TRACE is set (diagnostics)
     frs::DevBuf hbuf;      // host-API staging of hidden rows
     frs::DevBuf obuf;      // host-API staging of outputs
+    frs::DevBuf vp_buf;    // vocab-parallel verify: local + all-gathered (value, id) pairs
     void *pinned = nullptr;
     size_t pinned_bytes = 0;
     cudaStream_t stream = nullptr;  // owned stream for the host-buffer conveniences

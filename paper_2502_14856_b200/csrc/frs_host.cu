@@ -651,7 +651,8 @@ int frs_rng_uniforms(frs_rng *rng, int count, double *out) {
 // to the level's start. select_top_k is prefix-closed (drafting.cpp:93-118).
 int frs_draft_tree_sampled(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user, const float *hidden_table,
                            int width, int depth, int total, frs_rng *rng, int32_t *tokens, int32_t *parents,
-                           int32_t *depths, double *log_joint, int *count) {
+                           int32_t *depths, double *log_joint, int *count, float *root_probs, float *node_probs,
+                           int32_t *has_probs) {
     FRS_REQUIRE(h && rng && tokens && parents && depths && log_joint && count, "build_draft_tree: null pointer");
     if (width < 1) return fail(FRS_EINVAL, "draft params: beam_width must be >= 1");
     if (depth < 1) return fail(FRS_EINVAL, "draft params: search_depth must be >= 1");
@@ -679,6 +680,12 @@ int frs_draft_tree_sampled(frs_head *h, int32_t root_token, frs_hidden_fn fn, vo
     std::vector<double> uh;
     std::vector<int> idx;
     std::vector<float> pr, probs_host;
+    // keep_probs (drafting.cpp:140-141, 219, 236-238): the distribution of every expanded node,
+    // by candidate index (-1: the root anchor), copied out of the level's exact probabilities
+    const bool keep = root_probs || node_probs;
+    FRS_REQUIRE(!node_probs || has_probs, "build_draft_tree: node_probs needs has_probs");
+    std::vector<std::vector<float>> kept;  // by candidate index
+    std::vector<float> root_kept;
     // one level: hidden rows, device sampling (or host replay), children appended in beam order
     auto run_level = [&](int level, int nb, const std::vector<int> &parents_of_rows) -> int {
         if (fn) {
@@ -715,11 +722,23 @@ int frs_draft_tree_sampled(frs_head *h, int32_t root_token, frs_hidden_fn fn, vo
         for (int i = 0; i < nb; ++i)
             if (hb[3 * cells + nb + i] & FRS_FLAG_NONFINITE)
                 return fail(FRS_EINVAL, "softmax: non-finite logit");  // kernels.cpp:72-74
-        if (replay) {  // rewind and redo the whole level on the host (rows in order)
-            rng->engine = saved;
+        if (replay || keep) {  // rewind and redo the whole level on the host (rows in order) / keep_probs
+            if (replay) rng->engine = saved;
             probs_host.resize((size_t)nb * h->v_sub);
             FRS_CUDA_TRY(cudaMemcpy(probs_host.data(), h->smp_probs.ptr, probs_host.size() * sizeof(float),
                                     cudaMemcpyDeviceToHost));
+        }
+        if (keep) {
+            for (int i = 0; i < nb; ++i) {
+                const float *row = probs_host.data() + (size_t)i * h->v_sub;
+                const int par = parents_of_rows[i];
+                if (par < 0) {
+                    root_kept.assign(row, row + h->v_sub);
+                } else {
+                    if ((int)kept.size() <= par) kept.resize(par + 1);
+                    kept[par].assign(row, row + h->v_sub);
+                }
+            }
         }
         for (int i = 0; i < nb; ++i) {
             int m;
@@ -798,8 +817,14 @@ int frs_draft_tree_sampled(frs_head *h, int32_t root_token, frs_hidden_fn fn, vo
         parents[out] = cands[i].parent >= 0 ? remap[cands[i].parent] : -1;
         depths[out] = cands[i].depth;
         log_joint[out] = cands[i].log_joint;
+        if (node_probs) {  // recorded only for expanded nodes; others stay empty (drafting.h:31-33)
+            const bool ex = i < kept.size() && !kept[i].empty();
+            has_probs[out] = ex ? 1 : 0;
+            if (ex) std::memcpy(node_probs + (size_t)out * h->v_sub, kept[i].data(), sizeof(float) * h->v_sub);
+        }
         ++out;
     }
+    if (root_probs) std::memcpy(root_probs, root_kept.data(), sizeof(float) * h->v_sub);
     *count = out;
     return FRS_OK;
 }
@@ -1144,13 +1169,18 @@ static int model_provider_cb(void *user, int level, int n, const int32_t *tokens
 
 int frs_draft_tree_model(frs_head *h, frs_draft_model *dm, const int32_t *pending, int n_pending, int width,
                          int depth, int total, int mode, frs_rng *rng, int32_t *tokens, int32_t *parents,
-                         int32_t *depths, double *log_joint, int *count) {
+                         int32_t *depths, double *log_joint, int *count, float *root_probs, float *node_probs,
+                         int32_t *has_probs) {
     FRS_REQUIRE(h && dm && pending, "build_draft_tree: null pointer");
     if (n_pending < 1) return fail(FRS_EINVAL, "build_draft_tree: pending must end with the root token");
     ModelProvider mp{dm, pending, n_pending};
     mp.d = h->d;
+    if (!rng && (root_probs || node_probs))
+        return fail(FRS_ENOTSUP, "build_draft_tree: keep_probs is provided with an rng (sampled drafting, the "
+                                 "distributions verify_stochastic consumes)");
     int st = rng ? frs_draft_tree_sampled(h, pending[n_pending - 1], model_provider_cb, &mp, nullptr, width, depth,
-                                          total, rng, tokens, parents, depths, log_joint, count)
+                                          total, rng, tokens, parents, depths, log_joint, count, root_probs,
+                                          node_probs, has_probs)
                  : frs_draft_tree(h, pending[n_pending - 1], model_provider_cb, &mp, nullptr, width, depth, total,
                                   mode, tokens, parents, depths, log_joint, count);
     tl_beam_cands = nullptr;

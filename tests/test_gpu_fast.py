@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from paper_2502_14856_b200 import api
-from paper_2502_14856_b200._lib import FLAG_NONFINITE, FLAG_RECOMPUTED, FLAG_UNCERTIFIED
+from paper_2502_14856_b200._lib import FLAG_NONFINITE, FLAG_RECOMPUTED, FLAG_UNCERTIFIED, InvalidArgument
 
 pytestmark = pytest.mark.gpu
 PROB_RTOL = 1e-4  # relative tolerance on FAST probabilities (approximate Σexp denominator)
@@ -208,7 +208,8 @@ def test_vocab_parallel_emulated(cuda_ctx, restatement, G):
 
 
 def test_vocab_parallel_nccl_world1(cuda_ctx, restatement):
-    """The NCCL path of api.verify_head_argmax_vocab_parallel (all_gather + K5) on a 1-rank group."""
+    """The C-ABI vocab-parallel verify (frs_verify_head_argmax_vp: K3 + ncclAllGather + K5) on a
+    1-rank NCCL communicator made by the library (the unique id broadcast over a gloo group)."""
     import socket
     import torch.distributed as dist
     if dist.is_initialized():
@@ -217,17 +218,22 @@ def test_vocab_parallel_nccl_world1(cuda_ctx, restatement):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                            device_id=torch.device("cuda", 0))
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     try:
+        comm = api.NcclComm(cuda_ctx)
         rng = np.random.default_rng(3)
         V, d, m = 5000, 256, 7
         W = torch.from_numpy((rng.standard_normal((V, d)) * 0.02).astype(np.float32)).to(torch.bfloat16)
         h = rmsnorm(rng.standard_normal((m, d)))
-        ids, vals, _ = api.verify_head_argmax_vocab_parallel(cuda_ctx, torch.from_numpy(h).cuda(), W.cuda(), V)
         rid, rval = restatement.verify_argmax(h, W.float().numpy())
-        assert np.array_equal(ids.cpu().numpy(), rid)
-        assert np.array_equal(vals.cpu().numpy(), rval)
+        for mode in ("fast", "exact"):
+            ids, vals, _ = api.verify_head_argmax_vocab_parallel(cuda_ctx, torch.from_numpy(h).cuda(), W.cuda(), V, comm,
+                                                                 mode=mode)
+            assert np.array_equal(ids.cpu().numpy(), rid), mode
+            assert np.array_equal(vals.cpu().numpy(), rval), mode
+        with pytest.raises(InvalidArgument):
+            api.verify_head_argmax_vocab_parallel(cuda_ctx, torch.from_numpy(h).cuda(), W[:10].cuda(), V, comm)
+        comm.close()
     finally:
         dist.destroy_process_group()
 

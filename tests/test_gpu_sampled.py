@@ -163,3 +163,39 @@ def test_verify_stochastic_paths_cover_accept_and_reject():
     if not _LENS:
         pytest.skip("parity cases did not run")
     assert min(_LENS) == 0 and max(_LENS) >= 2, _LENS
+
+
+@pytest.mark.parametrize("seed,rng_seed,width,depth,total", [(7, 11, 4, 3, 12), (9, 5, 6, 4, 24), (13, 3, 3, 2, 6)])
+def test_sampled_tree_keep_probs_then_verify_stochastic(cuda_ctx, reference, seed, rng_seed, width, depth, total):
+    """The decode loop's stochastic step end to end through the C ABI: sampled drafting with
+    keep_probs on the device draft model (frs_draft_tree_model), its DraftResult distributions fed
+    to frs_verify_stochastic with the same engine — tree, root/node distributions, emitted tokens
+    and accepted path all equal the reference's build_draft_tree(rng, keep_probs) followed by
+    verify_stochastic (drafting.cpp:122-245, verification.cpp:76-178)."""
+    V, d, heads, max_seq = 900, 64, 4, 64
+    sess = reference.draft_session(V, d, heads, max_seq, seed)
+    draft = api.DraftModel(cuda_ctx, sess.weights(), heads, max_seq)
+    W = reference.model_lm_head(V, d, 1, heads, seed)
+    ordered = np.random.default_rng(seed).permutation(V)[:300].astype(np.int32)
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(V, ordered), dtype="f32")
+    g = np.random.default_rng(seed + 1)
+    h_t = g.standard_normal((total + 1, d)).astype(np.float32)
+    W_t = (g.standard_normal((V, d)) * 0.3).astype(np.float32)
+    pending = [5, 17, 42]
+    ref = reference.draft_verify_rng(V, d, heads, max_seq, seed, ordered, pending, width, depth, total, rng_seed, h_t,
+                                     W_t)
+    rng = api.Rng(rng_seed)
+    tree = api.build_draft_tree_model(head, draft, pending, api.DraftParams(width, depth, total), rng=rng,
+                                      keep_probs=True)
+    for key in ("tokens", "parents", "depths", "log_joint"):
+        assert np.array_equal(getattr(tree, key), ref[key]), key
+    assert np.array_equal(tree.root_probs, ref["root_probs"])
+    assert np.array_equal(tree.has_probs, ref["has_probs"])
+    assert np.array_equal(tree.node_probs, ref["node_probs"])
+    K = len(tree)
+    out = api.verify_stochastic(cuda_ctx, torch.from_numpy(h_t[:K + 1]).cuda(), torch.from_numpy(W_t).cuda(), tree,
+                                tree.root_probs, tree.node_probs, tree.has_probs, ordered, rng)
+    assert np.array_equal(out.emitted, ref["emitted"])
+    assert np.array_equal(out.accepted_path, ref["path"])
+    with pytest.raises(api.NotSupported):
+        api.build_draft_tree_model(head, draft, pending, api.DraftParams(width, depth, total), keep_probs=True)

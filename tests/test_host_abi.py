@@ -98,3 +98,14 @@ def test_acceptance_stats_match_reference(reference):
     s.add(3)
     s.add(0)
     assert s.histogram == [1, 0, 0, 1] and s.iterations == 2 and s.mean_accepted_length == 1.5
+
+
+def test_nccl_unique_id_through_the_abi():
+    """The vocab-parallel boundary resolves NCCL at run time (dlopen): the unique id a rank 0
+    broadcasts comes out of the library (no GPU needed for the id itself)."""
+    import ctypes as C
+    uid = (C.c_ubyte * 128)()
+    rc = lib().frs_nccl_get_unique_id(uid)
+    if rc != 0:
+        pytest.skip("NCCL not loadable here: " + lib().frs_last_error().decode())
+    assert any(bytes(uid))

@@ -2,8 +2,9 @@
 contiguous shard ranges, the all-gather of per-shard (value, id) argmax pairs, and the merge
 by (value desc, id asc) — checked against the oracle's full-vocabulary argmax, including
 ties that straddle the shard boundary. The per-shard argmax here is the oracle's (test-only);
-on GPUs the same plumbing runs K3 + NCCL + K5 (api.verify_head_argmax_vocab_parallel,
-tests/test_gpu_fast.py::test_vocab_parallel_emulated)."""
+on GPUs the same plumbing runs K3 + ncclAllGather + K5 inside the library
+(frs_verify_head_argmax_vp via api.verify_head_argmax_vocab_parallel,
+tests/test_gpu_fast.py::test_vocab_parallel_nccl_world1 / ::test_vocab_parallel_emulated)."""
 import os
 import socket
 
