@@ -2096,7 +2096,9 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
                     float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s,
                     bool argmax = false, int32_t id_offset = 0) {
     if (k > 64) return fail(FRS_ENOTSUP, "FAST draft head: k <= 64");
-    const int NP = 64;  // N = 128: the NP=32 variant measured slower (240 vs 133 us at C2)
+    // hidden rows per slab pass: 64 (N = 128) or 128 (N = 256, the widest cta_group::1 UMMA, the
+    // whole 512-column TMEM double-buffered); the NP=32 variant measured slower (240 vs 133 us)
+    const int NP = n > 64 ? 128 : 64;
     const int G = ctx->sm_count;
     FastWs w;
     int st = fast_workspace(ctx, NP, d, n, v_rows, w);
@@ -2131,7 +2133,8 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;
-    st = launch_main<64, false, true>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s);
+    st = NP == 128 ? launch_main<128, false, true>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s)
+                   : launch_main<64, false, true>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s);
     if (st) return st;
     FinArgs A{};
     A.h = h;
@@ -2168,9 +2171,11 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
     if (d % 8 != 0) return fail(FRS_ENOTSUP, "FAST head: hidden_dim must be a multiple of 8 (TMA row pitch)");
     const bool batched_ok = sel_stage(ctx, d) >= 4;
-    if (!argmax && n > 16 && batched_ok) {  // batched drafting: up to 64 rows per slab pass
-        for (int r0 = 0; r0 < n; r0 += 64) {
-            const int nr = std::min(64, n - r0);
+    static const int batch_env = std::getenv("FRS_BATCH_ROWS") ? std::atoi(std::getenv("FRS_BATCH_ROWS")) : 0;
+    const int batch = batch_env == 64 ? 64 : 128;  // rows per slab pass (FRS_BATCH_ROWS=64: A/B)
+    if (!argmax && n > 16 && batched_ok) {  // batched drafting: up to `batch` rows per slab pass
+        for (int r0 = 0; r0 < n; r0 += batch) {
+            const int nr = std::min(batch, n - r0);
             const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, v_rows, ordered_ids, k, temperature,
                                            out_ridx + (size_t)r0 * k, out_full + (size_t)r0 * k,
                                            out_prob + (size_t)r0 * k, out_rowmax ? out_rowmax + r0 : nullptr,
