@@ -40,8 +40,17 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-verify", action="store_true", help="skip the vocab-parallel verify measurement")
     p.add_argument("--no-decode", action="store_true", help="skip the head-path decode loop measurement")
+    p.add_argument("--no-sweep", action="store_true", help="skip the C3 V_sub sweep")
+    p.add_argument("--no-batched", action="store_true", help="skip the C5 batched level")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
+
+
+def lib_sha256():
+    import hashlib
+    from paper_2502_14856_b200 import _lib
+    with open(_lib.LIB_PATH, "rb") as fh:
+        return hashlib.sha256(fh.read()).hexdigest()
 
 
 def peaks():
@@ -116,11 +125,13 @@ def cpu_reference_rate(slab_f32, h_rows, k, seconds, threads):
     barrier = threading.Barrier(threads + 1)
     deadline = [0.0]
 
-    def worker(i):
+    def worker(i):  # at least one whole level per thread
         barrier.wait()
-        while time.perf_counter() < deadline[0]:
+        while True:
             run(h_rows)
             counts[i] += 1
+            if time.perf_counter() >= deadline[0]:
+                break
 
     ths = [threading.Thread(target=worker, args=(i,), daemon=True) for i in range(threads)]
     for t in ths:
@@ -223,13 +234,19 @@ def main():
     clocks = sampler.summary()
     elapsed_ms = e0.elapsed_time(e1)
     launches = ctx.launch_count - launches0
-    # untimed: per-call device time of an isolated call (CUDA events on the launch stream)
-    ctx.set_timing(True)
-    for i in range(100):
+    # untimed: device time of an ISOLATED call (CUDA events on the launch stream, host sync
+    # after each: no overlap with a previous call's tail, as in a dependent draft loop)
+    iso = []
+    for i in range(200):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
         api.draft_head_topk(ctx, pool[i % len(pool)], head, k, mode=mode, out=out)
-        torch.cuda.current_stream().synchronize()
-    kern_ms, kern_n = ctx.timing_read()
-    ctx.set_timing(False)
+        a1.record()
+        a1.synchronize()
+        iso.append(a0.elapsed_time(a1) * 1000.0)
+    iso.sort()
+    iso_pct = {f"p{q}": iso[min(len(iso) - 1, int(q / 100 * len(iso)))] for q in (10, 50, 90)}
+    kern_avg_s = iso_pct["p50"] / 1e6
     # certification outcome over the whole input pool (untimed): FAST rows that fell back
     flag_counts = {"rows": 0, "recomputed": 0, "uncertified": 0, "seq_sum": 0}
     for hp in pool:
@@ -247,16 +264,21 @@ def main():
     bytes_w = 2 if args.dtype == "bf16" else 4
     alg_bytes = v_sub * d * bytes_w + n * d * 4 + n * k * 12
     hbm_peak, peak_kind = peaks()
-    kern_avg_s = (kern_ms / max(kern_n, 1)) / 1000.0
     # the dominant kernel is the fused draft-head chain (hsplit -> main -> finalize -> fallback,
     # one CUDA graph): its steady-state duration is the device time per step of the timed region
     step_s = elapsed_ms / args.steps / 1000.0
     achieved = alg_bytes / step_s / 1e9
-    traffic = None
+    # dram__bytes of the dominant kernel from an ncu capture of THIS build (tools/ncu_traffic.sh
+    # writes the summary with the library's sha256); a summary of another build is not used
+    traffic, traffic_src = None, "no ncu summary for this build (run tools/ncu_traffic.sh)"
     prof = os.path.join(ROOT, "profiles", f"ncu_{mode}_{args.dtype}_summary.json")
     if os.path.exists(prof):
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            summ = json.load(fh)
+        if summ.get("lib_sha256") == lib_sha256():
+            traffic, traffic_src = summ.get("dram_bytes_per_launch"), summ.get("source")
+        else:
+            traffic_src = "ncu summary of another build (lib sha differs): not reported"
 
     # e2e through the public host-buffer API: pinned H2D of h, K2, D2H of ids/probs, sync.
     dh = api.DeviceHead(ctx, W, subset, dtype=args.dtype)
@@ -356,6 +378,84 @@ def main():
                   "note": "transformer layers excluded (SURVEY.md §8(d)); random-init weights"}
         del E, Wb
 
+    # C3 (BASELINE configs[2]): the V_sub sweep at the Llama-3-8B shape, FAST draft level back to
+    # back; slabs below 4x L2 rotate over copies so every step streams from HBM
+    vsub_sweep = None
+    if not args.no_sweep and mode == "fast":
+        vsub_sweep = []
+        for vs in (8192, 16384, 32768, 65536, 128256):
+            sub = api.subset_from_ranking(np.random.default_rng(1234).permutation(V).astype(np.int32), vs, V,
+                                          forced=[0, 1])
+            copies = max(1, min(8, -(-4 * 126 * 2 ** 20 // (vs * d * 2))))
+            heads = [api.restrict_lm_head(ctx, W, sub, dtype="bf16") for _ in range(copies)]
+            o2 = api.draft_head_topk(ctx, pool[0], heads[0], k, mode="fast")
+            for i in range(10):
+                api.draft_head_topk(ctx, pool[i % 8], heads[i % copies], k, mode="fast", out=o2)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 200
+            s0.record()
+            for i in range(reps):
+                api.draft_head_topk(ctx, pool[i % 8], heads[i % copies], k, mode="fast", out=o2)
+            s1.record()
+            torch.cuda.synchronize()
+            us = s0.elapsed_time(s1) * 1000.0 / reps
+            b = vs * d * 2 + n * d * 4 + n * k * 12
+            vsub_sweep.append({"v_sub": vs, "us_per_step": us, "GBps": b / us / 1e3, "frac_of_peak": b / us / 1e3 / hbm_peak,
+                               "slab_copies_rotated": copies})
+            del heads, o2
+
+    # C4 per-shard view at N=1: the verify head over contiguous shards V/G of the Qwen head (what
+    # one GPU of a G-way vocab-parallel group computes before the all-gather), G = 1/2/4/8
+    verify_shards = None
+    if not args.no_verify and world == 1:
+        qd, qV, qm = 3584, 152064, 61
+        gq = torch.Generator(device=dev).manual_seed(4343)
+        Wfull = (torch.randn(qV, qd, generator=gq, device=dev) * 0.02).to(torch.bfloat16)
+        hq1 = rmsnorm_rows(torch.randn(qm, qd, generator=gq, device=dev))
+        verify_shards = []
+        for G in (1, 2, 4, 8):
+            st_, cnt_ = api.vocab_shard(qV, G, G - 1)
+            Ws = Wfull[st_:st_ + cnt_]
+            for _ in range(5):
+                api.verify_head_argmax(ctx, hq1, Ws, id_offset=st_, mode=mode)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for _ in range(50):
+                api.verify_head_argmax(ctx, hq1, Ws, id_offset=st_, mode=mode)
+            s1.record()
+            torch.cuda.synchronize()
+            us = s0.elapsed_time(s1) * 1000.0 / 50
+            b = cnt_ * qd * 2 + qm * qd * 4
+            verify_shards.append({"G": G, "shard_rows": cnt_, "us_per_call": us, "GBps": b / us / 1e3,
+                                  "frac_of_peak": b / us / 1e3 / hbm_peak})
+        del Wfull
+
+    # C5 (BASELINE configs[4]) per level: 256 streams x 10 beam rows = 2560 hidden rows in one FAST
+    # head call (slab read once per 128 rows); streams are independent units, 256/G per GPU
+    batched = None
+    if not args.no_batched and mode == "fast":
+        rows5 = 2560 // world
+        hb_ = rmsnorm_rows(torch.randn(rows5, d, generator=g, device=dev))
+        ob = api.draft_head_topk(ctx, hb_, head, k, mode="fast")
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(5):
+            api.draft_head_topk(ctx, hb_, head, k, mode="fast", out=ob)
+        s1.record()
+        torch.cuda.synchronize()
+        us = s0.elapsed_time(s1) * 1000.0 / 5
+        if world > 1:
+            t = torch.tensor([us], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            us = float(t.item())
+        fl = ob.flags.cpu().numpy()
+        batched = {"workload": "C5 draft level: 256 streams x 10 beam rows, FAST head (ids certified per row)",
+                   "rows_per_gpu": rows5, "us_per_level": us, "rows_per_s": world * rows5 / us * 1e6,
+                   "tensor_tflops": 2.0 * 2 * rows5 * v_sub * d / us / 1e6,
+                   "rows_recomputed": int(((fl & api._lib.FLAG_RECOMPUTED) != 0).sum())}
+        del hb_, ob
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         slab32 = head.slab.float().cpu().numpy()
@@ -364,6 +464,21 @@ def main():
         cpu = {"value": rate, "unit": "draft-steps/s", "cores": threads, "kind": kind,
                "sample": f"{levels} whole draft levels (n={n}, V_sub={v_sub}, d={d}, fp32 slab = the bf16 "
                          f"values widened) in {el:.1f} s across {threads} threads"}
+        # the reference is single-threaded — one pinned core, median of 5 levels
+        aff = os.sched_getaffinity(0)
+        core = min(aff)
+        try:
+            os.sched_setaffinity(0, {core})
+            one = []
+            for _ in range(5):
+                r1, _, _, _ = cpu_reference_rate(slab32, pool[0].cpu().numpy(), k, 0.0, 1)
+                one.append(r1)
+        finally:
+            os.sched_setaffinity(0, aff)
+        one.sort()
+        cpu["one_core"] = {"value": one[2], "unit": "draft-steps/s", "cores": 1, "kind": kind,
+                           "core": core, "ms_per_level_median": 1000.0 / one[2],
+                           "sample": "5 single draft levels on one pinned core (median)"}
 
     if rank == 0:
         ms_per_step = elapsed_ms / args.steps
@@ -384,13 +499,14 @@ def main():
                          "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
                          "peak_source": peak_kind, "algorithmic_bytes_per_launch": alg_bytes,
                          "chain_us_steady": step_s * 1e6, "chain_us_isolated_call": kern_avg_s * 1e6,
-                         "traffic_kernel": "k_fast_main (ncu, profiles/)"},
+                         "chain_us_isolated_pct": iso_pct, "traffic_kernel": "k_fast_main", "traffic_source": traffic_src},
             "cpu_baseline": cpu,
             "e2e": {"value": world * e2e_steps / e2e_s, "unit": "draft-steps/s",
                     "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": 3 * n * k * 4,
                     "api": "frs_head_draft_host (C ABI, pinned host buffers, synchronous)"},
             "clocks": clocks, "gpu_launches": launches, "slab_build_ms": slab_build_ms, "row_flags": flag_counts,
-            "verify_vocab_parallel": verify_vp,
+            "verify_vocab_parallel": verify_vp, "verify_shards_c4": verify_shards, "vsub_sweep_c3": vsub_sweep,
+            "batched_c5": batched,
             "decode": decode,
         }
         print(json.dumps(line), flush=True)
