@@ -796,10 +796,11 @@ __device__ __forceinline__ float hist_edge(int j) {
 // gone). fin[0..ns) are the exact logits of the candidate set S (keys sel[], canonical order),
 // nsel the untruncated |S|; a_bound bounds every approximate logit outside S, eps the FAST
 // error. Writes the row's outputs, or queues it for k_fast_fallback with the reason.
-__device__ __forceinline__ void select_certify(const FinArgs &A, int i, int ns, int nsel, int kk, float a_bound, float eps,
+__device__ __forceinline__ uint32_t select_certify(const FinArgs &A, int i, int ns, int nsel, int kk, float a_bound, float eps,
                                             bool any_bad, double tot_approx, float mmax_approx, const float *s_fin,
                                             const unsigned long long *s_sel, unsigned long long *s_sorted,
-                                            unsigned long long *s_tab, int32_t *s_spos, const int32_t *s_ord) {
+                                            unsigned long long *s_tab, int32_t *s_spos, const int32_t *s_ord,
+                                            bool enqueue = true) {
     const int lane = threadIdx.x & 31;
     const float kNegInf = -__int_as_float(0x7f800000);
     const long long c_entry_ = clock64();
@@ -830,8 +831,8 @@ __device__ __forceinline__ void select_certify(const FinArgs &A, int i, int ns, 
         const float lb = dev::key_value(best);
         if (!(a_bound + eps < lb || a_bound == kNegInf)) why |= FRS_FLAG_CERT_BOUND;
         if (why) {
-            if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
-            return;
+            if (enqueue && lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
+            return why;
         }
         if (lane == 0) {
             A.out_full[i] = A.id_offset + dev::key_index(best);
@@ -839,7 +840,7 @@ __device__ __forceinline__ void select_certify(const FinArgs &A, int i, int ns, 
             if (A.out_flags) A.out_flags[i] = static_cast<uint32_t>(min(ns, 255)) << 8;  // |S| (info)
         }
         FRS_FTRACE(A, 7);
-        return;
+        return 0u;
     }
     const unsigned long long *tab = s_tab;  // glibc exp table, staged by the caller's prologue
     const bool unit_t = A.temperature == 1.0f;  // x = l / 1 is exact: skip the IEEE divisions
@@ -927,8 +928,8 @@ __device__ __forceinline__ void select_certify(const FinArgs &A, int i, int ns, 
         }
     }
     if (why) {
-        if (lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
-        return;
+        if (enqueue && lane == 0) A.fb_rows[atomicAdd(A.fb_count, 1u)] = static_cast<uint32_t>(i) | (why << 16);
+        return why;
     }
     FRS_CPROBE(A, 4);
     if (lane < A.k) {
@@ -969,6 +970,7 @@ __device__ __forceinline__ void select_certify(const FinArgs &A, int i, int ns, 
     }
     FRS_CPROBE(A, 6);
     FRS_FTRACE(A, 7);
+    return 0u;
 }
 
 // Finalize: grid (n, kFinCtas) in clusters of kFinCtas (one cluster per hidden row). The work
@@ -1310,29 +1312,85 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     FRS_FPROBE(A, 13);
     // cluster barrier: release our DSMEM stores, acquire everyone's in the leader
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    if (b != 0) return;
+    // draft rows (fin_ctas CTAs, v_rows <= a few 10k) recompute an uncertified row inside the
+    // cluster (below), so every CTA waits for the leader's verdict; verify rows use the grid-wide
+    // k_fast_fallback queue and the non-leaders leave now
+    const bool in_cluster_fb = !A.argmax;
+    if (b != 0 && !in_cluster_fb) return;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (warp != 0) return;
-    FRS_FPROBE(A, 14);
-
-    // ---- 4. the cluster leader, warp 0: selection + certification
-    float a_bound = fmaxf(s_thw[0], s_thw[1]);  // every row not recomputed has approx <= a_bound
-    int any_bad = 0;
-    for (int w = 0; w < kFinThreads / 32; ++w) {
-        a_bound = fmaxf(a_bound, s_abw[w]);
-        any_bad |= s_badw[w];
+    __shared__ uint32_t s_why;
+    if (b == 0 && warp == 0) {
+        FRS_FPROBE(A, 14);
+        // ---- 4. the cluster leader, warp 0: selection + certification
+        float a_bound = fmaxf(s_thw[0], s_thw[1]);  // every row not recomputed has approx <= a_bound
+        int any_bad = 0;
+        for (int w = 0; w < kFinThreads / 32; ++w) {
+            a_bound = fmaxf(a_bound, s_abw[w]);
+            any_bad |= s_badw[w];
+        }
+        float mm = kNegInf;
+        double tot = 0.0;
+        if (!A.argmax) {
+            for (int w = 0; w < SW; ++w) mm = fmaxf(mm, s_pmw[w]);
+            for (int w = 0; w < SW; ++w)
+                if (s_pmw[w] != kNegInf)
+                    tot += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
+        }
+        const int ns = nsel <= kCsMax ? s_cnt : 0;  // == nsel when nothing overflowed
+        uint32_t why = 0u;
+        if (!(kDiag && A.ablate == 3))
+            why = select_certify(A, i, ns, nsel, kk, a_bound, eps, any_bad != 0, tot, mm, s_fin, s_sel, s_sorted,
+                                 s_tab, s_spos, s_ord, /*enqueue=*/!in_cluster_fb);
+        // the verdict into every CTA's own s_why (remote stores before the barrier's release: no
+        // CTA reads another's shared memory after it, so the leader may retire right away)
+        if (in_cluster_fb && lane < A.fin_ctas) {
+            uint32_t ra;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&s_why)), "r"(lane));
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(why) : "memory");
+        }
     }
-    float mm = kNegInf;
-    double tot = 0.0;
-    if (!A.argmax) {
-        for (int w = 0; w < SW; ++w) mm = fmaxf(mm, s_pmw[w]);
-        for (int w = 0; w < SW; ++w)
-            if (s_pmw[w] != kNegInf) tot += s_psw[w] * static_cast<double>(exp2f((s_pmw[w] - mm) * 1.4426950408889634f));
+    if (!in_cluster_fb) return;
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const uint32_t why = s_why;
+    if (why == 0u) return;
+    // ---- 5. (rare: ~1 row in 4000) exact recompute of row i in the cluster, bit-identical to the
+    //         EXACT path: each CTA the dot_f32 logits of its contiguous share of slab rows, then
+    //         the leader's exact softmax + top-k (the grid-wide k_fast_fallback's arithmetic)
+    float *Lr = A.scratch + (size_t)i * 2 * A.v_rows;
+    {
+        const int C = A.fin_ctas;
+        const int r0 = static_cast<int>((long long)b * A.v_rows / C), r1 = static_cast<int>((long long)(b + 1) * A.v_rows / C);
+        float *sh = wt;  // the hidden row, natural order (the staging tiles are free now)
+        for (int e = tid; e < A.d; e += kFinThreads) sh[e] = A.h[(size_t)i * A.d + e];
+        __syncthreads();
+        const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
+        for (int j = r0 + tid; j < r1; j += kFinThreads) {
+            const uint4 *w = reinterpret_cast<const uint4 *>(A.slab + (size_t)j * A.d);
+            float c[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int t = 0; t < T; ++t) {
+                const uint4 u = __ldcs(w + t);
+                const float4 h0 = sh4[2 * t], h1 = sh4[2 * t + 1];
+                const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int l = 0; l < 8; ++l) {
+                    const float wv = __uint_as_float(l & 1 ? (uw[l >> 1] & 0xffff0000u) : (uw[l >> 1] << 16));
+                    c[l] = __fadd_rn(c[l], __fmul_rn(hv[l], wv));
+                }
+            }
+            Lr[j] = __fadd_rn(__fadd_rn(__fadd_rn(c[0], c[1]), __fadd_rn(c[2], c[3])),
+                             __fadd_rn(__fadd_rn(c[4], c[5]), __fadd_rn(c[6], c[7])));  // kernels.cpp:27
+        }
     }
-    const int ns = nsel <= kCsMax ? s_cnt : 0;  // == nsel when nothing overflowed
-    if (kDiag && A.ablate == 3) return;
-    select_certify(A, i, ns, nsel, kk, a_bound, eps, any_bad != 0, tot, mm, s_fin, s_sel, s_sorted, s_tab, s_spos,
-                   s_ord);
+    __threadfence();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (b != 0) return;
+    __shared__ dev::ReduceScratch rs_fb;
+    const uint32_t f2 = dev::softmax_topk_row(Lr, A.v_rows, A.k, A.temperature, A.ordered, Lr + A.v_rows,
+                                              A.out_ridx + (size_t)i * A.k, A.out_full + (size_t)i * A.k,
+                                              A.out_prob + (size_t)i * A.k, A.out_rowmax ? A.out_rowmax + i : nullptr,
+                                              A.out_total ? A.out_total + i : nullptr, rs_fb, true);
+    if (tid == 0 && A.out_flags) A.out_flags[i] = FRS_FLAG_RECOMPUTED | why | f2;
 }
 
 // Batched drafting (n > 16 hidden rows): per hidden row one CTA over the approximate logits
@@ -2028,7 +2086,7 @@ int launch_select(frs_ctx *ctx, const FinArgs &A0, int rows, cudaStream_t s) {
 }
 
 int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
-    if (A.ablate >= 13 && A.ablate <= 15) return FRS_OK;  // DIAGNOSTIC: main kernel only (outputs not written)
+    if (kDiag && A.ablate >= 13 && A.ablate <= 15) return FRS_OK;  // DIAGNOSTIC: main kernel only (outputs not written)
     auto kern = k_fast_finalize;
     const int TP = fin_pitch(A.d / 8);
     const size_t smem = (size_t)8 * TP * 4 + (size_t)A.fin_stage * 8 * TP * 4 + 64;
@@ -2050,8 +2108,9 @@ int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     cfg.numAttrs = 2;
     FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
     ++ctx->launches;
-    if (A.ablate == 7) return FRS_OK;  // DIAGNOSTIC: no fallback kernel
-    return launch_fallback(ctx, A, s);
+    if (kDiag && A.ablate == 7) return FRS_OK;  // DIAGNOSTIC: no fallback kernel
+    // draft rows recompute in their finalize cluster; only verify rows (argmax) use the queue
+    return A.argmax ? launch_fallback(ctx, A, s) : FRS_OK;
 }
 
 int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
@@ -2162,7 +2221,7 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
     A.id_offset = id_offset;
     if (argmax) A.k = 1;
     static const int ablate = std::getenv("FRS_ABLATE") ? std::atoi(std::getenv("FRS_ABLATE")) : 0;
-    A.ablate = ablate == 11 ? ablate : 0;
+    A.ablate = kDiag && ablate == 11 ? ablate : 0;
     return launch_select(ctx, A, n, s);
 }
 
@@ -2346,7 +2405,7 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
     A.argmax = argmax ? 1 : 0;
     A.id_offset = id_offset;
     static const int ablate = std::getenv("FRS_ABLATE") ? std::atoi(std::getenv("FRS_ABLATE")) : 0;
-    A.ablate = ablate;
+    A.ablate = kDiag ? ablate : 0;
     static const int fin_env = std::getenv("FRS_FIN_CTAS") ? std::atoi(std::getenv("FRS_FIN_CTAS")) : 0;  // DIAGNOSTIC
     A.fin_ctas = argmax ? 2 : (fin_env == 2 || fin_env == 4 ? fin_env : kFinCtas);  // argmax rows: ~1-3 candidates
     A.fin_stage = argmax ? 4 : kFinStage;
