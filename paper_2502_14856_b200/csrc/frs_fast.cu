@@ -1061,9 +1061,15 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     FRS_FTRACE(A, 2);
     const long long c_fin0_ = clock64();
     if (kDiag && A.ablate == 1) return;
-    // ---- 1. keys in registers, eps, histogram; softmax / bound partials
+    // ---- 1. keys in registers, eps, histogram; softmax / bound partials. Every L2 load of the
+    //         phase (keys, row max, max |W|^2, this warp's partials) is issued before any use,
+    //         so the phase costs one round trip
     const int kk = min(A.k, A.v_rows);
     constexpr int KPT = kMaxLists * R / kFinThreads;  // union keys per thread
+    constexpr int SW = 4;                             // warps merging the softmax partials
+    constexpr int PPL = kMaxLists / (32 * SW);        // partials per lane
+    constexpr int TPL = kMaxLists / 64;               // bounds per lane (warps SW, SW + 1)
+    static_assert(TPL == 2 * PPL, "partials register tile");
     unsigned long long kr[KPT];
     const unsigned long long *src = A.P.pkey + (size_t)i * E;
 #pragma unroll
@@ -1073,6 +1079,22 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     }
     const float M = dev::from_ordered(__ldcg(A.P.rowmax_bits + i));
     const float W2 = __uint_as_float(__ldcg(A.P.w2_bits));
+    const bool soft_w = warp < SW && !A.argmax && !(kDiag && A.ablate == 5), bnd_w = warp >= SW && warp < SW + 2;
+    float pa[TPL];  // softmax warps: pm[0..PPL) | ps[0..PPL); bound warps: pth
+    if (soft_w) {
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+            const int c = warp * 32 + lane + 32 * SW * u;
+            pa[u] = c < L ? __ldcg(A.P.pm + (size_t)i * L + c) : kNegInf;
+            pa[PPL + u] = c < L ? __ldcg(A.P.ps + (size_t)i * L + c) : 0.0f;
+        }
+    } else if (bnd_w) {
+#pragma unroll
+        for (int u = 0; u < TPL; ++u) {
+            const int c = (warp - SW) * 32 + lane + 64 * u;
+            pa[u] = c < L ? __ldcg(A.P.pth + (size_t)i * L + c) : kNegInf;
+        }
+    }
     double h2 = 0.0;
 #pragma unroll
     for (int q = 0; q < kFinThreads / 32; ++q) h2 += s_hn2[q];
@@ -1101,43 +1123,27 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
         if (lane == 0) s_afar[warp] = a_far;
     }
     FRS_FPROBE(A, 9);  // filter done (thread 0's share)
-    constexpr int SW = 4;                        // warps merging the softmax partials
-    constexpr int PPL = kMaxLists / (32 * SW);   // partials per lane
-    if (warp < SW && !A.argmax && !(kDiag && (kDiag && A.ablate == 5))) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
-        float pm[PPL], ps[PPL];
-#pragma unroll
-        for (int u = 0; u < PPL; ++u) {
-            const int c = warp * 32 + lane + 32 * SW * u;
-            pm[u] = c < L ? __ldcg(A.P.pm + (size_t)i * L + c) : kNegInf;
-            ps[u] = c < L ? __ldcg(A.P.ps + (size_t)i * L + c) : 0.0f;
-        }
+    if (soft_w) {  // softmax partials: max m_c, sum s_c exp(m_c - max)
         float mm = kNegInf;
 #pragma unroll
-        for (int u = 0; u < PPL; ++u) mm = fmaxf(mm, pm[u]);
+        for (int u = 0; u < PPL; ++u) mm = fmaxf(mm, pa[u]);
         mm = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(mm)));
         float t = 0.0f;
 #pragma unroll
         for (int u = 0; u < PPL; ++u)  // approximate domain anyway: one MUFU per partial
-            if (pm[u] != kNegInf) t += ps[u] * exp2f((pm[u] - mm) * 1.4426950408889634f);
+            if (pa[u] != kNegInf) t += pa[PPL + u] * exp2f((pa[u] - mm) * 1.4426950408889634f);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (lane == 0) {
             s_pmw[warp] = mm;
             s_psw[warp] = t;
         }
-    } else if (warp >= SW && warp < SW + 2) {  // th = max list bound
-        const int wb = warp - SW;
-        constexpr int TPL = kMaxLists / 64;
-        float a[TPL], th = kNegInf;
+    } else if (bnd_w) {  // th = max list bound
+        float th = kNegInf;
 #pragma unroll
-        for (int u = 0; u < TPL; ++u) {
-            const int c = wb * 32 + lane + 64 * u;
-            a[u] = c < L ? __ldcg(A.P.pth + (size_t)i * L + c) : kNegInf;
-        }
-#pragma unroll
-        for (int u = 0; u < TPL; ++u) th = fmaxf(th, a[u]);
+        for (int u = 0; u < TPL; ++u) th = fmaxf(th, pa[u]);
         th = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(th)));
-        if (lane == 0) s_thw[wb] = th;
+        if (lane == 0) s_thw[warp - SW] = th;
     }
     __syncthreads();
     FRS_FPROBE(A, 10);
@@ -1151,7 +1157,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
             const unsigned long long mine = s_surv[tid];
             int rank = 0;
 #pragma unroll 8
-            for (int c = 0; c < kSurvMax; ++c) rank += (c < nsurv) & (s_surv[c] > mine);
+            for (int c = 0; c < nsurv; ++c) rank += s_surv[c] > mine;
             if (rank == kk - 1) s_vk = mine;
         }
         __syncthreads();
