@@ -526,6 +526,199 @@ __global__ void __launch_bounds__(256)
         if ((threadIdx.x & 7) == 0 && g < groups) logits[(size_t)i * v_rows + j] = v;
     }
 }
+// ------------------------------------------- staged exact GEMV, short row ranges (round 1 kernel)
+// Kept for matrices with fewer than 2 x SMs 32-row groups (the draft layer's 4096-row
+// projections): rows split into ceil(V / SMs)-row blocks so every SM has work (4096 x 4096 fp32
+// at n = 10: 33.5 us vs 50 us for k_exact_gemv's one 32-row group per CTA).
+// The same dot_f32 arithmetic with the operands staged in shared memory by bulk copies
+// (cp.async.bulk + mbarrier ring) instead of per-thread loads, so the stream does not depend
+// on how many warps have rows to work on: a 4096-row projection at d = 4096 gives the
+// per-thread-load kernel 1024 busy warps out of 4736 (~0.8 TB/s); here every SM streams its
+// rows through a 4-6 stage ring (~100 KB in flight per SM).
+//  * CTA = one producer warp + 2 S consumer warps (S = ceil(n / 2) slices of 2 hidden rows).
+//    A block is RB <= 32 consecutive W rows; K is cut into KC-element chunks (rows chunk W[r,
+//    c KC .. +KC) and h[i, c KC .. +KC), one bulk copy per row; row pitch KC + 8 elements so
+//    the 128-bit (fp32) / 64-bit (bf16) reads of 4 rows x 2 lanes hit distinct banks).
+//  * consumer lane = (row rl = 16 (warp & 1) + lane / 2, chain quad cq = lane & 1): it owns
+//    the dot_f32 lane chains 4 cq .. 4 cq + 3 (kernels.cpp:19-26: s_l += a*b over indices = l
+//    mod 8) of its 2 hidden rows and walks the chunks in index order, so every chain's
+//    sequence of rounded mul / add is the reference's; the final tree ((s0+s1)+(s2+s3)) +
+//    ((s4+s5)+(s6+s7)) (kernels.cpp:27) is one xor-1 shuffle. Requires d % 8 == 0 (no scalar
+//    tail) and 16-byte aligned rows.
+// Bound: FP32 issue (2 instructions per MAC) for n >= ~6 at fp32 weights; HBM below.
+namespace gv1 {
+constexpr int KC = 256;     // k elements per chunk
+constexpr int RBMAX = 32;   // W rows per block
+constexpr int NMAX = 16;    // hidden rows per launch
+constexpr int PAD = 8;      // row pitch padding (elements)
+__device__ __forceinline__ uint32_t su32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t *b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "GW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra GW_%=;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void lds4(const float *p, float (&w)[4]) {
+    const float4 v = *reinterpret_cast<const float4 *>(p);
+    w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+}
+__device__ __forceinline__ void lds4(const unsigned short *p, float (&w)[4]) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(p);  // bf16 -> fp32 is exact
+    w[0] = __uint_as_float(v.x << 16), w[1] = __uint_as_float(v.x & 0xffff0000u);
+    w[2] = __uint_as_float(v.y << 16), w[3] = __uint_as_float(v.y & 0xffff0000u);
+}
+}  // namespace gv1
+
+template <typename WT>
+__global__ void __launch_bounds__(32 + 64 * (gv1::NMAX / 2))
+    k_exact_gemv_rb(const float *__restrict__ h, int n, int d, const WT *__restrict__ W, int v_rows, int rb, int nblocks,
+                 int stages, float *__restrict__ logits, int ld) {
+    using namespace gv1;
+    extern __shared__ __align__(128) unsigned char g_smem[];
+    const int S = (n + 1) >> 1;
+    const int pitch = KC + PAD;
+    const size_t w_bytes = (size_t)RBMAX * pitch * sizeof(WT);
+    const size_t h_bytes = (size_t)(2 * S) * KC * sizeof(float);
+    const size_t st_bytes = (w_bytes + h_bytes + 127) & ~size_t(127);
+    uint64_t *full = reinterpret_cast<uint64_t *>(g_smem + st_bytes * stages);
+    uint64_t *empty = full + stages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nchunks = (d + KC - 1) / KC;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 2 * S * 32);  // every consumer lane releases its own reads
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {  // producer
+        uint64_t pol_w, pol_h;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_h));
+        int it = 0;
+        for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+            const int r0 = blk * rb, nr = min(rb, v_rows - r0);
+            for (int c = 0; c < nchunks; ++c, ++it) {
+                const int st = it % stages;
+                const uint32_t ph = (it / stages) & 1;
+                const int k0 = c * KC, kc = min(KC, d - k0);
+                bar_wait(&empty[st], ph ^ 1);
+                unsigned char *base = g_smem + st_bytes * st;
+                if (lane == 0) bar_expect(&full[st], (uint32_t)((nr * sizeof(WT) + n * sizeof(float)) * kc));
+                __syncwarp();
+                if (lane < nr)
+                    g2s(reinterpret_cast<WT *>(base) + (size_t)lane * pitch, W + (size_t)(r0 + lane) * d + k0,
+                        (uint32_t)(kc * sizeof(WT)), &full[st], pol_w);
+                if (lane < n)
+                    g2s(reinterpret_cast<float *>(base + w_bytes) + (size_t)lane * KC, h + (size_t)lane * d + k0,
+                        (uint32_t)(kc * sizeof(float)), &full[st], pol_h);
+            }
+        }
+        return;
+    }
+    const int cw = warp - 1, slice = cw >> 1;
+    const int rl = 16 * (cw & 1) + (lane >> 1), cq = lane & 1;
+    const int i0 = 2 * slice;
+    int it = 0;
+    for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+        const int r0 = blk * rb;
+        float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int c = 0; c < nchunks; ++c, ++it) {
+            const int st = it % stages;
+            const uint32_t ph = (it / stages) & 1;
+            const int kc = min(KC, d - c * KC);
+            bar_wait(&full[st], ph);
+            const unsigned char *base = g_smem + st_bytes * st;
+            const WT *wr = reinterpret_cast<const WT *>(base) + (size_t)rl * pitch + 4 * cq;
+            const float *h0 = reinterpret_cast<const float *>(base + w_bytes) + (size_t)i0 * KC + 4 * cq;
+            const float *h1 = h0 + KC;
+            const int T = kc >> 3;
+            int t = 0;
+            for (; t + 4 <= T; t += 4) {
+                float w[4][4], x[4][4], y[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    gv1::lds4(wr + (t + u) * 8, w[u]);
+                    gv1::lds4(h0 + (t + u) * 8, x[u]);
+                    gv1::lds4(h1 + (t + u) * 8, y[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        a0[j] = __fadd_rn(a0[j], __fmul_rn(x[u][j], w[u][j]));
+                        a1[j] = __fadd_rn(a1[j], __fmul_rn(y[u][j], w[u][j]));
+                    }
+            }
+            for (; t < T; ++t) {
+                float w[4], x[4], y[4];
+                gv1::lds4(wr + t * 8, w);
+                gv1::lds4(h0 + t * 8, x);
+                gv1::lds4(h1 + t * 8, y);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    a0[j] = __fadd_rn(a0[j], __fmul_rn(x[j], w[j]));
+                    a1[j] = __fadd_rn(a1[j], __fmul_rn(y[j], w[j]));
+                }
+            }
+            bar_arrive(&empty[st]);
+        }
+        // ((s0+s1)+(s2+s3)) + ((s4+s5)+(s6+s7)): cq 0 holds s0..s3, cq 1 holds s4..s7
+        float q0 = __fadd_rn(__fadd_rn(a0[0], a0[1]), __fadd_rn(a0[2], a0[3]));
+        float q1 = __fadd_rn(__fadd_rn(a1[0], a1[1]), __fadd_rn(a1[2], a1[3]));
+        const float p0 = __shfl_xor_sync(0xffffffffu, q0, 1), p1 = __shfl_xor_sync(0xffffffffu, q1, 1);
+        const int row = r0 + rl;
+        if (cq == 0 && rl < rb && row < v_rows) {
+            if (i0 < n) logits[(size_t)i0 * ld + row] = __fadd_rn(q0, p0);
+            if (i0 + 1 < n) logits[(size_t)(i0 + 1) * ld + row] = __fadd_rn(q1, p1);
+        }
+    }
+}
+
+template <typename WT>
+int launch_gemv_rb(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int v_rows, float *logits, int ld,
+                cudaStream_t s) {
+    using namespace gv1;
+    const int S = (n + 1) / 2;
+    const size_t st_bytes = (((size_t)RBMAX * (KC + PAD) * sizeof(WT) + (size_t)(2 * S) * KC * sizeof(float)) + 127) &
+                            ~size_t(127);
+    const size_t budget = std::min<size_t>(ctx->smem_optin, 220 * 1024) - 2 * 8 * 8;
+    const int stages = static_cast<int>(std::min<size_t>(8, budget / st_bytes));
+    if (stages < 2) return fail(FRS_ENOTSUP, "exact gemv: shared memory too small");
+    const int G = ctx->sm_count;
+    const int rounds = (v_rows + G * RBMAX - 1) / (G * RBMAX);
+    const int rb = (v_rows + G * rounds - 1) / (G * rounds);
+    const int nblocks = (v_rows + rb - 1) / rb;
+    const size_t smem = st_bytes * stages + 2 * stages * sizeof(uint64_t);
+    auto kern = k_exact_gemv_rb<WT>;
+    FRS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ++ctx->launches;
+    kern<<<std::min(G, nblocks), 32 + 64 * S, smem, s>>>(h, n, d, W, v_rows, rb, nblocks, stages, logits, ld);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+
 // ---------------------------------------------------------------- staged exact GEMV
 // The reference's dot_f32 (kernels.cpp:13-32) for every (hidden row, W row) pair on CUDA cores,
 // operands staged in shared memory by TMA (cp.async.bulk.tensor) through an mbarrier ring.
@@ -885,9 +1078,21 @@ int launch_exact_logits(frs_ctx *ctx, const float *h, int n, int d, const void *
     if (gemv_enabled() && d % 8 == 0 && d >= 8 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(h) & 15) == 0) {
         timing_begin(ctx, s);
-        const int st = (w_dtype == FRS_DTYPE_BF16)
-                           ? launch_gemv(ctx, h, n, d, static_cast<const unsigned short *>(W), v_rows, logits, v_rows, s)
-                           : launch_gemv(ctx, h, n, d, static_cast<const float *>(W), v_rows, logits, v_rows, s);
+        int st = FRS_OK;
+        if ((v_rows + gv::GROUP - 1) / gv::GROUP < 2 * ctx->sm_count) {  // short row ranges per SM
+            for (int r0 = 0; r0 < n && !st; r0 += gv1::NMAX) {
+                const int nb = std::min(gv1::NMAX, n - r0);
+                st = (w_dtype == FRS_DTYPE_BF16)
+                         ? launch_gemv_rb(ctx, h + (size_t)r0 * d, nb, d, static_cast<const unsigned short *>(W), v_rows,
+                                          logits + (size_t)r0 * v_rows, v_rows, s)
+                         : launch_gemv_rb(ctx, h + (size_t)r0 * d, nb, d, static_cast<const float *>(W), v_rows,
+                                          logits + (size_t)r0 * v_rows, v_rows, s);
+            }
+        } else {
+            st = (w_dtype == FRS_DTYPE_BF16)
+                     ? launch_gemv(ctx, h, n, d, static_cast<const unsigned short *>(W), v_rows, logits, v_rows, s)
+                     : launch_gemv(ctx, h, n, d, static_cast<const float *>(W), v_rows, logits, v_rows, s);
+        }
         timing_end(ctx, s);
         return st;
     }
