@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -38,194 +39,227 @@ __device__ __forceinline__ float load_w(const __nv_bfloat16 *p) {
     return __uint_as_float(static_cast<uint32_t>(u) << 16);  // bf16 -> fp32 is exact
 }
 
-// masked_attention (kernels.cpp:124-171) for one query row per CTA: scores over the allowed
-// keys = dot_f32(q, k_j) * (1 / sqrtf(dh)) (8 lane chains, reference order), e_j = expf(s_j -
-// max) (glibc port), inv = float(1 / Σ e_j) with the index-order double sum pinned as in
-// softmax_probs_row, then out[c] = Σ_j (e_j * inv) * v[j][c] accumulated in key order per
-// column (one thread per column). Rows that permit no key: FRS_FLAG_EMPTY_ROW (the reference
-// throws) and zeros.
-// Two dot_f32 products (kernels.cpp:13-32: 8 lane chains, then the reference's tree) of h with
-// rows wa and wb, the words of both rows requested 16 chain steps at a time.
-__device__ __forceinline__ float2 dot2_lanes8(const float *h, const float *wa, const float *wb, int d) {
-    const int l = threadIdx.x & 7;
-    const int T = d >> 3;
-    float sa = 0.0f, sb = 0.0f;
-    for (int t0 = 0; t0 < T; t0 += 16) {
-        float va[16], vb[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const bool in = t0 + u < T;
-            va[u] = in ? __ldg(wa + 8 * (t0 + u) + l) : 0.0f;
-            vb[u] = in ? __ldg(wb + 8 * (t0 + u) + l) : 0.0f;
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-            if (t0 + u < T) {
-                const float x = h[8 * (t0 + u) + l];
-                sa = __fadd_rn(sa, __fmul_rn(x, va[u]));
-                sb = __fadd_rn(sb, __fmul_rn(x, vb[u]));
-            }
-    }
-#pragma unroll
-    for (int o = 1; o <= 4; o <<= 1) {
-        sa = __fadd_rn(sa, __shfl_xor_sync(0xffffffffu, sa, o));
-        sb = __fadd_rn(sb, __shfl_xor_sync(0xffffffffu, sb, o));
-    }
-    if (l == 0)
-        for (int e = 8 * T; e < d; ++e) {
-            sa = __fadd_rn(sa, __fmul_rn(h[e], __ldg(wa + e)));
-            sb = __fadd_rn(sb, __fmul_rn(h[e], __ldg(wb + e)));
-        }
-    return make_float2(sa, sb);
+// masked_attention (kernels.cpp:124-171), every head of a multi-head layer in two grids, K and
+// V each read once per (head, query-row block) instead of once per (query row, head):
+//  k_attn_scores  grid (heads, key blocks of 64, query-row blocks of 32): the q tile and the k
+//                 tile in shared memory (k rows padded by 4 floats: the 16-byte reads of 8
+//                 consecutive keys hit distinct banks); one thread per (row, key) dot carries
+//                 the 8 dot_f32 lane chains (kernels.cpp:13-32: index order per chain, then
+//                 ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)), then the scalar tail), times the
+//                 reference's 1/sqrtf(dh); scores of masked pairs are never written.
+//  k_attn_pv      grid (heads, 32-column slices of the values, query-row blocks): per row (one
+//                 warp) mx over the allowed keys, e_j = expf(s_j - mx) (glibc port), the double
+//                 Σ in index order pinned by bracketing a tree sum (replayed sequentially only
+//                 when the bracket straddles a float boundary of 1/Σ), p_j = e_j * float(1/Σ);
+//                 then one thread per (row, column) adds p_j * v_jc in key order over the allowed
+//                 keys (kernels.cpp:162-167) from 64-key value chunks staged in shared memory.
+//                 Rows with no allowed key: zeros and FRS_FLAG_EMPTY_ROW (the reference throws).
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
 }
-
-constexpr int kAttnKeys = 64;  // value rows staged per chunk (one 64-bit mask word)
-constexpr int kAttnCols = 4;   // value columns per thread (dv <= 4 x 256)
+constexpr int kAttnKeyBlk = 64;   // keys per score tile (one mask word)
+constexpr int kAttnRowBlk = 32;   // query rows per score tile
+constexpr int kAttnCols = 32;     // value columns per PV CTA
 
 __global__ void __launch_bounds__(256)
-    k_masked_attention(const float *__restrict__ q, int q_ld, const float *__restrict__ k, int k_ld,
-                       const float *__restrict__ v, int v_ld, const unsigned long long *__restrict__ mask, int m,
-                       int dh, int dv, float *__restrict__ out, int out_ld, float *__restrict__ scratch,
-                       uint32_t *__restrict__ flags) {
-    // blockIdx.y = head: columns [y dh, (y + 1) dh) of q / k (y dv of v / out) — cols_slice
-    // (model.cpp:255-258); the mask is shared by the heads
-    extern __shared__ float s_q[];
-    __shared__ dev::ReduceScratch rs;
-    const int r = blockIdx.x, hd = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
+    k_attn_scores(const float *__restrict__ q, int q_ld, const float *__restrict__ k, int k_ld,
+                  const unsigned long long *__restrict__ mask, int n, int m, int dh, float scale,
+                  float *__restrict__ S) {
+    extern __shared__ float s_att[];
+    const int hd = blockIdx.x, j0 = blockIdx.y * kAttnKeyBlk, r0 = blockIdx.z * kAttnRowBlk;
+    const int nk = min(kAttnKeyBlk, m - j0), nr = min(kAttnRowBlk, n - r0);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int pitch = ((dh + 3) & ~3) + 4;  // floats; pitch % 8 == 4 for 16-byte reads of 8 rows
+    float *sq = s_att, *sk = sq + (size_t)kAttnRowBlk * pitch;
     q += (size_t)hd * dh;
     k += (size_t)hd * dh;
-    v += (size_t)hd * dv;
-    out += (size_t)hd * dv;
+    const bool vec = (dh & 3) == 0 && (q_ld & 3) == 0 && (k_ld & 3) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15) == 0;
+    if (vec) {  // every tile word requested at once (cp.async, 16 bytes)
+        const int d4 = dh >> 2;
+        for (int e = tid; e < nr * d4; e += nt) {
+            const int r = e / d4, c = (e - r * d4) * 4;
+            cp_async16(sq + r * pitch + c, q + (size_t)(r0 + r) * q_ld + c);
+        }
+        for (int e = tid; e < nk * d4; e += nt) {
+            const int j = e / d4, c = (e - j * d4) * 4;
+            cp_async16(sk + j * pitch + c, k + (size_t)(j0 + j) * k_ld + c);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    } else {
+        for (int e = tid; e < nr * dh; e += nt) {
+            const int r = e / dh, c = e - r * dh;
+            sq[r * pitch + c] = q[(size_t)(r0 + r) * q_ld + c];
+        }
+        for (int e = tid; e < nk * dh; e += nt) {
+            const int j = e / dh, c = e - j * dh;
+            sk[j * pitch + c] = k[(size_t)(j0 + j) * k_ld + c];
+        }
+    }
+    __syncthreads();
+    const int stride = (m + 63) >> 6, D8 = dh & ~7;
+    for (int p = tid; p < nr * kAttnKeyBlk; p += nt) {
+        const int r = p / kAttnKeyBlk, j = p - r * kAttnKeyBlk;  // consecutive threads: consecutive keys
+        if (j >= nk) continue;
+        const int gr = r0 + r, gj = j0 + j;
+        if (!((mask[(size_t)gr * stride + (gj >> 6)] >> (gj & 63)) & 1ull)) continue;
+        const float *qa = sq + r * pitch, *ka = sk + j * pitch;
+        float c8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int t = 0; t < D8; t += 8) {
+            const float4 x0 = *reinterpret_cast<const float4 *>(qa + t), x1 = *reinterpret_cast<const float4 *>(qa + t + 4);
+            const float4 y0 = *reinterpret_cast<const float4 *>(ka + t), y1 = *reinterpret_cast<const float4 *>(ka + t + 4);
+            c8[0] = __fadd_rn(c8[0], __fmul_rn(x0.x, y0.x));
+            c8[1] = __fadd_rn(c8[1], __fmul_rn(x0.y, y0.y));
+            c8[2] = __fadd_rn(c8[2], __fmul_rn(x0.z, y0.z));
+            c8[3] = __fadd_rn(c8[3], __fmul_rn(x0.w, y0.w));
+            c8[4] = __fadd_rn(c8[4], __fmul_rn(x1.x, y1.x));
+            c8[5] = __fadd_rn(c8[5], __fmul_rn(x1.y, y1.y));
+            c8[6] = __fadd_rn(c8[6], __fmul_rn(x1.z, y1.z));
+            c8[7] = __fadd_rn(c8[7], __fmul_rn(x1.w, y1.w));
+        }
+        float dot = __fadd_rn(__fadd_rn(__fadd_rn(c8[0], c8[1]), __fadd_rn(c8[2], c8[3])),
+                              __fadd_rn(__fadd_rn(c8[4], c8[5]), __fadd_rn(c8[6], c8[7])));
+        for (int t = D8; t < dh; ++t) dot = __fadd_rn(dot, __fmul_rn(qa[t], ka[t]));  // kernels.cpp:28-30
+        S[((size_t)hd * n + gr) * m + gj] = __fmul_rn(dot, scale);
+    }
+}
+
+__global__ void __launch_bounds__(512)
+    k_attn_pv(const float *__restrict__ S, const float *__restrict__ v, int v_ld,
+              const unsigned long long *__restrict__ mask, int n, int m, int dv, int rows_per_cta, int whole,
+              float *__restrict__ out, int out_ld, uint32_t *__restrict__ flags) {
+    extern __shared__ float s_pv[];
+    __shared__ unsigned long long s_tab[32];
+    const int hd = blockIdx.x, c0 = blockIdx.y * kAttnCols, r0 = blockIdx.z * rows_per_cta;
+    const int nr = min(rows_per_cta, n - r0), nc = min(kAttnCols, dv - c0);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
     const int stride = (m + 63) >> 6;
-    const unsigned long long *words = mask + (size_t)r * stride;
-    auto allowed = [&](int j) { return ((words[j >> 6] >> (j & 63)) & 1ull) != 0; };
-    float *S = scratch + ((size_t)hd * gridDim.x + r) * m;
-    for (int c = tid; c < dh; c += nt) s_q[c] = q[(size_t)r * q_ld + c];
-    dev::load_exp_table(rs.tab);
-    __syncthreads();
-    const float scale = __fdiv_rn(1.0f, __fsqrt_rn(static_cast<float>(dh)));
-    for (int j0 = 0; j0 < m; j0 += nt / 4) {  // 8 lanes per key, two keys per lane group at once
-        const int ja = j0 + (tid >> 3), jb = ja + nt / 8;
-        const float2 dd = dot2_lanes8(s_q, k + (size_t)min(ja, m - 1) * k_ld, k + (size_t)min(jb, m - 1) * k_ld, dh);
-        if ((tid & 7) == 0) {
-            if (ja < m && allowed(ja)) S[ja] = __fmul_rn(dd.x, scale);
-            if (jb < m && allowed(jb)) S[jb] = __fmul_rn(dd.y, scale);
+    float *P = s_pv;                                  // [rows_per_cta][m] probabilities
+    float *sv = P + (((size_t)rows_per_cta * m + 3) & ~size_t(3));  // [whole ? m : 64][kAttnCols] values (16-B aligned)
+    __shared__ uint32_t s_rowflag[16];
+    if (tid < 32) s_tab[tid] = dev::kExp2fTable[tid];
+    // the whole value slice requested before the softmax when it fits (vec_all): its loads
+    // overlap the softmax instead of one round trip per 64-key chunk
+    const bool vec_all = whole && nc == kAttnCols && (v_ld & 3) == 0 && (dv & 3) == 0 &&
+                         (reinterpret_cast<uintptr_t>(v) & 15) == 0;
+    // the rows' scores into P (masked entries are stale, never read), all requests in flight
+    for (int e = tid; e < nr * m; e += blockDim.x) {
+        const int r = e / m, j = e - r * m;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(
+                         __cvta_generic_to_shared(P + (size_t)r * m + j))),
+                     "l"(S + ((size_t)hd * n + r0 + r) * m + j)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (vec_all) {
+        const float *vb = v + (size_t)hd * dv + c0;
+        for (int e = tid; e < m * (kAttnCols / 4); e += blockDim.x) {
+            const int j = e / (kAttnCols / 4), c = (e - j * (kAttnCols / 4)) * 4;
+            cp_async16(sv + (size_t)j * kAttnCols + c, vb + (size_t)j * v_ld + c);
         }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // the scores; the values may still be in flight
     __syncthreads();
-    float mx = -__int_as_float(0x7f800000);
-    int any = 0;
-    for (int j = tid; j < m; j += nt)
-        if (allowed(j)) {
-            mx = fmaxf(mx, S[j]);
-            any = 1;
-        }
-    mx = dev::block_reduce(mx, dev::MaxF(), rs.f);
-    any = dev::block_reduce(any, dev::OrI(), rs.i);
-    if (!any) {
-        for (int c = tid; c < dv; c += nt) out[(size_t)r * out_ld + c] = 0.0f;
-        if (tid == 0) flags[r] = FRS_FLAG_EMPTY_ROW;
-        return;
-    }
-    double part = 0.0;
-    int lsb = 0x7fffffff;
-    for (int j = tid; j < m; j += nt)
-        if (allowed(j)) {
-            const float e = dev::expf_glibc(__fsub_rn(S[j], mx), rs.tab);
-            S[j] = e;
-            part += static_cast<double>(e);
-            lsb = min(lsb, dev::lsb_exponent(e));
-        }
-    double total = dev::block_reduce(part, dev::SumD(), rs.d);
-    lsb = dev::block_reduce(lsb, dev::MinI(), rs.i);
-    uint32_t fl = 0;
-    bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
-    if (!exact && total > 0.0) {
-        const double del = static_cast<double>(m + 2 * nt) * 0x1p-52;
-        const double lo = __dmul_rd(total, 1.0 - del), hi = __dmul_ru(total, 1.0 + del);
-        exact = __double2float_rn(1.0 / lo) == __double2float_rn(1.0 / hi);
-    }
-    if (!exact) {
-        fl |= FRS_FLAG_SEQ_SUM;
-        __syncthreads();
-        if (tid == 0) {
-            double acc = 0.0;
-            for (int j = 0; j < m; ++j)
-                if (allowed(j)) acc += static_cast<double>(S[j]);
-            rs.d[0] = acc;
-        }
-        __syncthreads();
-        total = rs.d[0];
-    }
-    const float inv = __double2float_rn(1.0 / total);
-    __syncthreads();
-    for (int j = tid; j < m; j += nt)
-        if (allowed(j)) S[j] = __fmul_rn(S[j], inv);
-    __syncthreads();
-    // key-ordered accumulation per column (kernels.cpp:162-167): the values arrive in chunks of
-    // kAttnKeys keys staged in shared memory by the whole CTA (coalesced rows), so the per-key
-    // dependent adds wait on shared-memory latency instead of one L2 round trip per key
-    float *s_v = s_q + ((dh + 3) & ~3), *s_p = s_v + (size_t)kAttnKeys * dv;
-    const bool vec4 = (dv & 3) == 0 && (v_ld & 3) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0;
-    float acc[kAttnCols];
-#pragma unroll
-    for (int u = 0; u < kAttnCols; ++u) acc[u] = 0.0f;
-    for (int j0 = 0; j0 < m; j0 += kAttnKeys) {
-        const int nk = min(kAttnKeys, m - j0);
-        __syncthreads();
-        if (vec4) {  // all of a thread's loads of the chunk in flight at once
-            const int dv4 = dv >> 2, n4 = nk * dv4;
-            for (int base = 0; base < n4; base += nt * 8) {
-                float4 tmp[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int idx = base + u * nt + tid;
-                    if (idx < n4) {
-                        const int jj = idx / dv4, c4 = idx - jj * dv4;
-                        tmp[u] = __ldg(reinterpret_cast<const float4 *>(v + (size_t)(j0 + jj) * v_ld) + c4);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int idx = base + u * nt + tid;
-                    if (idx < n4) reinterpret_cast<float4 *>(s_v)[idx] = tmp[u];
-                }
+    // ---- softmax per row (one warp per row)
+    for (int r = warp; r < nr; r += nw) {
+        const int gr = r0 + r;
+        const unsigned long long *words = mask + (size_t)gr * stride;
+        float *Pr = P + (size_t)r * m;
+        const float *Sr = Pr;  // the row's scores, staged above (overwritten in place below)
+        float mx = -__int_as_float(0x7f800000);
+        int any = 0;
+        for (int j = lane; j < m; j += 32)
+            if ((words[j >> 6] >> (j & 63)) & 1ull) {
+                mx = fmaxf(mx, Sr[j]);
+                any = 1;
             }
+        mx = dev::from_ordered(__reduce_max_sync(0xffffffffu, dev::ordered_bits(mx)));
+        any = __any_sync(0xffffffffu, any);
+        uint32_t fl = 0;
+        if (!any) {
+            fl = FRS_FLAG_EMPTY_ROW;
+            for (int j = lane; j < m; j += 32) Pr[j] = 0.0f;
         } else {
-            for (int idx = tid; idx < nk * dv; idx += nt) {
-                const int jj = idx / dv, c = idx - jj * dv;
-                s_v[idx] = __ldg(v + (size_t)(j0 + jj) * v_ld + c);
+            double part = 0.0;
+            int lsb = 0x7fffffff;
+            for (int j = lane; j < m; j += 32) {
+                float e = 0.0f;
+                if ((words[j >> 6] >> (j & 63)) & 1ull) {
+                    e = dev::expf_glibc(__fsub_rn(Sr[j], mx), s_tab);
+                    part += static_cast<double>(e);
+                    lsb = min(lsb, dev::lsb_exponent(e));
+                }
+                Pr[j] = e;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                part += __shfl_xor_sync(0xffffffffu, part, o);
+                lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+            }
+            double total = part;
+            // every partial sum exact (all terms multiples of 2^(ilogb(total) - 51)): the tree sum
+            // is the index-order sum; else bracket the index-order sum around it (both within
+            // (m + 64) 2^-52 of the exact sum) and pin float(1 / total) from the two ends
+            bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
+            if (!exact && total > 0.0) {
+                const double del = static_cast<double>(m + 64) * 0x1p-52;
+                const double lo = __dmul_rd(total, 1.0 - del), hi = __dmul_ru(total, 1.0 + del);
+                exact = __double2float_rn(1.0 / lo) == __double2float_rn(1.0 / hi);
+            }
+            __syncwarp();
+            if (!exact) {  // replay the reference's index order (kernels.cpp:155-159)
+                fl |= FRS_FLAG_SEQ_SUM;
+                double acc = 0.0;
+                if (lane == 0)
+                    for (int j = 0; j < m; ++j)
+                        if ((words[j >> 6] >> (j & 63)) & 1ull) acc += static_cast<double>(Pr[j]);
+                total = __shfl_sync(0xffffffffu, acc, 0);
+            }
+            const float inv = __double2float_rn(1.0 / total);
+            for (int j = lane; j < m; j += 32) Pr[j] = __fmul_rn(Pr[j], inv);  // masked e are 0: never added
+        }
+        if (lane == 0) s_rowflag[r] = fl;
+    }
+    __syncthreads();
+    // ---- key-ordered accumulation, one thread per (row, column)
+    const int rr = tid / kAttnCols, cc = tid - rr * kAttnCols;
+    float acc = 0.0f;
+    const unsigned long long *wr = mask + (size_t)(r0 + min(rr, nr - 1)) * stride;
+    if (vec_all) asm volatile("cp.async.wait_all;" ::: "memory");
+    for (int j0 = 0; j0 < m; j0 += 64) {
+        const int nk = min(64, m - j0);
+        const float *svc = vec_all ? sv + (size_t)j0 * kAttnCols : sv;
+        if (!vec_all) {
+            __syncthreads();  // the previous chunk's readers are done
+            for (int e = tid; e < nk * kAttnCols; e += blockDim.x) {
+                const int j = e / kAttnCols, c = e - j * kAttnCols;
+                sv[e] = c < nc ? __ldg(v + (size_t)(j0 + j) * v_ld + (size_t)hd * dv + c0 + c) : 0.0f;
             }
         }
-        for (int jj = tid; jj < nk; jj += nt) s_p[jj] = allowed(j0 + jj) ? S[j0 + jj] : 0.0f;  // masked: never written
         __syncthreads();
-        const unsigned long long bits = words[j0 >> 6];  // kAttnKeys == 64: one mask word
+        if (rr < nr) {
+            const unsigned long long bits = wr[j0 >> 6];
+            const float *Pr = P + (size_t)rr * m + j0;
+            int jj = 0;
+            for (; jj + 8 <= nk; jj += 8) {  // products ahead of the predicated, key-ordered adds
+                float pr[8];
 #pragma unroll
-        for (int u = 0; u < kAttnCols; ++u) {
-            const int c = tid + u * nt;
-            if (c < dv) {
-                // operands read unconditionally (shared memory), so the loads of a batch issue
-                // ahead of the key-ordered add chain; only the add is predicated on the mask
-                float a = acc[u];
-                int jj = 0;
-                for (; jj + 8 <= nk; jj += 8) {
-                    float pr[8];
+                for (int e = 0; e < 8; ++e) pr[e] = __fmul_rn(Pr[jj + e], svc[(jj + e) * kAttnCols + cc]);
+                // a masked key adds +0.0: an exact no-op (acc starts at +0 and a round-to-nearest
+                // sum is never -0 unless both addends are), and the select keeps a non-finite value
+                // of a masked key out — the same result as the reference's skip, without branches
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) pr[e] = __fmul_rn(s_p[jj + e], s_v[(jj + e) * dv + c]);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if ((bits >> (jj + e)) & 1ull) a = __fadd_rn(a, pr[e]);
-                }
-                for (; jj < nk; ++jj)
-                    if ((bits >> jj) & 1ull) a = __fadd_rn(a, __fmul_rn(s_p[jj], s_v[jj * dv + c]));
-                acc[u] = a;
+                for (int e = 0; e < 8; ++e) acc = __fadd_rn(acc, ((bits >> (jj + e)) & 1ull) ? pr[e] : 0.0f);
             }
+            for (; jj < nk; ++jj)
+                acc = __fadd_rn(acc, ((bits >> jj) & 1ull) ? __fmul_rn(Pr[jj], svc[jj * kAttnCols + cc]) : 0.0f);
         }
     }
-#pragma unroll
-    for (int u = 0; u < kAttnCols; ++u)
-        if (tid + u * nt < dv) out[(size_t)r * out_ld + tid + u * nt] = acc[u];
-    if (tid == 0) flags[r] = fl;
+    if (rr < nr && cc < nc) out[(size_t)(r0 + rr) * out_ld + (size_t)hd * dv + c0 + cc] = acc;
+    if (blockIdx.y == 0 && tid < nr && s_rowflag[tid]) atomicOr(flags + r0 + tid, s_rowflag[tid]);
 }
 
 // One CTA per row: the exact softmax probabilities (kernels.cpp:62-91) of full-vocabulary
@@ -1164,13 +1198,29 @@ int launch_masked_attention_strided(frs_ctx *ctx, const float *q, int q_ld, cons
                                     float *out, int out_ld, uint32_t *flags, cudaStream_t s) {
     int st = ctx->attn_scratch.ensure((size_t)heads * n * m * sizeof(float));
     if (st) return st;
-    if (dv > kAttnCols * 256) return fail(FRS_ENOTSUP, "masked_attention: value width above 1024");
-    const size_t smem = (size_t)(((dh + 3) & ~3) + kAttnKeys * dv + kAttnKeys) * sizeof(float);
-    if (smem > 48 * 1024)
-        FRS_CUDA_TRY(cudaFuncSetAttribute(k_masked_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ++ctx->launches;
-    k_masked_attention<<<dim3(n, heads), 256, smem, s>>>(q, q_ld, k, k_ld, v, v_ld, mask, m, dh, dv, out, out_ld,
-                                                         static_cast<float *>(ctx->attn_scratch.ptr), flags);
+    // q / k / v / out columns of head h start at h dh (h dv) within rows of stride *_ld
+    const int pitch = ((dh + 3) & ~3) + 4;
+    const size_t smem_s = (size_t)(kAttnRowBlk + kAttnKeyBlk) * pitch * sizeof(float);
+    const size_t budget = std::min<size_t>(ctx->smem_optin, 200 * 1024);
+    if (smem_s > budget) return fail(FRS_ENOTSUP, "masked_attention: head width above the shared-memory tile");
+    int rows_pv = 16;  // query rows per PV CTA (16 x 32 threads), fewer for long key ranges
+    while (rows_pv > 1 && (size_t)rows_pv * m * 4 + 64 * kAttnCols * 4 > budget) rows_pv >>= 1;
+    // the whole value slice resident (m x 32 floats) when it fits next to the rows' probabilities
+    const size_t p_bytes = (((size_t)rows_pv * m + 3) & ~size_t(3)) * 4;
+    const int whole = p_bytes + (size_t)m * kAttnCols * 4 <= budget ? 1 : 0;
+    const size_t smem_p = p_bytes + (size_t)(whole ? m : 64) * kAttnCols * 4;
+    if (smem_p > budget) return fail(FRS_ENOTSUP, "masked_attention: key range above the shared-memory row buffer");
+    const float scale = 1.0f / std::sqrt(static_cast<float>(dh));  // kernels.cpp:135 (float division of 1 by sqrtf)
+    FRS_CUDA_TRY(cudaFuncSetAttribute(k_attn_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+    FRS_CUDA_TRY(cudaFuncSetAttribute(k_attn_pv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+    FRS_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)n * sizeof(uint32_t), s));
+    float *S = static_cast<float *>(ctx->attn_scratch.ptr);
+    ctx->launches += 2;
+    k_attn_scores<<<dim3(heads, (m + kAttnKeyBlk - 1) / kAttnKeyBlk, (n + kAttnRowBlk - 1) / kAttnRowBlk), 256, smem_s,
+                    s>>>(q, q_ld, k, k_ld, mask, n, m, dh, scale, S);
+    FRS_CUDA_TRY(cudaGetLastError());
+    k_attn_pv<<<dim3(heads, (dv + kAttnCols - 1) / kAttnCols, (n + rows_pv - 1) / rows_pv), rows_pv * kAttnCols, smem_p,
+                s>>>(S, v, v_ld, mask, n, m, dv, rows_pv, whole, out, out_ld, flags);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }
