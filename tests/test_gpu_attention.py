@@ -24,7 +24,10 @@ def tree_mask(ctx_len, parents):
     return allow
 
 
-@pytest.mark.parametrize("dh,dv,ctx_len,seed", [(64, 64, 200, 1), (128, 128, 517, 2), (100, 72, 63, 3), (8, 16, 1, 4)])
+@pytest.mark.parametrize("dh,dv,ctx_len,seed", [(64, 64, 200, 1), (128, 128, 517, 2), (100, 72, 63, 3), (8, 16, 1, 4),
+                                                 (64, 1000, 300, 7),   # wide values: many 32-column slices
+                                                 (32, 48, 7000, 8),    # long key range: chunked value staging
+                                                 (130, 33, 90, 9)])    # dh % 8 != 0 (scalar tail), ragged slice
 def test_tree_attention_matches_reference(cuda_ctx, reference, dh, dv, ctx_len, seed):
     rng = np.random.default_rng(seed)
     parents = [-1, -1, 0, 0, 1, 2, 2, 5, 6, 6, 9, 3, -1, 12, 13]
