@@ -181,6 +181,7 @@ struct Partials {
     float *logits;             // LOGITS mode: approximate logits [n][ld_logits] (batched drafting)
     int late_trigger;          // DIAGNOSTIC (FRS_ABLATE=8): launch_dependents at the end, not the start
     int ablate_main;           // DIAGNOSTIC (FRS_ABLATE=14/15): skip the publish / the epilogue math
+    int range_shift;           // DIAGNOSTIC (FRS_RANGE_SHIFT): CTA c streams the row range of CTA c + shift
     int ld_logits;
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
@@ -320,8 +321,9 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     // balanced partition: this CTA owns 32-row chunks [c_begin, c_end); tile t covers chunks
     // c_begin + CPT t .. (at most CPT), so the A tile of a short tile is partly stale (ignored)
     const int NCH = (v_rows + CH - 1) / CH;
-    const int c_begin = static_cast<int>((static_cast<long long>(cta) * NCH) / G);
-    const int c_end = static_cast<int>((static_cast<long long>(cta + 1) * NCH) / G);
+    const int pcta = kDiag ? (cta + P.range_shift) % G : cta;  // DIAGNOSTIC: rotate the ranges over the CTAs
+    const int c_begin = static_cast<int>((static_cast<long long>(pcta) * NCH) / G);
+    const int c_end = static_cast<int>((static_cast<long long>(pcta + 1) * NCH) / G);
     const int t_begin = 0, t_end = (c_end - c_begin + CPT - 1) / CPT;
     auto tile_chunks = [&](int t) { return min(CPT, c_end - (c_begin + t * CPT)); };
     auto tile_row0 = [&](int t) { return (c_begin + t * CPT) * CH; };
@@ -1992,6 +1994,8 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.P.late_trigger = late;
     static const int abl = std::getenv("FRS_ABLATE") ? std::atoi(std::getenv("FRS_ABLATE")) : 0;
     w.P.ablate_main = abl == 14 || abl == 15 ? abl : 0;
+    static const int shift = std::getenv("FRS_RANGE_SHIFT") ? std::atoi(std::getenv("FRS_RANGE_SHIFT")) : 0;
+    w.P.range_shift = kDiag ? shift : 0;
     w.P.rowmax_bits = reinterpret_cast<unsigned *>(static_cast<uint8_t *>(ctx->fast_ctr.ptr) + kCtrRowmax);
     w.P.w2_bits = w.P.rowmax_bits + 64;
     return FRS_OK;

@@ -10,6 +10,7 @@ h = torch.randn(n, d, generator=g, device=dev)
 out = api.draft_head_topk(ctx, h, head, 10, mode="fast")
 G = ctx.sm_count; L = 4 * G
 runs = []
+ranges = []
 for rep in range(12):
     api.draft_head_topk(ctx, h, head, 10, mode="fast", out=out); torch.cuda.synchronize()
     pm, ps, pth = (np.empty(n * L, np.float32) for _ in range(3))
@@ -19,8 +20,12 @@ for rep in range(12):
     t0 = st[:, 0].min()
     dur = (st[:, 2] - st[:, 0]) / 1000.0   # setup -> all TMA issued
     sm = st[:, 17]
+    shift = int(os.environ.get("FRS_RANGE_SHIFT", "0"))
+    rng_idx = (np.arange(G) + shift) % G     # the row range each CTA streamed
     bysm = np.zeros(G); bysm[sm] = dur
+    byrange = np.zeros(G); byrange[rng_idx] = dur
     runs.append(bysm)
+    ranges.append(byrange)
 R = np.array(runs[2:])
 print("per-SM stream us: mean over runs min/med/max", R.mean(0).min(), np.median(R.mean(0)), R.mean(0).max())
 print("run-to-run std per SM (median)", np.median(R.std(0)))
@@ -29,3 +34,5 @@ print("corr between runs (mean off-diag)", (c.sum() - len(c)) / (len(c) ** 2 - l
 order = np.argsort(R.mean(0))
 print("slowest SMs", order[-10:], R.mean(0)[order[-10:]].round(2))
 print("fastest SMs", order[:10], R.mean(0)[order[:10]].round(2))
+
+np.save(os.environ.get("OUT", "/tmp/sm_probe") + ".npy", np.stack([np.array(runs[2:]).mean(0), np.array(ranges[2:]).mean(0)]))
