@@ -773,6 +773,10 @@ int launch_gemv_rb(frs_ctx *ctx, const float *h, int n, int d, const WT *W, int 
 //  * Warps = RW x HG, hidden groups of nrg <= NRT rows (NRT = template register tile).
 // Requires d % 8 == 0 (no scalar tail) and 16-byte aligned rows / row strides; other shapes
 // take k_exact_logits.
+#ifndef FRS_GEMV_UNROLL
+#define FRS_GEMV_UNROLL 4  // steps per unrolled loop body (1 / 2 / 4: 140 / 143 / 135 us at C2)
+#endif
+constexpr int kGemvUnroll = FRS_GEMV_UNROLL;
 namespace gv {
 constexpr int NPASS = 32;   // hidden rows per launch
 constexpr int GROUP = 32;   // W rows per TMA box (one row warp)
@@ -913,7 +917,7 @@ __global__ void __launch_bounds__(32 + 32 * gv::maxw_of(NRT, JT), 1)
             const unsigned char *wb = base + (size_t)rw * JT * P * BOX + lane * PANEL;
             const float *hb = reinterpret_cast<const float *>(base + w_bytes) + (size_t)i0 * KC;
             if (gw < g_end) {  // a second group past g_end computes on stale words, never stored
-#pragma unroll 1
+#pragma unroll kGemvUnroll
                 for (int t = 0; t < T; ++t) {
                     const int p = t / SPP, cc = t - p * SPP;
                     float w[JT][8];
