@@ -86,6 +86,10 @@ FRS_API int frs_ctx_sm_count(const frs_ctx *ctx);
  * the roofline measurement: enable, run, then read the summed milliseconds and call count. */
 FRS_API int frs_ctx_set_timing(frs_ctx *ctx, int enable);
 FRS_API int frs_ctx_timing_read(frs_ctx *ctx, double *total_ms, int *count);
+/* Latency-bound callers (a dependent draft loop): repeated FAST calls with identical buffers and
+ * shapes replay one captured CUDA graph of the chain instead of eager launches (default off:
+ * back to back, eager launches keep the PDL overlap with the previous call's tail). */
+FRS_API int frs_ctx_set_graphs(frs_ctx *ctx, int enable);
 /* Diagnostic: copy the partials of the last FAST call to host buffers: per hidden row one list
  * per (CTA, TMEM lane quarter), L = 4 G lists (G = frs_ctx_sm_count): [n][L] max / sum-exp /
  * bound, [n][L][3] candidate keys, [2 G] max |W_j|^2. With FRS_TRACE set, pkey must have room

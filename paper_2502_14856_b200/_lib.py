@@ -124,6 +124,7 @@ class AcceptanceStatsC(C.Structure):  # frs_acceptance_stats (include/frspec_cud
 
 
 SIGNATURES += [
+    ("frs_ctx_set_graphs", _I, [_P, _I]),
     ("frs_nccl_get_unique_id", _I, [_P]),
     ("frs_nccl_comm_init", _I, [_P, _I, _P, _I, C.POINTER(_P)]),
     ("frs_nccl_comm_destroy", _I, [_P]),

@@ -81,6 +81,10 @@ class Context:
         check(lib().frs_ctx_timing_read(self.handle, C.byref(ms), C.byref(cnt)), "timing_read")
         return ms.value, cnt.value
 
+    def set_graphs(self, enable: bool) -> None:
+        """Replay repeated FAST calls as one captured CUDA graph (latency-bound callers)."""
+        check(lib().frs_ctx_set_graphs(self.handle, 1 if enable else 0), "set_graphs")
+
     @property
     def launch_count(self) -> int:
         v = C.c_uint64()

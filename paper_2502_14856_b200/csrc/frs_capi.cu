@@ -126,6 +126,14 @@ int frs_ctx_set_timing(frs_ctx *ctx, int enable) {
     return FRS_OK;
 }
 
+// Latency-bound callers (a dependent draft loop): repeated FAST calls with the same buffers and
+// shapes replay a captured CUDA graph of the chain (one launch) instead of eager launches.
+int frs_ctx_set_graphs(frs_ctx *ctx, int enable) {
+    FRS_REQUIRE(ctx, "null frs_ctx");
+    ctx->prefer_graphs = enable != 0;
+    return FRS_OK;
+}
+
 int frs_ctx_timing_read(frs_ctx *ctx, double *total_ms, int *count) {
     FRS_REQUIRE(ctx && total_ms && count, "frs_ctx_timing_read: null pointer");
     double tot = 0.0;
