@@ -361,7 +361,8 @@ def main():
     # Decode tokens/s (BASELINE metric's second half): the head-path loop through
     # the public API — build_draft_tree (6 levels, width 10, 60 tokens; device-resident beam
     # bookkeeping, identity draft layer: hidden(token) = rmsnorm(E[token])) + verify_greedy_table
-    # (61 rows over the full V = 128256 bf16 head, device gather + accept), one host sync each.
+    # (61 rows over the full V = 128256 bf16 head, device gather + accept), fused as
+    # decode_step_table (one host sync per iteration; the two-call loop is reported beside it).
     # Transformer layers are out of scope (stated); random-init heads accept ~1.4 tokens/iter.
     decode = None
     if not args.no_decode:
@@ -374,10 +375,18 @@ def main():
             tree = dh.build_draft_tree(token, params, mode=mode, hidden_table=E)
             token = int(api.verify_greedy_table(ctx, E, token, Wb, tree, mode=mode).emitted[-1])
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        t0 = time.perf_counter()  # two calls per iteration: host sync between draft and verify
         for _ in range(iters):
             tree = dh.build_draft_tree(token, params, mode=mode, hidden_table=E)
             outc = api.verify_greedy_table(ctx, E, token, Wb, tree, mode=mode)
+            token = int(outc.emitted[-1])
+        two_call_s = time.perf_counter() - t0
+        for _ in range(3):
+            token = int(api.decode_step_table(dh, E, token, Wb, params, mode=mode)[1].emitted[-1])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()  # frs_decode_step_table: one sync per iteration
+        for _ in range(iters):
+            tree, outc = api.decode_step_table(dh, E, token, Wb, params, mode=mode)
             emitted += outc.accepted_length()
             token = int(outc.emitted[-1])
         dec_s = time.perf_counter() - t0
@@ -389,6 +398,8 @@ def main():
         decode = {"workload": "head-path decode loop at C2: draft tree depth 6 / width 10 / 60 tokens (FR head, "
                               "V_sub 32768) + greedy verify of 61 rows over V = 128256 (bf16), identity draft layer",
                   "tokens_per_s": rate, "ms_per_iteration": 1000.0 * dec_s / iters,
+                  "api": "decode_step_table (tree + verify, one host sync per iteration)",
+                  "ms_per_iteration_two_calls": 1000.0 * two_call_s / iters,
                   "mean_accepted_length": emitted / iters, "iterations": iters, "streams": world,
                   "note": "transformer layers excluded (SURVEY.md §8(d)); random-init weights"}
         del E, Wb

@@ -295,6 +295,17 @@ FRS_API int frs_verify_greedy_table(frs_ctx *ctx, const float *table, int64_t V_
                                     const int32_t *parents, int k, int32_t *emitted, int *n_emitted, int32_t *path,
                                     int *n_path);
 
+/* One head-path decode iteration (drafting.cpp:122-245 then verification.cpp:42-71): the greedy
+ * draft tree from the head h over hidden rows table[h->vocab x d] (device), then verify_greedy of
+ * [root_token, tree tokens...] against the full head W [V x d] (device) in verify_mode, with no
+ * host round trip between the two (one synchronisation). Results equal frs_draft_tree followed
+ * by frs_verify_greedy_table; tokens/parents/depths/log_joint hold >= total entries, emitted
+ * total + 1, path total. */
+FRS_API int frs_decode_step_table(frs_head *h, const float *table, int32_t root_token, const void *W, int V,
+                                  int w_dtype, int verify_mode, int width, int depth, int total, int32_t *tokens,
+                                  int32_t *parents, int32_t *depths, double *log_joint, int *count,
+                                  int32_t *emitted, int *n_emitted, int32_t *path, int *n_path);
+
 /* Vocab-parallel verify head (SURVEY.md §8(b) frs_allgather_merge, §8(e)): every rank of an NCCL
  * communicator holds the contiguous LM-head shard [id_offset, id_offset + v_rows) (frs_vocab_shard)
  * and calls this with the same 1 + k hidden rows h [m x d]: K3 over its shard, ncclAllGather of

@@ -113,6 +113,8 @@ SIGNATURES = [
     ("frs_verify_greedy", _I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P, C.POINTER(_I)]),
     ("frs_verify_greedy_table", _I, [_P, _P, _I64, C.c_int32, _P, _I, _I, _I, _I, _P, _P, _I, _P, C.POINTER(_I), _P,
                                      C.POINTER(_I)]),
+    ("frs_decode_step_table", _I, [_P, _P, C.c_int32, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, C.POINTER(_I),
+                                   _P, C.POINTER(_I), _P, C.POINTER(_I)]),
 ]
 
 

@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass, field
-from typing import Callable, Optional, Sequence
+from typing import Callable, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -793,6 +793,29 @@ def verify_greedy_table(ctx: Context, table: torch.Tensor, root_token: int, lm_h
                                         lm_head.shape[0], lm_head.shape[1], dt, _mode(mode), _np_ptr(tok), _np_ptr(par),
                                         k, _np_ptr(em), C.byref(ne), _np_ptr(path), C.byref(npth)), "verify_greedy")
     return VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy())
+
+
+def decode_step_table(head: "DeviceHead", table: torch.Tensor, root_token: int, lm_head: torch.Tensor,
+                      params: "DraftParams" = None, mode="exact") -> Tuple[DraftTree, VerifyOutcome]:
+    """One head-path decode iteration: build_draft_tree(root_token, hidden_table=table) then
+    verify_greedy_table(table, root_token, lm_head, tree) with no host round trip in between
+    (frs_decode_step_table). Same results as the two calls."""
+    params = params or DraftParams()
+    total = params.total_draft_tokens
+    tok, par, dep = (np.empty(max(total, 1), np.int32) for _ in range(3))
+    lj, cnt = np.empty(max(total, 1), np.float64), C.c_int()
+    em, path = np.empty(total + 1, np.int32), np.empty(max(total, 1), np.int32)
+    ne, npth = C.c_int(), C.c_int()
+    dt = DTYPE_BF16 if lm_head.dtype == torch.bfloat16 else DTYPE_F32
+    if table.shape[1] != head.d or lm_head.shape[1] != head.d or table.shape[0] < head.vocab:
+        raise ValueError("decode_step: table [>= vocab x d] and verify head [V x d] must match the draft head")
+    check(lib().frs_decode_step_table(head.handle, _ptr(table), root_token, _ptr(lm_head), lm_head.shape[0], dt,
+                                      _mode(mode), params.beam_width, params.search_depth, total, _np_ptr(tok),
+                                      _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt), _np_ptr(em),
+                                      C.byref(ne), _np_ptr(path), C.byref(npth)), "decode_step")
+    n = cnt.value
+    return (DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy()),
+            VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy()))
 
 
 class AcceptanceStats:

@@ -487,6 +487,247 @@ __global__ void __launch_bounds__(1024)
     if (threadIdx.x == 0 && out_flags) out_flags[row] = flags;
 }
 
+// Same results as k_softmax_topk with out_total == nullptr, each row split over a cluster of
+// kSmC CTAs (kSmNT threads, KL logits per thread, all loaded at once): the glibc expf work is
+// FP64-throughput bound, so one CTA per row left 138 SMs idle for the 10-row draft levels of a
+// tree (64 us per level). The row max and the (p, lsb) partials travel by DSMEM stores into
+// every CTA (each CTA folds the kSmC values in rank order, so all agree bit for bit); 1 / Σ is
+// pinned exactly as in softmax_topk_row(tree_total_ok); top-k runs as warp pops -> CTA merge
+// of the warps' sorted lists -> the leader's merge of the CTAs' lists (pushed into its shared
+// memory). The keys (prob desc, index asc) are a total order, so the union's top-k is exact.
+constexpr int kSmC = 8, kSmNT = 512, kSmNW = kSmNT / 32, kSmKMax = 16;
+
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(const void *p, uint32_t rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(a)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
+    return a;
+}
+__device__ __forceinline__ void cl_st(uint32_t a, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st(uint32_t a, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st(uint32_t a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st(uint32_t a, unsigned long long v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+template <int KL>
+__global__ void __launch_bounds__(kSmNT)
+    k_softmax_topk_cl(const float *__restrict__ logits, int ld, int v, int k, float temperature,
+                      const int32_t *__restrict__ ordered, float *__restrict__ ework, int32_t *__restrict__ out_ridx,
+                      int32_t *__restrict__ out_full, float *__restrict__ out_prob, float *__restrict__ out_rowmax,
+                      uint32_t *__restrict__ out_flags) {
+    __shared__ unsigned long long s_tab[32];
+    __shared__ float s_wmx[kSmNW], s_cmx[kSmC];
+    __shared__ int s_wi[kSmNW], s_ci[kSmC], s_cbad[kSmC];
+    __shared__ double s_wd[kSmNW], s_cd[kSmC], s_seq;
+    __shared__ unsigned long long s_wtop[kSmNW][kSmKMax], s_all[kSmC][kSmKMax];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t r = cl_rank();
+    const int row = blockIdx.x / kSmC;
+    const int chunk = ((v + kSmC - 1) / kSmC + 3) & ~3;  // host: chunk <= KL * kSmNT
+    const int lo = static_cast<int>(r) * chunk, hi = min(v, lo + chunk);
+    const float *L = logits + (size_t)row * ld;
+    float *E = ework + (size_t)row * ld;
+    const bool unit_t = temperature == 1.0f;
+    dev::load_exp_table(s_tab);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // logits from the previous kernel (PDL)
+    float x[KL];
+#pragma unroll
+    for (int q = 0; q < KL; ++q) {
+        const int j = lo + q * kSmNT + tid;
+        x[q] = j < hi ? __ldcg(L + j) : 0.0f;
+    }
+    // row max (kernels.cpp:66-75): NaN never wins under either comparison, so any order agrees
+    float mx = -__int_as_float(0x7f800000);
+    int bad = 0;
+#pragma unroll
+    for (int q = 0; q < KL; ++q) {
+        if (lo + q * kSmNT + tid < hi) {
+            if (!isfinite(x[q])) bad = 1;
+            x[q] = unit_t ? x[q] : __fdiv_rn(x[q], temperature);
+            mx = (mx < x[q]) ? x[q] : mx;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        s_wmx[warp] = mx;
+        s_wi[warp] = bad;
+    }
+    __syncthreads();
+    if (tid < kSmC) {  // push this CTA's (max, bad) into CTA tid
+        float m = s_wmx[0];
+        int b = s_wi[0];
+        for (int w = 1; w < kSmNW; ++w) {
+            m = fmaxf(m, s_wmx[w]);
+            b |= s_wi[w];
+        }
+        cl_st(cl_map(&s_cmx[r], tid), m);
+        cl_st(cl_map(&s_cbad[r], tid), b);
+    }
+    cl_sync();
+    mx = s_cmx[0];
+    bad = s_cbad[0];
+    for (int c = 1; c < kSmC; ++c) {
+        mx = fmaxf(mx, s_cmx[c]);
+        bad |= s_cbad[c];
+    }
+    uint32_t flags = bad ? FRS_FLAG_NONFINITE : 0u;
+
+    // e_j = expf(y_j - max) and the double partial sums (kernels.cpp:76-85)
+    double part = 0.0;
+    int lsb = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < KL; ++q) {
+        const int j = lo + q * kSmNT + tid;
+        if (j < hi) {
+            const float e = dev::expf_glibc(__fsub_rn(x[q], mx), s_tab);
+            x[q] = e;
+            E[j] = e;
+            part += static_cast<double>(e);
+            lsb = min(lsb, dev::lsb_exponent(e));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        part += __shfl_xor_sync(0xffffffffu, part, o);
+        lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+    }
+    if (lane == 0) {
+        s_wd[warp] = part;
+        s_wi[warp] = lsb;
+    }
+    __syncthreads();
+    if (tid < kSmC) {
+        double p = s_wd[0];
+        int l = s_wi[0];
+        for (int w = 1; w < kSmNW; ++w) {
+            p += s_wd[w];
+            l = min(l, s_wi[w]);
+        }
+        cl_st(cl_map(&s_cd[r], tid), p);
+        cl_st(cl_map(&s_ci[r], tid), l);
+    }
+    cl_sync();
+    double total = s_cd[0];
+    lsb = s_ci[0];
+    for (int c = 1; c < kSmC; ++c) {
+        total += s_cd[c];
+        lsb = min(lsb, s_ci[c]);
+    }
+    // 1 / Σ pinned as in softmax_topk_row(tree_total_ok): the same decision in every CTA
+    bool exact = total > 0.0 && lsb >= ilogb(total) - 51;
+    if (!exact && total > 0.0) {
+        const double del = static_cast<double>(v + 2 * kSmC * kSmNT) * 0x1p-52;
+        const double lo_ = __dmul_rd(total, 1.0 - del), hi_ = __dmul_ru(total, 1.0 + del);
+        exact = __double2float_rn(1.0 / lo_) == __double2float_rn(1.0 / hi_);
+    }
+    if (!exact) {  // index-order replay by the leader over the row's e_j (global, cluster-visible)
+        flags |= FRS_FLAG_SEQ_SUM;
+        if (r == 0 && tid == 0) {
+            double acc = 0.0;
+            for (int j = 0; j < v; ++j) acc += static_cast<double>(__ldcg(E + j));
+            for (int c = 0; c < kSmC; ++c) cl_st(cl_map(&s_seq, c), acc);
+        }
+        cl_sync();
+        total = s_seq;
+    }
+    const float inv = __double2float_rn(1.0 / total);
+
+    // top-kk: sorted per-thread lists -> warp pops -> CTA merge -> leader merge
+    const int kk = min(k, v);
+    unsigned long long lst[KL];
+#pragma unroll
+    for (int q = 0; q < KL; ++q) lst[q] = 0ull;
+#pragma unroll
+    for (int q = 0; q < KL; ++q) {
+        const int j = lo + q * kSmNT + tid;
+        if (j < hi) {
+            unsigned long long key = dev::prob_key(__fmul_rn(x[q], inv), j);
+#pragma unroll
+            for (int u = 0; u < KL; ++u) {
+                const unsigned long long o = lst[u];
+                const bool gt = key > o;
+                lst[u] = gt ? key : o;
+                key = gt ? o : key;
+            }
+        }
+    }
+    for (int rr = 0; rr < kk; ++rr) {
+        unsigned long long best = lst[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+            best = t > best ? t : best;
+        }
+        if (lst[0] == best) {  // the owner (keys are distinct; empty lanes shift zeros)
+#pragma unroll
+            for (int u = 0; u + 1 < KL; ++u) lst[u] = lst[u + 1];
+            lst[KL - 1] = 0ull;
+        }
+        if (lane == 0) s_wtop[warp][rr] = best;
+    }
+    __syncthreads();
+    if (warp == 0) {  // merge the kSmNW sorted warp lists; push the CTA's top-kk to the leader
+        int p = 0;
+        for (int rr = 0; rr < kk; ++rr) {
+            const unsigned long long cur = (lane < kSmNW && p < kk) ? s_wtop[lane][p] : 0ull;
+            unsigned long long best = cur;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+                best = t > best ? t : best;
+            }
+            if (lane < kSmNW && cur == best) ++p;
+            if (lane == 0) cl_st(cl_map(&s_all[r][rr], 0), best);
+        }
+    }
+    cl_sync();
+    if (r != 0 || warp != 0) return;  // no DSMEM access after this point
+    int p = 0;
+    for (int rr = 0; rr < kk; ++rr) {
+        const unsigned long long cur = (lane < kSmC && p < kk) ? s_all[lane][p] : 0ull;
+        unsigned long long best = cur;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+            best = t > best ? t : best;
+        }
+        if (lane < kSmC && cur == best) ++p;
+        if (lane == 0) {
+            const int j = dev::key_index(best);
+            out_ridx[(size_t)row * k + rr] = j;
+            out_full[(size_t)row * k + rr] = ordered ? ordered[j] : j;
+            out_prob[(size_t)row * k + rr] = __uint_as_float(static_cast<uint32_t>(best >> 32));
+        }
+    }
+    if (lane == 0) {
+        for (int rr = kk; rr < k; ++rr) {
+            out_ridx[(size_t)row * k + rr] = -1;
+            out_full[(size_t)row * k + rr] = -1;
+            out_prob[(size_t)row * k + rr] = 0.0f;
+        }
+        if (out_rowmax) out_rowmax[row] = mx;
+        if (out_flags) out_flags[row] = flags;
+    }
+}
+
 // One CTA per row: argmax with ties to the lowest index (kernels.cpp:113-122).
 __global__ void __launch_bounds__(1024)
     k_argmax_rows(const float *__restrict__ logits, int ld, int v, int32_t id_offset, int32_t *__restrict__ out_id,
@@ -1178,8 +1419,33 @@ int launch_softmax_topk(frs_ctx *ctx, const float *logits, int n, int v, int k, 
     int st = ctx->scratch.ensure((size_t)n * v * sizeof(float));
     if (st) return st;
     ++ctx->launches;
-    k_softmax_topk<<<n, 1024, 0, s>>>(logits, v, v, k, temperature, ordered_ids, static_cast<float *>(ctx->scratch.ptr),
-                                      out_ridx, out_full, out_prob, out_rowmax, out_total, out_flags);
+    float *ework = static_cast<float *>(ctx->scratch.ptr);
+    const int chunk = ((v + kSmC - 1) / kSmC + 3) & ~3;
+    static const bool one_cta = std::getenv("FRS_SOFTMAX_ONE_CTA") != nullptr;  // DIAGNOSTIC
+    if (!out_total && k <= kSmKMax && chunk <= 16 * kSmNT && !one_cta) {  // cluster path (Σ not returned)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(n * kSmC);
+        cfg.blockDim = dim3(kSmNT);
+        cfg.stream = s;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = kSmC;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        if (chunk <= 8 * kSmNT)
+            FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_softmax_topk_cl<8>, logits, v, v, k, temperature, ordered_ids,
+                                            ework, out_ridx, out_full, out_prob, out_rowmax, out_flags));
+        else
+            FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_softmax_topk_cl<16>, logits, v, v, k, temperature, ordered_ids,
+                                            ework, out_ridx, out_full, out_prob, out_rowmax, out_flags));
+        return FRS_OK;
+    }
+    k_softmax_topk<<<n, 1024, 0, s>>>(logits, v, v, k, temperature, ordered_ids, ework, out_ridx, out_full, out_prob,
+                                      out_rowmax, out_total, out_flags);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }

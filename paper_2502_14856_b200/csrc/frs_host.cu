@@ -334,6 +334,10 @@ int tree_begin(void *ws, int max_cand, cudaStream_t s);
 int tree_level(void *ws, int max_cand, const int32_t *pk, int nb, int w_children, int width, bool prune, int total,
                int32_t *next_tok, cudaStream_t s);
 int tree_select(void *ws, int max_cand, int total, int32_t **out_dev, cudaStream_t s);
+int step_rows_accept(const int32_t *tree_out, int32_t root, int total, int32_t *rt, int32_t *pp, int32_t *kdev,
+                     cudaStream_t s);  // frs_misc.cu
+int accept_greedy_devk(const int32_t *argmax_ids, const int32_t *tokens, const int32_t *parents,
+                       const int32_t *kdev, int32_t *emitted, int32_t *path, int32_t *counts, cudaStream_t s);
 }  // namespace frs
 
 static int head_staging(frs_head *h, int rows, int k) {
@@ -380,6 +384,62 @@ int frs_head_draft_host(frs_head *h, const float *h_host, int n, int k, int mode
     return FRS_OK;
 }
 
+// Device-resident tree chain (frs_tree.cu): enqueues gather -> K2 -> k_tree_level per level and
+// the selection on the context stream, nothing synchronised; *out_dev = the selected tree
+// ([0] count | [1] flags | tokens[64] | parents[64] | depths[64] | probs[64]), or nullptr when
+// the shape needs the host bookkeeping. Callers ran head_staging(h, width, w).
+static int tree_device_enqueue(frs_head *h, int32_t root_token, const float *hidden_table, int width, int depth,
+                               int total, int w, int32_t **out_dev) {
+    *out_dev = nullptr;
+    static const bool no_dev_tree = std::getenv("FRS_HOST_TREE") != nullptr;  // DIAGNOSTIC
+    if (!hidden_table || total > 64 || (size_t)w * width > 960 || no_dev_tree) return FRS_OK;
+    int max_cand = w, nb = std::min(w, width);
+    for (int level = 1; level < depth; ++level) {
+        max_cand += nb * w;
+        nb = std::min(nb * w, width);
+    }
+    if (max_cand > 2048) return FRS_OK;
+    int st;
+    cudaStream_t s = h->ctx->stream;
+    float *hd = static_cast<float *>(h->hidden.ptr);
+    int32_t *tok_dev = static_cast<int32_t *>(h->lvl_tok.ptr);
+    if ((st = h->tree_ws.ensure(frs::tree_ws_bytes(max_cand)))) return st;
+    void *ws = h->tree_ws.ptr;
+    if ((st = frs::tree_begin(ws, max_cand, s))) return st;
+    h->h_tok[0] = root_token;
+    FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, h->h_tok, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    int rows = 1;
+    int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
+    for (int level = 0; level < depth && rows > 0; ++level) {
+        if ((st = frs_gather_rows(h->ctx, hidden_table, h->vocab, h->d, tok_dev, rows, hd, s))) return st;
+        const size_t cells = (size_t)rows * w;
+        if ((st = frs_draft_head_topk(h->ctx, hd, rows, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, w, 1.0f,
+                                      FRS_MODE_EXACT, pk, pk + cells, reinterpret_cast<float *>(pk + 2 * cells),
+                                      nullptr, nullptr, nullptr, nullptr, s)))
+            return st;
+        if ((st = frs::tree_level(ws, max_cand, pk, rows, w, width, level + 1 < depth, total, tok_dev, s))) return st;
+        rows = std::min(rows * w, width);
+    }
+    return frs::tree_select(ws, max_cand, total, out_dev, s);
+}
+
+// The selected tree read back from tree_device_enqueue's output; log_joint in the reference's
+// accumulation order (parents first). Returns the node count.
+static int tree_from_out(const int32_t *ho, int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint) {
+    const int K = ho[0];
+    const int32_t *tk = ho + 2, *pa = tk + 64, *dp = pa + 64, *pr = dp + 64;
+    for (int i = 0; i < K; ++i) {
+        float p;
+        std::memcpy(&p, pr + i, 4);
+        const double lg = std::log(static_cast<double>(p));
+        tokens[i] = tk[i];
+        parents[i] = pa[i];
+        depths[i] = dp[i];
+        log_joint[i] = pa[i] < 0 ? lg : log_joint[pa[i]] + lg;
+    }
+    return K;
+}
+
 // drafting.cpp:122-245, greedy, head path: per level the provider supplies the forwarded
 // rows' hidden states, the device runs K2, the host keeps the reference's beam bookkeeping.
 int frs_draft_tree(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user, const float *hidden_table,
@@ -411,50 +471,15 @@ int frs_draft_tree(frs_head *h, int32_t root_token, frs_hidden_fn fn, void *user
     // every level runs gather -> K2 -> k_tree_level with no host round trip, then one D2H of
     // the selected nodes. An uncertified ordering decision (see frs_tree.cu) falls through to
     // the host bookkeeping below.
-    if (!fn && hidden_table && total <= 64 && (size_t)w * width <= 960) {
-        int max_cand = w, nb = std::min(w, width);
-        for (int level = 1; level < depth; ++level) {
-            max_cand += nb * w;
-            nb = std::min(nb * w, width);
-        }
-        static const bool no_dev_tree = std::getenv("FRS_HOST_TREE") != nullptr;  // DIAGNOSTIC
-        if (max_cand <= 2048 && !no_dev_tree) {
-            if ((st = h->tree_ws.ensure(frs::tree_ws_bytes(max_cand)))) return st;
-            void *ws = h->tree_ws.ptr;
-            if ((st = frs::tree_begin(ws, max_cand, s))) return st;
-            h->h_tok[0] = root_token;
-            FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, h->h_tok, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-            int rows = 1;
-            int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
-            for (int level = 0; level < depth && rows > 0; ++level) {
-                if ((st = frs_gather_rows(h->ctx, hidden_table, h->vocab, h->d, tok_dev, rows, hd, s))) return st;
-                const size_t cells = (size_t)rows * w;
-                if ((st = frs_draft_head_topk(h->ctx, hd, rows, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, w,
-                                              1.0f, mode, pk, pk + cells, reinterpret_cast<float *>(pk + 2 * cells),
-                                              nullptr, nullptr, nullptr, nullptr, s)))
-                    return st;
-                if ((st = frs::tree_level(ws, max_cand, pk, rows, w, width, level + 1 < depth, total, tok_dev, s)))
-                    return st;
-                rows = std::min(rows * w, width);
-            }
-            int32_t *out_dev = nullptr;
-            if ((st = frs::tree_select(ws, max_cand, total, &out_dev, s))) return st;
+    if (!fn) {
+        int32_t *out_dev = nullptr;
+        if ((st = tree_device_enqueue(h, root_token, hidden_table, width, depth, total, w, &out_dev))) return st;
+        if (out_dev) {
             int32_t *ho = h->h_ridx;  // pinned staging
             FRS_CUDA_TRY(cudaMemcpyAsync(ho, out_dev, sizeof(int32_t) * (2 + 4 * 64), cudaMemcpyDeviceToHost, s));
             FRS_CUDA_TRY(cudaStreamSynchronize(s));
             if (ho[1] == 0) {
-                const int K = ho[0];
-                const int32_t *tk = ho + 2, *pa = tk + 64, *dp = pa + 64, *pr = dp + 64;
-                for (int i = 0; i < K; ++i) {  // the reference's log_joint, parents first
-                    float p;
-                    std::memcpy(&p, pr + i, 4);
-                    const double lg = std::log(static_cast<double>(p));
-                    tokens[i] = tk[i];
-                    parents[i] = pa[i];
-                    depths[i] = dp[i];
-                    log_joint[i] = pa[i] < 0 ? lg : log_joint[pa[i]] + lg;
-                }
-                *count = K;
+                *count = tree_from_out(ho, tokens, parents, depths, log_joint);
                 return FRS_OK;
             }
         }
@@ -624,6 +649,71 @@ int frs_verify_greedy_table(frs_ctx *ctx, const float *table, int64_t V_table, i
         FRS_REQUIRE(tokens[i] >= 0 && tokens[i] < V_table, "verify_greedy: token outside the hidden table");
     return verify_greedy_impl(ctx, nullptr, table, V_table, root_token, W, V, d, w_dtype, mode, tokens, parents, k,
                               emitted, n_emitted, path, n_path);
+}
+
+// One head-path decode iteration with no host round trip between drafting and verification:
+// the device-resident tree (tree_device_enqueue), the verify rows built from the selected tree
+// on the device (k_step_rows: [root, tokens..., root padding to 1 + total]), the verify head
+// argmax over them, the accept walk with the device node count, then ONE synchronisation for
+// both results. Same results as frs_draft_tree + frs_verify_greedy_table: verify rows are
+// independent of each other, padding rows are never read by the walk. Shapes outside the
+// device tree, or an uncertified tree ordering, run those two calls instead.
+int frs_decode_step_table(frs_head *h, const float *table, int32_t root_token, const void *W, int V, int w_dtype,
+                          int verify_mode, int width, int depth, int total, int32_t *tokens, int32_t *parents,
+                          int32_t *depths, double *log_joint, int *count, int32_t *emitted, int *n_emitted,
+                          int32_t *path, int *n_path) {
+    FRS_REQUIRE(h && table && W && tokens && parents && depths && log_joint && count && emitted && n_emitted &&
+                    path && n_path,
+                "decode_step: null pointer");
+    if (width < 1) return fail(FRS_EINVAL, "draft params: beam_width must be >= 1");
+    if (depth < 1) return fail(FRS_EINVAL, "draft params: search_depth must be >= 1");
+    if (total < width || total > 64)
+        return fail(FRS_EINVAL, "draft params: total_draft_tokens must lie in [beam_width, 64]");
+    FRS_REQUIRE(root_token >= 0 && root_token < h->vocab, "verify_greedy: root token outside the hidden table");
+    FRS_REQUIRE(verify_mode == FRS_MODE_EXACT || verify_mode == FRS_MODE_FAST, "decode_step: unknown mode");
+    frs_ctx *ctx = h->ctx;
+    FRS_CUDA_TRY(cudaSetDevice(ctx->device));
+    const int w = std::min(width, h->v_sub), d = h->d;
+    int st = head_staging(h, width, w);
+    if (st) return st;
+    cudaStream_t s = ctx->stream;
+    int32_t *out_dev = nullptr;
+    if ((st = tree_device_enqueue(h, root_token, table, width, depth, total, w, &out_dev))) return st;
+    if (out_dev) {
+        // device: argmax ids [65] | root+tokens [65] | parents [64] | emitted [65] | path [64] | counts [2] | k
+        if ((st = ctx->obuf.ensure(sizeof(int32_t) * 337)) || (st = ctx_pinned(ctx, sizeof(int32_t) * 336)) ||
+            (st = ctx->hbuf.ensure((size_t)(1 + total) * d * sizeof(float))))
+            return st;
+        int32_t *ids = static_cast<int32_t *>(ctx->obuf.ptr);
+        int32_t *rt = ids + 65, *pp = rt + 65, *d_em = pp + 64, *d_path = d_em + 65, *d_cnt = d_path + 64;
+        int32_t *kdev = d_cnt + 2;
+        float *hv = static_cast<float *>(ctx->hbuf.ptr);
+        ++ctx->launches;
+        if ((st = frs::step_rows_accept(out_dev, root_token, total, rt, pp, kdev, s))) return st;
+        if ((st = frs_gather_rows(ctx, table, h->vocab, d, rt, 1 + total, hv, s))) return st;
+        if ((st = frs_verify_head_argmax(ctx, hv, 1 + total, d, W, V, w_dtype, 0, verify_mode, ids, nullptr, nullptr,
+                                         s)))
+            return st;
+        ++ctx->launches;
+        if ((st = frs::accept_greedy_devk(ids, rt + 1, pp, kdev, d_em, d_path, d_cnt, s))) return st;
+        int32_t *ht = h->h_ridx, *hv_out = static_cast<int32_t *>(ctx->pinned) + 129;
+        FRS_CUDA_TRY(cudaMemcpyAsync(ht, out_dev, sizeof(int32_t) * (2 + 4 * 64), cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaMemcpyAsync(hv_out, d_em, sizeof(int32_t) * (65 + 64 + 2), cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaStreamSynchronize(s));
+        if (ht[1] == 0) {
+            *count = tree_from_out(ht, tokens, parents, depths, log_joint);
+            *n_emitted = hv_out[129];
+            *n_path = hv_out[130];
+            std::copy(hv_out, hv_out + *n_emitted, emitted);
+            std::copy(hv_out + 65, hv_out + 65 + *n_path, path);
+            return FRS_OK;
+        }
+    }
+    if ((st = frs_draft_tree(h, root_token, nullptr, nullptr, table, width, depth, total, FRS_MODE_EXACT, tokens,
+                             parents, depths, log_joint, count)))
+        return st;
+    return verify_greedy_impl(ctx, nullptr, table, h->vocab, root_token, W, V, d, w_dtype, verify_mode, tokens,
+                              parents, *count, emitted, n_emitted, path, n_path);
 }
 
 int frs_rng_create(uint64_t seed, frs_rng **out) {

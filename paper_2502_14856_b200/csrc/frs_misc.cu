@@ -57,8 +57,10 @@ __global__ void __launch_bounds__(256)
 // whose token equals the target argmax is accepted, otherwise the argmax is the bonus token.
 __global__ void k_accept_greedy(const int32_t *__restrict__ argmax_ids, const int32_t *__restrict__ tokens,
                                 const int32_t *__restrict__ parents, int k, int32_t *__restrict__ emitted,
-                                int32_t *__restrict__ path, int32_t *__restrict__ counts) {
+                                int32_t *__restrict__ path, int32_t *__restrict__ counts,
+                                const int32_t *__restrict__ k_dev) {
     const int lane = threadIdx.x;
+    if (k_dev) k = *k_dev;  // node count produced on the device (fused decode step)
     int node = -1, ne = 0, np = 0;
     for (int step = 0; step <= k; ++step) {  // a path has at most k nodes
         const int32_t best = argmax_ids[node + 1];
@@ -187,7 +189,37 @@ int slab_build(frs_ctx *ctx, const float *W, long long V, int d, const int32_t *
 
 int accept_greedy(const int32_t *argmax_ids, const int32_t *tokens, const int32_t *parents, int k,
                   int32_t *emitted, int32_t *path, int32_t *counts, cudaStream_t s) {
-    k_accept_greedy<<<1, 32, 0, s>>>(argmax_ids, tokens, parents, k, emitted, path, counts);
+    k_accept_greedy<<<1, 32, 0, s>>>(argmax_ids, tokens, parents, k, emitted, path, counts, nullptr);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+// Fused decode step (frs_host.cu): the selected tree `out` ([0] count | [1] flags | tokens[64] |
+// parents[64] ...) becomes the verify rows [root, tokens..., root padding up to 1 + total] and
+// the accept walk's parents / node count, all on the device.
+__global__ void k_step_rows(const int32_t *__restrict__ out, int32_t root, int total, int32_t *__restrict__ rt,
+                            int32_t *__restrict__ pp, int32_t *__restrict__ kdev) {
+    const int i = threadIdx.x, count = out[0];
+    if (i == 0) {
+        rt[0] = root;
+        *kdev = count;
+    }
+    if (i < total) {
+        rt[1 + i] = i < count ? out[2 + i] : root;
+        pp[i] = i < count ? out[2 + 64 + i] : -1;
+    }
+}
+
+int step_rows_accept(const int32_t *tree_out, int32_t root, int total, int32_t *rt, int32_t *pp, int32_t *kdev,
+                     cudaStream_t s) {
+    k_step_rows<<<1, 64, 0, s>>>(tree_out, root, total, rt, pp, kdev);
+    FRS_CUDA_TRY(cudaGetLastError());
+    return FRS_OK;
+}
+
+int accept_greedy_devk(const int32_t *argmax_ids, const int32_t *tokens, const int32_t *parents,
+                       const int32_t *kdev, int32_t *emitted, int32_t *path, int32_t *counts, cudaStream_t s) {
+    k_accept_greedy<<<1, 32, 0, s>>>(argmax_ids, tokens, parents, 64, emitted, path, counts, kdev);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }

@@ -245,3 +245,32 @@ def test_verify_greedy_table_matches_gathered(cuda_ctx, restatement):
     ids = restatement.verify_argmax(E[rows], W)[0]
     em, path = restatement.verify_greedy_ids(ids, tree.tokens, tree.parents)
     assert np.array_equal(a.emitted, em) and np.array_equal(a.accepted_path, path)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+@pytest.mark.parametrize("width,depth,total", [(10, 6, 60), (2, 2, 10), (4, 3, 4)])
+def test_decode_step_table_matches_two_calls(cuda_ctx, restatement, mode, width, depth, total):
+    """frs_decode_step_table (tree -> verify rows -> verify head -> accept on the device, one
+    sync) == build_draft_tree + verify_greedy_table, over a chain of iterations. (2, 2, 10):
+    the tree holds 6 < total nodes, so the verify rows carry root padding the walk never reads."""
+    rng = np.random.default_rng(15)
+    V, d, v_sub = 4096, 128, 1024
+    W = (rng.standard_normal((V, d)) * 0.05).astype(np.float32)
+    W = torch.from_numpy(W).to(torch.bfloat16).to(torch.float32).numpy()
+    E = rmsnorm(rng.standard_normal((V, d)))
+    ids = rng.permutation(V)[:v_sub].astype(np.int32)
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(V, ids), dtype="f32")
+    Ed, Wb = torch.from_numpy(E).cuda(), torch.from_numpy(W).cuda().to(torch.bfloat16)
+    params = api.DraftParams(width, depth, total)
+    token = 77
+    for _ in range(4):
+        tree, out = api.decode_step_table(head, Ed, token, Wb, params, mode=mode)
+        ref_tree = head.build_draft_tree(token, params, hidden_table=Ed)
+        ref = api.verify_greedy_table(cuda_ctx, Ed, token, Wb, ref_tree, mode=mode)
+        for key in ("tokens", "parents", "depths", "log_joint"):
+            assert np.array_equal(getattr(tree, key), getattr(ref_tree, key)), key
+        assert np.array_equal(out.emitted, ref.emitted) and np.array_equal(out.accepted_path, ref.accepted_path)
+        rows = np.concatenate([[token], tree.tokens])
+        em, path = restatement.verify_greedy_ids(restatement.verify_argmax(E[rows], W)[0], tree.tokens, tree.parents)
+        assert np.array_equal(out.emitted, em) and np.array_equal(out.accepted_path, path)
+        token = int(out.emitted[-1])
