@@ -380,7 +380,10 @@ class DraftLevel:
 
 
 def draft_head_topk(ctx: Context, h: torch.Tensor, head: RestrictedHead, k: int, temperature: float = 1.0,
-                    mode="exact", want_logits: bool = False, stream=None, out: Optional[DraftLevel] = None) -> DraftLevel:
+                    mode="exact", want_logits: bool = False, stream=None, out: Optional[DraftLevel] = None,
+                    want_total: bool = True) -> DraftLevel:
+    """want_total=False: Σ is not returned (out.total None); EXACT mode then pins 1 / Σ by
+    bracketing and splits each row over a CTA cluster (the tree levels' path)."""
     if h.dtype != torch.float32 or not h.is_cuda:
         raise InvalidArgument("draft head: h must be a CUDA float32 tensor")
     h = h.contiguous()
@@ -393,7 +396,8 @@ def draft_head_topk(ctx: Context, h: torch.Tensor, head: RestrictedHead, k: int,
     if out is None:
         out = DraftLevel(torch.empty((n, k), dtype=torch.int32, device=dev), torch.empty((n, k), dtype=torch.int32, device=dev),
                          torch.empty((n, k), dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.float32, device=dev),
-                         torch.empty(n, dtype=torch.float64, device=dev), torch.zeros(n, dtype=torch.int32, device=dev),
+                         torch.empty(n, dtype=torch.float64, device=dev) if want_total else None,
+                         torch.zeros(n, dtype=torch.int32, device=dev),
                          torch.empty((n, head.v_sub), dtype=torch.float32, device=dev) if want_logits else None)
     check(lib().frs_draft_head_topk(ctx.handle, _ptr(h), n, d, _ptr(head.slab), head.v_sub, head.dtype,
                                     _ptr(head.ordered_dev), k, temperature, _mode(mode), _ptr(out.ridx), _ptr(out.full),

@@ -1267,6 +1267,12 @@ GemvCfg gemv_cfg(int n, int d, int v_rows, int G, bool bf16) {
                 const int warps = rw * hg;
                 if (warps > gv::maxw_of(nrt, jt)) continue;
                 if (rw > 1 && (rw - 1) * jt >= gpc) continue;  // a whole row warp idle
+                {  // two ring stages must fit (launch_gemv_t's budget): wide row groups with few
+                   // hidden rows (short d, small n) would otherwise pick an unlaunchable ring
+                    const size_t kc = bf16 ? 128 : 64;
+                    const size_t stb = ((size_t)rw * jt * 2 * gv::BOX + (size_t)hg * nrt * kc * 4 + 1023) & ~size_t(1023);
+                    if (2 * stb > (size_t)227 * 1024 - 1024 - 2 * 8 * 8) continue;  // sm_100 opt-in limit
+                }
                 const int gb = rw * jt, nblk = (gpc + gb - 1) / gb;
                 const double per_step = 16.0 * nrt * jt + jt * (bf16 ? 9 : 2) + 2.0 * nrt + 4;  // instructions
                 const double wavefronts = jt * (bf16 ? 4.0 : 8.0) + 4.0 * nrt;  // h: 2 broadcast LDS.128 per row

@@ -274,3 +274,43 @@ def test_decode_step_table_matches_two_calls(cuda_ctx, restatement, mode, width,
         em, path = restatement.verify_greedy_ids(restatement.verify_argmax(E[rows], W)[0], tree.tokens, tree.parents)
         assert np.array_equal(out.emitted, em) and np.array_equal(out.accepted_path, path)
         token = int(out.emitted[-1])
+
+
+@pytest.mark.parametrize("v_sub,k,temperature", [(5, 10, 1.0), (100, 16, 1.0), (1000, 3, 0.7), (32768, 10, 1.0),
+                                                 (40000, 16, 1.0), (65536, 1, 1.3), (2000, 17, 1.0)])
+def test_draft_level_without_total_matches_oracle(cuda_ctx, restatement, v_sub, k, temperature):
+    """want_total=False: the cluster softmax + top-k (8 CTAs per row, k <= 16, v_sub <= 65536;
+    k = 17 takes the one-CTA kernel) gives the reference's ids, probabilities, row max."""
+    W, ids, h = make_case(16, 3, 128, v_sub, V=v_sub + 7, bf16=True)
+    h[2] = h[2] * 40.0  # a peaked row: tiny tail probabilities, many e_j = 0 or subnormal
+    Wd = torch.from_numpy(W).cuda()
+    head = api.restrict_lm_head(cuda_ctx, Wd, api.RankedSubset(W.shape[0], ids), dtype="bf16")
+    out = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, k, temperature, mode="exact",
+                              want_total=False)
+    torch.cuda.synchronize()
+    assert out.total is None
+    ref = restatement.draft_level(h, restatement.restrict(W, ids), ids, k, temperature)
+    kk = min(k, v_sub)
+    assert np.array_equal(out.ridx.cpu().numpy()[:, :kk], ref["ridx"][:, :kk])
+    assert np.array_equal(out.full.cpu().numpy()[:, :kk], ref["full"][:, :kk])
+    assert np.array_equal(out.prob.cpu().numpy()[:, :kk], ref["prob"][:, :kk])
+    assert np.array_equal(out.rowmax.cpu().numpy(), ref["mx"])
+    if k > v_sub:  # entries past V_sub: -1 / -1 / 0
+        assert (out.ridx.cpu().numpy()[:, kk:] == -1).all() and (out.prob.cpu().numpy()[:, kk:] == 0).all()
+
+
+def test_draft_level_without_total_exact_sum_and_nonfinite(cuda_ctx, restatement):
+    """Constant logits (every e_j = 1: the lsb test proves the tree sum exact) and a non-finite
+    row through the cluster path."""
+    v_sub, d = 3000, 64
+    W = np.zeros((v_sub, d), np.float32)
+    ids = np.arange(v_sub, dtype=np.int32)
+    h = rmsnorm(np.random.default_rng(17).standard_normal((2, d)))
+    head = api.restrict_lm_head(cuda_ctx, torch.from_numpy(W).cuda(), api.RankedSubset(v_sub, ids), dtype="f32")
+    out = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, 12, mode="exact", want_total=False)
+    ref = restatement.draft_level(h, W, ids, 12)
+    assert np.array_equal(out.ridx.cpu().numpy(), ref["ridx"]) and np.array_equal(out.prob.cpu().numpy(), ref["prob"])
+    h[1, 5] = np.nan
+    out = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, 12, mode="exact", want_total=False)
+    flags = out.flags.cpu().numpy()
+    assert flags[1] & FLAG_NONFINITE and not flags[0] & FLAG_NONFINITE
