@@ -300,14 +300,15 @@ def main():
     pinned = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
     pinned.copy_(pool[0].cpu())
     h_host = pinned.numpy()
+    host_out = (np.empty((n, k), np.int32), np.empty((n, k), np.int32), np.empty((n, k), np.float32))
     for _ in range(3):
-        dh.draft_host(h_host, k, mode=mode)
+        dh.draft_host(h_host, k, mode=mode, out=host_out)
     e2e_steps = max(20, min(args.steps, 500))
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        dh.draft_host(h_host, k, mode=mode)
+        dh.draft_host(h_host, k, mode=mode, out=host_out)
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
@@ -530,7 +531,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": world * e2e_steps / e2e_s, "unit": "draft-steps/s",
                     "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": 3 * n * k * 4,
-                    "api": "frs_head_draft_host (C ABI, pinned host buffers, synchronous)"},
+                    "api": "DeviceHead.draft_host -> frs_head_draft_host (C ABI, synchronous): pinned host "
+                           "rows read by the device over the bus, ids/probs written to pinned staging"},
             "clocks": clocks, "gpu_launches": launches, "slab_build_ms": slab_build_ms, "row_flags": flag_counts,
             "verify_vocab_parallel": verify_vp, "verify_shards_c4": verify_shards, "vsub_sweep_c3": vsub_sweep,
             "batched_c5": batched,

@@ -584,13 +584,24 @@ class DeviceHead:
         except Exception:
             pass
 
-    def draft_host(self, h: np.ndarray, k: int, mode="exact"):
-        """One level with HOST buffers (H2D, K2, D2H, sync): the e2e call."""
-        h = np.ascontiguousarray(h, np.float32)
+    def draft_host(self, h: np.ndarray, k: int, mode="exact", out=None):
+        """One level with HOST buffers (the e2e call): h [n x d] float32; returns (ridx, full,
+        prob) [n x k], written into `out` when given (three C-contiguous arrays, int32 / int32 /
+        float32). Pinned h (e.g. a pin_memory tensor's .numpy()) in FAST mode with n <= 16 is
+        read by the device directly, with no copy operation."""
+        if not (h.dtype == np.float32 and h.flags.c_contiguous):
+            h = np.ascontiguousarray(h, np.float32)
         n = h.shape[0]
-        ridx, full, prob = np.empty((n, k), np.int32), np.empty((n, k), np.int32), np.empty((n, k), np.float32)
-        check(lib().frs_head_draft_host(self.handle, _np_ptr(h), n, k, _mode(mode), _np_ptr(ridx), _np_ptr(full),
-                                        _np_ptr(prob)), "draft_host")
+        if out is None:
+            out = (np.empty((n, k), np.int32), np.empty((n, k), np.int32), np.empty((n, k), np.float32))
+        ridx, full, prob = out
+        if not all(a.flags.c_contiguous and a.size >= n * k for a in out) or ridx.dtype != np.int32 \
+                or full.dtype != np.int32 or prob.dtype != np.float32:
+            raise InvalidArgument("draft_host: out must be three C-contiguous [n x k] int32/int32/float32 arrays")
+        st = lib().frs_head_draft_host(self.handle, h.ctypes.data, n, k, _mode(mode), ridx.ctypes.data,
+                                       full.ctypes.data, prob.ctypes.data)
+        if st:
+            check(st, "draft_host")
         return ridx, full, prob
 
     def build_draft_tree(self, root_token: int, params: DraftParams = DraftParams(), mode="exact",

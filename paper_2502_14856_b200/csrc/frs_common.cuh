@@ -34,7 +34,7 @@ struct DevBuf {
 
 // CUDA-graph cache of repeated FAST calls (frs_fast.cu): the key is every pointer, size and
 // parameter the captured chain bakes in.
-constexpr int kGraphKeyWords = 19;
+constexpr int kGraphKeyWords = 20;
 struct GraphKey {
     uint64_t w[kGraphKeyWords];
     bool operator==(const GraphKey &o) const {
@@ -79,6 +79,9 @@ struct frs_ctx {
     uint64_t graph_clock = 0;
     cudaStream_t cap_stream = nullptr;    // private stream for graph capture
     bool prefer_graphs = false;           // set by host loops that wait on every call (frs_draft_tree)
+    const float *h_stage_src = nullptr;   // set by frs_head_draft_host around one FAST call: k_hsplit
+                                          // reads the hidden rows from this mapped pinned host
+                                          // pointer and writes them to the call's h (device)
 };
 
 namespace frs {

@@ -202,9 +202,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // p / (NP/2)), so the two epilogue warps of a TMEM lane quarter share the valid rows evenly.
 // 128 threads, no shared memory: it co-resides with the main kernel's CTAs, which PDL lets
 // launch (and run their prologue and first slab loads) while this grid is still running.
+// h_copy != nullptr: h is a mapped pinned HOST pointer (the host-buffer entry point reads the
+// rows over the bus here instead of a separate copy) and the fp32 rows are also written to
+// h_copy, the device copy the finalize's exact dots read.
 __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int n, int d, int NP,
                                                 __nv_bfloat16 *__restrict__ hs, unsigned *__restrict__ rowmax_bits,
-                                                unsigned *__restrict__ w2_bits, unsigned long long *xtrace) {
+                                                unsigned *__restrict__ w2_bits, unsigned long long *xtrace,
+                                                float *__restrict__ h_copy) {
     // launched programmatically after whatever precedes it on the stream: wait for it (h is
     // final, the previous call's fallback queue is drained), then let the main kernel launch
     griddep_wait();
@@ -218,8 +222,15 @@ __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total4; idx += gridDim.x * blockDim.x) {
         const int e = idx * 4, p = e / d, c = e - p * d;
         const int i = 2 * (p % (NP / 2)) + p / (NP / 2);  // hs row p holds hidden row i (see k_fast_main)
-        const float4 x = i < n ? __ldg(reinterpret_cast<const float4 *>(h + (size_t)i * d + c))
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < n) {
+            if (h_copy) {
+                x = *reinterpret_cast<const float4 *>(h + (size_t)i * d + c);
+                *reinterpret_cast<float4 *>(h_copy + (size_t)i * d + c) = x;
+            } else {
+                x = __ldg(reinterpret_cast<const float4 *>(h + (size_t)i * d + c));
+            }
+        }
         const __nv_bfloat162 h01 = __floats2bfloat162_rn(x.x, x.y), h23 = __floats2bfloat162_rn(x.z, x.w);
         const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
         const __nv_bfloat162 l01 = __floats2bfloat162_rn(x.x - f01.x, x.y - f01.y);
@@ -2198,7 +2209,7 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
         cfg.numAttrs = 1;
         if ((st = configure(k_hsplit, 0))) return st;
         FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, w.P.rowmax_bits, w.P.w2_bits,
-                                        static_cast<unsigned long long *>(nullptr)));
+                                        static_cast<unsigned long long *>(nullptr), static_cast<float *>(nullptr)));
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;
@@ -2301,7 +2312,8 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
                                  reinterpret_cast<uint64_t>(out_prob), reinterpret_cast<uint64_t>(out_rowmax),
                                  reinterpret_cast<uint64_t>(out_total), reinterpret_cast<uint64_t>(out_flags),
                                  reinterpret_cast<uint64_t>(ctx->fast_ws.ptr), reinterpret_cast<uint64_t>(ctx->fast_ctr.ptr),
-                                 reinterpret_cast<uint64_t>(ctx->trace.ptr)};
+                                 reinterpret_cast<uint64_t>(ctx->trace.ptr),
+                                 reinterpret_cast<uint64_t>(ctx->h_stage_src)};
         static_assert(sizeof(vals) / sizeof(vals[0]) == kGraphKeyWords, "graph key size");
         for (int q = 0; q < kGraphKeyWords; ++q) key.w[q] = vals[q];
         GraphEntry *e = graph_lookup(ctx, key);
@@ -2378,7 +2390,9 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
         if ((st = configure(k_hsplit, 0))) return st;
         static const bool skip_hs = std::getenv("FRS_ABLATE") && std::atoi(std::getenv("FRS_ABLATE")) == 10;
         if (!skip_hs)  // DIAGNOSTIC (FRS_ABLATE=10): measure the chain without the split kernel
-            FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, w.P.rowmax_bits, w.P.w2_bits, xtrace));
+            FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, ctx->h_stage_src ? ctx->h_stage_src : h, n, d, NP, w.hs,
+                                            w.P.rowmax_bits, w.P.w2_bits, xtrace,
+                                            ctx->h_stage_src ? const_cast<float *>(h) : nullptr));
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;

@@ -366,18 +366,41 @@ int frs_head_draft_host(frs_head *h, const float *h_host, int n, int k, int mode
     if (st) return st;
     cudaStream_t s = h->ctx->stream;
     float *hd = static_cast<float *>(h->hidden.ptr);
-    FRS_CUDA_TRY(cudaMemcpyAsync(hd, h_host, sizeof(float) * (size_t)n * h->d, cudaMemcpyHostToDevice, s));
-    // outputs packed [ridx | full | prob] on the device: ONE D2H into pinned staging (the
-    // caller's arrays may be pageable, where each async copy degrades to a staged sync copy)
     const size_t cells = (size_t)n * k;
-    int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
-    st = frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode, pk,
-                             pk + cells, reinterpret_cast<float *>(pk + 2 * cells), nullptr, nullptr, nullptr, nullptr,
-                             s);
-    if (st) return st;
-    FRS_CUDA_TRY(cudaMemcpyAsync(h->h_ridx, pk, cells * 12, cudaMemcpyDeviceToHost, s));
+    // FAST, one 16-row chain, pinned caller rows: no copy operations at all — k_hsplit reads the
+    // rows over the bus from the mapped pinned buffer (writing the device copy the finalize
+    // reads) and the finalize writes ids / probabilities straight into the pinned staging.
+    // Otherwise: one H2D of the rows, outputs packed [ridx | full | prob] on the device, ONE D2H
+    // (the caller's arrays may be pageable, where each async copy degrades to a staged sync copy).
+    cudaPointerAttributes pa{};
+    static const bool no_zero_copy = std::getenv("FRS_NO_ZERO_COPY") != nullptr;  // A/B switches
+    static const bool no_graphs = std::getenv("FRS_NO_HOST_GRAPHS") != nullptr;
+    const bool mapped = !no_zero_copy && mode == FRS_MODE_FAST && n <= 16 && h->dtype == FRS_DTYPE_BF16 &&
+                        cudaPointerGetAttributes(&pa, h_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                        pa.devicePointer != nullptr;
+    cudaGetLastError();  // cudaPointerGetAttributes leaves no sticky error; clear any non-sticky one
+    int32_t *hp = static_cast<int32_t *>(h->h_ridx);
+    if (mapped) {
+        // a synchronous call is latency-bound: replay the chain from a graph keyed on the buffers
+        const bool graphs = h->ctx->prefer_graphs;
+        h->ctx->h_stage_src = static_cast<const float *>(pa.devicePointer);
+        h->ctx->prefer_graphs = !no_graphs;
+        st = frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode, hp,
+                                 hp + cells, reinterpret_cast<float *>(hp + 2 * cells), nullptr, nullptr, nullptr,
+                                 nullptr, s);
+        h->ctx->h_stage_src = nullptr;
+        h->ctx->prefer_graphs = graphs;
+        if (st) return st;
+    } else {
+        FRS_CUDA_TRY(cudaMemcpyAsync(hd, h_host, sizeof(float) * (size_t)n * h->d, cudaMemcpyHostToDevice, s));
+        int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
+        st = frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode, pk,
+                                 pk + cells, reinterpret_cast<float *>(pk + 2 * cells), nullptr, nullptr, nullptr,
+                                 nullptr, s);
+        if (st) return st;
+        FRS_CUDA_TRY(cudaMemcpyAsync(hp, pk, cells * 12, cudaMemcpyDeviceToHost, s));
+    }
     FRS_CUDA_TRY(cudaStreamSynchronize(s));
-    const int32_t *hp = static_cast<const int32_t *>(h->h_ridx);
     std::memcpy(ridx, hp, cells * 4);
     std::memcpy(full, hp + cells, cells * 4);
     std::memcpy(prob, hp + 2 * cells, cells * 4);

@@ -249,3 +249,27 @@ def test_fast_verify_many_rows_batched(cuda_ctx, restatement):
     rid, rval = restatement.verify_argmax(h, W.float().numpy())
     assert np.array_equal(ids.cpu().numpy(), rid + 11)
     assert np.array_equal(vals.cpu().numpy(), rval)
+
+
+@pytest.mark.parametrize("n,pinned", [(10, True), (16, True), (1, True), (10, False), (20, True)])
+def test_fast_draft_host_buffers(cuda_ctx, restatement, n, pinned):
+    """frs_head_draft_host in FAST mode: pinned rows (n <= 16) are read by k_hsplit over the bus
+    and the ids / probabilities land in pinned staging with no copy operations; pageable rows
+    and n > 16 take the H2D / D2H path. Same outputs as the device-buffer call and the oracle."""
+    W, ids, h = case(31, n, 1024, 8192)
+    dh = api.DeviceHead(cuda_ctx, W, api.RankedSubset(W.shape[0], ids), dtype="bf16")
+    if pinned:
+        t = torch.empty((n, W.shape[1]), dtype=torch.float32, pin_memory=True)
+        t.copy_(torch.from_numpy(h))
+        h_host = t.numpy()
+    else:
+        h_host = h.copy()
+    for _ in range(2):  # repeated calls reuse the staging buffers
+        ridx, full, prob = dh.draft_host(h_host, 10, mode="fast")
+    head = api.restrict_lm_head(cuda_ctx, torch.from_numpy(W).cuda(), api.RankedSubset(W.shape[0], ids), dtype="bf16")
+    out = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, 10, mode="fast")
+    assert np.array_equal(ridx, out.ridx.cpu().numpy()) and np.array_equal(full, out.full.cpu().numpy())
+    assert np.array_equal(prob, out.prob.cpu().numpy())
+    ref = restatement.draft_level(h, restatement.restrict(W, ids), ids, 10)
+    assert np.array_equal(ridx, ref["ridx"]) and np.array_equal(full, ref["full"])
+    np.testing.assert_allclose(prob, ref["prob"], rtol=PROB_RTOL, atol=0)
