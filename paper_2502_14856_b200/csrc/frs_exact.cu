@@ -283,64 +283,74 @@ __global__ void __launch_bounds__(1024)
 // P_i + eb > u_lo equals the first with P_i - eb > u_hi (u's own bracket from T +- eb). An
 // uncertain draw (or the reference's upper-edge guard) stops the row with
 // FRS_FLAG_SAMPLE_UNCERTIFIED: the host replays that level from the probabilities.
-__global__ void __launch_bounds__(1024)
-    k_softmax_sample(const float *__restrict__ logits, int v, float temperature, const double *__restrict__ uniforms,
-                     int w, const int32_t *__restrict__ ordered, float *__restrict__ probs, float *__restrict__ work,
-                     int32_t *__restrict__ out_ridx, int32_t *__restrict__ out_full, float *__restrict__ out_prob,
-                     int32_t *__restrict__ out_count, uint32_t *__restrict__ out_flags) {
-    __shared__ dev::ReduceScratch rs;
-    __shared__ double s_cp[1024];
-    const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-    const float *L = logits + (size_t)row * v;
-    float *P = probs + (size_t)row * v, *Wk = work + (size_t)row * v;
-    uint32_t flags = dev::softmax_probs_row(L, v, temperature, P, rs);
-    __shared__ int s_pick, s_stop;
-    const int C = (v + 1023) / 1024, j0 = min(v, tid * C), j1 = min(v, j0 + C);
-    for (int j = j0; j < j1; ++j) Wk[j] = P[j];
-    // Prefix bookkeeping: a fresh scan (chunk sums + block scan) is within errP = 2^-46 T of the
-    // exact prefix; each later pick is subtracted in place (one rounding each, errP grows by
-    // 2^-52 T). The reference's running sums are within (v + 64) 2^-53 T of the exact ones.
-    // Rescan when the remaining mass halves, so the bounds stay relative to it.
+// The w certified draws of one row (drafting.cpp:44-74) by a block of NT threads over the
+// draw weights Wk[0..v) (= the row's probabilities; drawn entries are zeroed), uniforms in
+// s_uni (first 64) / uniforms. Returns the flags to OR in and the number of draws made.
+template <int NT>
+__device__ uint32_t sample_draws(float *Wk, int v, int w, int row, const double *s_uni,
+                                 const double *__restrict__ uniforms, const int32_t *__restrict__ ordered,
+                                 int32_t *__restrict__ out_ridx, int32_t *__restrict__ out_full,
+                                 float *__restrict__ out_prob, int &count) {
+    __shared__ double s_cp[NT];
+    __shared__ int s_pick, s_pchunk;
+    __shared__ float s_pval;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int C = (v + NT - 1) / NT, j0 = min(v, tid * C), j1 = min(v, j0 + C);
+    // Prefix bookkeeping: a fresh scan (chunk sums of C terms + a log2(NT)-deep block scan, all
+    // terms positive) is within errP = (C + log2 NT + 2) 2^-52 T of the exact prefix; each later
+    // pick is subtracted in place (one rounding each, errP grows by 2^-52 T). The reference's
+    // running sums are within (v + 64) 2^-53 T of the exact ones. Rescan when the remaining mass
+    // halves, so the bounds stay relative to it.
+    int lg = 0;
+    while ((1 << lg) < NT) ++lg;
     double errP = 0.0, t_scan = 0.0;
     bool need_scan = true;
-    __shared__ int s_pchunk;
-    int count = 0;
+    uint32_t flags = 0u;
+    count = 0;
     for (int k = 0; k < w; ++k) {
         if (need_scan) {
             double cs = 0.0;
-            for (int j = j0; j < j1; ++j) cs += static_cast<double>(Wk[j]);
+            // the chunk sum in a lane-rotated order (any order is within errP): chunks are
+            // C floats apart, so lane l starting at offset l keeps the 32 lanes on distinct banks
+            const int cnt = j1 - j0;
+            for (int i = 0; i < cnt; ++i) {
+                int o = i + lane;
+                o = o >= cnt ? o - cnt : o;
+                o = o >= cnt ? o % cnt : o;
+                cs += static_cast<double>(Wk[j0 + o]);
+            }
             __syncthreads();  // readers of the previous s_cp are done
             s_cp[tid] = cs;
             __syncthreads();
-            for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan of the chunk sums
+            for (int off = 1; off < NT; off <<= 1) {  // inclusive scan of the chunk sums
                 double x = s_cp[tid];
                 if (tid >= off) x += s_cp[tid - off];
                 __syncthreads();
                 s_cp[tid] = x;
                 __syncthreads();
             }
-            t_scan = s_cp[1023];
-            errP = t_scan * 0x1p-46;
+            t_scan = s_cp[NT - 1];
+            errP = t_scan * static_cast<double>(C + lg + 2) * 0x1p-52;
             need_scan = false;
         }
-        const double T = s_cp[1023];
+        const double T = s_cp[NT - 1];
         if (!(T > 0.0)) break;  // all mass drawn: the reference breaks (total <= 0)
         if (tid < 32) {
-            const double uni = uniforms[(size_t)row * w + k];
+            const double uni = k < 64 ? s_uni[k] : uniforms[(size_t)row * w + k];
             const double eb = errP + static_cast<double>(v + 64) * 0x1p-53 * T;
             const double u_lo = __dmul_rd(uni, T - eb), u_hi = __dmul_ru(uni, T + eb);
             // first chunk with CP + eb > u_lo, first with CP - eb > u_hi (CP is non-decreasing)
-            int c_lo = 1024, c_hi = 1024;
-            for (int c0 = 0; c0 < 1024; c0 += 32) {
+            int c_lo = NT, c_hi = NT;
+            for (int c0 = 0; c0 < NT; c0 += 32) {
                 const double cp = s_cp[c0 + lane];
                 const unsigned bl = __ballot_sync(0xffffffffu, cp + eb > u_lo);
                 const unsigned bh = __ballot_sync(0xffffffffu, cp - eb > u_hi);
-                if (c_lo == 1024 && bl) c_lo = c0 + __ffs(bl) - 1;
-                if (c_hi == 1024 && bh) c_hi = c0 + __ffs(bh) - 1;
-                if (c_hi != 1024) break;
+                if (c_lo == NT && bl) c_lo = c0 + __ffs(bl) - 1;
+                if (c_hi == NT && bh) c_hi = c0 + __ffs(bh) - 1;
+                if (c_hi != NT) break;
             }
             int pick = -1;
-            if (c_lo == c_hi && c_hi < 1024) {  // inside chunk c: element prefixes base + warp scan
+            if (c_lo == c_hi && c_hi < NT) {  // inside chunk c: element prefixes base + warp scan
                 const int c = c_lo, e0 = min(v, c * C), e1 = min(v, e0 + C);
                 double base = c > 0 ? s_cp[c - 1] : 0.0;
                 int i_lo = -1, i_hi = -1;
@@ -364,10 +374,12 @@ __global__ void __launch_bounds__(1024)
             if (lane == 0) {
                 s_pick = pick;
                 s_pchunk = c_lo;
-                if (pick >= 0) {
+                if (pick >= 0) {  // Wk[pick] is still P[pick]: only drawn entries are zeroed
+                    const float pv = Wk[pick];
+                    s_pval = pv;
                     out_ridx[(size_t)row * w + k] = pick;
                     out_full[(size_t)row * w + k] = ordered ? ordered[pick] : pick;
-                    out_prob[(size_t)row * w + k] = P[pick];
+                    out_prob[(size_t)row * w + k] = pv;
                     Wk[pick] = 0.0f;
                 }
             }
@@ -379,12 +391,49 @@ __global__ void __launch_bounds__(1024)
         }
         ++count;
         // subtract the drawn mass from the prefixes at and after its chunk
-        if (tid >= s_pchunk) s_cp[tid] -= static_cast<double>(P[s_pick]);
+        if (tid >= s_pchunk) s_cp[tid] -= static_cast<double>(s_pval);
         errP += T * 0x1p-52;
         __syncthreads();
-        need_scan = s_cp[1023] < 0.5 * t_scan;
+        need_scan = s_cp[NT - 1] < 0.5 * t_scan;
     }
-    (void)s_stop;
+    return flags;
+}
+
+// Sampled pick_children (drafting.cpp:44-74) for each row: exact probabilities (kernels.cpp:
+// 62-91, softmax_probs_row) into probs[row], then w draws without replacement with the caller's
+// uniforms (std::uniform_real_distribution<double> of the reference's mt19937_64, in draw
+// order). The reference sums work[] sequentially in double each draw and scans for the first
+// running sum above u = uni * total; here the prefix is a block scan of per-thread chunk sums,
+// and every decision is certified: the tree prefix P_i and the index-order acc_i differ by at
+// most eb = errP + (v + 64) 2^-53 T, so the pick is certain when the first i with P_i + eb > u_lo
+// equals the first with P_i - eb > u_hi (u's own bracket from T +- eb). An uncertain draw (or
+// the reference's upper-edge guard) stops the row with FRS_FLAG_SAMPLE_UNCERTIFIED: the host
+// replays that level from the probabilities. One CTA per row (rows longer than the cluster
+// kernel takes, or k_softmax_sample_cl unavailable).
+__global__ void __launch_bounds__(1024)
+    k_softmax_sample(const float *__restrict__ logits, int v, float temperature, const double *__restrict__ uniforms,
+                     int w, const int32_t *__restrict__ ordered, float *__restrict__ probs, float *__restrict__ work,
+                     int32_t *__restrict__ out_ridx, int32_t *__restrict__ out_full, float *__restrict__ out_prob,
+                     int32_t *__restrict__ out_count, uint32_t *__restrict__ out_flags, int wk_in_smem) {
+    __shared__ dev::ReduceScratch rs;
+    extern __shared__ float s_wk[];  // the draw weights when v floats fit (wk_in_smem)
+    const int row = blockIdx.x, tid = threadIdx.x;
+    const float *L = logits + (size_t)row * v;
+    float *P = probs + (size_t)row * v, *Wk = wk_in_smem ? s_wk : work + (size_t)row * v;
+    __shared__ double s_uni[64];  // this row's uniforms, read once
+    if (tid < min(w, 64)) s_uni[tid] = uniforms[(size_t)row * w + tid];
+    uint32_t flags;
+    if (wk_in_smem) {  // probabilities straight into the draw weights, written out alongside
+        flags = dev::softmax_probs_row(L, v, temperature, Wk, rs);
+        for (int j = tid; j < v; j += 1024) P[j] = Wk[j];
+    } else {
+        // work = probs (coalesced: the chunk sums and the draws read other threads' chunks)
+        flags = dev::softmax_probs_row(L, v, temperature, P, rs);
+        for (int j = tid; j < v; j += 1024) Wk[j] = P[j];
+        __syncthreads();
+    }
+    int count = 0;
+    flags |= sample_draws<1024>(Wk, v, w, row, s_uni, uniforms, ordered, out_ridx, out_full, out_prob, count);
     if (tid == 0) {
         out_count[row] = count;
         if (out_flags) out_flags[row] = flags;
@@ -525,28 +574,25 @@ __device__ __forceinline__ void cl_st(uint32_t a, unsigned long long v) {
     asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
 
+// Phase A of the cluster kernels: this CTA's slice [lo, hi) of the row (KL logits per thread,
+// j = lo + q kSmNT + tid) -> x[q] = e_j = expf(y_j - max) (also written to E, the row's global
+// scratch, for the index-order replay), the row max, 1 / Σ pinned as in
+// softmax_topk_row(tree_total_ok), and the flags — identical in every CTA of the cluster.
+struct ClSoftmax {
+    float mx, inv;
+    uint32_t flags;
+};
 template <int KL>
-__global__ void __launch_bounds__(kSmNT)
-    k_softmax_topk_cl(const float *__restrict__ logits, int ld, int v, int k, float temperature,
-                      const int32_t *__restrict__ ordered, float *__restrict__ ework, int32_t *__restrict__ out_ridx,
-                      int32_t *__restrict__ out_full, float *__restrict__ out_prob, float *__restrict__ out_rowmax,
-                      uint32_t *__restrict__ out_flags) {
+__device__ __forceinline__ ClSoftmax cl_softmax(const float *__restrict__ L, float *__restrict__ E, int v, int lo,
+                                                int hi, float temperature, uint32_t r, float (&x)[KL]) {
     __shared__ unsigned long long s_tab[32];
     __shared__ float s_wmx[kSmNW], s_cmx[kSmC];
     __shared__ int s_wi[kSmNW], s_ci[kSmC], s_cbad[kSmC];
     __shared__ double s_wd[kSmNW], s_cd[kSmC], s_seq;
-    __shared__ unsigned long long s_wtop[kSmNW][kSmKMax], s_all[kSmC][kSmKMax];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t r = cl_rank();
-    const int row = blockIdx.x / kSmC;
-    const int chunk = ((v + kSmC - 1) / kSmC + 3) & ~3;  // host: chunk <= KL * kSmNT
-    const int lo = static_cast<int>(r) * chunk, hi = min(v, lo + chunk);
-    const float *L = logits + (size_t)row * ld;
-    float *E = ework + (size_t)row * ld;
     const bool unit_t = temperature == 1.0f;
     dev::load_exp_table(s_tab);
     asm volatile("griddepcontrol.wait;" ::: "memory");  // logits from the previous kernel (PDL)
-    float x[KL];
 #pragma unroll
     for (int q = 0; q < KL; ++q) {
         const int j = lo + q * kSmNT + tid;
@@ -648,7 +694,26 @@ __global__ void __launch_bounds__(kSmNT)
         cl_sync();
         total = s_seq;
     }
-    const float inv = __double2float_rn(1.0 / total);
+    return ClSoftmax{mx, __double2float_rn(1.0 / total), flags};
+}
+
+template <int KL>
+__global__ void __launch_bounds__(kSmNT)
+    k_softmax_topk_cl(const float *__restrict__ logits, int ld, int v, int k, float temperature,
+                      const int32_t *__restrict__ ordered, float *__restrict__ ework, int32_t *__restrict__ out_ridx,
+                      int32_t *__restrict__ out_full, float *__restrict__ out_prob, float *__restrict__ out_rowmax,
+                      uint32_t *__restrict__ out_flags) {
+    __shared__ unsigned long long s_wtop[kSmNW][kSmKMax], s_all[kSmC][kSmKMax];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t r = cl_rank();
+    const int row = blockIdx.x / kSmC;
+    const int chunk = ((v + kSmC - 1) / kSmC + 3) & ~3;  // host: chunk <= KL * kSmNT
+    const int lo = static_cast<int>(r) * chunk, hi = min(v, lo + chunk);
+    float x[KL];
+    const ClSoftmax sm = cl_softmax<KL>(logits + (size_t)row * ld, ework + (size_t)row * ld, v, lo, hi, temperature,
+                                        r, x);
+    const float mx = sm.mx, inv = sm.inv;
+    const uint32_t flags = sm.flags;
 
     // top-kk: sorted per-thread lists -> warp pops -> CTA merge -> leader merge
     const int kk = min(k, v);
@@ -725,6 +790,49 @@ __global__ void __launch_bounds__(kSmNT)
         }
         if (out_rowmax) out_rowmax[row] = mx;
         if (out_flags) out_flags[row] = flags;
+    }
+}
+
+// k_softmax_sample with each row's softmax split over a cluster of kSmC CTAs (cl_softmax: the
+// FP64 expf work on 8 SMs instead of 1); every CTA writes its slice's probabilities to probs and
+// into the leader's shared draw weights (DSMEM stores), then the leader alone runs the w
+// certified draws (sample_draws<kSmNT>). Same outputs as k_softmax_sample.
+template <int KL>
+__global__ void __launch_bounds__(kSmNT)
+    k_softmax_sample_cl(const float *__restrict__ logits, int v, float temperature,
+                        const double *__restrict__ uniforms, int w, const int32_t *__restrict__ ordered,
+                        float *__restrict__ probs, float *__restrict__ ework, int32_t *__restrict__ out_ridx,
+                        int32_t *__restrict__ out_full, float *__restrict__ out_prob, int32_t *__restrict__ out_count,
+                        uint32_t *__restrict__ out_flags) {
+    extern __shared__ float s_wk[];  // [v]: the leader's draw weights
+    __shared__ double s_uni[64];
+    const int tid = threadIdx.x;
+    const uint32_t r = cl_rank();
+    const int row = blockIdx.x / kSmC;
+    const int chunk = ((v + kSmC - 1) / kSmC + 3) & ~3;  // host: chunk <= KL * kSmNT
+    const int lo = static_cast<int>(r) * chunk, hi = min(v, lo + chunk);
+    if (r == 0 && tid < min(w, 64)) s_uni[tid] = uniforms[(size_t)row * w + tid];
+    float x[KL];
+    const ClSoftmax sm = cl_softmax<KL>(logits + (size_t)row * v, ework + (size_t)row * v, v, lo, hi, temperature,
+                                        r, x);
+    float *P = probs + (size_t)row * v;
+#pragma unroll
+    for (int q = 0; q < KL; ++q) {
+        const int j = lo + q * kSmNT + tid;
+        if (j < hi) {
+            const float p = __fmul_rn(x[q], sm.inv);  // kernels.cpp:86-89
+            P[j] = p;
+            cl_st(cl_map(&s_wk[j], 0), p);
+        }
+    }
+    cl_sync();
+    if (r != 0) return;  // no DSMEM access after this point
+    int count = 0;
+    const uint32_t f =
+        sample_draws<kSmNT>(s_wk, v, w, row, s_uni, uniforms, ordered, out_ridx, out_full, out_prob, count);
+    if (tid == 0) {
+        out_count[row] = count;
+        if (out_flags) out_flags[row] = sm.flags | f;
     }
 }
 
@@ -1462,9 +1570,46 @@ int launch_softmax_sample(frs_ctx *ctx, const float *logits, int n, int v, float
     int st = ctx->scratch.ensure((size_t)n * v * sizeof(float));
     if (st) return st;
     ++ctx->launches;
-    k_softmax_sample<<<n, 1024, 0, s>>>(logits, v, temperature, uniforms, w, ordered_ids, probs,
-                                        static_cast<float *>(ctx->scratch.ptr), out_ridx, out_full, out_prob,
-                                        out_count, out_flags);
+    float *work = static_cast<float *>(ctx->scratch.ptr);
+    const size_t wk_bytes = (size_t)v * sizeof(float);
+    const bool wk_smem = wk_bytes <= 160 * 1024 && wk_bytes + 16 * 1024 <= (size_t)ctx->smem_optin;
+    const int chunk = ((v + kSmC - 1) / kSmC + 3) & ~3;
+    static const bool one_cta = std::getenv("FRS_SOFTMAX_ONE_CTA") != nullptr;  // DIAGNOSTIC
+    if (wk_smem && chunk <= 16 * kSmNT && !one_cta) {  // cluster softmax, the leader draws
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(n * kSmC);
+        cfg.blockDim = dim3(kSmNT);
+        cfg.dynamicSmemBytes = wk_bytes;
+        cfg.stream = s;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = kSmC;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        if (chunk <= 8 * kSmNT) {
+            FRS_CUDA_TRY(cudaFuncSetAttribute(k_softmax_sample_cl<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)wk_bytes));
+            FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_softmax_sample_cl<8>, logits, v, temperature, uniforms, w,
+                                            ordered_ids, probs, work, out_ridx, out_full, out_prob, out_count,
+                                            out_flags));
+        } else {
+            FRS_CUDA_TRY(cudaFuncSetAttribute(k_softmax_sample_cl<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)wk_bytes));
+            FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_softmax_sample_cl<16>, logits, v, temperature, uniforms, w,
+                                            ordered_ids, probs, work, out_ridx, out_full, out_prob, out_count,
+                                            out_flags));
+        }
+        return FRS_OK;
+    }
+    if (wk_smem)
+        FRS_CUDA_TRY(cudaFuncSetAttribute(k_softmax_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wk_bytes));
+    k_softmax_sample<<<n, 1024, wk_smem ? wk_bytes : 0, s>>>(logits, v, temperature, uniforms, w, ordered_ids, probs,
+                                                             work, out_ridx, out_full, out_prob, out_count, out_flags,
+                                                             wk_smem ? 1 : 0);
     FRS_CUDA_TRY(cudaGetLastError());
     return FRS_OK;
 }

@@ -54,6 +54,35 @@ def test_sampled_level_matches_reference(cuda_ctx, reference, scale, width, seed
     assert (fl & _lib.FLAG_SAMPLE_UNCERTIFIED).sum() <= 1
 
 
+@pytest.mark.parametrize("v_sub,width", [(32768, 10), (40000, 16), (50000, 10), (5, 10)])
+def test_sampled_level_large_rows(cuda_ctx, reference, v_sub, width):
+    """Against the reference's pick_children at C2 widths: the cluster sampler (8 CTAs per row
+    softmax, the leader draws from shared memory; 16 logits per thread above 32768) and, past
+    the 160 KB shared draw weights (50000), the one-CTA kernel with global draw weights."""
+    rng = np.random.default_rng(77)
+    V, d, n = v_sub + 100, 128, 4
+    W = (rng.standard_normal((V, d)) * 0.1).astype(np.float32)
+    ids = rng.permutation(V)[:v_sub].astype(np.int32)
+    h = rmsnorm(rng.standard_normal((n, d)))
+    head = api.restrict_lm_head(cuda_ctx, torch.from_numpy(W).cuda(), api.RankedSubset(V, ids), dtype="f32")
+    w = min(width, v_sub)
+    u = reference.uniforms(900, n * w)
+    out = api.draft_head_sample(cuda_ctx, torch.from_numpy(h).cuda(), head, width, torch.from_numpy(u.reshape(n, w)))
+    ex = api.draft_head_topk(cuda_ctx, torch.from_numpy(h).cuda(), head, 1, mode="exact", want_logits=True)
+    logits, probs = ex.logits.cpu().numpy(), out.probs.cpu().numpy()
+    cnt, fl = out.count.cpu().numpy(), out.flags.cpu().numpy()
+    for r in range(n):
+        ref_p = reference.softmax(logits[r], 1.0)
+        assert np.array_equal(probs[r], ref_p), r
+        picks, pr = reference.pick_sampled(ref_p, width, 900, skip=r * w)
+        if fl[r] & _lib.FLAG_SAMPLE_UNCERTIFIED:
+            continue
+        assert cnt[r] == picks.size
+        assert np.array_equal(out.ridx.cpu().numpy()[r, :cnt[r]], picks), r
+        assert np.array_equal(out.prob.cpu().numpy()[r, :cnt[r]], pr), r
+    assert (fl & _lib.FLAG_SAMPLE_UNCERTIFIED).sum() <= 1
+
+
 @pytest.mark.parametrize("name", ["c1_sampled_w4_s11", "c1_sampled_w10_s5"])
 def test_sampled_tree_matches_reference_build_draft_tree(cuda_ctx, reference, name):
     """C1 end to end in sampled mode: the reference's hidden states and its build_draft_tree(rng)
