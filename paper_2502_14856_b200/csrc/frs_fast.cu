@@ -209,10 +209,12 @@ __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int
                                                 __nv_bfloat16 *__restrict__ hs, unsigned *__restrict__ rowmax_bits,
                                                 unsigned *__restrict__ w2_bits, unsigned long long *xtrace,
                                                 float *__restrict__ h_copy) {
-    // launched programmatically after whatever precedes it on the stream: wait for it (h is
-    // final, the previous call's fallback queue is drained), then let the main kernel launch
+    // launched programmatically after whatever precedes it on the stream: let the main kernel
+    // launch at once (its CTAs take the SMs the previous grid leaves and issue their ring fill
+    // of slab stages, which needs nothing from this call), then wait for the predecessor (h is
+    // final, the previous call's fallback queue is drained) before writing anything
+    griddep_launch();  // the main kernel may launch now: it waits for this grid before reading hs
     griddep_wait();
-    griddep_launch();
     if (blockIdx.x == 0) {  // this call's atomicMax targets (the previous call is complete)
         if (threadIdx.x < 64) rowmax_bits[threadIdx.x] = 0u;  // below every ordered value
         if (threadIdx.x == 0) *w2_bits = 0u;
@@ -379,12 +381,30 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             // path (a lambda-based version of this loop streamed 15 % slower). A full tile is
             // one 128-row box; a short tile (the CTA's last) is loaded as 32-row boxes.
             const uint64_t pol_w = policy_evict_first(), pol_h = policy_evict_last();
-            int stage = 0;
-            uint32_t phase = 0;
-            bool waited = false;
-            for (int t = t_begin; t < t_end; ++t) {
+            // Ring fill before the dependency wait: the slab halves of the first STAGES stages
+            // (the slab needs nothing from the previous grid); their hs halves after it.
+            const int pre = min(STAGES, (t_end - t_begin) * KB);
+            for (int g = 0; g < pre; ++g) {
+                const int t = t_begin + g / KB, kb = g % KB, nch = tile_chunks(t), r0 = tile_row0(t);
+                mbar_expect_tx(&full[g], nch * (CH * BK * 2) + C::B_BYTES);
+                if (nch == CPT) {
+                    tma_load_2d(sA + g * C::A_BYTES, &mapW, &full[g], kb * BK, r0, pol_w);
+                } else {
+                    for (int c = 0; c < nch; ++c)
+                        tma_load_2d(sA + g * C::A_BYTES + c * (CH * BK * 2), &mapW32, &full[g], kb * BK, r0 + c * CH,
+                                    pol_w);
+                }
+            }
+            FRS_TRACE(P, 1);
+            griddep_wait();  // hs is written by k_hsplit (programmatic dependency)
+            FRS_TRACE(P, 9);
+            for (int g = 0; g < pre; ++g)
+                tma_load_2d(sB + g * C::B_BYTES, &mapH, &full[g], (g % KB) * BK, 0, pol_h);
+            int stage = pre % STAGES;
+            uint32_t phase = pre == STAGES ? 1u : 0u;
+            for (int t = t_begin + pre / KB, kb0 = pre % KB; t < t_end; ++t, kb0 = 0) {
                 const int nch = tile_chunks(t), r0 = tile_row0(t);
-                for (int kb = 0; kb < KB; ++kb) {
+                for (int kb = kb0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], nch * (CH * BK * 2) + C::B_BYTES);
                     if (nch == CPT) {
@@ -393,12 +413,6 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                         for (int c = 0; c < nch; ++c)
                             tma_load_2d(sA + stage * C::A_BYTES + c * (CH * BK * 2), &mapW32, &full[stage], kb * BK,
                                         r0 + c * CH, pol_w);
-                    }
-                    if (!waited) {  // hs is written by k_hsplit (programmatic dependency)
-                        FRS_TRACE(P, 1);
-                        griddep_wait();
-                        FRS_TRACE(P, 9);
-                        waited = true;
                     }
                     tma_load_2d(sB + stage * C::B_BYTES, &mapH, &full[stage], kb * BK, 0, pol_h);
                     if (++stage == STAGES) {
@@ -1008,6 +1022,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     float *ht = reinterpret_cast<float *>(fsm_raw);  // [8][TP]
     float *wt = ht + 8 * TP;                          // [8 cand][8][TP] fp32 (bf16 widened, exact)
     __shared__ unsigned long long s_mine[kCsMax], s_sel[kCsMax], s_tab[32], s_sorted[kCsMax];
+    __shared__ unsigned long long s_surv[kSurvMax], s_vk;
     __shared__ double s_hn2[kFinThreads / 32];
     __shared__ float s_abw[kFinThreads / 32], s_pmw[4], s_thw[2];
     __shared__ float s_psw[4];
@@ -1015,11 +1030,13 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     __shared__ float s_fin[kCsMax];      // leader: exact logits of S, in arrival (slot) order
     __shared__ int32_t s_ord[kCsMax], s_spos[kCsMax];
     __shared__ int s_nsel, s_nmine, s_cnt, s_nsurv, s_badw[kFinThreads / 32];
-    __shared__ unsigned long long s_surv[kSurvMax], s_vk;
     __shared__ float s_afar[kFinThreads / 32];
     FRS_FTRACE(A, 0);
-    // no early griddepcontrol.launch_dependents here: 148 fallback CTAs parked in
-    // griddepcontrol.wait next to this grid slowed it by ~2.7 us per call (measured)
+    // Draft rows: let the next call's chain launch now (its k_hsplit waits for this grid; its main
+    // kernel's CTAs take the SMs no finalize CTA holds and fill their stage rings while this
+    // grid runs). Verify rows: no early launch — 148 fallback CTAs parked in griddepcontrol.wait
+    // next to this grid slowed it by ~2.7 us per call (measured).
+    if (!A.argmax) griddep_launch();
 
     const int i = blockIdx.x, b = static_cast<int>(cluster_rank()), tid = threadIdx.x;
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = tid & 31;
