@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--no-decode", action="store_true", help="skip the head-path decode loop measurement")
     p.add_argument("--no-sweep", action="store_true", help="skip the C3 V_sub sweep")
     p.add_argument("--no-batched", action="store_true", help="skip the C5 batched level")
+    p.add_argument("--no-streams", action="store_true", help="skip the C5 256-stream decode measurement")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
 
@@ -366,6 +367,7 @@ def main():
     # decode_step_table (one host sync per iteration; the two-call loop is reported beside it).
     # Transformer layers are out of scope (stated); random-init heads accept ~1.4 tokens/iter.
     decode = None
+    decode_streams = None
     if not args.no_decode:
         ge = torch.Generator(device=dev).manual_seed(555 + rank)
         E = rmsnorm_rows(torch.randn(V, d, generator=ge, device=dev))
@@ -403,6 +405,34 @@ def main():
                   "ms_per_iteration_two_calls": 1000.0 * two_call_s / iters,
                   "mean_accepted_length": emitted / iters, "iterations": iters, "streams": world,
                   "note": "transformer layers excluded (SURVEY.md §8(d)); random-init weights"}
+        # C5 (BASELINE configs[4]): 256 independent decode streams, 256 / world per rank, one
+        # decode_step_table_multi call per iteration (every draft level one EXACT head call over
+        # all streams' beam rows, one FAST verify call over all streams' 61-row trees)
+        if not args.no_streams:
+            S = max(1, 256 // world)
+            roots = [int(x) for x in np.random.default_rng(99 + rank).integers(0, V, S)]
+            for _ in range(1):
+                roots = [int(o.emitted[-1]) for _, o in api.decode_step_table_multi(dh, E, roots, Wb, params, mode="fast")]
+            torch.cuda.synchronize()
+            s_iters, s_emitted = 2, 0
+            t0 = time.perf_counter()
+            for _ in range(s_iters):
+                res = api.decode_step_table_multi(dh, E, roots, Wb, params, mode="fast")
+                s_emitted += sum(o.accepted_length() for _, o in res)
+                roots = [int(o.emitted[-1]) for _, o in res]
+            ms_s = time.perf_counter() - t0
+            srate = s_emitted / ms_s
+            if world > 1:
+                t = torch.tensor([srate, ms_s], device=dev, dtype=torch.float64)
+                dist.all_reduce(t[:1], op=dist.ReduceOp.SUM)
+                dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
+                srate, ms_s = float(t[0].item()), float(t[1].item())
+            decode_streams = {"workload": "C5: 256 independent decode streams at C2 (tree 10/6/60 per stream, exact "
+                                          "draft levels batched across streams, FAST verify over all streams' rows)",
+                              "streams_total": S * world, "streams_per_rank": S, "tokens_per_s": srate,
+                              "ms_per_iteration": 1000.0 * ms_s / s_iters,
+                              "mean_accepted_length": s_emitted / (s_iters * S), "iterations": s_iters,
+                              "api": "decode_step_table_multi", "scaling": "weak (streams sharded over ranks)"}
         del E, Wb
 
     # C3 (BASELINE configs[2]): the V_sub sweep at the Llama-3-8B shape, FAST draft level back to
@@ -537,6 +567,7 @@ def main():
             "verify_vocab_parallel": verify_vp, "verify_shards_c4": verify_shards, "vsub_sweep_c3": vsub_sweep,
             "batched_c5": batched,
             "decode": decode,
+            "decode_streams_c5": decode_streams,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

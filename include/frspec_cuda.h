@@ -306,6 +306,17 @@ FRS_API int frs_decode_step_table(frs_head *h, const float *table, int32_t root_
                                   int32_t *parents, int32_t *depths, double *log_joint, int *count,
                                   int32_t *emitted, int *n_emitted, int32_t *path, int *n_path);
 
+/* S independent decode streams (BASELINE configs[4]), one head-path iteration each: per stream
+ * exactly frs_decode_step_table(roots[q]) (drafting.cpp:122-245, verification.cpp:42-71), with the
+ * streams batched — every draft level is one EXACT head call over all streams' beam rows (rows
+ * are independent, drafting.cpp:189-193) and the verify head one call over all streams'
+ * [root, tokens...] rows. Outputs per stream q: tokens/parents/depths/log_joint/path at
+ * [q * total], emitted at [q * (total + 1)], count/n_emitted/n_path at [q]. */
+FRS_API int frs_decode_step_table_multi(frs_head *h, const float *table, int S, const int32_t *roots, const void *W,
+                                        int V, int w_dtype, int verify_mode, int width, int depth, int total,
+                                        int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint,
+                                        int *count, int32_t *emitted, int *n_emitted, int32_t *path, int *n_path);
+
 /* Vocab-parallel verify head (SURVEY.md §8(b) frs_allgather_merge, §8(e)): every rank of an NCCL
  * communicator holds the contiguous LM-head shard [id_offset, id_offset + v_rows) (frs_vocab_shard)
  * and calls this with the same 1 + k hidden rows h [m x d]: K3 over its shard, ncclAllGather of

@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass, field
-from typing import Callable, Optional, Sequence, Tuple
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -831,6 +831,37 @@ def decode_step_table(head: "DeviceHead", table: torch.Tensor, root_token: int, 
     n = cnt.value
     return (DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy()),
             VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy()))
+
+
+def decode_step_table_multi(head: "DeviceHead", table: torch.Tensor, roots, lm_head: torch.Tensor,
+                            params: "DraftParams" = None, mode="fast") -> List[Tuple[DraftTree, VerifyOutcome]]:
+    """One head-path decode iteration for each of S independent streams (BASELINE configs[4]),
+    batched across streams (frs_decode_step_table_multi): per stream the same results as
+    decode_step_table(head, table, roots[q], lm_head, params, mode)."""
+    params = params or DraftParams()
+    total = params.total_draft_tokens
+    r = np.ascontiguousarray(np.asarray(roots, dtype=np.int32).reshape(-1))
+    S = int(r.size)
+    if S < 1:
+        raise ValueError("decode_step: at least one stream")
+    if table.shape[1] != head.d or lm_head.shape[1] != head.d or table.shape[0] < head.vocab:
+        raise ValueError("decode_step: table [>= vocab x d] and verify head [V x d] must match the draft head")
+    tok, par, dep = (np.empty(S * total, np.int32) for _ in range(3))
+    lj = np.empty(S * total, np.float64)
+    em, path = np.empty(S * (total + 1), np.int32), np.empty(S * total, np.int32)
+    cnt, ne, npth = (np.empty(S, np.int32) for _ in range(3))
+    dt = DTYPE_BF16 if lm_head.dtype == torch.bfloat16 else DTYPE_F32
+    check(lib().frs_decode_step_table_multi(head.handle, _ptr(table), S, _np_ptr(r), _ptr(lm_head), lm_head.shape[0],
+                                            dt, _mode(mode), params.beam_width, params.search_depth, total,
+                                            _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj), _np_ptr(cnt),
+                                            _np_ptr(em), _np_ptr(ne), _np_ptr(path), _np_ptr(npth)), "decode_step")
+    out = []
+    for q in range(S):
+        n, o = int(cnt[q]), q * total
+        tree = DraftTree(tok[o:o + n].copy(), par[o:o + n].copy(), dep[o:o + n].copy(), lj[o:o + n].copy())
+        e0 = q * (total + 1)
+        out.append((tree, VerifyOutcome(path[o:o + int(npth[q])].copy(), em[e0:e0 + int(ne[q])].copy())))
+    return out
 
 
 class AcceptanceStats:

@@ -2282,9 +2282,10 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
         return FRS_OK;
     }
     if (argmax && n > 64 && batched_ok) {  // verify of many rows: approximate logits + per-row argmax
-        // (the list path is faster up to 64 rows: 238 vs 354 us at C2's 61 rows)
-        for (int r0 = 0; r0 < n; r0 += 64) {
-            const int nr = std::min(64, n - r0);
+        // (the list path is faster up to 64 rows: 238 vs 354 us at C2's 61 rows); passes of 128
+        // rows (N = 256 UMMA): the pass is HBM / tensor balanced at the Llama-3-8B verify head
+        for (int r0 = 0; r0 < n; r0 += 128) {
+            const int nr = std::min(128, n - r0);
             const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, v_rows, nullptr, 1, 1.0f, nullptr,
                                            out_full + r0, out_prob ? out_prob + r0 : nullptr, nullptr, nullptr,
                                            out_flags ? out_flags + r0 : nullptr, s, true, id_offset);

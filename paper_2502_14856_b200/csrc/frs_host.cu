@@ -33,6 +33,9 @@ struct frs_head {
     int v_sub = 0, d = 0, dtype = FRS_DTYPE_F32;
     // per-level staging (device + pinned host)
     frs::DevBuf lvl_ridx, lvl_full, lvl_prob, lvl_tok, hidden, tree_ws, smp_u, smp_probs;
+    // multi-stream decode staging (frs_decode_step_table_multi): row tokens, hidden rows, packed
+    // level outputs / verify argmax ids
+    frs::DevBuf ms_tok, ms_hidden, ms_out;
     int32_t *h_ridx = nullptr, *h_full = nullptr, *h_tok = nullptr;
     float *h_prob = nullptr;
 };
@@ -737,6 +740,170 @@ int frs_decode_step_table(frs_head *h, const float *table, int32_t root_token, c
         return st;
     return verify_greedy_impl(ctx, nullptr, table, h->vocab, root_token, W, V, d, w_dtype, verify_mode, tokens,
                               parents, *count, emitted, n_emitted, path, n_path);
+}
+
+// S independent decode streams, one head-path iteration each (drafting.cpp:122-245 then
+// verification.cpp:42-71 per stream), batched across streams: every draft level is ONE EXACT
+// head call over all streams' beam rows (rows are independent: drafting.cpp:189-193), the
+// beam / select_top_k bookkeeping runs per stream on the host in the reference's order, and the
+// verify head is ONE call over all streams' [root, tokens...] rows followed by each stream's
+// accept walk. Per stream the results equal frs_decode_step_table (same arithmetic per row).
+// Outputs are [S][total] (tokens, parents, depths, log_joint, path), [S][total + 1] (emitted) and
+// [S] (count, n_emitted, n_path).
+int frs_decode_step_table_multi(frs_head *h, const float *table, int S, const int32_t *roots, const void *W, int V,
+                                int w_dtype, int verify_mode, int width, int depth, int total, int32_t *tokens,
+                                int32_t *parents, int32_t *depths, double *log_joint, int *count, int32_t *emitted,
+                                int *n_emitted, int32_t *path, int *n_path) {
+    FRS_REQUIRE(h && table && roots && W && tokens && parents && depths && log_joint && count && emitted &&
+                    n_emitted && path && n_path,
+                "decode_step: null pointer");
+    FRS_REQUIRE(S >= 1, "decode_step: at least one stream");
+    if (width < 1) return fail(FRS_EINVAL, "draft params: beam_width must be >= 1");
+    if (depth < 1) return fail(FRS_EINVAL, "draft params: search_depth must be >= 1");
+    if (total < width || total > 64)
+        return fail(FRS_EINVAL, "draft params: total_draft_tokens must lie in [beam_width, 64]");
+    for (int q = 0; q < S; ++q)
+        FRS_REQUIRE(roots[q] >= 0 && roots[q] < h->vocab, "verify_greedy: root token outside the hidden table");
+    FRS_REQUIRE(verify_mode == FRS_MODE_EXACT || verify_mode == FRS_MODE_FAST, "decode_step: unknown mode");
+    frs_ctx *ctx = h->ctx;
+    FRS_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int w = std::min(width, h->v_sub), d = h->d;  // drafting.cpp:40
+    const size_t max_rows = (size_t)S * std::max(width, 1 + total);
+    int st;
+    if ((st = h->ms_tok.ensure(max_rows * 4)) || (st = h->ms_hidden.ensure(max_rows * d * sizeof(float))) ||
+        (st = h->ms_out.ensure(std::max((size_t)S * width * w * 12, max_rows * 4))))
+        return st;
+    int32_t *tok_dev = static_cast<int32_t *>(h->ms_tok.ptr);
+    float *hd = static_cast<float *>(h->ms_hidden.ptr);
+    int32_t *pk = static_cast<int32_t *>(h->ms_out.ptr);
+    std::vector<int32_t> rtok, hout;
+    std::vector<std::vector<Cand>> cands(S);
+    std::vector<std::vector<int>> beam(S);
+    std::vector<int> roff(S + 1);
+    // one EXACT level over rtok (all streams' rows): packed [ridx | full | prob] back to the host
+    auto run_level = [&](int nrows) -> int {
+        FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, rtok.data(), sizeof(int32_t) * nrows, cudaMemcpyHostToDevice, s));
+        int rc = frs_gather_rows(ctx, table, h->vocab, d, tok_dev, nrows, hd, s);
+        if (rc) return rc;
+        const size_t cells = (size_t)nrows * w;
+        rc = frs_draft_head_topk(ctx, hd, nrows, d, h->slab, h->v_sub, h->dtype, h->ordered_dev, w, 1.0f,
+                                 FRS_MODE_EXACT, pk, pk + cells, reinterpret_cast<float *>(pk + 2 * cells), nullptr,
+                                 nullptr, nullptr, nullptr, s);
+        if (rc) return rc;
+        hout.resize(cells * 3);
+        FRS_CUDA_TRY(cudaMemcpyAsync(hout.data(), pk, cells * 12, cudaMemcpyDeviceToHost, s));
+        FRS_CUDA_TRY(cudaStreamSynchronize(s));
+        return FRS_OK;
+    };
+    auto child = [&](size_t cells, size_t o, int parent, int pdepth, double plj) {
+        float p;
+        std::memcpy(&p, &hout[2 * cells + o], 4);
+        return Cand{hout[cells + o], hout[o], parent, pdepth + 1, plj + std::log(static_cast<double>(p))};
+    };
+    // Forward 1 of search_depth: the roots (drafting.cpp:133-160), one row per stream
+    rtok.assign(roots, roots + S);
+    if ((st = run_level(S))) return st;
+    for (int q = 0; q < S; ++q)
+        for (int c = 0; c < w; ++c) {
+            beam[q].push_back(static_cast<int>(cands[q].size()));
+            cands[q].push_back(child((size_t)S * w, (size_t)q * w + c, -1, 0, 0.0));
+        }
+    for (int level = 1; level < depth; ++level) {
+        rtok.clear();
+        for (int q = 0; q < S; ++q) {
+            std::vector<int> &b = beam[q];
+            if (static_cast<int>(b.size()) > width) {  // drafting.cpp:164-176
+                std::sort(b.begin(), b.end(), ByLogJoint{&cands[q]});
+                b.resize(width);
+                std::sort(b.begin(), b.end());
+            }
+            roff[q] = static_cast<int>(rtok.size());
+            for (int i : b) rtok.push_back(cands[q][i].token);
+        }
+        roff[S] = static_cast<int>(rtok.size());
+        if (rtok.empty()) break;
+        if ((st = run_level(roff[S]))) return st;
+        const size_t cells = (size_t)roff[S] * w;
+        for (int q = 0; q < S; ++q) {  // drafting.cpp:199-220 (parent fields read by value)
+            std::vector<int> next;
+            for (size_t i = 0; i < beam[q].size(); ++i) {
+                const int pidx = beam[q][i];
+                const int pdepth = cands[q][pidx].depth;
+                const double plj = cands[q][pidx].log_joint;
+                for (int c = 0; c < w; ++c) {
+                    next.push_back(static_cast<int>(cands[q].size()));
+                    cands[q].push_back(child(cells, (size_t)(roff[q] + i) * w + c, pidx, pdepth, plj));
+                }
+            }
+            beam[q] = std::move(next);
+        }
+    }
+    // select_top_k (drafting.cpp:93-118, prefix_closed = false) and emit (230-244), per stream;
+    // then the verify rows [root, tokens...] of every stream
+    rtok.clear();
+    for (int q = 0; q < S; ++q) {
+        const std::vector<Cand> &cq = cands[q];
+        std::vector<int> order(cq.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::sort(order.begin(), order.end(), ByLogJoint{&cq});
+        std::vector<char> sel(cq.size(), 0);
+        int cnt = 0;
+        for (int c : order) {
+            if (sel[c]) continue;
+            if (cq[c].parent >= 0 && !sel[cq[c].parent]) continue;
+            if (cnt + 1 > total) continue;
+            sel[c] = 1;
+            ++cnt;
+        }
+        std::vector<int> remap(cq.size(), -1);
+        int out = 0;
+        int32_t *tq = tokens + (size_t)q * total, *pq = parents + (size_t)q * total, *dq = depths + (size_t)q * total;
+        double *lq = log_joint + (size_t)q * total;
+        for (size_t i = 0; i < cq.size(); ++i) {
+            if (!sel[i]) continue;
+            remap[i] = out;
+            tq[out] = cq[i].token;
+            pq[out] = cq[i].parent >= 0 ? remap[cq[i].parent] : -1;
+            dq[out] = cq[i].depth;
+            lq[out] = cq[i].log_joint;
+            ++out;
+        }
+        count[q] = out;
+        roff[q] = static_cast<int>(rtok.size());
+        rtok.push_back(roots[q]);
+        rtok.insert(rtok.end(), tq, tq + out);
+    }
+    roff[S] = static_cast<int>(rtok.size());
+    // verify head argmax over every stream's rows (rows are independent), then each stream's
+    // accept walk (verification.cpp:42-71): emit the argmax at the current node, follow the first
+    // child (by index) carrying it, stop at the bonus token
+    const int R = roff[S];
+    FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, rtok.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
+    if ((st = frs_gather_rows(ctx, table, h->vocab, d, tok_dev, R, hd, s))) return st;
+    if ((st = frs_verify_head_argmax(ctx, hd, R, d, W, V, w_dtype, 0, verify_mode, pk, nullptr, nullptr, s))) return st;
+    std::vector<int32_t> ids(R);
+    FRS_CUDA_TRY(cudaMemcpyAsync(ids.data(), pk, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, s));
+    FRS_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int q = 0; q < S; ++q) {
+        const int k = count[q];
+        const int32_t *tq = tokens + (size_t)q * total, *pq = parents + (size_t)q * total, *aq = ids.data() + roff[q];
+        int32_t *eq = emitted + (size_t)q * (total + 1), *wq = path + (size_t)q * total;
+        int node = -1, ne = 0, np = 0;
+        for (int step = 0; step <= k; ++step) {
+            const int32_t best = aq[node + 1];
+            int match = -1;
+            for (int c = 0; c < k && match < 0; ++c)
+                if (pq[c] == node && tq[c] == best) match = c;
+            eq[ne++] = best;
+            if (match < 0) break;
+            wq[np++] = match;
+            node = match;
+        }
+        n_emitted[q] = ne;
+        n_path[q] = np;
+    }
+    return FRS_OK;
 }
 
 int frs_rng_create(uint64_t seed, frs_rng **out) {

@@ -276,6 +276,52 @@ def test_decode_step_table_matches_two_calls(cuda_ctx, restatement, mode, width,
         token = int(out.emitted[-1])
 
 
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+@pytest.mark.parametrize("width,depth,total,S", [(10, 6, 60, 7), (2, 2, 10, 3), (4, 3, 4, 9)])
+def test_decode_step_table_multi_matches_per_stream(cuda_ctx, restatement, mode, width, depth, total, S):
+    """frs_decode_step_table_multi (S streams batched per draft level and in one verify call) ==
+    decode_step_table per stream, chained over iterations, and the oracle's verify walk."""
+    rng = np.random.default_rng(16)
+    V, d, v_sub = 4096, 128, 1024
+    W = (rng.standard_normal((V, d)) * 0.05).astype(np.float32)
+    W = torch.from_numpy(W).to(torch.bfloat16).to(torch.float32).numpy()
+    E = rmsnorm(rng.standard_normal((V, d)))
+    ids = rng.permutation(V)[:v_sub].astype(np.int32)
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(V, ids), dtype="f32")
+    Ed, Wb = torch.from_numpy(E).cuda(), torch.from_numpy(W).cuda().to(torch.bfloat16)
+    params = api.DraftParams(width, depth, total)
+    roots = [int(x) for x in rng.integers(0, V, S)]
+    roots[-1] = roots[0]  # two streams at the same token: identical results
+    for _ in range(3):
+        multi = api.decode_step_table_multi(head, Ed, roots, Wb, params, mode=mode)
+        assert len(multi) == S
+        for q, (tree, out) in enumerate(multi):
+            ref_tree, ref = api.decode_step_table(head, Ed, roots[q], Wb, params, mode=mode)
+            for key in ("tokens", "parents", "depths", "log_joint"):
+                assert np.array_equal(getattr(tree, key), getattr(ref_tree, key)), (q, key)
+            assert np.array_equal(out.emitted, ref.emitted) and np.array_equal(out.accepted_path, ref.accepted_path)
+            rows = np.concatenate([[roots[q]], tree.tokens])
+            em, path = restatement.verify_greedy_ids(restatement.verify_argmax(E[rows], W)[0], tree.tokens,
+                                                     tree.parents)
+            assert np.array_equal(out.emitted, em) and np.array_equal(out.accepted_path, path)
+        roots = [int(out.emitted[-1]) for _, out in multi]
+
+
+def test_decode_step_table_multi_rejects(cuda_ctx):
+    rng = np.random.default_rng(18)
+    V, d = 512, 64
+    W = (rng.standard_normal((V, d)) * 0.05).astype(np.float32)
+    E = rmsnorm(rng.standard_normal((V, d)))
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(V, np.arange(256, dtype=np.int32)), dtype="f32")
+    Ed, Wd = torch.from_numpy(E).cuda(), torch.from_numpy(W).cuda()
+    with pytest.raises(api.InvalidArgument, match="root token outside"):
+        api.decode_step_table_multi(head, Ed, [3, V], Wd, api.DraftParams(2, 2, 4))
+    with pytest.raises(api.InvalidArgument, match="total_draft_tokens"):
+        api.decode_step_table_multi(head, Ed, [3, 4], Wd, api.DraftParams(4, 2, 3))
+    with pytest.raises(ValueError, match="at least one stream"):
+        api.decode_step_table_multi(head, Ed, [], Wd, api.DraftParams(2, 2, 4))
+
+
 @pytest.mark.parametrize("v_sub,k,temperature", [(5, 10, 1.0), (100, 16, 1.0), (1000, 3, 0.7), (32768, 10, 1.0),
                                                  (40000, 16, 1.0), (65536, 1, 1.3), (2000, 17, 1.0)])
 def test_draft_level_without_total_matches_oracle(cuda_ctx, restatement, v_sub, k, temperature):
