@@ -47,11 +47,20 @@ def parse():
     return p.parse_args()
 
 
-def lib_sha256():
+def source_sha256():
+    """sha256 over the kernel sources and build recipe (csrc/, include/, build.py): the tag an ncu
+    traffic summary must carry to be reported (nvcc output is not byte-reproducible across
+    builds of the same sources, so the .so bytes cannot be the tag)."""
+    import glob
     import hashlib
-    from paper_2502_14856_b200 import _lib
-    with open(_lib.LIB_PATH, "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()
+    h = hashlib.sha256()
+    pk = os.path.join(ROOT, "paper_2502_14856_b200")
+    for f in sorted(glob.glob(os.path.join(pk, "csrc", "*")) + glob.glob(os.path.join(ROOT, "include", "*.h")) +
+                    [os.path.join(pk, "build.py")]):
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
 
 
 def peaks():
@@ -284,17 +293,17 @@ def main():
     # one CUDA graph): its steady-state duration is the device time per step of the timed region
     step_s = elapsed_ms / args.steps / 1000.0
     achieved = alg_bytes / step_s / 1e9
-    # dram__bytes of the dominant kernel from an ncu capture of THIS build (tools/ncu_traffic.sh
-    # writes the summary with the library's sha256); a summary of another build is not used
+    # dram__bytes of the dominant kernel from an ncu capture of THESE kernel sources
+    # (tools/ncu_traffic.sh tags the summary with source_sha256()); another source's is not used
     traffic, traffic_src = None, "no ncu summary for this build (run tools/ncu_traffic.sh)"
     prof = os.path.join(ROOT, "profiles", f"ncu_{mode}_{args.dtype}_summary.json")
     if os.path.exists(prof):
         with open(prof) as fh:
             summ = json.load(fh)
-        if summ.get("lib_sha256") == lib_sha256():
+        if summ.get("source_sha256") == source_sha256():
             traffic, traffic_src = summ.get("dram_bytes_per_launch"), summ.get("source")
         else:
-            traffic_src = "ncu summary of another build (lib sha differs): not reported"
+            traffic_src = "ncu summary of other kernel sources (source sha differs): not reported"
 
     # e2e through the public host-buffer API: pinned H2D of h, K2, D2H of ids/probs, sync.
     dh = api.DeviceHead(ctx, W, subset, dtype=args.dtype)

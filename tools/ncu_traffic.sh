@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 # dram__bytes of k_fast_main per launch for the CURRENT build (run under gpurun): writes
-# profiles/ncu_fast_bf16_summary.json tagged with the library's sha256 (bench.py reports the
-# traffic only when the tag matches the .so it loaded).
+# profiles/ncu_fast_bf16_summary.json tagged with the kernel sources' sha256 (bench.py reports
+# the traffic only when the tag matches the sources it runs).
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
@@ -23,9 +23,11 @@ for r in rows[hdr + 1:]:
     vals.setdefault(d["Metric Name"], []).append(float(d["Metric Value"].replace(",", "")) * scale)
 rd = statistics.median(vals["dram__bytes_read.sum"])
 wr = statistics.median(vals["dram__bytes_write.sum"])
-sha = hashlib.sha256(open("paper_2502_14856_b200/libfrspec_cuda.so", "rb").read()).hexdigest()
+import sys; sys.path.insert(0, ".")
+from bench import source_sha256
+sha = source_sha256()
 out = {"kernel": "k_fast_main<16,1,0>", "source": "tools/ncu_traffic.sh (ncu --metrics dram__bytes_*, C2, 5 launches, median)",
-       "lib_sha256": sha, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+       "source_sha256": sha, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
        "gpu_time_ns_median": statistics.median(vals.get("gpu__time_duration.sum", [0]))}
 json.dump(out, open("profiles/ncu_fast_bf16_summary.json", "w"), indent=1)
 json.dump(out, open("gpurun_out/ncu_fast_bf16_summary.json", "w"), indent=1)  # merged back by gpurun
