@@ -185,6 +185,7 @@ struct Partials {
     int ld_logits;
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
+    unsigned *main_done;       // [1] main CTAs whose outputs are published (release; reset by k_hsplit)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -208,7 +209,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int n, int d, int NP,
                                                 __nv_bfloat16 *__restrict__ hs, unsigned *__restrict__ rowmax_bits,
                                                 unsigned *__restrict__ w2_bits, unsigned long long *xtrace,
-                                                float *__restrict__ h_copy) {
+                                                float *__restrict__ h_copy, unsigned *__restrict__ main_done) {
     // launched programmatically after whatever precedes it on the stream: let the main kernel
     // launch at once (its CTAs take the SMs the previous grid leaves and issue their ring fill
     // of slab stages, which needs nothing from this call), then wait for the predecessor (h is
@@ -217,7 +218,10 @@ __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int
     griddep_wait();
     if (blockIdx.x == 0) {  // this call's atomicMax targets (the previous call is complete)
         if (threadIdx.x < 64) rowmax_bits[threadIdx.x] = 0u;  // below every ordered value
-        if (threadIdx.x == 0) *w2_bits = 0u;
+        if (threadIdx.x == 0) {
+            *w2_bits = 0u;
+            *main_done = 0u;
+        }
     }
     if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[0] = gtimer();
     const int total4 = NP * d / 4;  // d % 8 == 0 on the FAST path
@@ -717,6 +721,10 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
     __syncthreads();  // every TMEM read is done; s_rmax / s_w2max complete
     if (threadIdx.x < n && s_rmax[threadIdx.x]) atomicMax(P.rowmax_bits + threadIdx.x, s_rmax[threadIdx.x]);
     if (threadIdx.x == 64) atomicMax(P.w2_bits, s_w2max);
+    // this CTA's lists, bounds and maxima are published: one release increment after a barrier
+    // (the finalize acquires the count instead of waiting for the whole grid to retire)
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.main_done) : "memory");
     if (kDiag && P.late_trigger) griddep_launch();
     if (threadIdx.x == 0) FRS_TRACE(P, 7);
     if (kDiag && P.trace && threadIdx.x == 0) {  // DIAGNOSTIC: the SM this CTA ran on
@@ -765,6 +773,7 @@ struct FinArgs {
     int fin_ctas;                    // finalize cluster width (power of 2, <= kFinCtas): 8 draft, 2 verify
     int fin_stage;                   // candidates staged per round (<= kFinStage): 8 draft, 4 verify
     int surv_eps;                    // finalize survivor window (units of eps below the row max)
+    int flag_sync;                   // acquire the main CTAs' publish count instead of griddepcontrol.wait
     unsigned long long *fb_arrive;   // monotonic CTA arrival counter of k_fast_fallback
 };
 
@@ -1087,7 +1096,23 @@ __global__ void __launch_bounds__(kFinThreads) k_fast_finalize(FinArgs A) {
     __syncthreads();
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     FRS_FTRACE(A, 1);
-    griddep_wait();
+    // The main grid's outputs: every main CTA releases one increment of main_done after
+    // publishing, so acquiring main_done == G makes all of them visible — without waiting for
+    // the grid's retirement and the dependency flush (~1.3 us). All main CTAs are resident (this
+    // grid launches only after each of them has started), so the spin cannot starve them.
+    if (A.flag_sync) {
+        if (tid == 0) {
+            unsigned dn;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(dn) : "l"(A.P.main_done) : "memory");
+                if (dn >= static_cast<unsigned>(G)) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+    } else {
+        griddep_wait();
+    }
     FRS_FTRACE(A, 2);
     const long long c_fin0_ = clock64();
     if (kDiag && A.ablate == 1) return;
@@ -1970,7 +1995,7 @@ int make_map(CUtensorMap *map, const void *base, int rows, int cols, int box_row
 
 // row_ctr[64] u64 | fb_arrive u64 | fb_count u32 | fb_rows[64] u32 | rowmax_bits[64] u32 | w2_bits u32
 constexpr size_t kCtrRowmax = 64 * 8 + 8 + 4 + 64 * 4;
-constexpr size_t kCtrBytes = kCtrRowmax + 64 * 4 + 4;
+constexpr size_t kCtrBytes = kCtrRowmax + 64 * 4 + 4 + 4;  // + main_done
 
 struct FastWs {
     __nv_bfloat16 *hs;
@@ -2026,6 +2051,7 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.P.range_shift = kDiag ? shift : 0;
     w.P.rowmax_bits = reinterpret_cast<unsigned *>(static_cast<uint8_t *>(ctx->fast_ctr.ptr) + kCtrRowmax);
     w.P.w2_bits = w.P.rowmax_bits + 64;
+    w.P.main_done = w.P.w2_bits + 1;
     return FRS_OK;
 }
 
@@ -2226,7 +2252,8 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
         cfg.numAttrs = 1;
         if ((st = configure(k_hsplit, 0))) return st;
         FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, h, n, d, NP, w.hs, w.P.rowmax_bits, w.P.w2_bits,
-                                        static_cast<unsigned long long *>(nullptr), static_cast<float *>(nullptr)));
+                                        static_cast<unsigned long long *>(nullptr), static_cast<float *>(nullptr),
+                                        w.P.main_done));
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;
@@ -2410,7 +2437,7 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
         if (!skip_hs)  // DIAGNOSTIC (FRS_ABLATE=10): measure the chain without the split kernel
             FRS_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_hsplit, ctx->h_stage_src ? ctx->h_stage_src : h, n, d, NP, w.hs,
                                             w.P.rowmax_bits, w.P.w2_bits, xtrace,
-                                            ctx->h_stage_src ? const_cast<float *>(h) : nullptr));
+                                            ctx->h_stage_src ? const_cast<float *>(h) : nullptr, w.P.main_done));
         ++ctx->launches;
     }
     const float inv_t = 1.0f / temperature;
@@ -2452,7 +2479,12 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
     A.fin_ctas = argmax ? 2 : (fin_env == 2 || fin_env == 4 ? fin_env : kFinCtas);  // argmax rows: ~1-3 candidates
     A.fin_stage = argmax ? 4 : kFinStage;
     static const int surv_env = std::getenv("FRS_SURV_EPS") ? std::atoi(std::getenv("FRS_SURV_EPS")) : 0;  // DIAGNOSTIC
-    A.surv_eps = surv_env >= 4 ? surv_env : 16;
+    // survivor window below the row max, in eps: draft rows 16 (the top-k of a flat row spans a
+    // few eps); argmax rows 2: S = {keys >= M - 2 eps - margin} is the top key's own threshold, so
+    // the wider window only added survivors to rank and slab rows to prefetch
+    A.surv_eps = argmax ? 2 : (surv_env >= 4 ? surv_env : 16);
+    static const bool no_flag = std::getenv("FRS_NO_FLAG_SYNC") != nullptr;  // A/B
+    A.flag_sync = no_flag ? 0 : 1;
     return launch_fin(ctx, A, n, s);
 }
 
