@@ -244,6 +244,16 @@ __global__ void __launch_bounds__(512)
             const unsigned long long bits = wr[j0 >> 6];
             const float *Pr = P + (size_t)rr * m + j0;
             int jj = 0;
+            if (nk == 64 && bits == ~0ull) {  // every key of the chunk allowed (the causal context):
+                // the reference adds every product, so no per-key mask test (3x fewer instructions)
+                for (; jj < 64; jj += 8) {
+                    float pr[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) pr[e] = __fmul_rn(Pr[jj + e], svc[(jj + e) * kAttnCols + cc]);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc = __fadd_rn(acc, pr[e]);
+                }
+            }
             for (; jj + 8 <= nk; jj += 8) {  // products ahead of the predicated, key-ordered adds
                 float pr[8];
 #pragma unroll
@@ -1624,8 +1634,10 @@ int launch_masked_attention_strided(frs_ctx *ctx, const float *q, int q_ld, cons
     const size_t smem_s = (size_t)(kAttnRowBlk + kAttnKeyBlk) * pitch * sizeof(float);
     const size_t budget = std::min<size_t>(ctx->smem_optin, 200 * 1024);
     if (smem_s > budget) return fail(FRS_ENOTSUP, "masked_attention: head width above the shared-memory tile");
-    int rows_pv = 16;  // query rows per PV CTA (16 x 32 threads), fewer for long key ranges
-    while (rows_pv > 1 && (size_t)rows_pv * m * 4 + 64 * kAttnCols * 4 > budget) rows_pv >>= 1;
+    // query rows per PV CTA (rows x 32 threads): all of a short batch (no idle row warps at the
+    // barriers), at most 16, fewer for long key ranges
+    int rows_pv = std::min(16, n);
+    while (rows_pv > 1 && (size_t)rows_pv * m * 4 + 64 * kAttnCols * 4 > budget) rows_pv = (rows_pv + 1) / 2;
     // the whole value slice resident (m x 32 floats) when it fits next to the rows' probabilities
     const size_t p_bytes = (((size_t)rows_pv * m + 3) & ~size_t(3)) * 4;
     const int whole = p_bytes + (size_t)m * kAttnCols * 4 <= budget ? 1 : 0;
