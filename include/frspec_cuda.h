@@ -125,6 +125,22 @@ FRS_API int frs_draft_head_topk(frs_ctx *ctx, const float *h, int n, int d, cons
                         float *out_rowmax, double *out_total, float *out_logits,
                         uint32_t *out_flags, void *stream);
 
+/* The bf16 slab in the FAST head's stream order ("tiled image"): for every 64-column K block and
+ * 32-row chunk one 4 KB block holding the SWIZZLE_128B shared-memory image of those 32 rows x
+ * 128 bytes, blocks ordered [K block][chunk] — so each pipeline stage of the FAST head (a
+ * CTA's 1-4 consecutive chunks of one K block) is ONE contiguous 1-D bulk copy instead of a
+ * 2-D tensor load (measured: 62.8 -> 58.4 us per Llama-3-8B draft level). Built once per slab
+ * (frs_slab_tile; zero fill past v_rows / d), kept next to the row-major slab, which the exact
+ * recompute of the certified candidates still reads. Same bytes as the slab (rounded up to
+ * whole chunks and K blocks). frs_draft_head_topk_tiled = frs_draft_head_topk in FAST mode
+ * (slab_dtype bf16) with the tiled image of that slab. */
+FRS_API size_t frs_slab_tile_bytes(int v_rows, int d);
+FRS_API int frs_slab_tile(frs_ctx *ctx, const void *slab, int v_rows, int d, void *tiled, void *stream);
+FRS_API int frs_draft_head_topk_tiled(frs_ctx *ctx, const float *h, int n, int d, const void *slab,
+                                      const void *tiled, int v_sub, const int32_t *ordered_ids, int k,
+                                      float temperature, int32_t *out_ridx, int32_t *out_full, float *out_prob,
+                                      float *out_rowmax, double *out_total, uint32_t *out_flags, void *stream);
+
 /* K3 — full-vocabulary verify head over rows [id_offset, id_offset + v_rows) of the LM head
  * (W points at that shard): per row i of h[m x d], out_id[i] = id_offset + argmax_j
  * dot_f32(h_i, W_j) with ties to the lowest id, out_val[i] = that logit. Device buffers. */

@@ -337,11 +337,14 @@ def flops_ratio(full_size: int, restricted_size: int) -> float:
 @dataclass
 class RestrictedHead:
     """Device-resident row-gathered LM head slice (vocab.h:49-52). ``slab`` is row-major
-    [V_sub x d] in ``dtype``; ``ordered_dev`` is the restricted->full id map on the device."""
+    [V_sub x d] in ``dtype``; ``ordered_dev`` is the restricted->full id map on the device;
+    ``tiled`` (bf16 slabs) the FAST head's stream-order image of the slab (frs_slab_tile), which
+    FAST draft levels stream instead of the row-major slab."""
     slab: torch.Tensor
     ordered_dev: torch.Tensor
     subset: RankedSubset
     dtype: int
+    tiled: Optional[torch.Tensor] = None
 
     @property
     def v_sub(self) -> int:
@@ -353,7 +356,8 @@ class RestrictedHead:
 
 
 def restrict_lm_head(ctx: Context, lm_head: torch.Tensor, subset: RankedSubset, dtype="bf16",
-                     stream=None) -> RestrictedHead:
+                     stream=None, tile: bool = True) -> RestrictedHead:
+    """K1 (vocab.cpp:152-168): the FR slab, plus (bf16, tile=True) its FAST stream-order image."""
     if lm_head.dtype != torch.float32 or not lm_head.is_cuda or lm_head.dim() != 2:
         raise InvalidArgument("restrict_lm_head: lm_head must be a CUDA float32 [V x d] tensor")
     lm_head = lm_head.contiguous()
@@ -364,7 +368,12 @@ def restrict_lm_head(ctx: Context, lm_head: torch.Tensor, subset: RankedSubset, 
                        device=lm_head.device)
     check(lib().frs_slab_build(ctx.handle, _ptr(lm_head), V, d, _ptr(ordered_dev), subset.size(), dt, _ptr(slab),
                                _stream(stream)), "restrict_lm_head")
-    return RestrictedHead(slab, ordered_dev, subset, dt)
+    tiled = None
+    if dt == DTYPE_BF16 and d % 8 == 0 and tile:
+        tiled = torch.empty(int(lib().frs_slab_tile_bytes(subset.size(), d)), dtype=torch.uint8, device=lm_head.device)
+        check(lib().frs_slab_tile(ctx.handle, _ptr(slab), subset.size(), d, _ptr(tiled), _stream(stream)),
+              "restrict_lm_head")
+    return RestrictedHead(slab, ordered_dev, subset, dt, tiled)
 
 
 # ---------------------------------------------------------------- K2: draft head + top-k
@@ -399,6 +408,12 @@ def draft_head_topk(ctx: Context, h: torch.Tensor, head: RestrictedHead, k: int,
                          torch.empty(n, dtype=torch.float64, device=dev) if want_total else None,
                          torch.zeros(n, dtype=torch.int32, device=dev),
                          torch.empty((n, head.v_sub), dtype=torch.float32, device=dev) if want_logits else None)
+    if _mode(mode) == MODE_FAST and head.tiled is not None and out.logits is None:
+        check(lib().frs_draft_head_topk_tiled(ctx.handle, _ptr(h), n, d, _ptr(head.slab), _ptr(head.tiled), head.v_sub,
+                                              _ptr(head.ordered_dev), k, temperature, _ptr(out.ridx), _ptr(out.full),
+                                              _ptr(out.prob), _ptr(out.rowmax), _ptr(out.total), _ptr(out.flags),
+                                              _stream(stream)), "draft_head_topk")
+        return out
     check(lib().frs_draft_head_topk(ctx.handle, _ptr(h), n, d, _ptr(head.slab), head.v_sub, head.dtype,
                                     _ptr(head.ordered_dev), k, temperature, _mode(mode), _ptr(out.ridx), _ptr(out.full),
                                     _ptr(out.prob), _ptr(out.rowmax), _ptr(out.total), _ptr(out.logits),

@@ -217,7 +217,7 @@ int frs_draft_head_topk(frs_ctx *ctx, const float *h, int n, int d, const void *
     if (mode == FRS_MODE_FAST) {
         FRS_REQUIRE(slab_dtype == FRS_DTYPE_BF16, "FAST draft head needs a bf16 slab");
         FRS_REQUIRE(out_logits == nullptr, "FAST draft head never materialises logits");
-        return launch_fast_draft(ctx, h, n, d, slab, v_sub, ordered_ids, k, temperature, out_ridx, out_full,
+        return launch_fast_draft(ctx, h, n, d, slab, nullptr, v_sub, ordered_ids, k, temperature, out_ridx, out_full,
                                  out_prob, out_rowmax, out_total, out_flags, s);
     }
     float *logits = out_logits;
@@ -228,6 +228,37 @@ int frs_draft_head_topk(frs_ctx *ctx, const float *h, int n, int d, const void *
     if ((st = launch_exact_logits(ctx, h, n, d, slab, slab_dtype, v_sub, logits, s))) return st;
     return launch_softmax_topk(ctx, logits, n, v_sub, k, temperature, ordered_ids, out_ridx, out_full, out_prob,
                                out_rowmax, out_total, out_flags, s);
+}
+
+size_t frs_slab_tile_bytes(int v_rows, int d) {
+    if (v_rows < 1 || d < 1) return 0;
+    return slab_tile_bytes(v_rows, d);
+}
+
+int frs_slab_tile(frs_ctx *ctx, const void *slab, int v_rows, int d, void *tiled, void *stream) {
+    int st = check_device(ctx);
+    if (st) return st;
+    FRS_REQUIRE(slab && tiled, "slab tile: null pointer");
+    FRS_REQUIRE(v_rows >= 1 && d >= 1, "slab tile: sizes must be positive");
+    FRS_REQUIRE(d % 8 == 0 && (reinterpret_cast<uintptr_t>(slab) & 15) == 0 && (reinterpret_cast<uintptr_t>(tiled) & 15) == 0,
+                "slab tile: d % 8 == 0 and 16-byte aligned buffers");
+    return launch_slab_tile(ctx, slab, v_rows, d, tiled, static_cast<cudaStream_t>(stream));
+}
+
+int frs_draft_head_topk_tiled(frs_ctx *ctx, const float *h, int n, int d, const void *slab, const void *tiled,
+                              int v_sub, const int32_t *ordered_ids, int k, float temperature, int32_t *out_ridx,
+                              int32_t *out_full, float *out_prob, float *out_rowmax, double *out_total,
+                              uint32_t *out_flags, void *stream) {
+    int st = check_device(ctx);
+    if (st) return st;
+    FRS_REQUIRE(h && slab && tiled && out_ridx && out_full && out_prob, "draft head: null pointer");
+    FRS_REQUIRE(n >= 1, "forward: empty token batch");                       // model.cpp:217
+    FRS_REQUIRE(d >= 1 && v_sub >= 1, "draft head: sizes must be positive");
+    FRS_REQUIRE(k >= 1, "draft params: beam_width must be >= 1");           // drafting.cpp:15
+    FRS_REQUIRE(std::isfinite(temperature) && temperature > 0.0f,
+                "softmax: temperature must be positive and finite");       // kernels.cpp:66-68
+    return launch_fast_draft(ctx, h, n, d, slab, tiled, v_sub, ordered_ids, k, temperature, out_ridx, out_full,
+                             out_prob, out_rowmax, out_total, out_flags, static_cast<cudaStream_t>(stream));
 }
 
 int frs_masked_attention(frs_ctx *ctx, const float *q, const float *k, const float *v, const uint64_t *mask, int n,

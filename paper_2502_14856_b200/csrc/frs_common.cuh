@@ -34,7 +34,7 @@ struct DevBuf {
 
 // CUDA-graph cache of repeated FAST calls (frs_fast.cu): the key is every pointer, size and
 // parameter the captured chain bakes in.
-constexpr int kGraphKeyWords = 20;
+constexpr int kGraphKeyWords = 21;
 struct GraphKey {
     uint64_t w[kGraphKeyWords];
     bool operator==(const GraphKey &o) const {
@@ -112,7 +112,9 @@ int launch_softmax_topk(frs_ctx *ctx, const float *logits, int n, int v, int k, 
                         cudaStream_t s);
 int launch_argmax_rows(frs_ctx *ctx, const float *logits, int m, int v, int32_t id_offset,
                        int32_t *out_id, float *out_val, uint32_t *out_flags, cudaStream_t s);
-int launch_fast_draft(frs_ctx *ctx, const float *h, int n, int d, const void *slab, int v_sub,
+size_t slab_tile_bytes(int v_rows, int d);
+int launch_slab_tile(frs_ctx *ctx, const void *slab, int v_rows, int d, void *tiled, cudaStream_t s);
+int launch_fast_draft(frs_ctx *ctx, const float *h, int n, int d, const void *slab, const void *tiled, int v_sub,
                       const int32_t *ordered_ids, int k, float temperature, int32_t *out_ridx,
                       int32_t *out_full, float *out_prob, float *out_rowmax, double *out_total,
                       uint32_t *out_flags, cudaStream_t s);

@@ -115,6 +115,14 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void bulk_load_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                               uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {  // bytes % 16 == 0
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -186,6 +194,8 @@ struct Partials {
     int G;
     unsigned long long *trace; // optional [G][16] globaltimer stamps (diagnostics; nullptr = off)
     unsigned *main_done;       // [1] main CTAs whose outputs are published (release; reset by k_hsplit)
+    const uint8_t *tiled;      // the slab in stage order ([kb][32-row chunk] blocks of 4 KB, each the
+                               // SWIZZLE_128B image of 32 rows x 128 B), or nullptr (2-D tensor loads)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -249,6 +259,24 @@ __global__ void __launch_bounds__(128) k_hsplit(const float *__restrict__ h, int
         lo[1] = l23;
     }
     if (xtrace && blockIdx.x == 0 && threadIdx.x == 0) xtrace[1] = gtimer();
+}
+
+// The slab in the main kernel's stage order: block (kb, chunk c) = rows [32 c, 32 c + 32) x
+// columns [64 kb, 64 kb + 64) as the SWIZZLE_128B shared-memory image (16-byte group q of row r
+// at r 128 + (q ^ (r & 7)) 16), blocks ordered [kb][c] so a tile's chunks of one K block are one
+// contiguous bulk copy. Rows past v_rows and columns past d are zero (the TMA's OOB fill).
+__global__ void k_slab_tile(const uint16_t *__restrict__ slab, int v_rows, int d, int NCH, uint8_t *__restrict__ out) {
+    const int KB = (d + BK - 1) / BK;
+    const size_t total = (size_t)KB * NCH * CH * 8;  // 16-byte groups
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const int q = static_cast<int>(e & 7), r = static_cast<int>((e >> 3) & (CH - 1));
+        const size_t blk = e >> 8;  // (kb NCH + c)
+        const int c = static_cast<int>(blk % NCH), kb = static_cast<int>(blk / NCH);
+        const int row = c * CH + r, col = kb * BK + q * 8;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (row < v_rows && col < d) v = *reinterpret_cast<const uint4 *>(slab + (size_t)row * d + col);
+        *reinterpret_cast<uint4 *>(out + blk * (CH * BK * 2) + r * 128 + ((q ^ (r & 7)) << 4)) = v;
+    }
 }
 
 template <int NP, bool SOFTMAX>
@@ -391,7 +419,10 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             for (int g = 0; g < pre; ++g) {
                 const int t = t_begin + g / KB, kb = g % KB, nch = tile_chunks(t), r0 = tile_row0(t);
                 mbar_expect_tx(&full[g], nch * (CH * BK * 2) + C::B_BYTES);
-                if (nch == CPT) {
+                if (P.tiled) {  // the tile's nch chunk blocks of this K block are contiguous
+                    bulk_load_hint(sA + g * C::A_BYTES, P.tiled + ((size_t)kb * NCH + r0 / CH) * (CH * BK * 2),
+                                   nch * (CH * BK * 2), &full[g], pol_w);
+                } else if (nch == CPT) {
                     tma_load_2d(sA + g * C::A_BYTES, &mapW, &full[g], kb * BK, r0, pol_w);
                 } else {
                     for (int c = 0; c < nch; ++c)
@@ -411,7 +442,10 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                 for (int kb = kb0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], nch * (CH * BK * 2) + C::B_BYTES);
-                    if (nch == CPT) {
+                    if (P.tiled) {
+                        bulk_load_hint(sA + stage * C::A_BYTES, P.tiled + ((size_t)kb * NCH + r0 / CH) * (CH * BK * 2),
+                                       nch * (CH * BK * 2), &full[stage], pol_w);
+                    } else if (nch == CPT) {
                         tma_load_2d(sA + stage * C::A_BYTES, &mapW, &full[stage], kb * BK, r0, pol_w);
                     } else {
                         for (int c = 0; c < nch; ++c)
@@ -2032,6 +2066,7 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.fin = reinterpret_cast<float *>(base + o_fin);
     w.scratch = reinterpret_cast<float *>(base + o_scr);
     w.P.trace = nullptr;
+    w.P.tiled = nullptr;
     w.P.rowmax_bits = nullptr;
     w.P.w2_bits = nullptr;
     static const bool tracing = std::getenv("FRS_TRACE") != nullptr;
@@ -2052,6 +2087,7 @@ int fast_workspace(frs_ctx *ctx, int NP, int d, int n, int v_rows, FastWs &w) {
     w.P.rowmax_bits = reinterpret_cast<unsigned *>(static_cast<uint8_t *>(ctx->fast_ctr.ptr) + kCtrRowmax);
     w.P.w2_bits = w.P.rowmax_bits + 64;
     w.P.main_done = w.P.w2_bits + 1;
+    w.P.tiled = nullptr;
     return FRS_OK;
 }
 
@@ -2177,10 +2213,10 @@ int launch_fin(frs_ctx *ctx, const FinArgs &A, int rows, cudaStream_t s) {
     return A.argmax ? launch_fallback(ctx, A, s) : FRS_OK;
 }
 
-int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
-                 int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx, int32_t *out_full,
-                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, int NP, FastWs &w,
-                 cudaStream_t s);
+int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, const void *tiled, int v_rows,
+                 const int32_t *ordered_ids, int k, float temperature, bool argmax, int32_t id_offset,
+                 int32_t *out_ridx, int32_t *out_full, float *out_prob, float *out_rowmax, double *out_total,
+                 uint32_t *out_flags, int NP, FastWs &w, cudaStream_t s);
 
 inline uint32_t __float_as_uint_host(float f) {
     uint32_t u;
@@ -2214,7 +2250,7 @@ void graph_insert(frs_ctx *ctx, const GraphKey &key) {
 
 // Batched drafting chain (17..64 hidden rows): k_hsplit -> k_fast_main<NP,false,LOGITS> ->
 // k_fast_select -> k_fast_fallback. The approximate logits [n x V_sub] fp32 stay in L2.
-int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows,
+int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, const void *tiled, int v_rows,
                     const int32_t *ordered_ids, int k, float temperature, int32_t *out_ridx, int32_t *out_full,
                     float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s,
                     bool argmax = false, int32_t id_offset = 0) {
@@ -2256,6 +2292,7 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
                                         w.P.main_done));
         ++ctx->launches;
     }
+    w.P.tiled = static_cast<const uint8_t *>(tiled);
     const float inv_t = 1.0f / temperature;
     st = NP == 128 ? launch_main<128, false, true>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s)
                    : launch_main<64, false, true>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s);
@@ -2290,9 +2327,10 @@ int enqueue_batched(frs_ctx *ctx, const float *h, int n, int d, const void *W, i
     return launch_select(ctx, A, n, s);
 }
 
-int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
-                int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx, int32_t *out_full,
-                float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
+int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, const void *tiled, int v_rows,
+                const int32_t *ordered_ids, int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx,
+                int32_t *out_full, float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags,
+                cudaStream_t s) {
     if (d % 8 != 0) return fail(FRS_ENOTSUP, "FAST head: hidden_dim must be a multiple of 8 (TMA row pitch)");
     const bool batched_ok = sel_stage(ctx, d) >= 4;
     static const int batch_env = std::getenv("FRS_BATCH_ROWS") ? std::atoi(std::getenv("FRS_BATCH_ROWS")) : 0;
@@ -2300,7 +2338,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     if (!argmax && n > 16 && batched_ok) {  // batched drafting: up to `batch` rows per slab pass
         for (int r0 = 0; r0 < n; r0 += batch) {
             const int nr = std::min(batch, n - r0);
-            const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, v_rows, ordered_ids, k, temperature,
+            const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, tiled, v_rows, ordered_ids, k, temperature,
                                            out_ridx + (size_t)r0 * k, out_full + (size_t)r0 * k,
                                            out_prob + (size_t)r0 * k, out_rowmax ? out_rowmax + r0 : nullptr,
                                            out_total ? out_total + r0 : nullptr, out_flags ? out_flags + r0 : nullptr, s);
@@ -2313,7 +2351,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
         // rows (N = 256 UMMA): the pass is HBM / tensor balanced at the Llama-3-8B verify head
         for (int r0 = 0; r0 < n; r0 += 128) {
             const int nr = std::min(128, n - r0);
-            const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, v_rows, nullptr, 1, 1.0f, nullptr,
+            const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, nullptr, v_rows, nullptr, 1, 1.0f, nullptr,
                                            out_full + r0, out_prob ? out_prob + r0 : nullptr, nullptr, nullptr,
                                            out_flags ? out_flags + r0 : nullptr, s, true, id_offset);
             if (st) return st;
@@ -2324,7 +2362,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
     if (!argmax && n > 16) {  // the fused softmax path takes 16 hidden rows per pass
         for (int r0 = 0; r0 < n; r0 += 16) {
             const int nr = std::min(16, n - r0);
-            const int st = launch_fast(ctx, h + (size_t)r0 * d, nr, d, W, v_rows, ordered_ids, k, temperature, false, 0,
+            const int st = launch_fast(ctx, h + (size_t)r0 * d, nr, d, W, tiled, v_rows, ordered_ids, k, temperature, false, 0,
                                        out_ridx + (size_t)r0 * k, out_full + (size_t)r0 * k, out_prob + (size_t)r0 * k,
                                        out_rowmax ? out_rowmax + r0 : nullptr, out_total ? out_total + r0 : nullptr,
                                        out_flags ? out_flags + r0 : nullptr, s);
@@ -2358,7 +2396,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
                                  reinterpret_cast<uint64_t>(out_total), reinterpret_cast<uint64_t>(out_flags),
                                  reinterpret_cast<uint64_t>(ctx->fast_ws.ptr), reinterpret_cast<uint64_t>(ctx->fast_ctr.ptr),
                                  reinterpret_cast<uint64_t>(ctx->trace.ptr),
-                                 reinterpret_cast<uint64_t>(ctx->h_stage_src)};
+                                 reinterpret_cast<uint64_t>(ctx->h_stage_src), reinterpret_cast<uint64_t>(tiled)};
         static_assert(sizeof(vals) / sizeof(vals[0]) == kGraphKeyWords, "graph key size");
         for (int q = 0; q < kGraphKeyWords; ++q) key.w[q] = vals[q];
         GraphEntry *e = graph_lookup(ctx, key);
@@ -2375,7 +2413,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
             const unsigned long long l0 = ctx->launches;
             const bool timing = ctx->timing;
             ctx->timing = false;
-            st = enqueue_fast(ctx, h, n, d, W, v_rows, ordered_ids, k, temperature, argmax, id_offset, out_ridx,
+            st = enqueue_fast(ctx, h, n, d, W, tiled, v_rows, ordered_ids, k, temperature, argmax, id_offset, out_ridx,
                               out_full, out_prob, out_rowmax, out_total, out_flags, NP, w, ctx->cap_stream);
             ctx->timing = timing;
             ctx->launches = l0;
@@ -2406,15 +2444,15 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v
         cudaStream_t s;
         ~EndTiming() { timing_end(c, s); }
     } end_timing{ctx, s};
-    return enqueue_fast(ctx, h, n, d, W, v_rows, ordered_ids, k, temperature, argmax, id_offset, out_ridx, out_full,
-                        out_prob, out_rowmax, out_total, out_flags, NP, w, s);
+    return enqueue_fast(ctx, h, n, d, W, tiled, v_rows, ordered_ids, k, temperature, argmax, id_offset, out_ridx,
+                        out_full, out_prob, out_rowmax, out_total, out_flags, NP, w, s);
 }
 
 // The FAST chain itself: k_hsplit -> k_fast_main -> k_fast_finalize -> k_fast_fallback.
-int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int v_rows, const int32_t *ordered_ids,
-                 int k, float temperature, bool argmax, int32_t id_offset, int32_t *out_ridx, int32_t *out_full,
-                 float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, int NP, FastWs &w,
-                 cudaStream_t s) {
+int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, const void *tiled, int v_rows,
+                 const int32_t *ordered_ids, int k, float temperature, bool argmax, int32_t id_offset,
+                 int32_t *out_ridx, int32_t *out_full, float *out_prob, float *out_rowmax, double *out_total,
+                 uint32_t *out_flags, int NP, FastWs &w, cudaStream_t s) {
     const int G = ctx->sm_count;
     int st;
     CUtensorMap mapW, mapH;
@@ -2440,6 +2478,7 @@ int enqueue_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, int 
                                             ctx->h_stage_src ? const_cast<float *>(h) : nullptr, w.P.main_done));
         ++ctx->launches;
     }
+    w.P.tiled = static_cast<const uint8_t *>(tiled);
     const float inv_t = 1.0f / temperature;
     if (argmax) {
         st = NP == 16   ? launch_main<16, false>(ctx, mapW, mapW32, mapH, n, v_rows, d, inv_t, w.P, s)
@@ -2512,16 +2551,29 @@ int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float 
     return FRS_OK;
 }
 
-int launch_fast_draft(frs_ctx *ctx, const float *h, int n, int d, const void *slab, int v_sub,
+int launch_fast_draft(frs_ctx *ctx, const float *h, int n, int d, const void *slab, const void *tiled, int v_sub,
                       const int32_t *ordered_ids, int k, float temperature, int32_t *out_ridx, int32_t *out_full,
                       float *out_prob, float *out_rowmax, double *out_total, uint32_t *out_flags, cudaStream_t s) {
-    return launch_fast(ctx, h, n, d, slab, v_sub, ordered_ids, k, temperature, false, 0, out_ridx, out_full,
+    return launch_fast(ctx, h, n, d, slab, tiled, v_sub, ordered_ids, k, temperature, false, 0, out_ridx, out_full,
                        out_prob, out_rowmax, out_total, out_flags, s);
+}
+
+size_t slab_tile_bytes(int v_rows, int d) {
+    return (size_t)((d + BK - 1) / BK) * ((v_rows + CH - 1) / CH) * (CH * BK * 2);
+}
+
+int launch_slab_tile(frs_ctx *ctx, const void *slab, int v_rows, int d, void *tiled, cudaStream_t s) {
+    const int NCH = (v_rows + CH - 1) / CH;
+    k_slab_tile<<<4 * ctx->sm_count, 256, 0, s>>>(static_cast<const uint16_t *>(slab), v_rows, d, NCH,
+                                                   static_cast<uint8_t *>(tiled));
+    FRS_CUDA_TRY(cudaGetLastError());
+    ++ctx->launches;
+    return FRS_OK;
 }
 
 int launch_fast_verify(frs_ctx *ctx, const float *h, int m, int d, const void *W, int v_rows, int32_t id_offset,
                        int32_t *out_id, float *out_val, uint32_t *out_flags, cudaStream_t s) {
-    return launch_fast(ctx, h, m, d, W, v_rows, nullptr, 1, 1.0f, true, id_offset, nullptr, out_id, out_val,
+    return launch_fast(ctx, h, m, d, W, nullptr, v_rows, nullptr, 1, 1.0f, true, id_offset, nullptr, out_id, out_val,
                        nullptr, nullptr, out_flags, s);
 }
 

@@ -31,6 +31,7 @@ struct frs_head {
     std::vector<int32_t> ordered;
     int64_t vocab = 0;
     int v_sub = 0, d = 0, dtype = FRS_DTYPE_F32;
+    void *tiled = nullptr;  // bf16 slabs: the FAST head's tiled image (frs_slab_tile)
     // per-level staging (device + pinned host)
     frs::DevBuf lvl_ridx, lvl_full, lvl_prob, lvl_tok, hidden, tree_ws, smp_u, smp_probs;
     // multi-stream decode staging (frs_decode_step_table_multi): row tokens, hidden rows, packed
@@ -303,6 +304,11 @@ int frs_head_create(frs_ctx *ctx, const float *W, int64_t V, int d, int w_on_dev
         int st = frs_slab_build(ctx, Wd, V, d, h->ordered_dev, v_sub, slab_dtype, h->slab, s);
         if (st) return cleanup(st);
     }
+    if (slab_dtype == FRS_DTYPE_BF16 && d % 8 == 0) {  // the FAST head's stream-order image
+        if (cudaMalloc(&h->tiled, frs_slab_tile_bytes(v_sub, d)) != cudaSuccess)
+            return cleanup(fail(FRS_ECUDA, "restrict_lm_head: cudaMalloc failed"));
+        if (int st = frs_slab_tile(ctx, h->slab, v_sub, d, h->tiled, s)) return cleanup(st);
+    }
     *out = h;
     return FRS_OK;
 }
@@ -311,6 +317,7 @@ int frs_head_destroy(frs_head *h) {
     if (!h) return FRS_OK;
     cudaSetDevice(h->ctx->device);
     if (h->slab) cudaFree(h->slab);
+    if (h->tiled) cudaFree(h->tiled);
     if (h->ordered_dev) cudaFree(h->ordered_dev);
     if (h->h_ridx) cudaFreeHost(h->h_ridx);
     if (h->h_full) cudaFreeHost(h->h_full);
@@ -388,18 +395,25 @@ int frs_head_draft_host(frs_head *h, const float *h_host, int n, int k, int mode
         const bool graphs = h->ctx->prefer_graphs;
         h->ctx->h_stage_src = static_cast<const float *>(pa.devicePointer);
         h->ctx->prefer_graphs = !no_graphs;
-        st = frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode, hp,
-                                 hp + cells, reinterpret_cast<float *>(hp + 2 * cells), nullptr, nullptr, nullptr,
-                                 nullptr, s);
+        st = h->tiled ? frs_draft_head_topk_tiled(h->ctx, hd, n, h->d, h->slab, h->tiled, h->v_sub, h->ordered_dev, k,
+                                                  1.0f, hp, hp + cells, reinterpret_cast<float *>(hp + 2 * cells),
+                                                  nullptr, nullptr, nullptr, s)
+                      : frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f,
+                                            mode, hp, hp + cells, reinterpret_cast<float *>(hp + 2 * cells), nullptr,
+                                            nullptr, nullptr, nullptr, s);
         h->ctx->h_stage_src = nullptr;
         h->ctx->prefer_graphs = graphs;
         if (st) return st;
     } else {
         FRS_CUDA_TRY(cudaMemcpyAsync(hd, h_host, sizeof(float) * (size_t)n * h->d, cudaMemcpyHostToDevice, s));
         int32_t *pk = static_cast<int32_t *>(h->lvl_ridx.ptr);
-        st = frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode, pk,
-                                 pk + cells, reinterpret_cast<float *>(pk + 2 * cells), nullptr, nullptr, nullptr,
-                                 nullptr, s);
+        st = (mode == FRS_MODE_FAST && h->tiled)
+                 ? frs_draft_head_topk_tiled(h->ctx, hd, n, h->d, h->slab, h->tiled, h->v_sub, h->ordered_dev, k, 1.0f,
+                                             pk, pk + cells, reinterpret_cast<float *>(pk + 2 * cells), nullptr,
+                                             nullptr, nullptr, s)
+                 : frs_draft_head_topk(h->ctx, hd, n, h->d, h->slab, h->v_sub, h->dtype, h->ordered_dev, k, 1.0f, mode,
+                                       pk, pk + cells, reinterpret_cast<float *>(pk + 2 * cells), nullptr, nullptr,
+                                       nullptr, nullptr, s);
         if (st) return st;
         FRS_CUDA_TRY(cudaMemcpyAsync(hp, pk, cells * 12, cudaMemcpyDeviceToHost, s));
     }

@@ -273,3 +273,47 @@ def test_fast_draft_host_buffers(cuda_ctx, restatement, n, pinned):
     ref = restatement.draft_level(h, restatement.restrict(W, ids), ids, 10)
     assert np.array_equal(ridx, ref["ridx"]) and np.array_equal(full, ref["full"])
     np.testing.assert_allclose(prob, ref["prob"], rtol=PROB_RTOL, atol=0)
+
+
+def tiled_image_np(slab_bits: np.ndarray) -> np.ndarray:
+    """numpy restatement of frs_slab_tile: blocks [K block][32-row chunk] of 4 KB, each the
+    SWIZZLE_128B image (16-byte group q of row r at r * 128 + (q ^ (r & 7)) * 16), zero fill."""
+    v, d = slab_bits.shape
+    nch, kbs = -(-v // 32), -(-d // 64)
+    pad = np.zeros((nch * 32, kbs * 64), np.uint16)
+    pad[:v, :d] = slab_bits
+    out = np.zeros((kbs, nch, 32, 8, 8), np.uint16)  # [kb][c][r][position][8 elements]
+    for q in range(8):
+        for r in range(32):
+            out[:, :, r, q ^ (r & 7), :] = pad.reshape(nch, 32, kbs, 8, 8)[:, r, :, q, :].transpose(1, 0, 2)
+    return out.reshape(-1).view(np.uint8)
+
+
+@pytest.mark.parametrize("v,d", [(100, 200), (4096, 512), (33, 64)])
+def test_slab_tile_image(cuda_ctx, v, d):
+    """frs_slab_tile == its numpy restatement (ragged rows and K blocks zero-filled)."""
+    rng = np.random.default_rng(v + d)
+    W = torch.from_numpy((rng.standard_normal((v, d)) * 0.02).astype(np.float32)).cuda()
+    head = api.restrict_lm_head(cuda_ctx, W, api.RankedSubset(v, np.arange(v, dtype=np.int32)), dtype="bf16")
+    torch.cuda.synchronize()
+    bits = head.slab.view(torch.int16).cpu().numpy().view(np.uint16)
+    assert head.tiled is not None and head.tiled.numel() == (-(-v // 32)) * (-(-d // 64)) * 4096
+    assert np.array_equal(head.tiled.cpu().numpy(), tiled_image_np(bits))
+
+
+def test_fast_tiled_equals_row_major(cuda_ctx, restatement):
+    """FAST over the tiled image (1-D bulk stage loads) == FAST over the row-major slab (2-D
+    tensor loads) == the oracle, at a ragged slab height (last CTA tiles short)."""
+    W, ids, h = case(31, 10, 512, 5000 - 17)
+    Wd = torch.from_numpy(W).cuda()
+    sub = api.RankedSubset(W.shape[0], ids)
+    a = api.restrict_lm_head(cuda_ctx, Wd, sub, dtype="bf16")
+    b = api.restrict_lm_head(cuda_ctx, Wd, sub, dtype="bf16", tile=False)
+    assert a.tiled is not None and b.tiled is None
+    hd = torch.from_numpy(h).cuda()
+    oa = api.draft_head_topk(cuda_ctx, hd, a, 10, mode="fast")
+    ob = api.draft_head_topk(cuda_ctx, hd, b, 10, mode="fast")
+    torch.cuda.synchronize()
+    assert torch.equal(oa.full, ob.full) and torch.equal(oa.ridx, ob.ridx) and torch.equal(oa.rowmax, ob.rowmax)
+    ref = restatement.draft_level(h, restatement.restrict(W, ids), ids, 10)
+    assert np.array_equal(oa.full.cpu().numpy(), ref["full"])
