@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--rows", type=int, default=10)
     ap.add_argument("--d", type=int, default=4096)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--verify", action="store_true", help="trace the argmax (verify) chain over a [v_sub x d] shard")
     a = ap.parse_args()
     assert os.environ.get("FRS_TRACE"), "set FRS_TRACE=1"
     dev = torch.device("cuda", 0)
@@ -49,11 +50,19 @@ def main():
     W = (torch.randn(a.v_sub, a.d, generator=g, device=dev) * 0.02).float()
     head = api.restrict_lm_head(ctx, W, api.RankedSubset(a.v_sub, np.arange(a.v_sub)), dtype="bf16")
     h = torch.randn(a.rows, a.d, generator=g, device=dev)
-    out = api.draft_head_topk(ctx, h, head, 10, mode="fast")
+    if a.verify:  # the verify head over a shard: W itself (bf16 values), argmax per row
+        Wb = head.slab
+        call = lambda: api.verify_head_argmax(ctx, h, Wb, mode="fast")  # noqa: E731
+    else:
+        call = None
+    out = api.draft_head_topk(ctx, h, head, 10, mode="fast") if not a.verify else None
     G = ctx.sm_count
     res = []
     for _ in range(a.reps):
-        api.draft_head_topk(ctx, h, head, 10, mode="fast", out=out)
+        if call:
+            call()
+        else:
+            api.draft_head_topk(ctx, h, head, 10, mode="fast", out=out)
         torch.cuda.synchronize()
         n = a.rows
         L = 4 * G
@@ -89,8 +98,8 @@ def main():
                 us = (v - t0) / 1000.0
                 row[f"{s:02d} {name}"] = [round(float(us.min()), 2), round(float(np.median(us)), 2),
                                           round(float(us.max()), 2)]
-        for s, name in (SSLOTS if n > 16 else FSLOTS).items():
-            v = ft[::8, s] if n > 16 else ft[:, s]
+        for s, name in (SSLOTS if n > 16 and not a.verify else FSLOTS).items():
+            v = ft[::8, s] if n > 16 and not a.verify else ft[:, s]
             v = v[v > 0]
             if v.size:
                 us = (v - t0) / 1000.0
@@ -102,7 +111,7 @@ def main():
                         12: "fb row0: top-k done"}.items():
             if xt[s_] > 0:
                 row[f"X{s_} {name}"] = round(float((xt[s_] - t0) / 1000.0), 2)
-        if n > 16:  # batched path: k_fast_select stamps (row i at [i*8]); slot 8 = |S| | robust << 32
+        if n > 16 and not a.verify:  # batched path: k_fast_select stamps (row i at [i*8]); slot 8 = |S| | robust << 32
             sel8 = ft[::8, 8][:n]
             row["select |S| (min/med/max)"] = [int((sel8 & 0xffffffff).min()), int(np.median(sel8 & 0xffffffff)),
                                                int((sel8 & 0xffffffff).max())]
