@@ -566,7 +566,8 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
             const int row = tile_row0(t) + q * 32 + lane;
             const bool valid = q * 32 + lane < tile_rows(t);
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * N);
-            constexpr int CG = RPW < 16 ? RPW : 16;  // hidden rows per TMEM load group
+            // hidden rows per TMEM load group (8 for the 32-row argmax warps: 16 spilled registers at NP = 64)
+            constexpr int CG = RPW < 16 ? RPW : (TOPK == 1 && RPW > 16 ? 8 : 16);
 #pragma unroll
             for (int cg = 0; cg < RPW / CG; ++cg) {
                 const int c0 = cbase + cg * CG;
@@ -654,6 +655,44 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
         if (kDiag && P.trace && threadIdx.x == 128) P.trace[(size_t)blockIdx.x * kTrMain + 6] = static_cast<unsigned long long>(clock64() - c_pub0);
         constexpr int SLOT = C::SCRATCH_PER_WARP;
         uint8_t *scr = sA + we * SLOT;
+        if constexpr (TOPK == 1) {
+            // argmax lists (one key per lane and row): ONE pass over every row of the warp —
+            // lane r collects row r's 32 lane keys and bounds (rotation-skewed [source lane][row]
+            // layout: conflict-free reads) and keeps the top R + 1 by insertion (the 4-lane
+            // merges of the pass loop below ran RPW / 8 passes: ~4 us per verify call at NP = 64)
+            static_assert(RPW <= 32 && 32 * RPW * 12 <= C::SCRATCH_PER_WARP, "one-pass argmax publish scratch");
+            unsigned long long *sk1 = reinterpret_cast<unsigned long long *>(scr);  // [32][RPW]
+            float *sb1 = reinterpret_cast<float *>(scr + 32 * RPW * 8);           // [32][RPW]
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) {
+                const int c = lane * RPW + ((r + lane) & (RPW - 1));
+                sk1[c] = b1[r];
+                sb1[c] = bnd[r];
+            }
+            __syncwarp();
+            if (lane < nv) {
+                const int r = lane, i = 2 * r + half;
+                unsigned long long t0 = 0ull, t1 = 0ull, t2 = 0ull, t3 = 0ull;
+                float bmx = kNegInf;
+#pragma unroll 8
+                for (int src = 0; src < 32; ++src) {
+                    const int c = src * RPW + ((r + src) & (RPW - 1));
+                    const unsigned long long k = sk1[c];
+                    bmx = fmaxf(bmx, sb1[c]);
+                    // insert k into t0 >= t1 >= t2 >= t3 (keys are distinct or 0)
+                    const unsigned long long m0 = k > t0 ? k : t0, r0 = k > t0 ? t0 : k;
+                    const unsigned long long m1 = r0 > t1 ? r0 : t1, r1 = r0 > t1 ? t1 : r0;
+                    const unsigned long long m2 = r1 > t2 ? r1 : t2, r2 = r1 > t2 ? t2 : r1;
+                    t3 = r2 > t3 ? r2 : t3;
+                    t0 = m0, t1 = m1, t2 = m2;
+                }
+                const unsigned long long top[R] = {t0, t1, t2};
+#pragma unroll
+                for (int z = 0; z < R; ++z) P.pkey[((size_t)i * L + list) * R + z] = top[z];
+                P.pth[(size_t)i * L + list] = fmaxf(t3 ? dev::key_value(t3) : kNegInf, bmx);
+                if (t0) atomicMax(&s_rmax[i], static_cast<unsigned>(t0 >> 32));
+            }
+        } else {
         // per pass of 8 rows, lane-major with odd strides: the 8 rows a reader instruction
         // touches sit in distinct banks (row-major [row][lane] made every merge load 8-way
         // bank-conflicted)
@@ -746,6 +785,7 @@ __global__ void __launch_bounds__(MainCfg<NP, SOFTMAX>::THREADS, 1)
                 }
             }
         }
+        }  // TOPK == 2
         if (kDiag && P.trace && threadIdx.x == 128) P.trace[(size_t)blockIdx.x * kTrMain + 31] = static_cast<unsigned long long>(clock64() - c_pub0);
         }  // !LOGITS
         if (threadIdx.x == 128) FRS_TRACE(P, 18);

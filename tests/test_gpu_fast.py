@@ -301,10 +301,12 @@ def test_slab_tile_image(cuda_ctx, v, d):
     assert np.array_equal(head.tiled.cpu().numpy(), tiled_image_np(bits))
 
 
-def test_fast_tiled_equals_row_major(cuda_ctx, restatement):
+@pytest.mark.parametrize("n,d,v_sub", [(10, 512, 5000 - 17), (7, 200, 3001), (16, 4096, 32768)])
+def test_fast_tiled_equals_row_major(cuda_ctx, restatement, n, d, v_sub):
     """FAST over the tiled image (1-D bulk stage loads) == FAST over the row-major slab (2-D
-    tensor loads) == the oracle, at a ragged slab height (last CTA tiles short)."""
-    W, ids, h = case(31, 10, 512, 5000 - 17)
+    tensor loads) == the oracle: a ragged slab height (short last tiles), a hidden size that is
+    not a multiple of the 64-column K block (zero-filled image columns), the Llama-3-8B shape."""
+    W, ids, h = case(31, n, d, v_sub)
     Wd = torch.from_numpy(W).cuda()
     sub = api.RankedSubset(W.shape[0], ids)
     a = api.restrict_lm_head(cuda_ctx, Wd, sub, dtype="bf16")
@@ -313,6 +315,7 @@ def test_fast_tiled_equals_row_major(cuda_ctx, restatement):
     hd = torch.from_numpy(h).cuda()
     oa = api.draft_head_topk(cuda_ctx, hd, a, 10, mode="fast")
     ob = api.draft_head_topk(cuda_ctx, hd, b, 10, mode="fast")
+    assert not (oa.flags.cpu().numpy() & FLAG_UNCERTIFIED).any()
     torch.cuda.synchronize()
     assert torch.equal(oa.full, ob.full) and torch.equal(oa.ridx, ob.ridx) and torch.equal(oa.rowmax, ob.rowmax)
     ref = restatement.draft_level(h, restatement.restrict(W, ids), ids, 10)
