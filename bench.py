@@ -482,18 +482,21 @@ def main():
         for G in (1, 2, 4, 8):
             st_, cnt_ = api.vocab_shard(qV, G, G - 1)
             Ws = Wfull[st_:st_ + cnt_]
+            # the shard's tiled image (built once per shard, like the draft slab's): FAST streams it
+            Wt = api.tile_image(ctx, Ws) if mode == "fast" and Ws.dtype == torch.bfloat16 else None
             for _ in range(5):
-                api.verify_head_argmax(ctx, hq1, Ws, id_offset=st_, mode=mode)
+                api.verify_head_argmax(ctx, hq1, Ws, id_offset=st_, mode=mode, W_tiled=Wt)
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record()
             for _ in range(50):
-                api.verify_head_argmax(ctx, hq1, Ws, id_offset=st_, mode=mode)
+                api.verify_head_argmax(ctx, hq1, Ws, id_offset=st_, mode=mode, W_tiled=Wt)
             s1.record()
             torch.cuda.synchronize()
             us = s0.elapsed_time(s1) * 1000.0 / 50
             b = cnt_ * qd * 2 + qm * qd * 4
             verify_shards.append({"G": G, "shard_rows": cnt_, "us_per_call": us, "GBps": b / us / 1e3,
-                                  "frac_of_peak": b / us / 1e3 / hbm_peak})
+                                  "frac_of_peak": b / us / 1e3 / hbm_peak, "tiled_image": Wt is not None})
+            del Wt
         del Wfull
 
     # C5 (BASELINE configs[4]) per level: 256 streams x 10 beam rows = 2560 hidden rows in one FAST

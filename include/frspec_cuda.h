@@ -147,6 +147,11 @@ FRS_API int frs_draft_head_topk_tiled(frs_ctx *ctx, const float *h, int n, int d
 FRS_API int frs_verify_head_argmax(frs_ctx *ctx, const float *h, int m, int d, const void *W, int v_rows,
                            int w_dtype, int32_t id_offset, int mode, int32_t *out_id,
                            float *out_val, uint32_t *out_flags, void *stream);
+/* frs_verify_head_argmax in FAST mode over a bf16 shard W with its tiled image W_tiled
+ * (frs_slab_tile(ctx, W, v_rows, d, W_tiled, …)): the shard streams as 1-D bulk copies. */
+FRS_API int frs_verify_head_argmax_tiled(frs_ctx *ctx, const float *h, int m, int d, const void *W,
+                                         const void *W_tiled, int v_rows, int32_t id_offset, int32_t *out_id,
+                                         float *out_val, uint32_t *out_flags, void *stream);
 
 /* K4 — greedy accept walk (verification.cpp:42-71). argmax_ids[0] belongs to the root
  * position, argmax_ids[1+i] to draft node i. Writes out_emitted[<=k+1], out_path[<=k] and

@@ -73,6 +73,7 @@ SIGNATURES = [
     ("frs_slab_tile_bytes", C.c_size_t, [_I, _I]),
     ("frs_slab_tile", _I, [_P, _P, _I, _I, _P, _P]),
     ("frs_draft_head_topk_tiled", _I, [_P, _P, _I, _I, _P, _P, _I, _P, _I, _F, _P, _P, _P, _P, _P, _P, _P]),
+    ("frs_verify_head_argmax_tiled", _I, [_P, _P, _I, _I, _P, _P, _I, _I, _P, _P, _P, _P]),
     ("frs_verify_head_argmax", _I, [_P, _P, _I, _I, _P, _I, _I, C.c_int32, _I, _P, _P, _P, _P]),
     ("frs_accept_greedy", _I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
     ("frs_argmax_merge", _I, [_P, _P, _P, _I, _I, _P, _P, _P]),

@@ -422,9 +422,19 @@ def draft_head_topk(ctx: Context, h: torch.Tensor, head: RestrictedHead, k: int,
 
 
 # ---------------------------------------------------------------- K3/K4/K5
+def tile_image(ctx: Context, W: torch.Tensor, stream=None) -> torch.Tensor:
+    """The FAST heads' stream-order image of a CUDA bf16 [rows x d] matrix (frs_slab_tile)."""
+    if W.dtype != torch.bfloat16 or not W.is_cuda or W.dim() != 2 or not W.is_contiguous():
+        raise InvalidArgument("slab tile: W must be a contiguous CUDA bf16 [rows x d] tensor")
+    img = torch.empty(int(lib().frs_slab_tile_bytes(W.shape[0], W.shape[1])), dtype=torch.uint8, device=W.device)
+    check(lib().frs_slab_tile(ctx.handle, _ptr(W), W.shape[0], W.shape[1], _ptr(img), _stream(stream)), "slab_tile")
+    return img
+
+
 def verify_head_argmax(ctx: Context, h: torch.Tensor, W: torch.Tensor, id_offset: int = 0, mode="exact",
-                       stream=None):
-    """Per-row argmax of h . W^T with ties to the lowest id; W is a CUDA fp32/bf16 shard."""
+                       stream=None, W_tiled: Optional[torch.Tensor] = None):
+    """Per-row argmax of h . W^T with ties to the lowest id; W is a CUDA fp32/bf16 shard. FAST mode
+    with W_tiled (tile_image(ctx, W)) streams the shard's tiled image."""
     h = h.contiguous()
     m, d = h.shape
     if W.dim() != 2 or W.shape[1] != d:
@@ -433,6 +443,11 @@ def verify_head_argmax(ctx: Context, h: torch.Tensor, W: torch.Tensor, id_offset
     ids = torch.empty(m, dtype=torch.int32, device=h.device)
     vals = torch.empty(m, dtype=torch.float32, device=h.device)
     flags = torch.zeros(m, dtype=torch.int32, device=h.device)
+    if W_tiled is not None and _mode(mode) == MODE_FAST and dt == DTYPE_BF16:
+        check(lib().frs_verify_head_argmax_tiled(ctx.handle, _ptr(h), m, d, _ptr(W), _ptr(W_tiled), W.shape[0],
+                                                 id_offset, _ptr(ids), _ptr(vals), _ptr(flags), _stream(stream)),
+              "verify_head_argmax")
+        return ids, vals, flags
     check(lib().frs_verify_head_argmax(ctx.handle, _ptr(h), m, d, _ptr(W), W.shape[0], dt, id_offset, _mode(mode),
                                        _ptr(ids), _ptr(vals), _ptr(flags), _stream(stream)), "verify_head_argmax")
     return ids, vals, flags

@@ -307,12 +307,24 @@ int frs_verify_head_argmax(frs_ctx *ctx, const float *h, int m, int d, const voi
     FRS_REQUIRE(mode == FRS_MODE_EXACT || mode == FRS_MODE_FAST, "verify head: unknown mode");
     if (mode == FRS_MODE_FAST) {
         FRS_REQUIRE(w_dtype == FRS_DTYPE_BF16, "FAST verify head needs a bf16 LM head");
-        return launch_fast_verify(ctx, h, m, d, W, v_rows, id_offset, out_id, out_val, out_flags, s);
+        return launch_fast_verify(ctx, h, m, d, W, nullptr, v_rows, id_offset, out_id, out_val, out_flags, s);
     }
     if ((st = ctx->logits.ensure((size_t)m * v_rows * sizeof(float)))) return st;
     float *logits = static_cast<float *>(ctx->logits.ptr);
     if ((st = launch_exact_logits(ctx, h, m, d, W, w_dtype, v_rows, logits, s))) return st;
     return launch_argmax_rows(ctx, logits, m, v_rows, id_offset, out_id, out_val, out_flags, s);
+}
+
+int frs_verify_head_argmax_tiled(frs_ctx *ctx, const float *h, int m, int d, const void *W, const void *W_tiled,
+                                 int v_rows, int32_t id_offset, int32_t *out_id, float *out_val, uint32_t *out_flags,
+                                 void *stream) {
+    int st = check_device(ctx);
+    if (st) return st;
+    FRS_REQUIRE(h && W && W_tiled && out_id, "verify head: null pointer");
+    FRS_REQUIRE(m >= 1, "forward: empty token batch");
+    FRS_REQUIRE(d >= 1 && v_rows >= 1, "argmax: empty input");               // kernels.cpp:114-116
+    return launch_fast_verify(ctx, h, m, d, W, W_tiled, v_rows, id_offset, out_id, out_val, out_flags,
+                              static_cast<cudaStream_t>(stream));
 }
 
 int frs_accept_greedy(frs_ctx *ctx, const int32_t *argmax_ids, const int32_t *tokens, const int32_t *parents,

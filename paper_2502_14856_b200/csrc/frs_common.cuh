@@ -120,7 +120,7 @@ int launch_fast_draft(frs_ctx *ctx, const float *h, int n, int d, const void *sl
                       uint32_t *out_flags, cudaStream_t s);
 int debug_fast_partials(frs_ctx *ctx, int n, int d, float *pm, float *ps, float *pth, unsigned long long *pkey,
                         float *pw2);
-int launch_fast_verify(frs_ctx *ctx, const float *h, int m, int d, const void *W, int v_rows,
+int launch_fast_verify(frs_ctx *ctx, const float *h, int m, int d, const void *W, const void *tiled, int v_rows,
                        int32_t id_offset, int32_t *out_id, float *out_val, uint32_t *out_flags,
                        cudaStream_t s);
 

@@ -2391,7 +2391,7 @@ int launch_fast(frs_ctx *ctx, const float *h, int n, int d, const void *W, const
         // rows (N = 256 UMMA): the pass is HBM / tensor balanced at the Llama-3-8B verify head
         for (int r0 = 0; r0 < n; r0 += 128) {
             const int nr = std::min(128, n - r0);
-            const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, nullptr, v_rows, nullptr, 1, 1.0f, nullptr,
+            const int st = enqueue_batched(ctx, h + (size_t)r0 * d, nr, d, W, tiled, v_rows, nullptr, 1, 1.0f, nullptr,
                                            out_full + r0, out_prob ? out_prob + r0 : nullptr, nullptr, nullptr,
                                            out_flags ? out_flags + r0 : nullptr, s, true, id_offset);
             if (st) return st;
@@ -2611,9 +2611,9 @@ int launch_slab_tile(frs_ctx *ctx, const void *slab, int v_rows, int d, void *ti
     return FRS_OK;
 }
 
-int launch_fast_verify(frs_ctx *ctx, const float *h, int m, int d, const void *W, int v_rows, int32_t id_offset,
-                       int32_t *out_id, float *out_val, uint32_t *out_flags, cudaStream_t s) {
-    return launch_fast(ctx, h, m, d, W, nullptr, v_rows, nullptr, 1, 1.0f, true, id_offset, nullptr, out_id, out_val,
+int launch_fast_verify(frs_ctx *ctx, const float *h, int m, int d, const void *W, const void *tiled, int v_rows,
+                       int32_t id_offset, int32_t *out_id, float *out_val, uint32_t *out_flags, cudaStream_t s) {
+    return launch_fast(ctx, h, m, d, W, tiled, v_rows, nullptr, 1, 1.0f, true, id_offset, nullptr, out_id, out_val,
                        nullptr, nullptr, out_flags, s);
 }
 

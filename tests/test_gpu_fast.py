@@ -320,3 +320,21 @@ def test_fast_tiled_equals_row_major(cuda_ctx, restatement, n, d, v_sub):
     assert torch.equal(oa.full, ob.full) and torch.equal(oa.ridx, ob.ridx) and torch.equal(oa.rowmax, ob.rowmax)
     ref = restatement.draft_level(h, restatement.restrict(W, ids), ids, 10)
     assert np.array_equal(oa.full.cpu().numpy(), ref["full"])
+
+
+@pytest.mark.parametrize("m", [7, 61, 130])
+def test_fast_verify_tiled_equals_row_major(cuda_ctx, restatement, m):
+    """frs_verify_head_argmax_tiled (the shard's tiled image) == the 2-D tensor path == the
+    oracle's argmax, for list-path (<= 64 rows) and batched (> 64 rows) calls, with an id offset."""
+    rng = np.random.default_rng(m)
+    V, d = 9000 + 13, 256
+    W = torch.from_numpy((rng.standard_normal((V, d)) * 0.02).astype(np.float32)).to(torch.bfloat16)
+    h = rmsnorm(rng.standard_normal((m, d)))
+    Wd, hd = W.cuda(), torch.from_numpy(h).cuda()
+    Wt = api.tile_image(cuda_ctx, Wd)
+    a, va, _ = api.verify_head_argmax(cuda_ctx, hd, Wd, id_offset=50, mode="fast", W_tiled=Wt)
+    b, vb, _ = api.verify_head_argmax(cuda_ctx, hd, Wd, id_offset=50, mode="fast")
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(va, vb)
+    rid, _ = restatement.verify_argmax(h, W.float().numpy())
+    assert np.array_equal(a.cpu().numpy(), rid + 50)
