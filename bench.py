@@ -325,6 +325,33 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # C3 (BASELINE configs[2]): the V_sub sweep at the Llama-3-8B shape, FAST draft level back to
+    # back; slabs below 4x L2 rotate over copies so every step streams from HBM. Run right after
+    # the headline, before the verify / decode sections' multi-GB allocations
+    vsub_sweep = None
+    if not args.no_sweep and mode == "fast":
+        vsub_sweep = []
+        for vs in (8192, 16384, 32768, 65536, 128256):
+            sub = api.subset_from_ranking(np.random.default_rng(1234).permutation(V).astype(np.int32), vs, V,
+                                          forced=[0, 1])
+            copies = max(1, min(8, -(-4 * 126 * 2 ** 20 // (vs * d * 2))))
+            heads = [api.restrict_lm_head(ctx, W, sub, dtype="bf16") for _ in range(copies)]
+            o2 = api.draft_head_topk(ctx, pool[0], heads[0], k, mode="fast")
+            for i in range(10):
+                api.draft_head_topk(ctx, pool[i % len(pool)], heads[i % copies], k, mode="fast", out=o2)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 200
+            s0.record()
+            for i in range(reps):
+                api.draft_head_topk(ctx, pool[i % len(pool)], heads[i % copies], k, mode="fast", out=o2)
+            s1.record()
+            torch.cuda.synchronize()
+            us = s0.elapsed_time(s1) * 1000.0 / reps
+            b = vs * d * 2 + n * d * 4 + n * k * 12
+            vsub_sweep.append({"v_sub": vs, "us_per_step": us, "GBps": b / us / 1e3, "frac_of_peak": b / us / 1e3 / hbm_peak,
+                               "slab_copies_rotated": copies})
+            del heads, o2
+
     # C4 (BASELINE configs[3]): vocab-parallel verify head at the Qwen-2.5-7B shape — each rank
     # holds a contiguous vocabulary shard, computes its argmax pairs (K3), NCCL all-gathers them
     # and merges (K5); at N=1 the single shard is the whole head (no collective).
@@ -443,32 +470,6 @@ def main():
                               "mean_accepted_length": s_emitted / (s_iters * S), "iterations": s_iters,
                               "api": "decode_step_table_multi", "scaling": "weak (streams sharded over ranks)"}
         del E, Wb
-
-    # C3 (BASELINE configs[2]): the V_sub sweep at the Llama-3-8B shape, FAST draft level back to
-    # back; slabs below 4x L2 rotate over copies so every step streams from HBM
-    vsub_sweep = None
-    if not args.no_sweep and mode == "fast":
-        vsub_sweep = []
-        for vs in (8192, 16384, 32768, 65536, 128256):
-            sub = api.subset_from_ranking(np.random.default_rng(1234).permutation(V).astype(np.int32), vs, V,
-                                          forced=[0, 1])
-            copies = max(1, min(8, -(-4 * 126 * 2 ** 20 // (vs * d * 2))))
-            heads = [api.restrict_lm_head(ctx, W, sub, dtype="bf16") for _ in range(copies)]
-            o2 = api.draft_head_topk(ctx, pool[0], heads[0], k, mode="fast")
-            for i in range(10):
-                api.draft_head_topk(ctx, pool[i % 8], heads[i % copies], k, mode="fast", out=o2)
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 200
-            s0.record()
-            for i in range(reps):
-                api.draft_head_topk(ctx, pool[i % 8], heads[i % copies], k, mode="fast", out=o2)
-            s1.record()
-            torch.cuda.synchronize()
-            us = s0.elapsed_time(s1) * 1000.0 / reps
-            b = vs * d * 2 + n * d * 4 + n * k * 12
-            vsub_sweep.append({"v_sub": vs, "us_per_step": us, "GBps": b / us / 1e3, "frac_of_peak": b / us / 1e3 / hbm_peak,
-                               "slab_copies_rotated": copies})
-            del heads, o2
 
     # C4 per-shard view at N=1: the verify head over contiguous shards V/G of the Qwen head (what
     # one GPU of a G-way vocab-parallel group computes before the all-gather), G = 1/2/4/8
