@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--no-sweep", action="store_true", help="skip the C3 V_sub sweep")
     p.add_argument("--no-batched", action="store_true", help="skip the C5 batched level")
     p.add_argument("--no-streams", action="store_true", help="skip the C5 256-stream decode measurement")
+    p.add_argument("--sweep-only", action="store_true", help=argparse.SUPPRESS)  # the C3 sweep's own process
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
 
@@ -183,10 +184,70 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+
+def run_sweep(args):
+    """C3 (BASELINE configs[2]): the V_sub sweep at the Llama-3-8B shape, FAST draft level back to
+    back; slabs below 4x L2 rotate over copies so every step streams from HBM. Runs in a fresh
+    process (bench.py --sweep-only, spawned by the main run at N = 1): the slab copies and the
+    main run's multi-GB buffers measured 10-25 % slower streams when they followed each other in
+    one process (split caching-allocator blocks). Prints one JSON line {"vsub_sweep_c3": [...]}."""
+    import numpy as np
+    import torch
+    from paper_2502_14856_b200 import api
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    d, V, n, k = C2["d"], C2["vocab"], args.rows, C2["k"]
+    hbm_peak, _ = peaks()
+    ctx = api.Context(0)
+    W, _ = synth(dev, d, V, C2["v_sub"], seed=1234)
+    g = torch.Generator(device=dev).manual_seed(99)
+    pool = [rmsnorm_rows(torch.randn(n, d, generator=g, device=dev)) for _ in range(256)]
+    sweep = []
+    for vs in (8192, 16384, 32768, 65536, 128256):
+        sub = api.subset_from_ranking(np.random.default_rng(1234).permutation(V).astype(np.int32), vs, V, forced=[0, 1])
+        copies = max(1, min(8, -(-4 * 126 * 2 ** 20 // (vs * d * 2))))
+        heads = [api.restrict_lm_head(ctx, W, sub, dtype="bf16") for _ in range(copies)]
+        o2 = api.draft_head_topk(ctx, pool[0], heads[0], k, mode="fast")
+        for i in range(10):
+            api.draft_head_topk(ctx, pool[i % len(pool)], heads[i % copies], k, mode="fast", out=o2)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 200
+        s0.record()
+        for i in range(reps):
+            api.draft_head_topk(ctx, pool[i % len(pool)], heads[i % copies], k, mode="fast", out=o2)
+        s1.record()
+        torch.cuda.synchronize()
+        us = s0.elapsed_time(s1) * 1000.0 / reps
+        b = vs * d * 2 + n * d * 4 + n * k * 12
+        sweep.append({"v_sub": vs, "us_per_step": us, "GBps": b / us / 1e3, "frac_of_peak": b / us / 1e3 / hbm_peak,
+                      "slab_copies_rotated": copies})
+        del heads, o2
+    print(json.dumps({"vsub_sweep_c3": sweep}))
+
+
+def sweep_subprocess(args):
+    import subprocess
+    cmd = [sys.executable, os.path.abspath(__file__), "--sweep-only", "--rows", str(args.rows)]
+    env = dict(os.environ)
+    for key in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(key, None)
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+        for line in reversed(r.stdout.strip().splitlines()):
+            if line.startswith("{"):
+                return json.loads(line).get("vsub_sweep_c3")
+    except Exception as e:  # the sweep is a side measurement: report its absence, not a failure
+        print(f"bench: V_sub sweep subprocess failed: {e}", file=sys.stderr)
+    return None
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.sweep_only:
+        run_sweep(args)
         return
     import numpy as np
     import torch
@@ -325,32 +386,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
-    # C3 (BASELINE configs[2]): the V_sub sweep at the Llama-3-8B shape, FAST draft level back to
-    # back; slabs below 4x L2 rotate over copies so every step streams from HBM. Run right after
-    # the headline, before the verify / decode sections' multi-GB allocations
     vsub_sweep = None
-    if not args.no_sweep and mode == "fast":
-        vsub_sweep = []
-        for vs in (8192, 16384, 32768, 65536, 128256):
-            sub = api.subset_from_ranking(np.random.default_rng(1234).permutation(V).astype(np.int32), vs, V,
-                                          forced=[0, 1])
-            copies = max(1, min(8, -(-4 * 126 * 2 ** 20 // (vs * d * 2))))
-            heads = [api.restrict_lm_head(ctx, W, sub, dtype="bf16") for _ in range(copies)]
-            o2 = api.draft_head_topk(ctx, pool[0], heads[0], k, mode="fast")
-            for i in range(10):
-                api.draft_head_topk(ctx, pool[i % len(pool)], heads[i % copies], k, mode="fast", out=o2)
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 200
-            s0.record()
-            for i in range(reps):
-                api.draft_head_topk(ctx, pool[i % len(pool)], heads[i % copies], k, mode="fast", out=o2)
-            s1.record()
-            torch.cuda.synchronize()
-            us = s0.elapsed_time(s1) * 1000.0 / reps
-            b = vs * d * 2 + n * d * 4 + n * k * 12
-            vsub_sweep.append({"v_sub": vs, "us_per_step": us, "GBps": b / us / 1e3, "frac_of_peak": b / us / 1e3 / hbm_peak,
-                               "slab_copies_rotated": copies})
-            del heads, o2
 
     # C4 (BASELINE configs[3]): vocab-parallel verify head at the Qwen-2.5-7B shape — each rank
     # holds a contiguous vocabulary shard, computes its argmax pairs (K3), NCCL all-gathers them
@@ -525,6 +561,10 @@ def main():
                    "tensor_tflops": 2.0 * 2 * rows5 * v_sub * d / us / 1e6,
                    "rows_recomputed": int(((fl & api._lib.FLAG_RECOMPUTED) != 0).sum())}
         del hb_, ob
+
+    # C3 sweep in its own process (run_sweep): N = 1 only (a single-GPU configuration)
+    if world == 1 and not args.no_sweep and mode == "fast":
+        vsub_sweep = sweep_subprocess(args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
