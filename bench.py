@@ -444,6 +444,7 @@ def main():
         ge = torch.Generator(device=dev).manual_seed(555 + rank)
         E = rmsnorm_rows(torch.randn(V, d, generator=ge, device=dev))
         Wb = W.to(torch.bfloat16)
+        Wbt = api.tile_image(ctx, Wb) if mode == "fast" else None  # the verify head's tiled image
         params = api.DraftParams(10, 6, 60)
         token, emitted, iters = 1, 0, 40
         for _ in range(3):
@@ -457,11 +458,11 @@ def main():
             token = int(outc.emitted[-1])
         two_call_s = time.perf_counter() - t0
         for _ in range(3):
-            token = int(api.decode_step_table(dh, E, token, Wb, params, mode=mode)[1].emitted[-1])
+            token = int(api.decode_step_table(dh, E, token, Wb, params, mode=mode, lm_head_tiled=Wbt)[1].emitted[-1])
         torch.cuda.synchronize()
         t0 = time.perf_counter()  # frs_decode_step_table: one sync per iteration
         for _ in range(iters):
-            tree, outc = api.decode_step_table(dh, E, token, Wb, params, mode=mode)
+            tree, outc = api.decode_step_table(dh, E, token, Wb, params, mode=mode, lm_head_tiled=Wbt)
             emitted += outc.accepted_length()
             token = int(outc.emitted[-1])
         dec_s = time.perf_counter() - t0
@@ -484,12 +485,13 @@ def main():
             S = max(1, 256 // world)
             roots = [int(x) for x in np.random.default_rng(99 + rank).integers(0, V, S)]
             for _ in range(1):
-                roots = [int(o.emitted[-1]) for _, o in api.decode_step_table_multi(dh, E, roots, Wb, params, mode="fast")]
+                roots = [int(o.emitted[-1]) for _, o in api.decode_step_table_multi(dh, E, roots, Wb, params, mode="fast",
+                                                                                    lm_head_tiled=Wbt)]
             torch.cuda.synchronize()
             s_iters, s_emitted = 2, 0
             t0 = time.perf_counter()
             for _ in range(s_iters):
-                res = api.decode_step_table_multi(dh, E, roots, Wb, params, mode="fast")
+                res = api.decode_step_table_multi(dh, E, roots, Wb, params, mode="fast", lm_head_tiled=Wbt)
                 s_emitted += sum(o.accepted_length() for _, o in res)
                 roots = [int(o.emitted[-1]) for _, o in res]
             ms_s = time.perf_counter() - t0
@@ -505,7 +507,7 @@ def main():
                               "ms_per_iteration": 1000.0 * ms_s / s_iters,
                               "mean_accepted_length": s_emitted / (s_iters * S), "iterations": s_iters,
                               "api": "decode_step_table_multi", "scaling": "weak (streams sharded over ranks)"}
-        del E, Wb
+        del E, Wb, Wbt
 
     # C4 per-shard view at N=1: the verify head over contiguous shards V/G of the Qwen head (what
     # one GPU of a G-way vocab-parallel group computes before the all-gather), G = 1/2/4/8

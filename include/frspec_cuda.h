@@ -334,7 +334,14 @@ FRS_API int frs_decode_step_table(frs_head *h, const float *table, int32_t root_
  * [root, tokens...] rows. Outputs per stream q: tokens/parents/depths/log_joint/path at
  * [q * total], emitted at [q * (total + 1)], count/n_emitted/n_path at [q]. */
 FRS_API int frs_decode_step_table_multi(frs_head *h, const float *table, int S, const int32_t *roots, const void *W,
-                                        int V, int w_dtype, int verify_mode, int width, int depth, int total,
+                                        const void *W_tiled, int V, int w_dtype, int verify_mode, int width, int depth,
+                                        int total, int32_t *tokens, int32_t *parents, int32_t *depths,
+                                        double *log_joint, int *count, int32_t *emitted, int *n_emitted,
+                                        int32_t *path, int *n_path);
+/* frs_decode_step_table with the bf16 verify head's tiled image W_tiled (frs_slab_tile of W): the
+ * FAST verify head streams it; W_tiled may be NULL in frs_decode_step_table_multi. */
+FRS_API int frs_decode_step_table_tiled(frs_head *h, const float *table, int32_t root_token, const void *W,
+                                        const void *W_tiled, int V, int verify_mode, int width, int depth, int total,
                                         int32_t *tokens, int32_t *parents, int32_t *depths, double *log_joint,
                                         int *count, int32_t *emitted, int *n_emitted, int32_t *path, int *n_path);
 

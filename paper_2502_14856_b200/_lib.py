@@ -119,8 +119,10 @@ SIGNATURES = [
                                      C.POINTER(_I)]),
     ("frs_decode_step_table", _I, [_P, _P, C.c_int32, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, C.POINTER(_I),
                                    _P, C.POINTER(_I), _P, C.POINTER(_I)]),
-    ("frs_decode_step_table_multi", _I, [_P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P,
-                                         _P, _P]),
+    ("frs_decode_step_table_multi", _I, [_P, _P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
+                                         _P, _P, _P]),
+    ("frs_decode_step_table_tiled", _I, [_P, _P, C.c_int32, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P,
+                                         C.POINTER(_I), _P, C.POINTER(_I), _P, C.POINTER(_I)]),
 ]
 
 

@@ -841,7 +841,8 @@ def verify_greedy_table(ctx: Context, table: torch.Tensor, root_token: int, lm_h
 
 
 def decode_step_table(head: "DeviceHead", table: torch.Tensor, root_token: int, lm_head: torch.Tensor,
-                      params: "DraftParams" = None, mode="exact") -> Tuple[DraftTree, VerifyOutcome]:
+                      params: "DraftParams" = None, mode="exact",
+                      lm_head_tiled: Optional[torch.Tensor] = None) -> Tuple[DraftTree, VerifyOutcome]:
     """One head-path decode iteration: build_draft_tree(root_token, hidden_table=table) then
     verify_greedy_table(table, root_token, lm_head, tree) with no host round trip in between
     (frs_decode_step_table). Same results as the two calls."""
@@ -854,17 +855,25 @@ def decode_step_table(head: "DeviceHead", table: torch.Tensor, root_token: int, 
     dt = DTYPE_BF16 if lm_head.dtype == torch.bfloat16 else DTYPE_F32
     if table.shape[1] != head.d or lm_head.shape[1] != head.d or table.shape[0] < head.vocab:
         raise ValueError("decode_step: table [>= vocab x d] and verify head [V x d] must match the draft head")
-    check(lib().frs_decode_step_table(head.handle, _ptr(table), root_token, _ptr(lm_head), lm_head.shape[0], dt,
-                                      _mode(mode), params.beam_width, params.search_depth, total, _np_ptr(tok),
-                                      _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt), _np_ptr(em),
-                                      C.byref(ne), _np_ptr(path), C.byref(npth)), "decode_step")
+    if lm_head_tiled is not None and dt == DTYPE_BF16:  # the verify head's tiled image (tile_image)
+        check(lib().frs_decode_step_table_tiled(head.handle, _ptr(table), root_token, _ptr(lm_head), _ptr(lm_head_tiled),
+                                                lm_head.shape[0], _mode(mode), params.beam_width, params.search_depth,
+                                                total, _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj),
+                                                C.byref(cnt), _np_ptr(em), C.byref(ne), _np_ptr(path), C.byref(npth)),
+              "decode_step")
+    else:
+        check(lib().frs_decode_step_table(head.handle, _ptr(table), root_token, _ptr(lm_head), lm_head.shape[0], dt,
+                                          _mode(mode), params.beam_width, params.search_depth, total, _np_ptr(tok),
+                                          _np_ptr(par), _np_ptr(dep), _np_ptr(lj), C.byref(cnt), _np_ptr(em),
+                                          C.byref(ne), _np_ptr(path), C.byref(npth)), "decode_step")
     n = cnt.value
     return (DraftTree(tok[:n].copy(), par[:n].copy(), dep[:n].copy(), lj[:n].copy()),
             VerifyOutcome(path[: npth.value].copy(), em[: ne.value].copy()))
 
 
 def decode_step_table_multi(head: "DeviceHead", table: torch.Tensor, roots, lm_head: torch.Tensor,
-                            params: "DraftParams" = None, mode="fast") -> List[Tuple[DraftTree, VerifyOutcome]]:
+                            params: "DraftParams" = None, mode="fast",
+                            lm_head_tiled: Optional[torch.Tensor] = None) -> List[Tuple[DraftTree, VerifyOutcome]]:
     """One head-path decode iteration for each of S independent streams (BASELINE configs[4]),
     batched across streams (frs_decode_step_table_multi): per stream the same results as
     decode_step_table(head, table, roots[q], lm_head, params, mode)."""
@@ -881,7 +890,8 @@ def decode_step_table_multi(head: "DeviceHead", table: torch.Tensor, roots, lm_h
     em, path = np.empty(S * (total + 1), np.int32), np.empty(S * total, np.int32)
     cnt, ne, npth = (np.empty(S, np.int32) for _ in range(3))
     dt = DTYPE_BF16 if lm_head.dtype == torch.bfloat16 else DTYPE_F32
-    check(lib().frs_decode_step_table_multi(head.handle, _ptr(table), S, _np_ptr(r), _ptr(lm_head), lm_head.shape[0],
+    check(lib().frs_decode_step_table_multi(head.handle, _ptr(table), S, _np_ptr(r), _ptr(lm_head),
+                                            _ptr(lm_head_tiled) if dt == DTYPE_BF16 else None, lm_head.shape[0],
                                             dt, _mode(mode), params.beam_width, params.search_depth, total,
                                             _np_ptr(tok), _np_ptr(par), _np_ptr(dep), _np_ptr(lj), _np_ptr(cnt),
                                             _np_ptr(em), _np_ptr(ne), _np_ptr(path), _np_ptr(npth)), "decode_step")

@@ -628,13 +628,21 @@ static int ctx_pinned(frs_ctx *ctx, size_t bytes) {
     return FRS_OK;
 }
 
+// The verify head's argmax over m rows: FAST with the head's tiled image when the caller has one.
+static int verify_argmax_rows(frs_ctx *ctx, const float *hd, int m, int d, const void *W, const void *W_tiled, int V,
+                              int w_dtype, int mode, int32_t *ids, cudaStream_t s) {
+    if (W_tiled && mode == FRS_MODE_FAST && w_dtype == FRS_DTYPE_BF16)
+        return frs_verify_head_argmax_tiled(ctx, hd, m, d, W, W_tiled, V, 0, ids, nullptr, nullptr, s);
+    return frs_verify_head_argmax(ctx, hd, m, d, W, V, w_dtype, 0, mode, ids, nullptr, nullptr, s);
+}
+
 // verify_greedy (verification.cpp:42-71) on the device: verify head argmax over the 1 + k rows
 // of h_dev (root first), the accept walk, one packed D2H. table != nullptr: h_dev is ignored
 // and the rows are gathered from table[V_table x d] by [root_token, tokens...] on the device.
 static int verify_greedy_impl(frs_ctx *ctx, const float *h_dev, const float *table, int64_t V_table, int32_t root_token,
                               const void *W, int V, int d, int w_dtype, int mode, const int32_t *tokens,
                               const int32_t *parents, int k, int32_t *emitted, int *n_emitted, int32_t *path,
-                              int *n_path) {
+                              int *n_path, const void *W_tiled = nullptr) {
     if (k > 64) return fail(FRS_ECAPACITY, "build_tree_mask: nodes exceed the 64-bit mask");
     FRS_REQUIRE(k >= 0 && (k == 0 || (tokens && parents)), "verify_greedy: bad tree");
     for (int i = 0; i < k; ++i)
@@ -658,7 +666,7 @@ static int verify_greedy_impl(frs_ctx *ctx, const float *h_dev, const float *tab
         if ((st = frs_gather_rows(ctx, table, V_table, d, rt, 1 + k, static_cast<float *>(ctx->hbuf.ptr), s))) return st;
         hd = static_cast<const float *>(ctx->hbuf.ptr);
     }
-    st = frs_verify_head_argmax(ctx, hd, 1 + k, d, W, V, w_dtype, 0, mode, ids, nullptr, nullptr, s);
+    st = verify_argmax_rows(ctx, hd, 1 + k, d, W, W_tiled, V, w_dtype, mode, ids, s);
     if (st) return st;
     st = frs_accept_greedy(ctx, ids, rt + 1, pp, k, d_em, d_path, d_cnt, s);
     if (st) return st;
@@ -698,10 +706,10 @@ int frs_verify_greedy_table(frs_ctx *ctx, const float *table, int64_t V_table, i
 // both results. Same results as frs_draft_tree + frs_verify_greedy_table: verify rows are
 // independent of each other, padding rows are never read by the walk. Shapes outside the
 // device tree, or an uncertified tree ordering, run those two calls instead.
-int frs_decode_step_table(frs_head *h, const float *table, int32_t root_token, const void *W, int V, int w_dtype,
-                          int verify_mode, int width, int depth, int total, int32_t *tokens, int32_t *parents,
-                          int32_t *depths, double *log_joint, int *count, int32_t *emitted, int *n_emitted,
-                          int32_t *path, int *n_path) {
+static int decode_step_impl(frs_head *h, const float *table, int32_t root_token, const void *W, const void *W_tiled,
+                            int V, int w_dtype, int verify_mode, int width, int depth, int total, int32_t *tokens,
+                            int32_t *parents, int32_t *depths, double *log_joint, int *count, int32_t *emitted,
+                            int *n_emitted, int32_t *path, int *n_path) {
     FRS_REQUIRE(h && table && W && tokens && parents && depths && log_joint && count && emitted && n_emitted &&
                     path && n_path,
                 "decode_step: null pointer");
@@ -731,9 +739,7 @@ int frs_decode_step_table(frs_head *h, const float *table, int32_t root_token, c
         ++ctx->launches;
         if ((st = frs::step_rows_accept(out_dev, root_token, total, rt, pp, kdev, s))) return st;
         if ((st = frs_gather_rows(ctx, table, h->vocab, d, rt, 1 + total, hv, s))) return st;
-        if ((st = frs_verify_head_argmax(ctx, hv, 1 + total, d, W, V, w_dtype, 0, verify_mode, ids, nullptr, nullptr,
-                                         s)))
-            return st;
+        if ((st = verify_argmax_rows(ctx, hv, 1 + total, d, W, W_tiled, V, w_dtype, verify_mode, ids, s))) return st;
         ++ctx->launches;
         if ((st = frs::accept_greedy_devk(ids, rt + 1, pp, kdev, d_em, d_path, d_cnt, s))) return st;
         int32_t *ht = h->h_ridx, *hv_out = static_cast<int32_t *>(ctx->pinned) + 129;
@@ -753,7 +759,24 @@ int frs_decode_step_table(frs_head *h, const float *table, int32_t root_token, c
                              parents, depths, log_joint, count)))
         return st;
     return verify_greedy_impl(ctx, nullptr, table, h->vocab, root_token, W, V, d, w_dtype, verify_mode, tokens,
-                              parents, *count, emitted, n_emitted, path, n_path);
+                              parents, *count, emitted, n_emitted, path, n_path, W_tiled);
+}
+
+int frs_decode_step_table(frs_head *h, const float *table, int32_t root_token, const void *W, int V, int w_dtype,
+                          int verify_mode, int width, int depth, int total, int32_t *tokens, int32_t *parents,
+                          int32_t *depths, double *log_joint, int *count, int32_t *emitted, int *n_emitted,
+                          int32_t *path, int *n_path) {
+    return decode_step_impl(h, table, root_token, W, nullptr, V, w_dtype, verify_mode, width, depth, total, tokens,
+                            parents, depths, log_joint, count, emitted, n_emitted, path, n_path);
+}
+
+int frs_decode_step_table_tiled(frs_head *h, const float *table, int32_t root_token, const void *W, const void *W_tiled,
+                                int V, int verify_mode, int width, int depth, int total, int32_t *tokens,
+                                int32_t *parents, int32_t *depths, double *log_joint, int *count, int32_t *emitted,
+                                int *n_emitted, int32_t *path, int *n_path) {
+    FRS_REQUIRE(W_tiled, "decode_step: null pointer");
+    return decode_step_impl(h, table, root_token, W, W_tiled, V, FRS_DTYPE_BF16, verify_mode, width, depth, total,
+                            tokens, parents, depths, log_joint, count, emitted, n_emitted, path, n_path);
 }
 
 // S independent decode streams, one head-path iteration each (drafting.cpp:122-245 then
@@ -764,8 +787,9 @@ int frs_decode_step_table(frs_head *h, const float *table, int32_t root_token, c
 // accept walk. Per stream the results equal frs_decode_step_table (same arithmetic per row).
 // Outputs are [S][total] (tokens, parents, depths, log_joint, path), [S][total + 1] (emitted) and
 // [S] (count, n_emitted, n_path).
-int frs_decode_step_table_multi(frs_head *h, const float *table, int S, const int32_t *roots, const void *W, int V,
-                                int w_dtype, int verify_mode, int width, int depth, int total, int32_t *tokens,
+int frs_decode_step_table_multi(frs_head *h, const float *table, int S, const int32_t *roots, const void *W,
+                                const void *W_tiled, int V, int w_dtype, int verify_mode, int width, int depth,
+                                int total, int32_t *tokens,
                                 int32_t *parents, int32_t *depths, double *log_joint, int *count, int32_t *emitted,
                                 int *n_emitted, int32_t *path, int *n_path) {
     FRS_REQUIRE(h && table && roots && W && tokens && parents && depths && log_joint && count && emitted &&
@@ -895,7 +919,7 @@ int frs_decode_step_table_multi(frs_head *h, const float *table, int S, const in
     const int R = roff[S];
     FRS_CUDA_TRY(cudaMemcpyAsync(tok_dev, rtok.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
     if ((st = frs_gather_rows(ctx, table, h->vocab, d, tok_dev, R, hd, s))) return st;
-    if ((st = frs_verify_head_argmax(ctx, hd, R, d, W, V, w_dtype, 0, verify_mode, pk, nullptr, nullptr, s))) return st;
+    if ((st = verify_argmax_rows(ctx, hd, R, d, W, W_tiled, V, w_dtype, verify_mode, pk, s))) return st;
     std::vector<int32_t> ids(R);
     FRS_CUDA_TRY(cudaMemcpyAsync(ids.data(), pk, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, s));
     FRS_CUDA_TRY(cudaStreamSynchronize(s));

@@ -307,6 +307,33 @@ def test_decode_step_table_multi_matches_per_stream(cuda_ctx, restatement, mode,
         roots = [int(out.emitted[-1]) for _, out in multi]
 
 
+def test_decode_step_tiled_verify_head(cuda_ctx, restatement):
+    """decode_step_table / decode_step_table_multi with the verify head's tiled image (FAST) ==
+    without it, chained over iterations."""
+    rng = np.random.default_rng(19)
+    V, d, v_sub = 4096, 128, 1024
+    W = (rng.standard_normal((V, d)) * 0.05).astype(np.float32)
+    W = torch.from_numpy(W).to(torch.bfloat16).to(torch.float32).numpy()
+    E = rmsnorm(rng.standard_normal((V, d)))
+    ids = rng.permutation(V)[:v_sub].astype(np.int32)
+    head = api.DeviceHead(cuda_ctx, W, api.RankedSubset(V, ids), dtype="f32")
+    Ed, Wb = torch.from_numpy(E).cuda(), torch.from_numpy(W).cuda().to(torch.bfloat16)
+    Wt = api.tile_image(cuda_ctx, Wb)
+    params = api.DraftParams(10, 6, 60)
+    token = 77
+    for _ in range(3):
+        t1, o1 = api.decode_step_table(head, Ed, token, Wb, params, mode="fast", lm_head_tiled=Wt)
+        t2, o2 = api.decode_step_table(head, Ed, token, Wb, params, mode="fast")
+        assert np.array_equal(t1.tokens, t2.tokens) and np.array_equal(o1.emitted, o2.emitted)
+        assert np.array_equal(o1.accepted_path, o2.accepted_path)
+        token = int(o1.emitted[-1])
+    roots = [5, 77, 1000]
+    a = api.decode_step_table_multi(head, Ed, roots, Wb, params, mode="fast", lm_head_tiled=Wt)
+    b = api.decode_step_table_multi(head, Ed, roots, Wb, params, mode="fast")
+    for (ta, oa), (tb, ob) in zip(a, b):
+        assert np.array_equal(ta.tokens, tb.tokens) and np.array_equal(oa.emitted, ob.emitted)
+
+
 def test_decode_step_table_multi_rejects(cuda_ctx):
     rng = np.random.default_rng(18)
     V, d = 512, 64
