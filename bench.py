@@ -506,7 +506,7 @@ def main():
                               "streams_total": S * world, "streams_per_rank": S, "tokens_per_s": srate,
                               "ms_per_iteration": 1000.0 * ms_s / s_iters,
                               "mean_accepted_length": s_emitted / (s_iters * S), "iterations": s_iters,
-                              "api": "decode_step_table_multi", "scaling": "weak (streams sharded over ranks)"}
+                              "api": "decode_step_table_multi", "scaling": "strong (256 streams split over the ranks)"}
         del E, Wb, Wbt
 
     # C4 per-shard view at N=1: the verify head over contiguous shards V/G of the Qwen head (what
