@@ -125,3 +125,30 @@ def test_fast_bound_adversarial(cuda_ctx, restatement, kind):
     rec = (f & FLAG_RECOMPUTED) != 0
     # recomputed rows are bit-exact in probabilities too
     assert np.array_equal(out.prob.cpu().numpy()[rec], ref["prob"][rec])
+
+
+def test_decode_multi_stream_c2_shape(cuda_ctx, restatement):
+    """C5 at the Llama-3-8B shape: frs_decode_step_table_multi over 4 streams (d 4096, V 128256,
+    V_sub 32768, tree 10/6/60, FAST verify over the tiled image) == decode_step_table per stream,
+    and each stream's accept walk == the oracle's over the restatement's argmax of its rows."""
+    rng = np.random.default_rng(77)
+    V, d, v_sub = 128256, 4096, 32768
+    W = torch.from_numpy((rng.standard_normal((V, d)) * 0.02).astype(np.float32)).to(torch.bfloat16).float()
+    ids = rng.permutation(V)[:v_sub].astype(np.int32)
+    head = api.DeviceHead(cuda_ctx, W.numpy(), api.RankedSubset(V, ids), dtype="bf16")
+    E = rmsnorm(rng.standard_normal((V, d)))
+    Ed, Wb = torch.from_numpy(E).cuda(), W.cuda().to(torch.bfloat16)
+    Wt = api.tile_image(cuda_ctx, Wb)
+    params = api.DraftParams(10, 6, 60)
+    roots = [int(x) for x in rng.integers(0, V, 4)]
+    multi = api.decode_step_table_multi(head, Ed, roots, Wb, params, mode="fast", lm_head_tiled=Wt)
+    Wn = W.numpy()
+    for q, (tree, out) in enumerate(multi):
+        ref_tree, ref = api.decode_step_table(head, Ed, roots[q], Wb, params, mode="fast")
+        for key in ("tokens", "parents", "depths", "log_joint"):
+            assert np.array_equal(getattr(tree, key), getattr(ref_tree, key)), (q, key)
+        assert np.array_equal(out.emitted, ref.emitted) and np.array_equal(out.accepted_path, ref.accepted_path)
+        rows = np.concatenate([[roots[q]], tree.tokens])
+        em, path = restatement.verify_greedy_ids(restatement.verify_argmax(E[rows], Wn)[0], tree.tokens,
+                                                 tree.parents)
+        assert np.array_equal(out.emitted, em) and np.array_equal(out.accepted_path, path)
